@@ -1,0 +1,149 @@
+"""Oracle data-fidelity terms f, their gradients and proximal maps (fp64, one image).
+
+Periodic blur (BASELINE C1/C2/C5; readings Q8, Q9):
+  (Ax)[c,m,n]  = sum_{i,j} k[i,j] x[c, (m-i+kc) mod H, (n-j+kc) mod W]   true convolution
+  (A^T r)      = sum_{i,j} k[i,j] r[c, (m+i-kc) mod H, (n+j-kc) mod W]   correlation
+  f = 1/2 ||Ax - y||^2,  grad f = A^T(Ax - y)         (by analogy with P:964)
+  prox_{tau f}(v) = argmin_x 1/2||Ax-y||^2 + ||x-v||^2/(2 tau)
+                  = (I + tau A^T A)^{-1}(v + tau A^T y)
+                  = F^{-1}[ F(v + tau A^T y) / (1 + tau |K^|^2) ]   (A circulant)
+Inpainting (PAPER App. D.3.2):
+  f = 1/2 ||Mx - y||^2, grad f = M^T(Mx - y),
+  prox_{tau f}(v) = (tau M y + v) / (tau M + 1) componentwise.
+Coded-diffraction phase retrieval (BASELINE C4; reading Q7, Q14):
+  f = 1/2 sum_j || |F(D_j x)|^2 - y_j ||^2, F the unitary 2-D DFT,
+  grad f = sum_j 2 Re( conj(D_j) F^{-1}[ (|u_j|^2 - y_j) u_j ] ),  u_j = F(D_j x).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+# --------------------------------------------------------------------------- blur
+def blur_A(x, k):
+    """Direct periodic true convolution, written as the defining sum of shifted copies."""
+    s = k.shape[0]
+    kc = (s - 1) // 2
+    out = np.zeros_like(x, dtype=np.float64)
+    for i in range(s):
+        for j in range(s):
+            # np.roll(x, d)[m] = x[m - d]  =>  d = i - kc gives x[m - i + kc]
+            out += float(k[i, j]) * np.roll(x, (i - kc, j - kc), axis=(-2, -1))
+    return out
+
+
+def blur_AT(r, k):
+    """Adjoint of blur_A: correlation r[m + i - kc]."""
+    s = k.shape[0]
+    kc = (s - 1) // 2
+    out = np.zeros_like(r, dtype=np.float64)
+    for i in range(s):
+        for j in range(s):
+            out += float(k[i, j]) * np.roll(r, (-(i - kc), -(j - kc)), axis=(-2, -1))
+    return out
+
+
+def blur_f(x, y, k):
+    r = blur_A(x, k) - y
+    return 0.5 * float(np.sum(r * r))
+
+
+def blur_grad(x, y, k):
+    """grad f = A^T(Ax - y)."""
+    return blur_AT(blur_A(x, k) - y, k)
+
+
+def blur_transfer(k, H, W):
+    """K^ = unnormalised 2-D DFT of k zero-embedded in H x W with tap (kc,kc) at (0,0)."""
+    s = k.shape[0]
+    kc = (s - 1) // 2
+    kp = np.zeros((H, W))
+    for i in range(s):
+        for j in range(s):
+            kp[(i - kc) % H, (j - kc) % W] += float(k[i, j])
+    return np.fft.fft2(kp)
+
+
+def blur_prox(v, y, k, tau):
+    """prox_{tau f}(v) = F^{-1}[ F(v + tau A^T y) / (1 + tau |K^|^2) ] (per channel)."""
+    H, W = v.shape[-2:]
+    K = blur_transfer(k, H, W)
+    rhs = v + tau * blur_AT(y, k)
+    return np.real(np.fft.ifft2(np.fft.fft2(rhs, axes=(-2, -1)) / (1.0 + tau * np.abs(K) ** 2),
+                                axes=(-2, -1)))
+
+
+# --------------------------------------------------------------------------- inpainting
+def inpaint_f(x, y, m):
+    r = m * x - y
+    return 0.5 * float(np.sum(r * r))
+
+
+def inpaint_grad(x, y, m):
+    """grad f = M^T (M x - y); M diagonal, shared by the channels."""
+    return m * (m * x - y)
+
+
+def inpaint_prox(v, y, m, tau):
+    """(tau M y + v) / (tau M + 1), componentwise."""
+    return (tau * m * y + v) / (tau * m + 1.0)
+
+
+# --------------------------------------------------------------------------- phase retrieval
+def _dft(a):
+    return np.fft.fft2(a, axes=(-2, -1), norm="ortho")
+
+
+def _idft(a):
+    return np.fft.ifft2(a, axes=(-2, -1), norm="ortho")
+
+
+def phase_f(x, y, D):
+    """x: [1][H][W]; y: [J][H][W]; D: [J][H][W] complex."""
+    u = _dft(D * x[0][None])
+    r = np.abs(u) ** 2 - y
+    return 0.5 * float(np.sum(r * r))
+
+
+def phase_grad(x, y, D):
+    u = _dft(D * x[0][None])
+    w = (np.abs(u) ** 2 - y) * u
+    g = np.sum(2.0 * np.real(np.conj(D) * _idft(w)), axis=0)
+    return g[None]
+
+
+# --------------------------------------------------------------------------- dispatch
+class Fidelity:
+    """f(., y) for one image: value, gradient, prox (None when not closed form)."""
+
+    def __init__(self, kind, y, kernel=None, mask=None, phase=None):
+        self.kind = kind
+        self.y = np.asarray(y, dtype=np.float64)
+        self.k = None if kernel is None else np.asarray(kernel, dtype=np.float64)
+        self.m = None if mask is None else np.asarray(mask, dtype=np.float64)[None]
+        if phase is not None:
+            phase = np.asarray(phase, dtype=np.float64)
+            self.D = phase[..., 0] + 1j * phase[..., 1]
+
+    def value(self, x):
+        if self.kind == "blur":
+            return blur_f(x, self.y, self.k)
+        if self.kind == "inpaint":
+            return inpaint_f(x, self.y, self.m)
+        return phase_f(x, self.y, self.D)
+
+    def grad(self, x):
+        if self.kind == "blur":
+            return blur_grad(x, self.y, self.k)
+        if self.kind == "inpaint":
+            return inpaint_grad(x, self.y, self.m)
+        return phase_grad(x, self.y, self.D)
+
+    def prox(self, v, tau):
+        if self.kind == "blur":
+            return blur_prox(v, self.y, self.k, tau)
+        if self.kind == "inpaint":
+            return inpaint_prox(v, self.y, self.m, tau)
+        raise NotImplementedError("no closed-form prox for phase retrieval (cf. P:1079)")
