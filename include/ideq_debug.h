@@ -1,0 +1,34 @@
+/*
+ * ideq_debug.h -- test hooks of libideq.so (not needed by solver users).
+ *
+ * ideq_debug_conv runs ONE implicit-GEMM convolution layer of the network program
+ * exactly as the solver does (same weight re-arrangement, geometry and kernel),
+ * so tests can pin each layer kind and epilogue against the oracle's layer.
+ *
+ *   kind 0: conv3x3            out[co,m,n]  = sum W[co,ci,a,b] in[ci,m+a-1,n+b-1]   (W [Cout][Cin][3][3])
+ *   kind 1: conv3x3 adjoint    gin[ci,m,n]  = sum W[co,ci,a,b] g[co,m-a+1,n-b+1]
+ *   kind 2: down 2x2/s2        out[co,i,j]  = sum Wd[co,ci,a,b] in[ci,2i+a,2j+b]    (Wd [Cout][Cin][2][2])
+ *   kind 3: down adjoint       gin[ci,2i+a,2j+b] = sum_co Wd[co,ci,a,b] g[co,i,j]
+ *   kind 4: up 2x2/s2 (transp) out[co,2i+a,2j+b] = sum_ci Wu[ci,co,a,b] in[ci,i,j]  (Wu [Cin][Cout][2][2])
+ *   kind 5: up adjoint         gin[ci,i,j]  = sum Wu[ci,co,a,b] g[co,2i+a,2j+b]
+ * w: HOST fp32 tensor of the conv in the layouts above, shape (s0, s1, kh, kw).
+ * in/out/aux: DEVICE NHWC tensors of fp32 (precision 0) or bf16 (precision 1).
+ *   Hin, Win: spatial size of `in`; out has the kind's output size.
+ * epi: 0 store, 1 softplus, 2 out = acc + aux, 3 out = acc * (1 - exp(-aux)).
+ * use_tc: 1 = tcgen05 kernel (precision 1 only), 0 = FFMA kernel.
+ * Synchronises the device; returns an ideq_status code.
+ */
+#ifndef IDEQ_DEBUG_H
+#define IDEQ_DEBUG_H
+#include "ideq.h"
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+IDEQ_API int ideq_debug_conv(int kind, int precision, int use_tc, const float* w, int s0, int s1, int N, int Hin,
+                             int Win, const void* in, void* out, const void* aux, int epi, char* err, int errlen);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

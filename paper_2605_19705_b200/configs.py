@@ -46,6 +46,20 @@ CONFIGS = {
 }
 
 
+# Stress variants for parity: with the x0.1 init and lambda = 0.05 the
+# regularizer term lam*grad g is ~1e-3 of grad f, so trajectory parity alone would not
+# exercise the VJP. The stress variant uses init scale 0.3 and a larger lambda chosen so
+# that ||lam grad g(x0)|| >= 0.1 ||grad f(0.9 x_true)|| while the oracle stays
+# non-divergent over the parity horizon (checked in tests/test_oracle_configs.py).
+STRESS = {
+    "C1": dict(init_scale=0.3, lam=1.0),
+    "C2": dict(init_scale=0.3, lam=0.1),
+    "C3": dict(init_scale=0.3, lam=0.1),
+    "C4": dict(init_scale=0.3, lam=0.1),
+    "C5": dict(init_scale=0.3, lam=0.1),
+}
+
+
 def get(name: str, **overrides) -> dict:
     """A deep copy of config ``name`` with overrides applied (used for the
     reduced-size parity variants: fewer images, smaller H/W, fixed K)."""

@@ -1,0 +1,407 @@
+// tcgen05 / TMEM / TMA implicit-GEMM convolution for sm_100a (bf16 operands, fp32
+// accumulation in tensor memory) with the i-DEQ epilogues fused:
+//   forward  RB conv A : a = softplus(W * t)         (saved for the VJP)
+//   forward  RB conv B : t' = t + W * a
+//   adjoint  conv B^T  : q = (W~ * g) . sp'(a)        (sp' recomputed from saved a)
+//   adjoint  conv A^T  : g' = g + W~ * q
+//   2x2 stride-2 down / transposed up and their adjoints (patch / scatter geometry).
+//
+// GEMM view (ConvGeom in common.cuh): M = 128 output pixels of an R x Wt tile,
+// N = GEMM columns (output channels, or 4 x channels for the scatter layers),
+// K = taps x input channels, walked in K-blocks of KC = 32/64 channels of one tap.
+//
+// Warp roles (192 threads, persistent over tiles):
+//   warp 0      : TMA producer -- one 5-D box (KC ch x Wt x 1 x R x 1) of the input per
+//                 K-block (out-of-range rows/cols are zero-filled by TMA = conv padding)
+//                 and one 3-D box of the pre-arranged weights [kb][ncols][KC].
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16),
+//                 tcgen05.commit frees smem stages and publishes accumulators.
+//   warps 2..5  : epilogue -- tcgen05.ld 32 lanes x 32 columns, fused activation /
+//                 residual / sp' multiply, bf16 pack, 16-byte global stores.
+// TMEM holds two BN-column accumulators so the epilogue of tile i overlaps the MMAs
+// of tile i+1. Shared-memory stages form an mbarrier ring (full/empty).
+#include <cuda.h>
+#include <stdio.h>
+#include <string.h>
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ideq {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor, K-major, swizzled (SW128: layout 2, SW64: layout 4).
+//   bits [0,14) start>>4, [16,30) LBO>>4 (ignored for swizzled K-major), [32,46) SBO>>4,
+//   [46,48) version = 1 (sm_100), [49,52) base offset = 0, [61,64) layout type.
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(1u) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+
+// Instruction descriptor for kind::f16: bf16 x bf16 -> f32, both K-major, M=128, N=n.
+__device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
+  return (1u << 4)                       // D format f32
+         | (1u << 7)                     // A format bf16
+         | (1u << 10)                    // B format bf16
+         | ((uint32_t)(n >> 3) << 17)    // N >> 3
+         | ((uint32_t)(128 >> 4) << 24); // M >> 4
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ kernel
+struct TcParams {
+  ConvGeom g;
+  __nv_bfloat16* out;
+  const __nv_bfloat16* aux;
+  int BN, n_tiles, m_tiles, stages;
+  uint32_t a_bytes, b_bytes, tmem_cols;
+};
+
+constexpr int TC_THREADS = 192;
+
+template <int KC>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ TcParams P) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-byte aligned carve-up
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
+  const int S = P.stages;
+  const uint32_t a_stage = 128u * KC * 2u;
+  const uint32_t b_stage = (uint32_t)P.BN * KC * 2u;
+  const uint32_t sA = base;
+  const uint32_t sB = sA + S * a_stage;
+  const uint32_t sBar = sB + S * b_stage;  // 8-byte aligned (stage sizes are multiples of 1 KB)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
+  const uint32_t full0 = sBar, empty0 = sBar + 8u * S, tfull0 = sBar + 16u * S, tempty0 = tfull0 + 16u;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const ConvGeom& g = P.g;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
+    for (int a = 0; a < 2; ++a) { mbar_init(tfull0 + 8u * a, 1); mbar_init(tempty0 + 8u * a, 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const int nkb = g.ntaps * g.nchunk;
+  const int total = P.m_tiles * P.n_tiles;
+  const int per_img = g.tiles_h * g.tiles_w;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        const int mt = t / P.n_tiles, nt = t % P.n_tiles;
+        const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
+        const int h0 = th * g.R, w0 = tw * g.Wt;
+        for (int kb = 0; kb < nkb; ++kb) {
+          const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
+          mbar_wait(empty0 + 8u * s, ph ^ 1u);
+          mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
+          tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * KC, w0 + g.dw[tap], g.dp[tap], h0 + g.dh[tap],
+                      img);
+          tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * P.BN, kb);
+          if (++s == S) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc_bf16(P.BN);
+      constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
+      constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
+      int s = 0;
+      uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = blockIdx.x; t < total; t += gridDim.x) {
+        mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * P.BN);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(full0 + 8u * s, ph);
+          tc_fence_after();
+          const uint32_t a_addr = sA + s * a_stage, b_addr = sB + s * b_stage;
+#pragma unroll
+          for (int k = 0; k < KC / 16; ++k) {
+            const uint64_t ad = make_sdesc(a_addr + 32u * k, sbo, layout);
+            const uint64_t bd = make_sdesc(b_addr + 32u * k, sbo, layout);
+            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
+          }
+          mma_commit(empty0 + 8u * s);
+          if (++s == S) { s = 0; ph ^= 1u; }
+        }
+        mma_commit(tfull0 + 8u * acc);
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
+      }
+    }
+    __syncwarp();
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;  // pixel index within the tile
+    int acc = 0;
+    uint32_t aph = 0;
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const int mt = t / P.n_tiles, nt = t % P.n_tiles;
+      const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
+      const int oh = th * g.R + row / g.Wt, ow = tw * g.Wt + row % g.Wt;
+      const bool valid = row < g.R * g.Wt && oh < g.OH && ow < g.OW;
+      mbar_wait(tfull0 + 8u * acc, aph);
+      tc_fence_after();
+      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+        float v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * P.BN + c0), v);
+        if (valid) {
+          const int col = nt * P.BN + c0;
+          const long long o = out_offset(g, img, oh, ow, col);
+          if (g.epi == EPI_RESADD || g.epi == EPI_SIGMUL) {
+            const uint4* ap = reinterpret_cast<const uint4*>(P.aux + o);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 u = ap[q];
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                v[q * 8 + 2 * e] = apply_epi(g.epi, v[q * 8 + 2 * e], f.x);
+                v[q * 8 + 2 * e + 1] = apply_epi(g.epi, v[q * 8 + 2 * e + 1], f.y);
+              }
+            }
+          } else if (g.epi == EPI_SOFTPLUS) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = softplus_f(v[i]);
+          }
+          uint4* op = reinterpret_cast<uint4*>(P.out + o);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+            op[q] = u;
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+      if (++acc == 2) { acc = 0; aph ^= 1u; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
+                 : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+struct TcPlan {
+  CUtensorMap tmA, tmB;
+  TcParams P;
+  int KC, grid;
+  size_t smem;
+};
+
+bool tc_supported(const ConvGeom& g) {
+  if (!(g.KC == 32 || g.KC == 64)) return false;
+  if (g.R * g.Wt > 128 || g.Wt > 256 || g.R > 256) return false;
+  if (g.ncols % 32 != 0) return false;
+  const int BN = g.ncols >= 256 ? 256 : g.ncols;
+  if (g.ncols % BN != 0) return false;
+  if (g.CB % 32 != 0 || g.OCp % 8 != 0) return false;
+  if ((g.inC * 2) % 16 != 0) return false;
+  return true;
+}
+
+TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
+                     const __nv_bfloat16* aux, int num_sms, char* err, size_t errlen) {
+  if (!tc_supported(g)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
+  EncodeTiledFn enc = get_encode();
+  if (!enc) { snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable"); return nullptr; }
+  TcPlan* p = new TcPlan();
+  memset(p, 0, sizeof(TcPlan));
+  p->KC = g.KC;
+  const int BN = g.ncols >= 256 ? 256 : g.ncols;
+  // A: 5-D view (C', W', P, H', N) of the NHWC input
+  {
+    cuuint64_t dims[5] = {(cuuint64_t)g.inC, (cuuint64_t)g.inW, (cuuint64_t)g.inP, (cuuint64_t)g.inH, (cuuint64_t)g.N};
+    cuuint64_t strides[4];
+    strides[0] = (cuuint64_t)g.inC * 2;
+    strides[1] = strides[0] * g.inW;
+    strides[2] = strides[1] * g.inP;
+    strides[3] = strides[2] * g.inH;
+    cuuint32_t box[5] = {(cuuint32_t)g.KC, (cuuint32_t)g.Wt, 1u, (cuuint32_t)g.R, 1u};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    CUresult r = enc(&p->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(in), dims, strides, box,
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
+  }
+  // B: [kb][ncols][KC]
+  {
+    const int nkb = g.ntaps * g.nchunk;
+    cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {(cuuint64_t)g.KC * 2, (cuuint64_t)g.KC * 2 * g.ncols};
+    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box,
+                     es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map B encode failed (%d)", (int)r); delete p; return nullptr; }
+  }
+  TcParams& P = p->P;
+  P.g = g;
+  P.out = out;
+  P.aux = aux;
+  P.BN = BN;
+  P.n_tiles = g.ncols / BN;
+  P.m_tiles = g.N * g.tiles_h * g.tiles_w;
+  P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
+  P.b_bytes = (uint32_t)g.KC * 2u * BN;
+  uint32_t cols = 2u * BN;
+  uint32_t tc = 32;
+  while (tc < cols) tc <<= 1;
+  P.tmem_cols = tc;
+  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u;
+  const size_t budget = 200 * 1024;
+  int stages = (int)(budget / (a_stage + b_stage));
+  if (stages > 8) stages = 8;
+  if (stages < 2) { snprintf(err, errlen, "tcgen05 conv: smem too small"); delete p; return nullptr; }
+  P.stages = stages;
+  p->smem = 1024 + stages * (a_stage + b_stage) + (2 * stages + 4) * 8 + 16;
+  const int total = P.m_tiles * P.n_tiles;
+  p->grid = total < num_sms ? total : num_sms;
+  return p;
+}
+
+void tc_launch(const TcPlan* p, cudaStream_t s) {
+  if (p->KC == 64) {
+    conv_tc_kernel<64><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->P);
+  } else {
+    conv_tc_kernel<32><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->P);
+  }
+}
+
+void tc_free_plan(TcPlan* p) { delete p; }
+
+void init_attrs_tc() {
+
+  set_max_dyn_smem(conv_tc_kernel<64>);
+  set_max_dyn_smem(conv_tc_kernel<32>);
+}
+
+}  // namespace ideq

@@ -1,0 +1,1276 @@
+// Runtime and C ABI of the i-DEQ engine (include/ideq.h).
+//
+// The context owns: the network program (the ordered list of convolution launches
+// for U_theta(z) and its input VJP), every workspace, the operator data, the solver
+// state, and CUDA graphs of one iteration. All per-iteration work is enqueued on the
+// caller's stream; the host only polls a 4-byte active-image counter.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/ideq.h"
+#include "../../include/ideq_debug.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace ideq;
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen'ed; only when world > 1)
+typedef struct { char internal[128]; } nccl_uid;
+typedef void* nccl_comm;
+struct NcclApi {
+  void* h = nullptr;
+  int (*GetUniqueId)(nccl_uid*) = nullptr;
+  int (*CommInitRank)(nccl_comm*, int, nccl_uid, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t) = nullptr;
+  int (*CommDestroy)(nccl_comm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool load(std::string& err) {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) { h = dlopen(n, RTLD_NOW | RTLD_GLOBAL); if (h) break; }
+    if (!h) { err = "cannot dlopen libnccl.so.2"; return false; }
+    GetUniqueId = (int (*)(nccl_uid*))dlsym(h, "ncclGetUniqueId");
+    CommInitRank = (int (*)(nccl_comm*, int, nccl_uid, int))dlsym(h, "ncclCommInitRank");
+    AllReduce = (int (*)(const void*, void*, size_t, int, int, nccl_comm, cudaStream_t))dlsym(h, "ncclAllReduce");
+    CommDestroy = (int (*)(nccl_comm))dlsym(h, "ncclCommDestroy");
+    GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    if (!GetUniqueId || !CommInitRank || !AllReduce || !CommDestroy) { err = "libnccl missing symbols"; return false; }
+    return true;
+  }
+};
+NcclApi g_nccl;
+constexpr int NCCL_FLOAT32 = 7, NCCL_MAX = 2;
+
+// ------------------------------------------------------------------ program description
+enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2 };
+
+struct Layer {
+  LayerKind kind;
+  ConvGeom g{};
+  const void* in = nullptr;   // GEMM / FEAT2IMG input (feature tensor)
+  const void* wB = nullptr;   // device weights (GEMM: [kb][ncols][KC] of T; head/tail: fp32 [o][i][3][3])
+  void* out = nullptr;
+  const void* aux = nullptr;
+  // head/tail
+  const float* in_img = nullptr;
+  float* out_img = nullptr;
+  const float* aux_img = nullptr;
+  float alpha = 0.f;
+  int C = 0, wfeat = 0, epi = 0, N = 0, H = 0, W = 0;
+  TcPlan* plan = nullptr;
+  bool tc = false;  // tcgen05 path (bf16 U-Net layers) vs FFMA path
+  double flops = 0, bytes = 0;
+  std::string name;
+};
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct ideq_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  ideq_precision prec = IDEQ_PREC_FP32;
+  ideq_net_desc net{};
+  std::vector<float> blob;
+  int maxN = 0, H = 0, W = 0, C = 1;
+  int num_sms = 148;
+  std::string err;
+  bool poisoned = false;
+  size_t elt = 4;  // bytes per activation element
+
+  std::vector<DevBuf> allocs;
+  // weights per conv (device), keyed by name + direction
+  std::map<std::string, void*> wdev;
+  // feature buffers: per level 3 work buffers; saved activations
+  std::vector<std::vector<void*>> lvl_buf;  // [level][3]
+  std::map<std::string, void*> saved;
+  int prog_batch = -1;
+  std::vector<Layer> prog;  // forward then VJP
+  int n_fwd = 0;
+
+  // solver buffers (fp32 NCHW)
+  float *X1 = nullptr, *Z = nullptr, *G = nullptr, *Hc = nullptr, *fbuf = nullptr, *fbuf2 = nullptr;
+  float* partials = nullptr;
+  int parts_cap = 0;
+  int *active = nullptr, *status = nullptr, *iters = nullptr, *n_active = nullptr, *kdev = nullptr;
+  float *res = nullptr, *r_now = nullptr, *rmax = nullptr, *trace = nullptr;
+  int trace_cap = 65536;
+  int* h_pinned = nullptr;  // host mirror of n_active
+  float* dstage_y = nullptr;
+  float* dstage_x = nullptr;
+  size_t dstage_y_n = 0, dstage_x_n = 0;
+
+  // operator
+  bool op_set = false;
+  ideq_operator_desc op{};
+  int op_batch = 0;
+  float* d_kern = nullptr;
+  uint8_t* d_mask = nullptr;
+  float* d_phase = nullptr;
+
+  // distribution
+  int rank = 0, world = 1;
+  nccl_comm comm = nullptr;
+
+  // graphs
+  cudaGraphExec_t gexec_plain = nullptr, gexec_check = nullptr;
+  std::string graph_key;
+
+  // profiling
+  bool profiling = false;
+  ideq_profile prof{};
+  struct Ev { cudaEvent_t a, b; int cls; double flops, bytes; };
+  std::vector<Ev> pending;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+
+  int launches_per_iter = 0;
+  bool own_stream = false;
+};
+
+namespace {
+
+ideq_status fail(ideq_ctx* c, ideq_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  if (c) {
+    c->err = buf;
+    if (st == IDEQ_E_CUDA || st == IDEQ_E_NCCL) c->poisoned = true;
+  }
+  return st;
+}
+
+#define CK(call)                                                                                \
+  do {                                                                                          \
+    cudaError_t e_ = (call);                                                                    \
+    if (e_ != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+ideq_status dalloc(ideq_ctx* ctx, void** p, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, IDEQ_E_NOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+  }
+  ctx->allocs.push_back({*p, bytes});
+  return IDEQ_OK;
+}
+
+// ------------------------------------------------------------------ weights
+uint16_t f2bf(float f) {  // round-to-nearest-even
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return (uint16_t)(u >> 16);
+}
+
+struct WeightSlices {
+  std::map<std::string, std::pair<size_t, std::vector<int>>> t;  // name -> offset, shape
+};
+
+bool slice_weights(const ideq_net_desc& n, WeightSlices& ws, size_t& total) {
+  size_t o = 0;
+  auto add = [&](const std::string& name, std::vector<int> shp) {
+    size_t k = 1;
+    for (int s : shp) k *= (size_t)s;
+    ws.t[name] = {o, shp};
+    o += k;
+  };
+  const int C = n.channels;
+  if (n.arch == IDEQ_NET_TINY3) {
+    const int w = n.widths[0];
+    add("c1", {w, C, 3, 3});
+    add("c2", {w, w, 3, 3});
+    add("c3", {C, w, 3, 3});
+  } else {
+    const int* w = n.widths;
+    add("head", {w[0], C, 3, 3});
+    for (int l = 0; l < 4; ++l) {
+      for (int r = 0; r < n.res_blocks; ++r) {
+        add("e" + std::to_string(l) + "." + std::to_string(r) + ".A", {w[l], w[l], 3, 3});
+        add("e" + std::to_string(l) + "." + std::to_string(r) + ".B", {w[l], w[l], 3, 3});
+      }
+      if (l < 3) add("down" + std::to_string(l), {w[l + 1], w[l], 2, 2});
+    }
+    for (int l = 2; l >= 0; --l) {
+      add("up" + std::to_string(l), {w[l + 1], w[l], 2, 2});
+      for (int r = 0; r < n.res_blocks; ++r) {
+        add("d" + std::to_string(l) + "." + std::to_string(r) + ".A", {w[l], w[l], 3, 3});
+        add("d" + std::to_string(l) + "." + std::to_string(r) + ".B", {w[l], w[l], 3, 3});
+      }
+    }
+    add("tail", {C, w[0], 3, 3});
+  }
+  total = o;
+  return true;
+}
+
+// Build the [kb][ncols][KC] GEMM operand for one conv direction (host fp32).
+//   kind 0: conv3x3 fwd, 1: conv3x3 adjoint, 2: down fwd, 3: down adjoint, 4: up fwd, 5: up adjoint.
+std::vector<float> gemm_weights(int kind, const float* Wt, const std::vector<int>& shp, int KC, int& ncols,
+                                int& ntaps, int& ktap) {
+  std::vector<float> B;
+  if (kind == 0 || kind == 1) {  // W [co][ci][3][3]
+    const int co_n = shp[0], ci_n = shp[1];
+    ncols = kind == 0 ? co_n : ci_n;
+    ktap = kind == 0 ? ci_n : co_n;
+    ntaps = 9;
+    const int nch = ktap / KC;
+    B.assign((size_t)9 * nch * ncols * KC, 0.f);
+    for (int t = 0; t < 9; ++t) {
+      const int a = t / 3, b = t % 3;
+      for (int ch = 0; ch < nch; ++ch)
+        for (int n = 0; n < ncols; ++n)
+          for (int k = 0; k < KC; ++k) {
+            const int kk = ch * KC + k;
+            const int co = kind == 0 ? n : kk, ci = kind == 0 ? kk : n;
+            B[(((size_t)(t * nch + ch)) * ncols + n) * KC + k] = Wt[(((size_t)co * ci_n + ci) * 3 + a) * 3 + b];
+          }
+    }
+  } else if (kind == 2 || kind == 5) {  // patch GEMM on the fine grid: taps a, K = (b, c)
+    // down: Wd [co][ci][2][2], out cols co, k = (b, ci)       -> Wd[co][ci][a][b]
+    // upT : Wu [ci][co][2][2], out cols ci(coarse), k=(b, co) -> Wu[ci][co][a][b]
+    const int o_n = shp[0], f_n = shp[1];  // down: o=co(coarse) f=ci(fine); up: o=ci(coarse) f=co(fine)
+    ncols = o_n;
+    ktap = 2 * f_n;
+    ntaps = 2;
+    const int nch = ktap / KC;
+    B.assign((size_t)2 * nch * ncols * KC, 0.f);
+    for (int a = 0; a < 2; ++a)
+      for (int ch = 0; ch < nch; ++ch)
+        for (int n = 0; n < ncols; ++n)
+          for (int k = 0; k < KC; ++k) {
+            const int kk = ch * KC + k;
+            const int b = kk / f_n, f = kk % f_n;
+            B[(((size_t)(a * nch + ch)) * ncols + n) * KC + k] = Wt[(((size_t)n * f_n + f) * 2 + a) * 2 + b];
+          }
+  } else {  // 3: down adjoint, 4: up fwd -- 1x1 on the coarse grid, cols = (a, b, fine channel)
+    // downT: Wd [co][ci][2][2], input coarse g (co), cols (a,b,ci): Wd[k][ci][a][b]
+    // up   : Wu [ci][co][2][2], input coarse x (ci), cols (a,b,co): Wu[k][co][a][b]
+    const int k_n = shp[0], f_n = shp[1];
+    ncols = 4 * f_n;
+    ktap = k_n;
+    ntaps = 1;
+    const int nch = ktap / KC;
+    B.assign((size_t)nch * ncols * KC, 0.f);
+    for (int ch = 0; ch < nch; ++ch)
+      for (int n = 0; n < ncols; ++n)
+        for (int k = 0; k < KC; ++k) {
+          const int kk = ch * KC + k;
+          const int a = n / (2 * f_n), b = (n / f_n) % 2, f = n % f_n;
+          B[(((size_t)ch) * ncols + n) * KC + k] = Wt[(((size_t)kk * f_n + f) * 2 + a) * 2 + b];
+        }
+  }
+  return B;
+}
+
+// 3x3 weights of the adjoint of a head/tail conv: W~[i][o][a][b] = W[o][i][2-a][2-b].
+std::vector<float> flip_transpose3x3(const float* Wt, int o_n, int i_n) {
+  std::vector<float> F((size_t)i_n * o_n * 9);
+  for (int o = 0; o < o_n; ++o)
+    for (int i = 0; i < i_n; ++i)
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b)
+          F[(((size_t)i * o_n + o) * 3 + a) * 3 + b] = Wt[(((size_t)o * i_n + i) * 3 + (2 - a)) * 3 + (2 - b)];
+  return F;
+}
+
+// K-block width: the tcgen05 path stages 32/64 channels (64B/128B swizzle rows); the
+// FFMA path walks 16 channels at a time.
+int pick_kc(bool tc, int ktap) {
+  if (tc) return (ktap % 64 == 0) ? 64 : 32;
+  return 16;
+}
+
+bool use_tc(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_BF16 && ctx->net.arch == IDEQ_NET_UNET4; }
+
+ideq_status upload_gemm_weights(ideq_ctx* ctx, const std::string& key, const std::vector<float>& B) {
+  void* d = nullptr;
+  const size_t n = B.size();
+  ideq_status st = dalloc(ctx, &d, n * ctx->elt);
+  if (st) return st;
+  if (ctx->prec == IDEQ_PREC_BF16) {
+    std::vector<uint16_t> hb(n);
+    for (size_t i = 0; i < n; ++i) hb[i] = f2bf(B[i]);
+    CK(cudaMemcpy(d, hb.data(), n * 2, cudaMemcpyHostToDevice));
+  } else {
+    CK(cudaMemcpy(d, B.data(), n * 4, cudaMemcpyHostToDevice));
+  }
+  ctx->wdev[key] = d;
+  return IDEQ_OK;
+}
+
+ideq_status upload_f32(ideq_ctx* ctx, const std::string& key, const std::vector<float>& v) {
+  void* d = nullptr;
+  ideq_status st = dalloc(ctx, &d, v.size() * 4);
+  if (st) return st;
+  CK(cudaMemcpy(d, v.data(), v.size() * 4, cudaMemcpyHostToDevice));
+  ctx->wdev[key] = d;
+  return IDEQ_OK;
+}
+
+// ------------------------------------------------------------------ geometry builders
+void tile_grid(ConvGeom& g) {
+  g.Wt = g.OW < 128 ? g.OW : 128;
+  g.R = 128 / g.Wt;
+  if (g.R > g.OH) g.R = g.OH;
+  if (g.R < 1) g.R = 1;
+  g.tiles_h = (g.OH + g.R - 1) / g.R;
+  g.tiles_w = (g.OW + g.Wt - 1) / g.Wt;
+}
+
+// kind as in gemm_weights. Hin/Win: spatial size of the tensor the layer READS.
+ConvGeom make_geom(int kind, int N, int Hin, int Win, int cin_tensor, int ncols, int KC, int ktap, int epi) {
+  ConvGeom g{};
+  g.N = N;
+  g.KC = KC;
+  g.nchunk = ktap / KC;
+  g.epi = epi;
+  g.ncols = ncols;
+  if (kind == 0 || kind == 1) {
+    g.inC = cin_tensor; g.inW = Win; g.inP = 1; g.inH = Hin;
+    g.OH = Hin; g.OW = Win;
+    g.ntaps = 9;
+    for (int t = 0; t < 9; ++t) {
+      const int a = t / 3, b = t % 3;
+      g.dh[t] = kind == 0 ? a - 1 : 1 - a;
+      g.dw[t] = kind == 0 ? b - 1 : 1 - b;
+      g.dp[t] = 0;
+    }
+    g.OHo = Hin; g.OWo = Win; g.osh = 1; g.osw = 1; g.OCp = ncols; g.CB = ncols;
+  } else if (kind == 2 || kind == 5) {  // fine input -> coarse output
+    g.inC = 2 * cin_tensor; g.inW = Win / 2; g.inP = 2; g.inH = Hin / 2;
+    g.OH = Hin / 2; g.OW = Win / 2;
+    g.ntaps = 2;
+    for (int t = 0; t < 2; ++t) { g.dh[t] = 0; g.dw[t] = 0; g.dp[t] = t; }
+    g.OHo = Hin / 2; g.OWo = Win / 2; g.osh = 1; g.osw = 1; g.OCp = ncols; g.CB = ncols;
+  } else {  // coarse input -> fine output (scatter)
+    g.inC = cin_tensor; g.inW = Win; g.inP = 1; g.inH = Hin;
+    g.OH = Hin; g.OW = Win;
+    g.ntaps = 1;
+    g.dh[0] = 0; g.dw[0] = 0; g.dp[0] = 0;
+    const int fine_c = ncols / 4;
+    g.OHo = 2 * Hin; g.osh = 2; g.CB = 2 * fine_c; g.OWo = Win; g.osw = 1; g.OCp = 2 * fine_c;
+  }
+  tile_grid(g);
+  return g;
+}
+
+int act_epi(ideq_ctx* ctx, int epi) {
+  if (ctx->net.act == IDEQ_ACT_IDENTITY && (epi == EPI_SOFTPLUS || epi == EPI_SIGMUL)) return EPI_STORE;
+  return epi;
+}
+
+ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, int Hin, int Win, const void* in,
+                     void* out, const void* aux, int epi, const std::string& lname) {
+  Layer L;
+  L.kind = L_GEMM;
+  L.name = lname;
+  const std::string key = wname + "#" + std::to_string(kind) + (use_tc(ctx) ? "tc" : "simt");
+  int ncols = 0, ntaps = 0, ktap = 0;
+  // weights are uploaded once per (conv, direction)
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  auto& sl = ws.t[wname];
+  const float* Wt = ctx->blob.data() + sl.first;
+  // channel count of the READ tensor
+  int cin_tensor;
+  {
+    std::vector<float> dummy;
+    int nc, nt, kt;
+    (void)dummy;
+    // shape-derived quantities (without building B)
+    if (kind == 0) { nc = sl.second[0]; kt = sl.second[1]; }
+    else if (kind == 1) { nc = sl.second[1]; kt = sl.second[0]; }
+    else if (kind == 2 || kind == 5) { nc = sl.second[0]; kt = 2 * sl.second[1]; }
+    else { nc = 4 * sl.second[1]; kt = sl.second[0]; }
+    (void)nt;
+    ncols = nc;
+    ktap = kt;
+    cin_tensor = (kind == 2 || kind == 5) ? kt / 2 : kt;
+  }
+  L.tc = use_tc(ctx);
+  const int KC = pick_kc(L.tc, ktap);
+  if (!ctx->wdev.count(key)) {
+    std::vector<float> B = gemm_weights(kind, Wt, sl.second, KC, ncols, ntaps, ktap);
+    ideq_status st = upload_gemm_weights(ctx, key, B);
+    if (st) return st;
+  }
+  L.g = make_geom(kind, N, Hin, Win, cin_tensor, ncols, KC, ktap, act_epi(ctx, epi));
+  L.in = in;
+  L.wB = ctx->wdev[key];
+  L.out = out;
+  L.aux = aux;
+  const double P = (double)N * L.g.OH * L.g.OW;
+  L.flops = 2.0 * P * ncols * (double)(L.g.ntaps * ktap);
+  const double in_elems = (double)N * L.g.inH * L.g.inW * L.g.inP * L.g.inC;
+  const double out_elems = P * ncols;
+  L.bytes = ctx->elt * (in_elems + out_elems * ((L.g.epi == EPI_RESADD || L.g.epi == EPI_SIGMUL) ? 2.0 : 1.0)) +
+            ctx->elt * (double)ncols * L.g.ntaps * ktap;
+  if (L.tc) {
+    if (!tc_supported(L.g)) return fail(ctx, IDEQ_E_UNSUPPORTED, "layer %s: geometry not supported by tcgen05 path", lname.c_str());
+    char err[256] = {0};
+    L.plan = tc_make_plan(L.g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)out,
+                          (const __nv_bfloat16*)aux, ctx->num_sms, err, sizeof(err));
+    if (!L.plan) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
+  }
+  ctx->prog.push_back(L);
+  return IDEQ_OK;
+}
+
+ideq_status add_headtail(ideq_ctx* ctx, LayerKind kind, const std::string& wname, bool adjoint, int N,
+                         const float* in_img, const void* in_feat, void* out_feat, float* out_img, const void* aux,
+                         const float* aux_img, float alpha, int epi, const std::string& lname) {
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  auto& sl = ws.t[wname];
+  const float* Wt = ctx->blob.data() + sl.first;
+  const int o_n = sl.second[0], i_n = sl.second[1];
+  const std::string key = wname + (adjoint ? "#T" : "#F");
+  if (!ctx->wdev.count(key)) {
+    std::vector<float> v;
+    if (adjoint) v = flip_transpose3x3(Wt, o_n, i_n);
+    else v.assign(Wt, Wt + (size_t)o_n * i_n * 9);
+    ideq_status st = upload_f32(ctx, key, v);
+    if (st) return st;
+  }
+  Layer L;
+  L.kind = kind;
+  L.name = lname;
+  L.wB = ctx->wdev[key];
+  L.N = N; L.H = ctx->H; L.W = ctx->W;
+  L.C = ctx->C;
+  // feature width: image->feature layers produce it, feature->image layers consume it
+  if (kind == L_IMG2FEAT) L.wfeat = adjoint ? i_n : o_n;
+  else L.wfeat = adjoint ? o_n : i_n;
+  L.in_img = in_img;
+  L.in = in_feat;
+  L.out = out_feat;
+  L.out_img = out_img;
+  L.aux = aux;
+  L.aux_img = aux_img;
+  L.alpha = alpha;
+  L.epi = act_epi(ctx, epi);
+  const double P = (double)N * ctx->H * ctx->W;
+  L.flops = 2.0 * P * 9.0 * o_n * i_n;
+  L.bytes = P * (4.0 * ctx->C + ctx->elt * L.wfeat * ((aux || aux_img) ? 2.0 : 1.0));
+  ctx->prog.push_back(L);
+  return IDEQ_OK;
+}
+
+std::string rb(const char* p, int l, int r, const char* ab) {
+  return std::string(p) + std::to_string(l) + "." + std::to_string(r) + "." + ab;
+}
+
+// Build the forward + VJP program for batch N (buffers sized for maxN at create).
+ideq_status build_program(ideq_ctx* ctx, int N) {
+  if (ctx->prog_batch == N) return IDEQ_OK;
+  for (auto& L : ctx->prog) if (L.plan) tc_free_plan(L.plan);
+  ctx->prog.clear();
+  const auto& n = ctx->net;
+  const int C = ctx->C;
+  ideq_status st;
+  if (n.arch == IDEQ_NET_TINY3) {
+    void* a1 = ctx->saved["a1"];
+    void* a2 = ctx->saved["a2"];
+    void* q = ctx->lvl_buf[0][0];
+    void* q1 = ctx->lvl_buf[0][1];
+    const int H = ctx->H, W = ctx->W;
+    if ((st = add_headtail(ctx, L_IMG2FEAT, "c1", false, N, ctx->Z, nullptr, a1, nullptr, nullptr, nullptr, 0.f,
+                           EPI_SOFTPLUS, "c1")))
+      return st;
+    if ((st = add_gemm(ctx, "c2", 0, N, H, W, a1, a2, nullptr, EPI_SOFTPLUS, "c2"))) return st;
+    if ((st = add_headtail(ctx, L_FEAT2IMG, "c3", false, N, nullptr, a2, nullptr, ctx->Hc, nullptr,
+                           n.identity_skip ? nullptr : ctx->Z, n.identity_skip ? 0.f : -1.f, EPI_STORE, "c3")))
+      return st;
+    ctx->n_fwd = (int)ctx->prog.size();
+    if ((st = add_headtail(ctx, L_IMG2FEAT, "c3", true, N, ctx->Hc, nullptr, q, nullptr, a2, nullptr, 0.f,
+                           EPI_SIGMUL, "c3T")))
+      return st;
+    if ((st = add_gemm(ctx, "c2", 1, N, H, W, q, q1, a1, EPI_SIGMUL, "c2T"))) return st;
+    if ((st = add_headtail(ctx, L_FEAT2IMG, "c1", true, N, nullptr, q1, nullptr, ctx->G, nullptr,
+                           n.identity_skip ? nullptr : ctx->Hc, n.identity_skip ? 0.f : -1.f, EPI_STORE, "c1T")))
+      return st;
+  } else {
+    const int R = n.res_blocks;
+    int Hl[4], Wl[4];
+    for (int l = 0; l < 4; ++l) { Hl[l] = ctx->H >> l; Wl[l] = ctx->W >> l; }
+    auto B = [&](int l, int i) { return ctx->lvl_buf[l][i]; };
+    // ---- forward
+    if ((st = add_headtail(ctx, L_IMG2FEAT, "head", false, N, ctx->Z, nullptr, B(0, 0), nullptr, nullptr, nullptr,
+                           0.f, EPI_STORE, "head")))
+      return st;
+    int cur[4] = {0, 0, 0, 0};
+    int skip_idx[3] = {0, 0, 0};
+    for (int l = 0; l < 4; ++l) {
+      for (int r = 0; r < R; ++r) {
+        void* a = ctx->saved["e" + std::to_string(l) + "." + std::to_string(r)];
+        const int o = cur[l] == 0 ? 1 : 0;
+        if ((st = add_gemm(ctx, rb("e", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
+                           rb("e", l, r, "A"))))
+          return st;
+        if ((st = add_gemm(ctx, rb("e", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o), B(l, cur[l]), EPI_RESADD,
+                           rb("e", l, r, "B"))))
+          return st;
+        cur[l] = o;
+      }
+      if (l < 3) {
+        skip_idx[l] = cur[l];
+        if ((st = add_gemm(ctx, "down" + std::to_string(l), 2, N, Hl[l], Wl[l], B(l, cur[l]), B(l + 1, 0), nullptr,
+                           EPI_STORE, "down" + std::to_string(l))))
+          return st;
+        cur[l + 1] = 0;
+      }
+    }
+    for (int l = 2; l >= 0; --l) {
+      const int o = skip_idx[l] == 0 ? 1 : 0;
+      if ((st = add_gemm(ctx, "up" + std::to_string(l), 4, N, Hl[l + 1], Wl[l + 1], B(l + 1, cur[l + 1]), B(l, o),
+                         B(l, skip_idx[l]), EPI_RESADD, "up" + std::to_string(l))))
+        return st;
+      cur[l] = o;
+      for (int r = 0; r < R; ++r) {
+        void* a = ctx->saved["d" + std::to_string(l) + "." + std::to_string(r)];
+        const int o2 = cur[l] == 0 ? 1 : 0;
+        if ((st = add_gemm(ctx, rb("d", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
+                           rb("d", l, r, "A"))))
+          return st;
+        if ((st = add_gemm(ctx, rb("d", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o2), B(l, cur[l]), EPI_RESADD,
+                           rb("d", l, r, "B"))))
+          return st;
+        cur[l] = o2;
+      }
+    }
+    if ((st = add_headtail(ctx, L_FEAT2IMG, "tail", false, N, nullptr, B(0, cur[0]), nullptr, ctx->Hc, nullptr,
+                           n.identity_skip ? nullptr : ctx->Z, n.identity_skip ? 0.f : -1.f, EPI_STORE, "tail")))
+      return st;
+    ctx->n_fwd = (int)ctx->prog.size();
+    // ---- VJP, cotangent Hc
+    if ((st = add_headtail(ctx, L_IMG2FEAT, "tail", true, N, ctx->Hc, nullptr, B(0, 0), nullptr, nullptr, nullptr,
+                           0.f, EPI_STORE, "tailT")))
+      return st;
+    int g[4] = {0, 0, 0, 0};
+    int gs[3] = {0, 0, 0};
+    auto rb_vjp = [&](const char* p, int l, int r) -> ideq_status {
+      void* a = ctx->saved[std::string(p) + std::to_string(l) + "." + std::to_string(r)];
+      const int o = g[l] == 0 ? 1 : 0;
+      ideq_status s2;
+      // q = (B^T g) . sp'(a) ; g' = g + A^T q
+      if ((s2 = add_gemm(ctx, rb(p, l, r, "B"), 1, N, Hl[l], Wl[l], B(l, g[l]), B(l, 2), a, EPI_SIGMUL,
+                         rb(p, l, r, "BT"))))
+        return s2;
+      if ((s2 = add_gemm(ctx, rb(p, l, r, "A"), 1, N, Hl[l], Wl[l], B(l, 2), B(l, o), B(l, g[l]), EPI_RESADD,
+                         rb(p, l, r, "AT"))))
+        return s2;
+      g[l] = o;
+      return IDEQ_OK;
+    };
+    for (int l = 0; l <= 2; ++l) {
+      for (int r = R - 1; r >= 0; --r)
+        if ((st = rb_vjp("d", l, r))) return st;
+      gs[l] = g[l];
+      if ((st = add_gemm(ctx, "up" + std::to_string(l), 5, N, Hl[l], Wl[l], B(l, g[l]), B(l + 1, 0), nullptr,
+                         EPI_STORE, "up" + std::to_string(l) + "T")))
+        return st;
+      g[l + 1] = 0;
+    }
+    for (int l = 3; l >= 0; --l) {
+      if (l < 3) {
+        const int o = gs[l] == 0 ? 1 : 0;
+        if ((st = add_gemm(ctx, "down" + std::to_string(l), 3, N, Hl[l + 1], Wl[l + 1], B(l + 1, g[l + 1]), B(l, o),
+                           B(l, gs[l]), EPI_RESADD, "down" + std::to_string(l) + "T")))
+          return st;
+        g[l] = o;
+      }
+      for (int r = R - 1; r >= 0; --r)
+        if ((st = rb_vjp("e", l, r))) return st;
+    }
+    if ((st = add_headtail(ctx, L_FEAT2IMG, "head", true, N, nullptr, B(0, g[0]), nullptr, ctx->G, nullptr,
+                           n.identity_skip ? nullptr : ctx->Hc, n.identity_skip ? 0.f : -1.f, EPI_STORE, "headT")))
+      return st;
+  }
+  ctx->prog_batch = N;
+  ctx->graph_key.clear();
+  return IDEQ_OK;
+}
+
+// ------------------------------------------------------------------ launching (optionally profiled)
+cudaEvent_t next_event(ideq_ctx* ctx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    ctx->ev_pool.push_back(e);
+  }
+  return ctx->ev_pool[ctx->ev_used++];
+}
+
+struct Prof {
+  ideq_ctx* ctx;
+  int cls;
+  double flops, bytes;
+  cudaEvent_t a = nullptr;
+  Prof(ideq_ctx* c, int k, double f = 0, double b = 0) : ctx(c), cls(k), flops(f), bytes(b) {
+    if (ctx->profiling) { a = next_event(ctx); cudaEventRecord(a, ctx->stream); }
+  }
+  ~Prof() {
+    if (ctx->profiling) {
+      cudaEvent_t b = next_event(ctx);
+      cudaEventRecord(b, ctx->stream);
+      ctx->pending.push_back({a, b, cls, flops, bytes});
+    }
+  }
+};
+
+void collect_profile(ideq_ctx* ctx) {
+  if (ctx->pending.empty()) return;
+  cudaStreamSynchronize(ctx->stream);
+  for (auto& e : ctx->pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e.a, e.b);
+    ctx->prof.ms[e.cls] += ms;
+    ctx->prof.launches[e.cls] += 1;
+    ctx->prof.flops[e.cls] += e.flops;
+    ctx->prof.bytes[e.cls] += e.bytes;
+  }
+  ctx->pending.clear();
+  ctx->ev_used = 0;
+}
+
+void run_layer(ideq_ctx* ctx, const Layer& L) {
+  cudaStream_t s = ctx->stream;
+  const bool bf = ctx->prec == IDEQ_PREC_BF16;
+  if (L.kind == L_GEMM) {
+    if (L.tc) {
+      Prof p(ctx, IDEQ_K_CONV_TC, L.flops, L.bytes);
+      tc_launch(L.plan, s);
+    } else {
+      Prof p(ctx, IDEQ_K_CONV_SIMT, L.flops, L.bytes);
+      if (bf)
+        launch_conv_simt<__nv_bfloat16>(L.g, (const __nv_bfloat16*)L.in, (const __nv_bfloat16*)L.wB,
+                                        (__nv_bfloat16*)L.out, (const __nv_bfloat16*)L.aux, s);
+      else
+        launch_conv_simt<float>(L.g, (const float*)L.in, (const float*)L.wB, (float*)L.out, (const float*)L.aux, s);
+    }
+  } else if (L.kind == L_IMG2FEAT) {
+    Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
+    if (bf)
+      launch_img2feat<__nv_bfloat16>(L.in_img, (const float*)L.wB, (__nv_bfloat16*)L.out, (const __nv_bfloat16*)L.aux,
+                                     L.epi, L.N, L.C, L.H, L.W, L.wfeat, s);
+    else
+      launch_img2feat<float>(L.in_img, (const float*)L.wB, (float*)L.out, (const float*)L.aux, L.epi, L.N, L.C, L.H,
+                             L.W, L.wfeat, s);
+  } else {
+    Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
+    if (bf)
+      launch_feat2img<__nv_bfloat16>((const __nv_bfloat16*)L.in, (const float*)L.wB, L.out_img, L.aux_img, L.alpha,
+                                     L.N, L.C, L.H, L.W, L.wfeat, s);
+    else
+      launch_feat2img<float>((const float*)L.in, (const float*)L.wB, L.out_img, L.aux_img, L.alpha, L.N, L.C, L.H,
+                             L.W, L.wfeat, s);
+  }
+}
+
+void run_network(ideq_ctx* ctx) {
+  for (const auto& L : ctx->prog) run_layer(ctx, L);
+}
+
+// ------------------------------------------------------------------ fidelity + step
+StepArgs make_step_args(ideq_ctx* ctx, int N, const float* y, float* x0, const ideq_params* p) {
+  StepArgs a{};
+  a.N = N; a.C = ctx->C; a.H = ctx->H; a.W = ctx->W;
+  a.d = (long long)ctx->C * ctx->H * ctx->W;
+  a.z = ctx->Z; a.zout = ctx->Z; a.gg = ctx->G; a.y = y;
+  a.X0 = x0; a.X1 = ctx->X1;
+  a.mask = ctx->d_mask; a.fbuf = ctx->fbuf; a.fbuf2 = ctx->fbuf2;
+  a.kern = ctx->d_kern; a.ksize = ctx->op.ksize; a.kernel_per_image = ctx->op.kernel_per_image;
+  if (p) { a.lam = p->lambda; a.tau = p->tau; a.beta = p->beta; }
+  a.active = ctx->active; a.kdev = ctx->kdev; a.partials = ctx->partials;
+  return a;
+}
+
+int step_parts(ideq_ctx* ctx) {
+  if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.blur_impl == IDEQ_BLUR_DIRECT && ctx->op.step == IDEQ_STEP_GRAD)
+    return blur_parts_per_image(ctx->C, ctx->H, ctx->W);
+  const long long d = (long long)ctx->C * ctx->H * ctx->W;
+  long long parts = d / 4096;
+  if (parts < 1) parts = 1;
+  if (parts > 256) parts = 256;
+  return (int)parts;
+}
+
+void run_step(ideq_ctx* ctx, const StepArgs& a0) {
+  StepArgs a = a0;
+  a.parts = step_parts(ctx);
+  cudaStream_t s = ctx->stream;
+  const auto& op = ctx->op;
+  if (op.kind == IDEQ_OP_INPAINT) {
+    Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 7.0);
+    launch_pointwise_step(op.step == IDEQ_STEP_PROX ? STEP_PROX_INPAINT : STEP_GRAD_INPAINT, a, s);
+  } else if (op.kind == IDEQ_OP_BLUR) {
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 2.0 * a.N * a.d * op.ksize * op.ksize, (double)a.N * a.d * 12.0);
+      launch_blur_residual(a, s);
+    }
+    Prof p(ctx, IDEQ_K_STEP, 2.0 * a.N * a.d * op.ksize * op.ksize, (double)a.N * a.d * 4.0 * 6.0);
+    launch_blur_adjoint(1, a, ctx->fbuf, s);
+  }
+}
+
+FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
+  FinalizeArgs f{};
+  f.N = N;
+  f.parts = step_parts(ctx);
+  f.check_every = p ? p->check_every : 1;
+  f.stop_rule = p ? (int)p->stop_rule : 0;
+  f.tol = p ? p->tol : 0.f;
+  f.partials = ctx->partials;
+  f.active = ctx->active; f.status = ctx->status; f.iters = ctx->iters;
+  f.res = ctx->res; f.r_now = ctx->r_now; f.trace = ctx->trace; f.rmax = ctx->rmax;
+  f.n_active = ctx->n_active; f.kdev = ctx->kdev;
+  return f;
+}
+
+// One iteration: network (forward + VJP), fidelity + update + partials, finalize, advance.
+ideq_status enqueue_iteration(ideq_ctx* ctx, const StepArgs& a, const FinalizeArgs& f, bool with_allreduce) {
+  run_network(ctx);
+  run_step(ctx, a);
+  {
+    Prof p(ctx, IDEQ_K_REDUCE);
+    launch_finalize(f, ctx->stream);
+    launch_advance_a(f, ctx->stream);
+    if (with_allreduce && ctx->world > 1) {
+      int r = g_nccl.AllReduce(ctx->rmax, ctx->rmax, 1, NCCL_FLOAT32, NCCL_MAX, ctx->comm, ctx->stream);
+      if (r != 0) return fail(ctx, IDEQ_E_NCCL, "ncclAllReduce failed: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
+    }
+    launch_advance_b(f, ctx->stream);
+  }
+  return IDEQ_OK;
+}
+
+ideq_status check_ctx(ideq_ctx* ctx) {
+  if (!ctx) return IDEQ_E_INVALID;
+  if (ctx->poisoned) return fail(ctx, IDEQ_E_STATE, "context poisoned by an earlier CUDA/NCCL error: %s", ctx->err.c_str());
+  cudaError_t e = cudaSetDevice(ctx->device);
+  if (e != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "cudaSetDevice: %s", cudaGetErrorString(e));
+  return IDEQ_OK;
+}
+
+ideq_status validate_params(ideq_ctx* ctx, int batch, const ideq_params* p) {
+  if (!p) return fail(ctx, IDEQ_E_INVALID, "params is NULL");
+  if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch %d outside [1, %d]", batch, ctx->maxN);
+  if (!(p->tau > 0.f) || !(p->lambda >= 0.f) || !(p->beta >= 0.f && p->beta < 1.f) || p->max_iter < 1 ||
+      !(p->tol >= 0.f) || p->check_every < 1 || (p->stop_rule != IDEQ_STOP_PER_IMAGE && p->stop_rule != IDEQ_STOP_GLOBAL_MAX))
+    return fail(ctx, IDEQ_E_INVALID, "invalid params (tau>0, lambda>=0, 0<=beta<1, max_iter>=1, tol>=0, check_every>=1)");
+  if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "ideq_set_operator must be called before solving");
+  if (batch > ctx->op_batch && (ctx->op.kernel_per_image || ctx->op.kind == IDEQ_OP_INPAINT))
+    return fail(ctx, IDEQ_E_INVALID, "batch %d exceeds the operator's batch %d", batch, ctx->op_batch);
+  return IDEQ_OK;
+}
+
+ideq_status operator_runnable(ideq_ctx* ctx) {
+  const auto& op = ctx->op;
+  if (op.kind == IDEQ_OP_PHASE && op.step == IDEQ_STEP_PROX)
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "phase retrieval has no closed-form prox (cf. PAPER l.1079)");
+  if (op.kind == IDEQ_OP_PHASE) return fail(ctx, IDEQ_E_UNSUPPORTED, "phase retrieval FFT path not built yet");
+  if (op.kind == IDEQ_OP_BLUR && (op.step == IDEQ_STEP_PROX || op.blur_impl == IDEQ_BLUR_FFT))
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT blur path not built yet");
+  return IDEQ_OK;
+}
+
+ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const ideq_params* p,
+                         ideq_image_stat* stats, float* trace_host) {
+  ideq_status st;
+  if ((st = validate_params(ctx, N, p))) return st;
+  if ((st = operator_runnable(ctx))) return st;
+  if (!y || !x || !stats) return fail(ctx, IDEQ_E_INVALID, "NULL y/x/stats");
+  if ((st = build_program(ctx, N))) return st;
+  const long long d = (long long)ctx->C * ctx->H * ctx->W;
+  cudaStream_t s = ctx->stream;
+  // x^{-1} = x^0; z^0 = x^0
+  CK(cudaMemcpyAsync(ctx->X1, x, sizeof(float) * N * d, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(ctx->Z, x, sizeof(float) * N * d, cudaMemcpyDeviceToDevice, s));
+  FinalizeArgs f = make_fin(ctx, N, p);
+  if (f.parts > ctx->parts_cap) return fail(ctx, IDEQ_E_INVALID, "internal: partial buffer too small");
+  launch_init_state(f, s);
+  StepArgs a = make_step_args(ctx, N, y, x, p);
+  const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
+  const bool poll = p->tol > 0.f;
+  const int poll_every = global ? p->check_every : 4;
+  if (ctx->profiling) {
+    for (int k = 0; k < p->max_iter; ++k) {
+      const bool chk = global && ((k + 1) % p->check_every == 0);
+      if ((st = enqueue_iteration(ctx, a, f, chk))) return st;
+      if (poll && ((k + 1) % poll_every == 0)) {
+        CK(cudaMemcpyAsync(ctx->h_pinned, ctx->n_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (*ctx->h_pinned == 0) break;
+      }
+    }
+    collect_profile(ctx);
+  } else {
+    // capture one iteration (plain and with the convergence all-reduce)
+    char keybuf[256];
+    snprintf(keybuf, sizeof(keybuf), "%p|%p|%d|%a|%a|%a|%a|%d|%d", (const void*)y, (void*)x, N, p->lambda, p->tau,
+             p->beta, p->tol, p->check_every, (int)p->stop_rule);
+    if (ctx->graph_key != keybuf) {
+      if (ctx->gexec_plain) { cudaGraphExecDestroy(ctx->gexec_plain); ctx->gexec_plain = nullptr; }
+      if (ctx->gexec_check) { cudaGraphExecDestroy(ctx->gexec_check); ctx->gexec_check = nullptr; }
+      for (int v = 0; v < 2; ++v) {
+        if (v == 1 && !(global && ctx->world > 1)) break;
+        cudaGraph_t graph;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        ideq_status st2 = enqueue_iteration(ctx, a, f, v == 1);
+        cudaError_t ec = cudaStreamEndCapture(s, &graph);
+        if (st2) return st2;
+        if (ec != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "graph capture: %s", cudaGetErrorString(ec));
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, graph, 0));
+        cudaGraphDestroy(graph);
+        (v == 0 ? ctx->gexec_plain : ctx->gexec_check) = ge;
+      }
+      ctx->graph_key = keybuf;
+    }
+    for (int k = 0; k < p->max_iter; ++k) {
+      const bool chk = global && ctx->world > 1 && ((k + 1) % p->check_every == 0);
+      CK(cudaGraphLaunch(chk ? ctx->gexec_check : ctx->gexec_plain, s));
+      if (poll && ((k + 1) % poll_every == 0) && k + 1 < p->max_iter) {
+        CK(cudaMemcpyAsync(ctx->h_pinned, ctx->n_active, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (*ctx->h_pinned == 0) break;
+      }
+    }
+  }
+  launch_gather(ctx->iters, ctx->X1, x, N, d, s);
+  std::vector<int> it(N), stv(N);
+  std::vector<float> rs(N);
+  CK(cudaMemcpyAsync(it.data(), ctx->iters, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(stv.data(), ctx->status, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(rs.data(), ctx->res, sizeof(float) * N, cudaMemcpyDeviceToHost, s));
+  if (trace_host) {
+    const int nt = p->max_iter < ctx->trace_cap ? p->max_iter : ctx->trace_cap;
+    // iterations that never ran report NaN
+    std::vector<float> tr(nt);
+    CK(cudaMemcpyAsync(tr.data(), ctx->trace, sizeof(float) * nt, cudaMemcpyDeviceToHost, s));
+    int kdone = 0;
+    CK(cudaMemcpyAsync(&kdone, ctx->kdev, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < p->max_iter; ++k) trace_host[k] = (k < nt && k < kdone) ? tr[k] : NAN;
+  }
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  bool diverged = false;
+  for (int i = 0; i < N; ++i) {
+    stats[i].iters = it[i];
+    stats[i].residual = rs[i];
+    stats[i].status = stv[i];
+    if (stv[i] == 2) diverged = true;
+  }
+  if (diverged) return fail(ctx, IDEQ_E_DIVERGED, "at least one image produced a non-finite iterate");
+  return IDEQ_OK;
+}
+
+}  // namespace
+
+namespace ideq {
+void init_kernel_attributes() {
+  static bool done = false;
+  if (done) return;
+  init_attrs_simt();
+  init_attrs_tc();
+  init_attrs_step();
+  done = true;
+}
+}  // namespace ideq
+
+// ======================================================================== C ABI
+extern "C" {
+
+int ideq_abi_version(void) { return IDEQ_ABI_VERSION; }
+
+const char* ideq_last_error(const ideq_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+ideq_status ideq_get_nccl_id(unsigned char out[128]) {
+  if (!out) return IDEQ_E_INVALID;
+  std::string err;
+  if (!g_nccl.load(err)) return IDEQ_E_NCCL;
+  nccl_uid id;
+  if (g_nccl.GetUniqueId(&id) != 0) return IDEQ_E_NCCL;
+  memcpy(out, &id, 128);
+  return IDEQ_OK;
+}
+
+ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int device, void* cuda_stream, int max_batch,
+                        int H, int W, const ideq_dist* dist, ideq_ctx** out) {
+  if (!net || !out || !net->weights) return IDEQ_E_INVALID;
+  *out = nullptr;
+  std::unique_ptr<ideq_ctx> holder(new ideq_ctx());
+  ideq_ctx* ctx = holder.get();
+  ctx->net = *net;
+  ctx->prec = prec;
+  ctx->device = device;
+  ctx->stream = (cudaStream_t)cuda_stream;
+  ctx->maxN = max_batch;
+  ctx->H = H;
+  ctx->W = W;
+  ctx->C = net->channels;
+  ctx->elt = prec == IDEQ_PREC_BF16 ? 2 : 4;
+  if (prec != IDEQ_PREC_FP32 && prec != IDEQ_PREC_BF16) return IDEQ_E_INVALID;
+  if (max_batch < 1 || H < 1 || W < 1 || !(net->channels == 1 || net->channels == 3)) return IDEQ_E_INVALID;
+  WeightSlices ws;
+  size_t total = 0;
+  if (net->arch == IDEQ_NET_TINY3) {
+    const int w = net->widths[0];
+    if (!(w == 16 || w == 32 || w == 64)) return IDEQ_E_INVALID;
+  } else if (net->arch == IDEQ_NET_UNET4) {
+    if (H % 8 || W % 8 || net->res_blocks < 1) return IDEQ_E_INVALID;
+    if (!(net->widths[0] == 32 || net->widths[0] == 64)) return IDEQ_E_INVALID;
+    for (int l = 0; l < 4; ++l)
+      if (net->widths[l] < 16 || net->widths[l] % 16) return IDEQ_E_INVALID;
+    if (prec == IDEQ_PREC_BF16)
+      for (int l = 0; l < 4; ++l)
+        if (net->widths[l] % 32) return IDEQ_E_INVALID;
+  } else {
+    return IDEQ_E_INVALID;
+  }
+  slice_weights(*net, ws, total);
+  if (total != net->n_weights) return IDEQ_E_INVALID;
+  ctx->blob.assign(net->weights, net->weights + total);
+  ctx->net.weights = nullptr;
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    *out = holder.release();
+    return fail(*out, IDEQ_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
+  }
+  cudaDeviceProp prop;
+  if (cudaSetDevice(device) != cudaSuccess || cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    *out = holder.release();
+    return fail(*out, IDEQ_E_CUDA, "cannot use device %d", device);
+  }
+  if (prop.major != 10) {
+    *out = holder.release();
+    return fail(*out, IDEQ_E_CUDA, "device %d is sm_%d%d; this library is built for sm_100a only", device, prop.major,
+                prop.minor);
+  }
+  ctx->num_sms = prop.multiProcessorCount;
+  init_kernel_attributes();
+  if (!ctx->stream) {
+    // graph capture is not allowed on the legacy default stream: own a stream instead
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      *out = holder.release();
+      return fail(*out, IDEQ_E_CUDA, "cannot create a stream");
+    }
+    ctx->own_stream = true;
+  }
+
+  // ---- feature buffers
+  const int N = max_batch;
+  ideq_status st;
+  if (net->arch == IDEQ_NET_TINY3) {
+    const size_t e = (size_t)N * H * W * net->widths[0] * ctx->elt;
+    ctx->lvl_buf.assign(1, std::vector<void*>(3, nullptr));
+    for (int i = 0; i < 2; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[0][i], e))) { *out = holder.release(); return st; }
+    void* a1; void* a2;
+    if ((st = dalloc(ctx, &a1, e)) || (st = dalloc(ctx, &a2, e))) { *out = holder.release(); return st; }
+    ctx->saved["a1"] = a1;
+    ctx->saved["a2"] = a2;
+  } else {
+    ctx->lvl_buf.assign(4, std::vector<void*>(3, nullptr));
+    for (int l = 0; l < 4; ++l) {
+      const size_t e = (size_t)N * (H >> l) * (W >> l) * net->widths[l] * ctx->elt;
+      for (int i = 0; i < 3; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[l][i], e))) { *out = holder.release(); return st; }
+      for (int r = 0; r < net->res_blocks; ++r) {
+        void* a;
+        if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
+        ctx->saved["e" + std::to_string(l) + "." + std::to_string(r)] = a;
+        if (l < 3) {
+          if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
+          ctx->saved["d" + std::to_string(l) + "." + std::to_string(r)] = a;
+        }
+      }
+    }
+  }
+  // ---- solver state
+  const size_t plane = (size_t)N * ctx->C * H * W * sizeof(float);
+  void* p;
+#define AL(field, bytes)                                                          \
+  if ((st = dalloc(ctx, &p, (bytes)))) { *out = holder.release(); return st; } \
+  ctx->field = (decltype(ctx->field))p;
+  AL(X1, plane) AL(Z, plane) AL(G, plane) AL(Hc, plane) AL(fbuf, plane) AL(fbuf2, plane)
+  ctx->parts_cap = 1024;
+  AL(partials, (size_t)N * ctx->parts_cap * 3 * sizeof(float))
+  AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int))
+  AL(res, N * sizeof(float)) AL(r_now, N * sizeof(float)) AL(rmax, 16) AL(n_active, 16) AL(kdev, 16)
+  AL(trace, ctx->trace_cap * sizeof(float))
+#undef AL
+  if (cudaMallocHost(&ctx->h_pinned, 64) != cudaSuccess) { *out = holder.release(); return fail(*out, IDEQ_E_NOMEM, "pinned alloc"); }
+  cudaMemset(ctx->trace, 0xff, ctx->trace_cap * sizeof(float));
+
+  // ---- distribution
+  if (dist && dist->world > 1) {
+    std::string err;
+    if (!g_nccl.load(err)) { *out = holder.release(); return fail(*out, IDEQ_E_NCCL, "%s", err.c_str()); }
+    nccl_uid id;
+    memcpy(&id, dist->nccl_id, 128);
+    int r = g_nccl.CommInitRank(&ctx->comm, dist->world, id, dist->rank);
+    if (r != 0) { *out = holder.release(); return fail(*out, IDEQ_E_NCCL, "ncclCommInitRank failed (%d)", r); }
+    ctx->rank = dist->rank;
+    ctx->world = dist->world;
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { *out = holder.release(); return fail(*out, IDEQ_E_CUDA, "create: %s", cudaGetErrorString(e)); }
+  *out = holder.release();
+  return IDEQ_OK;
+}
+
+ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int batch) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!op || batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "bad operator or batch");
+  const int H = ctx->H, W = ctx->W;
+  if (op->kind == IDEQ_OP_BLUR) {
+    if (!op->kernels || op->ksize < 1 || op->ksize % 2 == 0 || op->ksize > 63)
+      return fail(ctx, IDEQ_E_INVALID, "blur needs an odd ksize <= 63 and kernels");
+    if (op->step == IDEQ_STEP_PROX && op->blur_impl != IDEQ_BLUR_FFT)
+      return fail(ctx, IDEQ_E_INVALID, "the blur prox needs blur_impl = FFT");
+    const size_t n = (size_t)(op->kernel_per_image ? batch : 1) * op->ksize * op->ksize;
+    void* p;
+    if ((st = dalloc(ctx, &p, n * 4))) return st;
+    CK(cudaMemcpy(p, op->kernels, n * 4, cudaMemcpyHostToDevice));
+    ctx->d_kern = (float*)p;
+  } else if (op->kind == IDEQ_OP_INPAINT) {
+    if (!op->masks) return fail(ctx, IDEQ_E_INVALID, "inpainting needs masks");
+    void* p;
+    if ((st = dalloc(ctx, &p, (size_t)batch * H * W))) return st;
+    CK(cudaMemcpy(p, op->masks, (size_t)batch * H * W, cudaMemcpyHostToDevice));
+    ctx->d_mask = (uint8_t*)p;
+  } else if (op->kind == IDEQ_OP_PHASE) {
+    if (ctx->C != 1) return fail(ctx, IDEQ_E_INVALID, "phase retrieval needs C = 1");
+    if (op->step == IDEQ_STEP_PROX) return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval");
+    if (!op->phase_masks || op->n_phase < 1) return fail(ctx, IDEQ_E_INVALID, "phase retrieval needs phase masks");
+    void* p;
+    const size_t n = (size_t)op->n_phase * H * W * 2;
+    if ((st = dalloc(ctx, &p, n * 4))) return st;
+    CK(cudaMemcpy(p, op->phase_masks, n * 4, cudaMemcpyHostToDevice));
+    ctx->d_phase = (float*)p;
+  } else {
+    return fail(ctx, IDEQ_E_INVALID, "unknown operator kind");
+  }
+  ctx->op = *op;
+  ctx->op.kernels = nullptr;
+  ctx->op.masks = nullptr;
+  ctx->op.phase_masks = nullptr;
+  ctx->op_batch = batch;
+  ctx->op_set = true;
+  ctx->graph_key.clear();
+  return IDEQ_OK;
+}
+
+ideq_status ideq_solve(ideq_ctx* ctx, const float* y, float* x_inout, int batch, const ideq_params* p,
+                       ideq_image_stat* stats, float* rmax_trace) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  return solve_device(ctx, y, x_inout, batch, p, stats, rmax_trace);
+}
+
+ideq_status ideq_solve_host(ideq_ctx* ctx, const float* y, float* x_inout, int batch, const ideq_params* p,
+                            ideq_image_stat* stats, float* rmax_trace) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!y || !x_inout) return fail(ctx, IDEQ_E_INVALID, "NULL y/x");
+  if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch out of range");
+  const size_t cy = ctx->op_set && ctx->op.kind == IDEQ_OP_PHASE ? (size_t)ctx->op.n_phase : (size_t)ctx->C;
+  const size_t ny = (size_t)batch * cy * ctx->H * ctx->W, nx = (size_t)batch * ctx->C * ctx->H * ctx->W;
+  if (ny > ctx->dstage_y_n) {
+    void* p2;
+    if ((st = dalloc(ctx, &p2, ny * 4))) return st;
+    ctx->dstage_y = (float*)p2;
+    ctx->dstage_y_n = ny;
+    ctx->graph_key.clear();
+  }
+  if (nx > ctx->dstage_x_n) {
+    void* p2;
+    if ((st = dalloc(ctx, &p2, nx * 4))) return st;
+    ctx->dstage_x = (float*)p2;
+    ctx->dstage_x_n = nx;
+    ctx->graph_key.clear();
+  }
+  CK(cudaMemcpyAsync(ctx->dstage_y, y, ny * 4, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaMemcpyAsync(ctx->dstage_x, x_inout, nx * 4, cudaMemcpyHostToDevice, ctx->stream));
+  st = solve_device(ctx, ctx->dstage_y, ctx->dstage_x, batch, p, stats, rmax_trace);
+  if (st != IDEQ_OK && st != IDEQ_E_DIVERGED) return st;
+  CK(cudaMemcpyAsync(x_inout, ctx->dstage_x, nx * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return st;
+}
+
+ideq_status ideq_grad_g(ideq_ctx* ctx, const float* z, float* grad_out, float* u_out, int batch) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!z || !grad_out) return fail(ctx, IDEQ_E_INVALID, "NULL z/grad");
+  if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch out of range");
+  if ((st = build_program(ctx, batch))) return st;
+  const size_t n = (size_t)batch * ctx->C * ctx->H * ctx->W;
+  CK(cudaMemcpyAsync(ctx->Z, z, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  run_network(ctx);
+  CK(cudaMemcpyAsync(grad_out, ctx->G, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  if (u_out) CK(cudaMemcpyAsync(u_out, ctx->Hc, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  collect_profile(ctx);
+  return IDEQ_OK;
+}
+
+ideq_status ideq_fidelity_grad(ideq_ctx* ctx, const float* y, const float* x, float* out, int batch) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "no operator");
+  if (!y || !x || !out || batch < 1 || batch > ctx->op_batch) return fail(ctx, IDEQ_E_INVALID, "bad arguments");
+  const auto& op = ctx->op;
+  if (op.kind == IDEQ_OP_INPAINT) {
+    launch_inpaint_grad(x, y, ctx->d_mask, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
+  } else if (op.kind == IDEQ_OP_BLUR && op.blur_impl == IDEQ_BLUR_DIRECT) {
+    StepArgs a = make_step_args(ctx, batch, y, nullptr, nullptr);
+    a.z = x;
+    a.active = nullptr;
+    a.fbuf2 = out;
+    launch_blur_residual(a, ctx->stream);
+    launch_blur_adjoint(0, a, ctx->fbuf, ctx->stream);
+  } else {
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "fidelity gradient not built for this operator yet");
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return IDEQ_OK;
+}
+
+ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, float tau, float* out, int batch) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "no operator");
+  if (!y || !v || !out || batch < 1 || batch > ctx->op_batch || !(tau > 0.f)) return fail(ctx, IDEQ_E_INVALID, "bad arguments");
+  if (ctx->op.kind == IDEQ_OP_INPAINT) {
+    launch_inpaint_prox(v, y, ctx->d_mask, tau, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
+  } else if (ctx->op.kind == IDEQ_OP_PHASE) {
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval (cf. PAPER l.1079)");
+  } else {
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT blur prox not built yet");
+  }
+  CK(cudaStreamSynchronize(ctx->stream));
+  CK(cudaGetLastError());
+  return IDEQ_OK;
+}
+
+ideq_status ideq_set_profiling(ideq_ctx* ctx, int enable) {
+  if (!ctx) return IDEQ_E_INVALID;
+  ctx->profiling = enable != 0;
+  return IDEQ_OK;
+}
+
+ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int reset) {
+  if (!ctx || !out) return IDEQ_E_INVALID;
+  collect_profile(ctx);
+  *out = ctx->prof;
+  if (reset) memset(&ctx->prof, 0, sizeof(ctx->prof));
+  return IDEQ_OK;
+}
+
+int ideq_launches_per_iteration(const ideq_ctx* ctx) {
+  if (!ctx) return 0;
+  int n = (int)ctx->prog.size();
+  if (ctx->op.kind == IDEQ_OP_BLUR) n += 2; else n += 1;
+  n += 3;  // finalize, advance_a, advance_b
+  return n;
+}
+
+int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0, int s1, int N, int Hin, int Win,
+                    const void* in, void* out, const void* aux, int epi, char* err, int errlen) {
+  auto seterr = [&](const char* m) { if (err && errlen > 0) { snprintf(err, errlen, "%s", m); } };
+  if (kind < 0 || kind > 5 || !w || !in || !out) { seterr("bad arguments"); return IDEQ_E_INVALID; }
+  if (use_tc_ && precision != IDEQ_PREC_BF16) { seterr("tcgen05 path is bf16 only"); return IDEQ_E_INVALID; }
+  init_kernel_attributes();
+  const int kh = (kind <= 1) ? 3 : 2;
+  std::vector<int> shp = {s0, s1, kh, kh};
+  int ncols = 0, ntaps = 0, ktap = 0;
+  if (kind == 0) { ncols = s0; ktap = s1; }
+  else if (kind == 1) { ncols = s1; ktap = s0; }
+  else if (kind == 2 || kind == 5) { ncols = s0; ktap = 2 * s1; }
+  else { ncols = 4 * s1; ktap = s0; }
+  const int cin_tensor = (kind == 2 || kind == 5) ? ktap / 2 : ktap;
+  const int KC = pick_kc(use_tc_ != 0, ktap);
+  if (ktap % KC) { seterr("channel count not a multiple of the K-block"); return IDEQ_E_INVALID; }
+  std::vector<float> B = gemm_weights(kind, w, shp, KC, ncols, ntaps, ktap);
+  ConvGeom g = make_geom(kind, N, Hin, Win, cin_tensor, ncols, KC, ktap, epi);
+  const size_t esz = precision == IDEQ_PREC_BF16 ? 2 : 4;
+  void* dW = nullptr;
+  if (cudaMalloc(&dW, B.size() * esz) != cudaSuccess) { seterr("cudaMalloc"); return IDEQ_E_NOMEM; }
+  if (precision == IDEQ_PREC_BF16) {
+    std::vector<uint16_t> hb(B.size());
+    for (size_t i = 0; i < B.size(); ++i) hb[i] = f2bf(B[i]);
+    cudaMemcpy(dW, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
+  } else {
+    cudaMemcpy(dW, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
+  }
+  int rc = IDEQ_OK;
+  if (use_tc_) {
+    if (!tc_supported(g)) { seterr("geometry unsupported by tcgen05 path"); cudaFree(dW); return IDEQ_E_UNSUPPORTED; }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    char e2[256] = {0};
+    TcPlan* plan = tc_make_plan(g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)dW, (__nv_bfloat16*)out,
+                                (const __nv_bfloat16*)aux, sms, e2, sizeof(e2));
+    if (!plan) { seterr(e2); cudaFree(dW); return IDEQ_E_CUDA; }
+    tc_launch(plan, 0);
+    tc_free_plan(plan);
+  } else if (precision == IDEQ_PREC_BF16) {
+    launch_conv_simt<__nv_bfloat16>(g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)dW, (__nv_bfloat16*)out,
+                                    (const __nv_bfloat16*)aux, 0);
+  } else {
+    launch_conv_simt<float>(g, (const float*)in, (const float*)dW, (float*)out, (const float*)aux, 0);
+  }
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) { seterr(cudaGetErrorString(e)); rc = IDEQ_E_CUDA; }
+  cudaFree(dW);
+  return rc;
+}
+
+void ideq_destroy(ideq_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->gexec_plain) cudaGraphExecDestroy(ctx->gexec_plain);
+  if (ctx->gexec_check) cudaGraphExecDestroy(ctx->gexec_check);
+  for (auto& L : ctx->prog) if (L.plan) tc_free_plan(L.plan);
+  for (auto& a : ctx->allocs) cudaFree(a.p);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+}  // extern "C"

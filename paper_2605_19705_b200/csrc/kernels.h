@@ -1,0 +1,90 @@
+// Internal kernel launch interface (not part of the public C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <algorithm>
+#include "common.cuh"
+
+namespace ideq {
+
+enum StepMode : int { STEP_PROX_INPAINT = 0, STEP_GRAD_BUF = 1, STEP_GRAD_INPAINT = 2, STEP_X1_BUF = 3 };
+
+struct StepArgs {
+  int N, C, H, W;
+  long long d;            // C*H*W
+  int parts;              // partial-sum slots per image
+  const float* z;         // z^k (read)
+  float* zout;            // z^{k+1} (written; may alias z)
+  const float* gg;        // grad g(z^k)
+  const float* y;         // observation
+  float* X0;              // iterate ping-pong buffers: x^k = X[k&1], x^{k+1} = X[(k+1)&1]
+  float* X1;
+  const uint8_t* mask;    // inpainting mask [N][H][W]
+  float* fbuf;            // fidelity scratch (A z - y, grad f or x^{k+1})
+  float* fbuf2;           // second scratch (A^T y)
+  const float* kern;      // blur kernel(s)
+  int ksize, kernel_per_image;
+  float lam, tau, beta;
+  const int* active;      // [N]
+  const int* kdev;        // iteration counter k
+  float* partials;        // [N][parts][3]
+};
+
+struct FinalizeArgs {
+  int N, parts, check_every, stop_rule;
+  float tol;
+  const float* partials;
+  int* active;
+  int* status;
+  int* iters;
+  float* res;
+  float* r_now;
+  float* trace;   // [max_iter] or null
+  float* rmax;    // 1 float (NCCL all-reduce target)
+  int* n_active;
+  int* kdev;
+};
+
+void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s);
+int blur_parts_per_image(int C, int H, int W);
+void launch_blur_residual(const StepArgs& a, cudaStream_t s);
+void launch_blur_adjoint(int mode, const StepArgs& a, const float* src, cudaStream_t s);
+void launch_finalize(const FinalizeArgs& f, cudaStream_t s);
+void launch_advance_a(const FinalizeArgs& f, cudaStream_t s);
+void launch_advance_b(const FinalizeArgs& f, cudaStream_t s);
+void launch_init_state(const FinalizeArgs& f, cudaStream_t s);
+void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s);
+void launch_inpaint_grad(const float* x, const float* y, const uint8_t* m, float* out, int N, int C, int H, int W,
+                         cudaStream_t s);
+void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float tau, float* out, int N, int C, int H,
+                         int W, cudaStream_t s);
+
+// ---- convolutions
+// FFMA implicit GEMM (any precision; fp32 math). wB: [ntaps*nchunk][ncols][KC].
+template <typename T>
+void launch_conv_simt(const ConvGeom& g, const T* in, const T* wB, T* out, const T* aux, cudaStream_t s);
+// C (1 or 3, NCHW fp32) -> w (NHWC T) 3x3 conv; w_t: [w][C][3][3] fp32 (already flipped for adjoints).
+template <typename T>
+void launch_img2feat(const float* in, const float* w_t, T* out, const T* aux, int epi, int N, int C, int H, int W,
+                     int wout, cudaStream_t s);
+// w (NHWC T) -> C (NCHW fp32) 3x3 conv; w_t: [C][w][3][3]; out = acc + alpha * aux (aux NCHW fp32 or null).
+template <typename T>
+void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux, float alpha, int N, int C, int H,
+                     int W, int win, cudaStream_t s);
+
+// tcgen05 implicit GEMM (bf16 operands, fp32 TMEM accumulators). Returns false if the
+// geometry is unsupported (the runtime then refuses the configuration).
+struct TcPlan;
+bool tc_supported(const ConvGeom& g);
+TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
+                     const __nv_bfloat16* aux, int num_sms, char* err, size_t errlen);
+void tc_launch(const TcPlan* p, cudaStream_t s);
+void tc_free_plan(TcPlan* p);
+
+// Raise the dynamic shared-memory limit of every kernel once (before any graph capture).
+void init_kernel_attributes();
+void init_attrs_simt();
+void init_attrs_tc();
+void init_attrs_step();
+
+}  // namespace ideq

@@ -1,0 +1,383 @@
+// Memory-bound kernels of the i-DEQ iteration: data-fidelity passes, the fused
+// update (extrapolation + fidelity step / prox + residual partials), the
+// per-image residual finalize / stop logic, and the output gather.
+//
+// Iterate state is fp32 NCHW [N][C][H][W] in both precisions (reading Q19).
+// Every kernel is deterministic: partial sums have a fixed block -> (image, part)
+// assignment and are combined in a fixed order in fp64 by ideq_finalize_kernel.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ideq {
+
+// ------------------------------------------------------------------ block reduction
+struct Partial3 { float d2, n2, bad; };
+
+__device__ __forceinline__ void block_reduce_store(Partial3 v, float* out3) {
+  __shared__ float red[3][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.d2 += __shfl_xor_sync(0xffffffffu, v.d2, o);
+    v.n2 += __shfl_xor_sync(0xffffffffu, v.n2, o);
+    v.bad += __shfl_xor_sync(0xffffffffu, v.bad, o);
+  }
+  if (lane == 0) { red[0][wid] = v.d2; red[1][wid] = v.n2; red[2][wid] = v.bad; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    Partial3 s{lane < nw ? red[0][lane] : 0.f, lane < nw ? red[1][lane] : 0.f, lane < nw ? red[2][lane] : 0.f};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s.d2 += __shfl_xor_sync(0xffffffffu, s.d2, o);
+      s.n2 += __shfl_xor_sync(0xffffffffu, s.n2, o);
+      s.bad += __shfl_xor_sync(0xffffffffu, s.bad, o);
+    }
+    if (lane == 0) { out3[0] = s.d2; out3[1] = s.n2; out3[2] = s.bad; }
+  }
+}
+
+// Common tail of every update: given x^{k+1} for one element, write it, write
+// z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4 of the NEXT iteration, fused
+// here so x^{k-1} is never re-read) and accumulate the residual partials.
+__device__ __forceinline__ void tail_elem(float x1, float xk, float beta, float* xn, float* zn, Partial3& acc) {
+  *xn = x1;
+  *zn = x1 + beta * (x1 - xk);
+  const float d = x1 - xk;
+  if (isfinite(x1)) { acc.d2 += d * d; } else { acc.bad += 1.f; }
+  acc.n2 += xk * xk;
+}
+
+// ------------------------------------------------------------------ pointwise step kernels
+// Block -> (image n, part) with `parts` blocks per image, each covering a fixed
+// contiguous chunk of the image's d = C*H*W elements.
+template <int MODE>
+__global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
+  const int n = blockIdx.y, part = blockIdx.x;
+  if (!a.active[n]) return;
+  const int k = *a.kdev;
+  const float* xk_base = (k & 1) ? a.X1 : a.X0;
+  float* xn_base = (k & 1) ? a.X0 : a.X1;
+  const long long d = a.d;
+  const long long chunk = (d + a.parts - 1) / a.parts;
+  const long long beg = part * chunk;
+  const long long end = min(d, beg + chunk);
+  const long long off = (long long)n * d;
+  const long long HW = (long long)a.H * a.W;
+  Partial3 acc{0.f, 0.f, 0.f};
+  for (long long e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    const long long i = off + e;
+    const float z = a.z[i], gg = a.gg[i], xk = xk_base[i];
+    float x1;
+    if (MODE == STEP_PROX_INPAINT) {
+      // v = z - tau lam grad g ; prox = (tau M y + v) / (tau M + 1)
+      const float m = (float)a.mask[(long long)n * HW + (e % HW)];
+      const float v = z - a.tau * a.lam * gg;
+      x1 = (a.tau * m * a.y[i] + v) / (a.tau * m + 1.f);
+    } else if (MODE == STEP_GRAD_BUF) {
+      // x = z - tau (grad f + lam grad g), grad f precomputed in a.fbuf
+      x1 = z - a.tau * (a.fbuf[i] + a.lam * gg);
+    } else if (MODE == STEP_GRAD_INPAINT) {
+      const float m = (float)a.mask[(long long)n * HW + (e % HW)];
+      x1 = z - a.tau * (m * (m * z - a.y[i]) + a.lam * gg);
+    } else {  // STEP_X1_BUF: x^{k+1} already computed (FFT prox output)
+      x1 = a.fbuf[i];
+    }
+    tail_elem(x1, xk, a.beta, xn_base + i, a.zout + i, acc);
+  }
+  block_reduce_store(acc, a.partials + ((long long)n * a.parts + part) * 3);
+}
+
+// ------------------------------------------------------------------ direct periodic blur
+// (A x)[m,n] = sum_{i,j} k[i,j] x[(m-i+kc) mod H, (n-j+kc) mod W]   (true convolution, Q8)
+// (A^T r)[m,n] = sum_{i,j} k[i,j] r[(m+i-kc) mod H, (n+j-kc) mod W] (correlation)
+// One block = one 32x32 output tile of one channel of one image; the input tile
+// with its (ks-1)-wide periodic halo is staged in shared memory.
+constexpr int BT = 32;
+
+__device__ __forceinline__ int wrapi(int v, int n) { v %= n; return v < 0 ? v + n : v; }
+
+template <bool ADJ>
+__device__ __forceinline__ void blur_tile(const float* __restrict__ src, const float* __restrict__ kern,
+                                          int ks, int H, int W, int m0, int n0, float* tile, float* ksm,
+                                          float out[4]) {
+  const int kc = (ks - 1) / 2;
+  const int TW = BT + ks - 1;
+  for (int t = threadIdx.x; t < ks * ks; t += blockDim.x) ksm[t] = kern[t];
+  // tile[u][v] holds src[m0 - kc + u][n0 - kc + v] (periodic)
+  for (int t = threadIdx.x; t < TW * TW; t += blockDim.x) {
+    const int u = t / TW, v = t % TW;
+    tile[t] = src[(long long)wrapi(m0 - kc + u, H) * W + wrapi(n0 - kc + v, W)];
+  }
+  __syncthreads();
+  const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;  // 8 rows of threads x 4 rows each
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int ty = ty0 + 8 * q;
+    float s = 0.f;
+    for (int i = 0; i < ks; ++i) {
+      for (int j = 0; j < ks; ++j) {
+        // forward: x[m - i + kc]  -> tile row ty - i + 2kc ; adjoint: r[m + i - kc] -> tile row ty + i
+        const int u = ADJ ? (ty + i) : (ty - i + 2 * kc);
+        const int v = ADJ ? (tx + j) : (tx - j + 2 * kc);
+        s = fmaf(ksm[i * ks + j], tile[u * TW + v], s);
+      }
+    }
+    out[q] = s;
+  }
+}
+
+// r = A z - y
+__global__ void __launch_bounds__(256) blur_residual_kernel(StepArgs a) {
+  extern __shared__ float sm[];
+  const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
+  if (a.active && !a.active[n]) return;
+  const int m0 = blockIdx.y * BT, n0 = blockIdx.x * BT;
+  const long long plane = ((long long)n * a.C + c) * a.H * a.W;
+  const float* kern = a.kern + (a.kernel_per_image ? (long long)n * a.ksize * a.ksize : 0);
+  float* ksm = sm;
+  float* tile = sm + a.ksize * a.ksize;
+  float out[4];
+  blur_tile<false>(a.z + plane, kern, a.ksize, a.H, a.W, m0, n0, tile, ksm, out);
+  const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int m = m0 + ty0 + 8 * q, nn = n0 + tx;
+    if (m < a.H && nn < a.W) {
+      const long long i = plane + (long long)m * a.W + nn;
+      a.fbuf[i] = out[q] - (a.y ? a.y[i] : 0.f);
+    }
+  }
+}
+
+// out = A^T src (used for A^T(Az - y) in the gradient step and A^T y for the prox)
+// MODE 0: plain store into a.fbuf2 ; MODE 1: fused gradient step + tail.
+template <int MODE>
+__global__ void __launch_bounds__(256) blur_adjoint_kernel(StepArgs a, const float* __restrict__ src) {
+  extern __shared__ float sm[];
+  const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
+  if (a.active && !a.active[n]) return;
+  const int m0 = blockIdx.y * BT, n0 = blockIdx.x * BT;
+  const long long plane = ((long long)n * a.C + c) * a.H * a.W;
+  const float* kern = a.kern + (a.kernel_per_image ? (long long)n * a.ksize * a.ksize : 0);
+  float* ksm = sm;
+  float* tile = sm + a.ksize * a.ksize;
+  float out[4];
+  blur_tile<true>(src + plane, kern, a.ksize, a.H, a.W, m0, n0, tile, ksm, out);
+  const int tx = threadIdx.x & 31, ty0 = threadIdx.x >> 5;
+  if (MODE == 0) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int m = m0 + ty0 + 8 * q, nn = n0 + tx;
+      if (m < a.H && nn < a.W) a.fbuf2[plane + (long long)m * a.W + nn] = out[q];
+    }
+    return;
+  }
+  const int k = *a.kdev;
+  const float* xk_base = (k & 1) ? a.X1 : a.X0;
+  float* xn_base = (k & 1) ? a.X0 : a.X1;
+  Partial3 acc{0.f, 0.f, 0.f};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int m = m0 + ty0 + 8 * q, nn = n0 + tx;
+    if (m < a.H && nn < a.W) {
+      const long long i = plane + (long long)m * a.W + nn;
+      // x^{k+1} = z - tau (A^T(Az - y) + lam grad g(z))   (Alg. 1 l.8)
+      const float x1 = a.z[i] - a.tau * (out[q] + a.lam * a.gg[i]);
+      tail_elem(x1, xk_base[i], a.beta, xn_base + i, a.zout + i, acc);
+    }
+  }
+  const int tiles = gridDim.x * gridDim.y;
+  const int part = c * tiles + blockIdx.y * gridDim.x + blockIdx.x;
+  block_reduce_store(acc, a.partials + ((long long)n * a.parts + part) * 3);
+}
+
+// ------------------------------------------------------------------ finalize / stop logic
+// One warp per image: fixed-order fp64 combine of the partials, r = sqrt(d2)/sqrt(n2),
+// divergence (any non-finite x^{k+1}: keep x^k, reading Q22) and the per-image stop
+// rule at check iterations (reading Q17).
+__global__ void finalize_kernel(FinalizeArgs f) {
+  const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (n >= f.N) return;
+  if (!f.active[n]) { if (lane == 0) f.r_now[n] = __int_as_float(0x7fc00000); return; }
+  const int k = *f.kdev;
+  double d2 = 0.0, n2 = 0.0, bad = 0.0;
+  for (int p = lane; p < f.parts; p += 32) {
+    const float* q = f.partials + ((long long)n * f.parts + p) * 3;
+    d2 += (double)q[0]; n2 += (double)q[1]; bad += (double)q[2];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+    n2 += __shfl_xor_sync(0xffffffffu, n2, o);
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if (lane != 0) return;
+  if (bad > 0.0 || !isfinite(d2)) {
+    f.status[n] = 2;
+    f.active[n] = 0;
+    f.r_now[n] = __int_as_float(0x7fc00000);
+    return;
+  }
+  const double r = n2 > 0.0 ? sqrt(d2) / sqrt(n2) : (double)INFINITY;
+  f.iters[n] = k + 1;
+  f.res[n] = (float)r;
+  f.r_now[n] = (float)r;
+  if (f.stop_rule == 0 && ((k + 1) % f.check_every) == 0 && (float)r <= f.tol) {
+    f.active[n] = 0;
+    f.status[n] = 0;
+  }
+}
+
+// Single block: max over the images updated in this iteration (trace), the local
+// max for the global rule (all-reduced between the two phases when world > 1),
+// then the global-max decision, the active count the host polls, and k += 1.
+__global__ void advance_a_kernel(FinalizeArgs f) {
+  __shared__ float smax[32];
+  float m = -1.f;
+  for (int n = threadIdx.x; n < f.N; n += blockDim.x) {
+    const float r = f.r_now[n];
+    if (!isnan(r)) m = fmaxf(m, r);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) smax[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, smax[w]);
+    m = fmaxf(m, smax[0]);
+    const int k = *f.kdev;
+    if (f.trace) f.trace[k] = m >= 0.f ? m : __int_as_float(0x7fc00000);
+    *f.rmax = m;  // -1 = no image updated on this rank
+  }
+}
+
+__global__ void advance_b_kernel(FinalizeArgs f) {
+  __shared__ int cnt[32];
+  __shared__ int stop_all;
+  const int k = *f.kdev;
+  if (threadIdx.x == 0) {
+    const float m = *f.rmax;  // global max after the all-reduce (or local when world == 1)
+    stop_all = (f.stop_rule == 1 && ((k + 1) % f.check_every) == 0 && m >= 0.f && m <= f.tol);
+  }
+  __syncthreads();
+  int c = 0;
+  for (int n = threadIdx.x; n < f.N; n += blockDim.x) {
+    if (f.active[n]) {
+      if (stop_all) { f.active[n] = 0; f.status[n] = 0; } else { ++c; }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) cnt[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += cnt[w];
+    *f.n_active = s;
+    *f.kdev = k + 1;
+  }
+}
+
+// x-hat_n = x^{iters_n}: images whose last accepted iterate sits in X1 are copied to X0.
+__global__ void gather_kernel(const int* __restrict__ iters, const float* __restrict__ X1, float* __restrict__ X0,
+                              long long d) {
+  const int n = blockIdx.y;
+  if ((iters[n] & 1) == 0) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < d; e += (long long)gridDim.x * blockDim.x)
+    X0[(long long)n * d + e] = X1[(long long)n * d + e];
+}
+
+__global__ void init_state_kernel(FinalizeArgs f) {
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < f.N; n += gridDim.x * blockDim.x) {
+    f.active[n] = 1;
+    f.status[n] = 1;
+    f.iters[n] = 0;
+    f.res[n] = __int_as_float(0x7fc00000);
+    f.r_now[n] = __int_as_float(0x7fc00000);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) { *f.kdev = 0; *f.n_active = f.N; }
+}
+
+// Elementwise helpers for the component entry points.
+__global__ void inpaint_grad_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                                    const uint8_t* __restrict__ mask, float* __restrict__ out,
+                                    long long total, long long HW, long long CHW) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const float m = (float)mask[(i / CHW) * HW + (i % HW)];
+    out[i] = m * (m * x[i] - y[i]);
+  }
+}
+
+__global__ void inpaint_prox_kernel(const float* __restrict__ v, const float* __restrict__ y,
+                                    const uint8_t* __restrict__ mask, float tau, float* __restrict__ out,
+                                    long long total, long long HW, long long CHW) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const float m = (float)mask[(i / CHW) * HW + (i % HW)];
+    out[i] = (tau * m * y[i] + v[i]) / (tau * m + 1.f);
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
+  dim3 grid(a.parts, a.N);
+  switch (mode) {
+    case STEP_PROX_INPAINT: pointwise_step_kernel<STEP_PROX_INPAINT><<<grid, 256, 0, s>>>(a); break;
+    case STEP_GRAD_BUF: pointwise_step_kernel<STEP_GRAD_BUF><<<grid, 256, 0, s>>>(a); break;
+    case STEP_GRAD_INPAINT: pointwise_step_kernel<STEP_GRAD_INPAINT><<<grid, 256, 0, s>>>(a); break;
+    default: pointwise_step_kernel<STEP_X1_BUF><<<grid, 256, 0, s>>>(a); break;
+  }
+}
+
+static size_t blur_smem(int ks) { return sizeof(float) * (ks * ks + (BT + ks - 1) * (BT + ks - 1)); }
+
+int blur_parts_per_image(int C, int H, int W) { return C * ((H + BT - 1) / BT) * ((W + BT - 1) / BT); }
+
+void launch_blur_residual(const StepArgs& a, cudaStream_t s) {
+  dim3 grid((a.W + BT - 1) / BT, (a.H + BT - 1) / BT, a.N * a.C);
+  const size_t sm = blur_smem(a.ksize);
+  blur_residual_kernel<<<grid, 256, sm, s>>>(a);
+}
+
+void launch_blur_adjoint(int mode, const StepArgs& a, const float* src, cudaStream_t s) {
+  dim3 grid((a.W + BT - 1) / BT, (a.H + BT - 1) / BT, a.N * a.C);
+  const size_t sm = blur_smem(a.ksize);
+  if (mode == 0) {
+    blur_adjoint_kernel<0><<<grid, 256, sm, s>>>(a, src);
+  } else {
+    blur_adjoint_kernel<1><<<grid, 256, sm, s>>>(a, src);
+  }
+}
+
+void init_attrs_step() {
+
+  set_max_dyn_smem(blur_residual_kernel);
+  set_max_dyn_smem(blur_adjoint_kernel<0>);
+  set_max_dyn_smem(blur_adjoint_kernel<1>);
+}
+
+void launch_finalize(const FinalizeArgs& f, cudaStream_t s) {
+  finalize_kernel<<<(f.N + 7) / 8, 256, 0, s>>>(f);
+}
+void launch_advance_a(const FinalizeArgs& f, cudaStream_t s) { advance_a_kernel<<<1, 1024, 0, s>>>(f); }
+void launch_advance_b(const FinalizeArgs& f, cudaStream_t s) { advance_b_kernel<<<1, 1024, 0, s>>>(f); }
+void launch_init_state(const FinalizeArgs& f, cudaStream_t s) { init_state_kernel<<<(f.N + 255) / 256, 256, 0, s>>>(f); }
+void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s) {
+  dim3 grid((unsigned)std::min<long long>((d + 255) / 256, 1024), N);
+  gather_kernel<<<grid, 256, 0, s>>>(iters, X1, X0, d);
+}
+void launch_inpaint_grad(const float* x, const float* y, const uint8_t* m, float* out, int N, int C, int H, int W,
+                         cudaStream_t s) {
+  const long long total = (long long)N * C * H * W;
+  inpaint_grad_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 65535), 256, 0, s>>>(
+      x, y, m, out, total, (long long)H * W, (long long)C * H * W);
+}
+void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float tau, float* out, int N, int C, int H,
+                         int W, cudaStream_t s) {
+  const long long total = (long long)N * C * H * W;
+  inpaint_prox_kernel<<<(unsigned)std::min<long long>((total + 255) / 256, 65535), 256, 0, s>>>(
+      v, y, m, tau, out, total, (long long)H * W, (long long)C * H * W);
+}
+
+}  // namespace ideq

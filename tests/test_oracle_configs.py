@@ -1,0 +1,51 @@
+"""CPU checks of the frozen configs against the oracle: the stress variants really make
+lam*grad g non-negligible and stay non-divergent, and the synthetic
+generator produces the value ranges the recipe states (DESIGN.md input recipe)."""
+import numpy as np
+import pytest
+
+from oracle import solver
+from paper_2605_19705_b200 import configs, synth
+
+MINI = dict(C1=dict(), C2=dict(batch=2, H=48, W=40), C3=dict(batch=2, H=48, W=40))
+
+
+@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10)])
+def test_stress_variant_is_strong_and_stable(name, K):
+    st = configs.STRESS[name]
+    cfg = configs.get(name, init_scale=st["init_scale"], **MINI[name])
+    prob = synth.make_problem(cfg)
+    net = solver.make_net(cfg, prob["weights"])
+    fids = solver.make_fidelities(cfg, prob)
+    x0 = prob["x0"][0].astype(np.float64)
+    gg = st["lam"] * net.grad_g(x0)
+    gf = fids[0].grad(0.9 * prob["x_true"][0].astype(np.float64))
+    assert np.linalg.norm(gg) >= 0.1 * np.linalg.norm(gf)
+    out = solver.solve_config(cfg, prob, max_iter=K, tol=0.0, lam=st["lam"])
+    assert (out["status"] == solver.MAX_ITER).all()
+    assert np.isfinite(out["x"]).all()
+
+
+def test_generator_ranges_and_determinism():
+    cfg = configs.get("C3", batch=2, H=64, W=64)
+    a = synth.make_problem(cfg)
+    b = synth.make_problem(cfg)
+    assert np.array_equal(a["y"], b["y"]) and np.array_equal(a["weights"], b["weights"])
+    assert a["x_true"].min() >= 0.0 and a["x_true"].max() <= 1.0
+    frac = a["masks"].mean()
+    assert 0.45 < frac < 0.55                               # Bernoulli(0.5)
+    assert np.all(a["y"][:, :, a["masks"][0] == 0][0] == 0)  # missing pixels are 0 (Q13)
+    k = synth.motion_kernel(np.random.default_rng(0))
+    assert k.shape == (15, 15) and abs(k.sum() - 1) < 1e-6 and (k >= 0).all()
+    g = synth.gaussian_kernel(25, 3.0)
+    assert abs(g.sum() - 1) < 1e-6 and np.allclose(g, g.T) and np.allclose(g, g[::-1, ::-1])
+
+
+def test_blur_lipschitz_is_one():
+    """L_f = max |K^|^2 = 1 for normalised non-negative kernels, so tau = 1
+    sits at the paper's tau < 1/L edge."""
+    from oracle import operators
+    for k in (synth.gaussian_kernel(9, 1.6), synth.gaussian_kernel(25, 3.0),
+              synth.motion_kernel(np.random.default_rng(3))):
+        K = operators.blur_transfer(k.astype(np.float64), 64, 64)
+        assert abs(np.abs(K).max() ** 2 - 1.0) < 1e-6
