@@ -1,0 +1,453 @@
+// Hand-written batched 2-D FFTs for the fidelity operators that need them:
+//
+//  * periodic blur prox (BASELINE C5): x = F^-1[ F(v + tau A^T y) / (1 + tau |K^|^2) ]
+//    (I + tau A^T A is circulant, so the prox is a diagonal solve in Fourier space;
+//    the DFT normalisation cancels). Real planes -> half spectrum [H][W/2+1].
+//  * coded-diffraction phase retrieval (BASELINE C4), unitary F:
+//    grad f = sum_j 2 Re( conj(D_j) F^-1[ (|u_j|^2 - y_j) u_j ] ),  u_j = F(D_j z).
+//
+// Each 2-D transform is a row pass (contiguous rows, one or more rows per block) and
+// a column pass (a block owns a strip of columns), each an in-shared-memory radix-2
+// FFT with fp32 twiddles computed in fp64 on the host. The pointwise work (prox
+// right-hand side, diagonal solve, phase residual, conj(D_j) combine) and the final
+// update + residual partials are fused into the passes, so every plane crosses HBM a
+// fixed small number of times. Sizes are powers of two up to 1024.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace ideq {
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {  // conj(a) * b
+  return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+// In-place radix-2 DIT FFT of one length-N row held in shared memory in BIT-REVERSED
+// order. `t` is this thread's index among the `tpr` threads that own the row. Every
+// thread of the block must call this (it synchronises the block between stages).
+// tw[k] = exp(-2 pi i k / N), k < N/2. inverse = unnormalised inverse transform.
+__device__ __forceinline__ void fft_row(float2* d, const float2* tw, int N, int logN, int t, int tpr, bool inverse) {
+  for (int s = 1; s <= logN; ++s) {
+    const int half = 1 << (s - 1);
+    const int step = N >> s;
+    for (int b = t; b < (N >> 1); b += tpr) {
+      const int j = b & (half - 1);
+      const int i0 = ((b >> (s - 1)) << s) + j;
+      const int i1 = i0 + half;
+      float2 w = tw[j * step];
+      if (inverse) w.y = -w.y;
+      const float2 a = d[i0];
+      const float2 c = cmul(w, d[i1]);
+      d[i0] = make_float2(a.x + c.x, a.y + c.y);
+      d[i1] = make_float2(a.x - c.x, a.y - c.y);
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ int bitrev(int i, int logN) { return (int)(__brev((unsigned)i) >> (32 - logN)); }
+
+__device__ __forceinline__ void load_twiddles(float2* s_tw, const float2* g_tw, int N) {
+  for (int k = threadIdx.x; k < N / 2; k += blockDim.x) s_tw[k] = g_tw[k];
+}
+
+// ------------------------------------------------------------------ shared tail (update + partials)
+struct P3 { float d2, n2, bad; };
+
+__device__ __forceinline__ void reduce_store_p3(P3 v, float* out3) {
+  __shared__ float red[3][32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v.d2 += __shfl_xor_sync(0xffffffffu, v.d2, o);
+    v.n2 += __shfl_xor_sync(0xffffffffu, v.n2, o);
+    v.bad += __shfl_xor_sync(0xffffffffu, v.bad, o);
+  }
+  if (lane == 0) { red[0][wid] = v.d2; red[1][wid] = v.n2; red[2][wid] = v.bad; }
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    P3 s{lane < nw ? red[0][lane] : 0.f, lane < nw ? red[1][lane] : 0.f, lane < nw ? red[2][lane] : 0.f};
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s.d2 += __shfl_xor_sync(0xffffffffu, s.d2, o);
+      s.n2 += __shfl_xor_sync(0xffffffffu, s.n2, o);
+      s.bad += __shfl_xor_sync(0xffffffffu, s.bad, o);
+    }
+    if (lane == 0) { out3[0] = s.d2; out3[1] = s.n2; out3[2] = s.bad; }
+  }
+}
+
+__device__ __forceinline__ void step_tail(float x1, long long i, const StepArgs& a, const float* xk_base,
+                                          float* xn_base, P3& acc) {
+  const float xk = xk_base[i];
+  xn_base[i] = x1;
+  a.zout[i] = x1 + a.beta * (x1 - xk);
+  const float d = x1 - xk;
+  if (isfinite(x1)) acc.d2 += d * d; else acc.bad += 1.f;
+  acc.n2 += xk * xk;
+}
+
+// ================================================================== blur (real planes)
+// Row pass, forward: one real row -> W-point complex FFT -> half spectrum (W/2+1).
+//   mode 0: input = src plane
+//   mode 1: input = v + tau A^T y = z - tau lam grad g + tau ATy   (prox right-hand side)
+__global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const float* __restrict__ src, int mode) {
+  extern __shared__ float2 sm2[];
+  const int W = f.W, logW = f.logW;
+  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int rpb = 256 / tpr;
+  float2* tw = sm2;
+  float2* rows = sm2 + W / 2;
+  load_twiddles(tw, f.tw_w, W);
+  const int r = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  const int h = blockIdx.x * rpb + r;
+  const int c = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;  // uniform per block
+  float2* d = rows + r * W;
+  const long long plane = ((long long)n * f.C + c) * f.H * W;
+  if (h < f.H) {
+    for (int i = t; i < W; i += tpr) {
+      const long long e = plane + (long long)h * W + i;
+      float v;
+      if (mode == 1) v = f.z[e] - f.tau * f.lam * f.gg[e] + f.tau * f.aty[e];
+      else v = src[e];
+      d[bitrev(i, logW)] = make_float2(v, 0.f);
+    }
+  }
+  __syncthreads();
+  fft_row(d, tw, W, logW, t, tpr, false);
+  if (h < f.H) {
+    const int Wh = W / 2 + 1;
+    float2* S = f.spec + ((long long)n * f.C + c) * f.H * Wh + (long long)h * Wh;
+    for (int i = t; i < Wh; i += tpr) S[i] = d[i];
+  }
+}
+
+// Column pass on the half spectrum: forward H-point FFT, pointwise op, inverse FFT.
+//   op 0: multiply by the real diagonal dgl[ky][kx] = 1 / (1 + tau |K^|^2)   (prox)
+//   op 1: multiply by conj(K^[ky][kx])                                     (A^T)
+//   op 2: forward only (no inverse): used to build K^ itself
+constexpr int FFT_CPB = 8;  // columns per block in column passes
+
+__global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
+  extern __shared__ float2 sm2[];
+  const int H = f.H, logH = f.logH;
+  const int Wh = f.W / 2 + 1;
+  float2* tw = sm2;
+  float2* cols = sm2 + H / 2;
+  load_twiddles(tw, f.tw_h, H);
+  const int tpc = 256 / FFT_CPB;
+  const int cc = threadIdx.x / tpc, t = threadIdx.x % tpc;
+  const int kx0 = blockIdx.x * FFT_CPB;
+  const int c = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* S = f.spec + ((long long)n * f.C + c) * H * Wh;
+  // coalesced-ish load: consecutive threads walk the FFT_CPB columns of a row
+  for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+    const int h = q / FFT_CPB, j = q % FFT_CPB;
+    const int kx = kx0 + j;
+    cols[j * H + bitrev(h, logH)] = kx < Wh ? S[(long long)h * Wh + kx] : make_float2(0.f, 0.f);
+  }
+  __syncthreads();
+  float2* d = cols + cc * H;
+  fft_row(d, tw, H, logH, t, tpc, false);
+  const int kx = kx0 + cc;
+  if (op == 2) {
+    for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+      const int h = q / FFT_CPB, j = q % FFT_CPB;
+      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+    }
+    return;
+  }
+  // pointwise op in natural order, written back bit-reversed for the inverse pass
+  __syncthreads();
+  float2 tmp[32];  // H / tpc <= 1024 / 32
+  int cnt = 0;
+  for (int ky = t; ky < H; ky += tpc) {
+    float2 v = d[ky];
+    if (kx < Wh) {
+      if (op == 0) {
+        const float g = f.dgl[(long long)ky * Wh + kx];
+        v.x *= g; v.y *= g;
+      } else {
+        v = cconjmul(f.khat[(long long)ky * Wh + kx], v);
+      }
+    }
+    tmp[cnt++] = v;
+  }
+  __syncthreads();
+  cnt = 0;
+  for (int ky = t; ky < H; ky += tpc) d[bitrev(ky, logH)] = tmp[cnt++];
+  __syncthreads();
+  fft_row(d, tw, H, logH, t, tpc, true);
+  for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+    const int h = q / FFT_CPB, j = q % FFT_CPB;
+    if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+  }
+}
+
+// Row pass, inverse: half spectrum -> Hermitian full row -> inverse FFT -> real / (H W).
+//   mode 0: store into dst plane ; mode 1: x^{k+1} -> update + residual partials.
+__global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  extern __shared__ float2 sm2[];
+  const int W = f.W, logW = f.logW, H = f.H;
+  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int rpb = 256 / tpr;
+  float2* tw = sm2;
+  float2* rows = sm2 + W / 2;
+  load_twiddles(tw, f.tw_w, W);
+  const int r = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  const int h = blockIdx.x * rpb + r;
+  const int c = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* d = rows + r * W;
+  const int Wh = W / 2 + 1;
+  if (h < H) {
+    const float2* S = f.spec + ((long long)n * f.C + c) * H * Wh + (long long)h * Wh;
+    for (int i = t; i < W; i += tpr) {
+      float2 v = i < Wh ? S[i] : S[W - i];
+      if (i >= Wh) v.y = -v.y;  // X[W-k] = conj(X[k]) for a real row (per column transform keeps it)
+      d[bitrev(i, logW)] = v;
+    }
+  }
+  __syncthreads();
+  fft_row(d, tw, W, logW, t, tpr, true);
+  const float scale = 1.f / ((float)H * (float)W);
+  const long long plane = ((long long)n * f.C + c) * H * W;
+  if (mode == 0) {
+    if (h < H)
+      for (int i = t; i < W; i += tpr) dst[plane + (long long)h * W + i] = d[i].x * scale;
+    return;
+  }
+  const int k = *a.kdev;
+  const float* xk_base = (k & 1) ? a.X1 : a.X0;
+  float* xn_base = (k & 1) ? a.X0 : a.X1;
+  P3 acc{0.f, 0.f, 0.f};
+  if (h < H)
+    for (int i = t; i < W; i += tpr) step_tail(d[i].x * scale, plane + (long long)h * W + i, a, xk_base, xn_base, acc);
+  const int part = c * gridDim.x + blockIdx.x;
+  reduce_store_p3(acc, a.partials + ((long long)n * a.parts + part) * 3);
+}
+
+// Note on the Hermitian expansion above: the column pass transforms each column kx of
+// the row spectra independently, so after the forward 2-D pass the stored half plane
+// is X[ky][kx], kx <= W/2. For the inverse row pass of row ky we need X'[ky][kx] for
+// all kx of the *column-inverted* data, which is the row spectrum of a real row, hence
+// Hermitian in kx: X'[ky][W-kx] = conj(X'[ky][kx]).
+
+// Embed the kernel: plane[(i-kc) mod H][(j-kc) mod W] = k[i][j] (tap (kc,kc) at the origin).
+// The runtime requires ksize <= min(H, W), so no two taps share a bin.
+__global__ void embed_kernel_kernel(const float* __restrict__ k, int ks, float* __restrict__ plane, int H, int W) {
+  const int kc = (ks - 1) / 2;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ks * ks; e += gridDim.x * blockDim.x) {
+    const int i = e / ks, j = e % ks;
+    const int r = ((i - kc) % H + H) % H, s = ((j - kc) % W + W) % W;
+    plane[r * W + s] = k[e];
+  }
+}
+
+// dgl = 1 / (1 + tau |K^|^2)
+__global__ void blur_diag_kernel(const float2* __restrict__ khat, float tau, float* __restrict__ dgl, int n) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    const float2 v = khat[e];
+    dgl[e] = 1.f / (1.f + tau * (v.x * v.x + v.y * v.y));
+  }
+}
+
+// ================================================================== phase retrieval (complex)
+// rows forward: U[n][j][h][:] = FFT_row( D_j[h][:] * z[n][0][h][:] )
+__global__ void __launch_bounds__(256) phase_rows_fwd_kernel(FftArgs f) {
+  extern __shared__ float2 sm2[];
+  const int W = f.W, logW = f.logW;
+  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int rpb = 256 / tpr;
+  float2* tw = sm2;
+  float2* rows = sm2 + W / 2;
+  load_twiddles(tw, f.tw_w, W);
+  const int r = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  const int h = blockIdx.x * rpb + r;
+  const int j = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* d = rows + r * W;
+  if (h < f.H) {
+    const float* zr = f.z + (long long)n * f.H * W + (long long)h * W;
+    const float2* Dr = f.pmask + ((long long)j * f.H + h) * W;
+    for (int i = t; i < W; i += tpr) {
+      const float zv = zr[i];
+      const float2 dv = Dr[i];
+      d[bitrev(i, logW)] = make_float2(dv.x * zv, dv.y * zv);
+    }
+  }
+  __syncthreads();
+  fft_row(d, tw, W, logW, t, tpr, false);
+  if (h < f.H) {
+    float2* U = f.spec + (((long long)n * f.J + j) * f.H + h) * W;
+    for (int i = t; i < W; i += tpr) U[i] = d[i];
+  }
+}
+
+// columns: forward FFT -> u = col / sqrt(HW) (unitary) -> w = (|u|^2 - y_j) u -> inverse FFT
+__global__ void __launch_bounds__(256) phase_cols_kernel(FftArgs f) {
+  extern __shared__ float2 sm2[];
+  const int H = f.H, logH = f.logH, W = f.W;
+  float2* tw = sm2;
+  float2* cols = sm2 + H / 2;
+  load_twiddles(tw, f.tw_h, H);
+  const int tpc = 256 / FFT_CPB;
+  const int cc = threadIdx.x / tpc, t = threadIdx.x % tpc;
+  const int kx0 = blockIdx.x * FFT_CPB;
+  const int j = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* U = f.spec + ((long long)n * f.J + j) * H * W;
+  const float* Y = f.y + ((long long)n * f.J + j) * H * W;
+  for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+    const int h = q / FFT_CPB, jj = q % FFT_CPB;
+    cols[jj * H + bitrev(h, logH)] = U[(long long)h * W + kx0 + jj];
+  }
+  __syncthreads();
+  float2* d = cols + cc * H;
+  fft_row(d, tw, H, logH, t, tpc, false);
+  const float s = rsqrtf((float)H * (float)W);
+  const int kx = kx0 + cc;
+  float2 tmp[32];
+  int cnt = 0;
+  for (int ky = t; ky < H; ky += tpc) {
+    const float2 v = d[ky];
+    const float2 u = make_float2(v.x * s, v.y * s);
+    const float m = u.x * u.x + u.y * u.y - Y[(long long)ky * W + kx];
+    tmp[cnt++] = make_float2(m * u.x, m * u.y);
+  }
+  __syncthreads();
+  cnt = 0;
+  for (int ky = t; ky < H; ky += tpc) d[bitrev(ky, logH)] = tmp[cnt++];
+  __syncthreads();
+  fft_row(d, tw, H, logH, t, tpc, true);
+  for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+    const int h = q / FFT_CPB, jj = q % FFT_CPB;
+    U[(long long)h * W + kx0 + jj] = cols[jj * H + h];
+  }
+}
+
+// rows inverse: for each j, v = IFFT_row(U)/sqrt(HW); grad f += 2 Re(conj(D_j) v).
+//   mode 0: store grad f into dst ; mode 1: x^{k+1} = z - tau (grad f + lam grad g) -> tail.
+__global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  extern __shared__ float2 sm2[];
+  const int W = f.W, logW = f.logW, H = f.H;
+  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int rpb = 256 / tpr;
+  float2* tw = sm2;
+  float2* rows = sm2 + W / 2;
+  load_twiddles(tw, f.tw_w, W);
+  const int r = threadIdx.x / tpr, t = threadIdx.x % tpr;
+  const int h = blockIdx.x * rpb + r;
+  const int n = blockIdx.y;
+  if (f.active && !f.active[n]) return;
+  float2* d = rows + r * W;
+  float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // W / tpr <= 4 for W <= 1024
+  const float s = rsqrtf((float)H * (float)W);
+  for (int j = 0; j < f.J; ++j) {
+    if (h < H) {
+      const float2* U = f.spec + (((long long)n * f.J + j) * H + h) * W;
+      for (int i = t; i < W; i += tpr) d[bitrev(i, logW)] = U[i];
+    }
+    __syncthreads();
+    fft_row(d, tw, W, logW, t, tpr, true);
+    if (h < H) {
+      const float2* Dr = f.pmask + ((long long)j * H + h) * W;
+      int q = 0;
+      for (int i = t; i < W; i += tpr, ++q) {
+        const float2 v = make_float2(d[i].x * s, d[i].y * s);
+        gacc[q] += 2.f * cconjmul(Dr[i], v).x;
+      }
+    }
+    __syncthreads();
+  }
+  const long long base = (long long)n * H * W + (long long)h * W;
+  if (mode == 0) {
+    if (h < H) {
+      int q = 0;
+      for (int i = t; i < W; i += tpr, ++q) dst[base + i] = gacc[q];
+    }
+    return;
+  }
+  const int k = *a.kdev;
+  const float* xk_base = (k & 1) ? a.X1 : a.X0;
+  float* xn_base = (k & 1) ? a.X0 : a.X1;
+  P3 acc{0.f, 0.f, 0.f};
+  if (h < H) {
+    int q = 0;
+    for (int i = t; i < W; i += tpr, ++q) {
+      const long long e = base + i;
+      // x^{k+1} = z - tau (grad f(z) + lam grad g(z))       (Alg. 1 l.8)
+      step_tail(a.z[e] - a.tau * (gacc[q] + a.lam * a.gg[e]), e, a, xk_base, xn_base, acc);
+    }
+  }
+  reduce_store_p3(acc, a.partials + ((long long)n * a.parts + blockIdx.x) * 3);
+}
+
+// ------------------------------------------------------------------ launchers
+static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
+
+static size_t row_smem(int W) {
+  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int rpb = 256 / tpr;
+  return sizeof(float2) * (W / 2 + (size_t)rpb * W);
+}
+static size_t col_smem(int H) { return sizeof(float2) * (H / 2 + (size_t)FFT_CPB * H); }
+static int rows_per_block(int W) { const int tpr = (W / 2) < 256 ? (W / 2) : 256; return 256 / tpr; }
+
+int fft_parts_per_image(int C, int H, int W) { return C * ((H + rows_per_block(W) - 1) / rows_per_block(W)); }
+int phase_parts_per_image(int H, int W) { return (H + rows_per_block(W) - 1) / rows_per_block(W); }
+
+bool fft_size_ok(int H, int W) {
+  auto pow2 = [](int v) { return v >= 4 && v <= 1024 && (v & (v - 1)) == 0; };
+  return pow2(H) && pow2(W);
+}
+
+void fft_fill_args(FftArgs& f) { f.logH = ilog2(f.H); f.logW = ilog2(f.W); }
+
+void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s) {
+  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
+  blur_rows_fwd_kernel<<<grid, 256, row_smem(f.W), s>>>(f, src, mode);
+}
+void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s) {
+  dim3 grid((f.W / 2 + 1 + FFT_CPB - 1) / FFT_CPB, f.C, N);
+  blur_cols_kernel<<<grid, 256, col_smem(f.H), s>>>(f, op);
+}
+void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
+  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
+  blur_rows_inv_kernel<<<grid, 256, row_smem(f.W), s>>>(f, a, dst, mode);
+}
+void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s) {
+  cudaMemsetAsync(plane, 0, sizeof(float) * H * W, s);
+  embed_kernel_kernel<<<(ks * ks + 255) / 256, 256, 0, s>>>(k, ks, plane, H, W);
+}
+void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStream_t s) {
+  blur_diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(khat, tau, dgl, n);
+}
+void launch_phase_rows_fwd(const FftArgs& f, int N, cudaStream_t s) {
+  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.J, N);
+  phase_rows_fwd_kernel<<<grid, 256, row_smem(f.W), s>>>(f);
+}
+void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s) {
+  dim3 grid(f.W / FFT_CPB, f.J, N);
+  phase_cols_kernel<<<grid, 256, col_smem(f.H), s>>>(f);
+}
+void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
+  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), N);
+  phase_rows_inv_kernel<<<grid, 256, row_smem(f.W), s>>>(f, a, dst, mode);
+}
+
+void init_attrs_fft() {
+  set_max_dyn_smem(blur_rows_fwd_kernel);
+  set_max_dyn_smem(blur_cols_kernel);
+  set_max_dyn_smem(blur_rows_inv_kernel);
+  set_max_dyn_smem(phase_rows_fwd_kernel);
+  set_max_dyn_smem(phase_cols_kernel);
+  set_max_dyn_smem(phase_rows_inv_kernel);
+}
+
+}  // namespace ideq
