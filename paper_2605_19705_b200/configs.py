@@ -34,7 +34,7 @@ CONFIGS = {
                precision="bf16"),
     "C4": dict(name="C4 coded-diffraction phase retrieval", seed_id=4, batch=16, C=1, H=256, W=256,
                net="unet4", widths=UNET32, res_blocks=2, identity_skip=True, act="softplus",
-               op="phase", n_phase=4, step="grad", lam=0.05, tau=None, beta=0.5,
+               op="phase", n_phase=4, step="grad", lam=0.05, tau=0.5 / 17, beta=0.5,
                max_iter=300, tol=1e-4, check_every=1, stop_rule="per_image",
                precision="bf16"),
     "C5": dict(name="C5 large-batch deblur", seed_id=5, batch=512, C=3, H=512, W=512,
@@ -55,7 +55,7 @@ STRESS = {
     "C1": dict(init_scale=0.3, lam=1.0),
     "C2": dict(init_scale=0.3, lam=0.1),
     "C3": dict(init_scale=0.3, lam=0.1),
-    "C4": dict(init_scale=0.3, lam=0.1),
+    "C4": dict(init_scale=0.3, lam=5.0),
     "C5": dict(init_scale=0.3, lam=0.1),
 }
 

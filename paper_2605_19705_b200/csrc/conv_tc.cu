@@ -123,44 +123,89 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3,
+                                             int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 // ------------------------------------------------------------------ kernel
 struct TcParams {
   ConvGeom g;
-  __nv_bfloat16* out;
-  const __nv_bfloat16* aux;
   int BN, n_tiles, m_tiles, stages;
   uint32_t a_bytes, b_bytes, tmem_cols;
+  uint32_t epi_box_bytes;  // one epilogue box: 128 rows x BOXC columns (bf16)
+  uint32_t epi_tx_bytes;   // TMA bytes of one aux tile (R*Wt rows x BN columns)
 };
 
 constexpr int TC_THREADS = 192;
 
-template <int KC>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+// Epilogue boxes are BOXC = min(BN, 64) columns wide: 128-byte rows (SW128) for 64 columns,
+// 64-byte rows (SW64) for 32. A thread owns one pixel row; 16-byte chunk j of row r lives at
+// chunk j ^ swz(r) so a quarter-warp touches 8 distinct bank groups.
+template <int BOXC>
+__device__ __forceinline__ uint32_t epi_chunk_addr(uint32_t box_base, int r, int j) {
+  if (BOXC == 64) return box_base + (uint32_t)r * 128u + (uint32_t)((j ^ (r & 7)) << 4);
+  return box_base + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
+}
+
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <int KC, int EPI, int BOXC>
+__global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmAux,
                    const __grid_constant__ TcParams P) {
+  constexpr bool HAS_AUX = (EPI == EPI_RESADD || EPI == EPI_SIGMUL);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  // 1024-byte aligned carve-up
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
   const int S = P.stages;
+  const int BN = P.BN;
   const uint32_t a_stage = 128u * KC * 2u;
-  const uint32_t b_stage = (uint32_t)P.BN * KC * 2u;
+  const uint32_t b_stage = (uint32_t)BN * KC * 2u;
+  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
   const uint32_t sA = base;
   const uint32_t sB = sA + S * a_stage;
-  const uint32_t sBar = sB + S * b_stage;  // 8-byte aligned (stage sizes are multiples of 1 KB)
+  const uint32_t sE = sB + S * b_stage;
+  const uint32_t sBar = sE + 2u * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4);
-  const uint32_t full0 = sBar, empty0 = sBar + 8u * S, tfull0 = sBar + 16u * S, tempty0 = tfull0 + 16u;
+  // barriers: full[S], empty[S], tfull[2], tempty[2], auxfull[2], epifree[2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 8);
+  const uint32_t full0 = sBar, empty0 = sBar + 8u * S;
+  const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 16u, auxfull0 = tempty0 + 16u, epifree0 = auxfull0 + 16u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const ConvGeom& g = P.g;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
-    for (int a = 0; a < 2; ++a) { mbar_init(tfull0 + 8u * a, 1); mbar_init(tempty0 + 8u * a, 4); }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull0 + 8u * a, 1);
+      mbar_init(tempty0 + 8u * a, 4);
+      mbar_init(auxfull0 + 8u * a, 1);
+      mbar_init(epifree0 + 8u * a, 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmOut);
+    if (HAS_AUX) prefetch_tmap(&tmAux);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
@@ -176,30 +221,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nkb = g.ntaps * g.nchunk;
   const int total = P.m_tiles * P.n_tiles;
   const int per_img = g.tiles_h * g.tiles_w;
+  const int nbox = BN / BOXC;
 
   if (warp == 0) {
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
+      int acc = 0;
+      uint32_t aph = 0;
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int mt = t / P.n_tiles, nt = t % P.n_tiles;
         const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
         const int h0 = th * g.R, w0 = tw * g.Wt;
+        // the aux tile goes into this tile's epilogue buffer; it is requested after the first
+        // min(S, nkb) operand stages so waiting for the buffer never starves the MMA warp
+        const int kb_aux = (S < nkb ? S : nkb) - 1;
         for (int kb = 0; kb < nkb; ++kb) {
           const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
           mbar_wait(empty0 + 8u * s, ph ^ 1u);
           mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
           tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * KC, w0 + g.dw[tap], g.dp[tap], h0 + g.dh[tap],
                       img);
-          tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * P.BN, kb);
+          tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * BN, kb);
           if (++s == S) { s = 0; ph ^= 1u; }
+          if (HAS_AUX && kb == kb_aux) {
+            mbar_wait(epifree0 + 8u * acc, aph ^ 1u);  // previous store from this buffer has drained
+            mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
+            for (int b = 0; b < nbox; ++b) {
+              const int col = nt * BN + b * BOXC;
+              tma_load_5d(sE + acc * epi_stage + b * P.epi_box_bytes, &tmAux, auxfull0 + 8u * acc, col % g.CB, w0,
+                          col / g.CB, h0, img);
+            }
+          }
         }
+        if (++acc == 2) { acc = 0; aph ^= 1u; }
       }
     }
     __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(P.BN);
+      const uint32_t idesc = make_idesc_bf16(BN);
       constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
       constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
       int s = 0;
@@ -209,7 +270,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * P.BN);
+        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(full0 + 8u * s, ph);
           tc_fence_after();
@@ -229,57 +290,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     __syncwarp();
   } else {
-    // epilogue warps 2..5 -> TMEM lane quadrant (warp % 4)
+    // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4, one pixel row per thread
     const int quad = warp & 3;
-    const int row = quad * 32 + lane;  // pixel index within the tile
+    const int row = quad * 32 + lane;
+    const bool leader = (warp == 2 && lane == 0);
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int mt = t / P.n_tiles, nt = t % P.n_tiles;
       const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
-      const int oh = th * g.R + row / g.Wt, ow = tw * g.Wt + row % g.Wt;
-      const bool valid = row < g.R * g.Wt && oh < g.OH && ow < g.OW;
+      const int h0 = th * g.R, w0 = tw * g.Wt;
+      const uint32_t ebuf = sE + acc * epi_stage;
+      if (HAS_AUX) {
+        mbar_wait(auxfull0 + 8u * acc, aph);
+      } else {
+        mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
+      }
       mbar_wait(tfull0 + 8u * acc, aph);
       tc_fence_after();
-      for (int c0 = 0; c0 < P.BN; c0 += 32) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * P.BN + c0), v);
-        if (valid) {
-          const int col = nt * P.BN + c0;
-          const long long o = out_offset(g, img, oh, ow, col);
-          if (g.epi == EPI_RESADD || g.epi == EPI_SIGMUL) {
-            const uint4* ap = reinterpret_cast<const uint4*>(P.aux + o);
+        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+        const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
+        const int j0 = (c0 % BOXC) / 8;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 u = ap[q];
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t a = epi_chunk_addr<BOXC>(box, row, j0 + q);
+          float o[8];
+          if (HAS_AUX) {
+            const uint4 u = ld_shared_v4(a);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                v[q * 8 + 2 * e] = apply_epi(g.epi, v[q * 8 + 2 * e], f.x);
-                v[q * 8 + 2 * e + 1] = apply_epi(g.epi, v[q * 8 + 2 * e + 1], f.y);
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = __bfloat1622float2(h2[e]);
+              if (EPI == EPI_RESADD) {
+                o[2 * e] = v[q * 8 + 2 * e] + f.x;
+                o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
+              } else {
+                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act(f.x);
+                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act(f.y);
               }
             }
-          } else if (g.epi == EPI_SOFTPLUS) {
+          } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = softplus_f(v[i]);
+            for (int e = 0; e < 8; ++e) o[e] = (EPI == EPI_SOFTPLUS) ? softplus_f(v[q * 8 + e]) : v[q * 8 + e];
           }
-          uint4* op = reinterpret_cast<uint4*>(P.out + o);
+          uint4 w;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 u;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
-            op[q] = u;
-          }
+          for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+          st_shared_v4(a, w);
         }
       }
+      // TMEM stage fully read: let the MMA warp reuse it
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+      // publish the tile: generic-proxy smem writes -> async proxy, then one TMA store per box
+      fence_async_smem();
+      epi_bar();
+      if (leader) {
+        for (int b = 0; b < nbox; ++b) {
+          const int col = nt * BN + b * BOXC;
+          tma_store_5d(&tmOut, ebuf + b * P.epi_box_bytes, col % g.CB, w0, col / g.CB, h0, img);
+        }
+        bulk_commit();
+        bulk_wait_read0();  // smem buffer reusable once the TMA engine has read it
+        mbar_arrive(epifree0 + 8u * acc);
+      }
       if (++acc == 2) { acc = 0; aph ^= 1u; }
     }
+    if (leader) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -308,21 +390,40 @@ static EncodeTiledFn get_encode() {
 }
 
 struct TcPlan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmOut, tmAux;
   TcParams P;
-  int KC, grid;
+  int KC, epi, boxc, grid;
   size_t smem;
 };
+
+static int tc_bn(const ConvGeom& g) { return g.ncols >= 128 ? 128 : g.ncols; }
 
 bool tc_supported(const ConvGeom& g) {
   if (!(g.KC == 32 || g.KC == 64)) return false;
   if (g.R * g.Wt > 128 || g.Wt > 256 || g.R > 256) return false;
   if (g.ncols % 32 != 0) return false;
-  const int BN = g.ncols >= 256 ? 256 : g.ncols;
+  const int BN = tc_bn(g);
   if (g.ncols % BN != 0) return false;
-  if (g.CB % 32 != 0 || g.OCp % 8 != 0) return false;
+  const int boxc = BN >= 64 ? 64 : 32;
+  if (g.CB % boxc != 0 || g.OCp % 8 != 0) return false;
   if ((g.inC * 2) % 16 != 0) return false;
+  if (g.OHo % g.osh != 0) return false;
   return true;
+}
+
+// 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
+static CUresult encode5(EncodeTiledFn enc, CUtensorMap* m, const void* ptr, int C, int W, int P, int H, int N,
+                        int boxc, int boxw, int boxh, CUtensorMapSwizzle sw) {
+  cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)P, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint64_t strides[4];
+  strides[0] = (cuuint64_t)C * 2;
+  strides[1] = strides[0] * W;
+  strides[2] = strides[1] * P;
+  strides[3] = strides[2] * H;
+  cuuint32_t box[5] = {(cuuint32_t)boxc, (cuuint32_t)boxw, 1u, (cuuint32_t)boxh, 1u};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
 TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
@@ -330,78 +431,107 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   if (!tc_supported(g)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
   EncodeTiledFn enc = get_encode();
   if (!enc) { snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable"); return nullptr; }
+  const bool has_aux = g.epi == EPI_RESADD || g.epi == EPI_SIGMUL;
+  if (has_aux && !aux) { snprintf(err, errlen, "epilogue needs an aux tensor"); return nullptr; }
   TcPlan* p = new TcPlan();
   memset(p, 0, sizeof(TcPlan));
   p->KC = g.KC;
-  const int BN = g.ncols >= 256 ? 256 : g.ncols;
-  // A: 5-D view (C', W', P, H', N) of the NHWC input
-  {
-    cuuint64_t dims[5] = {(cuuint64_t)g.inC, (cuuint64_t)g.inW, (cuuint64_t)g.inP, (cuuint64_t)g.inH, (cuuint64_t)g.N};
-    cuuint64_t strides[4];
-    strides[0] = (cuuint64_t)g.inC * 2;
-    strides[1] = strides[0] * g.inW;
-    strides[2] = strides[1] * g.inP;
-    strides[3] = strides[2] * g.inH;
-    cuuint32_t box[5] = {(cuuint32_t)g.KC, (cuuint32_t)g.Wt, 1u, (cuuint32_t)g.R, 1u};
-    cuuint32_t es[5] = {1, 1, 1, 1, 1};
-    CUresult r = enc(&p->tmA, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<__nv_bfloat16*>(in), dims, strides, box,
-                     es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
-  }
-  // B: [kb][ncols][KC]
+  p->epi = g.epi;
+  const int BN = tc_bn(g);
+  const int boxc = BN >= 64 ? 64 : 32;
+  p->boxc = boxc;
+  const CUtensorMapSwizzle swA = g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapSwizzle swE = boxc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUresult r = encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
+  if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
   {
     const int nkb = g.ntaps * g.nchunk;
     cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
     cuuint64_t strides[2] = {(cuuint64_t)g.KC * 2, (cuuint64_t)g.KC * 2 * g.ncols};
     cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
     cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box,
-                     es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swA, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map B encode failed (%d)", (int)r); delete p; return nullptr; }
+  }
+  // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
+  // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
+  r = encode5(enc, &p->tmOut, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+  if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map out encode failed (%d)", (int)r); delete p; return nullptr; }
+  if (has_aux) {
+    r = encode5(enc, &p->tmAux, aux, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map aux encode failed (%d)", (int)r); delete p; return nullptr; }
+  } else {
+    p->tmAux = p->tmOut;
   }
   TcParams& P = p->P;
   P.g = g;
-  P.out = out;
-  P.aux = aux;
   P.BN = BN;
   P.n_tiles = g.ncols / BN;
   P.m_tiles = g.N * g.tiles_h * g.tiles_w;
   P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
   P.b_bytes = (uint32_t)g.KC * 2u * BN;
+  P.epi_box_bytes = 128u * boxc * 2u;
+  P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
   uint32_t cols = 2u * BN;
   uint32_t tc = 32;
   while (tc < cols) tc <<= 1;
   P.tmem_cols = tc;
-  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u;
-  const size_t budget = 200 * 1024;
-  int stages = (int)(budget / (a_stage + b_stage));
+  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
+  // two CTAs per SM when the whole working set fits twice (small-N layers are latency-bound)
+  const size_t fixed = 1024 + 2 * e_stage + 256;
+  int stages = (int)((200 * 1024 - fixed) / (a_stage + b_stage));
   if (stages > 8) stages = 8;
+  int ctas = 1;
+  const int st2 = (int)(((227 * 1024) / 2 - fixed) / (a_stage + b_stage));
+  if (st2 >= 4 && tc * 2 <= 512) { stages = st2 > 6 ? 6 : st2; ctas = 2; }
   if (stages < 2) { snprintf(err, errlen, "tcgen05 conv: smem too small"); delete p; return nullptr; }
   P.stages = stages;
-  p->smem = 1024 + stages * (a_stage + b_stage) + (2 * stages + 4) * 8 + 16;
+  p->smem = fixed + stages * (a_stage + b_stage);
   const int total = P.m_tiles * P.n_tiles;
-  p->grid = total < num_sms ? total : num_sms;
+  const int maxg = num_sms * ctas;
+  p->grid = total < maxg ? total : maxg;
   return p;
+}
+
+template <int KC, int EPI, int BOXC>
+static void launch_one(const TcPlan* p, cudaStream_t s) {
+  conv_tc_kernel<KC, EPI, BOXC><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
+}
+
+template <int KC, int BOXC>
+static void launch_epi(const TcPlan* p, cudaStream_t s) {
+  switch (p->epi) {
+    case EPI_SOFTPLUS: launch_one<KC, EPI_SOFTPLUS, BOXC>(p, s); break;
+    case EPI_RESADD: launch_one<KC, EPI_RESADD, BOXC>(p, s); break;
+    case EPI_SIGMUL: launch_one<KC, EPI_SIGMUL, BOXC>(p, s); break;
+    default: launch_one<KC, EPI_STORE, BOXC>(p, s); break;
+  }
 }
 
 void tc_launch(const TcPlan* p, cudaStream_t s) {
   if (p->KC == 64) {
-    conv_tc_kernel<64><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->P);
+    if (p->boxc == 64) launch_epi<64, 64>(p, s); else launch_epi<64, 32>(p, s);
   } else {
-    conv_tc_kernel<32><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->P);
+    if (p->boxc == 64) launch_epi<32, 64>(p, s); else launch_epi<32, 32>(p, s);
   }
 }
 
 void tc_free_plan(TcPlan* p) { delete p; }
 
-void init_attrs_tc() {
+template <int KC, int BOXC>
+static void attrs_epi() {
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_STORE, BOXC>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_RESADD, BOXC>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SIGMUL, BOXC>);
+}
 
-  set_max_dyn_smem(conv_tc_kernel<64>);
-  set_max_dyn_smem(conv_tc_kernel<32>);
+void init_attrs_tc() {
+  attrs_epi<64, 64>();
+  attrs_epi<64, 32>();
+  attrs_epi<32, 64>();
+  attrs_epi<32, 32>();
 }
 
 }  // namespace ideq

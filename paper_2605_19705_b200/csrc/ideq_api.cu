@@ -122,6 +122,12 @@ struct ideq_ctx {
   float* d_kern = nullptr;
   uint8_t* d_mask = nullptr;
   float* d_phase = nullptr;
+  // FFT operators
+  float2* tw_h = nullptr;
+  float2* tw_w = nullptr;
+  float2* spec = nullptr;   // work spectrum
+  float2* khat = nullptr;   // [H][W/2+1]
+  float* dgl = nullptr;     // [H][W/2+1]
 
   // distribution
   int rank = 0, world = 1;
@@ -709,9 +715,23 @@ StepArgs make_step_args(ideq_ctx* ctx, int N, const float* y, float* x0, const i
   return a;
 }
 
+FftArgs make_fft_args(ideq_ctx* ctx, const float* y, const ideq_params* p) {
+  FftArgs f{};
+  f.C = ctx->C; f.H = ctx->H; f.W = ctx->W; f.J = ctx->op.n_phase;
+  fft_fill_args(f);
+  f.tw_h = ctx->tw_h; f.tw_w = ctx->tw_w; f.spec = ctx->spec;
+  f.z = ctx->Z; f.gg = ctx->G; f.aty = ctx->fbuf2;
+  if (p) { f.tau = p->tau; f.lam = p->lambda; }
+  f.dgl = ctx->dgl; f.khat = ctx->khat; f.pmask = (const float2*)ctx->d_phase; f.y = y;
+  f.active = ctx->active;
+  return f;
+}
+
 int step_parts(ideq_ctx* ctx) {
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.blur_impl == IDEQ_BLUR_DIRECT && ctx->op.step == IDEQ_STEP_GRAD)
     return blur_parts_per_image(ctx->C, ctx->H, ctx->W);
+  if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) return fft_parts_per_image(ctx->C, ctx->H, ctx->W);
+  if (ctx->op.kind == IDEQ_OP_PHASE) return phase_parts_per_image(ctx->H, ctx->W);
   const long long d = (long long)ctx->C * ctx->H * ctx->W;
   long long parts = d / 4096;
   if (parts < 1) parts = 1;
@@ -727,6 +747,21 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
   if (op.kind == IDEQ_OP_INPAINT) {
     Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 7.0);
     launch_pointwise_step(op.step == IDEQ_STEP_PROX ? STEP_PROX_INPAINT : STEP_GRAD_INPAINT, a, s);
+  } else if (op.kind == IDEQ_OP_BLUR && op.step == IDEQ_STEP_PROX) {
+    // x^{k+1} = F^-1[ F(z - tau lam grad g + tau A^T y) / (1 + tau |K^|^2) ]   (prox P:80-84)
+    FftArgs f = make_fft_args(ctx, a.y, nullptr);
+    f.tau = a.tau; f.lam = a.lam;
+    const double spec_b = (double)a.N * a.C * a.H * (a.W / 2 + 1) * 8.0;
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 0, (double)a.N * a.d * 12.0 + spec_b);
+      launch_blur_rows_fwd(f, nullptr, 1, a.N, s);
+    }
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 0, 2.0 * spec_b);
+      launch_blur_cols(f, 0, a.N, s);
+    }
+    Prof p(ctx, IDEQ_K_STEP, 0, spec_b + (double)a.N * a.d * 4.0 * 3.0);
+    launch_blur_rows_inv(f, a, nullptr, 1, a.N, s);
   } else if (op.kind == IDEQ_OP_BLUR) {
     {
       Prof p(ctx, IDEQ_K_FIDELITY, 2.0 * a.N * a.d * op.ksize * op.ksize, (double)a.N * a.d * 12.0);
@@ -734,7 +769,33 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
     }
     Prof p(ctx, IDEQ_K_STEP, 2.0 * a.N * a.d * op.ksize * op.ksize, (double)a.N * a.d * 4.0 * 6.0);
     launch_blur_adjoint(1, a, ctx->fbuf, s);
+  } else if (op.kind == IDEQ_OP_PHASE) {
+    // grad f = sum_j 2 Re(conj(D_j) F^-1[(|u_j|^2 - y_j) u_j]), x^{k+1} = z - tau(grad f + lam grad g)
+    FftArgs f = make_fft_args(ctx, a.y, nullptr);
+    f.tau = a.tau; f.lam = a.lam;
+    const double spec_b = (double)a.N * op.n_phase * a.H * a.W * 8.0;
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 0, (double)a.N * a.d * 4.0 + spec_b);
+      launch_phase_rows_fwd(f, a.N, s);
+    }
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 0, 2.0 * spec_b + (double)a.N * op.n_phase * a.H * a.W * 4.0);
+      launch_phase_cols(f, a.N, s);
+    }
+    Prof p(ctx, IDEQ_K_STEP, 0, spec_b + (double)a.N * a.d * 4.0 * 5.0);
+    launch_phase_rows_inv(f, a, nullptr, 1, a.N, s);
   }
+}
+
+// Per-solve operator constants: A^T y (FFT) and the diagonal 1 / (1 + tau |K^|^2).
+void prepare_blur_prox(ideq_ctx* ctx, const float* y, float tau, int N) {
+  FftArgs f = make_fft_args(ctx, y, nullptr);
+  f.active = nullptr;
+  StepArgs dummy{};
+  launch_blur_rows_fwd(f, y, 0, N, ctx->stream);
+  launch_blur_cols(f, 1, N, ctx->stream);
+  launch_blur_rows_inv(f, dummy, ctx->fbuf2, 0, N, ctx->stream);
+  launch_blur_diag(ctx->khat, tau, ctx->dgl, ctx->H * (ctx->W / 2 + 1), ctx->stream);
 }
 
 FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
@@ -792,9 +853,8 @@ ideq_status operator_runnable(ideq_ctx* ctx) {
   const auto& op = ctx->op;
   if (op.kind == IDEQ_OP_PHASE && op.step == IDEQ_STEP_PROX)
     return fail(ctx, IDEQ_E_UNSUPPORTED, "phase retrieval has no closed-form prox (cf. PAPER l.1079)");
-  if (op.kind == IDEQ_OP_PHASE) return fail(ctx, IDEQ_E_UNSUPPORTED, "phase retrieval FFT path not built yet");
-  if (op.kind == IDEQ_OP_BLUR && (op.step == IDEQ_STEP_PROX || op.blur_impl == IDEQ_BLUR_FFT))
-    return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT blur path not built yet");
+  if (op.kind == IDEQ_OP_BLUR && op.step == IDEQ_STEP_GRAD && op.blur_impl == IDEQ_BLUR_FFT)
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "the blur gradient step uses the direct convolution (blur_impl DIRECT)");
   return IDEQ_OK;
 }
 
@@ -813,6 +873,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   FinalizeArgs f = make_fin(ctx, N, p);
   if (f.parts > ctx->parts_cap) return fail(ctx, IDEQ_E_INVALID, "internal: partial buffer too small");
   launch_init_state(f, s);
+  if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
   const bool poll = p->tol > 0.f;
@@ -899,6 +960,7 @@ void init_kernel_attributes() {
   init_attrs_simt();
   init_attrs_tc();
   init_attrs_step();
+  init_attrs_fft();
   done = true;
 }
 }  // namespace ideq
@@ -1045,6 +1107,34 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   return IDEQ_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Twiddle tables (fp64 -> fp32, constant setup) and the work spectrum of the FFT operators.
+ideq_status setup_fft(ideq_ctx* ctx, size_t spec_elems) {
+  const int H = ctx->H, W = ctx->W;
+  if (!fft_size_ok(H, W)) return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT operators need power-of-two H, W in [4, 1024]");
+  ideq_status st;
+  void* p;
+  for (int which = 0; which < 2; ++which) {
+    const int n = which == 0 ? H : W;
+    std::vector<float2> tw(n / 2);
+    for (int k = 0; k < n / 2; ++k) {
+      const double a = -2.0 * M_PI * (double)k / (double)n;
+      tw[k] = make_float2((float)cos(a), (float)sin(a));
+    }
+    if ((st = dalloc(ctx, &p, sizeof(float2) * (n / 2 > 0 ? n / 2 : 1)))) return st;
+    CK(cudaMemcpy(p, tw.data(), sizeof(float2) * tw.size(), cudaMemcpyHostToDevice));
+    (which == 0 ? ctx->tw_h : ctx->tw_w) = (float2*)p;
+  }
+  if ((st = dalloc(ctx, &p, sizeof(float2) * spec_elems))) return st;
+  ctx->spec = (float2*)p;
+  return IDEQ_OK;
+}
+}  // namespace
+
+extern "C" {
+
 ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int batch) {
   ideq_status st;
   if ((st = check_ctx(ctx))) return st;
@@ -1060,6 +1150,27 @@ ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int b
     if ((st = dalloc(ctx, &p, n * 4))) return st;
     CK(cudaMemcpy(p, op->kernels, n * 4, cudaMemcpyHostToDevice));
     ctx->d_kern = (float*)p;
+    if (op->blur_impl == IDEQ_BLUR_FFT) {
+      if (op->kernel_per_image) return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT blur needs one kernel shared by the batch");
+      if (op->ksize > H || op->ksize > W) return fail(ctx, IDEQ_E_INVALID, "kernel larger than the image");
+      if ((st = setup_fft(ctx, (size_t)batch * ctx->C * H * (W / 2 + 1)))) return st;
+      // K^ = 2-D DFT of the kernel embedded with its centre tap at the origin (computed on device)
+      void* q;
+      if ((st = dalloc(ctx, &q, sizeof(float2) * H * (W / 2 + 1)))) return st;
+      ctx->khat = (float2*)q;
+      if ((st = dalloc(ctx, &q, sizeof(float) * H * (W / 2 + 1)))) return st;
+      ctx->dgl = (float*)q;
+      launch_embed_kernel(ctx->d_kern, op->ksize, ctx->fbuf, H, W, ctx->stream);
+      FftArgs f = make_fft_args(ctx, nullptr, nullptr);
+      f.C = 1;
+      f.active = nullptr;
+      launch_blur_rows_fwd(f, ctx->fbuf, 0, 1, ctx->stream);
+      launch_blur_cols(f, 2, 1, ctx->stream);
+      CK(cudaMemcpyAsync(ctx->khat, ctx->spec, sizeof(float2) * H * (W / 2 + 1), cudaMemcpyDeviceToDevice,
+                         ctx->stream));
+      CK(cudaStreamSynchronize(ctx->stream));
+      CK(cudaGetLastError());
+    }
   } else if (op->kind == IDEQ_OP_INPAINT) {
     if (!op->masks) return fail(ctx, IDEQ_E_INVALID, "inpainting needs masks");
     void* p;
@@ -1075,6 +1186,7 @@ ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int b
     if ((st = dalloc(ctx, &p, n * 4))) return st;
     CK(cudaMemcpy(p, op->phase_masks, n * 4, cudaMemcpyHostToDevice));
     ctx->d_phase = (float*)p;
+    if ((st = setup_fft(ctx, (size_t)batch * op->n_phase * H * W))) return st;
   } else {
     return fail(ctx, IDEQ_E_INVALID, "unknown operator kind");
   }
@@ -1158,8 +1270,16 @@ ideq_status ideq_fidelity_grad(ideq_ctx* ctx, const float* y, const float* x, fl
     a.fbuf2 = out;
     launch_blur_residual(a, ctx->stream);
     launch_blur_adjoint(0, a, ctx->fbuf, ctx->stream);
+  } else if (op.kind == IDEQ_OP_PHASE) {
+    FftArgs f = make_fft_args(ctx, y, nullptr);
+    f.z = x;
+    f.active = nullptr;
+    StepArgs dummy{};
+    launch_phase_rows_fwd(f, batch, ctx->stream);
+    launch_phase_cols(f, batch, ctx->stream);
+    launch_phase_rows_inv(f, dummy, out, 0, batch, ctx->stream);
   } else {
-    return fail(ctx, IDEQ_E_UNSUPPORTED, "fidelity gradient not built for this operator yet");
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "the blur gradient uses blur_impl DIRECT");
   }
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());
@@ -1175,8 +1295,18 @@ ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, fl
     launch_inpaint_prox(v, y, ctx->d_mask, tau, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
   } else if (ctx->op.kind == IDEQ_OP_PHASE) {
     return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval (cf. PAPER l.1079)");
+  } else if (ctx->op.blur_impl == IDEQ_BLUR_FFT) {
+    // prox_{tau f}(v) = F^-1[F(v + tau A^T y) / (1 + tau |K^|^2)]: the solver's passes with lam = 0
+    prepare_blur_prox(ctx, y, tau, batch);
+    FftArgs f = make_fft_args(ctx, y, nullptr);
+    f.z = v; f.gg = v; f.lam = 0.f; f.tau = tau;
+    f.active = nullptr;
+    StepArgs dummy{};
+    launch_blur_rows_fwd(f, nullptr, 1, batch, ctx->stream);
+    launch_blur_cols(f, 0, batch, ctx->stream);
+    launch_blur_rows_inv(f, dummy, out, 0, batch, ctx->stream);
   } else {
-    return fail(ctx, IDEQ_E_UNSUPPORTED, "FFT blur prox not built yet");
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "the blur prox needs blur_impl FFT");
   }
   CK(cudaStreamSynchronize(ctx->stream));
   CK(cudaGetLastError());

@@ -45,6 +45,37 @@ struct FinalizeArgs {
   int* kdev;
 };
 
+// ---- batched 2-D FFT passes (fft.cu)
+struct FftArgs {
+  int C, H, W, J, logH, logW;
+  const float2* tw_h;   // exp(-2 pi i k / H), k < H/2
+  const float2* tw_w;   // exp(-2 pi i k / W), k < W/2
+  float2* spec;         // blur: [N][C][H][W/2+1]; phase: [N][J][H][W]
+  const float* z;       // prox rhs / phase input
+  const float* gg;
+  const float* aty;
+  float tau, lam;
+  const float* dgl;     // [H][W/2+1] 1 / (1 + tau |K^|^2)
+  const float2* khat;   // [H][W/2+1]
+  const float2* pmask;  // [J][H][W]
+  const float* y;       // phase observations [N][J][H][W]
+  const int* active;
+};
+bool fft_size_ok(int H, int W);
+void fft_fill_args(FftArgs& f);
+int fft_parts_per_image(int C, int H, int W);
+int phase_parts_per_image(int H, int W);
+void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s);
+void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s);
+struct StepArgs;
+void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s);
+void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s);
+void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStream_t s);
+void launch_phase_rows_fwd(const FftArgs& f, int N, cudaStream_t s);
+void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s);
+void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s);
+void init_attrs_fft();
+
 void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s);
 int blur_parts_per_image(int C, int H, int W);
 void launch_blur_residual(const StepArgs& a, cudaStream_t s);

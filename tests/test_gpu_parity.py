@@ -14,10 +14,13 @@ from tests.gpu_util import psnr, rel_l2, torch_cuda
 
 pytestmark = pytest.mark.gpu
 
+# step size of the reduced phase-retrieval case (tools/freeze_tau_pr.py rule on the mini problem)
+TAU_PR_MINI = 0.5 / 21
+
 
 def _mini(name, **kw):
     base = dict(C1=dict(), C2=dict(batch=2, H=48, W=40), C3=dict(batch=2, H=48, W=40),
-                C4=dict(batch=2, H=32, W=32))[name]
+                C4=dict(batch=2, H=64, W=32, tau=TAU_PR_MINI), C5=dict(batch=2, H=64, W=128))[name]
     base.update(kw)
     return configs.get(name, **base)
 
@@ -56,7 +59,7 @@ def test_grad_g_component(name, precision, tol, scale):
         assert rel_l2(u[b].cpu().numpy(), uref) <= tol
 
 
-@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
 def test_fidelity_component(name):
     torch = torch_cuda()
     cfg = _mini(name)
@@ -64,10 +67,17 @@ def test_fidelity_component(name):
     s = _solver(cfg, prob, "fp32")
     fids = osolver.make_fidelities(cfg, prob)
     x = prob["x_true"].astype(np.float32)
+    if name == "C4":
+        x = (0.9 * x + 0.05).astype(np.float32)   # away from the noise-free zero of grad f
     out = torch.zeros_like(_dev(torch, x))
-    s.fidelity_grad(_dev(torch, prob["y"]), _dev(torch, x), out)
-    for b in range(x.shape[0]):
-        assert rel_l2(out[b].cpu().numpy(), fids[b].grad(x[b].astype(np.float64))) <= 1e-5
+    if name != "C5":
+        s.fidelity_grad(_dev(torch, prob["y"]), _dev(torch, x), out)
+        for b in range(x.shape[0]):
+            assert rel_l2(out[b].cpu().numpy(), fids[b].grad(x[b].astype(np.float64))) <= 1e-5
+    if name == "C5":
+        s.fidelity_prox(_dev(torch, prob["y"]), _dev(torch, x), 0.7, out)
+        for b in range(x.shape[0]):
+            assert rel_l2(out[b].cpu().numpy(), fids[b].prox(x[b].astype(np.float64), 0.7)) <= 2e-6
     if cfg["op"] == "inpaint":
         s.fidelity_prox(_dev(torch, prob["y"]), _dev(torch, x), 0.7, out)
         for b in range(x.shape[0]):
@@ -87,7 +97,7 @@ def _run_pair(name, precision, K, lam=None, **kw):
     return cfg, prob, xd.cpu().numpy(), st, tr, orc
 
 
-@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10)])
+@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10), ("C4", 10), ("C5", 10)])
 @pytest.mark.parametrize("stress", [False, True])
 def test_trajectory_fp32(name, K, stress):
     """fp32 iterates after K steps within 1e-4 relative L2, residual within 1e-6 (north_star).
@@ -105,7 +115,7 @@ def test_trajectory_fp32(name, K, stress):
     assert np.allclose(tr, orc["rmax_trace"], rtol=1e-3, atol=1e-6)
 
 
-@pytest.mark.parametrize("name,K", [("C2", 30), ("C3", 30)])
+@pytest.mark.parametrize("name,K", [("C2", 30), ("C3", 30), ("C4", 30), ("C5", 30)])
 def test_trajectory_bf16_psnr(name, K):
     """bf16 reconstruction PSNR within 0.05 dB of the oracle's (north_star)."""
     cfg, prob, x, st, tr, orc = _run_pair(name, "bf16", K)

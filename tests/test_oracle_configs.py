@@ -7,10 +7,11 @@ import pytest
 from oracle import solver
 from paper_2605_19705_b200 import configs, synth
 
-MINI = dict(C1=dict(), C2=dict(batch=2, H=48, W=40), C3=dict(batch=2, H=48, W=40))
+MINI = dict(C1=dict(), C2=dict(batch=2, H=48, W=40), C3=dict(batch=2, H=48, W=40),
+            C4=dict(batch=2, H=64, W=32, tau=0.5 / 21), C5=dict(batch=2, H=64, W=128))
 
 
-@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10)])
+@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10), ("C4", 10), ("C5", 10)])
 def test_stress_variant_is_strong_and_stable(name, K):
     st = configs.STRESS[name]
     cfg = configs.get(name, init_scale=st["init_scale"], **MINI[name])
@@ -19,7 +20,10 @@ def test_stress_variant_is_strong_and_stable(name, K):
     fids = solver.make_fidelities(cfg, prob)
     x0 = prob["x0"][0].astype(np.float64)
     gg = st["lam"] * net.grad_g(x0)
-    gf = fids[0].grad(0.9 * prob["x_true"][0].astype(np.float64))
+    if cfg["step"] == "grad":
+        gf = fids[0].grad(0.9 * prob["x_true"][0].astype(np.float64))
+    else:  # prox variants: compare with the data pull of one prox step from x0
+        gf = (x0 - fids[0].prox(x0, cfg["tau"])) / cfg["tau"]
     assert np.linalg.norm(gg) >= 0.1 * np.linalg.norm(gf)
     out = solver.solve_config(cfg, prob, max_iter=K, tol=0.0, lam=st["lam"])
     assert (out["status"] == solver.MAX_ITER).all()
