@@ -96,107 +96,175 @@ void launch_conv_simt(const ConvGeom& g, const T* in, const T* wB, T* out, const
   conv_simt_kernel<T><<<grid, 256, 0, s>>>(g, in, wB, out, aux);
 }
 
+// ------------------------------------------------------------------ vector helpers
+// 8 consecutive channels <-> 8 floats (16 B of bf16 or 32 B of fp32)
+__device__ __forceinline__ void load8(const __nv_bfloat16* p, float (&v)[8]) {
+  const uint4 u = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(h[e]); v[2 * e] = f.x; v[2 * e + 1] = f.y; }
+}
+__device__ __forceinline__ void load8(const float* p, float (&v)[8]) {
+  const float4 a = *reinterpret_cast<const float4*>(p), b = *reinterpret_cast<const float4*>(p + 4);
+  v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+__device__ __forceinline__ void store8(__nv_bfloat16* p, const float (&v)[8]) {
+  uint4 u;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) h[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+__device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
+  *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(p + 4) = make_float4(v[4], v[5], v[6], v[7]);
+}
+
 // ------------------------------------------------------------------ head-side: image -> features
 // out[n,h,w,co] = epi( sum_{ci,a,b} w_t[co][ci][a][b] in[n,ci,h+a-1,w+b-1] ), zero padding.
+// 16x16 output pixels per block; the (C x 18 x 18) input halo tile is staged in shared memory;
+// each thread owns one pixel and all WO outputs, stored as 16-byte vectors.
 template <typename T, int WO>
 __global__ void __launch_bounds__(256) img2feat_kernel(const float* __restrict__ in, const float* __restrict__ w_t,
                                                        T* __restrict__ out, const T* __restrict__ aux, int epi,
                                                        int N, int C, int H, int W) {
-  __shared__ float wsm[WO * 3 * 9];
+  __shared__ __align__(16) float wsm[3 * 9][WO];
+  __shared__ float tile[3][18][18 + 1];
   for (int t = threadIdx.x; t < WO * C * 9; t += blockDim.x) {
     const int co = t / (C * 9), r = t % (C * 9);
-    wsm[r * WO + co] = w_t[t];  // [ci*9 + a*3 + b][co]
+    wsm[r][co] = w_t[t];  // [ci*9 + a*3 + b][co]
+  }
+  const int n = blockIdx.z, h0 = blockIdx.y * 16, w0 = blockIdx.x * 16;
+  const long long HW = (long long)H * W;
+  for (int t = threadIdx.x; t < C * 18 * 18; t += blockDim.x) {
+    const int ci = t / 324, q = t % 324, u = q / 18, v = q % 18;
+    const int hh = h0 + u - 1, ww = w0 + v - 1;
+    tile[ci][u][v] = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? in[((long long)n * C + ci) * HW + (long long)hh * W + ww] : 0.f;
   }
   __syncthreads();
-  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  const long long HW = (long long)H * W;
-  if (pix >= (long long)N * HW) return;
-  const int n = (int)(pix / HW);
-  const int h = (int)((pix % HW) / W), w = (int)(pix % W);
-  float acc[WO];
+  const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
+  const int h = h0 + ty, w = w0 + tx;
+  if (h >= H || w >= W) return;
+  const long long pix = (long long)n * HW + (long long)h * W + w;
+  constexpr int G = WO < 32 ? WO : 32;  // outputs per register group (keeps acc in registers)
+#pragma unroll 1
+  for (int g0 = 0; g0 < WO; g0 += G) {
+    float acc[G];
 #pragma unroll
-  for (int co = 0; co < WO; ++co) acc[co] = 0.f;
-  for (int ci = 0; ci < C; ++ci) {
-    const float* plane = in + ((long long)n * C + ci) * HW;
+    for (int co = 0; co < G; ++co) acc[co] = 0.f;
+    for (int ci = 0; ci < C; ++ci) {
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
+      for (int a = 0; a < 3; ++a) {
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const int hh = h + a - 1, ww = w + b - 1;
-        const float v = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? plane[(long long)hh * W + ww] : 0.f;
-        const float* wr = wsm + (ci * 9 + a * 3 + b) * WO;
+        for (int b = 0; b < 3; ++b) {
+          const float v = tile[ci][ty + a][tx + b];
+          const float4* wr = reinterpret_cast<const float4*>(wsm[ci * 9 + a * 3 + b] + g0);
 #pragma unroll
-        for (int co = 0; co < WO; ++co) acc[co] = fmaf(wr[co], v, acc[co]);
+          for (int c4 = 0; c4 < G / 4; ++c4) {
+            const float4 w4 = wr[c4];  // broadcast LDS.128: 4 FMAs per shared load
+            acc[4 * c4] = fmaf(w4.x, v, acc[4 * c4]);
+            acc[4 * c4 + 1] = fmaf(w4.y, v, acc[4 * c4 + 1]);
+            acc[4 * c4 + 2] = fmaf(w4.z, v, acc[4 * c4 + 2]);
+            acc[4 * c4 + 3] = fmaf(w4.w, v, acc[4 * c4 + 3]);
+          }
+        }
       }
     }
-  }
-  T* o = out + pix * WO;
-  const T* x = aux ? aux + pix * WO : nullptr;
+    T* o = out + pix * WO + g0;
+    const T* x = aux ? aux + pix * WO + g0 : nullptr;
 #pragma unroll
-  for (int co = 0; co < WO; ++co) {
-    const float av = x ? ElemOps<T>::ld(x + co) : 0.f;
-    ElemOps<T>::st(o + co, apply_epi(epi, acc[co], av));
+    for (int c8 = 0; c8 < G; c8 += 8) {
+      float v[8], av[8];
+      if (x) load8(x + c8, av);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = apply_epi(epi, acc[c8 + e], x ? av[e] : 0.f);
+      store8(o + c8, v);
+    }
   }
 }
 
 template <typename T>
 void launch_img2feat(const float* in, const float* w_t, T* out, const T* aux, int epi, int N, int C, int H, int W,
                      int wout, cudaStream_t s) {
-  const long long P = (long long)N * H * W;
-  const unsigned blocks = (unsigned)((P + 255) / 256);
+  dim3 grid((W + 15) / 16, (H + 15) / 16, N);
   switch (wout) {
-    case 16: img2feat_kernel<T, 16><<<blocks, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
-    case 32: img2feat_kernel<T, 32><<<blocks, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
-    case 64: img2feat_kernel<T, 64><<<blocks, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
+    case 16: img2feat_kernel<T, 16><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
+    case 32: img2feat_kernel<T, 32><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
+    case 64: img2feat_kernel<T, 64><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
     default: break;  // rejected by the runtime at create
   }
 }
 
 // ------------------------------------------------------------------ tail-side: features -> image
 // out[n,c,h,w] = sum_{ci,a,b} w_t[c][ci][a][b] in[n,h+a-1,w+b-1,ci] + alpha * aux[n,c,h,w]
-// 16x16 output pixels per block; input tile 18x18xWI staged in shared memory.
+// 16x16 output pixels per block; the 18x18xWI input tile is loaded with 16-byte vectors and
+// kept as fp32 with a padded pixel stride (WI+4 floats) so float4 reads are conflict-free.
 template <typename T, int WI>
 __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in, const float* __restrict__ w_t,
                                                        float* __restrict__ out, const float* __restrict__ aux,
                                                        float alpha, int N, int C, int H, int W) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  float* wsm = reinterpret_cast<float*>(smraw);                  // [C][9][WI]
-  constexpr int PS = WI + (sizeof(T) == 4 ? 1 : 2);              // padded pixel stride (bank spread)
-  T* tile = reinterpret_cast<T*>(smraw + sizeof(float) * 3 * 9 * WI);  // [18][18][PS]
+  extern __shared__ __align__(16) float smf[];
+  constexpr int PS = WI + 4;
+  float4* wsm = reinterpret_cast<float4*>(smf);  // [9][WI] : (a*3+b, ci) -> (c0, c1, c2, 0)
+  float* tile = smf + 9 * WI * 4;                 // [18*18][PS]
   const int n = blockIdx.z;
   const int h0 = blockIdx.y * 16, w0 = blockIdx.x * 16;
-  for (int t = threadIdx.x; t < C * WI * 9; t += blockDim.x) {
-    const int c = t / (WI * 9), r = t % (WI * 9);
-    const int ci = r / 9, ab = r % 9;
-    wsm[(c * 9 + ab) * WI + ci] = w_t[t];
+  for (int t = threadIdx.x; t < 9 * WI; t += blockDim.x) {
+    const int ab = t / WI, ci = t % WI;
+    float4 w4;
+    w4.x = w_t[(0 * WI + ci) * 9 + ab];
+    w4.y = C > 1 ? w_t[(1 * WI + ci) * 9 + ab] : 0.f;
+    w4.z = C > 1 ? w_t[(2 * WI + ci) * 9 + ab] : 0.f;
+    w4.w = 0.f;
+    wsm[t] = w4;
   }
-  const T zero = T(0.f);
-  for (int t = threadIdx.x; t < 18 * 18 * WI; t += blockDim.x) {
-    const int ci = t % WI, q = t / WI;
+  constexpr int V = WI / 8;  // 16-byte (bf16) vectors per pixel
+  for (int t = threadIdx.x; t < 18 * 18 * V; t += blockDim.x) {
+    const int q = t / V, c8 = (t % V) * 8;
     const int u = q / 18, v = q % 18;
     const int hh = h0 + u - 1, ww = w0 + v - 1;
-    tile[q * PS + ci] = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? in[(((long long)n * H + hh) * W + ww) * WI + ci] : zero;
+    float f[8];
+    if (hh >= 0 && hh < H && ww >= 0 && ww < W) {
+      load8(in + (((long long)n * H + hh) * W + ww) * WI + c8, f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = 0.f;
+    }
+    float* dst = tile + q * PS + c8;
+    *reinterpret_cast<float4*>(dst) = make_float4(f[0], f[1], f[2], f[3]);
+    *reinterpret_cast<float4*>(dst + 4) = make_float4(f[4], f[5], f[6], f[7]);
   }
   __syncthreads();
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
   const int h = h0 + ty, w = w0 + tx;
-  float acc[3] = {0.f, 0.f, 0.f};
+  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const T* tp = tile + ((ty + a) * 18 + (tx + b)) * PS;
-      for (int ci = 0; ci < WI; ++ci) {
-        const float v = ElemOps<T>::ld(tp + ci);
-        for (int c = 0; c < C; ++c) acc[c] = fmaf(wsm[(c * 9 + a * 3 + b) * WI + ci], v, acc[c]);
+      const float* tp = tile + ((ty + a) * 18 + (tx + b)) * PS;
+      const float4* wp = wsm + (a * 3 + b) * WI;
+#pragma unroll 4
+      for (int ci = 0; ci < WI; ci += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(tp + ci);
+        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 ww = wp[ci + e];  // broadcast LDS.128 of the 3 output weights
+          acc0 = fmaf(ww.x, vv[e], acc0);
+          acc1 = fmaf(ww.y, vv[e], acc1);
+          acc2 = fmaf(ww.z, vv[e], acc2);
+        }
       }
     }
   }
   if (h >= H || w >= W) return;
   const long long HW = (long long)H * W;
-  for (int c = 0; c < C; ++c) {
-    const long long o = ((long long)n * C + c) * HW + (long long)h * W + w;
-    out[o] = acc[c] + (aux ? alpha * aux[o] : 0.f);
+  const long long o0 = (long long)n * C * HW + (long long)h * W + w;
+  out[o0] = acc0 + (aux ? alpha * aux[o0] : 0.f);
+  if (C > 1) {
+    out[o0 + HW] = acc1 + (aux ? alpha * aux[o0 + HW] : 0.f);
+    out[o0 + 2 * HW] = acc2 + (aux ? alpha * aux[o0 + 2 * HW] : 0.f);
   }
 }
 
@@ -204,20 +272,16 @@ template <typename T>
 void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux, float alpha, int N, int C, int H,
                      int W, int win, cudaStream_t s) {
   dim3 grid((W + 15) / 16, (H + 15) / 16, N);
-  const size_t sm = sizeof(float) * 3 * 9 * win + sizeof(T) * 18 * 18 * (win + 2);
+  const size_t sm = sizeof(float) * (9 * 4 * win + 18 * 18 * (win + 4));
   switch (win) {
-#define F2I(WI)                                                                                                \
-  case WI:                                                                                                     \
-    feat2img_kernel<T, WI><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W);                        \
-    break;
-    F2I(16) F2I(32) F2I(64)
-#undef F2I
+    case 16: feat2img_kernel<T, 16><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
+    case 32: feat2img_kernel<T, 32><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
+    case 64: feat2img_kernel<T, 64><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
     default: break;
   }
 }
 
 void init_attrs_simt() {
-
   set_max_dyn_smem(feat2img_kernel<float, 16>);
   set_max_dyn_smem(feat2img_kernel<float, 32>);
   set_max_dyn_smem(feat2img_kernel<float, 64>);

@@ -22,6 +22,7 @@
 // of tile i+1. Shared-memory stages form an mbarrier ring (full/empty).
 #include <cuda.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 #include "common.cuh"
 #include "kernels.h"
@@ -84,6 +85,13 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uin
   d |= (uint64_t)(layout & 7u) << 61;
   return d;
 }
+// Same, for a matrix whose start is not aligned to the swizzle repeat (a row-shifted window of
+// a halo tile): bits [49,52) carry the pattern phase (start >> 7) & 7.
+// Row-shifted windows of a swizzled halo tile (start not aligned to the 8-row swizzle atom):
+// the tensor core applies the 64B/128B swizzle on ABSOLUTE shared-memory address bits, exactly
+// as TMA wrote them, so the window is described by shifting the start address alone with the
+// base-offset field left at 0 (measured on B200: tools/halo_probe.py; the (addr>>7)&7
+// base-offset encodings give wrong results).
 
 // Instruction descriptor for kind::f16: bf16 x bf16 -> f32, both K-major, M=128, N=n.
 __device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
@@ -123,6 +131,27 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// bf16-mode epilogue transcendentals (outputs are rounded to bf16, rel. 2^-9): softplus via the
+// SFU exp/log; sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a
+// to avoid the cancellation of 1 - exp(-a).
+__device__ __forceinline__ float softplus_fast(float t) { return fmaxf(t, 0.f) + __logf(1.f + __expf(-fabsf(t))); }
+__device__ __forceinline__ float dsoftplus_from_act_fast(float a) {
+  return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - __expf(-a);
+}
+
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3,
                                              int c4) {
   asm volatile(
@@ -135,7 +164,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
 // ------------------------------------------------------------------ kernel
 struct TcParams {
@@ -144,9 +173,10 @@ struct TcParams {
   uint32_t a_bytes, b_bytes, tmem_cols;
   uint32_t epi_box_bytes;  // one epilogue box: 128 rows x BOXC columns (bf16)
   uint32_t epi_tx_bytes;   // TMA bytes of one aux tile (R*Wt rows x BN columns)
+  uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x 3 x KC halo buffer (1 KB aligned)
 };
 
-constexpr int TC_THREADS = 192;
+constexpr int TC_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
 // Epilogue boxes are BOXC = min(BN, 64) columns wide: 128-byte rows (SW128) for 64 columns,
 // 64-byte rows (SW64) for 32. A thread owns one pixel row; 16-byte chunk j of row r lives at
@@ -166,7 +196,11 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-template <int KC, int EPI, int BOXC>
+// HALO = true (3x3 convs on one-row tiles, single N tile): one TMA box of (Wt+2) x 3 input
+// pixels per channel chunk feeds all 9 taps through row-shifted UMMA descriptors, and the
+// layer's weights stay resident in shared memory for the persistent CTA's lifetime, so the
+// input crosses L2 ~3x instead of 9x and the weights once per CTA instead of once per tile.
+template <int KC, int EPI, int BOXC, bool HALO>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmAux,
@@ -180,24 +214,29 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const uint32_t a_stage = 128u * KC * 2u;
   const uint32_t b_stage = (uint32_t)BN * KC * 2u;
   const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
-  const uint32_t sA = base;
-  const uint32_t sB = sA + S * a_stage;
-  const uint32_t sE = sB + S * b_stage;
+  const ConvGeom& g = P.g;
+  const int nkb = g.ntaps * g.nchunk;
+  // non-HALO: [A stages][B stages][epi x2]; HALO: [resident W (nkb B boxes)][halo stages][epi x2]
+  const uint32_t sW = base;
+  const uint32_t sA = HALO ? sW + (uint32_t)nkb * b_stage : base;
+  const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
+  const uint32_t sE = HALO ? sB : sB + S * b_stage;
   const uint32_t sBar = sE + 2u * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
-  // barriers: full[S], empty[S], tfull[2], tempty[2], auxfull[2], epifree[2]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 8);
+  // barriers: full[S], empty[S], tfull[2], tempty[2], auxfull[2], epifree[2], wfull
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
   const uint32_t full0 = sBar, empty0 = sBar + 8u * S;
   const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 16u, auxfull0 = tempty0 + 16u, epifree0 = auxfull0 + 16u;
+  const uint32_t wfull = epifree0 + 16u;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const ConvGeom& g = P.g;
 
   if (threadIdx.x == 0) {
+    mbar_init(wfull, 1);
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
-      mbar_init(tempty0 + 8u * a, 4);
+      mbar_init(tempty0 + 8u * a, 8);
       mbar_init(auxfull0 + 8u * a, 1);
       mbar_init(epifree0 + 8u * a, 1);
     }
@@ -218,7 +257,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
-  const int nkb = g.ntaps * g.nchunk;
   const int total = P.m_tiles * P.n_tiles;
   const int per_img = g.tiles_h * g.tiles_w;
   const int nbox = BN / BOXC;
@@ -229,14 +267,25 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
+      if (HALO) {  // resident weights: every K-block of the (single) N tile, once per CTA
+        mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
+        for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
+      }
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         const int mt = t / P.n_tiles, nt = t % P.n_tiles;
         const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
         const int h0 = th * g.R, w0 = tw * g.Wt;
         // the aux tile goes into this tile's epilogue buffer; it is requested after the first
-        // min(S, nkb) operand stages so waiting for the buffer never starves the MMA warp
-        const int kb_aux = (S < nkb ? S : nkb) - 1;
-        for (int kb = 0; kb < nkb; ++kb) {
+        // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
+        const int nload = HALO ? g.nchunk : nkb;
+        const int kb_aux = (S < nload ? S : nload) - 1;
+        for (int kb = 0; kb < nload; ++kb) {
+          if (HALO) {
+            mbar_wait(empty0 + 8u * s, ph ^ 1u);
+            mbar_expect_tx(full0 + 8u * s, P.a_bytes);
+            tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
+            if (++s == S) { s = 0; ph ^= 1u; }
+          } else {
           const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
           mbar_wait(empty0 + 8u * s, ph ^ 1u);
           mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
@@ -244,6 +293,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                       img);
           tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * BN, kb);
           if (++s == S) { s = 0; ph ^= 1u; }
+          }
           if (HAS_AUX && kb == kb_aux) {
             mbar_wait(epifree0 + 8u * acc, aph ^ 1u);  // previous store from this buffer has drained
             mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
@@ -267,10 +317,35 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       uint32_t ph = 0;
       int acc = 0;
       uint32_t aph = 0;
+      if (HALO) mbar_wait(wfull, 0);
+      const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
         mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+        if (HALO) {
+          for (int ch = 0; ch < g.nchunk; ++ch) {
+            mbar_wait(full0 + 8u * s, ph);
+            tc_fence_after();
+            const uint32_t halo = sA + s * P.halo_stage;
+            for (int tap = 0; tap < 9; ++tap) {
+              const uint32_t p0 = (uint32_t)((g.dh[tap] + 1) * (g.Wt + 2) + (g.dw[tap] + 1));
+              const uint32_t a_addr = halo + p0 * hrow;
+              const uint32_t b_addr = sW + (uint32_t)(tap * g.nchunk + ch) * b_stage;
+#pragma unroll
+              for (int k = 0; k < KC / 16; ++k) {
+                const uint64_t ad = make_sdesc(a_addr + 32u * k, sbo, layout);
+                const uint64_t bd = make_sdesc(b_addr + 32u * k, sbo, layout);
+                mma_bf16(d_tmem, ad, bd, idesc, (ch | tap | k) ? 1u : 0u);
+              }
+            }
+            mma_commit(empty0 + 8u * s);
+            if (++s == S) { s = 0; ph ^= 1u; }
+          }
+          mma_commit(tfull0 + 8u * acc);
+          if (++acc == 2) { acc = 0; aph ^= 1u; }
+          continue;
+        }
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(full0 + 8u * s, ph);
           tc_fence_after();
@@ -290,10 +365,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
     __syncwarp();
   } else {
-    // ---------------- epilogue warps 2..5: TMEM lane quadrant = warp % 4, one pixel row per thread
+    // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
+    // thread; the two warps of a quadrant split the tile's columns in halves
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const bool leader = (warp == 2 && lane == 0);
+    const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
     int acc = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
@@ -309,13 +387,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       mbar_wait(tfull0 + 8u * acc, aph);
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        float v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+      for (int c0 = cbeg; c0 < cend; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
         const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
         const int j0 = (c0 % BOXC) / 8;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 2; ++q) {
           const uint32_t a = epi_chunk_addr<BOXC>(box, row, j0 + q);
           float o[8];
           if (HAS_AUX) {
@@ -328,13 +406,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 o[2 * e] = v[q * 8 + 2 * e] + f.x;
                 o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
               } else {
-                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act(f.x);
-                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act(f.y);
+                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast(f.x);
+                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast(f.y);
               }
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = (EPI == EPI_SOFTPLUS) ? softplus_f(v[q * 8 + e]) : v[q * 8 + e];
+            for (int e = 0; e < 8; ++e) o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast(v[q * 8 + e]) : v[q * 8 + e];
           }
           uint4 w;
           __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
@@ -392,7 +470,7 @@ static EncodeTiledFn get_encode() {
 struct TcPlan {
   CUtensorMap tmA, tmB, tmOut, tmAux;
   TcParams P;
-  int KC, epi, boxc, grid;
+  int KC, epi, boxc, grid, halo;
   size_t smem;
 };
 
@@ -409,6 +487,18 @@ bool tc_supported(const ConvGeom& g) {
   if ((g.inC * 2) % 16 != 0) return false;
   if (g.OHo % g.osh != 0) return false;
   return true;
+}
+
+// Halo variant: 3x3 taps (|dh|,|dw| <= 1, no parity planes), one-row tiles that fill the M=128
+// MMA, a single N tile, and resident weights that fit next to two halo buffers.
+static bool tc_halo_ok(const ConvGeom& g) {
+  if (g.ntaps != 9 || g.R != 1 || g.Wt != 128 || g.inP != 1) return false;
+  for (int t = 0; t < 9; ++t)
+    if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return false;
+  const int BN = tc_bn(g);
+  if (g.ncols != BN) return false;
+  const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * 2;
+  return wbytes <= 80 * 1024;
 }
 
 // 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
@@ -442,7 +532,10 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   p->boxc = boxc;
   const CUtensorMapSwizzle swA = g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   const CUtensorMapSwizzle swE = boxc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  CUresult r = encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
+  const char* nh = getenv("IDEQ_NO_HALO");  // A/B switch for measurements
+  p->halo = (tc_halo_ok(g) && !(nh && atoi(nh) != 0)) ? 1 : 0;
+  CUresult r = p->halo ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
+                       : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
   {
     const int nkb = g.ntaps * g.nchunk;
@@ -478,16 +571,31 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   while (tc < cols) tc <<= 1;
   P.tmem_cols = tc;
   const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
-  // two CTAs per SM when the whole working set fits twice (small-N layers are latency-bound)
   const size_t fixed = 1024 + 2 * e_stage + 256;
-  int stages = (int)((200 * 1024 - fixed) / (a_stage + b_stage));
-  if (stages > 8) stages = 8;
-  int ctas = 1;
-  const int st2 = (int)(((227 * 1024) / 2 - fixed) / (a_stage + b_stage));
-  if (st2 >= 4 && tc * 2 <= 512) { stages = st2 > 6 ? 6 : st2; ctas = 2; }
-  if (stages < 2) { snprintf(err, errlen, "tcgen05 conv: smem too small"); delete p; return nullptr; }
-  P.stages = stages;
-  p->smem = fixed + stages * (a_stage + b_stage);
+  int stages = 0, ctas = 1;
+  if (p->halo) {
+    // resident weights + a ring of (Wt+2) x 3 halo buffers
+    const size_t wbytes = (size_t)9 * g.nchunk * b_stage;
+    P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
+    P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
+    const size_t avail2 = (227 * 1024) / 2, avail1 = 220 * 1024;
+    const int s2 = (int)((avail2 - fixed - wbytes) / P.halo_stage);
+    const int s1 = (int)((avail1 - fixed - wbytes) / P.halo_stage);
+    if (s2 >= 2 && tc * 2 <= 512 && avail2 > fixed + wbytes) { stages = s2 > 4 ? 4 : s2; ctas = 2; }
+    else { stages = s1 > 4 ? 4 : s1; }
+    if (stages < 2) { snprintf(err, errlen, "tcgen05 halo conv: smem too small"); delete p; return nullptr; }
+    P.stages = stages;
+    p->smem = fixed + wbytes + stages * P.halo_stage;
+  } else {
+    // two CTAs per SM when the whole working set fits twice (small-N layers are latency-bound)
+    stages = (int)((200 * 1024 - fixed) / (a_stage + b_stage));
+    if (stages > 8) stages = 8;
+    const int st2 = (int)(((227 * 1024) / 2 - fixed) / (a_stage + b_stage));
+    if (st2 >= 4 && tc * 2 <= 512) { stages = st2 > 6 ? 6 : st2; ctas = 2; }
+    if (stages < 2) { snprintf(err, errlen, "tcgen05 conv: smem too small"); delete p; return nullptr; }
+    P.stages = stages;
+    p->smem = fixed + stages * (a_stage + b_stage);
+  }
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -496,7 +604,10 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
 
 template <int KC, int EPI, int BOXC>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
-  conv_tc_kernel<KC, EPI, BOXC><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
+  if (p->halo)
+    conv_tc_kernel<KC, EPI, BOXC, true><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
+  else
+    conv_tc_kernel<KC, EPI, BOXC, false><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
 }
 
 template <int KC, int BOXC>
@@ -517,21 +628,27 @@ void tc_launch(const TcPlan* p, cudaStream_t s) {
   }
 }
 
+int tc_plan_is_halo(const TcPlan* p) { return p->halo; }
+
 void tc_free_plan(TcPlan* p) { delete p; }
 
-template <int KC, int BOXC>
+template <int KC, int BOXC, bool HALO>
 static void attrs_epi() {
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_STORE, BOXC>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_RESADD, BOXC>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SIGMUL, BOXC>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_STORE, BOXC, HALO>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC, HALO>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_RESADD, BOXC, HALO>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SIGMUL, BOXC, HALO>);
 }
 
 void init_attrs_tc() {
-  attrs_epi<64, 64>();
-  attrs_epi<64, 32>();
-  attrs_epi<32, 64>();
-  attrs_epi<32, 32>();
+  attrs_epi<64, 64, false>();
+  attrs_epi<64, 32, false>();
+  attrs_epi<32, 64, false>();
+  attrs_epi<32, 32, false>();
+  attrs_epi<64, 64, true>();
+  attrs_epi<64, 32, true>();
+  attrs_epi<32, 64, true>();
+  attrs_epi<32, 32, true>();
 }
 
 }  // namespace ideq

@@ -37,7 +37,8 @@ def _epi_ref(acc, epi, aux):
 
 CASES = []
 for kind in range(6):
-    for cin, cout in [(32, 32), (64, 128)]:
+    pairs = [(32, 32), (64, 128)] + ([(64, 64)] if kind in (0, 1) else [])   # (64,64): resident-weight halo path
+    for cin, cout in pairs:
         for (H, W) in [(20, 40), (8, 272)]:
             if kind in (2, 3, 4, 5) and (H % 2 or W % 2):
                 continue
