@@ -95,9 +95,12 @@ typedef struct {
   size_t n_weights;
 } ideq_net_desc;
 
-/* Data parallelism over images: rank r owns a contiguous shard. world == 1 makes
- * no NCCL call. nccl_id comes from ideq_get_nccl_id on rank 0 (the caller
- * broadcasts it, e.g. through torch.distributed). */
+/* Data parallelism over images: rank r owns a contiguous shard. With a dist
+ * descriptor (any world >= 1) the context builds an NCCL communicator and the
+ * GLOBAL_MAX rule all-reduces (MAX) one float every check_every iterations; with
+ * dist == NULL no NCCL call is made. nccl_id comes from ideq_get_nccl_id on rank 0
+ * (the caller broadcasts it, e.g. through torch.distributed). NCCL is loaded at
+ * run time (libnccl.so.2); IDEQ_E_NCCL if it is missing or a call fails. */
 typedef struct {
   int rank, world;
   unsigned char nccl_id[128];

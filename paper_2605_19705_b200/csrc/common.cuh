@@ -35,6 +35,7 @@ enum Epi : int {
   EPI_SOFTPLUS = 1,  // out = sp(acc)                       (RB conv A forward; saved)
   EPI_RESADD = 2,    // out = acc + aux                     (RB conv B fwd / conv A^T, skip adds)
   EPI_SIGMUL = 3,    // out = acc * sp'(.) from aux = saved activation   (conv B^T)
+  EPI_IMG = 4,       // tcgen05 only: columns [0, C) -> fp32 NCHW image planes, + alpha * aux image
 };
 
 // ---------------------------------------------------------------- implicit-GEMM geometry

@@ -122,63 +122,75 @@ __device__ __forceinline__ void store8(float* p, const float (&v)[8]) {
 
 // ------------------------------------------------------------------ head-side: image -> features
 // out[n,h,w,co] = epi( sum_{ci,a,b} w_t[co][ci][a][b] in[n,ci,h+a-1,w+b-1] ), zero padding.
-// 16x16 output pixels per block; the (C x 18 x 18) input halo tile is staged in shared memory;
-// each thread owns one pixel and all WO outputs, stored as 16-byte vectors.
-template <typename T, int WO>
+// A block covers 16 x 32 output pixels; the (C x 34 x 18) input halo tile is staged in shared
+// memory; each thread owns two pixels (rows ty, ty+16) so every broadcast weight load feeds
+// 8 FMAs (the kernel is otherwise limited by shared-memory issue, not FMA).
+constexpr int HT_ROWS = 32;
+template <typename T, int WO, int C>
 __global__ void __launch_bounds__(256) img2feat_kernel(const float* __restrict__ in, const float* __restrict__ w_t,
                                                        T* __restrict__ out, const T* __restrict__ aux, int epi,
-                                                       int N, int C, int H, int W) {
+                                                       int N, int H, int W) {
   __shared__ __align__(16) float wsm[3 * 9][WO];
-  __shared__ float tile[3][18][18 + 1];
+  __shared__ float tile[3][HT_ROWS + 2][18 + 1];
   for (int t = threadIdx.x; t < WO * C * 9; t += blockDim.x) {
     const int co = t / (C * 9), r = t % (C * 9);
     wsm[r][co] = w_t[t];  // [ci*9 + a*3 + b][co]
   }
-  const int n = blockIdx.z, h0 = blockIdx.y * 16, w0 = blockIdx.x * 16;
+  const int n = blockIdx.z, h0 = blockIdx.y * HT_ROWS, w0 = blockIdx.x * 16;
   const long long HW = (long long)H * W;
-  for (int t = threadIdx.x; t < C * 18 * 18; t += blockDim.x) {
-    const int ci = t / 324, q = t % 324, u = q / 18, v = q % 18;
+  for (int t = threadIdx.x; t < C * (HT_ROWS + 2) * 18; t += blockDim.x) {
+    const int ci = t / ((HT_ROWS + 2) * 18), q = t % ((HT_ROWS + 2) * 18), u = q / 18, v = q % 18;
     const int hh = h0 + u - 1, ww = w0 + v - 1;
     tile[ci][u][v] = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? in[((long long)n * C + ci) * HW + (long long)hh * W + ww] : 0.f;
   }
   __syncthreads();
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  const int h = h0 + ty, w = w0 + tx;
-  if (h >= H || w >= W) return;
-  const long long pix = (long long)n * HW + (long long)h * W + w;
+  const int w = w0 + tx;
   constexpr int G = WO < 32 ? WO : 32;  // outputs per register group (keeps acc in registers)
 #pragma unroll 1
   for (int g0 = 0; g0 < WO; g0 += G) {
-    float acc[G];
+    float acc[2][G];
 #pragma unroll
-    for (int co = 0; co < G; ++co) acc[co] = 0.f;
-    for (int ci = 0; ci < C; ++ci) {
+    for (int co = 0; co < G; ++co) { acc[0][co] = 0.f; acc[1][co] = 0.f; }
+#pragma unroll
+    for (int ci = 0; ci < C; ++ci) {  // C is a template constant: the 9*C taps unroll fully
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
 #pragma unroll
         for (int b = 0; b < 3; ++b) {
-          const float v = tile[ci][ty + a][tx + b];
+          const float v0 = tile[ci][ty + a][tx + b];
+          const float v1 = tile[ci][ty + 16 + a][tx + b];
           const float4* wr = reinterpret_cast<const float4*>(wsm[ci * 9 + a * 3 + b] + g0);
 #pragma unroll
           for (int c4 = 0; c4 < G / 4; ++c4) {
-            const float4 w4 = wr[c4];  // broadcast LDS.128: 4 FMAs per shared load
-            acc[4 * c4] = fmaf(w4.x, v, acc[4 * c4]);
-            acc[4 * c4 + 1] = fmaf(w4.y, v, acc[4 * c4 + 1]);
-            acc[4 * c4 + 2] = fmaf(w4.z, v, acc[4 * c4 + 2]);
-            acc[4 * c4 + 3] = fmaf(w4.w, v, acc[4 * c4 + 3]);
+            const float4 w4 = wr[c4];
+            acc[0][4 * c4] = fmaf(w4.x, v0, acc[0][4 * c4]);
+            acc[0][4 * c4 + 1] = fmaf(w4.y, v0, acc[0][4 * c4 + 1]);
+            acc[0][4 * c4 + 2] = fmaf(w4.z, v0, acc[0][4 * c4 + 2]);
+            acc[0][4 * c4 + 3] = fmaf(w4.w, v0, acc[0][4 * c4 + 3]);
+            acc[1][4 * c4] = fmaf(w4.x, v1, acc[1][4 * c4]);
+            acc[1][4 * c4 + 1] = fmaf(w4.y, v1, acc[1][4 * c4 + 1]);
+            acc[1][4 * c4 + 2] = fmaf(w4.z, v1, acc[1][4 * c4 + 2]);
+            acc[1][4 * c4 + 3] = fmaf(w4.w, v1, acc[1][4 * c4 + 3]);
           }
         }
       }
     }
-    T* o = out + pix * WO + g0;
-    const T* x = aux ? aux + pix * WO + g0 : nullptr;
 #pragma unroll
-    for (int c8 = 0; c8 < G; c8 += 8) {
-      float v[8], av[8];
-      if (x) load8(x + c8, av);
+    for (int p = 0; p < 2; ++p) {
+      const int h = h0 + ty + 16 * p;
+      if (h >= H || w >= W) continue;
+      const long long pix = (long long)n * HW + (long long)h * W + w;
+      T* o = out + pix * WO + g0;
+      const T* x = aux ? aux + pix * WO + g0 : nullptr;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) v[e] = apply_epi(epi, acc[c8 + e], x ? av[e] : 0.f);
-      store8(o + c8, v);
+      for (int c8 = 0; c8 < G; c8 += 8) {
+        float v[8], av[8];
+        if (x) load8(x + c8, av);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] = apply_epi(epi, acc[p][c8 + e], x ? av[e] : 0.f);
+        store8(o + c8, v);
+      }
     }
   }
 }
@@ -186,19 +198,24 @@ __global__ void __launch_bounds__(256) img2feat_kernel(const float* __restrict__
 template <typename T>
 void launch_img2feat(const float* in, const float* w_t, T* out, const T* aux, int epi, int N, int C, int H, int W,
                      int wout, cudaStream_t s) {
-  dim3 grid((W + 15) / 16, (H + 15) / 16, N);
+  dim3 grid((W + 15) / 16, (H + HT_ROWS - 1) / HT_ROWS, N);
+#define I2F(WO)                                                                                          \
+  case WO:                                                                                               \
+    if (C == 1) img2feat_kernel<T, WO, 1><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, H, W);         \
+    else img2feat_kernel<T, WO, 3><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, H, W);                \
+    break;
   switch (wout) {
-    case 16: img2feat_kernel<T, 16><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
-    case 32: img2feat_kernel<T, 32><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
-    case 64: img2feat_kernel<T, 64><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, C, H, W); break;
+    I2F(16) I2F(32) I2F(64)
     default: break;  // rejected by the runtime at create
   }
+#undef I2F
 }
 
 // ------------------------------------------------------------------ tail-side: features -> image
 // out[n,c,h,w] = sum_{ci,a,b} w_t[c][ci][a][b] in[n,h+a-1,w+b-1,ci] + alpha * aux[n,c,h,w]
-// 16x16 output pixels per block; the 18x18xWI input tile is loaded with 16-byte vectors and
-// kept as fp32 with a padded pixel stride (WI+4 floats) so float4 reads are conflict-free.
+// A block covers 16 x 32 output pixels (two per thread, rows ty and ty+16); the 34x18xWI input
+// tile is loaded with 16-byte vectors and kept as fp32 with a padded pixel stride (WI+4 floats)
+// so float4 reads are conflict-free; weights are float4 (c0, c1, c2, 0) broadcasts.
 template <typename T, int WI>
 __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in, const float* __restrict__ w_t,
                                                        float* __restrict__ out, const float* __restrict__ aux,
@@ -206,9 +223,9 @@ __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in,
   extern __shared__ __align__(16) float smf[];
   constexpr int PS = WI + 4;
   float4* wsm = reinterpret_cast<float4*>(smf);  // [9][WI] : (a*3+b, ci) -> (c0, c1, c2, 0)
-  float* tile = smf + 9 * WI * 4;                 // [18*18][PS]
+  float* tile = smf + 9 * WI * 4;                 // [(HT_ROWS+2)*18][PS]
   const int n = blockIdx.z;
-  const int h0 = blockIdx.y * 16, w0 = blockIdx.x * 16;
+  const int h0 = blockIdx.y * HT_ROWS, w0 = blockIdx.x * 16;
   for (int t = threadIdx.x; t < 9 * WI; t += blockDim.x) {
     const int ab = t / WI, ci = t % WI;
     float4 w4;
@@ -218,8 +235,8 @@ __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in,
     w4.w = 0.f;
     wsm[t] = w4;
   }
-  constexpr int V = WI / 8;  // 16-byte (bf16) vectors per pixel
-  for (int t = threadIdx.x; t < 18 * 18 * V; t += blockDim.x) {
+  constexpr int V = WI / 8;  // 8-channel vectors per pixel
+  for (int t = threadIdx.x; t < (HT_ROWS + 2) * 18 * V; t += blockDim.x) {
     const int q = t / V, c8 = (t % V) * 8;
     const int u = q / 18, v = q % 18;
     const int hh = h0 + u - 1, ww = w0 + v - 1;
@@ -236,49 +253,99 @@ __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in,
   }
   __syncthreads();
   const int ty = threadIdx.x >> 4, tx = threadIdx.x & 15;
-  const int h = h0 + ty, w = w0 + tx;
-  float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f;
+  const int w = w0 + tx;
+  float acc[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const float* tp = tile + ((ty + a) * 18 + (tx + b)) * PS;
+      const float* tp0 = tile + ((ty + a) * 18 + (tx + b)) * PS;
+      const float* tp1 = tp0 + 16 * 18 * PS;
       const float4* wp = wsm + (a * 3 + b) * WI;
-#pragma unroll 4
-      for (int ci = 0; ci < WI; ci += 4) {
-        const float4 v = *reinterpret_cast<const float4*>(tp + ci);
-        const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int ci = 0; ci < WI; ci += 4) {  // fully unrolled: loads hoist ahead of their FMAs
+        const float4 v0 = *reinterpret_cast<const float4*>(tp0 + ci);
+        const float4 v1 = *reinterpret_cast<const float4*>(tp1 + ci);
+        const float a0[4] = {v0.x, v0.y, v0.z, v0.w};
+        const float a1[4] = {v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float4 ww = wp[ci + e];  // broadcast LDS.128 of the 3 output weights
-          acc0 = fmaf(ww.x, vv[e], acc0);
-          acc1 = fmaf(ww.y, vv[e], acc1);
-          acc2 = fmaf(ww.z, vv[e], acc2);
+          const float4 ww = wp[ci + e];
+          acc[0][0] = fmaf(ww.x, a0[e], acc[0][0]);
+          acc[0][1] = fmaf(ww.y, a0[e], acc[0][1]);
+          acc[0][2] = fmaf(ww.z, a0[e], acc[0][2]);
+          acc[1][0] = fmaf(ww.x, a1[e], acc[1][0]);
+          acc[1][1] = fmaf(ww.y, a1[e], acc[1][1]);
+          acc[1][2] = fmaf(ww.z, a1[e], acc[1][2]);
         }
       }
     }
   }
-  if (h >= H || w >= W) return;
   const long long HW = (long long)H * W;
-  const long long o0 = (long long)n * C * HW + (long long)h * W + w;
-  out[o0] = acc0 + (aux ? alpha * aux[o0] : 0.f);
-  if (C > 1) {
-    out[o0 + HW] = acc1 + (aux ? alpha * aux[o0 + HW] : 0.f);
-    out[o0 + 2 * HW] = acc2 + (aux ? alpha * aux[o0 + 2 * HW] : 0.f);
+#pragma unroll
+  for (int p = 0; p < 2; ++p) {
+    const int h = h0 + ty + 16 * p;
+    if (h >= H || w >= W) continue;
+    const long long o0 = (long long)n * C * HW + (long long)h * W + w;
+    out[o0] = acc[p][0] + (aux ? alpha * aux[o0] : 0.f);
+    if (C > 1) {
+      out[o0 + HW] = acc[p][1] + (aux ? alpha * aux[o0 + HW] : 0.f);
+      out[o0 + 2 * HW] = acc[p][2] + (aux ? alpha * aux[o0 + 2 * HW] : 0.f);
+    }
   }
 }
 
 template <typename T>
 void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux, float alpha, int N, int C, int H,
                      int W, int win, cudaStream_t s) {
-  dim3 grid((W + 15) / 16, (H + 15) / 16, N);
-  const size_t sm = sizeof(float) * (9 * 4 * win + 18 * 18 * (win + 4));
+  dim3 grid((W + 15) / 16, (H + HT_ROWS - 1) / HT_ROWS, N);
+  const size_t sm = sizeof(float) * (9 * 4 * win + (HT_ROWS + 2) * 18 * (win + 4));
   switch (win) {
     case 16: feat2img_kernel<T, 16><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
     case 32: feat2img_kernel<T, 32><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
     case 64: feat2img_kernel<T, 64><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
     default: break;
   }
+}
+
+// ------------------------------------------------------------------ im2col for the tensor-core head
+// out[n,h,w,k] = in[n, c, h+a-1, w+b-1] with k = c*9 + a*3 + b < 9C, zero elsewhere (k < 32):
+// turns the C -> w0 head conv (and the tail adjoint) into a K = 32 GEMM on tcgen05.
+__global__ void __launch_bounds__(256) im2col32_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
+                                                       int N, int C, int H, int W) {
+  const long long HW = (long long)H * W;
+  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (pix >= (long long)N * HW) return;
+  const int n = (int)(pix / HW), h = (int)((pix % HW) / W), w = (int)(pix % W);
+  float v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = 0.f;
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {  // constant indices keep v[] in registers; C <= 3
+    if (c >= C) break;
+    const float* plane = in + ((long long)n * C + c) * HW;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const int hh = h + a - 1, ww = w + b - 1;
+        v[c * 9 + a * 3 + b] = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? plane[(long long)hh * W + ww] : 0.f;
+      }
+    }
+  }
+  __nv_bfloat16* o = out + pix * 32;
+#pragma unroll
+  for (int k = 0; k < 32; k += 8) {
+    float t[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) t[e] = v[k + e];
+    store8(o + k, t);
+  }
+}
+
+void launch_im2col32(const float* in, __nv_bfloat16* out, int N, int C, int H, int W, cudaStream_t s) {
+  const long long P = (long long)N * H * W;
+  im2col32_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(in, out, N, C, H, W);
 }
 
 void init_attrs_simt() {

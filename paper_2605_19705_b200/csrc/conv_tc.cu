@@ -163,6 +163,12 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// wait until at most n (runtime, 1..3) bulk groups still have to read shared memory
+__device__ __forceinline__ void bulk_wait_read_lt(int n) {
+  if (n <= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+  else if (n == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
+  else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
+}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 
@@ -174,6 +180,13 @@ struct TcParams {
   uint32_t epi_box_bytes;  // one epilogue box: 128 rows x BOXC columns (bf16)
   uint32_t epi_tx_bytes;   // TMA bytes of one aux tile (R*Wt rows x BN columns)
   uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x 3 x KC halo buffer (1 KB aligned)
+  int nacc;                // TMEM accumulator stages (2..4)
+  // EPI_IMG: the first img_c GEMM columns are an image (tail / head adjoint); written as fp32
+  // NCHW planes [N][img_c][OH][OW] plus img_alpha * img_aux (same layout, may be null)
+  float* img_out;
+  const float* img_aux;
+  float img_alpha;
+  int img_c;
 };
 
 constexpr int TC_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
@@ -221,20 +234,22 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const uint32_t sA = HALO ? sW + (uint32_t)nkb * b_stage : base;
   const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
   const uint32_t sE = HALO ? sB : sB + S * b_stage;
-  const uint32_t sBar = sE + 2u * epi_stage;
+  const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
+  const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
-  // barriers: full[S], empty[S], tfull[2], tempty[2], auxfull[2], epifree[2], wfull
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 9);
+  // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1);
   const uint32_t full0 = sBar, empty0 = sBar + 8u * S;
-  const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 16u, auxfull0 = tempty0 + 16u, epifree0 = auxfull0 + 16u;
-  const uint32_t wfull = epifree0 + 16u;
+  const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 8u * NA, auxfull0 = tempty0 + 8u * NA,
+                 epifree0 = auxfull0 + 8u * NA;
+  const uint32_t wfull = epifree0 + 8u * NA;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NA; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
       mbar_init(tempty0 + 8u * a, 8);
       mbar_init(auxfull0 + 8u * a, 1);
@@ -304,7 +319,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             }
           }
         }
-        if (++acc == 2) { acc = 0; aph ^= 1u; }
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
       }
     }
     __syncwarp();
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             if (++s == S) { s = 0; ph ^= 1u; }
           }
           mma_commit(tfull0 + 8u * acc);
-          if (++acc == 2) { acc = 0; aph ^= 1u; }
+          if (++acc == NA) { acc = 0; aph ^= 1u; }
           continue;
         }
         for (int kb = 0; kb < nkb; ++kb) {
@@ -360,7 +375,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           if (++s == S) { s = 0; ph ^= 1u; }
         }
         mma_commit(tfull0 + 8u * acc);
-        if (++acc == 2) { acc = 0; aph ^= 1u; }
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
       }
     }
     __syncwarp();
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     const int row = quad * 32 + lane;
     const bool leader = (warp == 2 && lane == 0);
     const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
-    int acc = 0;
+    int acc = 0, ltile = 0;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
       const int mt = t / P.n_tiles, nt = t % P.n_tiles;
@@ -386,6 +401,32 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       }
       mbar_wait(tfull0 + 8u * acc, aph);
       tc_fence_after();
+      if (EPI == EPI_IMG) {
+        // image planes straight from TMEM: the warps of the first column half own columns 0..15
+        if (half == 0) {
+          float v[16];
+          tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN), v);
+          const int oh = h0 + row / g.Wt, ow = w0 + row % g.Wt;
+          if (row < g.R * g.Wt && oh < g.OH && ow < g.OW) {
+            const long long plane = (long long)g.OH * g.OW;
+            const long long o = (long long)img * P.img_c * plane + (long long)oh * g.OW + ow;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+              if (c < P.img_c) {
+                const float a = P.img_aux ? P.img_alpha * P.img_aux[o + c * plane] : 0.f;
+                P.img_out[o + c * plane] = v[c] + a;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+        epi_bar();
+        if (leader) mbar_arrive(epifree0 + 8u * acc);
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
+        continue;
+      }
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cend; c0 += 16) {
         float v[16];
@@ -434,10 +475,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           tma_store_5d(&tmOut, ebuf + b * P.epi_box_bytes, col % g.CB, w0, col / g.CB, h0, img);
         }
         bulk_commit();
-        bulk_wait_read0();  // smem buffer reusable once the TMA engine has read it
+        // release the buffer as soon as the TMA engine has read it: the next use is NA-1 tiles
+        // away, so the aux prefetch into it gets the most slack (measured faster than keeping
+        // store groups in flight, which delays every release by a tile)
+        bulk_wait_read0();
         mbar_arrive(epifree0 + 8u * acc);
       }
-      if (++acc == 2) { acc = 0; aph ^= 1u; }
+      ++ltile;
+      if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
     if (leader) bulk_wait0();
   }
@@ -549,7 +594,9 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   }
   // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
   // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
-  r = encode5(enc, &p->tmOut, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+  // EPI_IMG writes fp32 image planes directly: the (unused) output map points at the input
+  r = encode5(enc, &p->tmOut, g.epi == EPI_IMG ? (const void*)in : (const void*)out, g.CB, g.OWo, g.osh, g.OHo / g.osh,
+              g.N, boxc, g.Wt, g.R, swE);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map out encode failed (%d)", (int)r); delete p; return nullptr; }
   if (has_aux) {
     r = encode5(enc, &p->tmAux, aux, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
@@ -566,36 +613,35 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   P.b_bytes = (uint32_t)g.KC * 2u * BN;
   P.epi_box_bytes = 128u * boxc * 2u;
   P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
-  uint32_t cols = 2u * BN;
-  uint32_t tc = 32;
-  while (tc < cols) tc <<= 1;
-  P.tmem_cols = tc;
+  // Shared-memory / TMEM plan. Preference order: 4 accumulator stages for narrow N (more tiles
+  // in flight hide the per-tile epilogue latency), then 2 CTAs per SM, then deeper operand rings.
   const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
-  const size_t fixed = 1024 + 2 * e_stage + 256;
-  int stages = 0, ctas = 1;
+  const size_t wbytes = p->halo ? (size_t)9 * g.nchunk * b_stage : 0;
   if (p->halo) {
-    // resident weights + a ring of (Wt+2) x 3 halo buffers
-    const size_t wbytes = (size_t)9 * g.nchunk * b_stage;
     P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
     P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
-    const size_t avail2 = (227 * 1024) / 2, avail1 = 220 * 1024;
-    const int s2 = (int)((avail2 - fixed - wbytes) / P.halo_stage);
-    const int s1 = (int)((avail1 - fixed - wbytes) / P.halo_stage);
-    if (s2 >= 2 && tc * 2 <= 512 && avail2 > fixed + wbytes) { stages = s2 > 4 ? 4 : s2; ctas = 2; }
-    else { stages = s1 > 4 ? 4 : s1; }
-    if (stages < 2) { snprintf(err, errlen, "tcgen05 halo conv: smem too small"); delete p; return nullptr; }
-    P.stages = stages;
-    p->smem = fixed + wbytes + stages * P.halo_stage;
-  } else {
-    // two CTAs per SM when the whole working set fits twice (small-N layers are latency-bound)
-    stages = (int)((200 * 1024 - fixed) / (a_stage + b_stage));
-    if (stages > 8) stages = 8;
-    const int st2 = (int)(((227 * 1024) / 2 - fixed) / (a_stage + b_stage));
-    if (st2 >= 4 && tc * 2 <= 512) { stages = st2 > 6 ? 6 : st2; ctas = 2; }
-    if (stages < 2) { snprintf(err, errlen, "tcgen05 conv: smem too small"); delete p; return nullptr; }
-    P.stages = stages;
-    p->smem = fixed + stages * (a_stage + b_stage);
   }
+  const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
+  const int min_stages = p->halo ? 2 : 3, max_stages = p->halo ? 4 : 8;
+  int stages = 0, ctas = 1, nacc = 0;
+  uint32_t tcols = 0;
+  for (int na = (BN <= 64 ? 4 : 2); na >= 2 && !stages; na -= 2) {
+    uint32_t tc = 32;
+    while (tc < (uint32_t)na * BN) tc <<= 1;
+    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + 512;
+    for (int c = 2; c >= 1 && !stages; --c) {
+      const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
+      if (tc * c > 512 || avail <= fixed) continue;
+      int st = (int)((avail - fixed) / op_stage);
+      if (st > max_stages) st = max_stages;
+      if (st >= min_stages || (c == 1 && na == 2 && st >= 2)) { stages = st; ctas = c; nacc = na; tcols = tc; }
+    }
+  }
+  if (!stages) { snprintf(err, errlen, "tcgen05 conv: shared memory plan failed"); delete p; return nullptr; }
+  P.stages = stages;
+  P.nacc = nacc;
+  P.tmem_cols = tcols;
+  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + 512 + (size_t)stages * op_stage;
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -616,8 +662,16 @@ static void launch_epi(const TcPlan* p, cudaStream_t s) {
     case EPI_SOFTPLUS: launch_one<KC, EPI_SOFTPLUS, BOXC>(p, s); break;
     case EPI_RESADD: launch_one<KC, EPI_RESADD, BOXC>(p, s); break;
     case EPI_SIGMUL: launch_one<KC, EPI_SIGMUL, BOXC>(p, s); break;
+    case EPI_IMG: launch_one<KC, EPI_IMG, BOXC>(p, s); break;
     default: launch_one<KC, EPI_STORE, BOXC>(p, s); break;
   }
+}
+
+void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C) {
+  p->P.img_out = out;
+  p->P.img_aux = aux;
+  p->P.img_alpha = alpha;
+  p->P.img_c = C;
 }
 
 void tc_launch(const TcPlan* p, cudaStream_t s) {
@@ -638,6 +692,7 @@ static void attrs_epi() {
   set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC, HALO>);
   set_max_dyn_smem(conv_tc_kernel<KC, EPI_RESADD, BOXC, HALO>);
   set_max_dyn_smem(conv_tc_kernel<KC, EPI_SIGMUL, BOXC, HALO>);
+  set_max_dyn_smem(conv_tc_kernel<KC, EPI_IMG, BOXC, HALO>);
 }
 
 void init_attrs_tc() {

@@ -25,7 +25,7 @@ using namespace ideq;
 
 namespace {
 
-// ------------------------------------------------------------------ NCCL (dlopen'ed; only when world > 1)
+// ------------------------------------------------------------------ NCCL (dlopen'ed; whenever a dist descriptor is given)
 typedef struct { char internal[128]; } nccl_uid;
 typedef void* nccl_comm;
 struct NcclApi {
@@ -53,7 +53,7 @@ NcclApi g_nccl;
 constexpr int NCCL_FLOAT32 = 7, NCCL_MAX = 2;
 
 // ------------------------------------------------------------------ program description
-enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2 };
+enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IM2COL = 3 };
 
 struct Layer {
   LayerKind kind;
@@ -70,6 +70,7 @@ struct Layer {
   int C = 0, wfeat = 0, epi = 0, N = 0, H = 0, W = 0;
   TcPlan* plan = nullptr;
   bool tc = false;  // tcgen05 path (bf16 U-Net layers) vs FFMA path
+  bool headtail = false;  // head/tail layer (profiled in the head/tail class, not the conv roofline)
   double flops = 0, bytes = 0;
   std::string name;
 };
@@ -105,6 +106,7 @@ struct ideq_ctx {
 
   // solver buffers (fp32 NCHW)
   float *X1 = nullptr, *Z = nullptr, *G = nullptr, *Hc = nullptr, *fbuf = nullptr, *fbuf2 = nullptr;
+  void* im2col = nullptr;  // [N][H][W][32] bf16 (tensor-core head), bf16 U-Net only
   float* partials = nullptr;
   int parts_cap = 0;
   int *active = nullptr, *status = nullptr, *iters = nullptr, *n_active = nullptr, *kdev = nullptr;
@@ -270,6 +272,14 @@ std::vector<float> gemm_weights(int kind, const float* Wt, const std::vector<int
             const int b = kk / f_n, f = kk % f_n;
             B[(((size_t)(a * nch + ch)) * ncols + n) * KC + k] = Wt[(((size_t)n * f_n + f) * 2 + a) * 2 + b];
           }
+  } else if (kind == 6) {  // im2col'd 3x3 head: W [o][c][3][3], k = c*9 + a*3 + b < 9c, K = 32
+    const int o_n = shp[0], c_n = shp[1];
+    ncols = o_n;
+    ktap = 32;
+    ntaps = 1;
+    B.assign((size_t)ncols * KC, 0.f);
+    for (int n = 0; n < ncols; ++n)
+      for (int k = 0; k < 9 * c_n && k < 32; ++k) B[(size_t)n * KC + k] = Wt[(size_t)n * c_n * 9 + k];
   } else {  // 3: down adjoint, 4: up fwd -- 1x1 on the coarse grid, cols = (a, b, fine channel)
     // downT: Wd [co][ci][2][2], input coarse g (co), cols (a,b,ci): Wd[k][ci][a][b]
     // up   : Wu [ci][co][2][2], input coarse x (ci), cols (a,b,co): Wu[k][co][a][b]
@@ -370,6 +380,12 @@ ConvGeom make_geom(int kind, int N, int Hin, int Win, int cin_tensor, int ncols,
     g.ntaps = 2;
     for (int t = 0; t < 2; ++t) { g.dh[t] = 0; g.dw[t] = 0; g.dp[t] = t; }
     g.OHo = Hin / 2; g.OWo = Win / 2; g.osh = 1; g.osw = 1; g.OCp = ncols; g.CB = ncols;
+  } else if (kind == 6) {  // plain 1x1 on the im2col buffer
+    g.inC = cin_tensor; g.inW = Win; g.inP = 1; g.inH = Hin;
+    g.OH = Hin; g.OW = Win;
+    g.ntaps = 1;
+    g.dh[0] = 0; g.dw[0] = 0; g.dp[0] = 0;
+    g.OHo = Hin; g.OWo = Win; g.osh = 1; g.osw = 1; g.OCp = ncols; g.CB = ncols;
   } else {  // coarse input -> fine output (scatter)
     g.inC = cin_tensor; g.inW = Win; g.inP = 1; g.inH = Hin;
     g.OH = Hin; g.OW = Win;
@@ -387,43 +403,31 @@ int act_epi(ideq_ctx* ctx, int epi) {
   return epi;
 }
 
-ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, int Hin, int Win, const void* in,
-                     void* out, const void* aux, int epi, const std::string& lname) {
+// Core of every implicit-GEMM layer: `Wt` is the conv tensor of shape `shp` in the blob layout
+// of its kind (kind 6 = the im2col'd head, shape [w][C][3][3]); `key` names the uploaded
+// GEMM operand so each (conv, direction) is re-arranged and uploaded once.
+ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, const std::vector<int>& shp, int kind,
+                       int N, int Hin, int Win, const void* in, void* out, const void* aux, int epi,
+                       const std::string& lname, Layer** out_layer = nullptr) {
   Layer L;
   L.kind = L_GEMM;
   L.name = lname;
-  const std::string key = wname + "#" + std::to_string(kind) + (use_tc(ctx) ? "tc" : "simt");
   int ncols = 0, ntaps = 0, ktap = 0;
-  // weights are uploaded once per (conv, direction)
-  WeightSlices ws;
-  size_t tot;
-  slice_weights(ctx->net, ws, tot);
-  auto& sl = ws.t[wname];
-  const float* Wt = ctx->blob.data() + sl.first;
-  // channel count of the READ tensor
-  int cin_tensor;
-  {
-    std::vector<float> dummy;
-    int nc, nt, kt;
-    (void)dummy;
-    // shape-derived quantities (without building B)
-    if (kind == 0) { nc = sl.second[0]; kt = sl.second[1]; }
-    else if (kind == 1) { nc = sl.second[1]; kt = sl.second[0]; }
-    else if (kind == 2 || kind == 5) { nc = sl.second[0]; kt = 2 * sl.second[1]; }
-    else { nc = 4 * sl.second[1]; kt = sl.second[0]; }
-    (void)nt;
-    ncols = nc;
-    ktap = kt;
-    cin_tensor = (kind == 2 || kind == 5) ? kt / 2 : kt;
-  }
+  // shape-derived quantities; cin_tensor = channel count of the READ tensor
+  if (kind == 0) { ncols = shp[0]; ktap = shp[1]; }
+  else if (kind == 1) { ncols = shp[1]; ktap = shp[0]; }
+  else if (kind == 2 || kind == 5) { ncols = shp[0]; ktap = 2 * shp[1]; }
+  else if (kind == 6) { ncols = shp[0]; ktap = 32; }
+  else { ncols = 4 * shp[1]; ktap = shp[0]; }
+  const int cin_tensor = (kind == 2 || kind == 5) ? ktap / 2 : ktap;
   L.tc = use_tc(ctx);
-  const int KC = pick_kc(L.tc, ktap);
+  const int KC = kind == 6 ? 32 : pick_kc(L.tc, ktap);
   if (!ctx->wdev.count(key)) {
-    std::vector<float> B = gemm_weights(kind, Wt, sl.second, KC, ncols, ntaps, ktap);
+    std::vector<float> B = gemm_weights(kind, Wt, shp, KC, ncols, ntaps, ktap);
     ideq_status st = upload_gemm_weights(ctx, key, B);
     if (st) return st;
   }
-  L.g = make_geom(kind, N, Hin, Win, cin_tensor, ncols, KC, ktap, act_epi(ctx, epi));
+  L.g = make_geom(kind, N, Hin, Win, cin_tensor, ncols, KC, ktap, epi == EPI_IMG ? EPI_IMG : act_epi(ctx, epi));
   L.in = in;
   L.wB = ctx->wdev[key];
   L.out = out;
@@ -442,6 +446,86 @@ ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, i
     if (!L.plan) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
   }
   ctx->prog.push_back(L);
+  if (out_layer) *out_layer = &ctx->prog.back();
+  return IDEQ_OK;
+}
+
+ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, int Hin, int Win, const void* in,
+                     void* out, const void* aux, int epi, const std::string& lname) {
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  auto& sl = ws.t[wname];
+  const std::string key = wname + "#" + std::to_string(kind) + (use_tc(ctx) ? "tc" : "simt");
+  return add_gemm_w(ctx, key, ctx->blob.data() + sl.first, sl.second, kind, N, Hin, Win, in, out, aux, epi, lname);
+}
+
+// Tensor-core head/tail (bf16 U-Net). Image -> features (head, tail adjoint): im2col of the
+// C-channel fp32 image into K = 32 bf16 columns, then a 1x1 tcgen05 GEMM (kind 6).
+// Features -> image (tail, head adjoint): a 3x3 tcgen05 conv with the C output columns padded
+// to 32 (zero weights) and the EPI_IMG epilogue writing fp32 NCHW planes (+ alpha * aux).
+ideq_status add_tc_img2feat(ideq_ctx* ctx, const std::string& wname, bool adjoint, int N, const float* in_img,
+                            void* out_feat, const std::string& lname) {
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  auto& sl = ws.t[wname];
+  const float* Wt = ctx->blob.data() + sl.first;
+  const int o_n = sl.second[0], i_n = sl.second[1];
+  std::vector<float> w;                 // [w0][C][3][3]
+  if (adjoint) w = flip_transpose3x3(Wt, o_n, i_n);   // tail [C][w0] -> [w0][C]
+  else w.assign(Wt, Wt + (size_t)o_n * i_n * 9);
+  const int wo = adjoint ? i_n : o_n, ci = adjoint ? o_n : i_n;
+  Layer I;
+  I.kind = L_IM2COL;
+  I.name = lname + ".im2col";
+  I.in_img = in_img;
+  I.out = ctx->im2col;
+  I.N = N; I.C = ctx->C; I.H = ctx->H; I.W = ctx->W;
+  I.bytes = (double)N * ctx->H * ctx->W * (4.0 * ctx->C + 64.0);
+  ctx->prog.push_back(I);
+  Layer* L = nullptr;
+  ideq_status st = add_gemm_w(ctx, wname + (adjoint ? "#i2cT" : "#i2c"), w.data(), {wo, ci, 3, 3}, 6, N, ctx->H,
+                              ctx->W, ctx->im2col, out_feat, nullptr, EPI_STORE, lname, &L);
+  if (st) return st;
+  L->headtail = true;
+  return IDEQ_OK;
+}
+
+ideq_status add_tc_feat2img(ideq_ctx* ctx, const std::string& wname, bool adjoint, int N, const void* in_feat,
+                            float* out_img, const float* aux_img, float alpha, const std::string& lname) {
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  auto& sl = ws.t[wname];
+  const float* Wt = ctx->blob.data() + sl.first;
+  const int o_n = sl.second[0], i_n = sl.second[1];
+  std::vector<float> wp;
+  std::vector<int> shp;
+  int kind;
+  if (!adjoint) {  // tail [C][w0][3][3] -> [32][w0][3][3], rows >= C zero
+    wp.assign((size_t)32 * i_n * 9, 0.f);
+    std::copy(Wt, Wt + (size_t)o_n * i_n * 9, wp.begin());
+    shp = {32, i_n, 3, 3};
+    kind = 0;
+  } else {         // head [w0][C][3][3] -> [w0][32][3][3], columns >= C zero; kind 1 = adjoint
+    wp.assign((size_t)o_n * 32 * 9, 0.f);
+    for (int o = 0; o < o_n; ++o)
+      for (int i = 0; i < i_n; ++i)
+        for (int t = 0; t < 9; ++t) wp[((size_t)o * 32 + i) * 9 + t] = Wt[((size_t)o * i_n + i) * 9 + t];
+    shp = {o_n, 32, 3, 3};
+    kind = 1;
+  }
+  Layer* L = nullptr;
+  ideq_status st = add_gemm_w(ctx, wname + (adjoint ? "#imgT" : "#img"), wp.data(), shp, kind, N, ctx->H, ctx->W,
+                              in_feat, nullptr, nullptr, EPI_IMG, lname, &L);
+  if (st) return st;
+  L->headtail = true;
+  L->out_img = out_img;
+  L->aux_img = aux_img;
+  L->alpha = alpha;
+  L->flops = 2.0 * N * ctx->H * ctx->W * 9.0 * ctx->C * (adjoint ? o_n : i_n);
+  tc_plan_set_image(L->plan, out_img, aux_img, alpha, ctx->C);
   return IDEQ_OK;
 }
 
@@ -524,10 +608,15 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
     int Hl[4], Wl[4];
     for (int l = 0; l < 4; ++l) { Hl[l] = ctx->H >> l; Wl[l] = ctx->W >> l; }
     auto B = [&](int l, int i) { return ctx->lvl_buf[l][i]; };
+    const bool tc = use_tc(ctx);
+    const float* skip_aux_z = n.identity_skip ? nullptr : ctx->Z;
+    const float* skip_aux_c = n.identity_skip ? nullptr : ctx->Hc;
+    const float skip_alpha = n.identity_skip ? 0.f : -1.f;
     // ---- forward
-    if ((st = add_headtail(ctx, L_IMG2FEAT, "head", false, N, ctx->Z, nullptr, B(0, 0), nullptr, nullptr, nullptr,
-                           0.f, EPI_STORE, "head")))
-      return st;
+    st = tc ? add_tc_img2feat(ctx, "head", false, N, ctx->Z, B(0, 0), "head")
+            : add_headtail(ctx, L_IMG2FEAT, "head", false, N, ctx->Z, nullptr, B(0, 0), nullptr, nullptr, nullptr, 0.f,
+                           EPI_STORE, "head");
+    if (st) return st;
     int cur[4] = {0, 0, 0, 0};
     int skip_idx[3] = {0, 0, 0};
     for (int l = 0; l < 4; ++l) {
@@ -568,14 +657,16 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
         cur[l] = o2;
       }
     }
-    if ((st = add_headtail(ctx, L_FEAT2IMG, "tail", false, N, nullptr, B(0, cur[0]), nullptr, ctx->Hc, nullptr,
-                           n.identity_skip ? nullptr : ctx->Z, n.identity_skip ? 0.f : -1.f, EPI_STORE, "tail")))
-      return st;
+    st = tc ? add_tc_feat2img(ctx, "tail", false, N, B(0, cur[0]), ctx->Hc, skip_aux_z, skip_alpha, "tail")
+            : add_headtail(ctx, L_FEAT2IMG, "tail", false, N, nullptr, B(0, cur[0]), nullptr, ctx->Hc, nullptr,
+                           skip_aux_z, skip_alpha, EPI_STORE, "tail");
+    if (st) return st;
     ctx->n_fwd = (int)ctx->prog.size();
     // ---- VJP, cotangent Hc
-    if ((st = add_headtail(ctx, L_IMG2FEAT, "tail", true, N, ctx->Hc, nullptr, B(0, 0), nullptr, nullptr, nullptr,
-                           0.f, EPI_STORE, "tailT")))
-      return st;
+    st = tc ? add_tc_img2feat(ctx, "tail", true, N, ctx->Hc, B(0, 0), "tailT")
+            : add_headtail(ctx, L_IMG2FEAT, "tail", true, N, ctx->Hc, nullptr, B(0, 0), nullptr, nullptr, nullptr, 0.f,
+                           EPI_STORE, "tailT");
+    if (st) return st;
     int g[4] = {0, 0, 0, 0};
     int gs[3] = {0, 0, 0};
     auto rb_vjp = [&](const char* p, int l, int r) -> ideq_status {
@@ -612,9 +703,10 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
       for (int r = R - 1; r >= 0; --r)
         if ((st = rb_vjp("e", l, r))) return st;
     }
-    if ((st = add_headtail(ctx, L_FEAT2IMG, "head", true, N, nullptr, B(0, g[0]), nullptr, ctx->G, nullptr,
-                           n.identity_skip ? nullptr : ctx->Hc, n.identity_skip ? 0.f : -1.f, EPI_STORE, "headT")))
-      return st;
+    st = tc ? add_tc_feat2img(ctx, "head", true, N, B(0, g[0]), ctx->G, skip_aux_c, skip_alpha, "headT")
+            : add_headtail(ctx, L_FEAT2IMG, "head", true, N, nullptr, B(0, g[0]), nullptr, ctx->G, nullptr, skip_aux_c,
+                           skip_alpha, EPI_STORE, "headT");
+    if (st) return st;
   }
   ctx->prog_batch = N;
   ctx->graph_key.clear();
@@ -666,9 +758,12 @@ void collect_profile(ideq_ctx* ctx) {
 void run_layer(ideq_ctx* ctx, const Layer& L) {
   cudaStream_t s = ctx->stream;
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
-  if (L.kind == L_GEMM) {
+  if (L.kind == L_IM2COL) {
+    Prof p(ctx, IDEQ_K_HEADTAIL, 0, L.bytes);
+    launch_im2col32(L.in_img, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, s);
+  } else if (L.kind == L_GEMM) {
     if (L.tc) {
-      Prof p(ctx, IDEQ_K_CONV_TC, L.flops, L.bytes);
+      Prof p(ctx, L.headtail ? IDEQ_K_HEADTAIL : IDEQ_K_CONV_TC, L.flops, L.bytes);
       tc_launch(L.plan, s);
     } else {
       Prof p(ctx, IDEQ_K_CONV_SIMT, L.flops, L.bytes);
@@ -820,7 +915,7 @@ ideq_status enqueue_iteration(ideq_ctx* ctx, const StepArgs& a, const FinalizeAr
     Prof p(ctx, IDEQ_K_REDUCE);
     launch_finalize(f, ctx->stream);
     launch_advance_a(f, ctx->stream);
-    if (with_allreduce && ctx->world > 1) {
+    if (with_allreduce && ctx->comm) {
       int r = g_nccl.AllReduce(ctx->rmax, ctx->rmax, 1, NCCL_FLOAT32, NCCL_MAX, ctx->comm, ctx->stream);
       if (r != 0) return fail(ctx, IDEQ_E_NCCL, "ncclAllReduce failed: %s", g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?");
     }
@@ -898,7 +993,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
       if (ctx->gexec_plain) { cudaGraphExecDestroy(ctx->gexec_plain); ctx->gexec_plain = nullptr; }
       if (ctx->gexec_check) { cudaGraphExecDestroy(ctx->gexec_check); ctx->gexec_check = nullptr; }
       for (int v = 0; v < 2; ++v) {
-        if (v == 1 && !(global && ctx->world > 1)) break;
+        if (v == 1 && !(global && ctx->comm)) break;
         cudaGraph_t graph;
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         ideq_status st2 = enqueue_iteration(ctx, a, f, v == 1);
@@ -913,7 +1008,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
       ctx->graph_key = keybuf;
     }
     for (int k = 0; k < p->max_iter; ++k) {
-      const bool chk = global && ctx->world > 1 && ((k + 1) % p->check_every == 0);
+      const bool chk = global && ctx->comm && ((k + 1) % p->check_every == 0);
       CK(cudaGraphLaunch(chk ? ctx->gexec_check : ctx->gexec_plain, s));
       if (poll && ((k + 1) % poll_every == 0) && k + 1 < p->max_iter) {
         CK(cudaMemcpyAsync(ctx->h_pinned, ctx->n_active, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1081,6 +1176,7 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   if ((st = dalloc(ctx, &p, (bytes)))) { *out = holder.release(); return st; } \
   ctx->field = (decltype(ctx->field))p;
   AL(X1, plane) AL(Z, plane) AL(G, plane) AL(Hc, plane) AL(fbuf, plane) AL(fbuf2, plane)
+  if (prec == IDEQ_PREC_BF16 && net->arch == IDEQ_NET_UNET4) { AL(im2col, (size_t)N * H * W * 32 * 2) }
   ctx->parts_cap = 1024;
   AL(partials, (size_t)N * ctx->parts_cap * 3 * sizeof(float))
   AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int))
@@ -1091,7 +1187,7 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   cudaMemset(ctx->trace, 0xff, ctx->trace_cap * sizeof(float));
 
   // ---- distribution
-  if (dist && dist->world > 1) {
+  if (dist && dist->world >= 1) {
     std::string err;
     if (!g_nccl.load(err)) { *out = holder.release(); return fail(*out, IDEQ_E_NCCL, "%s", err.c_str()); }
     nccl_uid id;

@@ -151,7 +151,7 @@ class Solver:
         nd.weights = _fptr(self._w)
         nd.n_weights = self._w.size
         dist = None
-        if world > 1:
+        if nccl_id is not None:  # NCCL communicator (also for world == 1: single-rank all-reduce)
             dist = Dist()
             dist.rank, dist.world = rank, world
             C.memmove(dist.nccl_id, nccl_id, 128)

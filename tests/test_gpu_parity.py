@@ -159,6 +159,32 @@ def test_divergence_freezes_image():
     assert np.isfinite(xd[0].cpu().numpy()).all()
 
 
+def test_global_max_rule_with_nccl_single_rank():
+    """GLOBAL_MAX (BASELINE C5): the check-iteration graph with the NCCL MAX all-reduce (a
+    world-1 communicator on this one-GPU box) stops on the oracle's iteration and gives the
+    same iterates as the run without a communicator, bit for bit."""
+    torch = torch_cuda()
+    from paper_2605_19705_b200 import ideq
+    cfg = _mini("C5", check_every=3, tol=5e-3, max_iter=60)
+    prob = synth.make_problem(cfg)
+    orc = osolver.solve_config(cfg, prob)
+    outs = []
+    for use_nccl in (False, True):
+        nid = ideq.nccl_unique_id() if use_nccl else None
+        s = ideq.Solver(cfg, prob["weights"], precision="fp32", max_batch=2, rank=0, world=1, nccl_id=nid)
+        s.set_operator(prob)
+        xd = _dev(torch, prob["x0"])
+        st, code, _ = s.solve(_dev(torch, prob["y"]), xd, s.params())
+        outs.append((st, xd.cpu().numpy()))
+        s.close()
+    assert np.array_equal(outs[0][1], outs[1][1])
+    for st, x in outs:
+        assert (st["iters"] == orc["iters"]).all() and (st["status"] == orc["status"]).all()
+        assert orc["status"][0] == 0 and orc["iters"][0] % 3 == 0
+        for b in range(2):
+            assert rel_l2(x[b], orc["x"][b]) <= 1e-4
+
+
 def test_solve_host_matches_device():
     torch = torch_cuda()
     cfg = _mini("C3")
