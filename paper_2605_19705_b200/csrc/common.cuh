@@ -38,6 +38,20 @@ enum Epi : int {
   EPI_IMG = 4,       // tcgen05 only: columns [0, C) -> fp32 NCHW image planes, + alpha * aux image
 };
 
+// ---------------------------------------------------------------- division by a runtime constant
+// q = n / d for 0 <= n < 2^31 with one IMAD.HI + add + shift (no I2F/MUFU.RCP/F2I on the XU
+// pipe, which the per-tile index math of the persistent conv kernels otherwise saturates).
+struct FastDiv {
+  uint32_t d, m, s;
+  __host__ void init(uint32_t div) {
+    d = div < 1 ? 1 : div;
+    s = 0;
+    while ((1u << s) < d) ++s;
+    m = (uint32_t)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 // ---------------------------------------------------------------- implicit-GEMM geometry
 // The input tensor is viewed as a 5-D NHWC array (C', W', P, H', N): element
 // (c, w, p, h, n) sits at ((((n*H' + h)*P + p)*W' + w)*C' + c).

@@ -42,6 +42,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_n(uint32_t bar, uint32_t n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(n) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -147,7 +150,19 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 // bf16-mode epilogue transcendentals (outputs are rounded to bf16, rel. 2^-9): softplus via the
 // SFU exp/log; sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a
 // to avoid the cancellation of 1 - exp(-a).
-__device__ __forceinline__ float softplus_fast(float t) { return fmaxf(t, 0.f) + __logf(1.f + __expf(-fabsf(t))); }
+// log1p(u) on u in [0, 1] by a degree-6 Chebyshev-interpolated polynomial (|err| < 1.5e-6, far
+// below the bf16 rounding of the output), so softplus costs one MUFU.EX2 instead of EX2 + LG2.
+__device__ __forceinline__ float softplus_fast(float t) {
+  const float u = __expf(-fabsf(t));
+  float p = -0.01741407752407103f;
+  p = fmaf(p, u, 0.08269123711081523f);
+  p = fmaf(p, u, -0.19035433673230703f);
+  p = fmaf(p, u, 0.3157473167575014f);
+  p = fmaf(p, u, -0.4973732161578083f);
+  p = fmaf(p, u, 0.9998476974962173f);
+  p = fmaf(p, u, 1.4720650115540579e-06f);
+  return fmaxf(t, 0.f) + p;
+}
 __device__ __forceinline__ float dsoftplus_from_act_fast(float a) {
   return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - __expf(-a);
 }
@@ -171,6 +186,15 @@ __device__ __forceinline__ void bulk_wait_read_lt(int n) {
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// the two epilogue warps of one TMEM lane quadrant (immediate ids keep ptxas from reserving all 16)
+__device__ __forceinline__ void pair_bar(int quad) {
+  switch (quad) {
+    case 0: asm volatile("bar.sync 2, 64;" ::: "memory"); break;
+    case 1: asm volatile("bar.sync 3, 64;" ::: "memory"); break;
+    case 2: asm volatile("bar.sync 4, 64;" ::: "memory"); break;
+    default: asm volatile("bar.sync 5, 64;" ::: "memory"); break;
+  }
+}
 
 // ------------------------------------------------------------------ kernel
 struct TcParams {
@@ -187,7 +211,23 @@ struct TcParams {
   const float* img_aux;
   float img_alpha;
   int img_c;
+  FastDiv fd_ntiles, fd_perimg, fd_tw;  // tile index -> (m tile, n tile), (image, row tile, col tile)
+  int slab_mode;                        // 1: each TMEM lane quadrant stores its own 32-row slab
 };
+
+// tile t -> (image, output row h0, output col w0, n tile)
+struct TileIdx { int img, h0, w0, nt; };
+__device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t) {
+  TileIdx r;
+  const int mt = (int)P.fd_ntiles.div((uint32_t)t);
+  r.nt = t - mt * P.n_tiles;
+  r.img = (int)P.fd_perimg.div((uint32_t)mt);
+  const int rem = mt - r.img * (P.g.tiles_h * P.g.tiles_w);
+  const int th = (int)P.fd_tw.div((uint32_t)rem);
+  r.h0 = th * P.g.R;
+  r.w0 = (rem - th * P.g.tiles_w) * P.g.Wt;
+  return r;
+}
 
 constexpr int TC_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
 
@@ -217,7 +257,7 @@ template <int KC, int EPI, int BOXC, bool HALO>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmAux,
-                   const __grid_constant__ TcParams P) {
+                   const __grid_constant__ CUtensorMap tmSlab, const __grid_constant__ TcParams P) {
   constexpr bool HAS_AUX = (EPI == EPI_RESADD || EPI == EPI_SIGMUL);
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -253,12 +293,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       mbar_init(tfull0 + 8u * a, 1);
       mbar_init(tempty0 + 8u * a, 8);
       mbar_init(auxfull0 + 8u * a, 1);
-      mbar_init(epifree0 + 8u * a, 1);
+      mbar_init(epifree0 + 8u * a, 4);  // one arrival per TMEM lane quadrant
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
     prefetch_tmap(&tmOut);
+    prefetch_tmap(&tmSlab);
     if (HAS_AUX) prefetch_tmap(&tmAux);
   }
   if (warp == 1) {
@@ -273,7 +314,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const uint32_t tmem_base = *tmem_holder;
 
   const int total = P.m_tiles * P.n_tiles;
-  const int per_img = g.tiles_h * g.tiles_w;
   const int nbox = BN / BOXC;
 
   if (warp == 0) {
@@ -287,9 +327,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
       }
       for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const int mt = t / P.n_tiles, nt = t % P.n_tiles;
-        const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
-        const int h0 = th * g.R, w0 = tw * g.Wt;
+        const TileIdx ti = tile_index(P, t);
+        const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
         // the aux tile goes into this tile's epilogue buffer; it is requested after the first
         // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
         const int nload = HALO ? g.nchunk : nkb;
@@ -381,18 +420,28 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     __syncwarp();
   } else {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
-    // thread; the two warps of a quadrant split the tile's columns in halves
+    // thread; the two warps of a quadrant split the tile's columns in halves. Each quadrant
+    // publishes its own 32-row slab (pair barrier of 64 threads + one TMA store per column box),
+    // so no warp waits for the whole tile or for a store to drain: the slab's leader releases
+    // the epilogue buffer of the PREVIOUS tile once that tile's stores have been read.
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
-    const bool leader = (warp == 2 && lane == 0);
+    const bool qleader = (half == 0 && lane == 0);
+    const uint32_t rowbytes = (uint32_t)BOXC * 2u;
     const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
-    int acc = 0, ltile = 0;
+    const bool slab_live = quad * 32 < g.R * g.Wt;
+    // slab mode: 4 storers (one per quadrant); whole-tile mode (Wt neither a multiple nor a divisor
+    // of 32, e.g. ragged test shapes): warp 2 stores the tile after an 8-warp barrier
+    const bool storer = P.slab_mode ? qleader : (qleader && quad == 2);
+    const uint32_t arrivals = P.slab_mode ? 1u : 4u;
+    // slab origin inside the tile (pixel rows of the M tile are row-major R x Wt)
+    const int sh = (quad * 32) / g.Wt, sw = (quad * 32) % g.Wt;
+    int acc = 0, prev_acc = -1;
     uint32_t aph = 0;
     for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const int mt = t / P.n_tiles, nt = t % P.n_tiles;
-      const int img = mt / per_img, th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
-      const int h0 = th * g.R, w0 = tw * g.Wt;
+      const TileIdx ti = tile_index(P, t);
+      const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
         mbar_wait(auxfull0 + 8u * acc, aph);
@@ -422,8 +471,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-        epi_bar();
-        if (leader) mbar_arrive(epifree0 + 8u * acc);
+        if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals, nothing stored through smem
         if (++acc == NA) { acc = 0; aph ^= 1u; }
         continue;
       }
@@ -466,25 +514,40 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-      // publish the tile: generic-proxy smem writes -> async proxy, then one TMA store per box
+      // publish this quadrant's slab: generic-proxy smem writes -> async proxy, pair barrier,
+      // then one TMA store per column box of the slab
       fence_async_smem();
-      epi_bar();
-      if (leader) {
-        for (int b = 0; b < nbox; ++b) {
-          const int col = nt * BN + b * BOXC;
-          tma_store_5d(&tmOut, ebuf + b * P.epi_box_bytes, col % g.CB, w0, col / g.CB, h0, img);
+      if (P.slab_mode) pair_bar(quad);
+      else epi_bar();
+      if (storer) {
+        if (P.slab_mode) {
+          if (slab_live) {
+            for (int b = 0; b < nbox; ++b) {
+              const int col = nt * BN + b * BOXC;
+              tma_store_5d(&tmSlab, ebuf + b * P.epi_box_bytes + (uint32_t)(quad * 32) * rowbytes, col % g.CB,
+                           w0 + sw, col / g.CB, h0 + sh, img);
+            }
+          }
+        } else {
+          for (int b = 0; b < nbox; ++b) {
+            const int col = nt * BN + b * BOXC;
+            tma_store_5d(&tmOut, ebuf + b * P.epi_box_bytes, col % g.CB, w0, col / g.CB, h0, img);
+          }
         }
         bulk_commit();
-        // release the buffer as soon as the TMA engine has read it: the next use is NA-1 tiles
-        // away, so the aux prefetch into it gets the most slack (measured faster than keeping
-        // store groups in flight, which delays every release by a tile)
-        bulk_wait_read0();
-        mbar_arrive(epifree0 + 8u * acc);
+        // release the previous tile's buffer once its stores have been read
+        if (prev_acc >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive_n(epifree0 + 8u * prev_acc, arrivals);
+        }
+        prev_acc = acc;
       }
-      ++ltile;
       if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-    if (leader) bulk_wait0();
+    if (storer) {
+      bulk_wait0();
+      if (prev_acc >= 0) mbar_arrive_n(epifree0 + 8u * prev_acc, arrivals);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -513,7 +576,7 @@ static EncodeTiledFn get_encode() {
 }
 
 struct TcPlan {
-  CUtensorMap tmA, tmB, tmOut, tmAux;
+  CUtensorMap tmA, tmB, tmOut, tmAux, tmSlab;
   TcParams P;
   int KC, epi, boxc, grid, halo;
   size_t smem;
@@ -604,11 +667,26 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   } else {
     p->tmAux = p->tmOut;
   }
+  // 32-row epilogue slab (one TMEM lane quadrant): Wt >= 32 -> 32 pixels of one row; Wt < 32 ->
+  // 32 / Wt whole rows. Used when Wt is a multiple or a divisor of 32.
+  const int slab_mode = (g.Wt % 32 == 0 || 32 % g.Wt == 0) ? 1 : 0;
+  if (slab_mode) {
+    const int sw = g.Wt >= 32 ? 32 : g.Wt, sh = g.Wt >= 32 ? 1 : 32 / g.Wt;
+    r = encode5(enc, &p->tmSlab, g.epi == EPI_IMG ? (const void*)in : (const void*)out, g.CB, g.OWo, g.osh,
+                g.OHo / g.osh, g.N, boxc, sw, sh, swE);
+    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map slab encode failed (%d)", (int)r); delete p; return nullptr; }
+  } else {
+    p->tmSlab = p->tmOut;
+  }
   TcParams& P = p->P;
   P.g = g;
   P.BN = BN;
   P.n_tiles = g.ncols / BN;
   P.m_tiles = g.N * g.tiles_h * g.tiles_w;
+  P.slab_mode = slab_mode;
+  P.fd_ntiles.init((uint32_t)P.n_tiles);
+  P.fd_perimg.init((uint32_t)(g.tiles_h * g.tiles_w));
+  P.fd_tw.init((uint32_t)g.tiles_w);
   P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
   P.b_bytes = (uint32_t)g.KC * 2u * BN;
   P.epi_box_bytes = 128u * boxc * 2u;
@@ -651,9 +729,11 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
 template <int KC, int EPI, int BOXC>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
   if (p->halo)
-    conv_tc_kernel<KC, EPI, BOXC, true><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
+    conv_tc_kernel<KC, EPI, BOXC, true><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                           p->tmSlab, p->P);
   else
-    conv_tc_kernel<KC, EPI, BOXC, false><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux, p->P);
+    conv_tc_kernel<KC, EPI, BOXC, false><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                            p->tmSlab, p->P);
 }
 
 template <int KC, int BOXC>

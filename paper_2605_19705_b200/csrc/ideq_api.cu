@@ -1177,7 +1177,13 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   ctx->field = (decltype(ctx->field))p;
   AL(X1, plane) AL(Z, plane) AL(G, plane) AL(Hc, plane) AL(fbuf, plane) AL(fbuf2, plane)
   if (prec == IDEQ_PREC_BF16 && net->arch == IDEQ_NET_UNET4) { AL(im2col, (size_t)N * H * W * 32 * 2) }
-  ctx->parts_cap = 1024;
+  {  // residual partials per image: the largest count any fidelity/step kernel can produce at this size
+    int pc = 256;
+    const int cand[3] = {blur_parts_per_image(ctx->C, H, W), fft_parts_per_image(ctx->C, H, W),
+                         phase_parts_per_image(H, W)};
+    for (int v : cand) pc = v > pc ? v : pc;
+    ctx->parts_cap = pc;
+  }
   AL(partials, (size_t)N * ctx->parts_cap * 3 * sizeof(float))
   AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int))
   AL(res, N * sizeof(float)) AL(r_now, N * sizeof(float)) AL(rmax, 16) AL(n_active, 16) AL(kdev, 16)
