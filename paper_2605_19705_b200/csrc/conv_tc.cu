@@ -114,6 +114,34 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// elect.sync picks the same (lowest active) lane every time, so the MMAs and the commit that
+// tracks them are issued by one thread while the loop around them stays warp-uniform.
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "selp.u32 %0, 1, 0, e;\n\t}\n"
+      : "=r"(pred));
+  return pred != 0;
+}
+__device__ __forceinline__ void mma_bf16_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -203,7 +231,8 @@ struct TcParams {
   uint32_t a_bytes, b_bytes, tmem_cols;
   uint32_t epi_box_bytes;  // one epilogue box: 128 rows x BOXC columns (bf16)
   uint32_t epi_tx_bytes;   // TMA bytes of one aux tile (R*Wt rows x BN columns)
-  uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x 3 x KC halo buffer (1 KB aligned)
+  uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x (R+2) x KC halo buffer (1 KB aligned)
+  int stagesB;             // MODE 2: depth of the weight ring
   int nacc;                // TMEM accumulator stages (2..4)
   // EPI_IMG: the first img_c GEMM columns are an image (tail / head adjoint); written as fp32
   // NCHW planes [N][img_c][OH][OW] plus img_alpha * img_aux (same layout, may be null)
@@ -249,11 +278,15 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
-// HALO = true (3x3 convs on one-row tiles, single N tile): one TMA box of (Wt+2) x 3 input
-// pixels per channel chunk feeds all 9 taps through row-shifted UMMA descriptors, and the
-// layer's weights stay resident in shared memory for the persistent CTA's lifetime, so the
-// input crosses L2 ~3x instead of 9x and the weights once per CTA instead of once per tile.
-template <int KC, int EPI, int BOXC, bool HALO>
+// MODE (3x3 convs): 0 = plain implicit GEMM, one TMA box of the shifted input per (tap, chunk).
+// 1 and 2 = HALO: one TMA box of (Wt+2) x (R+2) input pixels per channel chunk feeds all 9 taps
+// through shifted UMMA descriptors. The M = 128 rows of a tile are either one image row of 128
+// pixels (R = 1) or 16 rows x 8 pixels (Wt = 8), the two shapes whose 8-row core groups sit at a
+// uniform stride inside the halo box (8 or 10 pixel rows = the descriptor's SBO), so the input
+// crosses L2 ~1.4x (2D) / ~3x (1-row) instead of 9x. MODE 1 keeps the layer's weights resident
+// in shared memory for the CTA's lifetime; MODE 2 streams them per (chunk, tap) through a second
+// ring (layers whose weights do not fit).
+template <int KC, int EPI, int BOXC, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmAux,
@@ -269,26 +302,31 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
   const ConvGeom& g = P.g;
   const int nkb = g.ntaps * g.nchunk;
-  // non-HALO: [A stages][B stages][epi x2]; HALO: [resident W (nkb B boxes)][halo stages][epi x2]
+  constexpr bool HALO = MODE != 0;
+  const int SB = MODE == 2 ? P.stagesB : 0;
+  // MODE 0: [A stages][B stages][epi]; MODE 1: [resident W (nkb B boxes)][halo stages][epi];
+  // MODE 2: [halo stages][B ring][epi]
   const uint32_t sW = base;
-  const uint32_t sA = HALO ? sW + (uint32_t)nkb * b_stage : base;
+  const uint32_t sA = MODE == 1 ? sW + (uint32_t)nkb * b_stage : base;
   const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
-  const uint32_t sE = HALO ? sB : sB + S * b_stage;
+  const uint32_t sE = MODE == 1 ? sB : sB + (MODE == 2 ? SB : S) * b_stage;
   const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
   const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
-  // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1);
+  // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB], emptyB[SB]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1 + 2 * SB);
   const uint32_t full0 = sBar, empty0 = sBar + 8u * S;
   const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 8u * NA, auxfull0 = tempty0 + 8u * NA,
                  epifree0 = auxfull0 + 8u * NA;
   const uint32_t wfull = epifree0 + 8u * NA;
+  const uint32_t fullB0 = wfull + 8u, emptyB0 = fullB0 + 8u * SB;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
+    for (int s = 0; s < SB; ++s) { mbar_init(fullB0 + 8u * s, 1); mbar_init(emptyB0 + 8u * s, 1); }
     for (int a = 0; a < NA; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
       mbar_init(tempty0 + 8u * a, 8);
@@ -317,39 +355,53 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int nbox = BN / BOXC;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      if (HALO) {  // resident weights: every K-block of the (single) N tile, once per CTA
+    // ---------------- TMA producer: the whole warp walks the loop (warp-uniform state stays in
+    // uniform registers); one elected lane arms the barriers and issues the copies
+    int s = 0, sb = 0;
+    uint32_t ph = 0, phb = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    if (MODE == 1) {  // resident weights: every K-block of the (single) N tile, once per CTA
+      if (elect_one()) {
         mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
         for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
       }
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileIdx ti = tile_index(P, t);
-        const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
-        // the aux tile goes into this tile's epilogue buffer; it is requested after the first
-        // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
-        const int nload = HALO ? g.nchunk : nkb;
-        const int kb_aux = (S < nload ? S : nload) - 1;
-        for (int kb = 0; kb < nload; ++kb) {
+      __syncwarp();
+    }
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      const TileIdx ti = tile_index(P, t);
+      const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
+      // the aux tile goes into this tile's epilogue buffer; it is requested after the first
+      // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
+      const int nload = HALO ? g.nchunk : nkb;
+      const int kb_aux = (S < nload ? S : nload) - 1;
+      for (int kb = 0; kb < nload; ++kb) {
+        mbar_wait(empty0 + 8u * s, ph ^ 1u);
+        if (elect_one()) {
           if (HALO) {
-            mbar_wait(empty0 + 8u * s, ph ^ 1u);
             mbar_expect_tx(full0 + 8u * s, P.a_bytes);
             tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
-            if (++s == S) { s = 0; ph ^= 1u; }
+            if (MODE == 2) {  // this chunk's 9 weight boxes through the B ring
+              for (int tap = 0; tap < 9; ++tap) {
+                mbar_wait(emptyB0 + 8u * sb, phb ^ 1u);
+                mbar_expect_tx(fullB0 + 8u * sb, P.b_bytes);
+                tma_load_3d(sB + sb * b_stage, &tmB, fullB0 + 8u * sb, 0, nt * BN, tap * g.nchunk + kb);
+                if (++sb == SB) { sb = 0; phb ^= 1u; }
+              }
+            }
           } else {
-          const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
-          mbar_wait(empty0 + 8u * s, ph ^ 1u);
-          mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
-          tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * KC, w0 + g.dw[tap], g.dp[tap], h0 + g.dh[tap],
-                      img);
-          tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * BN, kb);
-          if (++s == S) { s = 0; ph ^= 1u; }
+            const int tap = kb / g.nchunk, chunk = kb - tap * g.nchunk;
+            mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
+            tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * KC, w0 + g.dw[tap], g.dp[tap],
+                        h0 + g.dh[tap], img);
+            tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * BN, kb);
           }
-          if (HAS_AUX && kb == kb_aux) {
-            mbar_wait(epifree0 + 8u * acc, aph ^ 1u);  // previous store from this buffer has drained
+        }
+        __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1u; }
+        if (HAS_AUX && kb == kb_aux) {
+          mbar_wait(epifree0 + 8u * acc, aph ^ 1u);  // previous store from this buffer has drained
+          if (elect_one()) {
             mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
             for (int b = 0; b < nbox; ++b) {
               const int col = nt * BN + b * BOXC;
@@ -357,67 +409,74 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                           col / g.CB, h0, img);
             }
           }
+          __syncwarp();
         }
-        if (++acc == NA) { acc = 0; aph ^= 1u; }
       }
+      if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-    __syncwarp();
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc_bf16(BN);
-      constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
-      constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
-      int s = 0;
-      uint32_t ph = 0;
-      int acc = 0;
-      uint32_t aph = 0;
-      if (HALO) mbar_wait(wfull, 0);
-      const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
-      for (int t = blockIdx.x; t < total; t += gridDim.x) {
-        mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-        if (HALO) {
-          for (int ch = 0; ch < g.nchunk; ++ch) {
-            mbar_wait(full0 + 8u * s, ph);
-            tc_fence_after();
-            const uint32_t halo = sA + s * P.halo_stage;
-            for (int tap = 0; tap < 9; ++tap) {
-              const uint32_t p0 = (uint32_t)((g.dh[tap] + 1) * (g.Wt + 2) + (g.dw[tap] + 1));
-              const uint32_t a_addr = halo + p0 * hrow;
-              const uint32_t b_addr = sW + (uint32_t)(tap * g.nchunk + ch) * b_stage;
-#pragma unroll
-              for (int k = 0; k < KC / 16; ++k) {
-                const uint64_t ad = make_sdesc(a_addr + 32u * k, sbo, layout);
-                const uint64_t bd = make_sdesc(b_addr + 32u * k, sbo, layout);
-                mma_bf16(d_tmem, ad, bd, idesc, (ch | tap | k) ? 1u : 0u);
-              }
+    // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform descriptors
+    // (64-bit adds of byte offsets >> 4); one elected lane issues tcgen05.mma / commit. A
+    // single-thread issue loop measured ~110 clk per MMA on B200 (tools/umma_bench.cu) against
+    // a tensor floor of 16-128 clk; the uniform form reaches the floor for N >= 128.
+    const uint32_t idesc = make_idesc_bf16(BN);
+    constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
+    constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
+    // halo tiles: 8-row core groups of A are 8 pixels of one row (R = 1) or one 8-pixel row of a
+    // 16 x 8 tile, i.e. (Wt + 2) pixel rows apart inside the halo box
+    const uint32_t sboA = HALO ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
+    const uint64_t dA0 = make_sdesc(sA, sboA, layout);
+    const uint64_t dB0 = make_sdesc(MODE == 1 ? sW : sB, sbo, layout);
+    int s = 0, sb = 0;
+    uint32_t ph = 0, phb = 0;
+    int acc = 0;
+    uint32_t aph = 0;
+    if (MODE == 1) mbar_wait(wfull, 0);
+    const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
+    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+      mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      if (HALO) {
+        for (int ch = 0; ch < g.nchunk; ++ch) {
+          mbar_wait(full0 + 8u * s, ph);
+          tc_fence_after();
+          const uint64_t dh = dA0 + ((s * P.halo_stage) >> 4);
+          for (int tap = 0; tap < 9; ++tap) {
+            const uint32_t p0 = (uint32_t)((g.dh[tap] + 1) * (g.Wt + 2) + (g.dw[tap] + 1));
+            const uint64_t ad = dh + ((p0 * hrow) >> 4);
+            uint64_t bd;
+            if (MODE == 2) {
+              mbar_wait(fullB0 + 8u * sb, phb);
+              tc_fence_after();
+              bd = dB0 + (((uint32_t)sb * b_stage) >> 4);
+            } else {
+              bd = dB0 + (((uint32_t)(tap * g.nchunk + ch) * b_stage) >> 4);
             }
-            mma_commit(empty0 + 8u * s);
-            if (++s == S) { s = 0; ph ^= 1u; }
+#pragma unroll
+            for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
+            if (MODE == 2) {
+              mma_commit_elect(emptyB0 + 8u * sb);
+              if (++sb == SB) { sb = 0; phb ^= 1u; }
+            }
           }
-          mma_commit(tfull0 + 8u * acc);
-          if (++acc == NA) { acc = 0; aph ^= 1u; }
-          continue;
+          mma_commit_elect(empty0 + 8u * s);
+          if (++s == S) { s = 0; ph ^= 1u; }
         }
+      } else {
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(full0 + 8u * s, ph);
           tc_fence_after();
-          const uint32_t a_addr = sA + s * a_stage, b_addr = sB + s * b_stage;
+          const uint64_t ad = dA0 + ((s * a_stage) >> 4), bd = dB0 + ((s * b_stage) >> 4);
 #pragma unroll
-          for (int k = 0; k < KC / 16; ++k) {
-            const uint64_t ad = make_sdesc(a_addr + 32u * k, sbo, layout);
-            const uint64_t bd = make_sdesc(b_addr + 32u * k, sbo, layout);
-            mma_bf16(d_tmem, ad, bd, idesc, (kb | k) ? 1u : 0u);
-          }
-          mma_commit(empty0 + 8u * s);
+          for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) ? 1u : 0u);
+          mma_commit_elect(empty0 + 8u * s);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
-        mma_commit(tfull0 + 8u * acc);
-        if (++acc == NA) { acc = 0; aph ^= 1u; }
       }
+      mma_commit_elect(tfull0 + 8u * acc);
+      if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-    __syncwarp();
   } else {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
     // thread; the two warps of a quadrant split the tile's columns in halves. Each quadrant
@@ -597,16 +656,22 @@ bool tc_supported(const ConvGeom& g) {
   return true;
 }
 
-// Halo variant: 3x3 taps (|dh|,|dw| <= 1, no parity planes), one-row tiles that fill the M=128
-// MMA, a single N tile, and resident weights that fit next to two halo buffers.
-static bool tc_halo_ok(const ConvGeom& g) {
-  if (g.ntaps != 9 || g.R != 1 || g.Wt != 128 || g.inP != 1) return false;
+// Halo variants: 3x3 taps (|dh|,|dw| <= 1, no parity planes) on tiles whose 8-row core groups
+// sit at a uniform stride inside the halo box: 16 x 8 pixels (preferred: 1.4x halo) or one row of
+// 128 pixels. Returns 0 (plain), 1 (resident weights) or 2 (streamed weights) and the tile shape.
+static int tc_halo_mode(const ConvGeom& g, int& R, int& Wt) {
+  if (g.ntaps != 9 || g.inP != 1) return 0;
   for (int t = 0; t < 9; ++t)
-    if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return false;
+    if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return 0;
+  const char* nh = getenv("IDEQ_NO_HALO");  // A/B switches for measurements
+  if (nh && atoi(nh) != 0) return 0;
+  const char* n2 = getenv("IDEQ_NO_HALO2D");
+  if (g.OW % 8 == 0 && !(n2 && atoi(n2) != 0)) { R = 16; Wt = 8; }
+  else if (g.R == 1 && g.Wt == 128) { R = 1; Wt = 128; }
+  else return 0;
   const int BN = tc_bn(g);
-  if (g.ncols != BN) return false;
   const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * 2;
-  return wbytes <= 80 * 1024;
+  return (g.ncols == BN && wbytes <= 80 * 1024) ? 1 : 2;
 }
 
 // 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
@@ -624,9 +689,10 @@ static CUresult encode5(EncodeTiledFn enc, CUtensorMap* m, const void* ptr, int 
              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
+TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
                      const __nv_bfloat16* aux, int num_sms, char* err, size_t errlen) {
-  if (!tc_supported(g)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
+  if (!tc_supported(g_in)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
+  ConvGeom g = g_in;
   EncodeTiledFn enc = get_encode();
   if (!enc) { snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable"); return nullptr; }
   const bool has_aux = g.epi == EPI_RESADD || g.epi == EPI_SIGMUL;
@@ -640,8 +706,14 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   p->boxc = boxc;
   const CUtensorMapSwizzle swA = g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   const CUtensorMapSwizzle swE = boxc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  const char* nh = getenv("IDEQ_NO_HALO");  // A/B switch for measurements
-  p->halo = (tc_halo_ok(g) && !(nh && atoi(nh) != 0)) ? 1 : 0;
+  int hR = g.R, hW = g.Wt;
+  p->halo = tc_halo_mode(g, hR, hW);
+  if (p->halo) {  // halo tiles may re-shape the M tile (16 x 8 pixels)
+    g.R = hR;
+    g.Wt = hW;
+    g.tiles_h = (g.OH + g.R - 1) / g.R;
+    g.tiles_w = (g.OW + g.Wt - 1) / g.Wt;
+  }
   CUresult r = p->halo ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
                        : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
@@ -694,11 +766,15 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   // Shared-memory / TMEM plan. Preference order: 4 accumulator stages for narrow N (more tiles
   // in flight hide the per-tile epilogue latency), then 2 CTAs per SM, then deeper operand rings.
   const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
-  const size_t wbytes = p->halo ? (size_t)9 * g.nchunk * b_stage : 0;
+  const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * b_stage : 0;
   if (p->halo) {
     P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
     P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
   }
+  // MODE 2: a weight ring of SB stages (one (chunk, tap) box each) next to the halo ring
+  const int SBq = 6;
+  const size_t bring = p->halo == 2 ? (size_t)SBq * b_stage : 0;
+  P.stagesB = p->halo == 2 ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
   const int min_stages = p->halo ? 2 : 3, max_stages = p->halo ? 4 : 8;
   int stages = 0, ctas = 1, nacc = 0;
@@ -706,7 +782,7 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   for (int na = (BN <= 64 ? 4 : 2); na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * BN) tc <<= 1;
-    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + 512;
+    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
     for (int c = 2; c >= 1 && !stages; --c) {
       const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
@@ -719,7 +795,7 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
   P.stages = stages;
   P.nacc = nacc;
   P.tmem_cols = tcols;
-  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + 512 + (size_t)stages * op_stage;
+  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + 512 + (size_t)stages * op_stage;
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -728,12 +804,15 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
 
 template <int KC, int EPI, int BOXC>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
-  if (p->halo)
-    conv_tc_kernel<KC, EPI, BOXC, true><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                           p->tmSlab, p->P);
+  if (p->halo == 1)
+    conv_tc_kernel<KC, EPI, BOXC, 1><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                        p->tmSlab, p->P);
+  else if (p->halo == 2)
+    conv_tc_kernel<KC, EPI, BOXC, 2><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                        p->tmSlab, p->P);
   else
-    conv_tc_kernel<KC, EPI, BOXC, false><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                            p->tmSlab, p->P);
+    conv_tc_kernel<KC, EPI, BOXC, 0><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                        p->tmSlab, p->P);
 }
 
 template <int KC, int BOXC>
@@ -766,7 +845,7 @@ int tc_plan_is_halo(const TcPlan* p) { return p->halo; }
 
 void tc_free_plan(TcPlan* p) { delete p; }
 
-template <int KC, int BOXC, bool HALO>
+template <int KC, int BOXC, int HALO>
 static void attrs_epi() {
   set_max_dyn_smem(conv_tc_kernel<KC, EPI_STORE, BOXC, HALO>);
   set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC, HALO>);
@@ -776,14 +855,18 @@ static void attrs_epi() {
 }
 
 void init_attrs_tc() {
-  attrs_epi<64, 64, false>();
-  attrs_epi<64, 32, false>();
-  attrs_epi<32, 64, false>();
-  attrs_epi<32, 32, false>();
-  attrs_epi<64, 64, true>();
-  attrs_epi<64, 32, true>();
-  attrs_epi<32, 64, true>();
-  attrs_epi<32, 32, true>();
+  attrs_epi<64, 64, 0>();
+  attrs_epi<64, 32, 0>();
+  attrs_epi<32, 64, 0>();
+  attrs_epi<32, 32, 0>();
+  attrs_epi<64, 64, 1>();
+  attrs_epi<64, 32, 1>();
+  attrs_epi<32, 64, 1>();
+  attrs_epi<32, 32, 1>();
+  attrs_epi<64, 64, 2>();
+  attrs_epi<64, 32, 2>();
+  attrs_epi<32, 64, 2>();
+  attrs_epi<32, 32, 2>();
 }
 
 }  // namespace ideq

@@ -21,7 +21,7 @@ __device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
 }
 
-__global__ void __launch_bounds__(128, 1) umma_rate(int n, int iters, int shift_rows, int kc64, long long* out) {
+__global__ void __launch_bounds__(128, 1) umma_rate(int n, int iters, int shift_rows, int kc64, int mode, long long* out) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tmem_holder;
   __shared__ __align__(8) uint64_t bar;
@@ -42,7 +42,43 @@ __global__ void __launch_bounds__(128, 1) umma_rate(int n, int iters, int shift_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_holder;
-  if (threadIdx.x == 0) {
+  if (mode == 1 && warp == 0) {
+    // whole warp runs the loop (warp-uniform descriptor math in uniform registers); one elected
+    // lane issues; descriptors advance by adding (bytes >> 4) to the 64-bit value
+    const uint32_t layout = kc64 ? 2u : 4u, sbo = kc64 ? 1024u : 512u, rowb = kc64 ? 128u : 64u;
+    const uint32_t a0 = base + (uint32_t)shift_rows * rowb;
+    const uint32_t b0 = base + 40 * 1024;
+    const uint64_t ad0 = make_sdesc(a0, sbo, layout), bd0 = make_sdesc(b0, sbo, layout);
+    const uint32_t idesc = make_idesc_bf16(n);
+    const int ksteps = kc64 ? 4 : 2;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (k < ksteps) {
+          asm volatile(
+              "{\n\t.reg .pred p, e;\n\t"
+              "elect.sync _|e, 0xffffffff;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem),
+              "l"(ad0 + 2ull * k), "l"(bd0 + 2ull * k), "r"(idesc), "r"(1)
+              : "memory");
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar))
+                   : "memory");
+      asm volatile(
+          "{\n\t.reg .pred p;\nW1:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W1;\n}\n" ::"r"(
+              smem_u32(&bar))
+          : "memory");
+      long long t1 = clock64();
+      out[blockIdx.x] = t1 - t0;
+    }
+    __syncwarp();
+  }
+  if (mode == 0 && threadIdx.x == 0) {
     const uint32_t layout = kc64 ? 2u : 4u, sbo = kc64 ? 1024u : 512u, rowb = kc64 ? 128u : 64u;
     const uint32_t a0 = base + (uint32_t)shift_rows * rowb;  // A: 128 rows (+ shift) x KC
     const uint32_t b0 = base + 40 * 1024;                    // B: n rows x KC
@@ -82,11 +118,12 @@ int main() {
   const int iters = 2048;
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int mode = 0; mode <= 1; ++mode)
   for (int kc64 = 0; kc64 <= 1; ++kc64)
-    for (int shift = 0; shift <= 1; ++shift)
+    for (int shift = 0; shift <= (mode ? 0 : 1); ++shift)
       for (int n : {32, 64, 96, 128, 192, 256}) {
-        for (int g : {1, sms}) {
-          umma_rate<<<g, 128, 100 * 1024>>>(n, iters, shift, kc64, d);
+        for (int g : {sms}) {
+          umma_rate<<<g, 128, 100 * 1024>>>(n, iters, shift, kc64, mode, d);
           cudaError_t e = cudaDeviceSynchronize();
           if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
           long long h[1024];
@@ -94,7 +131,7 @@ int main() {
           long long mx = 0;
           for (int i = 0; i < g; ++i) mx = h[i] > mx ? h[i] : mx;
           const double mmas = (double)iters * (kc64 ? 4 : 2);
-          printf("KC=%d shift=%d N=%3d grid=%3d : %.1f clk/MMA (floor %.1f) -> %.0f%% of floor rate\n", kc64 ? 64 : 32,
+          printf("mode=%d KC=%d shift=%d N=%3d grid=%3d : %.1f clk/MMA (floor %.1f) -> %.0f%% of floor rate\n", mode, kc64 ? 64 : 32,
                  shift, n, g, mx / mmas, 128.0 * n / 256.0, 100.0 * (128.0 * n / 256.0) / (mx / mmas));
         }
       }
