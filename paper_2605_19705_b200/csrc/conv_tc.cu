@@ -321,7 +321,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const uint32_t wfull = epifree0 + 8u * NA;
   const uint32_t fullB0 = wfull + 8u, emptyB0 = fullB0 + 8u * SB;
 
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // warp index broadcast from lane 0 so the compiler knows it is warp-uniform (uniform datapath)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
@@ -349,7 +350,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem_base = *tmem_holder;
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // uniform, not a per-thread load
 
   const int total = P.m_tiles * P.n_tiles;
   const int nbox = BN / BOXC;
@@ -617,6 +618,177 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   }
 }
 
+// ------------------------------------------------------------------ fused head (image -> features)
+// out[n,h,w,co] = sum_k B[co][k] * patch[n,h,w,k], patch k = c*9 + a*3 + b (c < C <= 3, zero for
+// k >= 9C): the C -> NC 3x3 head conv (and the tail adjoint) as ONE kernel. Each thread builds its
+// pixel's K = 32 im2col row straight into the swizzled (SW64) shared A tile -- the 134 MB im2col
+// tensor of the two-kernel form never touches HBM -- then one elected lane issues two
+// M128 x NC x K16 tcgen05.mma into a TMEM accumulator that the same thread reads back with
+// tcgen05.ld (thread = pixel = TMEM lane) and stores as 16-byte bf16 chunks (a warp writes 32
+// consecutive pixels = one contiguous run). A and the accumulator are double-buffered.
+template <int NC>
+__global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restrict__ in,
+                                                          const __nv_bfloat16* __restrict__ wB,
+                                                          __nv_bfloat16* __restrict__ out, int N, int C, int H,
+                                                          int W, const FastDiv fdHW, const FastDiv fdW) {
+  __shared__ __align__(1024) unsigned char sAraw[2][128 * 64];
+  __shared__ __align__(1024) unsigned char sBraw[NC * 64];
+  extern __shared__ __align__(1024) unsigned char sOdyn[];  // output staging [2][128 * NC * 2] (bulk-copied)
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ uint32_t tmem_holder;
+  const int tid = threadIdx.x;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const uint32_t sA0 = smem_u32(sAraw[0]), sA1 = smem_u32(sAraw[1]), sB = smem_u32(sBraw);
+  // weights [NC][32] bf16 -> swizzled K-major B tile (64-byte rows, 16-byte chunk j at j ^ ((r >> 1) & 3))
+  for (int i = tid; i < NC * 4; i += 128) {
+    const int r = i >> 2, j = i & 3;
+    const uint4 v = *reinterpret_cast<const uint4*>(wB + r * 32 + j * 8);
+    st_shared_v4(sB + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4), v);
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(&bar[0]), 1);
+    mbar_init(smem_u32(&bar[1]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
+                 "r"((uint32_t)(2 * NC))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  fence_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = __shfl_sync(0xffffffffu, tmem_holder, 0);
+  const long long HW = (long long)H * W, total = (long long)N * HW;
+  const long long tiles = (total + 127) / 128;
+  const uint32_t idesc = make_idesc_bf16(NC);
+  const uint64_t dB = make_sdesc(sB, 512u, 4u);
+  constexpr uint32_t ROWB = NC * 2;  // output bytes per pixel
+  // 32-bit pixel indexing (N*H*W < 2^31 for every supported size) with multiply-shift division
+  // the patch of the NEXT tile is loaded into registers before this tile's MMA/epilogue, so the
+  // global-load latency overlaps the tensor-core round trip and the staging of the output
+  float pv[27];
+  auto load_patch = [&](long long tt) {
+    const long long px = tt * 128 + tid;
+#pragma unroll
+    for (int k = 0; k < 27; ++k) pv[k] = 0.f;
+    if (px < total) {
+      const uint32_t p32 = (uint32_t)px;
+      const uint32_t n = fdHW.div(p32), rem = p32 - n * (uint32_t)HW;
+      const uint32_t h = fdW.div(rem), w = rem - h * (uint32_t)W;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (c < C) {
+          const float* plane = in + ((long long)n * C + c) * HW;
+#pragma unroll
+          for (int a = 0; a < 3; ++a)
+#pragma unroll
+            for (int b = 0; b < 3; ++b) {
+              const int hh = (int)h + a - 1, ww = (int)w + b - 1;
+              if (hh >= 0 && hh < H && ww >= 0 && ww < W) pv[c * 9 + a * 3 + b] = __ldg(plane + hh * W + ww);
+            }
+        }
+      }
+    }
+  };
+  int it = 0;
+  long long t_prev = -1;
+  if (blockIdx.x < tiles) load_patch(blockIdx.x);
+  for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    const int buf = it & 1;
+    const uint32_t sA = buf ? sA1 : sA0;
+    float v[32];
+#pragma unroll
+    for (int k = 0; k < 27; ++k) v[k] = pv[k];
+#pragma unroll
+    for (int k = 27; k < 32; ++k) v[k] = 0.f;
+    if (t + gridDim.x < tiles) load_patch(t + gridDim.x);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 wv;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&wv);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[j * 8 + 2 * e], v[j * 8 + 2 * e + 1]);
+      st_shared_v4(sA + (uint32_t)tid * 64u + (uint32_t)((j ^ ((tid >> 1) & 3)) << 4), wv);
+    }
+    fence_async_smem();  // A tile (and the previous tile's output staging) -> async proxy
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (tid == 0) {
+      if (t_prev >= 0) {  // the previous tile's staged output: one bulk copy
+        const long long np = total - t_prev * 128 < 128 ? total - t_prev * 128 : 128;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t_prev * 128 * NC),
+                     "r"(smem_u32(sOdyn + (buf ^ 1) * 128 * NC * 2)), "r"((uint32_t)(np * ROWB))
+                     : "memory");
+        bulk_commit();
+      }
+      // the staging buffer this tile writes was bulk-copied one tile ago: wait until it was read
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    }
+    const uint32_t d_tmem = tmem_base + (uint32_t)(buf * NC);
+    if (warp == 0) {
+      const uint64_t dA = make_sdesc(sA, 512u, 4u);
+      mma_bf16_elect(d_tmem, dA, dB, idesc, 0u);
+      mma_bf16_elect(d_tmem, dA + 2u, dB + 2u, idesc, 1u);
+      mma_commit_elect(smem_u32(&bar[buf]));
+    }
+    mbar_wait(smem_u32(&bar[buf]), (uint32_t)((it >> 1) & 1));
+    __syncthreads();  // thread 0 has waited for the staging buffer's previous bulk copy
+    tc_fence_after();
+    const uint32_t so = smem_u32(sOdyn + buf * 128 * NC * 2) + (uint32_t)tid * ROWB;
+#pragma unroll
+    for (int c0 = 0; c0 < NC; c0 += 16) {
+      float r[16];
+      tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * NC + c0), r);
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        uint4 wv;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&wv);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(r[q * 8 + 2 * e], r[q * 8 + 2 * e + 1]);
+        st_shared_v4(so + (uint32_t)(c0 + q * 8) * 2u, wv);
+      }
+    }
+    tc_fence_before();
+    t_prev = t;
+  }
+  fence_async_smem();
+  __syncthreads();
+  if (tid == 0) {
+    if (t_prev >= 0) {
+      const long long np = total - t_prev * 128 < 128 ? total - t_prev * 128 : 128;
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t_prev * 128 * NC),
+                   "r"(smem_u32(sOdyn + ((it - 1) & 1) * 128 * NC * 2)), "r"((uint32_t)(np * ROWB))
+                   : "memory");
+      bulk_commit();
+    }
+    bulk_wait0();
+  }
+  tc_fence_after();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * NC))
+                 : "memory");
+}
+
+void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, int N, int C, int H, int W,
+                        int NC, int num_sms, cudaStream_t s) {
+  // the static shared memory (54 KB / 36 KB) caps residency so that the CTAs' TMEM allocations
+  // (2 x NC columns each) never exceed the SM's 512 columns
+  const int per_sm = NC == 64 ? 4 : 6;   // static smem admits at most 4 (NC 64) / 6 (NC 32) CTAs per SM
+  const size_t pad = (size_t)2 * 128 * NC * 2;  // output staging
+  const long long tiles = ((long long)N * H * W + 127) / 128;
+  const long long cap = (long long)num_sms * per_sm;
+  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+  FastDiv fdHW, fdW;
+  fdHW.init((uint32_t)(H * W));
+  fdW.init((uint32_t)W);
+  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW);
+  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW);
+}
+
 // ------------------------------------------------------------------ host side
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -855,6 +1027,8 @@ static void attrs_epi() {
 }
 
 void init_attrs_tc() {
+  set_max_dyn_smem(img2feat_tc_kernel<32>);
+  set_max_dyn_smem(img2feat_tc_kernel<64>);
   attrs_epi<64, 64, 0>();
   attrs_epi<64, 32, 0>();
   attrs_epi<32, 64, 0>();

@@ -53,7 +53,7 @@ NcclApi g_nccl;
 constexpr int NCCL_FLOAT32 = 7, NCCL_MAX = 2;
 
 // ------------------------------------------------------------------ program description
-enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IM2COL = 3 };
+enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IM2COL = 3, L_IMG2FEAT_TC = 4 };
 
 struct Layer {
   LayerKind kind;
@@ -460,8 +460,8 @@ ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, i
   return add_gemm_w(ctx, key, ctx->blob.data() + sl.first, sl.second, kind, N, Hin, Win, in, out, aux, epi, lname);
 }
 
-// Tensor-core head/tail (bf16 U-Net). Image -> features (head, tail adjoint): im2col of the
-// C-channel fp32 image into K = 32 bf16 columns, then a 1x1 tcgen05 GEMM (kind 6).
+// Tensor-core head/tail (bf16 U-Net). Image -> features (head, tail adjoint): one fused kernel
+// builds the K = 32 im2col row of each pixel in shared memory and runs a 1x1 tcgen05 GEMM.
 // Features -> image (tail, head adjoint): a 3x3 tcgen05 conv with the C output columns padded
 // to 32 (zero weights) and the EPI_IMG epilogue writing fp32 NCHW planes (+ alpha * aux).
 ideq_status add_tc_img2feat(ideq_ctx* ctx, const std::string& wname, bool adjoint, int N, const float* in_img,
@@ -476,19 +476,27 @@ ideq_status add_tc_img2feat(ideq_ctx* ctx, const std::string& wname, bool adjoin
   if (adjoint) w = flip_transpose3x3(Wt, o_n, i_n);   // tail [C][w0] -> [w0][C]
   else w.assign(Wt, Wt + (size_t)o_n * i_n * 9);
   const int wo = adjoint ? i_n : o_n, ci = adjoint ? o_n : i_n;
-  Layer I;
-  I.kind = L_IM2COL;
-  I.name = lname + ".im2col";
-  I.in_img = in_img;
-  I.out = ctx->im2col;
-  I.N = N; I.C = ctx->C; I.H = ctx->H; I.W = ctx->W;
-  I.bytes = (double)N * ctx->H * ctx->W * (4.0 * ctx->C + 64.0);
-  ctx->prog.push_back(I);
-  Layer* L = nullptr;
-  ideq_status st = add_gemm_w(ctx, wname + (adjoint ? "#i2cT" : "#i2c"), w.data(), {wo, ci, 3, 3}, 6, N, ctx->H,
-                              ctx->W, ctx->im2col, out_feat, nullptr, EPI_STORE, lname, &L);
-  if (st) return st;
-  L->headtail = true;
+  // fused im2col + 1x1 tcgen05 GEMM (one kernel); the weights are the K = 32 GEMM operand
+  const std::string key = wname + (adjoint ? "#i2cT" : "#i2c") + "tc";
+  if (!ctx->wdev.count(key)) {
+    int ncols = 0, ntaps = 0, ktap = 0;
+    std::vector<float> B = gemm_weights(6, w.data(), {wo, ci, 3, 3}, 32, ncols, ntaps, ktap);
+    ideq_status st = upload_gemm_weights(ctx, key, B);
+    if (st) return st;
+  }
+  if (wo != 32 && wo != 64) return fail(ctx, IDEQ_E_UNSUPPORTED, "head width %d: fused head needs 32 or 64", wo);
+  Layer L;
+  L.kind = L_IMG2FEAT_TC;
+  L.name = lname;
+  L.in_img = in_img;
+  L.wB = ctx->wdev[key];
+  L.out = out_feat;
+  L.N = N; L.C = ctx->C; L.H = ctx->H; L.W = ctx->W;
+  L.wfeat = wo;
+  L.headtail = true;
+  L.flops = 2.0 * N * ctx->H * ctx->W * 9.0 * ci * wo;
+  L.bytes = (double)N * ctx->H * ctx->W * (4.0 * ctx->C + 2.0 * wo);
+  ctx->prog.push_back(L);
   return IDEQ_OK;
 }
 
@@ -758,7 +766,11 @@ void collect_profile(ideq_ctx* ctx) {
 void run_layer(ideq_ctx* ctx, const Layer& L) {
   cudaStream_t s = ctx->stream;
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
-  if (L.kind == L_IM2COL) {
+  if (L.kind == L_IMG2FEAT_TC) {
+    Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
+    launch_img2feat_tc(L.in_img, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, L.wfeat,
+                       ctx->num_sms, s);
+  } else if (L.kind == L_IM2COL) {
     Prof p(ctx, IDEQ_K_HEADTAIL, 0, L.bytes);
     launch_im2col32(L.in_img, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, s);
   } else if (L.kind == L_GEMM) {
@@ -1176,7 +1188,6 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   if ((st = dalloc(ctx, &p, (bytes)))) { *out = holder.release(); return st; } \
   ctx->field = (decltype(ctx->field))p;
   AL(X1, plane) AL(Z, plane) AL(G, plane) AL(Hc, plane) AL(fbuf, plane) AL(fbuf2, plane)
-  if (prec == IDEQ_PREC_BF16 && net->arch == IDEQ_NET_UNET4) { AL(im2col, (size_t)N * H * W * 32 * 2) }
   {  // residual partials per image: the largest count any fidelity/step kernel can produce at this size
     int pc = 256;
     const int cand[3] = {blur_parts_per_image(ctx->C, H, W), fft_parts_per_image(ctx->C, H, W),

@@ -9,7 +9,7 @@ hdr = None; data = []
 for r in rows:
     if r and r[0] == 'ID': hdr = r; continue
     if hdr and len(r) == len(hdr): data.append(dict(zip(hdr, r)))
-start = next(i for i,d in enumerate(data) if 'im2col' in d['Kernel Name']) + 1
+start = next(i for i,d in enumerate(data) if 'img2feat' in d['Kernel Name'])
 tot = 0; out = []
 for n, d in zip(names, data[start:start+len(names)]):
     v = float(d['Metric Value']) / 1e3; tot += v
