@@ -948,10 +948,15 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   const size_t bring = p->halo == 2 ? (size_t)SBq * b_stage : 0;
   P.stagesB = p->halo == 2 ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
-  const int min_stages = p->halo ? 2 : 3, max_stages = p->halo ? 4 : 8;
+  // short-K layers (the 2x2 up / down scatters: 1-2 K-blocks per tile) are bound by the per-tile
+  // epilogue round trip (aux load, store), so they take 4 accumulator/epilogue stages and only the
+  // operand stages one tile needs
+  const int nkb_tile = p->halo ? g.nchunk : g.ntaps * g.nchunk;
+  const bool short_k = !p->halo && nkb_tile <= 2;
+  const int min_stages = p->halo ? 2 : (short_k ? 2 : 3), max_stages = p->halo ? 4 : (short_k ? 4 : 8);
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
-  for (int na = (BN <= 64 ? 4 : 2); na >= 2 && !stages; na -= 2) {
+  for (int na = (BN <= 64 || short_k ? 4 : 2); na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * BN) tc <<= 1;
     const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
