@@ -142,6 +142,65 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
       : "memory");
 }
+// ---- CTA pair (cta_group::2): cluster rank, peer addresses, remote arrivals, 2-SM MMA/commit/TMA
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t out;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
+  return out;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
+      "%4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive on the barrier at this shared-memory offset in BOTH CTAs of the pair once the MMAs complete
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  const uint16_t mask = 3;
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
+          bar),
+      "h"(mask)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
@@ -246,10 +305,11 @@ struct TcParams {
 
 // tile t -> (image, output row h0, output col w0, n tile)
 struct TileIdx { int img, h0, w0, nt; };
-__device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t) {
+__device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t, int pair_rank = -1) {
   TileIdx r;
-  const int mt = (int)P.fd_ntiles.div((uint32_t)t);
+  int mt = (int)P.fd_ntiles.div((uint32_t)t);
   r.nt = t - mt * P.n_tiles;
+  if (pair_rank >= 0) mt = 2 * mt + pair_rank;  // CTA pair: unit -> this CTA's M tile
   r.img = (int)P.fd_perimg.div((uint32_t)mt);
   const int rem = mt - r.img * (P.g.tiles_h * P.g.tiles_w);
   const int th = (int)P.fd_tw.div((uint32_t)rem);
@@ -298,18 +358,24 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int S = P.stages;
   const int BN = P.BN;
   const uint32_t a_stage = 128u * KC * 2u;
-  const uint32_t b_stage = (uint32_t)BN * KC * 2u;
+  // MODE 3 = MODE 2 on a CTA pair (cta_group::2, M = 256): each CTA holds its own 128-row A tile
+  // and HALF of every weight box (BN / 2 rows); the leader CTA issues the M256 x BN MMAs
+  constexpr bool PAIR = MODE == 3;
+  constexpr bool STREAMB = MODE >= 2;
+  const uint32_t b_stage = (uint32_t)(PAIR ? BN / 2 : BN) * KC * 2u;
   const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
   const ConvGeom& g = P.g;
   const int nkb = g.ntaps * g.nchunk;
   constexpr bool HALO = MODE != 0;
-  const int SB = MODE == 2 ? P.stagesB : 0;
+  const int SB = STREAMB ? P.stagesB : 0;
+  const uint32_t rank = PAIR ? cluster_rank() : 0u;
+  const bool leader = rank == 0;
   // MODE 0: [A stages][B stages][epi]; MODE 1: [resident W (nkb B boxes)][halo stages][epi];
   // MODE 2: [halo stages][B ring][epi]
   const uint32_t sW = base;
   const uint32_t sA = MODE == 1 ? sW + (uint32_t)nkb * b_stage : base;
   const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
-  const uint32_t sE = MODE == 1 ? sB : sB + (MODE == 2 ? SB : S) * b_stage;
+  const uint32_t sE = MODE == 1 ? sB : sB + (STREAMB ? SB : S) * b_stage;
   const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
   const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
@@ -326,11 +392,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
+    // PAIR: the leader's tempty counts both CTAs' epilogue warps
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
     for (int s = 0; s < SB; ++s) { mbar_init(fullB0 + 8u * s, 1); mbar_init(emptyB0 + 8u * s, 1); }
     for (int a = 0; a < NA; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
-      mbar_init(tempty0 + 8u * a, 8);
+      mbar_init(tempty0 + 8u * a, PAIR ? 16 : 8);
       mbar_init(auxfull0 + 8u * a, 1);
       mbar_init(epifree0 + 8u * a, 4);  // one arrival per TMEM lane quadrant
     }
@@ -342,17 +409,32 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     if (HAS_AUX) prefetch_tmap(&tmAux);
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(P.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(P.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                   "r"(P.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // barrier inits + TMEM allocation visible to the peer
+  else __syncthreads();
   tc_fence_after();
+  // PAIR: shared::cluster addresses of the leader's barriers (operand-full rings, TMEM-empty)
+  const uint32_t full0L = PAIR ? mapa_shared(full0, 0) : full0;
+  const uint32_t fullB0L = PAIR ? mapa_shared(fullB0, 0) : fullB0;
+  const uint32_t tempty0L = PAIR ? mapa_shared(tempty0, 0) : tempty0;
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // uniform, not a per-thread load
 
-  const int total = P.m_tiles * P.n_tiles;
+  // PAIR: work units are (pair of M tiles, N tile); CTA `rank` owns M tile 2j + rank
+  const int total = PAIR ? ((P.m_tiles + 1) / 2) * P.n_tiles : P.m_tiles * P.n_tiles;
+  const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nbox = BN / BOXC;
 
   if (warp == 0) {
@@ -369,8 +451,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       }
       __syncwarp();
     }
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileIdx ti = tile_index(P, t);
+    for (int t = t0; t < total; t += tstep) {
+      const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       // the aux tile goes into this tile's epilogue buffer; it is requested after the first
       // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
@@ -379,7 +461,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       for (int kb = 0; kb < nload; ++kb) {
         mbar_wait(empty0 + 8u * s, ph ^ 1u);
         if (elect_one()) {
-          if (HALO) {
+          if (PAIR) {  // the 2-SM TMA of both CTAs signals the LEADER's full barriers; only the
+                       // leader arms them (for both CTAs' bytes): a remote arrive would need a fence
+            if (leader) mbar_expect_tx(full0 + 8u * s, 2u * P.a_bytes);
+            tma_load_5d_pair(sA + s * P.halo_stage, &tmA, full0L + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
+            for (int tap = 0; tap < 9; ++tap) {  // this CTA's half (BN / 2 rows) of each weight box
+              mbar_wait(emptyB0 + 8u * sb, phb ^ 1u);
+              if (leader) mbar_expect_tx(fullB0 + 8u * sb, 2u * P.b_bytes);
+              tma_load_3d_pair(sB + sb * b_stage, &tmB, fullB0L + 8u * sb, 0, nt * BN + (int)rank * (BN / 2),
+                               tap * g.nchunk + kb);
+              if (++sb == SB) { sb = 0; phb ^= 1u; }
+            }
+          } else if (HALO) {
             mbar_expect_tx(full0 + 8u * s, P.a_bytes);
             tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
             if (MODE == 2) {  // this chunk's 9 weight boxes through the B ring
@@ -415,12 +508,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       }
       if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && leader) {
     // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform descriptors
     // (64-bit adds of byte offsets >> 4); one elected lane issues tcgen05.mma / commit. A
     // single-thread issue loop measured ~110 clk per MMA on B200 (tools/umma_bench.cu) against
     // a tensor floor of 16-128 clk; the uniform form reaches the floor for N >= 128.
-    const uint32_t idesc = make_idesc_bf16(BN);
+    // PAIR: M = 256 (instruction descriptor bits [24,29) = M >> 4)
+    const uint32_t idesc = PAIR ? ((make_idesc_bf16(BN) & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24))
+                                : make_idesc_bf16(BN);
     constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
     constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
     // halo tiles: 8-row core groups of A are 8 pixels of one row (R = 1) or one 8-pixel row of a
@@ -434,7 +529,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t aph = 0;
     if (MODE == 1) mbar_wait(wfull, 0);
     const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
+    for (int t = t0; t < total; t += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
@@ -447,21 +542,28 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             const uint32_t p0 = (uint32_t)((g.dh[tap] + 1) * (g.Wt + 2) + (g.dw[tap] + 1));
             const uint64_t ad = dh + ((p0 * hrow) >> 4);
             uint64_t bd;
-            if (MODE == 2) {
+            if (STREAMB) {
               mbar_wait(fullB0 + 8u * sb, phb);
               tc_fence_after();
               bd = dB0 + (((uint32_t)sb * b_stage) >> 4);
             } else {
               bd = dB0 + (((uint32_t)(tap * g.nchunk + ch) * b_stage) >> 4);
             }
+            if (PAIR) {
 #pragma unroll
-            for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
-            if (MODE == 2) {
-              mma_commit_elect(emptyB0 + 8u * sb);
+              for (int k = 0; k < KC / 16; ++k) mma_bf16_pair(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
+            } else {
+#pragma unroll
+              for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
+            }
+            if (STREAMB) {
+              if (PAIR) mma_commit_pair(emptyB0 + 8u * sb);
+              else mma_commit_elect(emptyB0 + 8u * sb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
             }
           }
-          mma_commit_elect(empty0 + 8u * s);
+          if (PAIR) mma_commit_pair(empty0 + 8u * s);
+          else mma_commit_elect(empty0 + 8u * s);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       } else {
@@ -475,10 +577,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       }
-      mma_commit_elect(tfull0 + 8u * acc);
+      if (PAIR) mma_commit_pair(tfull0 + 8u * acc);
+      else mma_commit_elect(tfull0 + 8u * acc);
       if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-  } else {
+  } else if (warp >= 2) {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
     // thread; the two warps of a quadrant split the tile's columns in halves. Each quadrant
     // publishes its own 32-row slab (pair barrier of 64 threads + one TMA store per column box),
@@ -499,8 +602,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     const int sh = (quad * 32) / g.Wt, sw = (quad * 32) % g.Wt;
     int acc = 0, prev_acc = -1;
     uint32_t aph = 0;
-    for (int t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileIdx ti = tile_index(P, t);
+    for (int t = t0; t < total; t += tstep) {
+      const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
@@ -530,7 +633,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+        if (lane == 0) { if (PAIR) mbar_arrive_cluster(tempty0L + 8u * acc); else mbar_arrive(tempty0 + 8u * acc); }
         if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals, nothing stored through smem
         if (++acc == NA) { acc = 0; aph ^= 1u; }
         continue;
@@ -573,7 +676,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       // TMEM stage fully read: let the MMA warp reuse it
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+      if (lane == 0) { if (PAIR) mbar_arrive_cluster(tempty0L + 8u * acc); else mbar_arrive(tempty0 + 8u * acc); }
       // publish this quadrant's slab: generic-proxy smem writes -> async proxy, pair barrier,
       // then one TMA store per column box of the slab
       fence_async_smem();
@@ -610,11 +713,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer's MMAs into this CTA's TMEM and its remote arrivals are done
+  else __syncthreads();
   tc_fence_after();
   if (warp == 1) {
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
-                 : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
+                   : "memory");
   }
 }
 
@@ -843,7 +951,12 @@ static int tc_halo_mode(const ConvGeom& g, int& R, int& Wt) {
   else return 0;
   const int BN = tc_bn(g);
   const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * 2;
-  return (g.ncols == BN && wbytes <= 80 * 1024) ? 1 : 2;
+  if (g.ncols == BN && wbytes <= 80 * 1024) return 1;
+  // streamed weights. IDEQ_PAIR=1 runs them on CTA pairs (cta_group::2, M = 256, half of every
+  // weight box per SM): correct (tests/test_gpu_layers.py) but measured slower on B200 than the
+  // single-CTA ring (C3 level 2/3: 46-51 us vs 34-40 us per layer), so it is opt-in.
+  const char* pr = getenv("IDEQ_PAIR");
+  return (BN % 32 == 0 && pr && atoi(pr) != 0) ? 3 : 2;
 }
 
 // 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
@@ -893,7 +1006,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     const int nkb = g.ntaps * g.nchunk;
     cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
     cuuint64_t strides[2] = {(cuuint64_t)g.KC * 2, (cuuint64_t)g.KC * 2 * g.ncols};
-    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
+    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)(p->halo == 3 ? BN / 2 : BN), 1u};
     cuuint32_t es[3] = {1, 1, 1};
     r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swA, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -932,12 +1045,13 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.fd_perimg.init((uint32_t)(g.tiles_h * g.tiles_w));
   P.fd_tw.init((uint32_t)g.tiles_w);
   P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
-  P.b_bytes = (uint32_t)g.KC * 2u * BN;
+  P.b_bytes = (uint32_t)g.KC * 2u * (p->halo == 3 ? BN / 2 : BN);  // PAIR: this CTA's half
   P.epi_box_bytes = 128u * boxc * 2u;
   P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
   // Shared-memory / TMEM plan. Preference order: 4 accumulator stages for narrow N (more tiles
   // in flight hide the per-tile epilogue latency), then 2 CTAs per SM, then deeper operand rings.
-  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
+  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)(p->halo == 3 ? BN / 2 : BN) * g.KC * 2u,
+               e_stage = (size_t)BN * 128u * 2u;
   const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * b_stage : 0;
   if (p->halo) {
     P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
@@ -945,8 +1059,9 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   }
   // MODE 2: a weight ring of SB stages (one (chunk, tap) box each) next to the halo ring
   const int SBq = 6;
-  const size_t bring = p->halo == 2 ? (size_t)SBq * b_stage : 0;
-  P.stagesB = p->halo == 2 ? SBq : 0;
+  const bool streamb = p->halo >= 2;
+  const size_t bring = streamb ? (size_t)SBq * b_stage : 0;
+  P.stagesB = streamb ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
   // short-K layers (the 2x2 up / down scatters: 1-2 K-blocks per tile) are bound by the per-tile
   // epilogue round trip (aux load, store), so they take 4 accumulator/epilogue stages and only the
@@ -960,7 +1075,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     uint32_t tc = 32;
     while (tc < (uint32_t)na * BN) tc <<= 1;
     const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
-    for (int c = 2; c >= 1 && !stages; --c) {
+    for (int c = (p->halo == 3 ? 1 : 2); c >= 1 && !stages; --c) {  // a CTA pair: one CTA per SM
       const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
       int st = (int)((avail - fixed) / op_stage);
@@ -973,6 +1088,12 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.nacc = nacc;
   P.tmem_cols = tcols;
   p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + 512 + (size_t)stages * op_stage;
+  if (p->halo == 3) {  // units of (2 M tiles, 1 N tile); two CTAs (one cluster) per unit
+    const int units = ((P.m_tiles + 1) / 2) * P.n_tiles;
+    const int maxu = num_sms / 2;
+    p->grid = 2 * (units < maxu ? units : maxu);
+    return p;
+  }
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -987,6 +1108,21 @@ static void launch_one(const TcPlan* p, cudaStream_t s) {
   else if (p->halo == 2)
     conv_tc_kernel<KC, EPI, BOXC, 2><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
                                                                         p->tmSlab, p->P);
+  else if (p->halo == 3) {  // CTA pairs: cluster of 2 on one TPC
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p->grid);
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = p->smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P);
+  }
   else
     conv_tc_kernel<KC, EPI, BOXC, 0><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
                                                                         p->tmSlab, p->P);
@@ -1046,6 +1182,10 @@ void init_attrs_tc() {
   attrs_epi<64, 32, 2>();
   attrs_epi<32, 64, 2>();
   attrs_epi<32, 32, 2>();
+  attrs_epi<64, 64, 3>();
+  attrs_epi<64, 32, 3>();
+  attrs_epi<32, 64, 3>();
+  attrs_epi<32, 32, 3>();
 }
 
 }  // namespace ideq

@@ -82,3 +82,33 @@ def test_layer_vs_oracle(path, kind, cin, cout, H, W, epi):
     tol = 1e-5 if prec == "fp32" else 8e-3
     assert np.isfinite(got).all()
     assert rel_l2(got, ref) <= tol, (path, rel_l2(got, ref))
+
+
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("kind,cin,cout,N,H,W,epi", [(0, 64, 128, 3, 8, 40, 2), (1, 128, 64, 3, 8, 40, 3),
+                                                     (0, 128, 256, 1, 24, 24, 1)])
+def test_streamed_weight_layer_odd_tile_count(kind, cin, cout, N, H, W, epi, pair, monkeypatch):
+    """Streamed-weight 3x3 layers, single CTA (MODE 2) and on CTA pairs (IDEQ_PAIR=1: MODE 3,
+    cta_group::2, two M tiles per unit); an odd number of 16x8 tiles leaves the last pair's second
+    tile outside the batch (zero-filled loads, clipped stores). Checked against the oracle layer."""
+    monkeypatch.setenv("IDEQ_PAIR", "1" if pair else "0")
+    torch = torch_cuda()
+    from paper_2605_19705_b200 import ideq
+    rng = np.random.default_rng(7 + kind)
+    fn, wshape = KINDS[kind]
+    w = rng.standard_normal(wshape(cin, cout)) * np.sqrt(1.0 / (cin * 4))
+    x = rng.standard_normal((N, cin, H, W))
+    w32 = w.astype(np.float32)
+    xr, wr = bf16_round(x), bf16_round(w32)
+    ref_acc = np.stack([fn(xr[n], wr) for n in range(N)])
+    aux = auxr = None
+    if epi in (2, 3):
+        aux = rng.uniform(0.05, 2.0, ref_acc.shape) if epi == 3 else rng.standard_normal(ref_acc.shape)
+        auxr = bf16_round(aux)
+    ref = _epi_ref(ref_acc, epi, auxr)
+    out = torch.zeros((N, ref.shape[2], ref.shape[3], ref.shape[1]), device="cuda", dtype=torch.bfloat16)
+    ideq.debug_conv(kind, "bf16", True, w32, N, H, W, nhwc_dev(x, "bf16"), out,
+                    nhwc_dev(aux, "bf16") if aux is not None else None, epi)
+    got = from_nhwc_dev(out)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, ref) <= 8e-3
