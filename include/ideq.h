@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define IDEQ_ABI_VERSION 1
+#define IDEQ_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define IDEQ_API __attribute__((visibility("default")))
@@ -154,12 +154,26 @@ typedef struct {
   float tol;                 /* stop when r <= tol; tol = 0 => exactly max_iter         */
   int check_every;           /* convergence checked when (k+1) % check_every == 0      */
   ideq_stop_rule stop_rule;  /* GLOBAL_MAX: max over active images (all ranks) <= tol  */
+  /* Adaptive restart, Eq. 5 (l.119-121): after every accepted step k_r += 1 and
+   * S += ||x^{k+1} - x^k||^2; when k_r * S > B^2 the inertia is reset (the next
+   * z = x^{k+1}). restart = 0: off (the paper's inference runs without restart,
+   * l.796); 1: Alg. 1 semantics (l.225: "x^{-1}, x^0 <- x^k, k <- 0", k_r and S
+   * reset); 2: Alg. 2 semantics (l.647: "x^{k-1} <- x^k" only). restart_B >= 0. */
+  int restart;
+  float restart_B;
+  /* Averaging, Alg. 1/2 steps 12-13 (l.232-237): x-hat = mean(z^0 .. z^{K0}),
+   * K0 = argmin_{floor(K/2) < k < K-1} ||x^{k+1} - x^k|| (first minimum; K =
+   * max_iter); empty window or diverged image -> x-hat = last accepted iterate.
+   * Requires tol == 0 (fixed iteration count). 0: off (Remark 1, l.189-193). */
+  int averaging;
 } ideq_params;
 
 typedef struct {
   int iters;       /* accepted iterations; x-hat = x^{iters}                  */
   float residual;  /* last accepted r                                          */
   int status;      /* 0 converged, 1 hit max_iter, 2 diverged                  */
+  int restarts;    /* number of Eq. 5 restarts                                 */
+  int k0;          /* averaging: K0, or -1 when x-hat is the last iterate      */
 } ideq_image_stat;
 
 /* Solve with DEVICE y [batch][C|J][H][W] and DEVICE x_inout (in: x^0, out:

@@ -108,6 +108,15 @@ struct ideq_ctx {
   float *X1 = nullptr, *Z = nullptr, *G = nullptr, *Hc = nullptr, *fbuf = nullptr, *fbuf2 = nullptr;
   void* im2col = nullptr;  // [N][H][W][32] bf16 (tensor-core head), bf16 U-Net only
   float* partials = nullptr;
+  // NEXT-1 (restart / averaging) state
+  int* rk = nullptr;
+  double* rsum = nullptr;
+  int* flags = nullptr;
+  int* nrest = nullptr;
+  float* best = nullptr;
+  int* k0 = nullptr;
+  float* Zsum = nullptr;
+  float* Xsnap = nullptr;
   int parts_cap = 0;
   int *active = nullptr, *status = nullptr, *iters = nullptr, *n_active = nullptr, *kdev = nullptr;
   float *res = nullptr, *r_now = nullptr, *rmax = nullptr, *trace = nullptr;
@@ -916,6 +925,13 @@ FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
   f.active = ctx->active; f.status = ctx->status; f.iters = ctx->iters;
   f.res = ctx->res; f.r_now = ctx->r_now; f.trace = ctx->trace; f.rmax = ctx->rmax;
   f.n_active = ctx->n_active; f.kdev = ctx->kdev;
+  const bool next1 = p && (p->restart || p->averaging);
+  f.restart = p ? p->restart : 0;
+  f.B2 = p ? (double)p->restart_B * (double)p->restart_B : 0.0;
+  f.averaging = p ? p->averaging : 0;
+  f.K = p ? p->max_iter : 0;
+  f.rk = ctx->rk; f.rsum = ctx->rsum; f.nrest = ctx->nrest; f.best = ctx->best; f.k0 = ctx->k0;
+  f.flags = next1 ? ctx->flags : nullptr;  // null: the plain path pays nothing for NEXT-1
   return f;
 }
 
@@ -926,6 +942,13 @@ ideq_status enqueue_iteration(ideq_ctx* ctx, const StepArgs& a, const FinalizeAr
   {
     Prof p(ctx, IDEQ_K_REDUCE);
     launch_finalize(f, ctx->stream);
+    if (f.flags) {  // restart (z^{k+1} := x^{k+1}) and averaging bookkeeping
+      PostArgs pa{};
+      pa.N = f.N; pa.d = a.d; pa.flags = f.flags; pa.kdev = f.kdev; pa.X0 = a.X0; pa.X1 = a.X1; pa.Z = ctx->Z;
+      pa.Zsum = f.averaging ? ctx->Zsum : nullptr;
+      pa.Xsnap = ctx->Xsnap;
+      launch_post_step(pa, ctx->stream);
+    }
     launch_advance_a(f, ctx->stream);
     if (with_allreduce && ctx->comm) {
       int r = g_nccl.AllReduce(ctx->rmax, ctx->rmax, 1, NCCL_FLOAT32, NCCL_MAX, ctx->comm, ctx->stream);
@@ -950,6 +973,11 @@ ideq_status validate_params(ideq_ctx* ctx, int batch, const ideq_params* p) {
   if (!(p->tau > 0.f) || !(p->lambda >= 0.f) || !(p->beta >= 0.f && p->beta < 1.f) || p->max_iter < 1 ||
       !(p->tol >= 0.f) || p->check_every < 1 || (p->stop_rule != IDEQ_STOP_PER_IMAGE && p->stop_rule != IDEQ_STOP_GLOBAL_MAX))
     return fail(ctx, IDEQ_E_INVALID, "invalid params (tau>0, lambda>=0, 0<=beta<1, max_iter>=1, tol>=0, check_every>=1)");
+  if (p->restart < 0 || p->restart > 2 || (p->restart && !(p->restart_B >= 0.f)))
+    return fail(ctx, IDEQ_E_INVALID, "restart must be 0, 1 (Alg. 1) or 2 (Alg. 2) with restart_B >= 0");
+  if (p->averaging != 0 && p->averaging != 1) return fail(ctx, IDEQ_E_INVALID, "averaging must be 0 or 1");
+  if (p->averaging && p->tol != 0.f)
+    return fail(ctx, IDEQ_E_INVALID, "averaging (Alg. 1 steps 12-13) needs a fixed iteration count: tol = 0");
   if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "ideq_set_operator must be called before solving");
   if (batch > ctx->op_batch && (ctx->op.kernel_per_image || ctx->op.kind == IDEQ_OP_INPAINT))
     return fail(ctx, IDEQ_E_INVALID, "batch %d exceeds the operator's batch %d", batch, ctx->op_batch);
@@ -977,6 +1005,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   // x^{-1} = x^0; z^0 = x^0
   CK(cudaMemcpyAsync(ctx->X1, x, sizeof(float) * N * d, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemcpyAsync(ctx->Z, x, sizeof(float) * N * d, cudaMemcpyDeviceToDevice, s));
+  if (p->averaging) CK(cudaMemcpyAsync(ctx->Zsum, x, sizeof(float) * N * d, cudaMemcpyDeviceToDevice, s));  // z^0
   FinalizeArgs f = make_fin(ctx, N, p);
   if (f.parts > ctx->parts_cap) return fail(ctx, IDEQ_E_INVALID, "internal: partial buffer too small");
   launch_init_state(f, s);
@@ -999,8 +1028,8 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   } else {
     // capture one iteration (plain and with the convergence all-reduce)
     char keybuf[256];
-    snprintf(keybuf, sizeof(keybuf), "%p|%p|%d|%a|%a|%a|%a|%d|%d", (const void*)y, (void*)x, N, p->lambda, p->tau,
-             p->beta, p->tol, p->check_every, (int)p->stop_rule);
+    snprintf(keybuf, sizeof(keybuf), "%p|%p|%d|%a|%a|%a|%a|%d|%d|%d|%a|%d", (const void*)y, (void*)x, N, p->lambda,
+             p->tau, p->beta, p->tol, p->check_every, (int)p->stop_rule, p->restart, p->restart_B, p->averaging);
     if (ctx->graph_key != keybuf) {
       if (ctx->gexec_plain) { cudaGraphExecDestroy(ctx->gexec_plain); ctx->gexec_plain = nullptr; }
       if (ctx->gexec_check) { cudaGraphExecDestroy(ctx->gexec_check); ctx->gexec_check = nullptr; }
@@ -1030,7 +1059,10 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
     }
   }
   launch_gather(ctx->iters, ctx->X1, x, N, d, s);
-  std::vector<int> it(N), stv(N);
+  if (p->averaging) launch_avg_out(ctx->k0, ctx->status, ctx->iters, p->max_iter, ctx->Xsnap, x, N, d, s);
+  std::vector<int> it(N), stv(N), nr(N, 0), k0v(N, -1);
+  if (p->restart) CK(cudaMemcpyAsync(nr.data(), ctx->nrest, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  if (p->averaging) CK(cudaMemcpyAsync(k0v.data(), ctx->k0, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
   std::vector<float> rs(N);
   CK(cudaMemcpyAsync(it.data(), ctx->iters, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(stv.data(), ctx->status, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
@@ -1052,6 +1084,9 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
     stats[i].iters = it[i];
     stats[i].residual = rs[i];
     stats[i].status = stv[i];
+    stats[i].restarts = nr[i];
+    // K0 only where x-hat IS the average (same condition as avg_out_kernel)
+    stats[i].k0 = (p->averaging && stv[i] != 2 && it[i] == p->max_iter) ? k0v[i] : -1;
     if (stv[i] == 2) diverged = true;
   }
   if (diverged) return fail(ctx, IDEQ_E_DIVERGED, "at least one image produced a non-finite iterate");
@@ -1197,6 +1232,8 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   }
   AL(partials, (size_t)N * ctx->parts_cap * 3 * sizeof(float))
   AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int))
+  AL(rk, N * sizeof(int)) AL(rsum, N * sizeof(double)) AL(flags, N * sizeof(int)) AL(nrest, N * sizeof(int))
+  AL(best, N * sizeof(float)) AL(k0, N * sizeof(int)) AL(Zsum, plane) AL(Xsnap, plane)
   AL(res, N * sizeof(float)) AL(r_now, N * sizeof(float)) AL(rmax, 16) AL(n_active, 16) AL(kdev, 16)
   AL(trace, ctx->trace_cap * sizeof(float))
 #undef AL

@@ -43,6 +43,28 @@ struct FinalizeArgs {
   float* rmax;    // 1 float (NCCL all-reduce target)
   int* n_active;
   int* kdev;
+  // NEXT-1: restart (Eq. 5) and averaging (Alg. 1/2 steps 12-13)
+  int restart;        // 0 off, 1 Alg. 1 semantics, 2 Alg. 2 semantics
+  double B2;          // restart_B^2
+  int averaging, K;   // K = max_iter
+  int* rk;            // [N] iterations since the last (Alg. 1) restart
+  double* rsum;       // [N] sum of ||x^{t+1} - x^t||^2 since then
+  int* flags;         // [N] bit0 stepped this iteration, bit1 restart, bit2 new averaging minimum
+  int* nrest;         // [N] restart count
+  float* best;        // [N] smallest increment in the averaging window so far
+  int* k0;            // [N] its iteration index (-1: none)
+};
+
+struct PostArgs {
+  int N;
+  long long d;
+  const int* flags;
+  const int* kdev;
+  float* X0;
+  float* X1;
+  float* Z;      // z^{k+1} (restart: := x^{k+1})
+  float* Zsum;   // running sum of z^0..z^k (averaging) or null
+  float* Xsnap;  // averaging snapshot mean(z^0..z^K0)
 };
 
 // ---- batched 2-D FFT passes (fft.cu)
@@ -85,6 +107,9 @@ void launch_advance_a(const FinalizeArgs& f, cudaStream_t s);
 void launch_advance_b(const FinalizeArgs& f, cudaStream_t s);
 void launch_init_state(const FinalizeArgs& f, cudaStream_t s);
 void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s);
+void launch_post_step(const PostArgs& a, cudaStream_t s);
+void launch_avg_out(const int* k0, const int* status, const int* iters, int K, const float* Xsnap, float* X, int N,
+                    long long d, cudaStream_t s);
 void launch_inpaint_grad(const float* x, const float* y, const uint8_t* m, float* out, int N, int C, int H, int W,
                          cudaStream_t s);
 void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float tau, float* out, int N, int C, int H,

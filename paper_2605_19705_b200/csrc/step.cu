@@ -200,7 +200,10 @@ __global__ void finalize_kernel(FinalizeArgs f) {
   const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (n >= f.N) return;
-  if (!f.active[n]) { if (lane == 0) f.r_now[n] = __int_as_float(0x7fc00000); return; }
+  if (!f.active[n]) {
+    if (lane == 0) { f.r_now[n] = __int_as_float(0x7fc00000); if (f.flags) f.flags[n] = 0; }
+    return;
+  }
   const int k = *f.kdev;
   double d2 = 0.0, n2 = 0.0, bad = 0.0;
   for (int p = lane; p < f.parts; p += 32) {
@@ -218,7 +221,27 @@ __global__ void finalize_kernel(FinalizeArgs f) {
     f.status[n] = 2;
     f.active[n] = 0;
     f.r_now[n] = __int_as_float(0x7fc00000);
+    if (f.flags) f.flags[n] = 0;
     return;
+  }
+  if (f.flags) {  // NEXT-1 bookkeeping of the accepted step (fp64, like the oracle)
+    int fl = 1;
+    if (f.restart) {  // Eq. 5: k * sum_{t<k} ||x^{t+1} - x^t||^2 > B^2
+      int kr = f.rk[n] + 1;
+      double S = f.rsum[n] + d2;
+      if ((double)kr * S > f.B2) {
+        fl |= 2;
+        f.nrest[n] += 1;
+        if (f.restart == 1) { kr = 0; S = 0.0; }  // Alg. 1: k <- 0; Alg. 2 keeps both
+      }
+      f.rk[n] = kr;
+      f.rsum[n] = S;
+    }
+    if (f.averaging && k > f.K / 2 && k < f.K - 1) {  // window floor(K/2) < k < K-1
+      const float inc = (float)sqrt(d2);
+      if (inc < f.best[n]) { f.best[n] = inc; f.k0[n] = k; fl |= 4; }  // strict: first minimum
+    }
+    f.flags[n] = fl;
   }
   const double r = n2 > 0.0 ? sqrt(d2) / sqrt(n2) : (double)INFINITY;
   f.iters[n] = k + 1;
@@ -289,6 +312,52 @@ __global__ void gather_kernel(const int* __restrict__ iters, const float* __rest
     X0[(long long)n * d + e] = X1[(long long)n * d + e];
 }
 
+// After finalize, per image that stepped: restart -> z^{k+1} := x^{k+1} (the inertia reset of
+// Eq. 5 / Alg. 1 l.10 / Alg. 2 l.10); averaging -> snapshot mean(z^0..z^k) on a new window
+// minimum, then add z^{k+1} to the running sum (O(1) planes instead of the whole trajectory).
+__global__ void __launch_bounds__(256) post_step_kernel(PostArgs a) {
+  const int n = blockIdx.y;
+  const int fl = a.flags[n];
+  if (!(fl & 1)) return;
+  const bool rs = (fl & 2) != 0, snap = (fl & 4) != 0;
+  if (!rs && !a.Zsum) return;
+  const int k = *a.kdev;
+  const float* xn = ((k & 1) ? a.X0 : a.X1) + (long long)n * a.d;
+  float* z = a.Z + (long long)n * a.d;
+  const float inv = 1.f / (float)(k + 1);
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < a.d; e += (long long)gridDim.x * blockDim.x) {
+    float z1 = z[e];
+    if (rs) { z1 = xn[e]; z[e] = z1; }
+    if (a.Zsum) {
+      float* zs = a.Zsum + (long long)n * a.d;
+      const float sum = zs[e];
+      if (snap) a.Xsnap[(long long)n * a.d + e] = sum * inv;
+      zs[e] = sum + z1;
+    }
+  }
+}
+
+void launch_post_step(const PostArgs& a, cudaStream_t s) {
+  const long long bx = (a.d + 256 * 8 - 1) / (256 * 8);
+  post_step_kernel<<<dim3((unsigned)(bx < 1 ? 1 : bx), a.N), 256, 0, s>>>(a);
+}
+
+// x-hat = the averaging snapshot for images with a K0 (not diverged)
+__global__ void avg_out_kernel(const int* __restrict__ k0, const int* __restrict__ status,
+                               const int* __restrict__ iters, int K, const float* __restrict__ Xsnap,
+                               float* __restrict__ X, long long d) {
+  const int n = blockIdx.y;
+  if (k0[n] < 0 || status[n] == 2 || iters[n] != K) return;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < d; e += (long long)gridDim.x * blockDim.x)
+    X[(long long)n * d + e] = Xsnap[(long long)n * d + e];
+}
+
+void launch_avg_out(const int* k0, const int* status, const int* iters, int K, const float* Xsnap, float* X, int N,
+                    long long d, cudaStream_t s) {
+  const long long bx = (d + 256 * 8 - 1) / (256 * 8);
+  avg_out_kernel<<<dim3((unsigned)(bx < 1 ? 1 : bx), N), 256, 0, s>>>(k0, status, iters, K, Xsnap, X, d);
+}
+
 __global__ void init_state_kernel(FinalizeArgs f) {
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < f.N; n += gridDim.x * blockDim.x) {
     f.active[n] = 1;
@@ -296,6 +365,14 @@ __global__ void init_state_kernel(FinalizeArgs f) {
     f.iters[n] = 0;
     f.res[n] = __int_as_float(0x7fc00000);
     f.r_now[n] = __int_as_float(0x7fc00000);
+    if (f.flags) {
+      f.flags[n] = 0;
+      f.rk[n] = 0;
+      f.rsum[n] = 0.0;
+      f.nrest[n] = 0;
+      f.best[n] = __int_as_float(0x7f800000);
+      f.k0[n] = -1;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) { *f.kdev = 0; *f.n_active = f.N; }
 }

@@ -45,11 +45,13 @@ class OperatorDesc(C.Structure):
 
 class Params(C.Structure):
     _fields_ = [("lam", C.c_float), ("tau", C.c_float), ("beta", C.c_float), ("max_iter", C.c_int),
-                ("tol", C.c_float), ("check_every", C.c_int), ("stop_rule", C.c_int)]
+                ("tol", C.c_float), ("check_every", C.c_int), ("stop_rule", C.c_int), ("restart", C.c_int),
+                ("restart_B", C.c_float), ("averaging", C.c_int)]
 
 
 class ImageStat(C.Structure):
-    _fields_ = [("iters", C.c_int), ("residual", C.c_float), ("status", C.c_int)]
+    _fields_ = [("iters", C.c_int), ("residual", C.c_float), ("status", C.c_int), ("restarts", C.c_int),
+                ("k0", C.c_int)]
 
 
 class Profile(C.Structure):
@@ -213,7 +215,8 @@ class Solver:
         self._check(self.lib.ideq_set_operator(self.ctx, C.byref(op), nb))
 
     # ---------------------------------------------------------------- solve
-    def params(self, lam=None, tau=None, beta=None, max_iter=None, tol=None, check_every=None, stop_rule=None):
+    def params(self, lam=None, tau=None, beta=None, max_iter=None, tol=None, check_every=None, stop_rule=None,
+               restart=0, restart_B=0.0, averaging=False):
         cfg = self.cfg
         p = Params()
         p.lam = cfg["lam"] if lam is None else lam
@@ -223,6 +226,9 @@ class Solver:
         p.tol = cfg["tol"] if tol is None else tol
         p.check_every = cfg["check_every"] if check_every is None else check_every
         p.stop_rule = STOP[cfg["stop_rule"] if stop_rule is None else stop_rule]
+        p.restart = int(restart)
+        p.restart_B = float(restart_B)
+        p.averaging = int(bool(averaging))
         return p
 
     def solve(self, y, x, params: Params, trace: bool = False, batch: int = None):
@@ -288,4 +294,5 @@ def debug_conv(kind: int, precision: str, use_tc: bool, w: np.ndarray, N: int, H
 
 def _stats(stats):
     return dict(iters=np.array([s.iters for s in stats]), residual=np.array([s.residual for s in stats]),
-                status=np.array([s.status for s in stats]))
+                status=np.array([s.status for s in stats]), restarts=np.array([s.restarts for s in stats]),
+                k0=np.array([s.k0 for s in stats]))
