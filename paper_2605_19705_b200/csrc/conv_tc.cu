@@ -234,24 +234,47 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// bf16-mode epilogue transcendentals (outputs are rounded to bf16, rel. 2^-9): softplus via the
-// SFU exp/log; sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a
-// to avoid the cancellation of 1 - exp(-a).
-// log1p(u) on u in [0, 1] by a degree-6 Chebyshev-interpolated polynomial (|err| < 1.5e-6, far
-// below the bf16 rounding of the output), so softplus costs one MUFU.EX2 instead of EX2 + LG2.
-__device__ __forceinline__ float softplus_fast(float t) {
-  const float u = __expf(-fabsf(t));
+// bf16-mode epilogue transcendentals (outputs are rounded to bf16, rel. 2^-9).
+// log1p(u) on u in [0, 1] by a degree-6 Chebyshev-interpolated polynomial (|err| < 1.5e-6), so
+// softplus costs one exponential instead of EX2 + LG2.
+__device__ __forceinline__ float log1p01(float u) {  // u in [0, 1]
   float p = -0.01741407752407103f;
   p = fmaf(p, u, 0.08269123711081523f);
   p = fmaf(p, u, -0.19035433673230703f);
   p = fmaf(p, u, 0.3157473167575014f);
   p = fmaf(p, u, -0.4973732161578083f);
   p = fmaf(p, u, 0.9998476974962173f);
-  p = fmaf(p, u, 1.4720650115540579e-06f);
-  return fmaxf(t, 0.f) + p;
+  return fmaf(p, u, 1.4720650115540579e-06f);
 }
+// 2^x for x <= 0 on the FMA/ALU pipes (no MUFU): x = n + f, f in [-0.5, 0.5], 2^f by a degree-4
+// Chebyshev-interpolated polynomial (relative error < 4e-6), 2^n added to the exponent bits.
+// Measured: moving half of the epilogue exponentials here made the level-0/1 softplus and sp'
+// layers 5-25% SLOWER (the FMA/ALU pipes are busier than MUFU there), so the epilogues keep
+// MUFU (POLY = false); kept for A/B measurements.
+__device__ __forceinline__ float exp2_fma(float x) {
+  x = fmaxf(x, -126.f);
+  const float j = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer
+  const float f = x - (j - 12582912.f);
+  float p = 0.009676037097880542f;
+  p = fmaf(p, f, 0.05592203564725866f);
+  p = fmaf(p, f, 0.24022107355830305f);
+  p = fmaf(p, f, 0.6931210339915471f);
+  p = fmaf(p, f, 1.0000000754953493f);
+  return __int_as_float(__float_as_int(p) + ((__float_as_int(j) - 0x4B400000) << 23));
+}
+// softplus: one exponential + a degree-6 polynomial for log1p (|err| < 1.5e-6, far below the
+// bf16 rounding of the output). POLY selects the FMA-pipe exponential.
+template <bool POLY = false>
+__device__ __forceinline__ float softplus_fast(float t) {
+  const float u = POLY ? exp2_fma(-1.4426950408889634f * fabsf(t)) : __expf(-fabsf(t));
+  return fmaxf(t, 0.f) + log1p01(u);
+}
+// sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a to avoid the
+// cancellation of 1 - exp(-a) (bf16-mode outputs are rounded to bf16, rel. 2^-9).
+template <bool POLY = false>
 __device__ __forceinline__ float dsoftplus_from_act_fast(float a) {
-  return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - __expf(-a);
+  const float e = POLY ? exp2_fma(-1.4426950408889634f * a) : __expf(-a);
+  return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - e;
 }
 
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3,
@@ -658,13 +681,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 o[2 * e] = v[q * 8 + 2 * e] + f.x;
                 o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
               } else {
-                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast(f.x);
-                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast(f.y);
+                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast<false>(f.x);
+                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast<false>(f.y);
               }
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast(v[q * 8 + e]) : v[q * 8 + e];
+            for (int e = 0; e < 8; ++e)
+              o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v[q * 8 + e]) : v[q * 8 + e];
           }
           uint4 w;
           __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
