@@ -13,6 +13,10 @@ Inpainting (PAPER App. D.3.2):
 Coded-diffraction phase retrieval (BASELINE C4; reading Q7, Q14):
   f = 1/2 sum_j || |F(D_j x)|^2 - y_j ||^2, F the unitary 2-D DFT,
   grad f = sum_j 2 Re( conj(D_j) F^{-1}[ (|u_j|^2 - y_j) u_j ] ),  u_j = F(D_j x).
+Rician denoising (PAPER App. D.3.3):
+  f = sum x^2 / (2 sigma^2) - log I0(x y / sigma^2),
+  grad f = x / sigma^2 - (y / sigma^2) B(x y / sigma^2),  B = I1 / I0;  no closed-form prox.
+  I0, I1 via the exponentially scaled library routines scipy.special.i0e / i1e (library step).
 
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
 """
@@ -114,12 +118,41 @@ def phase_grad(x, y, D):
     return g[None]
 
 
+# --------------------------------------------------------------------------- Rician
+def bessel_ratio(t):
+    """B(t) = I1(t) / I0(t) = i1e(t) / i0e(t): the e^{-t} scalings cancel, no overflow."""
+    from scipy.special import i0e, i1e
+    t = np.asarray(t, dtype=np.float64)
+    return i1e(t) / i0e(t)
+
+
+def log_i0(t):
+    """log I0(t) = t + log i0e(t) for t >= 0 (I0 is even)."""
+    from scipy.special import i0e
+    t = np.abs(np.asarray(t, dtype=np.float64))
+    return t + np.log(i0e(t))
+
+
+def rician_f(x, y, sigma):
+    """f = sum x^2 / (2 sigma^2) - log I0(x y / sigma^2)."""
+    s2 = sigma * sigma
+    return float(np.sum(x * x / (2.0 * s2) - log_i0(x * y / s2)))
+
+
+def rician_grad(x, y, sigma):
+    """grad f = x / sigma^2 - (y / sigma^2) B(x y / sigma^2). B is odd: B(-t) = -B(t)."""
+    s2 = sigma * sigma
+    t = x * y / s2
+    return x / s2 - (y / s2) * np.sign(t) * bessel_ratio(np.abs(t))
+
+
 # --------------------------------------------------------------------------- dispatch
 class Fidelity:
     """f(., y) for one image: value, gradient, prox (None when not closed form)."""
 
-    def __init__(self, kind, y, kernel=None, mask=None, phase=None):
+    def __init__(self, kind, y, kernel=None, mask=None, phase=None, sigma=None):
         self.kind = kind
+        self.sigma = sigma
         self.y = np.asarray(y, dtype=np.float64)
         self.k = None if kernel is None else np.asarray(kernel, dtype=np.float64)
         self.m = None if mask is None else np.asarray(mask, dtype=np.float64)[None]
@@ -132,6 +165,8 @@ class Fidelity:
             return blur_f(x, self.y, self.k)
         if self.kind == "inpaint":
             return inpaint_f(x, self.y, self.m)
+        if self.kind == "rician":
+            return rician_f(x, self.y, self.sigma)
         return phase_f(x, self.y, self.D)
 
     def grad(self, x):
@@ -139,6 +174,8 @@ class Fidelity:
             return blur_grad(x, self.y, self.k)
         if self.kind == "inpaint":
             return inpaint_grad(x, self.y, self.m)
+        if self.kind == "rician":
+            return rician_grad(x, self.y, self.sigma)
         return phase_grad(x, self.y, self.D)
 
     def prox(self, v, tau):
@@ -146,4 +183,4 @@ class Fidelity:
             return blur_prox(v, self.y, self.k, tau)
         if self.kind == "inpaint":
             return inpaint_prox(v, self.y, self.m, tau)
-        raise NotImplementedError("no closed-form prox for phase retrieval (cf. P:1079)")
+        raise NotImplementedError("no closed-form prox for phase retrieval / Rician (P:1079)")

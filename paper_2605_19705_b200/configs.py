@@ -46,6 +46,16 @@ CONFIGS = {
 }
 
 
+# Configurations of the §8(f) NEXT rows (not BASELINE configs; parity cases only).
+# R1: Rician denoising (PAPER App. D.3.3), gradient variant only (no closed-form prox,
+# P:1079). tau < 1/L with L_f <= 1/sigma^2 (B' <= 1/2 makes the Hessian of f at most 1/sigma^2):
+# tau = 0.9 sigma^2; lambda scaled so that tau * lambda = 0.045 as in the blur/inpainting configs.
+CONFIGS["R1"] = dict(name="R1 Rician denoising", seed_id=6, batch=4, C=1, H=128, W=128,
+                     net="unet4", widths=UNET32, res_blocks=2, identity_skip=True, act="softplus",
+                     op="rician", sigma=0.05, step="grad", lam=20.0, tau=0.9 * 0.05 ** 2, beta=0.5,
+                     max_iter=100, tol=1e-4, check_every=1, stop_rule="per_image", precision="bf16")
+
+
 # Stress variants for parity: with the x0.1 init and lambda = 0.05 the
 # regularizer term lam*grad g is ~1e-3 of grad f, so trajectory parity alone would not
 # exercise the VJP. The stress variant uses init scale 0.3 and a larger lambda chosen so
@@ -57,6 +67,7 @@ STRESS = {
     "C3": dict(init_scale=0.3, lam=0.1),
     "C4": dict(init_scale=0.3, lam=5.0),
     "C5": dict(init_scale=0.3, lam=0.1),
+    "R1": dict(init_scale=0.3, lam=200.0),
 }
 
 

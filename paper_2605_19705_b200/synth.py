@@ -17,7 +17,7 @@ import numpy as np
 __all__ = [
     "piecewise_smooth", "gaussian_kernel", "motion_kernel", "bernoulli_mask",
     "phase_masks", "he_normal_weights", "unet_weight_shapes", "tiny_weight_shapes",
-    "simulate_blur", "simulate_inpaint", "simulate_phase", "make_problem",
+    "simulate_blur", "simulate_inpaint", "simulate_phase", "simulate_rician", "make_problem",
 ]
 
 
@@ -161,6 +161,14 @@ def simulate_phase(x: np.ndarray, D: np.ndarray, noise_rng) -> np.ndarray:
     return y.astype(np.float32)
 
 
+def simulate_rician(x: np.ndarray, sigma: float, noise_rng) -> np.ndarray:
+    """Magnitude measurement y = sqrt((x + n_real)^2 + n_imag^2), n ~ N(0, sigma^2) iid
+    (PAPER App. D.3.3). Returns float32, same shape as x."""
+    nr = sigma * noise_rng.standard_normal(x.shape)
+    ni = sigma * noise_rng.standard_normal(x.shape)
+    return np.sqrt((x.astype(np.float64) + nr) ** 2 + ni ** 2).astype(np.float32)
+
+
 # --------------------------------------------------------------------------- problems
 def make_problem(cfg: dict, images=None) -> dict:
     """Build the inputs of one config (see configs.py). ``images`` selects a subset
@@ -209,6 +217,9 @@ def make_problem(cfg: dict, images=None) -> dict:
             ms.append(m)
             y = simulate_inpaint(x, m, cfg["sigma"], noise_rng)
             x0 = y.copy()                                     # zero-filled start
+        elif op == "rician":
+            y = simulate_rician(x, cfg["sigma"], noise_rng)
+            x0 = y.copy()
         elif op == "phase":
             y = simulate_phase(x, prob["phase_masks"], noise_rng)
             x0 = np.full((C, H, W), np.sqrt(max(float(y.astype(np.float64).mean()), 0.0)), dtype=np.float32)
