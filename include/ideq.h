@@ -115,7 +115,7 @@ IDEQ_API ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, 
                         void* cuda_stream, int max_batch, int H, int W,
                         const ideq_dist* dist, ideq_ctx** out);
 
-typedef enum { IDEQ_OP_BLUR = 0, IDEQ_OP_INPAINT = 1, IDEQ_OP_PHASE = 2 } ideq_op_kind;
+typedef enum { IDEQ_OP_BLUR = 0, IDEQ_OP_INPAINT = 1, IDEQ_OP_PHASE = 2, IDEQ_OP_RICIAN = 3 } ideq_op_kind;
 typedef enum { IDEQ_STEP_GRAD = 0, IDEQ_STEP_PROX = 1 } ideq_step;   /* Alg. 1 vs Alg. 2 */
 typedef enum { IDEQ_BLUR_DIRECT = 0, IDEQ_BLUR_FFT = 1 } ideq_blur_impl;
 
@@ -129,6 +129,9 @@ typedef enum { IDEQ_BLUR_DIRECT = 0, IDEQ_BLUR_FFT = 1 } ideq_blur_impl;
  *            prox = (tau M y + v)/(tau M + 1) (l.1029); M shared by channels.
  *   PHASE  : f = 1/2 sum_j || |F(D_j x)|^2 - y_j ||^2, F unitary 2-D DFT,
  *            C must be 1; gradient step only.
+ *   RICIAN : f = sum x^2/(2 sigma^2) - log I0(x y / sigma^2) (App. D.3.3, l.1071),
+ *            grad = x/sigma^2 - (y/sigma^2) B(x y/sigma^2), B = I1/I0 (l.1075);
+ *            gradient step only (no closed-form prox, l.1079); sigma > 0.
  * kernels: HOST fp32 [1 or batch][ksize][ksize]; masks: HOST u8 [batch][H][W]
  * (1 = observed); phase_masks: HOST fp32 [n_phase][H][W][2] (re, im), shared.
  * Copied; `batch` is the number of images that later solves will use.
@@ -142,6 +145,7 @@ typedef struct {
   const unsigned char* masks;
   int n_phase;
   const float* phase_masks;
+  float sigma;  /* RICIAN noise level sigma_y > 0 */
 } ideq_operator_desc;
 
 IDEQ_API ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int batch);

@@ -827,6 +827,7 @@ StepArgs make_step_args(ideq_ctx* ctx, int N, const float* y, float* x0, const i
   a.mask = ctx->d_mask; a.fbuf = ctx->fbuf; a.fbuf2 = ctx->fbuf2;
   a.kern = ctx->d_kern; a.ksize = ctx->op.ksize; a.kernel_per_image = ctx->op.kernel_per_image;
   if (p) { a.lam = p->lambda; a.tau = p->tau; a.beta = p->beta; }
+  a.inv_s2 = ctx->op.kind == IDEQ_OP_RICIAN ? 1.f / (ctx->op.sigma * ctx->op.sigma) : 0.f;
   a.active = ctx->active; a.kdev = ctx->kdev; a.partials = ctx->partials;
   return a;
 }
@@ -863,6 +864,9 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
   if (op.kind == IDEQ_OP_INPAINT) {
     Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 7.0);
     launch_pointwise_step(op.step == IDEQ_STEP_PROX ? STEP_PROX_INPAINT : STEP_GRAD_INPAINT, a, s);
+  } else if (op.kind == IDEQ_OP_RICIAN) {
+    Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 6.0);
+    launch_pointwise_step(STEP_GRAD_RICIAN, a, s);
   } else if (op.kind == IDEQ_OP_BLUR && op.step == IDEQ_STEP_PROX) {
     // x^{k+1} = F^-1[ F(z - tau lam grad g + tau A^T y) / (1 + tau |K^|^2) ]   (prox P:80-84)
     FftArgs f = make_fft_args(ctx, a.y, nullptr);
@@ -988,6 +992,8 @@ ideq_status operator_runnable(ideq_ctx* ctx) {
   const auto& op = ctx->op;
   if (op.kind == IDEQ_OP_PHASE && op.step == IDEQ_STEP_PROX)
     return fail(ctx, IDEQ_E_UNSUPPORTED, "phase retrieval has no closed-form prox (cf. PAPER l.1079)");
+  if (op.kind == IDEQ_OP_RICIAN && op.step == IDEQ_STEP_PROX)
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "the Rician fidelity has no closed-form prox (PAPER l.1079)");
   if (op.kind == IDEQ_OP_BLUR && op.step == IDEQ_STEP_GRAD && op.blur_impl == IDEQ_BLUR_FFT)
     return fail(ctx, IDEQ_E_UNSUPPORTED, "the blur gradient step uses the direct convolution (blur_impl DIRECT)");
   return IDEQ_OK;
@@ -1337,6 +1343,9 @@ ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int b
     CK(cudaMemcpy(p, op->phase_masks, n * 4, cudaMemcpyHostToDevice));
     ctx->d_phase = (float*)p;
     if ((st = setup_fft(ctx, (size_t)batch * op->n_phase * H * W))) return st;
+  } else if (op->kind == IDEQ_OP_RICIAN) {
+    if (op->step == IDEQ_STEP_PROX) return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form Rician prox (PAPER l.1079)");
+    if (!(op->sigma > 0.f)) return fail(ctx, IDEQ_E_INVALID, "Rician sigma must be > 0");
   } else {
     return fail(ctx, IDEQ_E_INVALID, "unknown operator kind");
   }
@@ -1413,6 +1422,9 @@ ideq_status ideq_fidelity_grad(ideq_ctx* ctx, const float* y, const float* x, fl
   const auto& op = ctx->op;
   if (op.kind == IDEQ_OP_INPAINT) {
     launch_inpaint_grad(x, y, ctx->d_mask, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
+  } else if (op.kind == IDEQ_OP_RICIAN) {
+    launch_rician_grad(x, y, 1.f / (op.sigma * op.sigma), out, (long long)batch * ctx->C * ctx->H * ctx->W,
+                       ctx->stream);
   } else if (op.kind == IDEQ_OP_BLUR && op.blur_impl == IDEQ_BLUR_DIRECT) {
     StepArgs a = make_step_args(ctx, batch, y, nullptr, nullptr);
     a.z = x;
@@ -1443,8 +1455,8 @@ ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, fl
   if (!y || !v || !out || batch < 1 || batch > ctx->op_batch || !(tau > 0.f)) return fail(ctx, IDEQ_E_INVALID, "bad arguments");
   if (ctx->op.kind == IDEQ_OP_INPAINT) {
     launch_inpaint_prox(v, y, ctx->d_mask, tau, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
-  } else if (ctx->op.kind == IDEQ_OP_PHASE) {
-    return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval (cf. PAPER l.1079)");
+  } else if (ctx->op.kind == IDEQ_OP_PHASE || ctx->op.kind == IDEQ_OP_RICIAN) {
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval / Rician (PAPER l.1079)");
   } else if (ctx->op.blur_impl == IDEQ_BLUR_FFT) {
     // prox_{tau f}(v) = F^-1[F(v + tau A^T y) / (1 + tau |K^|^2)]: the solver's passes with lam = 0
     prepare_blur_prox(ctx, y, tau, batch);

@@ -7,7 +7,7 @@
 
 namespace ideq {
 
-enum StepMode : int { STEP_PROX_INPAINT = 0, STEP_GRAD_BUF = 1, STEP_GRAD_INPAINT = 2, STEP_X1_BUF = 3 };
+enum StepMode : int { STEP_PROX_INPAINT = 0, STEP_GRAD_BUF = 1, STEP_GRAD_INPAINT = 2, STEP_X1_BUF = 3, STEP_GRAD_RICIAN = 4 };
 
 struct StepArgs {
   int N, C, H, W;
@@ -25,6 +25,7 @@ struct StepArgs {
   const float* kern;      // blur kernel(s)
   int ksize, kernel_per_image;
   float lam, tau, beta;
+  float inv_s2;           // Rician: 1 / sigma^2
   const int* active;      // [N]
   const int* kdev;        // iteration counter k
   float* partials;        // [N][parts][3]
@@ -108,6 +109,7 @@ void launch_advance_b(const FinalizeArgs& f, cudaStream_t s);
 void launch_init_state(const FinalizeArgs& f, cudaStream_t s);
 void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s);
 void launch_post_step(const PostArgs& a, cudaStream_t s);
+void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s);
 void launch_avg_out(const int* k0, const int* status, const int* iters, int K, const float* Xsnap, float* X, int N,
                     long long d, cudaStream_t s);
 void launch_inpaint_grad(const float* x, const float* y, const uint8_t* m, float* out, int N, int C, int H, int W,

@@ -48,6 +48,44 @@ __device__ __forceinline__ void tail_elem(float x1, float xk, float beta, float*
   acc.n2 += xk * xk;
 }
 
+// ------------------------------------------------------------------ Rician fidelity (App. D.3.3)
+// B(t) = I1(t) / I0(t) for t >= 0 in fp32: the defining power series below t = 20 (terms
+// (t/2)^{2k} / (k!)^2 stay far from fp32 overflow there), the asymptotic expansion
+// 1 - 1/(2t) - 1/(8t^2) - 1/(8t^3) - 25/(128 t^4) above (|error| < 1.5e-7 at t = 20).
+__device__ __forceinline__ float bessel_ratio_f(float t) {
+  if (t < 20.f) {
+    const float q = 0.25f * t * t;
+    float a = 1.f, i0 = 1.f, i1 = 1.f;  // i1 accumulates sum a_k / (k + 1)
+    for (int k = 1; k < 64; ++k) {
+      a *= q / (float)(k * k);
+      i0 += a;
+      i1 += a / (float)(k + 1);
+      if (a < 1e-9f * i0) break;
+    }
+    return 0.5f * t * i1 / i0;
+  }
+  const float r = 1.f / t;
+  return 1.f - r * (0.5f + r * (0.125f + r * (0.125f + r * (25.f / 128.f))));
+}
+// grad f = x / sigma^2 - (y / sigma^2) B(x y / sigma^2); B is odd
+__device__ __forceinline__ float rician_grad_f(float x, float y, float inv_s2) {
+  const float t = x * y * inv_s2;
+  const float b = bessel_ratio_f(fabsf(t));
+  return x * inv_s2 - y * inv_s2 * copysignf(b, t);
+}
+
+__global__ void __launch_bounds__(256) rician_grad_kernel(const float* __restrict__ x, const float* __restrict__ y,
+                                                          float inv_s2, float* __restrict__ out, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = rician_grad_f(x[i], y[i], inv_s2);
+}
+
+void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s) {
+  long long b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  rician_grad_kernel<<<(unsigned)b, 256, 0, s>>>(x, y, inv_s2, out, n);
+}
+
 // ------------------------------------------------------------------ pointwise step kernels
 // Block -> (image n, part) with `parts` blocks per image, each covering a fixed
 // contiguous chunk of the image's d = C*H*W elements.
@@ -77,6 +115,8 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
     } else if (MODE == STEP_GRAD_BUF) {
       // x = z - tau (grad f + lam grad g), grad f precomputed in a.fbuf
       x1 = z - a.tau * (a.fbuf[i] + a.lam * gg);
+    } else if (MODE == STEP_GRAD_RICIAN) {
+      x1 = z - a.tau * (rician_grad_f(z, a.y[i], a.inv_s2) + a.lam * gg);   // Alg. 1 l.8
     } else if (MODE == STEP_GRAD_INPAINT) {
       const float m = (float)a.mask[(long long)n * HW + (e % HW)];
       x1 = z - a.tau * (m * (m * z - a.y[i]) + a.lam * gg);
@@ -403,6 +443,7 @@ void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
     case STEP_PROX_INPAINT: pointwise_step_kernel<STEP_PROX_INPAINT><<<grid, 256, 0, s>>>(a); break;
     case STEP_GRAD_BUF: pointwise_step_kernel<STEP_GRAD_BUF><<<grid, 256, 0, s>>>(a); break;
     case STEP_GRAD_INPAINT: pointwise_step_kernel<STEP_GRAD_INPAINT><<<grid, 256, 0, s>>>(a); break;
+    case STEP_GRAD_RICIAN: pointwise_step_kernel<STEP_GRAD_RICIAN><<<grid, 256, 0, s>>>(a); break;
     default: pointwise_step_kernel<STEP_X1_BUF><<<grid, 256, 0, s>>>(a); break;
   }
 }

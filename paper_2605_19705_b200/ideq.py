@@ -20,7 +20,7 @@ STATUS_NAMES = ["OK", "INVALID", "DIVERGED", "UNSUPPORTED", "CUDA", "NCCL", "NOM
 PREC = {"fp32": 0, "bf16": 1}
 ARCH = {"tiny3": 0, "unet4": 1}
 ACT = {"softplus": 0, "identity": 1}
-OP = {"blur": 0, "inpaint": 1, "phase": 2}
+OP = {"blur": 0, "inpaint": 1, "phase": 2, "rician": 3}
 STEP = {"grad": 0, "prox": 1}
 BLUR = {"direct": 0, "fft": 1}
 STOP = {"per_image": 0, "global_max": 1}
@@ -40,7 +40,8 @@ class Dist(C.Structure):
 class OperatorDesc(C.Structure):
     _fields_ = [("kind", C.c_int), ("step", C.c_int), ("blur_impl", C.c_int), ("ksize", C.c_int),
                 ("kernel_per_image", C.c_int), ("kernels", C.POINTER(C.c_float)),
-                ("masks", C.POINTER(C.c_ubyte)), ("n_phase", C.c_int), ("phase_masks", C.POINTER(C.c_float))]
+                ("masks", C.POINTER(C.c_ubyte)), ("n_phase", C.c_int), ("phase_masks", C.POINTER(C.c_float)),
+                ("sigma", C.c_float)]
 
 
 class Params(C.Structure):
@@ -206,6 +207,8 @@ class Solver:
             m = np.ascontiguousarray(prob["masks"], dtype=np.uint8)
             op.masks = m.ctypes.data_as(C.POINTER(C.c_ubyte))
             self._keep.append(m)
+        elif cfg["op"] == "rician":
+            op.sigma = float(cfg["sigma"])
         else:
             d = np.ascontiguousarray(prob["phase_masks"], dtype=np.float32)
             op.n_phase = d.shape[0]

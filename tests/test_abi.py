@@ -49,6 +49,7 @@ def test_struct_layouts_match_header():
     """ctypes mirrors of the ABI structs have the C sizes (x86-64 SysV)."""
     from paper_2605_19705_b200 import ideq
     assert ctypes.sizeof(ideq.Params) == 10 * 4
+    assert ctypes.sizeof(ideq.OperatorDesc) == 64  # 5 ints + 3 pointers (+pad) + int + pointer + float (+pad)
     assert ctypes.sizeof(ideq.ImageStat) == 20
     assert ctypes.sizeof(ideq.Dist) == 8 + 128
     assert ctypes.sizeof(ideq.NetDesc) == 56  # 9 ints + 4 pad + pointer + size_t
