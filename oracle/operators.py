@@ -13,6 +13,10 @@ Inpainting (PAPER App. D.3.2):
 Coded-diffraction phase retrieval (BASELINE C4; reading Q7, Q14):
   f = 1/2 sum_j || |F(D_j x)|^2 - y_j ||^2, F the unitary 2-D DFT,
   grad f = sum_j 2 Re( conj(D_j) F^{-1}[ (|u_j|^2 - y_j) u_j ] ),  u_j = F(D_j x).
+Compressed-sensing MRI (PAPER App. D.3.1; readings Q18, R7):
+  x real (zero phase), y complex k-space, F the unitary 2-D DFT, M a binary mask:
+  f = 1/2 ||M F x - y||^2, grad f = Re F^{-1} M^T (M F x - y),
+  prox_{tau f}(v) = Re F^{-1}[ (F v + tau M y) / (1 + tau M) ] (P:985 read in k-space, Q18).
 Rician denoising (PAPER App. D.3.3):
   f = sum x^2 / (2 sigma^2) - log I0(x y / sigma^2),
   grad f = x / sigma^2 - (y / sigma^2) B(x y / sigma^2),  B = I1 / I0;  no closed-form prox.
@@ -118,6 +122,23 @@ def phase_grad(x, y, D):
     return g[None]
 
 
+# --------------------------------------------------------------------------- MRI
+def mri_f(x, y, m):
+    """x: [1][H][W] real; y: [H][W] complex; m: [H][W] in {0, 1}."""
+    r = m * _dft(x[0]) - y
+    return 0.5 * float(np.sum(np.abs(r) ** 2))
+
+
+def mri_grad(x, y, m):
+    """Re F^{-1} M^T (M F x - y); F^{-1} = F^H for the unitary DFT."""
+    return np.real(_idft(m * (m * _dft(x[0]) - y)))[None]
+
+
+def mri_prox(v, y, m, tau):
+    """Re F^{-1}[(F v + tau M y) / (1 + tau M)] (reading Q18)."""
+    return np.real(_idft((_dft(v[0]) + tau * m * y) / (1.0 + tau * m)))[None]
+
+
 # --------------------------------------------------------------------------- Rician
 def bessel_ratio(t):
     """B(t) = I1(t) / I0(t) = i1e(t) / i0e(t): the e^{-t} scalings cancel, no overflow."""
@@ -153,6 +174,11 @@ class Fidelity:
     def __init__(self, kind, y, kernel=None, mask=None, phase=None, sigma=None):
         self.kind = kind
         self.sigma = sigma
+        if kind == "mri":  # y: [H][W][2] (re, im) -> complex; mask: [H][W] k-space
+            y = np.asarray(y, dtype=np.float64)
+            self.y = y[..., 0] + 1j * y[..., 1]
+            self.km = np.asarray(mask, dtype=np.float64)
+            return
         self.y = np.asarray(y, dtype=np.float64)
         self.k = None if kernel is None else np.asarray(kernel, dtype=np.float64)
         self.m = None if mask is None else np.asarray(mask, dtype=np.float64)[None]
@@ -167,6 +193,8 @@ class Fidelity:
             return inpaint_f(x, self.y, self.m)
         if self.kind == "rician":
             return rician_f(x, self.y, self.sigma)
+        if self.kind == "mri":
+            return mri_f(x, self.y, self.km)
         return phase_f(x, self.y, self.D)
 
     def grad(self, x):
@@ -176,6 +204,8 @@ class Fidelity:
             return inpaint_grad(x, self.y, self.m)
         if self.kind == "rician":
             return rician_grad(x, self.y, self.sigma)
+        if self.kind == "mri":
+            return mri_grad(x, self.y, self.km)
         return phase_grad(x, self.y, self.D)
 
     def prox(self, v, tau):
@@ -183,4 +213,6 @@ class Fidelity:
             return blur_prox(v, self.y, self.k, tau)
         if self.kind == "inpaint":
             return inpaint_prox(v, self.y, self.m, tau)
+        if self.kind == "mri":
+            return mri_prox(v, self.y, self.km, tau)
         raise NotImplementedError("no closed-form prox for phase retrieval / Rician (P:1079)")

@@ -88,6 +88,8 @@ def make_fidelities(cfg, prob):
             fids.append(Fidelity("blur", prob["y"][b], kernel=k))
         elif cfg["op"] == "inpaint":
             fids.append(Fidelity("inpaint", prob["y"][b], mask=prob["masks"][b]))
+        elif cfg["op"] == "mri":
+            fids.append(Fidelity("mri", prob["y"][b], mask=prob["kmask"]))
         elif cfg["op"] == "rician":
             fids.append(Fidelity("rician", prob["y"][b], sigma=cfg["sigma"]))
         else:

@@ -55,6 +55,14 @@ CONFIGS["R1"] = dict(name="R1 Rician denoising", seed_id=6, batch=4, C=1, H=128,
                      op="rician", sigma=0.05, step="grad", lam=20.0, tau=0.9 * 0.05 ** 2, beta=0.5,
                      max_iter=100, tol=1e-4, check_every=1, stop_rule="per_image", precision="bf16")
 
+# M1: compressed-sensing MRI (PAPER App. D.3.1; §4.1 x8 acceleration, sigma_y = 1/255
+# P:1000), real magnitude image with zero phase, proximal variant (Alg. 2) with the
+# closed-form prox (reading Q18). L_f = 1: tau = 1 is the blur/inpainting choice.
+CONFIGS["M1"] = dict(name="M1 MRI x8", seed_id=7, batch=4, C=1, H=256, W=256,
+                     net="unet4", widths=UNET32, res_blocks=2, identity_skip=True, act="softplus",
+                     op="mri", accel=8, sigma=1.0 / 255, step="prox", lam=0.05, tau=1.0, beta=0.5,
+                     max_iter=100, tol=1e-4, check_every=1, stop_rule="per_image", precision="bf16")
+
 
 # Stress variants for parity: with the x0.1 init and lambda = 0.05 the
 # regularizer term lam*grad g is ~1e-3 of grad f, so trajectory parity alone would not
@@ -68,6 +76,7 @@ STRESS = {
     "C4": dict(init_scale=0.3, lam=5.0),
     "C5": dict(init_scale=0.3, lam=0.1),
     "R1": dict(init_scale=0.3, lam=200.0),
+    "M1": dict(init_scale=0.3, lam=0.1),
 }
 
 

@@ -17,7 +17,7 @@ import numpy as np
 __all__ = [
     "piecewise_smooth", "gaussian_kernel", "motion_kernel", "bernoulli_mask",
     "phase_masks", "he_normal_weights", "unet_weight_shapes", "tiny_weight_shapes",
-    "simulate_blur", "simulate_inpaint", "simulate_phase", "simulate_rician", "make_problem",
+    "simulate_blur", "simulate_inpaint", "simulate_phase", "simulate_rician", "cartesian_mask", "simulate_mri", "make_problem",
 ]
 
 
@@ -161,6 +161,27 @@ def simulate_phase(x: np.ndarray, D: np.ndarray, noise_rng) -> np.ndarray:
     return y.astype(np.float32)
 
 
+def cartesian_mask(H: int, W: int, accel: int) -> np.ndarray:
+    """Cartesian k-space mask (PAPER §4.1 "acceleration factor x8"; the paper's fastMRI mask
+    generator is unstated): keep every phase-encode column kx with kx = 0 mod accel plus a fully
+    sampled low-frequency band of max(4, W/32) columns around kx = 0. Both sets are closed under
+    kx -> -kx, so the mask is Hermitian-symmetric (reading R7). Returns u8 [H][W]."""
+    kx = np.arange(W)
+    kxs = np.minimum(kx, W - kx)                    # |frequency| index
+    band = max(4, W // 32)
+    keep = (kx % accel == 0) | (kxs <= band // 2)
+    return np.broadcast_to(keep[None, :], (H, W)).astype(np.uint8).copy()
+
+
+def simulate_mri(x: np.ndarray, mask: np.ndarray, sigma: float, noise_rng) -> np.ndarray:
+    """y = M F x + n, F the unitary 2-D DFT, n complex Gaussian (re, im ~ N(0, sigma^2)) on the
+    sampled entries. x: [1][H][W]; returns float32 [H][W][2] (re, im)."""
+    u = np.fft.fft2(x[0].astype(np.float64), norm="ortho")
+    n = sigma * (noise_rng.standard_normal(u.shape) + 1j * noise_rng.standard_normal(u.shape))
+    y = mask * (u + n)
+    return np.stack([y.real, y.imag], axis=-1).astype(np.float32)
+
+
 def simulate_rician(x: np.ndarray, sigma: float, noise_rng) -> np.ndarray:
     """Magnitude measurement y = sqrt((x + n_real)^2 + n_imag^2), n ~ N(0, sigma^2) iid
     (PAPER App. D.3.3). Returns float32, same shape as x."""
@@ -193,6 +214,8 @@ def make_problem(cfg: dict, images=None) -> dict:
     op = cfg["op"]
     if op == "phase":
         prob["phase_masks"] = phase_masks(np.random.default_rng([cid, 3]), cfg["n_phase"], H, W)
+    if op == "mri":
+        prob["kmask"] = cartesian_mask(H, W, cfg["accel"])
     if op == "blur" and not cfg.get("kernel_per_image", False):
         prob["kernel"] = gaussian_kernel(cfg["ksize"], cfg["ksigma"])
     for i in idx:
@@ -220,6 +243,11 @@ def make_problem(cfg: dict, images=None) -> dict:
         elif op == "rician":
             y = simulate_rician(x, cfg["sigma"], noise_rng)
             x0 = y.copy()
+        elif op == "mri":
+            y = simulate_mri(x, prob["kmask"], cfg["sigma"], noise_rng)
+            # zero-filled start: x^0 = Re F^{-1} y (the standard MRI initialisation)
+            x0 = np.real(np.fft.ifft2(y[..., 0].astype(np.float64) + 1j * y[..., 1], norm="ortho"))[None]
+            x0 = x0.astype(np.float32)
         elif op == "phase":
             y = simulate_phase(x, prob["phase_masks"], noise_rng)
             x0 = np.full((C, H, W), np.sqrt(max(float(y.astype(np.float64).mean()), 0.0)), dtype=np.float32)
