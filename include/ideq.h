@@ -115,7 +115,7 @@ IDEQ_API ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, 
                         void* cuda_stream, int max_batch, int H, int W,
                         const ideq_dist* dist, ideq_ctx** out);
 
-typedef enum { IDEQ_OP_BLUR = 0, IDEQ_OP_INPAINT = 1, IDEQ_OP_PHASE = 2, IDEQ_OP_RICIAN = 3 } ideq_op_kind;
+typedef enum { IDEQ_OP_BLUR = 0, IDEQ_OP_INPAINT = 1, IDEQ_OP_PHASE = 2, IDEQ_OP_RICIAN = 3, IDEQ_OP_MRI = 4 } ideq_op_kind;
 typedef enum { IDEQ_STEP_GRAD = 0, IDEQ_STEP_PROX = 1 } ideq_step;   /* Alg. 1 vs Alg. 2 */
 typedef enum { IDEQ_BLUR_DIRECT = 0, IDEQ_BLUR_FFT = 1 } ideq_blur_impl;
 
@@ -129,6 +129,12 @@ typedef enum { IDEQ_BLUR_DIRECT = 0, IDEQ_BLUR_FFT = 1 } ideq_blur_impl;
  *            prox = (tau M y + v)/(tau M + 1) (l.1029); M shared by channels.
  *   PHASE  : f = 1/2 sum_j || |F(D_j x)|^2 - y_j ||^2, F unitary 2-D DFT,
  *            C must be 1; gradient step only.
+ *   MRI    : f = 1/2||M F x - y||^2 (App. D.3.1, l.964), x real (zero phase, l.995),
+ *            F the unitary 2-D DFT, y complex k-space [batch][H][W][2] (re, im),
+ *            grad = Re F^-1 M (M F x - y) (l.969), prox = Re F^-1[(F v + tau M y) /
+ *            (1 + tau M)] (l.985 in k-space, reading Q18); masks: HOST u8 [H][W]
+ *            k-space mask shared by the batch, Hermitian-symmetric (M[-ky][-kx] =
+ *            M[ky][kx], reading R7; otherwise IDEQ_E_INVALID); C = 1, power-of-two H, W.
  *   RICIAN : f = sum x^2/(2 sigma^2) - log I0(x y / sigma^2) (App. D.3.3, l.1071),
  *            grad = x/sigma^2 - (y/sigma^2) B(x y/sigma^2), B = I1/I0 (l.1075);
  *            gradient step only (no closed-form prox, l.1079); sigma > 0.

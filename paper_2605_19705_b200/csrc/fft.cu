@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
 //   op 0: multiply by the real diagonal dgl[ky][kx] = 1 / (1 + tau |K^|^2)   (prox)
 //   op 1: multiply by conj(K^[ky][kx])                                     (A^T)
 //   op 2: forward only (no inverse): used to build K^ itself
+//   op 3: inverse only (the half spectrum is already in k-space: MRI A^T y)
 constexpr int FFT_CPB = 8;  // columns per block in column passes
 
 __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
@@ -153,8 +154,16 @@ __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
   }
   __syncthreads();
   float2* d = cols + cc * H;
-  fft_row(d, tw, H, logH, t, tpc, false);
   const int kx = kx0 + cc;
+  if (op == 3) {  // loaded bit-reversed: straight into the inverse transform
+    fft_row(d, tw, H, logH, t, tpc, true);
+    for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
+      const int h = q / FFT_CPB, j = q % FFT_CPB;
+      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+    }
+    return;
+  }
+  fft_row(d, tw, H, logH, t, tpc, false);
   if (op == 2) {
     for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
       const int h = q / FFT_CPB, j = q % FFT_CPB;
@@ -237,6 +246,34 @@ __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs 
 // is X[ky][kx], kx <= W/2. For the inverse row pass of row ky we need X'[ky][kx] for
 // all kx of the *column-inverted* data, which is the row spectrum of a real row, hence
 // Hermitian in kx: X'[ky][W-kx] = conj(X'[ky][kx]).
+
+// ================================================================== MRI (App. D.3.1)
+// Half spectrum of the Hermitian part of M y, scaled: spec[ky][kx] = scale * M[ky][kx] *
+// (y[ky][kx] + conj(y[-ky][-kx])) / 2, kx <= W/2. With a Hermitian-symmetric mask, the real part
+// of F^-1(M y) is F^-1 of this Hermitian array (reading R7), i.e. a C2R transform of the half plane.
+__global__ void mri_fill_kernel(const float* __restrict__ y, const uint8_t* __restrict__ kmask, float2* __restrict__ spec,
+                                int H, int W, float scale) {
+  const int Wh = W / 2 + 1;
+  const int n = blockIdx.y;
+  const float2* yc = reinterpret_cast<const float2*>(y) + (long long)n * H * W;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < H * Wh; e += gridDim.x * blockDim.x) {
+    const int ky = e / Wh, kx = e % Wh;
+    const float m = (float)kmask[ky * W + kx];
+    const float2 a = yc[ky * W + kx];
+    const float2 b = yc[((H - ky) % H) * W + (W - kx) % W];
+    spec[(long long)n * H * Wh + e] = make_float2(0.5f * scale * m * (a.x + b.x), 0.5f * scale * m * (a.y - b.y));
+  }
+}
+// mhalf = M on the half plane (gradient pass), dgl = 1 / (1 + tau M) (prox pass)
+__global__ void mri_masks_kernel(const uint8_t* __restrict__ kmask, float* __restrict__ mhalf, float* __restrict__ dgl,
+                                 float tau, int H, int W) {
+  const int Wh = W / 2 + 1;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < H * Wh; e += gridDim.x * blockDim.x) {
+    const float m = (float)kmask[(e / Wh) * W + e % Wh];
+    mhalf[e] = m;
+    dgl[e] = 1.f / (1.f + tau * m);
+  }
+}
 
 // Embed the kernel: plane[(i-kc) mod H][(j-kc) mod W] = k[i][j] (tap (kc,kc) at the origin).
 // The runtime requires ksize <= min(H, W), so no two taps share a bin.
@@ -424,6 +461,15 @@ void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int m
 void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s) {
   cudaMemsetAsync(plane, 0, sizeof(float) * H * W, s);
   embed_kernel_kernel<<<(ks * ks + 255) / 256, 256, 0, s>>>(k, ks, plane, H, W);
+}
+void launch_mri_fill(const float* y, const uint8_t* kmask, float2* spec, int N, int H, int W, float scale,
+                     cudaStream_t s) {
+  const int n = H * (W / 2 + 1);
+  mri_fill_kernel<<<dim3((n + 255) / 256, N), 256, 0, s>>>(y, kmask, spec, H, W, scale);
+}
+void launch_mri_masks(const uint8_t* kmask, float* mhalf, float* dgl, float tau, int H, int W, cudaStream_t s) {
+  const int n = H * (W / 2 + 1);
+  mri_masks_kernel<<<(n + 255) / 256, 256, 0, s>>>(kmask, mhalf, dgl, tau, H, W);
 }
 void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStream_t s) {
   blur_diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(khat, tau, dgl, n);

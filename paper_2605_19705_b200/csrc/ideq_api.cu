@@ -132,6 +132,8 @@ struct ideq_ctx {
   int op_batch = 0;
   float* d_kern = nullptr;
   uint8_t* d_mask = nullptr;
+  uint8_t* d_kmask = nullptr;  // MRI k-space mask [H][W]
+  float* mhalf = nullptr;      // MRI mask on the half spectrum [H][W/2+1]
   float* d_phase = nullptr;
   // FFT operators
   float2* tw_h = nullptr;
@@ -847,7 +849,8 @@ FftArgs make_fft_args(ideq_ctx* ctx, const float* y, const ideq_params* p) {
 int step_parts(ideq_ctx* ctx) {
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.blur_impl == IDEQ_BLUR_DIRECT && ctx->op.step == IDEQ_STEP_GRAD)
     return blur_parts_per_image(ctx->C, ctx->H, ctx->W);
-  if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) return fft_parts_per_image(ctx->C, ctx->H, ctx->W);
+  if ((ctx->op.kind == IDEQ_OP_BLUR || ctx->op.kind == IDEQ_OP_MRI) && ctx->op.step == IDEQ_STEP_PROX)
+    return fft_parts_per_image(ctx->C, ctx->H, ctx->W);
   if (ctx->op.kind == IDEQ_OP_PHASE) return phase_parts_per_image(ctx->H, ctx->W);
   const long long d = (long long)ctx->C * ctx->H * ctx->W;
   long long parts = d / 4096;
@@ -867,7 +870,21 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
   } else if (op.kind == IDEQ_OP_RICIAN) {
     Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 6.0);
     launch_pointwise_step(STEP_GRAD_RICIAN, a, s);
-  } else if (op.kind == IDEQ_OP_BLUR && op.step == IDEQ_STEP_PROX) {
+  } else if (op.kind == IDEQ_OP_MRI && op.step == IDEQ_STEP_GRAD) {
+    // F^-1 M F z through the half-spectrum passes, then x^{k+1} = z - tau(grad f + lam grad g)
+    FftArgs f = make_fft_args(ctx, a.y, nullptr);
+    f.dgl = ctx->mhalf;
+    const double spec_b = (double)a.N * a.H * (a.W / 2 + 1) * 8.0;
+    {
+      Prof p(ctx, IDEQ_K_FIDELITY, 0, (double)a.N * a.d * 4.0 + 4.0 * spec_b);
+      StepArgs dummy{};
+      launch_blur_rows_fwd(f, ctx->Z, 0, a.N, s);
+      launch_blur_cols(f, 0, a.N, s);
+      launch_blur_rows_inv(f, dummy, ctx->fbuf, 0, a.N, s);
+    }
+    Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 8.0);
+    launch_pointwise_step(STEP_GRAD_MRI, a, s);
+  } else if ((op.kind == IDEQ_OP_BLUR || op.kind == IDEQ_OP_MRI) && op.step == IDEQ_STEP_PROX) {
     // x^{k+1} = F^-1[ F(z - tau lam grad g + tau A^T y) / (1 + tau |K^|^2) ]   (prox P:80-84)
     FftArgs f = make_fft_args(ctx, a.y, nullptr);
     f.tau = a.tau; f.lam = a.lam;
@@ -908,6 +925,18 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
 }
 
 // Per-solve operator constants: A^T y (FFT) and the diagonal 1 / (1 + tau |K^|^2).
+// MRI constants of a solve: fbuf2 = Re F^-1(M y) (the A^T y of the k-space prox and gradient),
+// mhalf = M and dgl = 1 / (1 + tau M) on the half spectrum.
+void prepare_mri(ideq_ctx* ctx, const float* y, float tau, int N) {
+  FftArgs f = make_fft_args(ctx, y, nullptr);
+  f.active = nullptr;
+  StepArgs dummy{};
+  launch_mri_fill(y, ctx->d_kmask, ctx->spec, N, ctx->H, ctx->W, sqrtf((float)ctx->H * (float)ctx->W), ctx->stream);
+  launch_blur_cols(f, 3, N, ctx->stream);
+  launch_blur_rows_inv(f, dummy, ctx->fbuf2, 0, N, ctx->stream);
+  launch_mri_masks(ctx->d_kmask, ctx->mhalf, ctx->dgl, tau, ctx->H, ctx->W, ctx->stream);
+}
+
 void prepare_blur_prox(ideq_ctx* ctx, const float* y, float tau, int N) {
   FftArgs f = make_fft_args(ctx, y, nullptr);
   f.active = nullptr;
@@ -1016,6 +1045,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if (f.parts > ctx->parts_cap) return fail(ctx, IDEQ_E_INVALID, "internal: partial buffer too small");
   launch_init_state(f, s);
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
+  if (ctx->op.kind == IDEQ_OP_MRI) prepare_mri(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
   const bool poll = p->tol > 0.f;
@@ -1343,6 +1373,22 @@ ideq_status ideq_set_operator(ideq_ctx* ctx, const ideq_operator_desc* op, int b
     CK(cudaMemcpy(p, op->phase_masks, n * 4, cudaMemcpyHostToDevice));
     ctx->d_phase = (float*)p;
     if ((st = setup_fft(ctx, (size_t)batch * op->n_phase * H * W))) return st;
+  } else if (op->kind == IDEQ_OP_MRI) {
+    if (ctx->C != 1) return fail(ctx, IDEQ_E_INVALID, "MRI needs C = 1 (real magnitude image, zero phase)");
+    if (!op->masks) return fail(ctx, IDEQ_E_INVALID, "MRI needs a k-space mask [H][W]");
+    for (int ky = 0; ky < H; ++ky)  // reading R7: the k-space prox is the real-image prox only then
+      for (int kx = 0; kx < W; ++kx)
+        if ((op->masks[ky * W + kx] != 0) != (op->masks[((H - ky) % H) * W + (W - kx) % W] != 0))
+          return fail(ctx, IDEQ_E_INVALID, "MRI mask must be Hermitian-symmetric (M[-ky][-kx] == M[ky][kx])");
+    void* p;
+    if ((st = dalloc(ctx, &p, (size_t)H * W))) return st;
+    CK(cudaMemcpy(p, op->masks, (size_t)H * W, cudaMemcpyHostToDevice));
+    ctx->d_kmask = (uint8_t*)p;
+    if ((st = setup_fft(ctx, (size_t)batch * H * (W / 2 + 1)))) return st;
+    if ((st = dalloc(ctx, &p, sizeof(float) * H * (W / 2 + 1)))) return st;
+    ctx->mhalf = (float*)p;
+    if ((st = dalloc(ctx, &p, sizeof(float) * H * (W / 2 + 1)))) return st;
+    ctx->dgl = (float*)p;
   } else if (op->kind == IDEQ_OP_RICIAN) {
     if (op->step == IDEQ_STEP_PROX) return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form Rician prox (PAPER l.1079)");
     if (!(op->sigma > 0.f)) return fail(ctx, IDEQ_E_INVALID, "Rician sigma must be > 0");
@@ -1372,7 +1418,9 @@ ideq_status ideq_solve_host(ideq_ctx* ctx, const float* y, float* x_inout, int b
   if ((st = check_ctx(ctx))) return st;
   if (!y || !x_inout) return fail(ctx, IDEQ_E_INVALID, "NULL y/x");
   if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch out of range");
-  const size_t cy = ctx->op_set && ctx->op.kind == IDEQ_OP_PHASE ? (size_t)ctx->op.n_phase : (size_t)ctx->C;
+  const size_t cy = !ctx->op_set ? (size_t)ctx->C
+                    : ctx->op.kind == IDEQ_OP_PHASE ? (size_t)ctx->op.n_phase
+                    : ctx->op.kind == IDEQ_OP_MRI ? (size_t)2 : (size_t)ctx->C;  // MRI: complex k-space
   const size_t ny = (size_t)batch * cy * ctx->H * ctx->W, nx = (size_t)batch * ctx->C * ctx->H * ctx->W;
   if (ny > ctx->dstage_y_n) {
     void* p2;
@@ -1422,6 +1470,16 @@ ideq_status ideq_fidelity_grad(ideq_ctx* ctx, const float* y, const float* x, fl
   const auto& op = ctx->op;
   if (op.kind == IDEQ_OP_INPAINT) {
     launch_inpaint_grad(x, y, ctx->d_mask, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
+  } else if (op.kind == IDEQ_OP_MRI) {
+    prepare_mri(ctx, y, 1.f, batch);
+    FftArgs f = make_fft_args(ctx, y, nullptr);
+    f.dgl = ctx->mhalf;
+    f.active = nullptr;
+    StepArgs dummy{};
+    launch_blur_rows_fwd(f, x, 0, batch, ctx->stream);
+    launch_blur_cols(f, 0, batch, ctx->stream);
+    launch_blur_rows_inv(f, dummy, ctx->fbuf, 0, batch, ctx->stream);
+    launch_sub(ctx->fbuf, ctx->fbuf2, out, (long long)batch * ctx->H * ctx->W, ctx->stream);
   } else if (op.kind == IDEQ_OP_RICIAN) {
     launch_rician_grad(x, y, 1.f / (op.sigma * op.sigma), out, (long long)batch * ctx->C * ctx->H * ctx->W,
                        ctx->stream);
@@ -1455,6 +1513,15 @@ ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, fl
   if (!y || !v || !out || batch < 1 || batch > ctx->op_batch || !(tau > 0.f)) return fail(ctx, IDEQ_E_INVALID, "bad arguments");
   if (ctx->op.kind == IDEQ_OP_INPAINT) {
     launch_inpaint_prox(v, y, ctx->d_mask, tau, out, batch, ctx->C, ctx->H, ctx->W, ctx->stream);
+  } else if (ctx->op.kind == IDEQ_OP_MRI) {
+    prepare_mri(ctx, y, tau, batch);
+    FftArgs f = make_fft_args(ctx, y, nullptr);
+    f.z = v; f.gg = v; f.lam = 0.f; f.tau = tau;
+    f.active = nullptr;
+    StepArgs dummy{};
+    launch_blur_rows_fwd(f, nullptr, 1, batch, ctx->stream);
+    launch_blur_cols(f, 0, batch, ctx->stream);
+    launch_blur_rows_inv(f, dummy, out, 0, batch, ctx->stream);
   } else if (ctx->op.kind == IDEQ_OP_PHASE || ctx->op.kind == IDEQ_OP_RICIAN) {
     return fail(ctx, IDEQ_E_UNSUPPORTED, "no closed-form prox for phase retrieval / Rician (PAPER l.1079)");
   } else if (ctx->op.blur_impl == IDEQ_BLUR_FFT) {

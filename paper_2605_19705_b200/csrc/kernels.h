@@ -7,7 +7,7 @@
 
 namespace ideq {
 
-enum StepMode : int { STEP_PROX_INPAINT = 0, STEP_GRAD_BUF = 1, STEP_GRAD_INPAINT = 2, STEP_X1_BUF = 3, STEP_GRAD_RICIAN = 4 };
+enum StepMode : int { STEP_PROX_INPAINT = 0, STEP_GRAD_BUF = 1, STEP_GRAD_INPAINT = 2, STEP_X1_BUF = 3, STEP_GRAD_RICIAN = 4, STEP_GRAD_MRI = 5 };
 
 struct StepArgs {
   int N, C, H, W;
@@ -109,6 +109,10 @@ void launch_advance_b(const FinalizeArgs& f, cudaStream_t s);
 void launch_init_state(const FinalizeArgs& f, cudaStream_t s);
 void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s);
 void launch_post_step(const PostArgs& a, cudaStream_t s);
+void launch_mri_fill(const float* y, const uint8_t* kmask, float2* spec, int N, int H, int W, float scale,
+                     cudaStream_t s);
+void launch_mri_masks(const uint8_t* kmask, float* mhalf, float* dgl, float tau, int H, int W, cudaStream_t s);
+void launch_sub(const float* a, const float* b, float* out, long long n, cudaStream_t s);
 void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s);
 void launch_avg_out(const int* k0, const int* status, const int* iters, int K, const float* Xsnap, float* X, int N,
                     long long d, cudaStream_t s);

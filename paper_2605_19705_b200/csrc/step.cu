@@ -80,6 +80,17 @@ __global__ void __launch_bounds__(256) rician_grad_kernel(const float* __restric
     out[i] = rician_grad_f(x[i], y[i], inv_s2);
 }
 
+__global__ void sub_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
+                           long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+void launch_sub(const float* a, const float* b, float* out, long long n, cudaStream_t s) {
+  long long g = (n + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  sub_kernel<<<(unsigned)g, 256, 0, s>>>(a, b, out, n);
+}
+
 void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s) {
   long long b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
@@ -115,6 +126,9 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
     } else if (MODE == STEP_GRAD_BUF) {
       // x = z - tau (grad f + lam grad g), grad f precomputed in a.fbuf
       x1 = z - a.tau * (a.fbuf[i] + a.lam * gg);
+    } else if (MODE == STEP_GRAD_MRI) {
+      // grad f = Re F^-1 M (M F z - y) = fbuf - fbuf2 with fbuf = F^-1 M F z, fbuf2 = Re F^-1 M y
+      x1 = z - a.tau * (a.fbuf[i] - a.fbuf2[i] + a.lam * gg);                   // Alg. 1 l.8
     } else if (MODE == STEP_GRAD_RICIAN) {
       x1 = z - a.tau * (rician_grad_f(z, a.y[i], a.inv_s2) + a.lam * gg);   // Alg. 1 l.8
     } else if (MODE == STEP_GRAD_INPAINT) {
@@ -444,6 +458,7 @@ void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
     case STEP_GRAD_BUF: pointwise_step_kernel<STEP_GRAD_BUF><<<grid, 256, 0, s>>>(a); break;
     case STEP_GRAD_INPAINT: pointwise_step_kernel<STEP_GRAD_INPAINT><<<grid, 256, 0, s>>>(a); break;
     case STEP_GRAD_RICIAN: pointwise_step_kernel<STEP_GRAD_RICIAN><<<grid, 256, 0, s>>>(a); break;
+    case STEP_GRAD_MRI: pointwise_step_kernel<STEP_GRAD_MRI><<<grid, 256, 0, s>>>(a); break;
     default: pointwise_step_kernel<STEP_X1_BUF><<<grid, 256, 0, s>>>(a); break;
   }
 }

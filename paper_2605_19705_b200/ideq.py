@@ -20,7 +20,7 @@ STATUS_NAMES = ["OK", "INVALID", "DIVERGED", "UNSUPPORTED", "CUDA", "NCCL", "NOM
 PREC = {"fp32": 0, "bf16": 1}
 ARCH = {"tiny3": 0, "unet4": 1}
 ACT = {"softplus": 0, "identity": 1}
-OP = {"blur": 0, "inpaint": 1, "phase": 2, "rician": 3}
+OP = {"blur": 0, "inpaint": 1, "phase": 2, "rician": 3, "mri": 4}
 STEP = {"grad": 0, "prox": 1}
 BLUR = {"direct": 0, "fft": 1}
 STOP = {"per_image": 0, "global_max": 1}
@@ -209,6 +209,10 @@ class Solver:
             self._keep.append(m)
         elif cfg["op"] == "rician":
             op.sigma = float(cfg["sigma"])
+        elif cfg["op"] == "mri":
+            m = np.ascontiguousarray(prob["kmask"], dtype=np.uint8)
+            op.masks = m.ctypes.data_as(C.POINTER(C.c_ubyte))
+            self._keep.append(m)
         else:
             d = np.ascontiguousarray(prob["phase_masks"], dtype=np.float32)
             op.n_phase = d.shape[0]
