@@ -221,6 +221,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait: several loads in flight, then one tcgen05.wait::ld (tmem_wait)
+__device__ __forceinline__ void tmem_ld16_nw(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
   uint32_t r[16];
   asm volatile(
@@ -324,6 +335,11 @@ struct TcParams {
   int img_c;
   FastDiv fd_ntiles, fd_perimg, fd_tw;  // tile index -> (m tile, n tile), (image, row tile, col tile)
   int slab_mode;                        // 1: each TMEM lane quadrant stores its own 32-row slab
+  // MODE 4 (taps in N): a job is R full image rows (R*W = 128*T pixels, T = 1 or 2 M tiles);
+  // row_blk[s] = first of the 3 resident weight blocks of row shift dh = s - 1 (dw ascending,
+  // or descending when dw_desc); the MMA N is 3*BN and each TMEM stage holds T*3*BN columns
+  int row_T, row_blk[3], dw_desc;
+  uint32_t acc_cols;
 };
 
 // tile t -> (image, output row h0, output col w0, n tile)
@@ -341,7 +357,7 @@ __device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t, int pair
   return r;
 }
 
-constexpr int TC_THREADS = 320;  // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int TC_THREADS = 352;  // warp 0 TMA operands, warp 1 MMA, warps 2..9 epilogue, warp 10 TMA aux
 
 // Epilogue boxes are BOXC = min(BN, 64) columns wide: 128-byte rows (SW128) for 64 columns,
 // 64-byte rows (SW64) for 32. A thread owns one pixel row; 16-byte chunk j of row r lives at
@@ -369,6 +385,10 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
 // crosses L2 ~1.4x (2D) / ~3x (1-row) instead of 9x. MODE 1 keeps the layer's weights resident
 // in shared memory for the CTA's lifetime; MODE 2 streams them per (chunk, tap) through a second
 // ring (layers whose weights do not fit).
+// MODE 4 (taps in N, full image rows): the three horizontal taps of a row shift become N columns
+// (N = 3 * Cout, one MMA per row shift and K step, A read 3x less from shared memory) and the
+// epilogue adds the dw = -1 / +1 partial products of the neighbouring pixels (warp shuffles plus a
+// cross-warp exchange through shared memory; zero at the row ends = the conv's zero padding).
 template <int KC, int EPI, int BOXC, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -384,9 +404,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   // MODE 3 = MODE 2 on a CTA pair (cta_group::2, M = 256): each CTA holds its own 128-row A tile
   // and HALF of every weight box (BN / 2 rows); the leader CTA issues the M256 x BN MMAs
   constexpr bool PAIR = MODE == 3;
-  constexpr bool STREAMB = MODE >= 2;
+  constexpr bool STREAMB = MODE == 2 || MODE == 3;
   const uint32_t b_stage = (uint32_t)(PAIR ? BN / 2 : BN) * KC * 2u;
-  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
+  constexpr bool ROW = MODE == 4;
+  const int RT = ROW ? P.row_T : 1;                             // M tiles per job
+  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u * (uint32_t)RT;  // BN/BOXC boxes of 128*RT x BOXC
   const ConvGeom& g = P.g;
   const int nkb = g.ntaps * g.nchunk;
   constexpr bool HALO = MODE != 0;
@@ -396,11 +418,12 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   // MODE 0: [A stages][B stages][epi]; MODE 1: [resident W (nkb B boxes)][halo stages][epi];
   // MODE 2: [halo stages][B ring][epi]
   const uint32_t sW = base;
-  const uint32_t sA = MODE == 1 ? sW + (uint32_t)nkb * b_stage : base;
+  const uint32_t sA = (MODE == 1 || ROW) ? sW + (uint32_t)nkb * b_stage : base;
   const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
-  const uint32_t sE = MODE == 1 ? sB : sB + (STREAMB ? SB : S) * b_stage;
+  const uint32_t sE = (MODE == 1 || ROW) ? sB : sB + (STREAMB ? SB : S) * b_stage;
   const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
-  const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
+  const uint32_t sX = sE + (uint32_t)NA * epi_stage;  // ROW: neighbour exchange [2 halves][2 par][2 chunk][T][4 q][2][16] fp32
+  const uint32_t sBar = sX + (ROW ? 8192u : 0u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
   // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB], emptyB[SB]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1 + 2 * SB);
@@ -467,7 +490,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
-    if (MODE == 1) {  // resident weights: every K-block of the (single) N tile, once per CTA
+    if (MODE == 1 || ROW) {  // resident weights: every K-block of the (single) N tile, once per CTA
       if (elect_one()) {
         mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
         for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
@@ -477,10 +500,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     for (int t = t0; t < total; t += tstep) {
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
-      // the aux tile goes into this tile's epilogue buffer; it is requested after the first
-      // min(S, loads) operand stages so waiting for the buffer never starves the MMA warp
       const int nload = HALO ? g.nchunk : nkb;
-      const int kb_aux = (S < nload ? S : nload) - 1;
       for (int kb = 0; kb < nload; ++kb) {
         mbar_wait(empty0 + 8u * s, ph ^ 1u);
         if (elect_one()) {
@@ -495,6 +515,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                                tap * g.nchunk + kb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
             }
+          } else if (ROW) {  // (R + 2) full rows, no horizontal halo
+            mbar_expect_tx(full0 + 8u * s, P.a_bytes);
+            tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, 0, 0, h0 - 1, img);
           } else if (HALO) {
             mbar_expect_tx(full0 + 8u * s, P.a_bytes);
             tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
@@ -516,20 +539,30 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         }
         __syncwarp();
         if (++s == S) { s = 0; ph ^= 1u; }
-        if (HAS_AUX && kb == kb_aux) {
-          mbar_wait(epifree0 + 8u * acc, aph ^ 1u);  // previous store from this buffer has drained
-          if (elect_one()) {
-            mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
-            for (int b = 0; b < nbox; ++b) {
-              const int col = nt * BN + b * BOXC;
-              tma_load_5d(sE + acc * epi_stage + b * P.epi_box_bytes, &tmAux, auxfull0 + 8u * acc, col % g.CB, w0,
-                          col / g.CB, h0, img);
-            }
-          }
-          __syncwarp();
-        }
       }
       if (++acc == NA) { acc = 0; aph ^= 1u; }
+    }
+  } else if (warp == 10) {
+    // ---------------- aux producer: the epilogue's second operand (residual / saved activation)
+    // goes into the tile's epilogue buffer as soon as that buffer's previous store has been read,
+    // without ever stalling the operand producer behind the epilogue
+    if (HAS_AUX) {
+      int acc = 0;
+      uint32_t aph = 0;
+      for (int t = t0; t < total; t += tstep) {
+        const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+        mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
+        if (elect_one()) {
+          mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
+          for (int b = 0; b < nbox; ++b) {
+            const int col = ti.nt * BN + b * BOXC;
+            tma_load_5d(sE + acc * epi_stage + b * P.epi_box_bytes, &tmAux, auxfull0 + 8u * acc, col % g.CB, ti.w0,
+                        col / g.CB, ti.h0, ti.img);
+          }
+        }
+        __syncwarp();
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
+      }
     }
   } else if (warp == 1 && leader) {
     // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform descriptors
@@ -543,20 +576,38 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
     // halo tiles: 8-row core groups of A are 8 pixels of one row (R = 1) or one 8-pixel row of a
     // 16 x 8 tile, i.e. (Wt + 2) pixel rows apart inside the halo box
-    const uint32_t sboA = HALO ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
+    const uint32_t sboA = (HALO && !ROW) ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
     const uint64_t dA0 = make_sdesc(sA, sboA, layout);
-    const uint64_t dB0 = make_sdesc(MODE == 1 ? sW : sB, sbo, layout);
+    const uint64_t dB0 = make_sdesc((MODE == 1 || ROW) ? sW : sB, sbo, layout);
+    const uint32_t idesc3 = make_idesc_bf16(3 * BN);  // ROW: N = 3 taps x Cout
     int s = 0, sb = 0;
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
-    if (MODE == 1) mbar_wait(wfull, 0);
+    if (MODE == 1 || ROW) mbar_wait(wfull, 0);
     const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
     for (int t = t0; t < total; t += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
-      if (HALO) {
+      const uint32_t d_tmem = tmem_base + (ROW ? (uint32_t)acc * P.acc_cols : (uint32_t)(acc * BN));
+      if (ROW) {
+        // one halo buffer of R + 2 full rows; per M tile and row shift: N = 3 * BN MMAs
+        mbar_wait(full0 + 8u * s, ph);
+        tc_fence_after();
+        const uint64_t dh = dA0 + ((s * P.halo_stage) >> 4);
+        for (int tau = 0; tau < RT; ++tau) {
+          for (int sh = 0; sh < 3; ++sh) {
+            const uint32_t p0 = (uint32_t)(sh * g.OW + tau * 128);
+            const uint64_t ad = dh + ((p0 * hrow) >> 4);
+            const uint64_t bd = dB0 + (((uint32_t)P.row_blk[sh] * b_stage) >> 4);
+#pragma unroll
+            for (int k = 0; k < KC / 16; ++k)
+              mma_bf16_elect(d_tmem + (uint32_t)(tau * 3 * BN), ad + 2u * k, bd + 2u * k, idesc3, (sh | k) ? 1u : 0u);
+          }
+        }
+        mma_commit_elect(empty0 + 8u * s);
+        if (++s == S) { s = 0; ph ^= 1u; }
+      } else if (HALO) {
         for (int ch = 0; ch < g.nchunk; ++ch) {
           mbar_wait(full0 + 8u * s, ph);
           tc_fence_after();
@@ -604,7 +655,147 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       else mma_commit_elect(tfull0 + 8u * acc);
       if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
-  } else if (warp >= 2) {
+  } else if (ROW && warp >= 2 && warp < 10) {
+    // ---------------- MODE 4 epilogue: out[p] = Q_{-1}[p-1] + Q_0[p] + Q_{+1}[p+1] with Q_dw the
+    // TMEM column block of tap dw; neighbours inside a warp by shuffles, across the warps of a
+    // column half through shared memory (one 128-thread named barrier per 16-column chunk)
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const bool qleader = (half == 0 && lane == 0);
+    const uint32_t rowbytes = (uint32_t)BOXC * 2u;
+    const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
+    const int Wimg = g.OW;
+    const int blkL = P.dw_desc ? 2 : 0, blkR = P.dw_desc ? 0 : 2;  // TMEM blocks of dw = -1 / +1
+    float* xbase = reinterpret_cast<float*>(gbase + (sX - base));
+    int acc = 0, prev_acc = -1, jpar = 0;
+    uint32_t aph = 0;
+    for (int t = t0; t < total; t += tstep) {
+      const TileIdx ti = tile_index(P, t);
+      const int img = ti.img, h0 = ti.h0;
+      const uint32_t ebuf = sE + acc * epi_stage;
+      if (HAS_AUX) {
+        mbar_wait(auxfull0 + 8u * acc, aph);
+      } else {
+        mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
+      }
+      mbar_wait(tfull0 + 8u * acc, aph);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * P.acc_cols;
+      int ci = 0;
+#pragma unroll 1
+      for (int c0 = cbeg; c0 < cend; c0 += 16, ++ci) {
+        // exchange slots of (half, job parity, chunk): [tau][quad][side][16]
+        float* xs = xbase + (((half * 2 + jpar) * 2 + ci) * 2) * 4 * 2 * 16;
+#pragma unroll 1
+        for (int tau = 0; tau < RT; ++tau) {  // pass 1: publish the warp's boundary partial products
+          uint32_t pl[16], pr[16];
+          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkL * BN + c0), pl);
+          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkR * BN + c0), pr);
+          tmem_wait();
+          float* xq = xs + (tau * 4 + quad) * 2 * 16;
+          if (lane == 31) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xq[e] = __uint_as_float(pl[e]);
+          }
+          if (lane == 0) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xq[16 + e] = __uint_as_float(pr[e]);
+          }
+        }
+        if (half == 0) asm volatile("bar.sync 6, 128;" ::: "memory");
+        else asm volatile("bar.sync 7, 128;" ::: "memory");
+#pragma unroll 1
+        for (int tau = 0; tau < RT; ++tau) {  // pass 2: combine and apply the fused epilogue
+          uint32_t plu[16], pcu[16], pru[16];
+          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkL * BN + c0), plu);
+          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + BN + c0), pcu);
+          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkR * BN + c0), pru);
+          tmem_wait();
+          float pl[16], pc[16], pr[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            pl[e] = __uint_as_float(plu[e]);
+            pc[e] = __uint_as_float(pcu[e]);
+            pr[e] = __uint_as_float(pru[e]);
+          }
+          const int pix = tau * 128 + quad * 32 + lane;
+          const int col = pix % Wimg;
+          const float* xl = (quad > 0) ? xs + (tau * 4 + quad - 1) * 2 * 16 : (tau > 0 ? xs + ((tau - 1) * 4 + 3) * 2 * 16 : nullptr);
+          const float* xr = (quad < 3) ? xs + (tau * 4 + quad + 1) * 2 * 16 + 16
+                                       : (tau + 1 < RT ? xs + ((tau + 1) * 4) * 2 * 16 + 16 : nullptr);
+          float v[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float left = __shfl_up_sync(0xffffffffu, pl[e], 1);
+            float right = __shfl_down_sync(0xffffffffu, pr[e], 1);
+            if (lane == 0) left = xl ? xl[e] : 0.f;
+            if (lane == 31) right = xr ? xr[e] : 0.f;
+            if (col == 0) left = 0.f;
+            if (col == Wimg - 1) right = 0.f;
+            v[e] = left + pc[e] + right;
+          }
+          const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
+          const int j0 = (c0 % BOXC) / 8;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const uint32_t a = epi_chunk_addr<BOXC>(box, pix, j0 + q);
+            float o[8];
+            if (HAS_AUX) {
+              const uint4 u = ld_shared_v4(a);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                if (EPI == EPI_RESADD) {
+                  o[2 * e] = v[q * 8 + 2 * e] + f.x;
+                  o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
+                } else {
+                  o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast<false>(f.x);
+                  o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast<false>(f.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v[q * 8 + e]) : v[q * 8 + e];
+            }
+            uint4 w;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+            st_shared_v4(a, w);
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+      fence_async_smem();
+      pair_bar(quad);
+      if (qleader) {
+        for (int tau = 0; tau < RT; ++tau) {
+          const int p0 = tau * 128 + quad * 32;
+          for (int b = 0; b < nbox; ++b) {
+            const int colg = b * BOXC;
+            tma_store_5d(&tmSlab, ebuf + b * P.epi_box_bytes + (uint32_t)p0 * rowbytes, colg % g.CB, p0 % Wimg,
+                         colg / g.CB, h0 + p0 / Wimg, img);
+          }
+        }
+        bulk_commit();
+        if (prev_acc >= 0) {
+          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          mbar_arrive(epifree0 + 8u * prev_acc);
+        }
+        prev_acc = acc;
+      }
+      jpar ^= 1;
+      if (++acc == NA) { acc = 0; aph ^= 1u; }
+    }
+    if (qleader) {
+      bulk_wait0();
+      if (prev_acc >= 0) mbar_arrive(epifree0 + 8u * prev_acc);
+    }
+  } else if (warp >= 2 && warp < 10) {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
     // thread; the two warps of a quadrant split the tile's columns in halves. Each quadrant
     // publishes its own 32-row slab (pair barrier of 64 threads + one TMA store per column box),
@@ -960,6 +1151,26 @@ bool tc_supported(const ConvGeom& g) {
   return true;
 }
 
+// MODE 4: the taps of each row shift dh = s - 1 must be three consecutive weight blocks with dw
+// ascending (-1, 0, +1) or, for every s, descending (the flipped adjoint weights).
+static bool row_taps(const ConvGeom& g, int blk[3], int& desc) {
+  desc = -1;
+  for (int sh = 0; sh < 3; ++sh) {
+    int t0 = -1;
+    for (int t = 0; t < 9; ++t)
+      if (g.dh[t] == sh - 1) { t0 = t; break; }
+    if (t0 < 0 || t0 + 2 >= 9) return false;
+    for (int j = 0; j < 3; ++j)
+      if (g.dh[t0 + j] != sh - 1) return false;
+    const int d = (g.dw[t0] == -1 && g.dw[t0 + 1] == 0 && g.dw[t0 + 2] == 1) ? 0
+                : (g.dw[t0] == 1 && g.dw[t0 + 1] == 0 && g.dw[t0 + 2] == -1) ? 1 : -1;
+    if (d < 0 || (desc >= 0 && d != desc)) return false;
+    desc = d;
+    blk[sh] = t0;
+  }
+  return true;
+}
+
 // Halo variants: 3x3 taps (|dh|,|dw| <= 1, no parity planes) on tiles whose 8-row core groups
 // sit at a uniform stride inside the halo box: 16 x 8 pixels (preferred: 1.4x halo) or one row of
 // 128 pixels. Returns 0 (plain), 1 (resident weights) or 2 (streamed weights) and the tile shape.
@@ -969,6 +1180,25 @@ static int tc_halo_mode(const ConvGeom& g, int& R, int& Wt) {
     if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return 0;
   const char* nh = getenv("IDEQ_NO_HALO");  // A/B switches for measurements
   if (nh && atoi(nh) != 0) return 0;
+  {  // MODE 4 (taps in N) on full image rows: Cout 32/64 in one N tile, one channel chunk.
+     // Opt-in (IDEQ_ROW=1): correct (tests/test_gpu_layers.py) but measured 2-3x SLOWER on B200
+     // than the 16x8 halo tiles -- the neighbour combine (two SHFL per output element on top of
+     // the softplus exponential) saturates the XU pipe (ncu: 140%), which the smem savings of the
+     // 3x-wider MMAs cannot repay.
+    const char* rw = getenv("IDEQ_ROW");
+    const char* nr = (rw && atoi(rw) != 0) ? nullptr : "1";
+    const int BN = tc_bn(g), W = g.OW;
+    const int T = W >= 128 ? W / 128 : 1;
+    const bool ok = !(nr && atoi(nr) != 0) && g.epi != EPI_IMG && g.nchunk == 1 && g.ncols == BN &&
+                    (BN == 32 || BN == 64) && (W == 32 || W == 64 || W == 128 || W == 256) &&
+                    (size_t)9 * BN * g.KC * 2 <= 80 * 1024 && 2 * T * 3 * BN <= 512;
+    int blk[3], desc;
+    if (ok && row_taps(g, blk, desc)) {
+      R = W >= 128 ? 1 : 128 / W;
+      Wt = W;
+      return 4;
+    }
+  }
   const char* n2 = getenv("IDEQ_NO_HALO2D");
   if (g.OW % 8 == 0 && !(n2 && atoi(n2) != 0)) { R = 16; Wt = 8; }
   else if (g.R == 1 && g.Wt == 128) { R = 1; Wt = 128; }
@@ -1023,8 +1253,9 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     g.tiles_h = (g.OH + g.R - 1) / g.R;
     g.tiles_w = (g.OW + g.Wt - 1) / g.Wt;
   }
-  CUresult r = p->halo ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
-                       : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
+  CUresult r = p->halo == 4 ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R + 2, swA)
+             : p->halo      ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
+                            : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
   {
     const int nkb = g.ntaps * g.nchunk;
@@ -1070,20 +1301,27 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.fd_tw.init((uint32_t)g.tiles_w);
   P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
   P.b_bytes = (uint32_t)g.KC * 2u * (p->halo == 3 ? BN / 2 : BN);  // PAIR: this CTA's half
-  P.epi_box_bytes = 128u * boxc * 2u;
+  const int rowT = p->halo == 4 ? (g.Wt * g.R) / 128 : 1;  // M tiles per MODE 4 job
+  P.epi_box_bytes = 128u * (uint32_t)rowT * boxc * 2u;
+  P.row_T = rowT;
+  if (p->halo == 4) {
+    row_taps(g, P.row_blk, P.dw_desc);
+    P.acc_cols = (uint32_t)(rowT * 3 * BN);
+  }
   P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
   // Shared-memory / TMEM plan. Preference order: 4 accumulator stages for narrow N (more tiles
   // in flight hide the per-tile epilogue latency), then 2 CTAs per SM, then deeper operand rings.
   const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)(p->halo == 3 ? BN / 2 : BN) * g.KC * 2u,
-               e_stage = (size_t)BN * 128u * 2u;
-  const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * b_stage : 0;
+               e_stage = (size_t)BN * 128u * 2u * rowT;
+  const size_t wbytes = (p->halo == 1 || p->halo == 4) ? (size_t)9 * g.nchunk * b_stage : 0;
   if (p->halo) {
-    P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
+    P.a_bytes = p->halo == 4 ? (uint32_t)g.KC * 2u * g.Wt * (g.R + 2) : (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
     P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
   }
+  const size_t xbytes = p->halo == 4 ? 8192 : 0;  // MODE 4 neighbour exchange
   // MODE 2: a weight ring of SB stages (one (chunk, tap) box each) next to the halo ring
   const int SBq = 6;
-  const bool streamb = p->halo >= 2;
+  const bool streamb = p->halo == 2 || p->halo == 3;
   const size_t bring = streamb ? (size_t)SBq * b_stage : 0;
   P.stagesB = streamb ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
@@ -1095,10 +1333,11 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   const int min_stages = p->halo ? 2 : (short_k ? 2 : 3), max_stages = p->halo ? 4 : (short_k ? 4 : 8);
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
-  for (int na = (BN <= 64 || short_k ? 4 : 2); na >= 2 && !stages; na -= 2) {
+  const uint32_t acc_w = p->halo == 4 ? P.acc_cols : (uint32_t)BN;  // TMEM columns per stage
+  for (int na = ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2); na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
-    while (tc < (uint32_t)na * BN) tc <<= 1;
-    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
+    while (tc < (uint32_t)na * acc_w) tc <<= 1;
+    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + xbytes + 512;
     for (int c = (p->halo == 3 ? 1 : 2); c >= 1 && !stages; --c) {  // a CTA pair: one CTA per SM
       const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
@@ -1111,7 +1350,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.stages = stages;
   P.nacc = nacc;
   P.tmem_cols = tcols;
-  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + 512 + (size_t)stages * op_stage;
+  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + xbytes + 512 + (size_t)stages * op_stage;
   if (p->halo == 3) {  // units of (2 M tiles, 1 N tile); two CTAs (one cluster) per unit
     const int units = ((P.m_tiles + 1) / 2) * P.n_tiles;
     const int maxu = num_sms / 2;
@@ -1131,6 +1370,9 @@ static void launch_one(const TcPlan* p, cudaStream_t s) {
                                                                         p->tmSlab, p->P);
   else if (p->halo == 2)
     conv_tc_kernel<KC, EPI, BOXC, 2><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
+                                                                        p->tmSlab, p->P);
+  else if (p->halo == 4)
+    conv_tc_kernel<KC, EPI, BOXC, 4><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
                                                                         p->tmSlab, p->P);
   else if (p->halo == 3) {  // CTA pairs: cluster of 2 on one TPC
     cudaLaunchConfig_t cfg = {};
@@ -1206,6 +1448,10 @@ void init_attrs_tc() {
   attrs_epi<64, 32, 2>();
   attrs_epi<32, 64, 2>();
   attrs_epi<32, 32, 2>();
+  attrs_epi<64, 64, 4>();
+  attrs_epi<64, 32, 4>();
+  attrs_epi<32, 64, 4>();
+  attrs_epi<32, 32, 4>();
   attrs_epi<64, 64, 3>();
   attrs_epi<64, 32, 3>();
   attrs_epi<32, 64, 3>();

@@ -112,3 +112,40 @@ def test_streamed_weight_layer_odd_tile_count(kind, cin, cout, N, H, W, epi, pai
     got = from_nhwc_dev(out)
     assert np.isfinite(got).all()
     assert rel_l2(got, ref) <= 8e-3
+
+
+ROW_CASES = []
+for kind in (0, 1):
+    for c, Ws in ((32, (32, 64, 128, 256)), (64, (32, 64, 128))):
+        for W in Ws:
+            for epi in (0, 1, 2, 3):
+                ROW_CASES.append((kind, c, W, epi))
+
+
+@pytest.mark.parametrize("kind,c,W,epi", ROW_CASES)
+def test_taps_in_n_row_layer(kind, c, W, epi, monkeypatch):
+    """MODE 4 (taps folded into N on full image rows, shuffle + exchange epilogue) for every
+    image width it serves, both conv directions and every fused epilogue, vs the oracle layer.
+    H = 11 is ragged for every row-group size. MODE 4 is opt-in (IDEQ_ROW=1)."""
+    monkeypatch.setenv("IDEQ_ROW", "1")
+    torch = torch_cuda()
+    from paper_2605_19705_b200 import ideq
+    rng = np.random.default_rng(1000 + kind * 100 + c + W + epi)
+    fn, wshape = KINDS[kind]
+    w = rng.standard_normal(wshape(c, c)) * np.sqrt(1.0 / (c * 4))
+    N, H = 2, 11
+    x = rng.standard_normal((N, c, H, W))
+    w32 = w.astype(np.float32)
+    xr, wr = bf16_round(x), bf16_round(w32)
+    ref_acc = np.stack([fn(xr[n], wr) for n in range(N)])
+    aux = auxr = None
+    if epi in (2, 3):
+        aux = rng.uniform(0.05, 2.0, ref_acc.shape) if epi == 3 else rng.standard_normal(ref_acc.shape)
+        auxr = bf16_round(aux)
+    ref = _epi_ref(ref_acc, epi, auxr)
+    out = torch.zeros((N, H, W, c), device="cuda", dtype=torch.bfloat16)
+    ideq.debug_conv(kind, "bf16", True, w32, N, H, W, nhwc_dev(x, "bf16"), out,
+                    nhwc_dev(aux, "bf16") if aux is not None else None, epi)
+    got = from_nhwc_dev(out)
+    assert np.isfinite(got).all()
+    assert rel_l2(got, ref) <= 8e-3, rel_l2(got, ref)
