@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
   const long long end = min(d, beg + chunk);
   const long long off = (long long)n * d;
   const long long HW = (long long)a.H * a.W;
+  const uint8_t* mrow = a.mask ? a.mask + (long long)n * HW : nullptr;
+  // pixel index within the channel plane, advanced incrementally (no 64-bit modulo per element)
+  uint32_t pix = (uint32_t)((beg + threadIdx.x) % HW);
   Partial3 acc{0.f, 0.f, 0.f};
   for (long long e = beg + threadIdx.x; e < end; e += blockDim.x) {
     const long long i = off + e;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
     float x1;
     if (MODE == STEP_PROX_INPAINT) {
       // v = z - tau lam grad g ; prox = (tau M y + v) / (tau M + 1)
-      const float m = (float)a.mask[(long long)n * HW + (e % HW)];
+      const float m = (float)mrow[pix];
       const float v = z - a.tau * a.lam * gg;
       x1 = (a.tau * m * a.y[i] + v) / (a.tau * m + 1.f);
     } else if (MODE == STEP_GRAD_BUF) {
@@ -132,12 +135,14 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
     } else if (MODE == STEP_GRAD_RICIAN) {
       x1 = z - a.tau * (rician_grad_f(z, a.y[i], a.inv_s2) + a.lam * gg);   // Alg. 1 l.8
     } else if (MODE == STEP_GRAD_INPAINT) {
-      const float m = (float)a.mask[(long long)n * HW + (e % HW)];
+      const float m = (float)mrow[pix];
       x1 = z - a.tau * (m * (m * z - a.y[i]) + a.lam * gg);
     } else {  // STEP_X1_BUF: x^{k+1} already computed (FFT prox output)
       x1 = a.fbuf[i];
     }
     tail_elem(x1, xk, a.beta, xn_base + i, a.zout + i, acc);
+    pix += blockDim.x;
+    while (pix >= (uint32_t)HW) pix -= (uint32_t)HW;
   }
   block_reduce_store(acc, a.partials + ((long long)n * a.parts + part) * 3);
 }
