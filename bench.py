@@ -164,11 +164,18 @@ def run_reference(args, cfg, rank, world):
 
 
 def _config_dict(cfg, per_rank, world):
-    return {"workload": f"{cfg['name']} (BASELINE config C3): {per_rank}x{cfg['C']}x{cfg['H']}x{cfg['W']} per GPU, "
-                        f"U-Net {'/'.join(map(str, cfg['widths']))}, inpainting prox, beta={cfg['beta']}",
+    opdesc = {"inpaint": f"{cfg['step']} inpainting (Bernoulli masks)",
+              "blur": f"{cfg['step']} periodic blur {cfg.get('ksize')}x{cfg.get('ksize')} ({cfg.get('blur_impl', 'direct')})",
+              "phase": f"{cfg.get('n_phase', 4)}-mask coded-diffraction phase retrieval (gradient)",
+              "rician": "Rician denoising (gradient)", "mri": f"x{cfg.get('accel')} Cartesian MRI ({cfg['step']})"}[cfg["op"]]
+    net = f"U-Net {'/'.join(map(str, cfg['widths']))}" if cfg["net"] == "unet4" else "tiny3"
+    tag = cfg["name"].split()[0]
+    return {"workload": f"{cfg['name']} (BASELINE config {tag}): {per_rank}x{cfg['C']}x{cfg['H']}x{cfg['W']} per GPU, "
+                        f"{net}, {opdesc}, beta={cfg['beta']}",
             "global_batch": per_rank * world, "per_gpu_batch": per_rank, "H": cfg["H"], "W": cfg["W"],
-            "C": cfg["C"], "net": f"unet4-{cfg['widths'][0]}", "parallelism": f"dp{world}",
-            "l2": "no flush: per-iteration working set (~1 GB saved activations + iterate planes) >> 126 MB L2",
+            "C": cfg["C"], "net": f"unet4-{cfg['widths'][0]}" if cfg["net"] == "unet4" else "tiny3",
+            "parallelism": f"dp{world}",
+            "l2": "no flush: per-iteration working set (saved activations + iterate planes) >> 126 MB L2",
             "timed": "one ideq_solve of K iterations, tol=0 (no early stop)"}
 
 
@@ -179,6 +186,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3")
+    ap.add_argument("--batch", type=int, default=0, help="images per GPU (default: the config's per-GPU batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tol-run", action="store_true",
                     help="skip the ms-to-tolerance solve (the metric's second half: tol = 1e-4, per-image stop)")
@@ -200,7 +208,9 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    per = cfg["batch"]
+    # per-GPU images: the config's batch, except C5 whose 512 images are sharded 64 per GPU at P = 8
+    # (its weak-scaling unit); --batch overrides
+    per = args.batch or (cfg["batch"] // 8 if args.config == "C5" else cfg["batch"])
     images = list(range(rank * per, (rank + 1) * per))
     prob = synth.make_problem(cfg, images=images)
     stream = torch.cuda.Stream()
