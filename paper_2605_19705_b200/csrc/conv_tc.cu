@@ -340,7 +340,17 @@ struct TcParams {
   // or descending when dw_desc); the MMA N is 3*BN and each TMEM stage holds T*3*BN columns
   int row_T, row_blk[3], dw_desc;
   uint32_t acc_cols;
+  // per-image active flags of the solver (null: compute every tile). Tiles of frozen images are
+  // skipped by every warp role alike, so the barrier rings stay in step (not used by CTA pairs).
+  const int* active;
 };
+
+// Frozen-image test on the shared bitmask, broadcast from lane 0 so that the compiler keeps the
+// warp roles' loops (descriptor math, ring indices) on the uniform datapath.
+__device__ __forceinline__ bool tile_frozen(const uint32_t* s_act, int img) {
+  const int bit = (int)((s_act[img >> 5] >> (img & 31)) & 1u);
+  return __shfl_sync(0xffffffffu, bit, 0) == 0;
+}
 
 // tile t -> (image, output row h0, output col w0, n tile)
 struct TileIdx { int img, h0, w0, nt; };
@@ -435,6 +445,19 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   // warp index broadcast from lane 0 so the compiler knows it is warp-uniform (uniform datapath)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+  // active-image bitmask (<= 1024 images), read once per CTA so the per-tile skip test is a
+  // shared-memory load instead of a dependent global load in every warp role's loop
+  // the flags are loaded here (up to 3 per thread) and folded into the bitmask after the barrier
+  // and TMEM set-up below, so the load latency hides behind the prologue
+  __shared__ uint32_t s_act[32];
+  int actf[3] = {0, 0, 0};
+  if (P.active) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int i = (warp + r * (TC_THREADS / 32)) * 32 + lane;
+      if (i < g.N && i < 1024) actf[r] = P.active[i];
+    }
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
@@ -465,6 +488,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                    "r"(P.tmem_cols)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
+  if (P.active) {  // one ballot per warp and 32-image word
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int w = warp + r * (TC_THREADS / 32);
+      const uint32_t bits = __ballot_sync(0xffffffffu, actf[r] != 0);
+      if (lane == 0 && w < 32 && w * 32 < g.N) s_act[w] = bits;
     }
   }
   tc_fence_before();
@@ -499,6 +530,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
     for (int t = t0; t < total; t += tstep) {
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+      if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const int nload = HALO ? g.nchunk : nkb;
       for (int kb = 0; kb < nload; ++kb) {
@@ -551,6 +583,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       uint32_t aph = 0;
       for (int t = t0; t < total; t += tstep) {
         const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+        if (P.active && tile_frozen(s_act, ti.img)) continue;
         mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
         if (elect_one()) {
           mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
@@ -587,6 +620,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     if (MODE == 1 || ROW) mbar_wait(wfull, 0);
     const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
     for (int t = t0; t < total; t += tstep) {
+      if (P.active && tile_frozen(s_act, tile_index(P, t).img)) continue;
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (ROW ? (uint32_t)acc * P.acc_cols : (uint32_t)(acc * BN));
@@ -671,6 +705,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t aph = 0;
     for (int t = t0; t < total; t += tstep) {
       const TileIdx ti = tile_index(P, t);
+      if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0;
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
@@ -818,6 +853,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t aph = 0;
     for (int t = t0; t < total; t += tstep) {
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+      if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
@@ -1130,6 +1166,7 @@ static EncodeTiledFn get_encode() {
 }
 
 struct TcPlan {
+  const int* active_ptr;  // the solver's per-image active flags (tile skipping)
   CUtensorMap tmA, tmB, tmOut, tmAux, tmSlab;
   TcParams P;
   int KC, epi, boxc, grid, halo;
@@ -1404,6 +1441,17 @@ static void launch_epi(const TcPlan* p, cudaStream_t s) {
     default: launch_one<KC, EPI_STORE, BOXC>(p, s); break;
   }
 }
+
+void tc_plan_set_active(TcPlan* p, const int* active) {
+  // a CTA pair must walk the same units; the in-kernel bitmask covers 1024 images
+  const char* ns = getenv("IDEQ_NO_SKIP");  // A/B switch for measurements
+  p->active_ptr = (p->halo == 3 || p->P.g.N > 1024 || (ns && atoi(ns) != 0)) ? nullptr : active;
+  p->P.active = nullptr;
+}
+
+// Tile skipping costs ~3% of a fixed-count iteration (measured), so it is switched on only for
+// solves that can freeze images (tol > 0); the CUDA graph of each parameter set captures the choice.
+void tc_plan_enable_skip(TcPlan* p, bool on) { p->P.active = on ? p->active_ptr : nullptr; }
 
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C) {
   p->P.img_out = out;

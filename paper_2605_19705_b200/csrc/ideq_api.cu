@@ -455,6 +455,7 @@ ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, c
     L.plan = tc_make_plan(L.g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)out,
                           (const __nv_bfloat16*)aux, ctx->num_sms, err, sizeof(err));
     if (!L.plan) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
+    tc_plan_set_active(L.plan, ctx->active);  // frozen (converged / diverged) images cost nothing
   }
   ctx->prog.push_back(L);
   if (out_layer) *out_layer = &ctx->prog.back();
@@ -1047,6 +1048,8 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
   if (ctx->op.kind == IDEQ_OP_MRI) prepare_mri(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
+  for (auto& L : ctx->prog)  // skip frozen images' tiles only when images can freeze early
+    if (L.plan) tc_plan_enable_skip(L.plan, p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE);
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
   const bool poll = p->tol > 0.f;
   const int poll_every = global ? p->check_every : 4;
@@ -1453,6 +1456,7 @@ ideq_status ideq_grad_g(ideq_ctx* ctx, const float* z, float* grad_out, float* u
   if ((st = build_program(ctx, batch))) return st;
   const size_t n = (size_t)batch * ctx->C * ctx->H * ctx->W;
   CK(cudaMemcpyAsync(ctx->Z, z, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+  launch_init_state(make_fin(ctx, batch, nullptr), ctx->stream);  // every image active: no tile skipped
   run_network(ctx);
   CK(cudaMemcpyAsync(grad_out, ctx->G, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (u_out) CK(cudaMemcpyAsync(u_out, ctx->Hc, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));

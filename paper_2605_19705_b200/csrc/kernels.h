@@ -143,6 +143,8 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
 void tc_launch(const TcPlan* p, cudaStream_t s);
 void tc_free_plan(TcPlan* p);
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C);
+void tc_plan_set_active(TcPlan* p, const int* active);
+void tc_plan_enable_skip(TcPlan* p, bool on);
 int tc_plan_is_halo(const TcPlan* p);
 // im2col of a C-channel fp32 NCHW image into [N][H][W][32] bf16: k = c*9 + a*3 + b (zero beyond 9C)
 void launch_im2col32(const float* in, __nv_bfloat16* out, int N, int C, int H, int W, cudaStream_t s);
