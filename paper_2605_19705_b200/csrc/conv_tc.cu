@@ -989,7 +989,8 @@ template <int NC>
 __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restrict__ in,
                                                           const __nv_bfloat16* __restrict__ wB,
                                                           __nv_bfloat16* __restrict__ out, int N, int C, int H,
-                                                          int W, const FastDiv fdHW, const FastDiv fdW) {
+                                                          int W, const FastDiv fdHW, const FastDiv fdW,
+                                                          const int* __restrict__ active) {
   __shared__ __align__(1024) unsigned char sAraw[2][128 * 64];
   __shared__ __align__(1024) unsigned char sBraw[NC * 64];
   extern __shared__ __align__(1024) unsigned char sOdyn[];  // output staging [2][128 * NC * 2] (bulk-copied)
@@ -1052,10 +1053,20 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
       }
     }
   };
+  // tiles whose pixels all belong to frozen images (early-stopping solves) are skipped
+  auto next_live = [&](long long tt) {
+    if (active)
+      while (tt < tiles && !active[(int)fdHW.div((uint32_t)(tt * 128))] &&
+             !active[(int)fdHW.div((uint32_t)(tt * 128 + 127 < total ? tt * 128 + 127 : total - 1))])
+        tt += gridDim.x;
+    return tt;
+  };
   int it = 0;
   long long t_prev = -1;
-  if (blockIdx.x < tiles) load_patch(blockIdx.x);
-  for (long long t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+  long long tnext = next_live(blockIdx.x);
+  if (tnext < tiles) load_patch(tnext);
+  for (long long t = tnext; t < tiles; t = tnext, ++it) {
+    tnext = next_live(t + gridDim.x);
     const int buf = it & 1;
     const uint32_t sA = buf ? sA1 : sA0;
     float v[32];
@@ -1063,7 +1074,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     for (int k = 0; k < 27; ++k) v[k] = pv[k];
 #pragma unroll
     for (int k = 27; k < 32; ++k) v[k] = 0.f;
-    if (t + gridDim.x < tiles) load_patch(t + gridDim.x);
+    if (tnext < tiles) load_patch(tnext);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint4 wv;
@@ -1132,7 +1143,8 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
                  : "memory");
 }
 
-void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, int N, int C, int H, int W,
+void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, const int* active, int N, int C,
+                        int H, int W,
                         int NC, int num_sms, cudaStream_t s) {
   // the static shared memory (54 KB / 36 KB) caps residency so that the CTAs' TMEM allocations
   // (2 x NC columns each) never exceed the SM's 512 columns
@@ -1144,8 +1156,8 @@ void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16*
   FastDiv fdHW, fdW;
   fdHW.init((uint32_t)(H * W));
   fdW.init((uint32_t)W);
-  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW);
-  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW);
+  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW, active);
+  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW, active);
 }
 
 // ------------------------------------------------------------------ host side

@@ -152,6 +152,7 @@ struct ideq_ctx {
 
   // profiling
   bool profiling = false;
+  bool skip_frozen = false;  // current solve may freeze images early: kernels skip their work
   ideq_profile prof{};
   struct Ev { cudaEvent_t a, b; int cls; double flops, bytes; };
   std::vector<Ev> pending;
@@ -780,8 +781,8 @@ void run_layer(ideq_ctx* ctx, const Layer& L) {
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
   if (L.kind == L_IMG2FEAT_TC) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
-    launch_img2feat_tc(L.in_img, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, L.wfeat,
-                       ctx->num_sms, s);
+    launch_img2feat_tc(L.in_img, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)L.out, ctx->skip_frozen ? ctx->active : nullptr,
+                       L.N, L.C, L.H, L.W, L.wfeat, ctx->num_sms, s);
   } else if (L.kind == L_IM2COL) {
     Prof p(ctx, IDEQ_K_HEADTAIL, 0, L.bytes);
     launch_im2col32(L.in_img, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, s);
@@ -1048,8 +1049,9 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
   if (ctx->op.kind == IDEQ_OP_MRI) prepare_mri(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
+  ctx->skip_frozen = p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE;
   for (auto& L : ctx->prog)  // skip frozen images' tiles only when images can freeze early
-    if (L.plan) tc_plan_enable_skip(L.plan, p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE);
+    if (L.plan) tc_plan_enable_skip(L.plan, ctx->skip_frozen);
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
   const bool poll = p->tol > 0.f;
   const int poll_every = global ? p->check_every : 4;
@@ -1457,6 +1459,9 @@ ideq_status ideq_grad_g(ideq_ctx* ctx, const float* z, float* grad_out, float* u
   const size_t n = (size_t)batch * ctx->C * ctx->H * ctx->W;
   CK(cudaMemcpyAsync(ctx->Z, z, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   launch_init_state(make_fin(ctx, batch, nullptr), ctx->stream);  // every image active: no tile skipped
+  ctx->skip_frozen = false;
+  for (auto& L : ctx->prog)
+    if (L.plan) tc_plan_enable_skip(L.plan, false);
   run_network(ctx);
   CK(cudaMemcpyAsync(grad_out, ctx->G, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (u_out) CK(cudaMemcpyAsync(u_out, ctx->Hc, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
