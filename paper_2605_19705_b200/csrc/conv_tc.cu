@@ -1190,11 +1190,13 @@ static int tc_bn(const ConvGeom& g) { return g.ncols >= 128 ? 128 : g.ncols; }
 bool tc_supported(const ConvGeom& g) {
   if (!(g.KC == 32 || g.KC == 64)) return false;
   if (g.R * g.Wt > 128 || g.Wt > 256 || g.R > 256) return false;
-  if (g.ncols % 32 != 0) return false;
+  // EPI_IMG (tail / head adjoint: C <= 3 image columns) runs with N = 16; its epilogue writes
+  // fp32 planes from registers and never uses the smem boxes / store maps
+  if (g.epi == EPI_IMG ? (g.ncols != 16 && g.ncols != 32) : (g.ncols % 32 != 0)) return false;
   const int BN = tc_bn(g);
   if (g.ncols % BN != 0) return false;
   const int boxc = BN >= 64 ? 64 : 32;
-  if (g.CB % boxc != 0 || g.OCp % 8 != 0) return false;
+  if (g.epi != EPI_IMG && (g.CB % boxc != 0 || g.OCp % 8 != 0)) return false;
   if ((g.inC * 2) % 16 != 0) return false;
   if (g.OHo % g.osh != 0) return false;
   return true;
@@ -1316,6 +1318,12 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
             CU_TENSOR_MAP_INTERLEAVE_NONE, swA, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map B encode failed (%d)", (int)r); delete p; return nullptr; }
   }
+  const int slab_mode = (g.Wt % 32 == 0 || 32 % g.Wt == 0) ? 1 : 0;
+  if (g.epi == EPI_IMG) {  // no smem-staged output: the store / aux / slab maps are never used
+    p->tmOut = p->tmA;
+    p->tmAux = p->tmA;
+    p->tmSlab = p->tmA;
+  } else {
   // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
   // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
   // EPI_IMG writes fp32 image planes directly: the (unused) output map points at the input
@@ -1330,7 +1338,6 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   }
   // 32-row epilogue slab (one TMEM lane quadrant): Wt >= 32 -> 32 pixels of one row; Wt < 32 ->
   // 32 / Wt whole rows. Used when Wt is a multiple or a divisor of 32.
-  const int slab_mode = (g.Wt % 32 == 0 || 32 % g.Wt == 0) ? 1 : 0;
   if (slab_mode) {
     const int sw = g.Wt >= 32 ? 32 : g.Wt, sh = g.Wt >= 32 ? 1 : 32 / g.Wt;
     r = encode5(enc, &p->tmSlab, g.epi == EPI_IMG ? (const void*)in : (const void*)out, g.CB, g.OWo, g.osh,
@@ -1338,6 +1345,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map slab encode failed (%d)", (int)r); delete p; return nullptr; }
   } else {
     p->tmSlab = p->tmOut;
+  }
   }
   TcParams& P = p->P;
   P.g = g;

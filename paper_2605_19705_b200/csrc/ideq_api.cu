@@ -476,7 +476,7 @@ ideq_status add_gemm(ideq_ctx* ctx, const std::string& wname, int kind, int N, i
 // Tensor-core head/tail (bf16 U-Net). Image -> features (head, tail adjoint): one fused kernel
 // builds the K = 32 im2col row of each pixel in shared memory and runs a 1x1 tcgen05 GEMM.
 // Features -> image (tail, head adjoint): a 3x3 tcgen05 conv with the C output columns padded
-// to 32 (zero weights) and the EPI_IMG epilogue writing fp32 NCHW planes (+ alpha * aux).
+// to 16 (zero weights) and the EPI_IMG epilogue writing fp32 NCHW planes (+ alpha * aux).
 ideq_status add_tc_img2feat(ideq_ctx* ctx, const std::string& wname, bool adjoint, int N, const float* in_img,
                             void* out_feat, const std::string& lname) {
   WeightSlices ws;
@@ -524,17 +524,20 @@ ideq_status add_tc_feat2img(ideq_ctx* ctx, const std::string& wname, bool adjoin
   std::vector<float> wp;
   std::vector<int> shp;
   int kind;
-  if (!adjoint) {  // tail [C][w0][3][3] -> [32][w0][3][3], rows >= C zero
-    wp.assign((size_t)32 * i_n * 9, 0.f);
+  // the C <= 3 image columns padded to an MMA N of 16 (zero weights): the layer is bound by the
+  // shared-memory operand reads, which N = 16 cuts from 5 KB to 4.5 KB per MMA
+  constexpr int NP = 16;
+  if (!adjoint) {  // tail [C][w0][3][3] -> [16][w0][3][3], rows >= C zero
+    wp.assign((size_t)NP * i_n * 9, 0.f);
     std::copy(Wt, Wt + (size_t)o_n * i_n * 9, wp.begin());
-    shp = {32, i_n, 3, 3};
+    shp = {NP, i_n, 3, 3};
     kind = 0;
-  } else {         // head [w0][C][3][3] -> [w0][32][3][3], columns >= C zero; kind 1 = adjoint
-    wp.assign((size_t)o_n * 32 * 9, 0.f);
+  } else {         // head [w0][C][3][3] -> [w0][16][3][3], columns >= C zero; kind 1 = adjoint
+    wp.assign((size_t)o_n * NP * 9, 0.f);
     for (int o = 0; o < o_n; ++o)
       for (int i = 0; i < i_n; ++i)
-        for (int t = 0; t < 9; ++t) wp[((size_t)o * 32 + i) * 9 + t] = Wt[((size_t)o * i_n + i) * 9 + t];
-    shp = {o_n, 32, 3, 3};
+        for (int t = 0; t < 9; ++t) wp[((size_t)o * NP + i) * 9 + t] = Wt[((size_t)o * i_n + i) * 9 + t];
+    shp = {o_n, NP, 3, 3};
     kind = 1;
   }
   Layer* L = nullptr;
