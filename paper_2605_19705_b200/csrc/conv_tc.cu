@@ -447,20 +447,18 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   // active-image bitmask (<= 1024 images), read once per CTA so the per-tile skip test is a
   // shared-memory load instead of a dependent global load in every warp role's loop
-  // the flags are loaded here (up to 3 per thread) and folded into the bitmask after the barrier
-  // and TMEM set-up below, so the load latency hides behind the prologue
+  // Programmatic dependent launch: the next layer may be scheduled now; its CTAs run their
+  // prologue as SMs free up and wait (griddepcontrol.wait) for this grid before touching data.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ uint32_t s_act[32];
-  int actf[3] = {0, 0, 0};
-  if (P.active) {
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int i = (warp + r * (TC_THREADS / 32)) * 32 + lane;
-      if (i < g.N && i < 1024) actf[r] = P.active[i];
-    }
-  }
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
+    if (MODE == 1 || ROW) {  // resident weights (constant since create): loaded before the wait
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
+      for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
+    }
     // PAIR: the leader's tempty counts both CTAs' epilogue warps
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
     for (int s = 0; s < SB; ++s) { mbar_init(fullB0 + 8u * s, 1); mbar_init(emptyB0 + 8u * s, 1); }
@@ -490,11 +488,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
   }
-  if (P.active) {  // one ballot per warp and 32-image word
+  // everything below reads what earlier kernels wrote: wait for them (no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (P.active) {  // one flag per thread, one ballot per warp and 32-image word
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
       const int w = warp + r * (TC_THREADS / 32);
-      const uint32_t bits = __ballot_sync(0xffffffffu, actf[r] != 0);
+      const int i = w * 32 + lane;
+      const uint32_t bits = __ballot_sync(0xffffffffu, i < g.N && i < 1024 && P.active[i] != 0);
       if (lane == 0 && w < 32 && w * 32 < g.N) s_act[w] = bits;
     }
   }
@@ -521,13 +522,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
-    if (MODE == 1 || ROW) {  // resident weights: every K-block of the (single) N tile, once per CTA
-      if (elect_one()) {
-        mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
-        for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
-      }
-      __syncwarp();
-    }
     for (int t = t0; t < total; t += tstep) {
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
       if (P.active && tile_frozen(s_act, ti.img)) continue;
@@ -1420,35 +1414,40 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   return p;
 }
 
+// Every conv launch carries the programmatic-stream-serialization attribute (PDL): it may start
+// while its predecessor drains; the kernel waits (griddepcontrol.wait) before reading activations.
+// CTA pairs (MODE 3) add the cluster dimension. IDEQ_NO_PDL=1 launches plainly (A/B switch).
 template <int KC, int EPI, int BOXC>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
-  if (p->halo == 1)
-    conv_tc_kernel<KC, EPI, BOXC, 1><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                        p->tmSlab, p->P);
-  else if (p->halo == 2)
-    conv_tc_kernel<KC, EPI, BOXC, 2><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                        p->tmSlab, p->P);
-  else if (p->halo == 4)
-    conv_tc_kernel<KC, EPI, BOXC, 4><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                        p->tmSlab, p->P);
-  else if (p->halo == 3) {  // CTA pairs: cluster of 2 on one TPC
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)p->grid);
-    cfg.blockDim = dim3(TC_THREADS);
-    cfg.dynamicSmemBytes = p->smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 2;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P);
+  static const bool no_pdl = [] { const char* e = getenv("IDEQ_NO_PDL"); return e && atoi(e) != 0; }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)p->grid);
+  cfg.blockDim = dim3(TC_THREADS);
+  cfg.dynamicSmemBytes = p->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (!no_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
   }
-  else
-    conv_tc_kernel<KC, EPI, BOXC, 0><<<p->grid, TC_THREADS, p->smem, s>>>(p->tmA, p->tmB, p->tmOut, p->tmAux,
-                                                                        p->tmSlab, p->P);
+  if (p->halo == 3) {  // CTA pairs: cluster of 2 on one TPC
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = 2;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  switch (p->halo) {
+    case 1: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 1>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+    case 2: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 2>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+    case 3: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+    case 4: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 4>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+    default: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 0>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+  }
 }
 
 template <int KC, int BOXC>
