@@ -308,46 +308,6 @@ void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux
   }
 }
 
-// ------------------------------------------------------------------ im2col for the tensor-core head
-// out[n,h,w,k] = in[n, c, h+a-1, w+b-1] with k = c*9 + a*3 + b < 9C, zero elsewhere (k < 32):
-// turns the C -> w0 head conv (and the tail adjoint) into a K = 32 GEMM on tcgen05.
-__global__ void __launch_bounds__(256) im2col32_kernel(const float* __restrict__ in, __nv_bfloat16* __restrict__ out,
-                                                       int N, int C, int H, int W) {
-  const long long HW = (long long)H * W;
-  const long long pix = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (pix >= (long long)N * HW) return;
-  const int n = (int)(pix / HW), h = (int)((pix % HW) / W), w = (int)(pix % W);
-  float v[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = 0.f;
-#pragma unroll
-  for (int c = 0; c < 3; ++c) {  // constant indices keep v[] in registers; C <= 3
-    if (c >= C) break;
-    const float* plane = in + ((long long)n * C + c) * HW;
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const int hh = h + a - 1, ww = w + b - 1;
-        v[c * 9 + a * 3 + b] = (hh >= 0 && hh < H && ww >= 0 && ww < W) ? plane[(long long)hh * W + ww] : 0.f;
-      }
-    }
-  }
-  __nv_bfloat16* o = out + pix * 32;
-#pragma unroll
-  for (int k = 0; k < 32; k += 8) {
-    float t[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) t[e] = v[k + e];
-    store8(o + k, t);
-  }
-}
-
-void launch_im2col32(const float* in, __nv_bfloat16* out, int N, int C, int H, int W, cudaStream_t s) {
-  const long long P = (long long)N * H * W;
-  im2col32_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(in, out, N, C, H, W);
-}
-
 void init_attrs_simt() {
   set_max_dyn_smem(feat2img_kernel<float, 16>);
   set_max_dyn_smem(feat2img_kernel<float, 32>);

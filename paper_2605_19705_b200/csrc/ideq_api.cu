@@ -53,7 +53,7 @@ NcclApi g_nccl;
 constexpr int NCCL_FLOAT32 = 7, NCCL_MAX = 2;
 
 // ------------------------------------------------------------------ program description
-enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IM2COL = 3, L_IMG2FEAT_TC = 4 };
+enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IMG2FEAT_TC = 4 };
 
 struct Layer {
   LayerKind kind;
@@ -106,7 +106,6 @@ struct ideq_ctx {
 
   // solver buffers (fp32 NCHW)
   float *X1 = nullptr, *Z = nullptr, *G = nullptr, *Hc = nullptr, *fbuf = nullptr, *fbuf2 = nullptr;
-  void* im2col = nullptr;  // [N][H][W][32] bf16 (tensor-core head), bf16 U-Net only
   float* partials = nullptr;
   // NEXT-1 (restart / averaging) state
   int* rk = nullptr;
@@ -786,9 +785,6 @@ void run_layer(ideq_ctx* ctx, const Layer& L) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
     launch_img2feat_tc(L.in_img, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)L.out, ctx->skip_frozen ? ctx->active : nullptr,
                        L.N, L.C, L.H, L.W, L.wfeat, ctx->num_sms, s);
-  } else if (L.kind == L_IM2COL) {
-    Prof p(ctx, IDEQ_K_HEADTAIL, 0, L.bytes);
-    launch_im2col32(L.in_img, (__nv_bfloat16*)L.out, L.N, L.C, L.H, L.W, s);
   } else if (L.kind == L_GEMM) {
     if (L.tc) {
       Prof p(ctx, L.headtail ? IDEQ_K_HEADTAIL : IDEQ_K_CONV_TC, L.flops, L.bytes);

@@ -147,7 +147,6 @@ void tc_plan_set_active(TcPlan* p, const int* active);
 void tc_plan_enable_skip(TcPlan* p, bool on);
 int tc_plan_is_halo(const TcPlan* p);
 // im2col of a C-channel fp32 NCHW image into [N][H][W][32] bf16: k = c*9 + a*3 + b (zero beyond 9C)
-void launch_im2col32(const float* in, __nv_bfloat16* out, int N, int C, int H, int W, cudaStream_t s);
 void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, const int* active, int N, int C,
                         int H, int W,
                         int NC, int num_sms, cudaStream_t s);
