@@ -208,6 +208,22 @@ IDEQ_API ideq_status ideq_fidelity_grad(ideq_ctx* ctx, const float* y, const flo
 IDEQ_API ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, float tau,
                                float* out, int batch);
 
+/* JFB training gradient at the fixed point.
+ * Loss L = 1/2 sum_i ||T(x_hat_i) - x*_i||^2 with ONE more i-DEQ step at x_hat treated as a
+ * constant (x^{k-1} = x^k = x_hat, so z = x_hat):
+ *   gradient step (Alg. 1 l.8): T = z - tau (grad f(z) + lam grad g_theta(z))
+ *   prox step (Alg. 2 l.7):     T = prox_{tau f}(z - tau lam grad g_theta(z))  (inpainting only)
+ * y, x_hat, x_star: DEVICE, NCHW fp32, `batch` images (the operator set by ideq_set_operator).
+ * p: lambda and tau are read (beta is irrelevant at z = x_hat).
+ * dtheta: HOST, n_weights floats, the blob order of ideq_create; overwritten.
+ * dlam, dtau, dbeta, loss: HOST scalars (dbeta = 0 exactly).
+ * Requires the fp32 context (IDEQ_PREC_FP32), identity skip and softplus (else
+ * IDEQ_E_UNSUPPORTED), a prox step only with the inpainting operator. Synchronous; allocates
+ * its tape per call (sized for parity / small-batch training, not the inference hot path). */
+IDEQ_API ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, const float* x_star,
+                                   int batch, const ideq_params* p, float* dtheta, float* dlam,
+                                   float* dtau, float* dbeta, float* loss);
+
 /* Profiling: when enabled, solves launch eagerly (no CUDA graph) and bracket every
  * kernel launch with CUDA events on the context stream; ideq_get_profile returns
  * per-kernel-class totals accumulated since the last reset. */

@@ -1550,6 +1550,341 @@ ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const float* v, fl
   return IDEQ_OK;
 }
 
+// ======================================================================== JFB gradient (NEXT-4)
+// dL/dtheta, dL/dlam, dL/dtau of L = 1/2 sum_i ||T(x_hat_i) - x*_i||^2 with one more i-DEQ step at
+// the fixed point (z = x_hat, so dL/dbeta = 0); see jfb.cu and oracle/jfb.py. fp32 FFMA path.
+namespace {
+
+struct JfbRun {
+  ideq_ctx* ctx;
+  int N;
+  cudaStream_t s;
+  std::vector<void*> mem;
+  std::map<std::string, float*> dw;  // per weight tensor: gradient in the layer's operand / blob layout
+  WeightSlices ws;
+  ideq_status st = IDEQ_OK;
+  float* wsp = nullptr;  // split partials of the weight-gradient reductions (grown on demand)
+  size_t wsp_n = 0;
+
+  float* work(size_t n) {
+    if (n > wsp_n) {
+      if (wsp) { cudaStreamSynchronize(s); cudaFree(wsp); wsp = nullptr; }
+      if (cudaMalloc(&wsp, n * sizeof(float)) != cudaSuccess) { cudaGetLastError(); st = IDEQ_E_NOMEM; wsp_n = 0; return nullptr; }
+      wsp_n = n;
+    }
+    return wsp;
+  }
+  float* buf(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, (n ? n : 1) * sizeof(float)) != cudaSuccess) { cudaGetLastError(); st = IDEQ_E_NOMEM; return nullptr; }
+    cudaMemsetAsync(p, 0, (n ? n : 1) * sizeof(float), s);
+    mem.push_back(p);
+    return (float*)p;
+  }
+  ~JfbRun() {
+    for (void* p : mem) cudaFree(p);
+    if (wsp) cudaFree(wsp);
+  }
+
+  // shape-derived GEMM quantities of a layer, as in add_gemm_w
+  void dims(int kind, const std::vector<int>& shp, int& ncols, int& ktap, int& cin) {
+    if (kind == 0) { ncols = shp[0]; ktap = shp[1]; }
+    else if (kind == 1) { ncols = shp[1]; ktap = shp[0]; }
+    else if (kind == 2 || kind == 5) { ncols = shp[0]; ktap = 2 * shp[1]; }
+    else { ncols = 4 * shp[1]; ktap = shp[0]; }
+    cin = (kind == 2 || kind == 5) ? ktap / 2 : ktap;
+  }
+  const float* weights(const std::string& wname, int kind, int KC) {
+    const std::string key = wname + "#" + std::to_string(kind) + "simt";
+    if (!ctx->wdev.count(key)) {
+      auto& sl = ws.t[wname];
+      int ncols, ntaps, ktap;
+      std::vector<float> B = gemm_weights(kind, ctx->blob.data() + sl.first, sl.second, KC, ncols, ntaps, ktap);
+      if (upload_gemm_weights(ctx, key, B)) { st = IDEQ_E_CUDA; return nullptr; }
+    }
+    return (const float*)ctx->wdev[key];
+  }
+  ConvGeom geom(const std::string& wname, int kind, int Hin, int Win, int epi) {
+    int ncols, ktap, cin;
+    dims(kind, ws.t[wname].second, ncols, ktap, cin);
+    return make_geom(kind, N, Hin, Win, cin, ncols, pick_kc(false, ktap), ktap, epi);
+  }
+  void conv(const std::string& wname, int kind, int Hin, int Win, const float* in, float* out, const float* aux,
+            int epi) {
+    ConvGeom g = geom(wname, kind, Hin, Win, epi);
+    const float* w = weights(wname, kind, g.KC);
+    if (w) launch_conv_simt<float>(g, in, w, out, aux, s);
+  }
+  // weight gradient of the FORWARD layer (kind 0 / 2 / 4) for one stream, accumulated
+  void wgrad(const std::string& wname, int kind, int Hin, int Win, const float* in, const float* gout) {
+    ConvGeom g = geom(wname, kind, Hin, Win, EPI_STORE);
+    float*& d = dw[wname];
+    if (!d) d = buf((size_t)g.ntaps * g.nchunk * g.ncols * g.KC);
+    float* w = work(wgrad_workspace(g));
+    if (d && w) launch_wgrad_geom(g, in, gout, d, w, s);
+  }
+  const float* headtail_w(const std::string& wname, bool adjoint) {
+    const std::string key = wname + (adjoint ? "#T" : "#F");
+    if (!ctx->wdev.count(key)) {
+      auto& sl = ws.t[wname];
+      const float* Wt = ctx->blob.data() + sl.first;
+      std::vector<float> v;
+      if (adjoint) v = flip_transpose3x3(Wt, sl.second[0], sl.second[1]);
+      else v.assign(Wt, Wt + (size_t)sl.second[0] * sl.second[1] * 9);
+      if (upload_f32(ctx, key, v)) { st = IDEQ_E_CUDA; return nullptr; }
+    }
+    return (const float*)ctx->wdev[key];
+  }
+  void head_wgrad(const std::string& wname, const float* img, const float* gf, int C, int H, int W, int wf) {
+    float* d = dw_blob(wname);
+    float* w = work(headtail_wgrad_workspace(N, C, H, wf));
+    if (d && w) launch_head_wgrad(img, gf, d, w, N, C, H, W, wf, s);
+  }
+  void tail_wgrad(const std::string& wname, const float* f, const float* gimg, int C, int H, int W, int wf) {
+    float* d = dw_blob(wname);
+    float* w = work(headtail_wgrad_workspace(N, C, H, wf));
+    if (d && w) launch_tail_wgrad(f, gimg, d, w, N, C, H, W, wf, s);
+  }
+  float* dw_blob(const std::string& wname) {  // head / tail: gradient directly in blob layout
+    float*& d = dw[wname];
+    if (!d) {
+      auto& shp = ws.t[wname].second;
+      d = buf((size_t)shp[0] * shp[1] * shp[2] * shp[3]);
+    }
+    return d;
+  }
+};
+
+}  // namespace
+
+ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, const float* x_star, int batch,
+                          const ideq_params* p, float* dtheta, float* dlam, float* dtau, float* dbeta, float* loss) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!y || !x_hat || !x_star || !p || !dtheta || !dlam || !dtau || !dbeta || !loss)
+    return fail(ctx, IDEQ_E_INVALID, "NULL argument");
+  if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch out of range");
+  if (ctx->prec != IDEQ_PREC_FP32) return fail(ctx, IDEQ_E_UNSUPPORTED, "the JFB gradient runs in the fp32 mode");
+  if (!ctx->net.identity_skip) return fail(ctx, IDEQ_E_UNSUPPORTED, "the JFB gradient assumes N = z + U");
+  if (ctx->net.act != IDEQ_ACT_SOFTPLUS) return fail(ctx, IDEQ_E_UNSUPPORTED, "the JFB gradient assumes softplus");
+  if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "no operator");
+  const bool prox = ctx->op.step == IDEQ_STEP_PROX;
+  if (prox && ctx->op.kind != IDEQ_OP_INPAINT)
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "JFB prox variant: inpainting (closed-form Jacobian) only");
+  const int C = ctx->C, H = ctx->H, W = ctx->W;
+  const long long nimg = (long long)batch * C * H * W;
+  JfbRun J;
+  J.ctx = ctx;
+  J.N = batch;
+  J.s = ctx->stream;
+  size_t tot;
+  slice_weights(ctx->net, J.ws, tot);
+  cudaStream_t s = ctx->stream;
+  // ---- grad g(z), U(z) at z = x_hat; grad f(z) (gradient variant)
+  float* gg = J.buf(nimg);
+  float* U = J.buf(nimg);
+  float* gf = J.buf(nimg);
+  float* v = J.buf(nimg);
+  float* terms = J.buf(3 * nimg);
+  double* dsum = nullptr;
+  double* dpart = nullptr;
+  if (J.st || cudaMalloc(&dsum, 4 * sizeof(double)) != cudaSuccess || cudaMalloc(&dpart, 3 * 256 * sizeof(double)) != cudaSuccess)
+    return fail(ctx, IDEQ_E_NOMEM, "JFB workspace");
+  J.mem.push_back(dsum);
+  J.mem.push_back(dpart);
+  if ((st = ideq_grad_g(ctx, x_hat, gg, U, batch))) return st;
+  if (!prox && (st = ideq_fidelity_grad(ctx, y, x_hat, gf, batch))) return st;
+  launch_jfb_residual(x_hat, x_star, gg, gf, y, ctx->d_mask, prox ? 1 : 0, p->lambda, p->tau, nimg, (long long)H * W,
+                      (long long)C * H * W, v, terms, s);
+  launch_sums(terms, nimg, 3, dpart, dsum, s);
+  // ---- two-stream forward (primal z, tangent v) with a tape, reverse with weight gradients
+  const auto& n = ctx->net;
+  const long long HW = (long long)H * W;
+  if (n.arch == IDEQ_NET_TINY3) {
+    const int w = n.widths[0];
+    const long long nf = (long long)batch * HW * w;
+    float *p1 = J.buf(nf), *a1 = J.buf(nf), *p1d = J.buf(nf), *a1d = J.buf(nf);
+    float *p2 = J.buf(nf), *a2 = J.buf(nf), *p2d = J.buf(nf), *a2d = J.buf(nf);
+    float *Ud = J.buf(nimg), *Up = J.buf(nimg);
+    if (J.st) return fail(ctx, J.st, "JFB workspace");
+    launch_img2feat<float>(x_hat, J.headtail_w("c1", false), p1, nullptr, EPI_STORE, batch, C, H, W, w, s);
+    launch_img2feat<float>(v, J.headtail_w("c1", false), p1d, nullptr, EPI_STORE, batch, C, H, W, w, s);
+    launch_sp_forward(p1, a1, nf, s);
+    launch_sp_tangent(a1, p1d, a1d, nf, s);
+    J.conv("c2", 0, H, W, a1, p2, nullptr, EPI_STORE);
+    J.conv("c2", 0, H, W, a1d, p2d, nullptr, EPI_STORE);
+    launch_sp_forward(p2, a2, nf, s);
+    launch_sp_tangent(a2, p2d, a2d, nf, s);
+    launch_feat2img<float>(a2, J.headtail_w("c3", false), Up, nullptr, 0.f, batch, C, H, W, w, s);
+    launch_feat2img<float>(a2d, J.headtail_w("c3", false), Ud, nullptr, 0.f, batch, C, H, W, w, s);
+    // reverse: U_bar = U_dot, U_dot_bar = U
+    J.tail_wgrad("c3", a2, Ud, C, H, W, w);
+    J.tail_wgrad("c3", a2d, Up, C, H, W, w);
+    float *a2b = J.buf(nf), *a2db = J.buf(nf), *p2b = J.buf(nf), *p2db = J.buf(nf);
+    float *a1b = J.buf(nf), *a1db = J.buf(nf), *p1b = J.buf(nf), *p1db = J.buf(nf);
+    if (J.st) return fail(ctx, J.st, "JFB workspace");
+    launch_img2feat<float>(Ud, J.headtail_w("c3", true), a2b, nullptr, EPI_STORE, batch, C, H, W, w, s);
+    launch_img2feat<float>(Up, J.headtail_w("c3", true), a2db, nullptr, EPI_STORE, batch, C, H, W, w, s);
+    launch_sp_reverse(a2, p2d, a2b, a2db, p2b, p2db, nf, s);
+    J.wgrad("c2", 0, H, W, a1, p2b);
+    J.wgrad("c2", 0, H, W, a1d, p2db);
+    J.conv("c2", 1, H, W, p2b, a1b, nullptr, EPI_STORE);
+    J.conv("c2", 1, H, W, p2db, a1db, nullptr, EPI_STORE);
+    launch_sp_reverse(a1, p1d, a1b, a1db, p1b, p1db, nf, s);
+    J.head_wgrad("c1", x_hat, p1b, C, H, W, w);
+    J.head_wgrad("c1", v, p1db, C, H, W, w);
+  } else {
+    const int R = n.res_blocks;
+    int Hl[4], Wl[4], wl[4];
+    for (int l = 0; l < 4; ++l) { Hl[l] = H >> l; Wl[l] = W >> l; wl[l] = n.widths[l]; }
+    auto fsz = [&](int l) { return (long long)batch * Hl[l] * Wl[l] * wl[l]; };
+    struct Rec { int kind, l; std::string nA, nB; const float *x, *xd; float *a, *pd, *ad; };
+    std::vector<Rec> tape;
+    float* t = J.buf(fsz(0));
+    float* td = J.buf(fsz(0));
+    if (J.st) return fail(ctx, J.st, "JFB workspace");
+    launch_img2feat<float>(x_hat, J.headtail_w("head", false), t, nullptr, EPI_STORE, batch, C, H, W, wl[0], s);
+    launch_img2feat<float>(v, J.headtail_w("head", false), td, nullptr, EPI_STORE, batch, C, H, W, wl[0], s);
+    const float* skip[3] = {nullptr, nullptr, nullptr};
+    const float* skipd[3] = {nullptr, nullptr, nullptr};
+    auto rb_fwd = [&](const char* pre, int l, int r) {
+      const std::string nA = std::string(pre) + std::to_string(l) + "." + std::to_string(r) + ".A";
+      const std::string nB = std::string(pre) + std::to_string(l) + "." + std::to_string(r) + ".B";
+      const long long nf = fsz(l);
+      float *pp = J.buf(nf), *a = J.buf(nf), *pd = J.buf(nf), *ad = J.buf(nf), *t2 = J.buf(nf), *t2d = J.buf(nf);
+      if (J.st) return;
+      J.conv(nA, 0, Hl[l], Wl[l], t, pp, nullptr, EPI_STORE);
+      launch_sp_forward(pp, a, nf, s);
+      J.conv(nA, 0, Hl[l], Wl[l], td, pd, nullptr, EPI_STORE);
+      launch_sp_tangent(a, pd, ad, nf, s);
+      J.conv(nB, 0, Hl[l], Wl[l], a, t2, t, EPI_RESADD);
+      J.conv(nB, 0, Hl[l], Wl[l], ad, t2d, td, EPI_RESADD);
+      tape.push_back({0, l, nA, nB, t, td, a, pd, ad});
+      t = t2;
+      td = t2d;
+    };
+    for (int l = 0; l < 4; ++l) {
+      for (int r = 0; r < R; ++r) rb_fwd("e", l, r);
+      if (l < 3) {
+        skip[l] = t;
+        skipd[l] = td;
+        tape.push_back({1, l, "down" + std::to_string(l), "", t, td, nullptr, nullptr, nullptr});
+        float *c = J.buf(fsz(l + 1)), *cd = J.buf(fsz(l + 1));
+        if (J.st) return fail(ctx, J.st, "JFB workspace");
+        J.conv("down" + std::to_string(l), 2, Hl[l], Wl[l], t, c, nullptr, EPI_STORE);
+        J.conv("down" + std::to_string(l), 2, Hl[l], Wl[l], td, cd, nullptr, EPI_STORE);
+        t = c;
+        td = cd;
+      }
+    }
+    for (int l = 2; l >= 0; --l) {
+      tape.push_back({2, l, "up" + std::to_string(l), "", t, td, nullptr, nullptr, nullptr});
+      float *f = J.buf(fsz(l)), *fd = J.buf(fsz(l));
+      if (J.st) return fail(ctx, J.st, "JFB workspace");
+      J.conv("up" + std::to_string(l), 4, Hl[l + 1], Wl[l + 1], t, f, skip[l], EPI_RESADD);
+      J.conv("up" + std::to_string(l), 4, Hl[l + 1], Wl[l + 1], td, fd, skipd[l], EPI_RESADD);
+      t = f;
+      td = fd;
+      for (int r = 0; r < R; ++r) rb_fwd("d", l, r);
+    }
+    if (J.st) return fail(ctx, J.st, "JFB workspace");
+    float *Up = J.buf(nimg), *Ud = J.buf(nimg);
+    float *gb = J.buf(fsz(0)), *gdb = J.buf(fsz(0));
+    if (J.st) return fail(ctx, J.st, "JFB workspace");
+    launch_feat2img<float>(t, J.headtail_w("tail", false), Up, nullptr, 0.f, batch, C, H, W, wl[0], s);
+    launch_feat2img<float>(td, J.headtail_w("tail", false), Ud, nullptr, 0.f, batch, C, H, W, wl[0], s);
+    // reverse: U_bar = U_dot, U_dot_bar = U
+    J.tail_wgrad("tail", t, Ud, C, H, W, wl[0]);
+    J.tail_wgrad("tail", td, Up, C, H, W, wl[0]);
+    launch_img2feat<float>(Ud, J.headtail_w("tail", true), gb, nullptr, EPI_STORE, batch, C, H, W, wl[0], s);
+    launch_img2feat<float>(Up, J.headtail_w("tail", true), gdb, nullptr, EPI_STORE, batch, C, H, W, wl[0], s);
+    const float* sb[3] = {nullptr, nullptr, nullptr};
+    const float* sdb[3] = {nullptr, nullptr, nullptr};
+    for (int i = (int)tape.size() - 1; i >= 0; --i) {
+      const Rec& rc = tape[i];
+      const int l = rc.l;
+      const long long nf = fsz(l);
+      if (rc.kind == 0) {  // t' = t + B(sp(A t))
+        float *ab = J.buf(nf), *adb = J.buf(nf), *pb = J.buf(nf), *pdb = J.buf(nf), *g2 = J.buf(nf), *g2d = J.buf(nf);
+        if (J.st) return fail(ctx, J.st, "JFB workspace");
+        J.conv(rc.nB, 1, Hl[l], Wl[l], gb, ab, nullptr, EPI_STORE);
+        J.conv(rc.nB, 1, Hl[l], Wl[l], gdb, adb, nullptr, EPI_STORE);
+        J.wgrad(rc.nB, 0, Hl[l], Wl[l], rc.a, gb);
+        J.wgrad(rc.nB, 0, Hl[l], Wl[l], rc.ad, gdb);
+        launch_sp_reverse(rc.a, rc.pd, ab, adb, pb, pdb, nf, s);
+        J.wgrad(rc.nA, 0, Hl[l], Wl[l], rc.x, pb);
+        J.wgrad(rc.nA, 0, Hl[l], Wl[l], rc.xd, pdb);
+        J.conv(rc.nA, 1, Hl[l], Wl[l], pb, g2, gb, EPI_RESADD);
+        J.conv(rc.nA, 1, Hl[l], Wl[l], pdb, g2d, gdb, EPI_RESADD);
+        gb = g2;
+        gdb = g2d;
+      } else if (rc.kind == 2) {  // t = up(x) + s_l: the skip's cotangent is t's
+        sb[l] = gb;
+        sdb[l] = gdb;
+        float *c = J.buf(fsz(l + 1)), *cd = J.buf(fsz(l + 1));
+        if (J.st) return fail(ctx, J.st, "JFB workspace");
+        J.wgrad(rc.nA, 4, Hl[l + 1], Wl[l + 1], rc.x, gb);
+        J.wgrad(rc.nA, 4, Hl[l + 1], Wl[l + 1], rc.xd, gdb);
+        J.conv(rc.nA, 5, Hl[l], Wl[l], gb, c, nullptr, EPI_STORE);
+        J.conv(rc.nA, 5, Hl[l], Wl[l], gdb, cd, nullptr, EPI_STORE);
+        gb = c;
+        gdb = cd;
+      } else {  // x -> down(x), and x = s_l
+        float *f = J.buf(nf), *fd = J.buf(nf);
+        if (J.st) return fail(ctx, J.st, "JFB workspace");
+        J.wgrad(rc.nA, 2, Hl[l], Wl[l], rc.x, gb);
+        J.wgrad(rc.nA, 2, Hl[l], Wl[l], rc.xd, gdb);
+        J.conv(rc.nA, 3, Hl[l + 1], Wl[l + 1], gb, f, sb[l], EPI_RESADD);
+        J.conv(rc.nA, 3, Hl[l + 1], Wl[l + 1], gdb, fd, sdb[l], EPI_RESADD);
+        gb = f;
+        gdb = fd;
+      }
+    }
+    J.head_wgrad("head", x_hat, gb, C, H, W, wl[0]);
+    J.head_wgrad("head", v, gdb, C, H, W, wl[0]);
+  }
+  if (J.st) return fail(ctx, J.st, "JFB workspace / weights");
+  // ---- scale by -tau lam, bring back, map each layer operand layout to the blob order
+  const float scale = -p->tau * p->lambda;
+  std::vector<float> host;
+  for (auto& kv : J.dw) {
+    const std::string& name = kv.first;
+    auto& sl = J.ws.t[name];
+    const std::vector<int>& shp = sl.second;
+    const size_t nw = (size_t)shp[0] * shp[1] * shp[2] * shp[3];
+    const bool headtail = (name == "head" || name == "tail" || name == "c1" || name == "c3");
+    if (headtail) {
+      launch_scale(kv.second, scale, (long long)nw, s);
+      CK(cudaMemcpyAsync(dtheta + sl.first, kv.second, nw * sizeof(float), cudaMemcpyDeviceToHost, s));
+      continue;
+    }
+    const int kind = name.compare(0, 4, "down") == 0 ? 2 : name.compare(0, 2, "up") == 0 ? 4 : 0;
+    int ncols, ktap, cin;
+    J.dims(kind, shp, ncols, ktap, cin);
+    const int KC = pick_kc(false, ktap);
+    // operand index of every blob element: gemm_weights applied to the blob positions themselves
+    std::vector<float> pos(nw);
+    for (size_t i = 0; i < nw; ++i) pos[i] = (float)i;
+    int nc2, nt2, kt2;
+    std::vector<float> map = gemm_weights(kind, pos.data(), shp, KC, nc2, nt2, kt2);
+    const size_t nb = map.size();
+    launch_scale(kv.second, scale, (long long)nb, s);
+    host.resize(nb);
+    CK(cudaMemcpyAsync(host.data(), kv.second, nb * sizeof(float), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (size_t b = 0; b < nb; ++b) dtheta[sl.first + (size_t)map[b]] = host[b];  // permutation only
+  }
+  double sums[3];
+  CK(cudaMemcpyAsync(sums, dsum, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  *loss = (float)sums[0];
+  *dlam = (float)sums[1];
+  *dtau = (float)sums[2];
+  *dbeta = 0.f;  // z = x_hat + beta (x_hat - x_hat)
+  return IDEQ_OK;
+}
+
 ideq_status ideq_set_profiling(ideq_ctx* ctx, int enable) {
   if (!ctx) return IDEQ_E_INVALID;
   ctx->profiling = enable != 0;

@@ -113,6 +113,23 @@ void launch_mri_fill(const float* y, const uint8_t* kmask, float2* spec, int N, 
                      cudaStream_t s);
 void launch_mri_masks(const uint8_t* kmask, float* mhalf, float* dgl, float tau, int H, int W, cudaStream_t s);
 void launch_sub(const float* a, const float* b, float* out, long long n, cudaStream_t s);
+// ---- JFB training gradient (jfb.cu)
+size_t wgrad_workspace(const ConvGeom& g);  // floats of split partials launch_wgrad_geom needs
+void launch_wgrad_geom(const ConvGeom& g, const float* in, const float* gout, float* dB, float* ws, cudaStream_t s);
+size_t headtail_wgrad_workspace(int N, int C, int H, int wf);
+void launch_head_wgrad(const float* img, const float* gf, float* dW, float* ws, int N, int C, int H, int W, int wf,
+                       cudaStream_t s);
+void launch_tail_wgrad(const float* f, const float* gimg, float* dW, float* ws, int N, int C, int H, int W, int wf,
+                       cudaStream_t s);
+void launch_sp_forward(const float* p, float* a, long long n, cudaStream_t s);
+void launch_sp_tangent(const float* a, const float* pd, float* ad, long long n, cudaStream_t s);
+void launch_sp_reverse(const float* a, const float* pd, const float* ab, const float* adb, float* pb, float* pdb,
+                       long long n, cudaStream_t s);
+void launch_scale(float* x, float s, long long n, cudaStream_t st);
+void launch_jfb_residual(const float* z, const float* xs, const float* gg, const float* gf, const float* y,
+                         const uint8_t* mask, int prox, float lam, float tau, long long n, long long HW, long long CHW,
+                         float* v, float* terms, cudaStream_t s);
+void launch_sums(const float* x, long long n, int k, double* part, double* out, cudaStream_t s);
 void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s);
 void launch_avg_out(const int* k0, const int* status, const int* iters, int K, const float* Xsnap, float* X, int N,
                     long long d, cudaStream_t s);

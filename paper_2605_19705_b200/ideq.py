@@ -62,7 +62,8 @@ class Profile(C.Structure):
 
 SYMBOLS = ["ideq_get_nccl_id", "ideq_create", "ideq_set_operator", "ideq_solve", "ideq_solve_host", "ideq_grad_g",
            "ideq_fidelity_grad", "ideq_fidelity_prox", "ideq_set_profiling", "ideq_get_profile",
-           "ideq_launches_per_iteration", "ideq_last_error", "ideq_destroy", "ideq_abi_version", "ideq_debug_conv"]
+           "ideq_launches_per_iteration", "ideq_last_error", "ideq_destroy", "ideq_abi_version", "ideq_debug_conv",
+           "ideq_jfb_grad"]
 
 _lib = None
 
@@ -268,6 +269,16 @@ class Solver:
 
     def fidelity_prox(self, y, v, tau, out):
         self._check(self.lib.ideq_fidelity_prox(self.ctx, _ptr(y), _ptr(v), float(tau), _ptr(out), v.shape[0]))
+
+    def jfb_grad(self, y, x_hat, x_star, params):
+        """JFB gradient at x_hat (include/ideq.h ideq_jfb_grad): (loss, dtheta[n_weights], dlam, dtau, dbeta)."""
+        dth = np.zeros(self._w.size, dtype=np.float32)
+        out = [C.c_float() for _ in range(4)]
+        self._check(self.lib.ideq_jfb_grad(self.ctx, _ptr(y), _ptr(x_hat), _ptr(x_star), x_hat.shape[0],
+                                           C.byref(params), dth.ctypes.data_as(C.c_void_p),
+                                           *[C.byref(o) for o in out]))
+        dlam, dtau, dbeta, loss = (o.value for o in out)
+        return loss, dth, dlam, dtau, dbeta
 
     # ---------------------------------------------------------------- profiling
     def set_profiling(self, on: bool):
