@@ -84,6 +84,12 @@ struct DevBuf {
 
 struct ideq_ctx {
   int device = 0;
+  // ideq_jfb_grad scratch, reused across calls: the tape blocks in allocation order, the split
+  // partials of the weight-gradient reductions
+  std::vector<std::pair<void*, size_t>> jfb_pool;
+  float* jfb_ws = nullptr;
+  size_t jfb_ws_n = 0;
+  std::map<std::string, std::vector<uint32_t>> jfb_map;  // operand index -> blob index per layer
   cudaStream_t stream = nullptr;
   ideq_precision prec = IDEQ_PREC_FP32;
   ideq_net_desc net{};
@@ -1559,31 +1565,35 @@ struct JfbRun {
   ideq_ctx* ctx;
   int N;
   cudaStream_t s;
-  std::vector<void*> mem;
   std::map<std::string, float*> dw;  // per weight tensor: gradient in the layer's operand / blob layout
   WeightSlices ws;
   ideq_status st = IDEQ_OK;
-  float* wsp = nullptr;  // split partials of the weight-gradient reductions (grown on demand)
-  size_t wsp_n = 0;
 
+  size_t nbuf = 0;  // tape blocks handed out by this call (index into ctx->jfb_pool)
   float* work(size_t n) {
-    if (n > wsp_n) {
-      if (wsp) { cudaStreamSynchronize(s); cudaFree(wsp); wsp = nullptr; }
-      if (cudaMalloc(&wsp, n * sizeof(float)) != cudaSuccess) { cudaGetLastError(); st = IDEQ_E_NOMEM; wsp_n = 0; return nullptr; }
-      wsp_n = n;
+    if (n > ctx->jfb_ws_n) {
+      if (ctx->jfb_ws) { cudaStreamSynchronize(s); cudaFree(ctx->jfb_ws); ctx->jfb_ws = nullptr; ctx->jfb_ws_n = 0; }
+      if (cudaMalloc(&ctx->jfb_ws, n * sizeof(float)) != cudaSuccess) {
+        cudaGetLastError(); ctx->jfb_ws = nullptr; st = IDEQ_E_NOMEM; return nullptr;
+      }
+      ctx->jfb_ws_n = n;
     }
-    return wsp;
+    return ctx->jfb_ws;
   }
+  // zeroed device block; the i-th request of a call reuses the i-th block of the previous call
+  // when it is large enough (the request sequence depends only on the shapes)
   float* buf(size_t n) {
-    void* p = nullptr;
-    if (cudaMalloc(&p, (n ? n : 1) * sizeof(float)) != cudaSuccess) { cudaGetLastError(); st = IDEQ_E_NOMEM; return nullptr; }
-    cudaMemsetAsync(p, 0, (n ? n : 1) * sizeof(float), s);
-    mem.push_back(p);
-    return (float*)p;
-  }
-  ~JfbRun() {
-    for (void* p : mem) cudaFree(p);
-    if (wsp) cudaFree(wsp);
+    const size_t bytes = (n ? n : 1) * sizeof(float);
+    auto& pool = ctx->jfb_pool;
+    if (nbuf == pool.size()) pool.push_back({nullptr, 0});
+    auto& b = pool[nbuf++];
+    if (b.second < bytes) {
+      if (b.first) { cudaStreamSynchronize(s); cudaFree(b.first); b = {nullptr, 0}; }
+      if (cudaMalloc(&b.first, bytes) != cudaSuccess) { cudaGetLastError(); st = IDEQ_E_NOMEM; return nullptr; }
+      b.second = bytes;
+    }
+    cudaMemsetAsync(b.first, 0, bytes, s);
+    return (float*)b.first;
   }
 
   // shape-derived GEMM quantities of a layer, as in add_gemm_w
@@ -1686,12 +1696,9 @@ ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, con
   float* gf = J.buf(nimg);
   float* v = J.buf(nimg);
   float* terms = J.buf(3 * nimg);
-  double* dsum = nullptr;
-  double* dpart = nullptr;
-  if (J.st || cudaMalloc(&dsum, 4 * sizeof(double)) != cudaSuccess || cudaMalloc(&dpart, 3 * 256 * sizeof(double)) != cudaSuccess)
-    return fail(ctx, IDEQ_E_NOMEM, "JFB workspace");
-  J.mem.push_back(dsum);
-  J.mem.push_back(dpart);
+  double* dsum = (double*)J.buf(8);          // 4 doubles
+  double* dpart = (double*)J.buf(2 * 3 * 256);  // 3 x 256 doubles
+  if (J.st) return fail(ctx, IDEQ_E_NOMEM, "JFB workspace");
   if ((st = ideq_grad_g(ctx, x_hat, gg, U, batch))) return st;
   if (!prox && (st = ideq_fidelity_grad(ctx, y, x_hat, gf, batch))) return st;
   launch_jfb_residual(x_hat, x_star, gg, gf, y, ctx->d_mask, prox ? 1 : 0, p->lambda, p->tau, nimg, (long long)H * W,
@@ -1862,11 +1869,15 @@ ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, con
     int ncols, ktap, cin;
     J.dims(kind, shp, ncols, ktap, cin);
     const int KC = pick_kc(false, ktap);
-    // operand index of every blob element: gemm_weights applied to the blob positions themselves
-    std::vector<float> pos(nw);
-    for (size_t i = 0; i < nw; ++i) pos[i] = (float)i;
-    int nc2, nt2, kt2;
-    std::vector<float> map = gemm_weights(kind, pos.data(), shp, KC, nc2, nt2, kt2);
+    // operand index -> blob index: gemm_weights applied to the blob positions themselves (cached)
+    std::vector<uint32_t>& map = ctx->jfb_map[name];
+    if (map.empty()) {
+      std::vector<float> pos(nw);
+      for (size_t i = 0; i < nw; ++i) pos[i] = (float)i;  // exact: nw < 2^24
+      int nc2, nt2, kt2;
+      std::vector<float> m = gemm_weights(kind, pos.data(), shp, KC, nc2, nt2, kt2);
+      map.assign(m.begin(), m.end());
+    }
     const size_t nb = map.size();
     launch_scale(kv.second, scale, (long long)nb, s);
     host.resize(nb);
@@ -1968,6 +1979,8 @@ void ideq_destroy(ideq_ctx* ctx) {
   if (ctx->gexec_check) cudaGraphExecDestroy(ctx->gexec_check);
   for (auto& L : ctx->prog) if (L.plan) tc_free_plan(L.plan);
   for (auto& a : ctx->allocs) cudaFree(a.p);
+  for (auto& b : ctx->jfb_pool) cudaFree(b.first);
+  if (ctx->jfb_ws) cudaFree(ctx->jfb_ws);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   if (ctx->comm && g_nccl.CommDestroy) g_nccl.CommDestroy(ctx->comm);

@@ -16,35 +16,87 @@ namespace ideq {
 
 // dB[kb][col][k] += sum_{n, oh, ow} in(n, oh + dh[tap], ow + dw[tap], dp[tap], chunk*KC + k)
 //                                    * gout[out_offset(n, oh, ow, col)]
-// i.e. the gradient of <gout, layer(in)> w.r.t. the layer's GEMM operand B. Two passes, both in a
-// fixed order (deterministic): blockIdx.y splits the N*OH*OW output pixels into S contiguous
-// ranges, one thread per (kb, col, k) and range writes a partial; the second kernel adds the S
-// partials in range order. Consecutive threads walk k (consecutive input channels: coalesced), a
-// warp shares each gout element.
-__global__ void __launch_bounds__(256) wgrad_geom_kernel(ConvGeom g, const float* __restrict__ in,
-                                                         const float* __restrict__ gout, float* __restrict__ part,
-                                                         long long per) {
-  const long long total = (long long)g.ntaps * g.nchunk * g.ncols * g.KC;
-  const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int k = (int)(idx % g.KC);
-  const int col = (int)((idx / g.KC) % g.ncols);
-  const int kb = (int)(idx / ((long long)g.KC * g.ncols));
-  const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
-  const int c = chunk * g.KC + k;
+// i.e. the gradient of <gout, layer(in)> w.r.t. the layer's GEMM operand B: per tap a
+// [ncols x ktap] = G^T A contraction over the N*OH*OW output pixels. Tiled FFMA GEMM: a CTA owns a
+// TM x TN (cols x channels) tile of one tap and a contiguous pixel range (blockIdx.y); each step
+// stages P = 32 pixels of G (gout columns) and A (shifted input channels, float4 loads) in shared
+// memory, every thread accumulates a 4 x 4 register block. Partials per pixel range are summed in
+// range order by wgrad_sum_kernel (fixed order: deterministic).
+template <int TM, int TN>
+__global__ void __launch_bounds__(TM * TN / 16) wgrad_tile_kernel(ConvGeom g, const float* __restrict__ in,
+                                                                  const float* __restrict__ gout,
+                                                                  float* __restrict__ part, long long per, int ktap) {
+  constexpr int P = 32, NT = TM * TN / 16, TX = TN / 4;
+  __shared__ __align__(16) float sG[P][TM];
+  __shared__ __align__(16) float sA[P][TN];
+  __shared__ long long sGo[P], sAo[P];
+  const int ncb = g.ncols / TM, nkb = ktap / TN;
+  int bid = blockIdx.x;
+  const int cb = bid % ncb;
+  bid /= ncb;
+  const int kb2 = bid % nkb, tap = bid / nkb;
+  const int col0 = cb * TM, c0 = kb2 * TN;
   const long long npix = (long long)g.N * g.OH * g.OW;
-  const long long p0 = blockIdx.y * per, p1 = p0 + per < npix ? p0 + per : npix;
-  float acc = 0.f;
-  for (long long q = p0; q < p1; ++q) {
-    const int ow = (int)(q % g.OW);
-    const long long r = q / g.OW;
-    const int oh = (int)(r % g.OH), n = (int)(r / g.OH);
-    const int h = oh + g.dh[tap], w = ow + g.dw[tap];
-    if (h < 0 || h >= g.inH || w < 0 || w >= g.inW) continue;
-    const float x = in[((((long long)n * g.inH + h) * g.inP + g.dp[tap]) * g.inW + w) * g.inC + c];
-    acc = fmaf(x, gout[out_offset(g, n, oh, ow, col)], acc);
+  const long long q0 = blockIdx.y * per, q1 = q0 + per < npix ? q0 + per : npix;
+  const int tid = threadIdx.x, tx = tid % TX, ty = tid / TX;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (long long qb = q0; qb < q1; qb += P) {
+    for (int p = tid; p < P; p += NT) {
+      const long long q = qb + p;
+      long long go = -1, ao = -1;
+      if (q < q1) {
+        const int ow = (int)(q % g.OW);
+        const long long r = q / g.OW;
+        const int oh = (int)(r % g.OH), n = (int)(r / g.OH);
+        go = out_offset(g, n, oh, ow, 0);
+        const int h = oh + g.dh[tap], w = ow + g.dw[tap];
+        if (h >= 0 && h < g.inH && w >= 0 && w < g.inW)
+          ao = ((((long long)n * g.inH + h) * g.inP + g.dp[tap]) * g.inW + w) * g.inC;
+      }
+      sGo[p] = go;
+      sAo[p] = ao;
+    }
+    __syncthreads();
+    for (int e = tid; e < P * TN / 4; e += NT) {
+      const int p = e / (TN / 4), c4 = e % (TN / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (sAo[p] >= 0) v = __ldg(reinterpret_cast<const float4*>(in + sAo[p] + c0 + c4 * 4));
+      *reinterpret_cast<float4*>(&sA[p][c4 * 4]) = v;
+    }
+    for (int e = tid; e < P * TM; e += NT) {
+      const int p = e / TM, cc = e % TM, col = col0 + cc;
+      float v = 0.f;
+      if (sGo[p] >= 0) v = __ldg(gout + sGo[p] + (long long)(col / g.CB) * g.OWo * g.OCp + col % g.CB);
+      sG[p][cc] = v;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int p = 0; p < P; ++p) {
+      const float4 gv = *reinterpret_cast<const float4*>(&sG[p][ty * 4]);
+      const float4 av = *reinterpret_cast<const float4*>(&sA[p][tx * 4]);
+      const float gg[4] = {gv.x, gv.y, gv.z, gv.w}, aa[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(gg[i], aa[j], acc[i][j]);
+    }
+    __syncthreads();
   }
-  part[blockIdx.y * total + idx] = acc;
+  const long long total = (long long)g.ntaps * g.nchunk * g.ncols * g.KC;
+  float* dst = part + blockIdx.y * total;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int col = col0 + ty * 4 + i;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + tx * 4 + j;
+      dst[((long long)(tap * g.nchunk + c / g.KC) * g.ncols + col) * g.KC + c % g.KC] = acc[i][j];
+    }
+  }
 }
 __global__ void wgrad_sum_kernel(const float* __restrict__ part, int S, long long total, float* __restrict__ dB) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
@@ -54,24 +106,47 @@ __global__ void wgrad_sum_kernel(const float* __restrict__ part, int S, long lon
   }
 }
 
-// pixel splits: enough (kb, col, k, split) threads for ~4 waves, each range >= 256 pixels
-static int wgrad_splits(long long total, long long npix) {
-  long long S = (148LL * 2048 * 4 + total - 1) / total;
-  const long long smax = (npix + 255) / 256;
+static int tile_dim(int n) { return n % 64 == 0 ? 64 : n % 32 == 0 ? 32 : 16; }
+// pixel ranges: ~2048 threads per SM of (tile, range) CTAs, each range >= 128 pixels
+static int wgrad_splits(const ConvGeom& g, long long* per_out) {
+  const int ktap = g.nchunk * g.KC, TM = tile_dim(g.ncols), TN = tile_dim(ktap);
+  const long long blocks = (long long)g.ntaps * (g.ncols / TM) * (ktap / TN), nt = TM * TN / 16;
+  const long long npix = (long long)g.N * g.OH * g.OW;
+  long long S = (148LL * 2048 + blocks * nt - 1) / (blocks * nt);
+  const long long smax = (npix + 127) / 128;
   if (S > smax) S = smax;
   if (S > 1024) S = 1024;
-  return (int)(S < 1 ? 1 : S);
+  if (S < 1) S = 1;
+  const long long per = (npix + S - 1) / S;
+  if (per_out) *per_out = per;
+  return (int)((npix + per - 1) / per);
 }
 size_t wgrad_workspace(const ConvGeom& g) {
   const long long total = (long long)g.ntaps * g.nchunk * g.ncols * g.KC;
-  return (size_t)wgrad_splits(total, (long long)g.N * g.OH * g.OW) * total;
+  return (size_t)wgrad_splits(g, nullptr) * total;
+}
+template <int TM, int TN>
+static void wgrad_tile(const ConvGeom& g, const float* in, const float* gout, float* ws, long long per, int S,
+                       cudaStream_t s) {
+  const int ktap = g.nchunk * g.KC;
+  const unsigned blocks = (unsigned)(g.ntaps * (g.ncols / TM) * (ktap / TN));
+  wgrad_tile_kernel<TM, TN><<<dim3(blocks, S), TM * TN / 16, 0, s>>>(g, in, gout, ws, per, ktap);
+}
+template <int TM>
+static void wgrad_tile_n(int TN, const ConvGeom& g, const float* in, const float* gout, float* ws, long long per,
+                         int S, cudaStream_t s) {
+  if (TN == 64) wgrad_tile<TM, 64>(g, in, gout, ws, per, S, s);
+  else if (TN == 32) wgrad_tile<TM, 32>(g, in, gout, ws, per, S, s);
+  else wgrad_tile<TM, 16>(g, in, gout, ws, per, S, s);
 }
 void launch_wgrad_geom(const ConvGeom& g, const float* in, const float* gout, float* dB, float* ws, cudaStream_t s) {
   const long long total = (long long)g.ntaps * g.nchunk * g.ncols * g.KC;
-  const long long npix = (long long)g.N * g.OH * g.OW;
-  const int S = wgrad_splits(total, npix);
-  const long long per = (npix + S - 1) / S;
-  wgrad_geom_kernel<<<dim3((unsigned)((total + 255) / 256), S), 256, 0, s>>>(g, in, gout, ws, per);
+  long long per = 0;
+  const int S = wgrad_splits(g, &per);
+  const int TM = tile_dim(g.ncols), TN = tile_dim(g.nchunk * g.KC);
+  if (TM == 64) wgrad_tile_n<64>(TN, g, in, gout, ws, per, S, s);
+  else if (TM == 32) wgrad_tile_n<32>(TN, g, in, gout, ws, per, S, s);
+  else wgrad_tile_n<16>(TN, g, in, gout, ws, per, S, s);
   long long gb = (total + 255) / 256;
   wgrad_sum_kernel<<<(unsigned)(gb > 148 * 8 ? 148 * 8 : gb), 256, 0, s>>>(ws, S, total, dB);
 }
