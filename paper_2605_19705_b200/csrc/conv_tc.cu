@@ -27,6 +27,13 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#ifndef IDEQ_SP_MUFU
+#define IDEQ_SP_MUFU 0
+#endif
+#ifndef IDEQ_DSP_MUFU
+#define IDEQ_DSP_MUFU 0
+#endif
+
 namespace ideq {
 
 // ------------------------------------------------------------------ PTX helpers
@@ -275,17 +282,40 @@ __device__ __forceinline__ float exp2_fma(float x) {
 }
 // softplus: one exponential + a degree-6 polynomial for log1p (|err| < 1.5e-6, far below the
 // bf16 rounding of the output). POLY selects the FMA-pipe exponential.
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2_approx(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 template <bool POLY = false>
 __device__ __forceinline__ float softplus_fast(float t) {
+#if IDEQ_SP_MUFU
+  // max(t, 0) + ln2 * log2(1 + 2^(-|t| log2 e)): two MUFU ops and 4 FMA/ALU instructions
+  // (lg2.approx abs. error ~1e-7 on [1, 2], far below the bf16 rounding of the output)
+  const float u = ex2_approx(-1.4426950408889634f * fabsf(t));
+  return fmaf(0.6931471805599453f, lg2_approx(1.f + u), fmaxf(t, 0.f));
+#else
   const float u = POLY ? exp2_fma(-1.4426950408889634f * fabsf(t)) : __expf(-fabsf(t));
   return fmaxf(t, 0.f) + log1p01(u);
+#endif
 }
 // sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a to avoid the
 // cancellation of 1 - exp(-a) (bf16-mode outputs are rounded to bf16, rel. 2^-9).
 template <bool POLY = false>
 __device__ __forceinline__ float dsoftplus_from_act_fast(float a) {
+#if IDEQ_DSP_MUFU
+  // 1 - 2^(-a log2 e): the absolute error ~2e-7 of ex2.approx near a = 0 is negligible against
+  // the O(1) sp' of the other channels in the sum this factor feeds (and the bf16 rounding)
+  return 1.f - ex2_approx(-1.4426950408889634f * a);
+#else
   const float e = POLY ? exp2_fma(-1.4426950408889634f * a) : __expf(-a);
   return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - e;
+#endif
 }
 
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3,

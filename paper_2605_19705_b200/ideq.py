@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libideq.so")
+LIB_PATH = os.environ.get("IDEQ_LIB") or os.path.join(_HERE, "lib", "libideq.so")  # IDEQ_LIB: A/B builds
 
 # ---- enums (include/ideq.h)
 OK, E_INVALID, E_DIVERGED, E_UNSUPPORTED, E_CUDA, E_NCCL, E_NOMEM, E_STATE = range(8)
