@@ -28,10 +28,10 @@
 #include "kernels.h"
 
 #ifndef IDEQ_SP_MUFU
-#define IDEQ_SP_MUFU 0
+#define IDEQ_SP_MUFU 1
 #endif
 #ifndef IDEQ_DSP_MUFU
-#define IDEQ_DSP_MUFU 0
+#define IDEQ_DSP_MUFU 1
 #endif
 
 namespace ideq {
