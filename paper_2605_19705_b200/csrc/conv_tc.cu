@@ -373,6 +373,12 @@ struct TcParams {
   // per-image active flags of the solver (null: compute every tile). Tiles of frozen images are
   // skipped by every warp role alike, so the barrier rings stay in step (not used by CTA pairs).
   const int* active;
+  // direct epilogue (opt-in, 3x3 halo layers with BN <= 64): the aux operand is read from global
+  // memory into registers and the outputs are stored from registers (NHWC rows of ncols
+  // channels), bypassing the shared-memory staging + TMA store + aux TMA of the default path
+  int direct;
+  __nv_bfloat16* out_ptr;
+  const __nv_bfloat16* aux_ptr;
 };
 
 // Frozen-image test on the shared bitmask, broadcast from lane 0 so that the compiler keeps the
@@ -408,6 +414,16 @@ __device__ __forceinline__ uint32_t epi_chunk_addr(uint32_t box_base, int r, int
   return box_base + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
 }
 
+__device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_global_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -602,7 +618,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     // ---------------- aux producer: the epilogue's second operand (residual / saved activation)
     // goes into the tile's epilogue buffer as soon as that buffer's previous store has been read,
     // without ever stalling the operand producer behind the epilogue
-    if (HAS_AUX) {
+    if (HAS_AUX && !P.direct) {
       int acc = 0;
       uint32_t aph = 0;
       for (int t = t0; t < total; t += tstep) {
@@ -879,6 +895,73 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
       if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
+      if (EPI != EPI_IMG && !PAIR && P.direct) {
+        // ---- direct epilogue (BN <= 64: this thread's half row is 16 or 32 columns)
+        const int oh = h0 + row / g.Wt, ow = w0 + row % g.Wt;
+        const bool valid = row < g.R * g.Wt && oh < g.OH && ow < g.OW;
+        const long long pix = ((long long)img * g.OH + oh) * g.OW + ow;
+        const long long cofs = pix * g.ncols + (long long)nt * BN + cbeg;
+        const int ngrp = (cend - cbeg) >> 4;  // 16-column groups: 1 or 2
+        uint4 ax[4];
+        if (HAS_AUX) {  // issued before the accumulator wait: the loads overlap this tile's MMAs
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ax[i] = make_uint4(0u, 0u, 0u, 0u);
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              if (i < 2 * ngrp) ax[i] = ld_global_nc_v4(P.aux_ptr + cofs + i * 8);
+          }
+        }
+        mbar_wait(tfull0 + 8u * acc, aph);
+        tc_fence_after();
+        uint32_t r[2][16];
+        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cbeg);
+        tmem_ld16_nw(tb, r[0]);
+        if (ngrp == 2) tmem_ld16_nw(tb + 16u, r[1]);
+        tmem_wait();
+        // the accumulator is in registers: the MMA warp may reuse this TMEM stage
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+#pragma unroll
+        for (int gi = 0; gi < 2; ++gi) {
+          if (gi < ngrp) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              float o[8];
+              if (HAS_AUX) {
+                const uint4 u = ax[gi * 2 + q];
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(h2[e]);
+                  const float v0 = __uint_as_float(r[gi][q * 8 + 2 * e]), v1 = __uint_as_float(r[gi][q * 8 + 2 * e + 1]);
+                  if (EPI == EPI_RESADD) {
+                    o[2 * e] = v0 + f.x;
+                    o[2 * e + 1] = v1 + f.y;
+                  } else {
+                    o[2 * e] = v0 * dsoftplus_from_act_fast<false>(f.x);
+                    o[2 * e + 1] = v1 * dsoftplus_from_act_fast<false>(f.y);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const float v = __uint_as_float(r[gi][q * 8 + e]);
+                  o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v) : v;
+                }
+              }
+              uint4 w;
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+              if (valid) st_global_v4(P.out_ptr + cofs + gi * 16 + q * 8, w);
+            }
+          }
+        }
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
+        continue;
+      }
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
         mbar_wait(auxfull0 + 8u * acc, aph);
@@ -1431,6 +1514,18 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.stages = stages;
   P.nacc = nacc;
   P.tmem_cols = tcols;
+  {
+    // opt-in (IDEQ_DIRECT=1): correct (the GPU suite passes with it on) but measured 30% SLOWER on
+    // the C3 bench (7.27k vs 10.27k img-it/s): register-to-global 16-byte stores at a 64-byte pixel
+    // stride use the same L1/shared data path at half sector efficiency, so they cost more than the
+    // staged tile + TMA store they replace
+    static const bool want_direct = [] { const char* e = getenv("IDEQ_DIRECT"); return e && atoi(e) != 0; }();
+    P.direct = (want_direct && (p->halo == 1 || p->halo == 2) && g.epi != EPI_IMG && (BN == 32 || BN == 64) &&
+                g.osh == 1 && g.osw == 1 && g.CB == g.ncols && g.OCp == g.ncols && g.OHo == g.OH && g.OWo == g.OW)
+                   ? 1 : 0;
+    P.out_ptr = out;
+    P.aux_ptr = aux;
+  }
   p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + xbytes + 512 + (size_t)stages * op_stage;
   if (p->halo == 3) {  // units of (2 M tiles, 1 N tile); two CTAs (one cluster) per unit
     const int units = ((P.m_tiles + 1) / 2) * P.n_tiles;
