@@ -326,6 +326,12 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t sr
       "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t src, int c0, int c1) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -1095,12 +1101,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 template <int NC>
 __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restrict__ in,
                                                           const __nv_bfloat16* __restrict__ wB,
-                                                          __nv_bfloat16* __restrict__ out, int N, int C, int H,
-                                                          int W, const FastDiv fdHW, const FastDiv fdW,
+                                                          const __grid_constant__ CUtensorMap tmO, int N, int C,
+                                                          int H, int W, const FastDiv fdHW, const FastDiv fdW,
                                                           const int* __restrict__ active) {
   __shared__ __align__(1024) unsigned char sAraw[2][128 * 64];
   __shared__ __align__(1024) unsigned char sBraw[NC * 64];
-  extern __shared__ __align__(1024) unsigned char sOdyn[];  // output staging [2][128 * NC * 2] (bulk-copied)
+  // output staging [2][128 pixels x NC] in the TMA store's swizzle (SW64 for NC = 32, SW128 for
+  // 64): conflict-free 16-byte writes (a linear layout at a 64/128-byte pixel stride put 8 lanes
+  // on 2 / 1 bank groups), un-swizzled by the TMA tensor store
+  extern __shared__ __align__(1024) unsigned char sOraw[];
+  unsigned char* sOdyn = sOraw + ((1024u - (smem_u32(sOraw) & 1023u)) & 1023u);
   __shared__ __align__(8) uint64_t bar[2];
   __shared__ uint32_t tmem_holder;
   const int tid = threadIdx.x;
@@ -1132,7 +1142,6 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   const long long tiles = (total + 127) / 128;
   const uint32_t idesc = make_idesc_bf16(NC);
   const uint64_t dB = make_sdesc(sB, 512u, 4u);
-  constexpr uint32_t ROWB = NC * 2;  // output bytes per pixel
   // 32-bit pixel indexing (N*H*W < 2^31 for every supported size) with multiply-shift division
   // the patch of the NEXT tile is loaded into registers before this tile's MMA/epilogue, so the
   // global-load latency overlaps the tensor-core round trip and the staging of the output
@@ -1195,11 +1204,8 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     __syncthreads();
     tc_fence_after();
     if (tid == 0) {
-      if (t_prev >= 0) {  // the previous tile's staged output: one bulk copy
-        const long long np = total - t_prev * 128 < 128 ? total - t_prev * 128 : 128;
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t_prev * 128 * NC),
-                     "r"(smem_u32(sOdyn + (buf ^ 1) * 128 * NC * 2)), "r"((uint32_t)(np * ROWB))
-                     : "memory");
+      if (t_prev >= 0) {  // the previous tile's staged output: one TMA tensor store (rows past the end clipped)
+        tma_store_2d(&tmO, smem_u32(sOdyn + (buf ^ 1) * 128 * NC * 2), 0, (int)(t_prev * 128));
         bulk_commit();
       }
       // the staging buffer this tile writes was bulk-copied one tile ago: wait until it was read
@@ -1215,7 +1221,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     mbar_wait(smem_u32(&bar[buf]), (uint32_t)((it >> 1) & 1));
     __syncthreads();  // thread 0 has waited for the staging buffer's previous bulk copy
     tc_fence_after();
-    const uint32_t so = smem_u32(sOdyn + buf * 128 * NC * 2) + (uint32_t)tid * ROWB;
+    const uint32_t so = smem_u32(sOdyn + buf * 128 * NC * 2);
 #pragma unroll
     for (int c0 = 0; c0 < NC; c0 += 16) {
       float r[16];
@@ -1226,7 +1232,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
         __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&wv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(r[q * 8 + 2 * e], r[q * 8 + 2 * e + 1]);
-        st_shared_v4(so + (uint32_t)(c0 + q * 8) * 2u, wv);
+        st_shared_v4(epi_chunk_addr<NC>(so, tid, c0 / 8 + q), wv);
       }
     }
     tc_fence_before();
@@ -1236,10 +1242,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   __syncthreads();
   if (tid == 0) {
     if (t_prev >= 0) {
-      const long long np = total - t_prev * 128 < 128 ? total - t_prev * 128 : 128;
-      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + t_prev * 128 * NC),
-                   "r"(smem_u32(sOdyn + ((it - 1) & 1) * 128 * NC * 2)), "r"((uint32_t)(np * ROWB))
-                   : "memory");
+      tma_store_2d(&tmO, smem_u32(sOdyn + ((it - 1) & 1) * 128 * NC * 2), 0, (int)(t_prev * 128));
       bulk_commit();
     }
     bulk_wait0();
@@ -1248,23 +1251,6 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * NC))
                  : "memory");
-}
-
-void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, const int* active, int N, int C,
-                        int H, int W,
-                        int NC, int num_sms, cudaStream_t s) {
-  // the static shared memory (54 KB / 36 KB) caps residency so that the CTAs' TMEM allocations
-  // (2 x NC columns each) never exceed the SM's 512 columns
-  const int per_sm = NC == 64 ? 4 : 6;   // static smem admits at most 4 (NC 64) / 6 (NC 32) CTAs per SM
-  const size_t pad = (size_t)2 * 128 * NC * 2;  // output staging
-  const long long tiles = ((long long)N * H * W + 127) / 128;
-  const long long cap = (long long)num_sms * per_sm;
-  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
-  FastDiv fdHW, fdW;
-  fdHW.init((uint32_t)(H * W));
-  fdW.init((uint32_t)W);
-  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW, active);
-  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, out, N, C, H, W, fdHW, fdW, active);
 }
 
 // ------------------------------------------------------------------ host side
@@ -1282,6 +1268,42 @@ static EncodeTiledFn get_encode() {
       fn = reinterpret_cast<EncodeTiledFn>(p);
   }
   return fn;
+}
+
+// output [pixels][NC] bf16 as a 2-D tensor, 128-pixel boxes in the staging swizzle (encoded once,
+// when the program is built)
+struct I2FPlan { CUtensorMap tmO; };
+I2FPlan* img2feat_make_plan(__nv_bfloat16* out, int N, int H, int W, int NC, char* err, size_t errlen) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc) { snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable"); return nullptr; }
+  I2FPlan* p = new I2FPlan();
+  const long long total = (long long)N * H * W;
+  cuuint64_t dims[2] = {(cuuint64_t)NC, (cuuint64_t)total};
+  cuuint64_t strides[1] = {(cuuint64_t)NC * 2};
+  cuuint32_t box[2] = {(cuuint32_t)NC, 128u};
+  cuuint32_t es[2] = {1, 1};
+  const CUresult r = enc(&p->tmO, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, out, dims, strides, box, es,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, NC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) { snprintf(err, errlen, "img2feat output tensor map encode failed (%d)", (int)r); delete p; return nullptr; }
+  return p;
+}
+void img2feat_free_plan(I2FPlan* p) { delete p; }
+
+void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* active, int N, int C,
+                        int H, int W, int NC, int num_sms, cudaStream_t s) {
+  // the static shared memory (54 KB / 36 KB) caps residency so that the CTAs' TMEM allocations
+  // (2 x NC columns each) never exceed the SM's 512 columns
+  const int per_sm = NC == 64 ? 4 : 6;   // static smem admits at most 4 (NC 64) / 6 (NC 32) CTAs per SM
+  const size_t pad = (size_t)2 * 128 * NC * 2 + 1024;  // output staging (+ alignment slack)
+  const long long total = (long long)N * H * W, tiles = (total + 127) / 128;
+  const long long cap = (long long)num_sms * per_sm;
+  const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
+  FastDiv fdHW, fdW;
+  fdHW.init((uint32_t)(H * W));
+  fdW.init((uint32_t)W);
+  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
+  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
 }
 
 struct TcPlan {

@@ -69,6 +69,7 @@ struct Layer {
   float alpha = 0.f;
   int C = 0, wfeat = 0, epi = 0, N = 0, H = 0, W = 0;
   TcPlan* plan = nullptr;
+  I2FPlan* i2f = nullptr;  // fused head (L_IMG2FEAT_TC): output tensor map
   bool tc = false;  // tcgen05 path (bf16 U-Net layers) vs FFMA path
   bool headtail = false;  // head/tail layer (profiled in the head/tail class, not the conv roofline)
   double flops = 0, bytes = 0;
@@ -512,6 +513,11 @@ ideq_status add_tc_img2feat(ideq_ctx* ctx, const std::string& wname, bool adjoin
   L.N = N; L.C = ctx->C; L.H = ctx->H; L.W = ctx->W;
   L.wfeat = wo;
   L.headtail = true;
+  {
+    char err[256] = {0};
+    L.i2f = img2feat_make_plan((__nv_bfloat16*)out_feat, N, ctx->H, ctx->W, wo, err, sizeof(err));
+    if (!L.i2f) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
+  }
   L.flops = 2.0 * N * ctx->H * ctx->W * 9.0 * ci * wo;
   L.bytes = (double)N * ctx->H * ctx->W * (4.0 * ctx->C + 2.0 * wo);
   ctx->prog.push_back(L);
@@ -606,7 +612,7 @@ std::string rb(const char* p, int l, int r, const char* ab) {
 // Build the forward + VJP program for batch N (buffers sized for maxN at create).
 ideq_status build_program(ideq_ctx* ctx, int N) {
   if (ctx->prog_batch == N) return IDEQ_OK;
-  for (auto& L : ctx->prog) if (L.plan) tc_free_plan(L.plan);
+  for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
   ctx->prog.clear();
   const auto& n = ctx->net;
   const int C = ctx->C;
@@ -789,7 +795,7 @@ void run_layer(ideq_ctx* ctx, const Layer& L) {
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
   if (L.kind == L_IMG2FEAT_TC) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
-    launch_img2feat_tc(L.in_img, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)L.out, ctx->skip_frozen ? ctx->active : nullptr,
+    launch_img2feat_tc(L.i2f, L.in_img, (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->active : nullptr,
                        L.N, L.C, L.H, L.W, L.wfeat, ctx->num_sms, s);
   } else if (L.kind == L_GEMM) {
     if (L.tc) {
@@ -1977,7 +1983,7 @@ void ideq_destroy(ideq_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->gexec_plain) cudaGraphExecDestroy(ctx->gexec_plain);
   if (ctx->gexec_check) cudaGraphExecDestroy(ctx->gexec_check);
-  for (auto& L : ctx->prog) if (L.plan) tc_free_plan(L.plan);
+  for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
   for (auto& a : ctx->allocs) cudaFree(a.p);
   for (auto& b : ctx->jfb_pool) cudaFree(b.first);
   if (ctx->jfb_ws) cudaFree(ctx->jfb_ws);

@@ -164,9 +164,11 @@ void tc_plan_set_active(TcPlan* p, const int* active);
 void tc_plan_enable_skip(TcPlan* p, bool on);
 int tc_plan_is_halo(const TcPlan* p);
 // im2col of a C-channel fp32 NCHW image into [N][H][W][32] bf16: k = c*9 + a*3 + b (zero beyond 9C)
-void launch_img2feat_tc(const float* in, const __nv_bfloat16* wB, __nv_bfloat16* out, const int* active, int N, int C,
-                        int H, int W,
-                        int NC, int num_sms, cudaStream_t s);
+struct I2FPlan;  // fused head: the output tensor map (conv_tc.cu)
+I2FPlan* img2feat_make_plan(__nv_bfloat16* out, int N, int H, int W, int NC, char* err, size_t errlen);
+void img2feat_free_plan(I2FPlan* p);
+void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* active, int N, int C,
+                        int H, int W, int NC, int num_sms, cudaStream_t s);
 
 // Raise the dynamic shared-memory limit of every kernel once (before any graph capture).
 void init_kernel_attributes();
