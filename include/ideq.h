@@ -218,8 +218,9 @@ IDEQ_API ideq_status ideq_fidelity_prox(ideq_ctx* ctx, const float* y, const flo
  * dtheta: HOST, n_weights floats, the blob order of ideq_create; overwritten.
  * dlam, dtau, dbeta, loss: HOST scalars (dbeta = 0 exactly).
  * Requires the fp32 context (IDEQ_PREC_FP32), identity skip and softplus (else
- * IDEQ_E_UNSUPPORTED), a prox step only with the inpainting operator. Synchronous; allocates
- * its tape per call (sized for parity / small-batch training, not the inference hot path). */
+ * IDEQ_E_UNSUPPORTED), a prox step only with the inpainting operator. Synchronous; its tape
+ * (two streams of every activation) lives in a per-context scratch pool that grows on first use
+ * and is reused by later calls of the same shape (freed by ideq_destroy). */
 IDEQ_API ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, const float* x_star,
                                    int batch, const ideq_params* p, float* dtheta, float* dlam,
                                    float* dtau, float* dbeta, float* loss);

@@ -24,7 +24,8 @@ def _dev(torch, a):
 
 CASES = [("C1", "grad", dict(batch=2)),
          ("C3", "grad", dict(batch=2, H=32, W=32, widths=(32, 32, 64, 64))),
-         ("C3", "prox", dict(batch=2, H=32, W=48, widths=(32, 32, 64, 64)))]
+         ("C3", "prox", dict(batch=2, H=32, W=48, widths=(32, 32, 64, 64))),
+         ("C3", "prox", dict(batch=1))]          # full C3 size: 256^2 RGB, U-Net-32 (oracle ~5 s)
 
 
 @pytest.mark.parametrize("name,step,kw", CASES)
@@ -40,6 +41,8 @@ def test_jfb_grad_parity(name, step, kw):
     lam, tau = 0.7, 0.6
     loss, dth, dlam, dtau, dbeta = s.jfb_grad(_dev(torch, prob["y"]), _dev(torch, x_hat), _dev(torch, xs),
                                               s.params(lam=lam, tau=tau))
+    again = s.jfb_grad(_dev(torch, prob["y"]), _dev(torch, x_hat), _dev(torch, xs), s.params(lam=lam, tau=tau))
+    assert np.array_equal(again[1], dth) and again[0] == loss    # pooled scratch reused: deterministic
     net = osolver.make_net(cfg, prob["weights"])
     fids = osolver.make_fidelities(cfg, prob)
     want = [jfb.jfb_grads(net, fids[b], x_hat[b].astype(np.float64), xs[b].astype(np.float64), lam, tau, step)
