@@ -861,7 +861,7 @@ FftArgs make_fft_args(ideq_ctx* ctx, const float* y, const ideq_params* p) {
 
 int step_parts(ideq_ctx* ctx) {
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.blur_impl == IDEQ_BLUR_DIRECT && ctx->op.step == IDEQ_STEP_GRAD)
-    return blur_parts_per_image(ctx->C, ctx->H, ctx->W);
+    return blur_parts_per_image(ctx->C, ctx->H, ctx->W, ctx->op.ksize);
   if ((ctx->op.kind == IDEQ_OP_BLUR || ctx->op.kind == IDEQ_OP_MRI) && ctx->op.step == IDEQ_STEP_PROX)
     return fft_parts_per_image(ctx->C, ctx->H, ctx->W);
   if (ctx->op.kind == IDEQ_OP_PHASE) return phase_parts_per_image(ctx->H, ctx->W);
@@ -1277,7 +1277,7 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
   AL(X1, plane) AL(Z, plane) AL(G, plane) AL(Hc, plane) AL(fbuf, plane) AL(fbuf2, plane)
   {  // residual partials per image: the largest count any fidelity/step kernel can produce at this size
     int pc = 256;
-    const int cand[3] = {blur_parts_per_image(ctx->C, H, W), fft_parts_per_image(ctx->C, H, W),
+    const int cand[3] = {blur_parts_per_image(ctx->C, H, W, 0) /* 32-pixel tiles: the larger count */, fft_parts_per_image(ctx->C, H, W),
                          phase_parts_per_image(H, W)};
     for (int v : cand) pc = v > pc ? v : pc;
     ctx->parts_cap = pc;

@@ -100,7 +100,7 @@ void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int 
 void init_attrs_fft();
 
 void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s);
-int blur_parts_per_image(int C, int H, int W);
+int blur_parts_per_image(int C, int H, int W, int ks);  // residual partials of the direct blur step
 void launch_blur_residual(const StepArgs& a, cudaStream_t s);
 void launch_blur_adjoint(int mode, const StepArgs& a, const float* src, cudaStream_t s);
 void launch_finalize(const FinalizeArgs& f, cudaStream_t s);
