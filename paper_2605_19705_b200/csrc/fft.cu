@@ -24,30 +24,74 @@ __device__ __forceinline__ float2 cconjmul(float2 a, float2 b) {  // conj(a) * b
   return make_float2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
 }
 
-// In-place radix-2 DIT FFT of one length-N row held in shared memory in BIT-REVERSED
-// order. `t` is this thread's index among the `tpr` threads that own the row. Every
-// thread of the block must call this (it synchronises the block between stages).
-// tw[k] = exp(-2 pi i k / N), k < N/2. inverse = unnormalised inverse transform.
+// Shared-memory rows are padded by one float2 per 16 (pd): the bit-reversed scatter of a row
+// (consecutive i -> indices N/32 apart) and the short-stride butterflies of the first passes
+// otherwise fall on 1-2 bank groups (up to 16-way conflicts). Column buffers additionally get an
+// odd pitch so the FFT_CPB columns a warp loads row by row land on different banks.
+__host__ __device__ __forceinline__ int pd(int i) { return i + (i >> 4); }
+__host__ __device__ __forceinline__ int row_pitch(int N) { return N + N / 16; }
+__host__ __device__ __forceinline__ int col_pitch(int N) { return N + N / 16 + 1; }
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+
+// In-place DIT FFT of one length-N row held in shared memory in BIT-REVERSED order. `t` is this
+// thread's index among the `tpr` threads that own the row. Every thread of the block must call
+// this (it synchronises the block between passes). tw[k] = exp(-2 pi i k / N), k < N/2.
+// inverse = unnormalised inverse transform. The radix-2 stages are fused in pairs (radix-4
+// passes: each thread combines 4 points in registers through both stages), so a 256-point row
+// takes 4 shared-memory round trips and barriers instead of 8; an odd log N starts with one
+// radix-2 pass.
 __device__ __forceinline__ void fft_row(float2* d, const float2* tw, int N, int logN, int t, int tpr, bool inverse) {
-  for (int s = 1; s <= logN; ++s) {
-    const int half = 1 << (s - 1);
-    const int step = N >> s;
+  int s = 1;
+  if (logN & 1) {  // stage 1: pairs (2b, 2b + 1), twiddle 1
     for (int b = t; b < (N >> 1); b += tpr) {
-      const int j = b & (half - 1);
-      const int i0 = ((b >> (s - 1)) << s) + j;
-      const int i1 = i0 + half;
-      float2 w = tw[j * step];
-      if (inverse) w.y = -w.y;
-      const float2 a = d[i0];
-      const float2 c = cmul(w, d[i1]);
-      d[i0] = make_float2(a.x + c.x, a.y + c.y);
-      d[i1] = make_float2(a.x - c.x, a.y - c.y);
+      const float2 a = d[pd(2 * b)], c = d[pd(2 * b + 1)];
+      d[pd(2 * b)] = cadd(a, c);
+      d[pd(2 * b + 1)] = csub(a, c);
+    }
+    __syncthreads();
+    s = 2;
+  }
+  for (; s < logN; s += 2) {  // stages s and s + 1
+    const int h = 1 << (s - 1);
+    const int step1 = N >> s, step2 = N >> (s + 1);
+    for (int b = t; b < (N >> 2); b += tpr) {
+      const int j = b & (h - 1);
+      const int i0 = ((b >> (s - 1)) << (s + 1)) + j;
+      float2 w1 = tw[j * step1], w2 = tw[j * step2], w3 = tw[(j + h) * step2];
+      if (inverse) { w1.y = -w1.y; w2.y = -w2.y; w3.y = -w3.y; }
+      const int p0 = pd(i0), p1 = pd(i0 + h), p2 = pd(i0 + 2 * h), p3 = pd(i0 + 3 * h);
+      const float2 x0 = d[p0], x1 = d[p1], x2 = d[p2], x3 = d[p3];
+      // stage s: butterflies (i0, i0 + h) and (i0 + 2h, i0 + 3h), both at offset j of their 2h block
+      const float2 t1 = cmul(w1, x1), t3 = cmul(w1, x3);
+      const float2 a0 = cadd(x0, t1), a1 = csub(x0, t1), b0 = cadd(x2, t3), b1 = csub(x2, t3);
+      // stage s + 1: butterflies (i0, i0 + 2h) at offset j and (i0 + h, i0 + 3h) at offset j + h
+      const float2 u2 = cmul(w2, b0), u3 = cmul(w3, b1);
+      d[p0] = cadd(a0, u2);
+      d[p2] = csub(a0, u2);
+      d[p1] = cadd(a1, u3);
+      d[p3] = csub(a1, u3);
     }
     __syncthreads();
   }
 }
 
 __device__ __forceinline__ int bitrev(int i, int logN) { return (int)(__brev((unsigned)i) >> (32 - logN)); }
+
+// natural -> bit-reversed order in place (the owner of the smaller index swaps each pair), then a
+// block barrier
+__device__ __forceinline__ void bitrev_permute(float2* d, int N, int logN, int t, int tpr) {
+  for (int i = t; i < N; i += tpr) {
+    const int r = bitrev(i, logN);
+    if (i < r) {
+      const float2 a = d[pd(i)];
+      d[pd(i)] = d[pd(r)];
+      d[pd(r)] = a;
+    }
+  }
+  __syncthreads();
+}
 
 __device__ __forceinline__ void load_twiddles(float2* s_tw, const float2* g_tw, int N) {
   for (int k = threadIdx.x; k < N / 2; k += blockDim.x) s_tw[k] = g_tw[k];
@@ -106,7 +150,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
   const int h = blockIdx.x * rpb + r;
   const int c = blockIdx.y, n = blockIdx.z;
   if (f.active && !f.active[n]) return;  // uniform per block
-  float2* d = rows + r * W;
+  float2* d = rows + r * row_pitch(W);
   const long long plane = ((long long)n * f.C + c) * f.H * W;
   if (h < f.H) {
     for (int i = t; i < W; i += tpr) {
@@ -114,7 +158,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
       float v;
       if (mode == 1) v = f.z[e] - f.tau * f.lam * f.gg[e] + f.tau * f.aty[e];
       else v = src[e];
-      d[bitrev(i, logW)] = make_float2(v, 0.f);
+      d[pd(bitrev(i, logW))] = make_float2(v, 0.f);
     }
   }
   __syncthreads();
@@ -122,7 +166,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
   if (h < f.H) {
     const int Wh = W / 2 + 1;
     float2* S = f.spec + ((long long)n * f.C + c) * f.H * Wh + (long long)h * Wh;
-    for (int i = t; i < Wh; i += tpr) S[i] = d[i];
+    for (int i = t; i < Wh; i += tpr) S[i] = d[pd(i)];
   }
 }
 
@@ -150,16 +194,16 @@ __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
   for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
     const int h = q / FFT_CPB, j = q % FFT_CPB;
     const int kx = kx0 + j;
-    cols[j * H + bitrev(h, logH)] = kx < Wh ? S[(long long)h * Wh + kx] : make_float2(0.f, 0.f);
+    cols[j * col_pitch(H) + pd(bitrev(h, logH))] = kx < Wh ? S[(long long)h * Wh + kx] : make_float2(0.f, 0.f);
   }
   __syncthreads();
-  float2* d = cols + cc * H;
+  float2* d = cols + cc * col_pitch(H);
   const int kx = kx0 + cc;
   if (op == 3) {  // loaded bit-reversed: straight into the inverse transform
     fft_row(d, tw, H, logH, t, tpc, true);
     for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
       const int h = q / FFT_CPB, j = q % FFT_CPB;
-      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * col_pitch(H) + pd(h)];
     }
     return;
   }
@@ -167,16 +211,14 @@ __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
   if (op == 2) {
     for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
       const int h = q / FFT_CPB, j = q % FFT_CPB;
-      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+      if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * col_pitch(H) + pd(h)];
     }
     return;
   }
-  // pointwise op in natural order, written back bit-reversed for the inverse pass
-  __syncthreads();
-  float2 tmp[32];  // H / tpc <= 1024 / 32
-  int cnt = 0;
+  // pointwise op in natural order (in place), then the bit-reversal permutation for the inverse
+  // pass (pairwise swaps; fft_row ended with a barrier)
   for (int ky = t; ky < H; ky += tpc) {
-    float2 v = d[ky];
+    float2 v = d[pd(ky)];
     if (kx < Wh) {
       if (op == 0) {
         const float g = f.dgl[(long long)ky * Wh + kx];
@@ -185,16 +227,14 @@ __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
         v = cconjmul(f.khat[(long long)ky * Wh + kx], v);
       }
     }
-    tmp[cnt++] = v;
+    d[pd(ky)] = v;
   }
   __syncthreads();
-  cnt = 0;
-  for (int ky = t; ky < H; ky += tpc) d[bitrev(ky, logH)] = tmp[cnt++];
-  __syncthreads();
+  bitrev_permute(d, H, logH, t, tpc);
   fft_row(d, tw, H, logH, t, tpc, true);
   for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
     const int h = q / FFT_CPB, j = q % FFT_CPB;
-    if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * H + h];
+    if (kx0 + j < Wh) S[(long long)h * Wh + kx0 + j] = cols[j * col_pitch(H) + pd(h)];
   }
 }
 
@@ -212,14 +252,14 @@ __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs 
   const int h = blockIdx.x * rpb + r;
   const int c = blockIdx.y, n = blockIdx.z;
   if (f.active && !f.active[n]) return;
-  float2* d = rows + r * W;
+  float2* d = rows + r * row_pitch(W);
   const int Wh = W / 2 + 1;
   if (h < H) {
     const float2* S = f.spec + ((long long)n * f.C + c) * H * Wh + (long long)h * Wh;
     for (int i = t; i < W; i += tpr) {
       float2 v = i < Wh ? S[i] : S[W - i];
       if (i >= Wh) v.y = -v.y;  // X[W-k] = conj(X[k]) for a real row (per column transform keeps it)
-      d[bitrev(i, logW)] = v;
+      d[pd(bitrev(i, logW))] = v;
     }
   }
   __syncthreads();
@@ -228,7 +268,7 @@ __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs 
   const long long plane = ((long long)n * f.C + c) * H * W;
   if (mode == 0) {
     if (h < H)
-      for (int i = t; i < W; i += tpr) dst[plane + (long long)h * W + i] = d[i].x * scale;
+      for (int i = t; i < W; i += tpr) dst[plane + (long long)h * W + i] = d[pd(i)].x * scale;
     return;
   }
   const int k = *a.kdev;
@@ -236,7 +276,7 @@ __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs 
   float* xn_base = (k & 1) ? a.X0 : a.X1;
   P3 acc{0.f, 0.f, 0.f};
   if (h < H)
-    for (int i = t; i < W; i += tpr) step_tail(d[i].x * scale, plane + (long long)h * W + i, a, xk_base, xn_base, acc);
+    for (int i = t; i < W; i += tpr) step_tail(d[pd(i)].x * scale, plane + (long long)h * W + i, a, xk_base, xn_base, acc);
   const int part = c * gridDim.x + blockIdx.x;
   reduce_store_p3(acc, a.partials + ((long long)n * a.parts + part) * 3);
 }
@@ -308,21 +348,21 @@ __global__ void __launch_bounds__(256) phase_rows_fwd_kernel(FftArgs f) {
   const int h = blockIdx.x * rpb + r;
   const int j = blockIdx.y, n = blockIdx.z;
   if (f.active && !f.active[n]) return;
-  float2* d = rows + r * W;
+  float2* d = rows + r * row_pitch(W);
   if (h < f.H) {
     const float* zr = f.z + (long long)n * f.H * W + (long long)h * W;
     const float2* Dr = f.pmask + ((long long)j * f.H + h) * W;
     for (int i = t; i < W; i += tpr) {
       const float zv = zr[i];
       const float2 dv = Dr[i];
-      d[bitrev(i, logW)] = make_float2(dv.x * zv, dv.y * zv);
+      d[pd(bitrev(i, logW))] = make_float2(dv.x * zv, dv.y * zv);
     }
   }
   __syncthreads();
   fft_row(d, tw, W, logW, t, tpr, false);
   if (h < f.H) {
     float2* U = f.spec + (((long long)n * f.J + j) * f.H + h) * W;
-    for (int i = t; i < W; i += tpr) U[i] = d[i];
+    for (int i = t; i < W; i += tpr) U[i] = d[pd(i)];
   }
 }
 
@@ -342,29 +382,25 @@ __global__ void __launch_bounds__(256) phase_cols_kernel(FftArgs f) {
   const float* Y = f.y + ((long long)n * f.J + j) * H * W;
   for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
     const int h = q / FFT_CPB, jj = q % FFT_CPB;
-    cols[jj * H + bitrev(h, logH)] = U[(long long)h * W + kx0 + jj];
+    cols[jj * col_pitch(H) + pd(bitrev(h, logH))] = U[(long long)h * W + kx0 + jj];
   }
   __syncthreads();
-  float2* d = cols + cc * H;
+  float2* d = cols + cc * col_pitch(H);
   fft_row(d, tw, H, logH, t, tpc, false);
   const float s = rsqrtf((float)H * (float)W);
   const int kx = kx0 + cc;
-  float2 tmp[32];
-  int cnt = 0;
   for (int ky = t; ky < H; ky += tpc) {
-    const float2 v = d[ky];
+    const float2 v = d[pd(ky)];
     const float2 u = make_float2(v.x * s, v.y * s);
     const float m = u.x * u.x + u.y * u.y - Y[(long long)ky * W + kx];
-    tmp[cnt++] = make_float2(m * u.x, m * u.y);
+    d[pd(ky)] = make_float2(m * u.x, m * u.y);
   }
   __syncthreads();
-  cnt = 0;
-  for (int ky = t; ky < H; ky += tpc) d[bitrev(ky, logH)] = tmp[cnt++];
-  __syncthreads();
+  bitrev_permute(d, H, logH, t, tpc);
   fft_row(d, tw, H, logH, t, tpc, true);
   for (int q = threadIdx.x; q < H * FFT_CPB; q += blockDim.x) {
     const int h = q / FFT_CPB, jj = q % FFT_CPB;
-    U[(long long)h * W + kx0 + jj] = cols[jj * H + h];
+    U[(long long)h * W + kx0 + jj] = cols[jj * col_pitch(H) + pd(h)];
   }
 }
 
@@ -382,13 +418,13 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
   const int h = blockIdx.x * rpb + r;
   const int n = blockIdx.y;
   if (f.active && !f.active[n]) return;
-  float2* d = rows + r * W;
+  float2* d = rows + r * row_pitch(W);
   float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // W / tpr <= 4 for W <= 1024
   const float s = rsqrtf((float)H * (float)W);
   for (int j = 0; j < f.J; ++j) {
     if (h < H) {
       const float2* U = f.spec + (((long long)n * f.J + j) * H + h) * W;
-      for (int i = t; i < W; i += tpr) d[bitrev(i, logW)] = U[i];
+      for (int i = t; i < W; i += tpr) d[pd(bitrev(i, logW))] = U[i];
     }
     __syncthreads();
     fft_row(d, tw, W, logW, t, tpr, true);
@@ -396,7 +432,7 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
       const float2* Dr = f.pmask + ((long long)j * H + h) * W;
       int q = 0;
       for (int i = t; i < W; i += tpr, ++q) {
-        const float2 v = make_float2(d[i].x * s, d[i].y * s);
+        const float2 v = make_float2(d[pd(i)].x * s, d[pd(i)].y * s);
         gacc[q] += 2.f * cconjmul(Dr[i], v).x;
       }
     }
@@ -431,9 +467,9 @@ static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 static size_t row_smem(int W) {
   const int tpr = (W / 2) < 256 ? (W / 2) : 256;
   const int rpb = 256 / tpr;
-  return sizeof(float2) * (W / 2 + (size_t)rpb * W);
+  return sizeof(float2) * (W / 2 + (size_t)rpb * row_pitch(W));
 }
-static size_t col_smem(int H) { return sizeof(float2) * (H / 2 + (size_t)FFT_CPB * H); }
+static size_t col_smem(int H) { return sizeof(float2) * (H / 2 + (size_t)FFT_CPB * col_pitch(H)); }
 static int rows_per_block(int W) { const int tpr = (W / 2) < 256 ? (W / 2) : 256; return 256 / tpr; }
 
 int fft_parts_per_image(int C, int H, int W) { return C * ((H + rows_per_block(W) - 1) / rows_per_block(W)); }
