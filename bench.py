@@ -188,6 +188,9 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--batch", type=int, default=0, help="images per GPU (default: the config's per-GPU batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--restart", type=float, default=0.0,
+                    help="NEXT-1: adaptive restart with this B (Eq. 5, Alg. 1 semantics) in every timed solve")
+    ap.add_argument("--averaging", action="store_true", help="NEXT-1: averaging (Alg. 1 steps 12-13) in the timed solves")
     ap.add_argument("--no-tol-run", action="store_true",
                     help="skip the ms-to-tolerance solve (the metric's second half: tol = 1e-4, per-image stop)")
     args = ap.parse_args()
@@ -231,8 +234,10 @@ def main():
             return float(t.item())
         return v
 
+    nx1 = dict(restart=1 if args.restart > 0 else 0, restart_B=args.restart, averaging=args.averaging)
+
     # ---- warm-up (also captures the CUDA graph of one iteration)
-    s.solve(y, x, s.params(max_iter=args.warmup, tol=0.0))
+    s.solve(y, x, s.params(max_iter=args.warmup, tol=0.0, **nx1))
     x.copy_(torch.tensor(prob["x0"]))
     barrier()
 
@@ -241,7 +246,7 @@ def main():
     with ClockSampler(local) as clk:
         barrier()
         e0.record(stream)
-        stats, code, _ = s.solve(y, x, s.params(max_iter=args.steps, tol=0.0))
+        stats, code, _ = s.solve(y, x, s.params(max_iter=args.steps, tol=0.0, **nx1))
         e1.record(stream)
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
@@ -253,7 +258,7 @@ def main():
     xh = torch.tensor(prob["x0"]).pin_memory().numpy()
     barrier()
     t0 = time.perf_counter()
-    s.solve_host(yh, xh, s.params(max_iter=args.steps, tol=0.0))
+    s.solve_host(yh, xh, s.params(max_iter=args.steps, tol=0.0, **nx1))
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
     e2e_v = per * world * args.steps / e2e_s
@@ -264,7 +269,7 @@ def main():
     x.copy_(torch.tensor(prob["x0"]))
     s.set_profiling(True)
     s.profile(reset=True)
-    s.solve(y, x, s.params(max_iter=kprof, tol=0.0))
+    s.solve(y, x, s.params(max_iter=kprof, tol=0.0, **nx1))
     prof = s.profile(reset=True)
     s.set_profiling(False)
     peaks, peak_src = _peaks()
@@ -274,7 +279,7 @@ def main():
     total_ms = sum(v["ms"] for v in prof.values())
     traffic = None
     tp = os.path.join(ROOT, "profiles", "conv_tc_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and args.config == "C3" and per == cfg["batch"]:  # captured on C3 only
         try:
             traffic = json.load(open(tp)).get("bytes_per_launch")
         except Exception:
@@ -289,11 +294,11 @@ def main():
 
     # ---- ms to tolerance (tol = 1e-4, per-image stop)
     tol_info = None
-    if not args.no_tol_run:
+    if not args.no_tol_run and not args.averaging:  # averaging needs a fixed iteration count (reading R5)
         x.copy_(torch.tensor(prob["x0"]))
         barrier()
         e0.record(stream)
-        st2, _, _ = s.solve(y, x, s.params(max_iter=cfg["max_iter"], tol=1e-4))
+        st2, _, _ = s.solve(y, x, s.params(max_iter=cfg["max_iter"], tol=1e-4, **nx1))
         e1.record(stream)
         barrier()
         tol_info = {"ms": max_over_ranks(e0.elapsed_time(e1)), "tol": 1e-4,
@@ -303,8 +308,10 @@ def main():
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded piecewise-smooth images, random-init "
-            "U-Net weights; stands in for the paper's BSDS500 inpainting split)",
-            "config": _config_dict(cfg, per, world),
+            "U-Net weights" + {"inpaint": "; stands in for the paper's BSDS500 inpainting split)",
+                               "mri": "; stand-in phantoms for the paper's fastMRI knee data)"}.get(cfg["op"], ")"),
+            "config": dict(_config_dict(cfg, per, world), **({"restart_B": args.restart} if args.restart > 0 else {}),
+                           **({"averaging": True} if args.averaging else {})),
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": (yh.nbytes + xh.nbytes) / args.steps,
                     "d2h_bytes_per_step": xh.nbytes / args.steps,
                     "note": "one ideq_solve_host call of K iterations: H2D of y and x0, D2H of x-hat inside"},
