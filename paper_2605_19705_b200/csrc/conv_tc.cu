@@ -1097,14 +1097,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 // tensor of the two-kernel form never touches HBM -- then one elected lane issues two
 // M128 x NC x K16 tcgen05.mma into a TMEM accumulator that the same thread reads back with
 // tcgen05.ld (thread = pixel = TMEM lane) and stores as 16-byte bf16 chunks (a warp writes 32
-// consecutive pixels = one contiguous run). A and the accumulator are double-buffered.
+// consecutive pixels = one contiguous run). The output staging is double-buffered
+// (asynchronous tensor stores); A and the accumulator are single (the loop waits for each MMA),
+// which lets 8 CTAs share an SM to hide the per-tile round trip.
 template <int NC>
 __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restrict__ in,
                                                           const __nv_bfloat16* __restrict__ wB,
                                                           const __grid_constant__ CUtensorMap tmO, int N, int C,
                                                           int H, int W, const FastDiv fdHW, const FastDiv fdW,
                                                           const int* __restrict__ active) {
-  __shared__ __align__(1024) unsigned char sAraw[2][128 * 64];
+  __shared__ __align__(1024) unsigned char sAraw[128 * 64];  // one A tile: the loop waits for each MMA
   __shared__ __align__(1024) unsigned char sBraw[NC * 64];
   // output staging [2][128 pixels x NC] in the TMA store's swizzle (SW64 for NC = 32, SW128 for
   // 64): conflict-free 16-byte writes (a linear layout at a 64/128-byte pixel stride put 8 lanes
@@ -1115,7 +1117,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   __shared__ uint32_t tmem_holder;
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const uint32_t sA0 = smem_u32(sAraw[0]), sA1 = smem_u32(sAraw[1]), sB = smem_u32(sBraw);
+  const uint32_t sA = smem_u32(sAraw), sB = smem_u32(sBraw);
   // weights [NC][32] bf16 -> swizzled K-major B tile (64-byte rows, 16-byte chunk j at j ^ ((r >> 1) & 3))
   for (int i = tid; i < NC * 4; i += 128) {
     const int r = i >> 2, j = i & 3;
@@ -1129,7 +1131,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_holder)),
-                 "r"((uint32_t)(2 * NC))
+                 "r"((uint32_t)NC)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -1154,17 +1156,32 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
       const uint32_t p32 = (uint32_t)px;
       const uint32_t n = fdHW.div(p32), rem = p32 - n * (uint32_t)HW;
       const uint32_t h = fdW.div(rem), w = rem - h * (uint32_t)W;
+      if (h >= 1 && h + 1 < (uint32_t)H && w >= 1 && w + 1 < (uint32_t)W) {
+        // interior pixel (all but the image border): one base pointer, 27 loads at fixed offsets
+        const float* p0 = in + ((long long)n * C) * HW + (long long)(h - 1) * W + (w - 1);
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        if (c < C) {
-          const float* plane = in + ((long long)n * C + c) * HW;
+        for (int c = 0; c < 3; ++c) {
+          if (c < C) {
+            const float* pc = p0 + (long long)c * HW;
 #pragma unroll
-          for (int a = 0; a < 3; ++a)
+            for (int a = 0; a < 3; ++a)
 #pragma unroll
-            for (int b = 0; b < 3; ++b) {
-              const int hh = (int)h + a - 1, ww = (int)w + b - 1;
-              if (hh >= 0 && hh < H && ww >= 0 && ww < W) pv[c * 9 + a * 3 + b] = __ldg(plane + hh * W + ww);
-            }
+              for (int b = 0; b < 3; ++b) pv[c * 9 + a * 3 + b] = __ldg(pc + a * W + b);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          if (c < C) {
+            const float* plane = in + ((long long)n * C + c) * HW;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+#pragma unroll
+              for (int b = 0; b < 3; ++b) {
+                const int hh = (int)h + a - 1, ww = (int)w + b - 1;
+                if (hh >= 0 && hh < H && ww >= 0 && ww < W) pv[c * 9 + a * 3 + b] = __ldg(plane + hh * W + ww);
+              }
+          }
         }
       }
     }
@@ -1183,8 +1200,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   if (tnext < tiles) load_patch(tnext);
   for (long long t = tnext; t < tiles; t = tnext, ++it) {
     tnext = next_live(t + gridDim.x);
-    const int buf = it & 1;
-    const uint32_t sA = buf ? sA1 : sA0;
+    const int buf = it & 1;  // output staging buffer (the only double-buffered resource)
     float v[32];
 #pragma unroll
     for (int k = 0; k < 27; ++k) v[k] = pv[k];
@@ -1211,21 +1227,21 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
       // the staging buffer this tile writes was bulk-copied one tile ago: wait until it was read
       asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
     }
-    const uint32_t d_tmem = tmem_base + (uint32_t)(buf * NC);
+    const uint32_t d_tmem = tmem_base;
     if (warp == 0) {
       const uint64_t dA = make_sdesc(sA, 512u, 4u);
       mma_bf16_elect(d_tmem, dA, dB, idesc, 0u);
       mma_bf16_elect(d_tmem, dA + 2u, dB + 2u, idesc, 1u);
-      mma_commit_elect(smem_u32(&bar[buf]));
+      mma_commit_elect(smem_u32(&bar[0]));
     }
-    mbar_wait(smem_u32(&bar[buf]), (uint32_t)((it >> 1) & 1));
+    mbar_wait(smem_u32(&bar[0]), (uint32_t)(it & 1));
     __syncthreads();  // thread 0 has waited for the staging buffer's previous bulk copy
     tc_fence_after();
     const uint32_t so = smem_u32(sOdyn + buf * 128 * NC * 2);
 #pragma unroll
     for (int c0 = 0; c0 < NC; c0 += 16) {
       float r[16];
-      tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * NC + c0), r);
+      tmem_ld16(tmem_base + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, r);
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         uint4 wv;
@@ -1249,7 +1265,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   }
   tc_fence_after();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)(2 * NC))
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"((uint32_t)NC)
                  : "memory");
 }
 
@@ -1292,9 +1308,9 @@ void img2feat_free_plan(I2FPlan* p) { delete p; }
 
 void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* active, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s) {
-  // the static shared memory (54 KB / 36 KB) caps residency so that the CTAs' TMEM allocations
-  // (2 x NC columns each) never exceed the SM's 512 columns
-  const int per_sm = NC == 64 ? 4 : 6;   // static smem admits at most 4 (NC 64) / 6 (NC 32) CTAs per SM
+  // residency is capped by shared memory; the CTAs' TMEM allocations (NC columns each, <= 8 x 32 or
+  // 5 x 64) stay within the SM's 512 columns
+  const int per_sm = NC == 64 ? 5 : 8;   // shared memory (27 KB / 45 KB per CTA) admits 8 (NC 32) / 5 (NC 64) CTAs per SM
   const size_t pad = (size_t)2 * 128 * NC * 2 + 1024;  // output staging (+ alignment slack)
   const long long total = (long long)N * H * W, tiles = (total + 127) / 128;
   const long long cap = (long long)num_sms * per_sm;
