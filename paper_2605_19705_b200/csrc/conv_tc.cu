@@ -1206,7 +1206,6 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     for (int k = 0; k < 27; ++k) v[k] = pv[k];
 #pragma unroll
     for (int k = 27; k < 32; ++k) v[k] = 0.f;
-    if (tnext < tiles) load_patch(tnext);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint4 wv;
@@ -1219,6 +1218,10 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    // the next tile's patch loads are issued only now: the proxy fence above (MEMBAR.ALL.CTA)
+    // waits for every outstanding load of the thread, so loads issued before it would stall it;
+    // from here they overlap the MMA round trip and this tile's epilogue
+    if (tnext < tiles) load_patch(tnext);
     if (tid == 0) {
       if (t_prev >= 0) {  // the previous tile's staged output: one TMA tensor store (rows past the end clipped)
         tma_store_2d(&tmO, smem_u32(sOdyn + (buf ^ 1) * 128 * NC * 2), 0, (int)(t_prev * 128));
