@@ -217,3 +217,30 @@ def test_determinism_and_batch_independence():
         x1 = _dev(torch, sub["x0"])
         s1.solve(_dev(torch, sub["y"]), x1, s1.params(max_iter=6, tol=0.0))
         assert torch.equal(x1[0], xa[2])
+
+
+@pytest.mark.parametrize("ks,H,W", [(25, 64, 96), (9, 72, 40), (7, 48, 40)])
+def test_direct_blur_kernel_sizes(ks, H, W):
+    """Direct-blur gradient step at every register-blocked kernel size (9, 15 in C2 above, 25) and
+    one fallback size (7): grad f component within 1e-5 and an fp32 trajectory within 1e-4 / 1e-6
+    (C5 geometry with the gradient variant; 64 x 64 blur tiles with ragged edges)."""
+    torch = torch_cuda()
+    cfg = _mini("C5", H=H, W=W, step="grad", blur_impl="direct", ksize=ks, ksigma=ks / 8.0)
+    prob = synth.make_problem(cfg)
+    s = _solver(cfg, prob, "fp32")
+    fids = osolver.make_fidelities(cfg, prob)
+    # away from the truth: at x_true, A^T(Ax - y) = -A^T n is the noise smoothed by the kernel
+    # (|.| ~ sigma / k), and the fp32 rounding of Ax (~1e-7 |Ax|) is then 1e-5..1e-4 of it
+    x = (0.9 * prob["x_true"] + 0.05).astype(np.float32)
+    out = torch.zeros_like(_dev(torch, x))
+    s.fidelity_grad(_dev(torch, prob["y"]), _dev(torch, x), out)
+    for b in range(x.shape[0]):
+        assert rel_l2(out[b].cpu().numpy(), fids[b].grad(x[b].astype(np.float64))) <= 1e-5
+    K = 6
+    xd = _dev(torch, prob["x0"])
+    st, code, _ = s.solve(_dev(torch, prob["y"]), xd, s.params(max_iter=K, tol=0.0))
+    orc = osolver.solve_config(cfg, prob, max_iter=K, tol=0.0)
+    xg = xd.cpu().numpy()
+    for b in range(xg.shape[0]):
+        assert rel_l2(xg[b], orc["x"][b]) <= 1e-4
+        assert abs(st["residual"][b] - orc["residual"][b]) <= 1e-6
