@@ -87,6 +87,30 @@ __device__ __forceinline__ float apply_epi(int epi, float acc, float aux) {
   }
 }
 
+// Programmatic dependent launch for the per-iteration kernels: launched with the programmatic
+// stream-serialization attribute, each waits (griddepcontrol.wait) for its predecessor grid to
+// complete and flush before touching any global data, then lets its own successor be scheduled,
+// so the launch latency of the next kernel overlaps this one. IDEQ_NO_PDL=1 launches plainly.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // Allow a kernel the largest dynamic shared memory the device grants on top of its
 // static shared memory (the opt-in limit is per block, static + dynamic).
 template <typename K>

@@ -18,6 +18,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __restrict__ in,
                                                         const T* __restrict__ wB, T* __restrict__ out,
                                                         const T* __restrict__ aux) {
+  pdl_enter();
   __shared__ __align__(16) float As[SM_BK][SM_BM + 4];
   __shared__ __align__(16) float Bs[SM_BK][SM_BN + 4];
   const int tid = threadIdx.x;
@@ -45,33 +46,45 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
-  const int nkb = g.ntaps * g.nchunk;
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int tap = kb / g.nchunk, chunk = kb % g.nchunk;
+  // K loop over (tap, chunk, 16-channel slice) steps, software-pipelined: the next step's
+  // operands are loaded into registers while this step's products run from shared memory, so
+  // the global-load latency is paid once instead of per step (the small-grid / latency-bound
+  // cases: C1, the JFB tape passes)
+  const int nkb = g.ntaps * g.nchunk, nkk = g.KC / SM_BK, nsteps = nkb * nkk;
+  float ra[8], rb[4];
+  auto load_step = [&](int st) {
+    const int kb = st / nkk, kk = (st - kb * nkk) * SM_BK;
+    const int tap = kb / g.nchunk, chunk = kb - tap * g.nchunk;
     const int ih = loh + g.dh[tap], iw = low + g.dw[tap];
     const bool inb = lvalid && ih >= 0 && ih < g.inH && iw >= 0 && iw < g.inW;
     const T* src = in + ((((long long)img * g.inH + ih) * g.inP + g.dp[tap]) * g.inW + iw) * g.inC + chunk * g.KC;
     const T* wsrc = wB + ((long long)kb * g.ncols + n0 + bcol) * g.KC;
-    for (int kk = 0; kk < g.KC; kk += SM_BK) {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) As[lhalf * 8 + j][lpx] = inb ? ElemOps<T>::ld(src + kk + lhalf * 8 + j) : 0.f;
+    for (int j = 0; j < 8; ++j) ra[j] = inb ? ElemOps<T>::ld(src + kk + lhalf * 8 + j) : 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) Bs[bk + j][bcol] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
-      __syncthreads();
+    for (int j = 0; j < 4; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
+  };
+  if (nsteps > 0) load_step(0);
+  for (int st = 0; st < nsteps; ++st) {
 #pragma unroll
-      for (int k = 0; k < SM_BK; ++k) {
-        const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
-        const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
-        const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
-        const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-        const float bv[4] = {b.x, b.y, b.z, b.w};
+    for (int j = 0; j < 8; ++j) As[lhalf * 8 + j][lpx] = ra[j];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+    for (int j = 0; j < 4; ++j) Bs[bk + j][bcol] = rb[j];
+    __syncthreads();
+    if (st + 1 < nsteps) load_step(st + 1);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
-      }
-      __syncthreads();
+    for (int k = 0; k < SM_BK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
+      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
+    __syncthreads();
   }
   // epilogue
 #pragma unroll
@@ -93,7 +106,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
 template <typename T>
 void launch_conv_simt(const ConvGeom& g, const T* in, const T* wB, T* out, const T* aux, cudaStream_t s) {
   dim3 grid(g.N * g.tiles_h * g.tiles_w, (g.ncols + SM_BN - 1) / SM_BN);
-  conv_simt_kernel<T><<<grid, 256, 0, s>>>(g, in, wB, out, aux);
+  launch_k(conv_simt_kernel<T>, grid, 256, 0, s, g, in, wB, out, aux);
 }
 
 // ------------------------------------------------------------------ vector helpers
@@ -130,6 +143,7 @@ template <typename T, int WO, int C>
 __global__ void __launch_bounds__(256) img2feat_kernel(const float* __restrict__ in, const float* __restrict__ w_t,
                                                        T* __restrict__ out, const T* __restrict__ aux, int epi,
                                                        int N, int H, int W) {
+  pdl_enter();
   __shared__ __align__(16) float wsm[3 * 9][WO];
   __shared__ float tile[3][HT_ROWS + 2][18 + 1];
   for (int t = threadIdx.x; t < WO * C * 9; t += blockDim.x) {
@@ -201,8 +215,8 @@ void launch_img2feat(const float* in, const float* w_t, T* out, const T* aux, in
   dim3 grid((W + 15) / 16, (H + HT_ROWS - 1) / HT_ROWS, N);
 #define I2F(WO)                                                                                          \
   case WO:                                                                                               \
-    if (C == 1) img2feat_kernel<T, WO, 1><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, H, W);         \
-    else img2feat_kernel<T, WO, 3><<<grid, 256, 0, s>>>(in, w_t, out, aux, epi, N, H, W);                \
+    if (C == 1) launch_k(img2feat_kernel<T, WO, 1>, grid, 256, 0, s, in, w_t, out, aux, epi, N, H, W);         \
+    else launch_k(img2feat_kernel<T, WO, 3>, grid, 256, 0, s, in, w_t, out, aux, epi, N, H, W);                \
     break;
   switch (wout) {
     I2F(16) I2F(32) I2F(64)
@@ -220,6 +234,7 @@ template <typename T, int WI>
 __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in, const float* __restrict__ w_t,
                                                        float* __restrict__ out, const float* __restrict__ aux,
                                                        float alpha, int N, int C, int H, int W) {
+  pdl_enter();
   extern __shared__ __align__(16) float smf[];
   constexpr int PS = WI + 4;
   float4* wsm = reinterpret_cast<float4*>(smf);  // [9][WI] : (a*3+b, ci) -> (c0, c1, c2, 0)
@@ -301,9 +316,9 @@ void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux
   dim3 grid((W + 15) / 16, (H + HT_ROWS - 1) / HT_ROWS, N);
   const size_t sm = sizeof(float) * (9 * 4 * win + (HT_ROWS + 2) * 18 * (win + 4));
   switch (win) {
-    case 16: feat2img_kernel<T, 16><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
-    case 32: feat2img_kernel<T, 32><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
-    case 64: feat2img_kernel<T, 64><<<grid, 256, sm, s>>>(in, w_t, out, aux, alpha, N, C, H, W); break;
+    case 16: launch_k(feat2img_kernel<T, 16>, grid, 256, sm, s, in, w_t, out, aux, alpha, N, C, H, W); break;
+    case 32: launch_k(feat2img_kernel<T, 32>, grid, 256, sm, s, in, w_t, out, aux, alpha, N, C, H, W); break;
+    case 64: launch_k(feat2img_kernel<T, 64>, grid, 256, sm, s, in, w_t, out, aux, alpha, N, C, H, W); break;
     default: break;
   }
 }

@@ -139,6 +139,7 @@ __device__ __forceinline__ void step_tail(float x1, long long i, const StepArgs&
 //   mode 0: input = src plane
 //   mode 1: input = v + tau A^T y = z - tau lam grad g + tau ATy   (prox right-hand side)
 __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const float* __restrict__ src, int mode) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW;
   const int tpr = (W / 2) < 256 ? (W / 2) : 256;
@@ -178,6 +179,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
 constexpr int FFT_CPB = 8;  // columns per block in column passes
 
 __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int H = f.H, logH = f.logH;
   const int Wh = f.W / 2 + 1;
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
 // Row pass, inverse: half spectrum -> Hermitian full row -> inverse FFT -> real / (H W).
 //   mode 0: store into dst plane ; mode 1: x^{k+1} -> update + residual partials.
 __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW, H = f.H;
   const int tpr = (W / 2) < 256 ? (W / 2) : 256;
@@ -337,6 +340,7 @@ __global__ void blur_diag_kernel(const float2* __restrict__ khat, float tau, flo
 // ================================================================== phase retrieval (complex)
 // rows forward: U[n][j][h][:] = FFT_row( D_j[h][:] * z[n][0][h][:] )
 __global__ void __launch_bounds__(256) phase_rows_fwd_kernel(FftArgs f) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW;
   const int tpr = (W / 2) < 256 ? (W / 2) : 256;
@@ -368,6 +372,7 @@ __global__ void __launch_bounds__(256) phase_rows_fwd_kernel(FftArgs f) {
 
 // columns: forward FFT -> u = col / sqrt(HW) (unitary) -> w = (|u|^2 - y_j) u -> inverse FFT
 __global__ void __launch_bounds__(256) phase_cols_kernel(FftArgs f) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int H = f.H, logH = f.logH, W = f.W;
   float2* tw = sm2;
@@ -407,6 +412,7 @@ __global__ void __launch_bounds__(256) phase_cols_kernel(FftArgs f) {
 // rows inverse: for each j, v = IFFT_row(U)/sqrt(HW); grad f += 2 Re(conj(D_j) v).
 //   mode 0: store grad f into dst ; mode 1: x^{k+1} = z - tau (grad f + lam grad g) -> tail.
 __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW, H = f.H;
   const int tpr = (W / 2) < 256 ? (W / 2) : 256;
@@ -484,15 +490,15 @@ void fft_fill_args(FftArgs& f) { f.logH = ilog2(f.H); f.logW = ilog2(f.W); }
 
 void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
-  blur_rows_fwd_kernel<<<grid, 256, row_smem(f.W), s>>>(f, src, mode);
+  launch_k(blur_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f, src, mode);
 }
 void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s) {
   dim3 grid((f.W / 2 + 1 + FFT_CPB - 1) / FFT_CPB, f.C, N);
-  blur_cols_kernel<<<grid, 256, col_smem(f.H), s>>>(f, op);
+  launch_k(blur_cols_kernel, grid, 256, col_smem(f.H), s, f, op);
 }
 void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
-  blur_rows_inv_kernel<<<grid, 256, row_smem(f.W), s>>>(f, a, dst, mode);
+  launch_k(blur_rows_inv_kernel, grid, 256, row_smem(f.W), s, f, a, dst, mode);
 }
 void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s) {
   cudaMemsetAsync(plane, 0, sizeof(float) * H * W, s);
@@ -512,15 +518,15 @@ void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStre
 }
 void launch_phase_rows_fwd(const FftArgs& f, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.J, N);
-  phase_rows_fwd_kernel<<<grid, 256, row_smem(f.W), s>>>(f);
+  launch_k(phase_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f);
 }
 void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s) {
   dim3 grid(f.W / FFT_CPB, f.J, N);
-  phase_cols_kernel<<<grid, 256, col_smem(f.H), s>>>(f);
+  launch_k(phase_cols_kernel, grid, 256, col_smem(f.H), s, f);
 }
 void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), N);
-  phase_rows_inv_kernel<<<grid, 256, row_smem(f.W), s>>>(f, a, dst, mode);
+  launch_k(phase_rows_inv_kernel, grid, 256, row_smem(f.W), s, f, a, dst, mode);
 }
 
 void init_attrs_fft() {

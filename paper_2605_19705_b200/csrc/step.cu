@@ -76,25 +76,27 @@ __device__ __forceinline__ float rician_grad_f(float x, float y, float inv_s2) {
 
 __global__ void __launch_bounds__(256) rician_grad_kernel(const float* __restrict__ x, const float* __restrict__ y,
                                                           float inv_s2, float* __restrict__ out, long long n) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] = rician_grad_f(x[i], y[i], inv_s2);
 }
 
 __global__ void sub_kernel(const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ out,
                            long long n) {
+  pdl_enter();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
     out[i] = a[i] - b[i];
 }
 void launch_sub(const float* a, const float* b, float* out, long long n, cudaStream_t s) {
   long long g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
-  sub_kernel<<<(unsigned)g, 256, 0, s>>>(a, b, out, n);
+  launch_k(sub_kernel, (unsigned)g, 256, 0, s, a, b, out, n);
 }
 
 void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out, long long n, cudaStream_t s) {
   long long b = (n + 255) / 256;
   if (b > 148 * 16) b = 148 * 16;
-  rician_grad_kernel<<<(unsigned)b, 256, 0, s>>>(x, y, inv_s2, out, n);
+  launch_k(rician_grad_kernel, (unsigned)b, 256, 0, s, x, y, inv_s2, out, n);
 }
 
 // ------------------------------------------------------------------ pointwise step kernels
@@ -102,6 +104,7 @@ void launch_rician_grad(const float* x, const float* y, float inv_s2, float* out
 // contiguous chunk of the image's d = C*H*W elements.
 template <int MODE>
 __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
+  pdl_enter();
   const int n = blockIdx.y, part = blockIdx.x;
   if (!a.active[n]) return;
   const int k = *a.kdev;
@@ -188,6 +191,7 @@ __device__ __forceinline__ void blur_tile(const float* __restrict__ src, const f
 
 // r = A z - y
 __global__ void __launch_bounds__(256) blur_residual_kernel(StepArgs a) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
   if (a.active && !a.active[n]) return;
@@ -213,6 +217,7 @@ __global__ void __launch_bounds__(256) blur_residual_kernel(StepArgs a) {
 // MODE 0: plain store into a.fbuf2 ; MODE 1: fused gradient step + tail.
 template <int MODE>
 __global__ void __launch_bounds__(256) blur_adjoint_kernel(StepArgs a, const float* __restrict__ src) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
   if (a.active && !a.active[n]) return;
@@ -313,6 +318,7 @@ __device__ __forceinline__ void blur_tile2(const float* __restrict__ src, const 
 
 template <int KS>
 __global__ void __launch_bounds__(128) blur_residual2_kernel(StepArgs a) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
   if (a.active && !a.active[n]) return;
@@ -338,6 +344,7 @@ __global__ void __launch_bounds__(128) blur_residual2_kernel(StepArgs a) {
 
 template <int KS, int MODE>
 __global__ void __launch_bounds__(128) blur_adjoint2_kernel(StepArgs a, const float* __restrict__ src) {
+  pdl_enter();
   extern __shared__ float sm[];
   const int n = blockIdx.z / a.C, c = blockIdx.z % a.C;
   if (a.active && !a.active[n]) return;
@@ -389,6 +396,7 @@ static bool blur2_ks(int ks) { return ks == 9 || ks == 15 || ks == 25; }
 // divergence (any non-finite x^{k+1}: keep x^k, reading Q22) and the per-image stop
 // rule at check iterations (reading Q17).
 __global__ void finalize_kernel(FinalizeArgs f) {
+  pdl_enter();
   const int n = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (n >= f.N) return;
@@ -449,6 +457,7 @@ __global__ void finalize_kernel(FinalizeArgs f) {
 // max for the global rule (all-reduced between the two phases when world > 1),
 // then the global-max decision, the active count the host polls, and k += 1.
 __global__ void advance_a_kernel(FinalizeArgs f) {
+  pdl_enter();
   __shared__ float smax[32];
   float m = -1.f;
   for (int n = threadIdx.x; n < f.N; n += blockDim.x) {
@@ -469,6 +478,7 @@ __global__ void advance_a_kernel(FinalizeArgs f) {
 }
 
 __global__ void advance_b_kernel(FinalizeArgs f) {
+  pdl_enter();
   __shared__ int cnt[32];
   __shared__ int stop_all;
   const int k = *f.kdev;
@@ -508,6 +518,7 @@ __global__ void gather_kernel(const int* __restrict__ iters, const float* __rest
 // Eq. 5 / Alg. 1 l.10 / Alg. 2 l.10); averaging -> snapshot mean(z^0..z^k) on a new window
 // minimum, then add z^{k+1} to the running sum (O(1) planes instead of the whole trajectory).
 __global__ void __launch_bounds__(256) post_step_kernel(PostArgs a) {
+  pdl_enter();
   const int n = blockIdx.y;
   const int fl = a.flags[n];
   if (!(fl & 1)) return;
@@ -531,7 +542,7 @@ __global__ void __launch_bounds__(256) post_step_kernel(PostArgs a) {
 
 void launch_post_step(const PostArgs& a, cudaStream_t s) {
   const long long bx = (a.d + 256 * 8 - 1) / (256 * 8);
-  post_step_kernel<<<dim3((unsigned)(bx < 1 ? 1 : bx), a.N), 256, 0, s>>>(a);
+  launch_k(post_step_kernel, dim3((unsigned)(bx < 1 ? 1 : bx), a.N), 256, 0, s, a);
 }
 
 // x-hat = the averaging snapshot for images with a K0 (not diverged)
@@ -592,12 +603,12 @@ __global__ void inpaint_prox_kernel(const float* __restrict__ v, const float* __
 void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
   dim3 grid(a.parts, a.N);
   switch (mode) {
-    case STEP_PROX_INPAINT: pointwise_step_kernel<STEP_PROX_INPAINT><<<grid, 256, 0, s>>>(a); break;
-    case STEP_GRAD_BUF: pointwise_step_kernel<STEP_GRAD_BUF><<<grid, 256, 0, s>>>(a); break;
-    case STEP_GRAD_INPAINT: pointwise_step_kernel<STEP_GRAD_INPAINT><<<grid, 256, 0, s>>>(a); break;
-    case STEP_GRAD_RICIAN: pointwise_step_kernel<STEP_GRAD_RICIAN><<<grid, 256, 0, s>>>(a); break;
-    case STEP_GRAD_MRI: pointwise_step_kernel<STEP_GRAD_MRI><<<grid, 256, 0, s>>>(a); break;
-    default: pointwise_step_kernel<STEP_X1_BUF><<<grid, 256, 0, s>>>(a); break;
+    case STEP_PROX_INPAINT: launch_k(pointwise_step_kernel<STEP_PROX_INPAINT>, grid, 256, 0, s, a); break;
+    case STEP_GRAD_BUF: launch_k(pointwise_step_kernel<STEP_GRAD_BUF>, grid, 256, 0, s, a); break;
+    case STEP_GRAD_INPAINT: launch_k(pointwise_step_kernel<STEP_GRAD_INPAINT>, grid, 256, 0, s, a); break;
+    case STEP_GRAD_RICIAN: launch_k(pointwise_step_kernel<STEP_GRAD_RICIAN>, grid, 256, 0, s, a); break;
+    case STEP_GRAD_MRI: launch_k(pointwise_step_kernel<STEP_GRAD_MRI>, grid, 256, 0, s, a); break;
+    default: launch_k(pointwise_step_kernel<STEP_X1_BUF>, grid, 256, 0, s, a); break;
   }
 }
 
@@ -612,9 +623,9 @@ template <int KS>
 static void launch_blur2(int which, const StepArgs& a, const float* src, cudaStream_t s) {
   dim3 grid((a.W + BT2 - 1) / BT2, (a.H + BT2 - 1) / BT2, a.N * a.C);
   const size_t sm = Blur2<KS>::smem;
-  if (which == 0) blur_residual2_kernel<KS><<<grid, 128, sm, s>>>(a);
-  else if (which == 1) blur_adjoint2_kernel<KS, 0><<<grid, 128, sm, s>>>(a, src);
-  else blur_adjoint2_kernel<KS, 1><<<grid, 128, sm, s>>>(a, src);
+  if (which == 0) launch_k(blur_residual2_kernel<KS>, grid, 128, sm, s, a);
+  else if (which == 1) launch_k(blur_adjoint2_kernel<KS, 0>, grid, 128, sm, s, a, src);
+  else launch_k(blur_adjoint2_kernel<KS, 1>, grid, 128, sm, s, a, src);
 }
 static bool launch_blur2_any(int which, const StepArgs& a, const float* src, cudaStream_t s) {
   switch (a.ksize) {
@@ -629,7 +640,7 @@ void launch_blur_residual(const StepArgs& a, cudaStream_t s) {
   if (launch_blur2_any(0, a, nullptr, s)) return;
   dim3 grid((a.W + BT - 1) / BT, (a.H + BT - 1) / BT, a.N * a.C);
   const size_t sm = blur_smem(a.ksize);
-  blur_residual_kernel<<<grid, 256, sm, s>>>(a);
+  launch_k(blur_residual_kernel, grid, 256, sm, s, a);
 }
 
 void launch_blur_adjoint(int mode, const StepArgs& a, const float* src, cudaStream_t s) {
@@ -637,9 +648,9 @@ void launch_blur_adjoint(int mode, const StepArgs& a, const float* src, cudaStre
   dim3 grid((a.W + BT - 1) / BT, (a.H + BT - 1) / BT, a.N * a.C);
   const size_t sm = blur_smem(a.ksize);
   if (mode == 0) {
-    blur_adjoint_kernel<0><<<grid, 256, sm, s>>>(a, src);
+    launch_k(blur_adjoint_kernel<0>, grid, 256, sm, s, a, src);
   } else {
-    blur_adjoint_kernel<1><<<grid, 256, sm, s>>>(a, src);
+    launch_k(blur_adjoint_kernel<1>, grid, 256, sm, s, a, src);
   }
 }
 
@@ -654,10 +665,10 @@ void init_attrs_step() {
 }
 
 void launch_finalize(const FinalizeArgs& f, cudaStream_t s) {
-  finalize_kernel<<<(f.N + 7) / 8, 256, 0, s>>>(f);
+  launch_k(finalize_kernel, (f.N + 7) / 8, 256, 0, s, f);
 }
-void launch_advance_a(const FinalizeArgs& f, cudaStream_t s) { advance_a_kernel<<<1, 1024, 0, s>>>(f); }
-void launch_advance_b(const FinalizeArgs& f, cudaStream_t s) { advance_b_kernel<<<1, 1024, 0, s>>>(f); }
+void launch_advance_a(const FinalizeArgs& f, cudaStream_t s) { launch_k(advance_a_kernel, 1, 1024, 0, s, f); }
+void launch_advance_b(const FinalizeArgs& f, cudaStream_t s) { launch_k(advance_b_kernel, 1, 1024, 0, s, f); }
 void launch_init_state(const FinalizeArgs& f, cudaStream_t s) { init_state_kernel<<<(f.N + 255) / 256, 256, 0, s>>>(f); }
 void launch_gather(const int* iters, const float* X1, float* X0, int N, long long d, cudaStream_t s) {
   dim3 grid((unsigned)std::min<long long>((d + 255) / 256, 1024), N);
@@ -676,4 +687,11 @@ void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float
       v, y, m, tau, out, total, (long long)H * W, (long long)C * H * W);
 }
 
+}  // namespace ideq
+
+namespace ideq {
+bool pdl_enabled() {
+  static const bool on = [] { const char* e = getenv("IDEQ_NO_PDL"); return !(e && atoi(e) != 0); }();
+  return on;
+}
 }  // namespace ideq
