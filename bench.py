@@ -217,7 +217,8 @@ def main():
     images = list(range(rank * per, (rank + 1) * per))
     prob = synth.make_problem(cfg, images=images)
     stream = torch.cuda.Stream()
-    s = ideq.Solver(cfg, prob["weights"], precision="bf16", device=local, stream=stream, max_batch=per)
+    prec = cfg.get("precision", "bf16")   # C1 is an fp32 config (BASELINE), the others bf16
+    s = ideq.Solver(cfg, prob["weights"], precision=prec, device=local, stream=stream, max_batch=per)
     s.set_operator(prob)
     y = torch.tensor(prob["y"]).cuda()
     x = torch.tensor(prob["x0"]).cuda()
@@ -284,7 +285,18 @@ def main():
             traffic = json.load(open(tp)).get("bytes_per_launch")
         except Exception:
             traffic = None
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+    if tc["ms"] == 0 and prof["conv_simt"]["ms"] > 0:  # FFMA path (C1 fp32): ALU roofline
+        sm = prof["conv_simt"]
+        ffma_peak = 148 * 128 * 2 * 1965e6 / 1e12   # derived: SMs x FP32 lanes x 2 x max SM clock
+        roofline = {"bound": "alu", "achieved": sm["flops"] / (sm["ms"] / 1000.0) / 1e12, "peak": ffma_peak,
+                    "unit": "TFLOP/s", "frac": sm["flops"] / (sm["ms"] / 1000.0) / 1e12 / ffma_peak, "traffic": None,
+                    "kernel": "conv_simt_kernel (all FFMA conv launches of a step)",
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz",
+                    "share_of_step": sm["ms"] / total_ms if total_ms else None,
+                    "per_class_ms_per_step": {k: v["ms"] / kprof for k, v in prof.items()},
+                    "algorithmic_flops_per_step": sm["flops"] / kprof}
+    else:
+      roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "kernel": "conv_tc_kernel (all tcgen05 conv launches of a step)",
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
@@ -307,7 +319,7 @@ def main():
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded piecewise-smooth images, random-init "
+            "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "bf16", "data": "synthetic (seeded piecewise-smooth images, random-init "
             "U-Net weights" + {"inpaint": "; stands in for the paper's BSDS500 inpainting split)",
                                "mri": "; stand-in phantoms for the paper's fastMRI knee data)"}.get(cfg["op"], ")"),
             "config": dict(_config_dict(cfg, per, world), **({"restart_B": args.restart} if args.restart > 0 else {}),

@@ -10,16 +10,19 @@
 namespace ideq {
 
 // ------------------------------------------------------------------ implicit GEMM (FFMA)
-// Tile: 128 output pixels (the same R x Wt pixel tile the tcgen05 path uses) x 64 GEMM
-// columns; 256 threads, 8 pixels x 4 columns each; K staged 16 channels at a time.
-constexpr int SM_BM = 128, SM_BN = 64, SM_BK = 16;
+// Tile: BM output pixels (128: the R x Wt pixel tile the tcgen05 path uses; 32 for small grids
+// such as the one-image C1 config, so the launch spreads over 4x more SMs) x 64 GEMM columns;
+// 256 threads, BM/16 pixels x 4 columns each; K staged 16 channels at a time.
+constexpr int SM_BN = 64, SM_BK = 16;
 
-template <typename T>
+template <typename T, int BM>
 __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __restrict__ in,
                                                         const T* __restrict__ wB, T* __restrict__ out,
                                                         const T* __restrict__ aux) {
   pdl_enter();
-  __shared__ __align__(16) float As[SM_BK][SM_BM + 4];
+  constexpr int PX = BM / 16;          // pixels per thread (compute) = channels per thread (A load)
+  constexpr int TPP = 16 / PX;         // A-load threads per pixel
+  __shared__ __align__(16) float As[SM_BK][BM + 4];
   __shared__ __align__(16) float Bs[SM_BK][SM_BN + 4];
   const int tid = threadIdx.x;
   const int mt = blockIdx.x;
@@ -30,8 +33,8 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
   const int oh0 = th * g.R, ow0 = tw * g.Wt;
   const int tile_px = g.R * g.Wt;
 
-  // A-load role: pixel lpx, 8 channels starting at lhalf*8
-  const int lpx = tid >> 1, lhalf = tid & 1;
+  // A-load role: pixel lpx, PX channels starting at lhalf * PX
+  const int lpx = tid / TPP, lhalf = tid % TPP;
   const int loh = oh0 + lpx / g.Wt, low = ow0 + lpx % g.Wt;
   const bool lvalid = lpx < tile_px && loh < g.OH && low < g.OW;
   // B-load role: column bcol, 4 k-values starting at bk
@@ -40,9 +43,9 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
 
   // compute role
   const int ty = tid >> 4, tx = tid & 15;
-  float acc[8][4];
+  float acc[PX][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < PX; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
 
@@ -51,7 +54,7 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
   // the global-load latency is paid once instead of per step (the small-grid / latency-bound
   // cases: C1, the JFB tape passes)
   const int nkb = g.ntaps * g.nchunk, nkk = g.KC / SM_BK, nsteps = nkb * nkk;
-  float ra[8], rb[4];
+  float ra[PX], rb[4];
   auto load_step = [&](int st) {
     const int kb = st / nkk, kk = (st - kb * nkk) * SM_BK;
     const int tap = kb / g.nchunk, chunk = kb - tap * g.nchunk;
@@ -60,27 +63,31 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
     const T* src = in + ((((long long)img * g.inH + ih) * g.inP + g.dp[tap]) * g.inW + iw) * g.inC + chunk * g.KC;
     const T* wsrc = wB + ((long long)kb * g.ncols + n0 + bcol) * g.KC;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) ra[j] = inb ? ElemOps<T>::ld(src + kk + lhalf * 8 + j) : 0.f;
+    for (int j = 0; j < PX; ++j) ra[j] = inb ? ElemOps<T>::ld(src + kk + lhalf * PX + j) : 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
   };
   if (nsteps > 0) load_step(0);
   for (int st = 0; st < nsteps; ++st) {
 #pragma unroll
-    for (int j = 0; j < 8; ++j) As[lhalf * 8 + j][lpx] = ra[j];
+    for (int j = 0; j < PX; ++j) As[lhalf * PX + j][lpx] = ra[j];
 #pragma unroll
     for (int j = 0; j < 4; ++j) Bs[bk + j][bcol] = rb[j];
     __syncthreads();
     if (st + 1 < nsteps) load_step(st + 1);
 #pragma unroll
     for (int k = 0; k < SM_BK; ++k) {
-      const float4 a0 = *reinterpret_cast<const float4*>(&As[k][ty * 8]);
-      const float4 a1 = *reinterpret_cast<const float4*>(&As[k][ty * 8 + 4]);
+      float av[PX];
+#pragma unroll
+      for (int i = 0; i < PX; i += 2) {
+        const float2 a2 = *reinterpret_cast<const float2*>(&As[k][ty * PX + i]);
+        av[i] = a2.x;
+        av[i + 1] = a2.y;
+      }
       const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
-      const float av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
       const float bv[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i)
+      for (int i = 0; i < PX; ++i)
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
@@ -88,8 +95,8 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
   }
   // epilogue
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int px = ty * 8 + i;
+  for (int i = 0; i < PX; ++i) {
+    const int px = ty * PX + i;
     const int oh = oh0 + px / g.Wt, ow = ow0 + px % g.Wt;
     if (px >= tile_px || oh >= g.OH || ow >= g.OW) continue;
 #pragma unroll
@@ -105,8 +112,19 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
 
 template <typename T>
 void launch_conv_simt(const ConvGeom& g, const T* in, const T* wB, T* out, const T* aux, cudaStream_t s) {
-  dim3 grid(g.N * g.tiles_h * g.tiles_w, (g.ncols + SM_BN - 1) / SM_BN);
-  launch_k(conv_simt_kernel<T>, grid, 256, 0, s, g, in, wB, out, aux);
+  const int nct = (g.ncols + SM_BN - 1) / SM_BN;
+  if ((long long)g.N * g.tiles_h * g.tiles_w * nct < 2 * 148) {  // small grid: 32-pixel tiles
+    ConvGeom g2 = g;
+    g2.Wt = g.OW < 32 ? g.OW : 32;
+    g2.R = 32 / g2.Wt;
+    if (g2.R > g.OH) g2.R = g.OH;
+    if (g2.R < 1) g2.R = 1;
+    g2.tiles_h = (g.OH + g2.R - 1) / g2.R;
+    g2.tiles_w = (g.OW + g2.Wt - 1) / g2.Wt;
+    launch_k(conv_simt_kernel<T, 32>, dim3(g2.N * g2.tiles_h * g2.tiles_w, nct), 256, 0, s, g2, in, wB, out, aux);
+    return;
+  }
+  launch_k(conv_simt_kernel<T, 128>, dim3(g.N * g.tiles_h * g.tiles_w, nct), 256, 0, s, g, in, wB, out, aux);
 }
 
 // ------------------------------------------------------------------ vector helpers
