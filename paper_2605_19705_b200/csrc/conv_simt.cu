@@ -161,13 +161,14 @@ template <typename T, int WO, int C>
 __global__ void __launch_bounds__(256) img2feat_kernel(const float* __restrict__ in, const float* __restrict__ w_t,
                                                        T* __restrict__ out, const T* __restrict__ aux, int epi,
                                                        int N, int H, int W) {
-  pdl_enter();
   __shared__ __align__(16) float wsm[3 * 9][WO];
   __shared__ float tile[3][HT_ROWS + 2][18 + 1];
+  // the weights (constant since create) are staged before waiting for the predecessor grid
   for (int t = threadIdx.x; t < WO * C * 9; t += blockDim.x) {
     const int co = t / (C * 9), r = t % (C * 9);
     wsm[r][co] = w_t[t];  // [ci*9 + a*3 + b][co]
   }
+  pdl_enter();
   const int n = blockIdx.z, h0 = blockIdx.y * HT_ROWS, w0 = blockIdx.x * 16;
   const long long HW = (long long)H * W;
   for (int t = threadIdx.x; t < C * (HT_ROWS + 2) * 18; t += blockDim.x) {
@@ -252,7 +253,6 @@ template <typename T, int WI>
 __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in, const float* __restrict__ w_t,
                                                        float* __restrict__ out, const float* __restrict__ aux,
                                                        float alpha, int N, int C, int H, int W) {
-  pdl_enter();
   extern __shared__ __align__(16) float smf[];
   constexpr int PS = WI + 4;
   float4* wsm = reinterpret_cast<float4*>(smf);  // [9][WI] : (a*3+b, ci) -> (c0, c1, c2, 0)
@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(256) feat2img_kernel(const T* __restrict__ in,
     w4.w = 0.f;
     wsm[t] = w4;
   }
+  pdl_enter();  // weights staged; now wait for the producer of `in`
   constexpr int V = WI / 8;  // 8-channel vectors per pixel
   for (int t = threadIdx.x; t < (HT_ROWS + 2) * 18 * V; t += blockDim.x) {
     const int q = t / V, c8 = (t % V) * 8;
