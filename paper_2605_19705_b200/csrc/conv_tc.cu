@@ -1140,6 +1140,10 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, tmem_holder, 0);
+  // programmatic dependent launch: the prologue above (weights, barriers, TMEM) overlapped the
+  // previous kernel; the image and the active flags are read only after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const long long HW = (long long)H * W, total = (long long)N * HW;
   const long long tiles = (total + 127) / 128;
   const uint32_t idesc = make_idesc_bf16(NC);
@@ -1321,8 +1325,8 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
   FastDiv fdHW, fdW;
   fdHW.init((uint32_t)(H * W));
   fdW.init((uint32_t)W);
-  if (NC == 64) img2feat_tc_kernel<64><<<grid, 128, pad, s>>>(in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
-  else img2feat_tc_kernel<32><<<grid, 128, pad, s>>>(in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
+  if (NC == 64) launch_k(img2feat_tc_kernel<64>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
+  else launch_k(img2feat_tc_kernel<32>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
 }
 
 struct TcPlan {
