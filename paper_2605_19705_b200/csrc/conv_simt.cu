@@ -78,11 +78,19 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
 #pragma unroll
     for (int k = 0; k < SM_BK; ++k) {
       float av[PX];
+      if constexpr (PX % 4 == 0) {
 #pragma unroll
-      for (int i = 0; i < PX; i += 2) {
-        const float2 a2 = *reinterpret_cast<const float2*>(&As[k][ty * PX + i]);
-        av[i] = a2.x;
-        av[i + 1] = a2.y;
+        for (int i = 0; i < PX; i += 4) {
+          const float4 a4 = *reinterpret_cast<const float4*>(&As[k][ty * PX + i]);
+          av[i] = a4.x; av[i + 1] = a4.y; av[i + 2] = a4.z; av[i + 3] = a4.w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < PX; i += 2) {
+          const float2 a2 = *reinterpret_cast<const float2*>(&As[k][ty * PX + i]);
+          av[i] = a2.x;
+          av[i + 1] = a2.y;
+        }
       }
       const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
       const float bv[4] = {b.x, b.y, b.z, b.w};
