@@ -90,7 +90,7 @@ __device__ __forceinline__ float apply_epi(int epi, float acc, float aux) {
 // Programmatic dependent launch for the per-iteration kernels: launched with the programmatic
 // stream-serialization attribute, each waits (griddepcontrol.wait) for its predecessor grid to
 // complete and flush before touching any global data, then lets its own successor be scheduled,
-// so the launch latency of the next kernel overlaps this one. IDEQ_NO_PDL=1 launches plainly.
+// so the launch latency of the next kernel overlaps this one. Opt-in: IDEQ_PDL_SMALL=1 (step.cu).
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

@@ -690,8 +690,13 @@ void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float
 }  // namespace ideq
 
 namespace ideq {
+// Off by default: on B200 the programmatic launch of the small per-iteration kernels (and of the
+// fused head) measured ~1% SLOWER on the C3 bench (10.20k vs 10.32k img-it/s, 3 interleaved A/B
+// pairs, tools/ab_lib.sh) and no better on the latency-bound C1 -- the early-launched CTAs wait
+// in SM slots while the persistent conv grids run. IDEQ_PDL_SMALL=1 turns it on (the kernels
+// call griddepcontrol.wait either way; without the launch attribute it returns at once).
 bool pdl_enabled() {
-  static const bool on = [] { const char* e = getenv("IDEQ_NO_PDL"); return !(e && atoi(e) != 0); }();
+  static const bool on = [] { const char* e = getenv("IDEQ_PDL_SMALL"); return e && atoi(e) != 0; }();
   return on;
 }
 }  // namespace ideq
