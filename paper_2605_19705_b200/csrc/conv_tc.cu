@@ -378,7 +378,13 @@ struct TcParams {
   uint32_t acc_cols;
   // per-image active flags of the solver (null: compute every tile). Tiles of frozen images are
   // skipped by every warp role alike, so the barrier rings stay in step (not used by CTA pairs).
-  const int* active;
+  // live-tile list (tol > 0 per-image solves): the solver keeps a compacted list of its active
+  // images (act_list[0 .. *n_act)); every warp role walks the tiles of those images only, in the
+  // same order, so work stays balanced over the CTAs when images freeze (null: every tile)
+  const int* act_list;
+  const int* n_act;
+  FastDiv fd_tpi;   // tiles per image (M tiles x N tiles)
+  int tpi;
   // direct epilogue (opt-in, 3x3 halo layers with BN <= 64): the aux operand is read from global
   // memory into registers and the outputs are stored from registers (NHWC rows of ncols
   // channels), bypassing the shared-memory staging + TMA store + aux TMA of the default path
@@ -387,11 +393,13 @@ struct TcParams {
   const __nv_bfloat16* aux_ptr;
 };
 
-// Frozen-image test on the shared bitmask, broadcast from lane 0 so that the compiler keeps the
-// warp roles' loops (descriptor math, ring indices) on the uniform datapath.
-__device__ __forceinline__ bool tile_frozen(const uint32_t* s_act, int img) {
-  const int bit = (int)((s_act[img >> 5] >> (img & 31)) & 1u);
-  return __shfl_sync(0xffffffffu, bit, 0) == 0;
+// k-th live tile -> raw tile index (identity without a live list). The list lives in global
+// memory (written by the previous iteration's bookkeeping kernel) and is read through the
+// read-only path; every role computes the same sequence.
+__device__ __forceinline__ int live_tile(const TcParams& P, int L) {
+  if (!P.act_list) return L;
+  const int q = (int)P.fd_tpi.div((uint32_t)L);
+  return __ldg(P.act_list + q) * P.tpi + (L - q * P.tpi);
 }
 
 // tile t -> (image, output row h0, output col w0, n tile)
@@ -497,12 +505,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   // warp index broadcast from lane 0 so the compiler knows it is warp-uniform (uniform datapath)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
-  // active-image bitmask (<= 1024 images), read once per CTA so the per-tile skip test is a
-  // shared-memory load instead of a dependent global load in every warp role's loop
   // Programmatic dependent launch: the next layer may be scheduled now; its CTAs run their
   // prologue as SMs free up and wait (griddepcontrol.wait) for this grid before touching data.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  __shared__ uint32_t s_act[32];
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
@@ -542,15 +547,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   }
   // everything below reads what earlier kernels wrote: wait for them (no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (P.active) {  // one flag per thread, one ballot per warp and 32-image word
-#pragma unroll
-    for (int r = 0; r < 3; ++r) {
-      const int w = warp + r * (TC_THREADS / 32);
-      const int i = w * 32 + lane;
-      const uint32_t bits = __ballot_sync(0xffffffffu, i < g.N && i < 1024 && P.active[i] != 0);
-      if (lane == 0 && w < 32 && w * 32 < g.N) s_act[w] = bits;
-    }
-  }
   tc_fence_before();
   if (PAIR) cluster_sync_all();  // barrier inits + TMEM allocation visible to the peer
   else __syncthreads();
@@ -566,6 +562,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
   const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const int nbox = BN / BOXC;
+  // tiles this launch walks: all of them, or the live list's (read after griddepcontrol.wait)
+  const int tot_it = (P.act_list && !PAIR) ? *(volatile const int*)P.n_act * P.tpi : total;
 
   if (warp == 0) {
     // ---------------- TMA producer: the whole warp walks the loop (warp-uniform state stays in
@@ -574,9 +572,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
-    for (int t = t0; t < total; t += tstep) {
+    for (int L = t0; L < tot_it; L += tstep) {
+      const int t = live_tile(P, L);
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
-      if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const int nload = HALO ? g.nchunk : nkb;
       for (int kb = 0; kb < nload; ++kb) {
@@ -627,9 +625,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     if (HAS_AUX && !P.direct) {
       int acc = 0;
       uint32_t aph = 0;
-      for (int t = t0; t < total; t += tstep) {
-        const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
-        if (P.active && tile_frozen(s_act, ti.img)) continue;
+      for (int L = t0; L < tot_it; L += tstep) {
+        const TileIdx ti = tile_index(P, live_tile(P, L), PAIR ? (int)rank : -1);
         mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
         if (elect_one()) {
           mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
@@ -665,8 +662,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     uint32_t aph = 0;
     if (MODE == 1 || ROW) mbar_wait(wfull, 0);
     const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
-    for (int t = t0; t < total; t += tstep) {
-      if (P.active && tile_frozen(s_act, tile_index(P, t).img)) continue;
+    for (int L = t0; L < tot_it; L += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (ROW ? (uint32_t)acc * P.acc_cols : (uint32_t)(acc * BN));
@@ -749,9 +745,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     float* xbase = reinterpret_cast<float*>(gbase + (sX - base));
     int acc = 0, prev_acc = -1, jpar = 0;
     uint32_t aph = 0;
-    for (int t = t0; t < total; t += tstep) {
-      const TileIdx ti = tile_index(P, t);
-      if (P.active && tile_frozen(s_act, ti.img)) continue;
+    for (int L = t0; L < tot_it; L += tstep) {
+      const TileIdx ti = tile_index(P, live_tile(P, L));
       const int img = ti.img, h0 = ti.h0;
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
@@ -897,9 +892,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     const int sh = (quad * 32) / g.Wt, sw = (quad * 32) % g.Wt;
     int acc = 0, prev_acc = -1;
     uint32_t aph = 0;
-    for (int t = t0; t < total; t += tstep) {
+    for (int L = t0; L < tot_it; L += tstep) {
+      const int t = live_tile(P, L);
       const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
-      if (P.active && tile_frozen(s_act, ti.img)) continue;
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       if (EPI != EPI_IMG && !PAIR && P.direct) {
         // ---- direct epilogue (BN <= 64: this thread's half row is 16 or 32 columns)
@@ -1330,7 +1325,7 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
 }
 
 struct TcPlan {
-  const int* active_ptr;  // the solver's per-image active flags (tile skipping)
+  const int* list_ptr;  // the solver's compacted active-image list (tile skipping)
   CUtensorMap tmA, tmB, tmOut, tmAux, tmSlab;
   TcParams P;
   int KC, epi, boxc, grid, halo;
@@ -1631,16 +1626,20 @@ static void launch_epi(const TcPlan* p, cudaStream_t s) {
   }
 }
 
-void tc_plan_set_active(TcPlan* p, const int* active) {
-  // a CTA pair must walk the same units; the in-kernel bitmask covers 1024 images
+void tc_plan_set_active(TcPlan* p, const int* act_list, const int* n_act) {
+  // a CTA pair must walk the same units (its tile loop keeps the full order)
   const char* ns = getenv("IDEQ_NO_SKIP");  // A/B switch for measurements
-  p->active_ptr = (p->halo == 3 || p->P.g.N > 1024 || (ns && atoi(ns) != 0)) ? nullptr : active;
-  p->P.active = nullptr;
+  const bool ok = !(p->halo == 3 || (ns && atoi(ns) != 0));
+  p->list_ptr = ok ? act_list : nullptr;
+  p->P.n_act = n_act;
+  p->P.act_list = nullptr;
+  p->P.tpi = p->P.g.tiles_h * p->P.g.tiles_w * p->P.n_tiles;
+  p->P.fd_tpi.init((uint32_t)p->P.tpi);
 }
 
-// Tile skipping costs ~3% of a fixed-count iteration (measured), so it is switched on only for
-// solves that can freeze images (tol > 0); the CUDA graph of each parameter set captures the choice.
-void tc_plan_enable_skip(TcPlan* p, bool on) { p->P.active = on ? p->active_ptr : nullptr; }
+// The live list is switched on only for solves that can freeze images (tol > 0); the CUDA graph
+// of each parameter set captures the choice.
+void tc_plan_enable_skip(TcPlan* p, bool on) { p->P.act_list = on ? p->list_ptr : nullptr; }
 
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C) {
   p->P.img_out = out;

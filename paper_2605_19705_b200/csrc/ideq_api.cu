@@ -125,6 +125,7 @@ struct ideq_ctx {
   float* Xsnap = nullptr;
   int parts_cap = 0;
   int *active = nullptr, *status = nullptr, *iters = nullptr, *n_active = nullptr, *kdev = nullptr;
+  int* act_list = nullptr;  // compacted active-image indices (conv tile loops of tol > 0 solves)
   float *res = nullptr, *r_now = nullptr, *rmax = nullptr, *trace = nullptr;
   int trace_cap = 65536;
   int* h_pinned = nullptr;  // host mirror of n_active
@@ -462,7 +463,7 @@ ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, c
     L.plan = tc_make_plan(L.g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)out,
                           (const __nv_bfloat16*)aux, ctx->num_sms, err, sizeof(err));
     if (!L.plan) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
-    tc_plan_set_active(L.plan, ctx->active);  // frozen (converged / diverged) images cost nothing
+    tc_plan_set_active(L.plan, ctx->act_list, ctx->n_active);  // frozen images cost nothing
   }
   ctx->prog.push_back(L);
   if (out_layer) *out_layer = &ctx->prog.back();
@@ -970,7 +971,7 @@ FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
   f.partials = ctx->partials;
   f.active = ctx->active; f.status = ctx->status; f.iters = ctx->iters;
   f.res = ctx->res; f.r_now = ctx->r_now; f.trace = ctx->trace; f.rmax = ctx->rmax;
-  f.n_active = ctx->n_active; f.kdev = ctx->kdev;
+  f.n_active = ctx->n_active; f.kdev = ctx->kdev; f.act_list = ctx->act_list;
   const bool next1 = p && (p->restart || p->averaging);
   f.restart = p ? p->restart : 0;
   f.B2 = p ? (double)p->restart_B * (double)p->restart_B : 0.0;
@@ -1283,7 +1284,7 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
     ctx->parts_cap = pc;
   }
   AL(partials, (size_t)N * ctx->parts_cap * 3 * sizeof(float))
-  AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int))
+  AL(active, N * sizeof(int)) AL(status, N * sizeof(int)) AL(iters, N * sizeof(int)) AL(act_list, N * sizeof(int))
   AL(rk, N * sizeof(int)) AL(rsum, N * sizeof(double)) AL(flags, N * sizeof(int)) AL(nrest, N * sizeof(int))
   AL(best, N * sizeof(float)) AL(k0, N * sizeof(int)) AL(Zsum, plane) AL(Xsnap, plane)
   AL(res, N * sizeof(float)) AL(r_now, N * sizeof(float)) AL(rmax, 16) AL(n_active, 16) AL(kdev, 16)

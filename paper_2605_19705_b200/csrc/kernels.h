@@ -43,6 +43,7 @@ struct FinalizeArgs {
   float* trace;   // [max_iter] or null
   float* rmax;    // 1 float (NCCL all-reduce target)
   int* n_active;
+  int* act_list;  // [N] compacted indices of the active images (first *n_active), for the conv tile loops
   int* kdev;
   // NEXT-1: restart (Eq. 5) and averaging (Alg. 1/2 steps 12-13)
   int restart;        // 0 off, 1 Alg. 1 semantics, 2 Alg. 2 semantics
@@ -160,7 +161,7 @@ TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bflo
 void tc_launch(const TcPlan* p, cudaStream_t s);
 void tc_free_plan(TcPlan* p);
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C);
-void tc_plan_set_active(TcPlan* p, const int* active);
+void tc_plan_set_active(TcPlan* p, const int* act_list, const int* n_act);  // live-image list for tile skipping
 void tc_plan_enable_skip(TcPlan* p, bool on);
 int tc_plan_is_halo(const TcPlan* p);
 // im2col of a C-channel fp32 NCHW image into [N][H][W][32] bf16: k = c*9 + a*3 + b (zero beyond 9C)

@@ -503,6 +503,19 @@ __global__ void advance_b_kernel(FinalizeArgs f) {
     *f.n_active = s;
     *f.kdev = k + 1;
   }
+  // compacted list of the active images in index order (the conv kernels' live tiles); the
+  // launch has one thread per image (N <= 1024 when skipping is on; the list is unused otherwise)
+  if (f.act_list && f.N <= (int)blockDim.x) {
+    __syncthreads();  // thread 0 has read the counts in cnt[] before they are overwritten
+    const int n = threadIdx.x, lane = n & 31, w = n >> 5;
+    const int a = (n < f.N && f.active[n]) ? 1 : 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, a);
+    if (lane == 0) cnt[w] = __popc(bal);   // cnt reused: its totals were consumed above
+    __syncthreads();
+    int off = 0;
+    for (int i = 0; i < w; ++i) off += cnt[i];
+    if (a) f.act_list[off + __popc(bal & ((1u << lane) - 1u))] = n;
+  }
 }
 
 // x-hat_n = x^{iters_n}: images whose last accepted iterate sits in X1 are copied to X0.
@@ -564,6 +577,7 @@ void launch_avg_out(const int* k0, const int* status, const int* iters, int K, c
 __global__ void init_state_kernel(FinalizeArgs f) {
   for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < f.N; n += gridDim.x * blockDim.x) {
     f.active[n] = 1;
+    if (f.act_list) f.act_list[n] = n;
     f.status[n] = 1;
     f.iters[n] = 0;
     f.res[n] = __int_as_float(0x7fc00000);
