@@ -1100,7 +1100,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
                                                           const __nv_bfloat16* __restrict__ wB,
                                                           const __grid_constant__ CUtensorMap tmO, int N, int C,
                                                           int H, int W, const FastDiv fdHW, const FastDiv fdW,
-                                                          const int* __restrict__ active) {
+                                                          const int* __restrict__ act_list, const int* n_act) {
   __shared__ __align__(1024) unsigned char sAraw[128 * 64];  // one A tile: the loop waits for each MMA
   __shared__ __align__(1024) unsigned char sBraw[NC * 64];
   // output staging [2][128 pixels x NC] in the TMA store's swizzle (SW64 for NC = 32, SW128 for
@@ -1185,20 +1185,23 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
       }
     }
   };
-  // tiles whose pixels all belong to frozen images (early-stopping solves) are skipped
-  auto next_live = [&](long long tt) {
-    if (active)
-      while (tt < tiles && !active[(int)fdHW.div((uint32_t)(tt * 128))] &&
-             !active[(int)fdHW.div((uint32_t)(tt * 128 + 127 < total ? tt * 128 + 127 : total - 1))])
-        tt += gridDim.x;
-    return tt;
+  // early-stopping solves: walk only the tiles of the active images (the solver's compacted
+  // list; images are whole 128-pixel tiles when H*W % 128 == 0, else every tile is computed)
+  const long long tpi = HW / 128;
+  const bool use_list = act_list != nullptr && (HW % 128) == 0;
+  const long long nlog = use_list ? (long long)(*(volatile const int*)n_act) * tpi : tiles;
+  auto raw_tile = [&](long long L) -> long long {
+    if (!use_list) return L;
+    const long long q = L / tpi;
+    return (long long)__ldg(act_list + q) * tpi + (L - q * tpi);
   };
   int it = 0;
   long long t_prev = -1;
-  long long tnext = next_live(blockIdx.x);
-  if (tnext < tiles) load_patch(tnext);
-  for (long long t = tnext; t < tiles; t = tnext, ++it) {
-    tnext = next_live(t + gridDim.x);
+  long long Lnext = blockIdx.x;
+  if (Lnext < nlog) load_patch(raw_tile(Lnext));
+  for (long long L = Lnext; L < nlog; L = Lnext, ++it) {
+    Lnext = L + gridDim.x;
+    const long long t = raw_tile(L);
     const int buf = it & 1;  // output staging buffer (the only double-buffered resource)
     float v[32];
 #pragma unroll
@@ -1220,7 +1223,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
     // the next tile's patch loads are issued only now: the proxy fence above (MEMBAR.ALL.CTA)
     // waits for every outstanding load of the thread, so loads issued before it would stall it;
     // from here they overlap the MMA round trip and this tile's epilogue
-    if (tnext < tiles) load_patch(tnext);
+    if (Lnext < nlog) load_patch(raw_tile(Lnext));
     if (tid == 0) {
       if (t_prev >= 0) {  // the previous tile's staged output: one TMA tensor store (rows past the end clipped)
         tma_store_2d(&tmO, smem_u32(sOdyn + (buf ^ 1) * 128 * NC * 2), 0, (int)(t_prev * 128));
@@ -1308,7 +1311,8 @@ I2FPlan* img2feat_make_plan(__nv_bfloat16* out, int N, int H, int W, int NC, cha
 }
 void img2feat_free_plan(I2FPlan* p) { delete p; }
 
-void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* active, int N, int C,
+void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* act_list,
+                        const int* n_act, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s) {
   // residency is capped by shared memory; the CTAs' TMEM allocations (NC columns each, <= 8 x 32 or
   // 5 x 64) stay within the SM's 512 columns
@@ -1320,8 +1324,10 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
   FastDiv fdHW, fdW;
   fdHW.init((uint32_t)(H * W));
   fdW.init((uint32_t)W);
-  if (NC == 64) launch_k(img2feat_tc_kernel<64>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
-  else launch_k(img2feat_tc_kernel<32>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, active);
+  if (NC == 64)
+    launch_k(img2feat_tc_kernel<64>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, act_list, n_act);
+  else
+    launch_k(img2feat_tc_kernel<32>, grid, 128, pad, s, in, wB, plan->tmO, N, C, H, W, fdHW, fdW, act_list, n_act);
 }
 
 struct TcPlan {

@@ -796,7 +796,8 @@ void run_layer(ideq_ctx* ctx, const Layer& L) {
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
   if (L.kind == L_IMG2FEAT_TC) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
-    launch_img2feat_tc(L.i2f, L.in_img, (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->active : nullptr,
+    launch_img2feat_tc(L.i2f, L.in_img, (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->act_list : nullptr,
+                       ctx->n_active,
                        L.N, L.C, L.H, L.W, L.wfeat, ctx->num_sms, s);
   } else if (L.kind == L_GEMM) {
     if (L.tc) {

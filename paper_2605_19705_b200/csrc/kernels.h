@@ -168,7 +168,8 @@ int tc_plan_is_halo(const TcPlan* p);
 struct I2FPlan;  // fused head: the output tensor map (conv_tc.cu)
 I2FPlan* img2feat_make_plan(__nv_bfloat16* out, int N, int H, int W, int NC, char* err, size_t errlen);
 void img2feat_free_plan(I2FPlan* p);
-void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* active, int N, int C,
+void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* act_list,
+                        const int* n_act, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s);
 
 // Raise the dynamic shared-memory limit of every kernel once (before any graph capture).
