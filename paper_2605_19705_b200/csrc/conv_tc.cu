@@ -1544,12 +1544,18 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
   const uint32_t acc_w = p->halo == 4 ? P.acc_cols : (uint32_t)BN;  // TMEM columns per stage
-  for (int na = ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2); na >= 2 && !stages; na -= 2) {
+  // A/B knobs for measurements: IDEQ_NA2=1 starts at 2 accumulator stages, IDEQ_CTA3=1 lets
+  // resident-weight layers try 3 CTAs per SM
+  static const bool na2 = [] { const char* e = getenv("IDEQ_NA2"); return e && atoi(e) != 0; }();
+  static const bool cta3 = [] { const char* e = getenv("IDEQ_CTA3"); return e && atoi(e) != 0; }();
+  static const bool na8 = [] { const char* e = getenv("IDEQ_NA8"); return e && atoi(e) != 0; }();
+  const int na0 = na2 ? 2 : (na8 && 8 * acc_w <= 256 && p->halo) ? 8 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
+  for (int na = na0; na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * acc_w) tc <<= 1;
     const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + xbytes + 512;
-    for (int c = (p->halo == 3 ? 1 : 2); c >= 1 && !stages; --c) {  // a CTA pair: one CTA per SM
-      const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
+    for (int c = (p->halo == 3 ? 1 : (cta3 && p->halo == 1) ? 3 : 2); c >= 1 && !stages; --c) {  // a CTA pair: one CTA per SM
+      const size_t avail = c == 3 ? (227 * 1024) / 3 - 1024 : c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
       int st = (int)((avail - fixed) / op_stage);
       if (st > max_stages) st = max_stages;
