@@ -305,7 +305,10 @@ def main():
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
                 "share_of_step": tc["ms"] / total_ms if total_ms else None,
                 "per_class_ms_per_step": {k: v["ms"] / kprof for k, v in prof.items()},
-                "algorithmic_flops_per_step": tc["flops"] / kprof}
+                "algorithmic_flops_per_step": tc["flops"] / kprof,
+                # algorithmic HBM bytes per launch (each activation read / written once, weights
+                # once) beside the ncu-measured `traffic` of the same launches
+                "algorithmic_bytes_per_launch": (tc["bytes"] / tc["launches"]) if tc["launches"] else None}
 
     # ---- ms to tolerance (tol = 1e-4, per-image stop)
     tol_info = None

@@ -1549,7 +1549,9 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   static const bool na2 = [] { const char* e = getenv("IDEQ_NA2"); return e && atoi(e) != 0; }();
   static const bool cta3 = [] { const char* e = getenv("IDEQ_CTA3"); return e && atoi(e) != 0; }();
   static const bool na8 = [] { const char* e = getenv("IDEQ_NA8"); return e && atoi(e) != 0; }();
-  const int na0 = na2 ? 2 : (na8 && 8 * acc_w <= 256 && p->halo) ? 8 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
+  static const bool na6 = [] { const char* e = getenv("IDEQ_NA6"); return e && atoi(e) != 0; }();
+  const int na0 = na2 ? 2 : (na8 && 8 * acc_w <= 256 && p->halo) ? 8
+                : (na6 && acc_w == 64 && p->halo) ? 6 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
   for (int na = na0; na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * acc_w) tc <<= 1;
