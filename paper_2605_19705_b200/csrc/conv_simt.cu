@@ -11,68 +11,109 @@ namespace ideq {
 
 // ------------------------------------------------------------------ implicit GEMM (FFMA)
 // Tile: BM output pixels (128: the R x Wt pixel tile the tcgen05 path uses; 32 for small grids
-// such as the one-image C1 config, so the launch spreads over 4x more SMs) x 64 GEMM columns;
-// 256 threads, BM/16 pixels x 4 columns each; K staged 16 channels at a time.
+// such as the one-image C1 config, so the launch spreads over 4x more SMs) x BN GEMM columns
+// (64, or 128 for layers with >= 128 columns: 8 x 8 register blocks, a third fewer shared loads
+// per FMA); 256 threads, BM/16 pixels x BN/16 columns each; K staged 16 channels at a time.
 constexpr int SM_BN = 64, SM_BK = 16;
 
-template <typename T, int BM>
+// 16-byte vector of consecutive channels -> floats
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void ld(const float* p, float* v) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+};
+template <> struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void ld(const __nv_bfloat16* p, float* v) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) { const float2 f = __bfloat1622float2(h[e]); v[2 * e] = f.x; v[2 * e + 1] = f.y; }
+  }
+};
+
+template <typename T, int BM, int BN = SM_BN>
 __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __restrict__ in,
                                                         const T* __restrict__ wB, T* __restrict__ out,
                                                         const T* __restrict__ aux) {
   pdl_enter();
   constexpr int PX = BM / 16;          // pixels per thread (compute) = channels per thread (A load)
-  constexpr int TPP = 16 / PX;         // A-load threads per pixel
   __shared__ __align__(16) float As[SM_BK][BM + 4];
-  __shared__ __align__(16) float Bs[SM_BK][SM_BN + 4];
+  constexpr int CPT = BN / 16;         // columns per thread (compute) = k-values per thread (B load)
+  __shared__ __align__(16) float Bs[SM_BK][BN + 4];
   const int tid = threadIdx.x;
   const int mt = blockIdx.x;
-  const int n0 = blockIdx.y * SM_BN;
+  const int n0 = blockIdx.y * BN;
   const int per_img = g.tiles_h * g.tiles_w;
   const int img = mt / per_img;
   const int th = (mt % per_img) / g.tiles_w, tw = mt % g.tiles_w;
   const int oh0 = th * g.R, ow0 = tw * g.Wt;
   const int tile_px = g.R * g.Wt;
 
-  // A-load role: pixel lpx, PX channels starting at lhalf * PX
-  const int lpx = tid / TPP, lhalf = tid % TPP;
-  const int loh = oh0 + lpx / g.Wt, low = ow0 + lpx % g.Wt;
-  const bool lvalid = lpx < tile_px && loh < g.OH && low < g.OW;
-  // B-load role: column bcol, 4 k-values starting at bk
-  const int bcol = tid >> 2, bk = (tid & 3) * 4;
+  // A-load role: 16-byte vectors of VEC consecutive channels; vector v = tid + q * 256 holds
+  // channels (v % CPV) * VEC .. of tile pixel v / CPV, so a warp reads whole 32-byte sectors of
+  // neighbouring pixels (one scalar load per channel at a pixel stride left 1 of 8 bytes used)
+  constexpr int VEC = Vec16<T>::N, CPV = SM_BK / VEC, NVEC = BM * CPV, VPT = (NVEC + 255) / 256;
+  int vpx[VPT], vcg[VPT], voh[VPT], vow[VPT];
+  bool vok[VPT];
+#pragma unroll
+  for (int q = 0; q < VPT; ++q) {
+    const int v = tid + q * 256;
+    vpx[q] = v / CPV;
+    vcg[q] = (v % CPV) * VEC;
+    voh[q] = oh0 + vpx[q] / g.Wt;
+    vow[q] = ow0 + vpx[q] % g.Wt;
+    vok[q] = v < NVEC && vpx[q] < tile_px && voh[q] < g.OH && vow[q] < g.OW;
+  }
+  // B-load role: column bcol, CPT k-values starting at bk
+  const int bcol = tid / (16 / CPT), bk = (tid % (16 / CPT)) * CPT;
   const bool bvalid = (n0 + bcol) < g.ncols;
 
   // compute role
   const int ty = tid >> 4, tx = tid & 15;
-  float acc[PX][4];
+  float acc[PX][CPT];
 #pragma unroll
   for (int i = 0; i < PX; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < CPT; ++j) acc[i][j] = 0.f;
 
   // K loop over (tap, chunk, 16-channel slice) steps, software-pipelined: the next step's
   // operands are loaded into registers while this step's products run from shared memory, so
   // the global-load latency is paid once instead of per step (the small-grid / latency-bound
   // cases: C1, the JFB tape passes)
   const int nkb = g.ntaps * g.nchunk, nkk = g.KC / SM_BK, nsteps = nkb * nkk;
-  float ra[PX], rb[4];
+  float ra[VPT][VEC], rb[CPT];
   auto load_step = [&](int st) {
     const int kb = st / nkk, kk = (st - kb * nkk) * SM_BK;
     const int tap = kb / g.nchunk, chunk = kb - tap * g.nchunk;
-    const int ih = loh + g.dh[tap], iw = low + g.dw[tap];
-    const bool inb = lvalid && ih >= 0 && ih < g.inH && iw >= 0 && iw < g.inW;
-    const T* src = in + ((((long long)img * g.inH + ih) * g.inP + g.dp[tap]) * g.inW + iw) * g.inC + chunk * g.KC;
+#pragma unroll
+    for (int q = 0; q < VPT; ++q) {
+      const int ih = voh[q] + g.dh[tap], iw = vow[q] + g.dw[tap];
+      if (vok[q] && ih >= 0 && ih < g.inH && iw >= 0 && iw < g.inW) {
+        const T* src = in + ((((long long)img * g.inH + ih) * g.inP + g.dp[tap]) * g.inW + iw) * g.inC + chunk * g.KC;
+        Vec16<T>::ld(src + kk + vcg[q], ra[q]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) ra[q][e] = 0.f;
+      }
+    }
     const T* wsrc = wB + ((long long)kb * g.ncols + n0 + bcol) * g.KC;
 #pragma unroll
-    for (int j = 0; j < PX; ++j) ra[j] = inb ? ElemOps<T>::ld(src + kk + lhalf * PX + j) : 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
+    for (int j = 0; j < CPT; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
   };
   if (nsteps > 0) load_step(0);
   for (int st = 0; st < nsteps; ++st) {
 #pragma unroll
-    for (int j = 0; j < PX; ++j) As[lhalf * PX + j][lpx] = ra[j];
+    for (int q = 0; q < VPT; ++q)
+      if (tid + q * 256 < NVEC) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) Bs[bk + j][bcol] = rb[j];
+        for (int e = 0; e < VEC; ++e) As[vcg[q] + e][vpx[q]] = ra[q][e];
+      }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) Bs[bk + j][bcol] = rb[j];
     __syncthreads();
     if (st + 1 < nsteps) load_step(st + 1);
 #pragma unroll
@@ -92,12 +133,24 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
           av[i + 1] = a2.y;
         }
       }
-      const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * 4]);
-      const float bv[4] = {b.x, b.y, b.z, b.w};
+      float bv[CPT];
+      if constexpr (CPT % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < CPT; j += 4) {
+          const float4 b = *reinterpret_cast<const float4*>(&Bs[k][tx * CPT + j]);
+          bv[j] = b.x; bv[j + 1] = b.y; bv[j + 2] = b.z; bv[j + 3] = b.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < CPT; j += 2) {
+          const float2 b = *reinterpret_cast<const float2*>(&Bs[k][tx * CPT + j]);
+          bv[j] = b.x; bv[j + 1] = b.y;
+        }
+      }
 #pragma unroll
       for (int i = 0; i < PX; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        for (int j = 0; j < CPT; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
@@ -108,8 +161,8 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
     const int oh = oh0 + px / g.Wt, ow = ow0 + px % g.Wt;
     if (px >= tile_px || oh >= g.OH || ow >= g.OW) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int col = n0 + tx * 4 + j;
+    for (int j = 0; j < CPT; ++j) {
+      const int col = n0 + tx * CPT + j;
       if (col >= g.ncols) continue;
       const long long o = out_offset(g, img, oh, ow, col);
       const float av = (g.epi == EPI_RESADD || g.epi == EPI_SIGMUL) ? ElemOps<T>::ld(aux + o) : 0.f;
@@ -130,6 +183,22 @@ void launch_conv_simt(const ConvGeom& g, const T* in, const T* wB, T* out, const
     g2.tiles_h = (g.OH + g2.R - 1) / g2.R;
     g2.tiles_w = (g.OW + g2.Wt - 1) / g2.Wt;
     launch_k(conv_simt_kernel<T, 32>, dim3(g2.N * g2.tiles_h * g2.tiles_w, nct), 256, 0, s, g2, in, wB, out, aux);
+    return;
+  }
+  if (g.ncols == 32) {  // 32-column layers: 256-pixel tiles (16 x 2 per thread), no idle columns
+    ConvGeom g2 = g;
+    g2.Wt = g.OW < 256 ? g.OW : 256;
+    g2.R = 256 / g2.Wt;
+    if (g2.R > g.OH) g2.R = g.OH;
+    if (g2.R < 1) g2.R = 1;
+    g2.tiles_h = (g.OH + g2.R - 1) / g2.R;
+    g2.tiles_w = (g.OW + g2.Wt - 1) / g2.Wt;
+    launch_k(conv_simt_kernel<T, 256, 32>, dim3(g2.N * g2.tiles_h * g2.tiles_w, 1), 256, 0, s, g2, in, wB, out, aux);
+    return;
+  }
+  if (g.ncols >= 128 && g.ncols % 128 == 0) {  // wide layers: 128-column tiles, 8 x 8 per thread
+    launch_k(conv_simt_kernel<T, 128, 128>, dim3(g.N * g.tiles_h * g.tiles_w, g.ncols / 128), 256, 0, s, g, in, wB,
+             out, aux);
     return;
   }
   launch_k(conv_simt_kernel<T, 128>, dim3(g.N * g.tiles_h * g.tiles_w, nct), 256, 0, s, g, in, wB, out, aux);
