@@ -101,8 +101,16 @@ __global__ void __launch_bounds__(256) conv_simt_kernel(ConvGeom g, const T* __r
       }
     }
     const T* wsrc = wB + ((long long)kb * g.ncols + n0 + bcol) * g.KC;
+    if constexpr (sizeof(T) == 4 && CPT % 4 == 0) {  // fp32 weights: 16-byte loads
 #pragma unroll
-    for (int j = 0; j < CPT; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
+      for (int j = 0; j < CPT; j += 4) {
+        if (bvalid) Vec16<T>::ld(wsrc + kk + bk + j, rb + j);
+        else rb[j] = rb[j + 1] = rb[j + 2] = rb[j + 3] = 0.f;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < CPT; ++j) rb[j] = bvalid ? ElemOps<T>::ld(wsrc + kk + bk + j) : 0.f;
+    }
   };
   if (nsteps > 0) load_step(0);
   for (int st = 0; st < nsteps; ++st) {
