@@ -292,6 +292,14 @@ __device__ __forceinline__ float lg2_approx(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+#ifndef IDEQ_SP_MIX
+#define IDEQ_SP_MIX 1
+#endif
+// IDEQ_SP_MIX (A/B build): odd elements take log1p from the FMA-pipe polynomial instead of MUFU lg2
+__device__ __forceinline__ float softplus_poly_log(float t) {
+  const float u = ex2_approx(-1.4426950408889634f * fabsf(t));
+  return fmaxf(t, 0.f) + log1p01(u);
+}
 template <bool POLY = false>
 __device__ __forceinline__ float softplus_fast(float t) {
 #if IDEQ_SP_MUFU
@@ -833,7 +841,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             } else {
 #pragma unroll
               for (int e = 0; e < 8; ++e)
-                o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v[q * 8 + e]) : v[q * 8 + e];
+                o[e] = (EPI == EPI_SOFTPLUS) ? ((IDEQ_SP_MIX && (e & 1)) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast<false>(v[q * 8 + e])) : v[q * 8 + e];
             }
             uint4 w;
             __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
@@ -1023,7 +1031,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v[q * 8 + e]) : v[q * 8 + e];
+              o[e] = (EPI == EPI_SOFTPLUS) ? ((IDEQ_SP_MIX && (e & 1)) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast<false>(v[q * 8 + e])) : v[q * 8 + e];
           }
           uint4 w;
           __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
