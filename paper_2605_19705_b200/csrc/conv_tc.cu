@@ -1552,11 +1552,14 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
   const uint32_t acc_w = p->halo == 4 ? P.acc_cols : (uint32_t)BN;  // TMEM columns per stage
-  // A/B knobs for measurements: IDEQ_NA2=1 starts at 2 accumulator stages, IDEQ_CTA3=1 lets
-  // resident-weight layers try 3 CTAs per SM
+  // A/B knobs for measurements: IDEQ_NA2=1 starts at 2 accumulator stages (22% slower),
+  // IDEQ_CTA3=1 lets resident-weight layers try 3 CTAs per SM (registers admit 2),
+  // IDEQ_NA6=1 gives the 64-column halo layers 6 stages (1.4% slower)
   static const bool na2 = [] { const char* e = getenv("IDEQ_NA2"); return e && atoi(e) != 0; }();
   static const bool cta3 = [] { const char* e = getenv("IDEQ_CTA3"); return e && atoi(e) != 0; }();
-  static const bool na8 = [] { const char* e = getenv("IDEQ_NA8"); return e && atoi(e) != 0; }();
+  // 8 accumulator stages for the N <= 32 halo layers (level 0): +0.3..1.6% in 3 interleaved A/B
+  // runs (more tiles in flight behind the epilogue); IDEQ_NA8=0 restores 4
+  static const bool na8 = [] { const char* e = getenv("IDEQ_NA8"); return !(e && atoi(e) == 0); }();
   static const bool na6 = [] { const char* e = getenv("IDEQ_NA6"); return e && atoi(e) != 0; }();
   const int na0 = na2 ? 2 : (na8 && 8 * acc_w <= 256 && p->halo) ? 8
                 : (na6 && acc_w == 64 && p->halo) ? 6 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
