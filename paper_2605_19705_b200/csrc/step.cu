@@ -390,6 +390,9 @@ __global__ void __launch_bounds__(128) blur_adjoint2_kernel(StepArgs a, const fl
 }
 
 static bool blur2_ks(int ks) { return ks == 9 || ks == 15 || ks == 25; }
+// the register-blocked kernel needs whole 64 x 64 tiles to pay off; smaller planes (C1's 32 x 32)
+// keep the 32 x 32-tile kernel (a 64-tile block would leave 3/4 of its threads' outputs idle)
+static bool use_blur2(int ks, int H, int W) { return blur2_ks(ks) && H >= BT2 && W >= BT2; }
 
 // ------------------------------------------------------------------ finalize / stop logic
 // One warp per image: fixed-order fp64 combine of the partials, r = sqrt(d2)/sqrt(n2),
@@ -629,7 +632,7 @@ void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
 static size_t blur_smem(int ks) { return sizeof(float) * (ks * ks + (BT + ks - 1) * (BT + ks - 1)); }
 
 int blur_parts_per_image(int C, int H, int W, int ks) {
-  const int bt = blur2_ks(ks) ? BT2 : BT;
+  const int bt = use_blur2(ks, H, W) ? BT2 : BT;
   return C * ((H + bt - 1) / bt) * ((W + bt - 1) / bt);
 }
 
@@ -642,6 +645,7 @@ static void launch_blur2(int which, const StepArgs& a, const float* src, cudaStr
   else launch_k(blur_adjoint2_kernel<KS, 1>, grid, 128, sm, s, a, src);
 }
 static bool launch_blur2_any(int which, const StepArgs& a, const float* src, cudaStream_t s) {
+  if (!use_blur2(a.ksize, a.H, a.W)) return false;
   switch (a.ksize) {
     case 9: launch_blur2<9>(which, a, src, s); return true;
     case 15: launch_blur2<15>(which, a, src, s); return true;
