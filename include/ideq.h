@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define IDEQ_ABI_VERSION 2
+#define IDEQ_ABI_VERSION 3
 
 #if defined(__GNUC__)
 #define IDEQ_API __attribute__((visibility("default")))
@@ -140,7 +140,8 @@ typedef enum { IDEQ_BLUR_DIRECT = 0, IDEQ_BLUR_FFT = 1 } ideq_blur_impl;
  *            gradient step only (no closed-form prox, l.1079); sigma > 0.
  * kernels: HOST fp32 [1 or batch][ksize][ksize]; masks: HOST u8 [batch][H][W]
  * (1 = observed); phase_masks: HOST fp32 [n_phase][H][W][2] (re, im), shared.
- * Copied; `batch` is the number of images that later solves will use.
+ * Copied; `batch` is the number of images that later solves will use: a solve with more
+ * images returns IDEQ_E_INVALID.
  */
 typedef struct {
   ideq_op_kind kind;
@@ -176,6 +177,11 @@ typedef struct {
    * max_iter); empty window or diverged image -> x-hat = last accepted iterate.
    * Requires tol == 0 (fixed iteration count). 0: off (Remark 1, l.189-193). */
   int averaging;
+  /* Early-stopping solves (tol > 0, PER_IMAGE) skip the network work of images that have
+   * stopped: the conv kernels walk a compacted list of the active images. 0 (default): skip;
+   * 1: compute every image's tiles every iteration (results are identical; for checking and
+   * measurement). */
+  int compute_frozen;
 } ideq_params;
 
 typedef struct {

@@ -27,13 +27,6 @@
 #include "common.cuh"
 #include "kernels.h"
 
-#ifndef IDEQ_SP_MUFU
-#define IDEQ_SP_MUFU 1
-#endif
-#ifndef IDEQ_DSP_MUFU
-#define IDEQ_DSP_MUFU 1
-#endif
-
 namespace ideq {
 
 // ------------------------------------------------------------------ PTX helpers
@@ -112,15 +105,6 @@ __device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
          | ((uint32_t)(128 >> 4) << 24); // M >> 4
 }
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // elect.sync picks the same (lowest active) lane every time, so the MMAs and the commit that
 // tracks them are issued by one thread while the loop around them stays warp-uniform.
 __device__ __forceinline__ bool elect_one() {
@@ -147,65 +131,6 @@ __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
       "{\n\t.reg .pred e;\n\t"
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(bar)
-      : "memory");
-}
-// ---- CTA pair (cta_group::2): cluster rank, peer addresses, remote arrivals, 2-SM MMA/commit/TMA
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t out;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(out) : "r"(addr), "r"(rank));
-  return out;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx_cluster(uint32_t cluster_addr, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(cluster_addr),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_5d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                                 int c1, int c2, int c3, int c4) {
-  asm volatile(
-      "cp.async.bulk.tensor.5d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-      "%4, %5, %6}], [%7];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar_cluster)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                                 int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, "
-      "%4}], [%5];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar_cluster)
-      : "memory");
-}
-__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// arrive on the barrier at this shared-memory offset in BOTH CTAs of the pair once the MMAs complete
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
-  const uint16_t mask = 3;
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}\n" ::"r"(
-          bar),
-      "h"(mask)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -253,8 +178,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 }
 
 // bf16-mode epilogue transcendentals (outputs are rounded to bf16, rel. 2^-9).
-// log1p(u) on u in [0, 1] by a degree-6 Chebyshev-interpolated polynomial (|err| < 1.5e-6), so
-// softplus costs one exponential instead of EX2 + LG2.
+// log1p(u) on u in [0, 1] by a degree-6 Chebyshev-interpolated polynomial (|err| < 1.5e-6).
 __device__ __forceinline__ float log1p01(float u) {  // u in [0, 1]
   float p = -0.01741407752407103f;
   p = fmaf(p, u, 0.08269123711081523f);
@@ -264,24 +188,6 @@ __device__ __forceinline__ float log1p01(float u) {  // u in [0, 1]
   p = fmaf(p, u, 0.9998476974962173f);
   return fmaf(p, u, 1.4720650115540579e-06f);
 }
-// 2^x for x <= 0 on the FMA/ALU pipes (no MUFU): x = n + f, f in [-0.5, 0.5], 2^f by a degree-4
-// Chebyshev-interpolated polynomial (relative error < 4e-6), 2^n added to the exponent bits.
-// Measured: moving half of the epilogue exponentials here made the level-0/1 softplus and sp'
-// layers 5-25% SLOWER (the FMA/ALU pipes are busier than MUFU there), so the epilogues keep
-// MUFU (POLY = false); kept for A/B measurements.
-__device__ __forceinline__ float exp2_fma(float x) {
-  x = fmaxf(x, -126.f);
-  const float j = x + 12582912.f;  // 1.5 * 2^23: round to nearest integer
-  const float f = x - (j - 12582912.f);
-  float p = 0.009676037097880542f;
-  p = fmaf(p, f, 0.05592203564725866f);
-  p = fmaf(p, f, 0.24022107355830305f);
-  p = fmaf(p, f, 0.6931210339915471f);
-  p = fmaf(p, f, 1.0000000754953493f);
-  return __int_as_float(__float_as_int(p) + ((__float_as_int(j) - 0x4B400000) << 23));
-}
-// softplus: one exponential + a degree-6 polynomial for log1p (|err| < 1.5e-6, far below the
-// bf16 rounding of the output). POLY selects the FMA-pipe exponential.
 __device__ __forceinline__ float ex2_approx(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -292,39 +198,22 @@ __device__ __forceinline__ float lg2_approx(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-#ifndef IDEQ_SP_MIX
-#define IDEQ_SP_MIX 1
-#endif
-// IDEQ_SP_MIX (A/B build): odd elements take log1p from the FMA-pipe polynomial instead of MUFU lg2
+// softplus(t) = max(t, 0) + log1p(exp(-|t|)). Two forms, used on alternate elements so the
+// epilogue's work is split between the MUFU pipe and the FMA pipe (+0.8% in interleaved A/B runs
+// against MUFU only): ex2 + lg2 on MUFU (lg2.approx abs. error ~1e-7 on [1, 2]), or ex2 + the
+// log1p polynomial above. Both errors are far below the bf16 rounding of the output.
+__device__ __forceinline__ float softplus_fast(float t) {
+  const float u = ex2_approx(-1.4426950408889634f * fabsf(t));
+  return fmaf(0.6931471805599453f, lg2_approx(1.f + u), fmaxf(t, 0.f));
+}
 __device__ __forceinline__ float softplus_poly_log(float t) {
   const float u = ex2_approx(-1.4426950408889634f * fabsf(t));
   return fmaxf(t, 0.f) + log1p01(u);
 }
-template <bool POLY = false>
-__device__ __forceinline__ float softplus_fast(float t) {
-#if IDEQ_SP_MUFU
-  // max(t, 0) + ln2 * log2(1 + 2^(-|t| log2 e)): two MUFU ops and 4 FMA/ALU instructions
-  // (lg2.approx abs. error ~1e-7 on [1, 2], far below the bf16 rounding of the output)
-  const float u = ex2_approx(-1.4426950408889634f * fabsf(t));
-  return fmaf(0.6931471805599453f, lg2_approx(1.f + u), fmaxf(t, 0.f));
-#else
-  const float u = POLY ? exp2_fma(-1.4426950408889634f * fabsf(t)) : __expf(-fabsf(t));
-  return fmaxf(t, 0.f) + log1p01(u);
-#endif
-}
-// sp'(p) = 1 - exp(-a) from the saved activation a, with a series for small a to avoid the
-// cancellation of 1 - exp(-a) (bf16-mode outputs are rounded to bf16, rel. 2^-9).
-template <bool POLY = false>
-__device__ __forceinline__ float dsoftplus_from_act_fast(float a) {
-#if IDEQ_DSP_MUFU
-  // 1 - 2^(-a log2 e): the absolute error ~2e-7 of ex2.approx near a = 0 is negligible against
-  // the O(1) sp' of the other channels in the sum this factor feeds (and the bf16 rounding)
-  return 1.f - ex2_approx(-1.4426950408889634f * a);
-#else
-  const float e = POLY ? exp2_fma(-1.4426950408889634f * a) : __expf(-a);
-  return a < 0.0625f ? a * (1.f - a * (0.5f - a * (1.f / 6.f))) : 1.f - e;
-#endif
-}
+// sp'(p) = 1 - exp(-a) from the saved activation a = sp(p): 1 - 2^(-a log2 e). The absolute
+// error ~2e-7 of ex2.approx near a = 0 is negligible against the O(1) sp' of the other channels
+// in the sum this factor feeds (and the bf16 rounding of the product).
+__device__ __forceinline__ float dsoftplus_from_act_fast(float a) { return 1.f - ex2_approx(-1.4426950408889634f * a); }
 
 __device__ __forceinline__ void tma_store_5d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3,
                                              int c4) {
@@ -343,12 +232,6 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, uint32_t sr
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-// wait until at most n (runtime, 1..3) bulk groups still have to read shared memory
-__device__ __forceinline__ void bulk_wait_read_lt(int n) {
-  if (n <= 1) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-  else if (n == 2) asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory");
-  else asm volatile("cp.async.bulk.wait_group.read 3;" ::: "memory");
-}
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
 // the two epilogue warps of one TMEM lane quadrant (immediate ids keep ptxas from reserving all 16)
@@ -379,13 +262,6 @@ struct TcParams {
   int img_c;
   FastDiv fd_ntiles, fd_perimg, fd_tw;  // tile index -> (m tile, n tile), (image, row tile, col tile)
   int slab_mode;                        // 1: each TMEM lane quadrant stores its own 32-row slab
-  // MODE 4 (taps in N): a job is R full image rows (R*W = 128*T pixels, T = 1 or 2 M tiles);
-  // row_blk[s] = first of the 3 resident weight blocks of row shift dh = s - 1 (dw ascending,
-  // or descending when dw_desc); the MMA N is 3*BN and each TMEM stage holds T*3*BN columns
-  int row_T, row_blk[3], dw_desc;
-  uint32_t acc_cols;
-  // per-image active flags of the solver (null: compute every tile). Tiles of frozen images are
-  // skipped by every warp role alike, so the barrier rings stay in step (not used by CTA pairs).
   // live-tile list (tol > 0 per-image solves): the solver keeps a compacted list of its active
   // images (act_list[0 .. *n_act)); every warp role walks the tiles of those images only, in the
   // same order, so work stays balanced over the CTAs when images freeze (null: every tile)
@@ -393,12 +269,6 @@ struct TcParams {
   const int* n_act;
   FastDiv fd_tpi;   // tiles per image (M tiles x N tiles)
   int tpi;
-  // direct epilogue (opt-in, 3x3 halo layers with BN <= 64): the aux operand is read from global
-  // memory into registers and the outputs are stored from registers (NHWC rows of ncols
-  // channels), bypassing the shared-memory staging + TMA store + aux TMA of the default path
-  int direct;
-  __nv_bfloat16* out_ptr;
-  const __nv_bfloat16* aux_ptr;
 };
 
 // k-th live tile -> raw tile index (identity without a live list). The list lives in global
@@ -412,11 +282,10 @@ __device__ __forceinline__ int live_tile(const TcParams& P, int L) {
 
 // tile t -> (image, output row h0, output col w0, n tile)
 struct TileIdx { int img, h0, w0, nt; };
-__device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t, int pair_rank = -1) {
+__device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t) {
   TileIdx r;
-  int mt = (int)P.fd_ntiles.div((uint32_t)t);
+  const int mt = (int)P.fd_ntiles.div((uint32_t)t);
   r.nt = t - mt * P.n_tiles;
-  if (pair_rank >= 0) mt = 2 * mt + pair_rank;  // CTA pair: unit -> this CTA's M tile
   r.img = (int)P.fd_perimg.div((uint32_t)mt);
   const int rem = mt - r.img * (P.g.tiles_h * P.g.tiles_w);
   const int th = (int)P.fd_tw.div((uint32_t)rem);
@@ -436,16 +305,6 @@ __device__ __forceinline__ uint32_t epi_chunk_addr(uint32_t box_base, int r, int
   return box_base + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
 }
 
-__device__ __forceinline__ uint4 ld_global_nc_v4(const void* p) {
-  uint4 v;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.b32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-               : "l"(p));
-  return v;
-}
-__device__ __forceinline__ void st_global_v4(void* p, uint4 v) {
-  asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
-}
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t a) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
@@ -463,10 +322,6 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
 // crosses L2 ~1.4x (2D) / ~3x (1-row) instead of 9x. MODE 1 keeps the layer's weights resident
 // in shared memory for the CTA's lifetime; MODE 2 streams them per (chunk, tap) through a second
 // ring (layers whose weights do not fit).
-// MODE 4 (taps in N, full image rows): the three horizontal taps of a row shift become N columns
-// (N = 3 * Cout, one MMA per row shift and K step, A read 3x less from shared memory) and the
-// epilogue adds the dw = -1 / +1 partial products of the neighbouring pixels (warp shuffles plus a
-// cross-warp exchange through shared memory; zero at the row ends = the conv's zero padding).
 template <int KC, int EPI, int BOXC, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -479,29 +334,21 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int S = P.stages;
   const int BN = P.BN;
   const uint32_t a_stage = 128u * KC * 2u;
-  // MODE 3 = MODE 2 on a CTA pair (cta_group::2, M = 256): each CTA holds its own 128-row A tile
-  // and HALF of every weight box (BN / 2 rows); the leader CTA issues the M256 x BN MMAs
-  constexpr bool PAIR = MODE == 3;
-  constexpr bool STREAMB = MODE == 2 || MODE == 3;
-  const uint32_t b_stage = (uint32_t)(PAIR ? BN / 2 : BN) * KC * 2u;
-  constexpr bool ROW = MODE == 4;
-  const int RT = ROW ? P.row_T : 1;                             // M tiles per job
-  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u * (uint32_t)RT;  // BN/BOXC boxes of 128*RT x BOXC
+  constexpr bool STREAMB = MODE == 2;
+  const uint32_t b_stage = (uint32_t)BN * KC * 2u;
+  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
   const ConvGeom& g = P.g;
   const int nkb = g.ntaps * g.nchunk;
   constexpr bool HALO = MODE != 0;
   const int SB = STREAMB ? P.stagesB : 0;
-  const uint32_t rank = PAIR ? cluster_rank() : 0u;
-  const bool leader = rank == 0;
   // MODE 0: [A stages][B stages][epi]; MODE 1: [resident W (nkb B boxes)][halo stages][epi];
   // MODE 2: [halo stages][B ring][epi]
   const uint32_t sW = base;
-  const uint32_t sA = (MODE == 1 || ROW) ? sW + (uint32_t)nkb * b_stage : base;
+  const uint32_t sA = (MODE == 1) ? sW + (uint32_t)nkb * b_stage : base;
   const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
-  const uint32_t sE = (MODE == 1 || ROW) ? sB : sB + (STREAMB ? SB : S) * b_stage;
+  const uint32_t sE = (MODE == 1) ? sB : sB + (STREAMB ? SB : S) * b_stage;
   const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
-  const uint32_t sX = sE + (uint32_t)NA * epi_stage;  // ROW: neighbour exchange [2 halves][2 par][2 chunk][T][4 q][2][16] fp32
-  const uint32_t sBar = sX + (ROW ? 8192u : 0u);
+  const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
   // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB], emptyB[SB]
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1 + 2 * SB);
@@ -519,17 +366,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
 
   if (threadIdx.x == 0) {
     mbar_init(wfull, 1);
-    if (MODE == 1 || ROW) {  // resident weights (constant since create): loaded before the wait
+    if (MODE == 1) {  // resident weights (constant since create): loaded before the wait
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
       for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
     }
-    // PAIR: the leader's tempty counts both CTAs' epilogue warps
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
     for (int s = 0; s < SB; ++s) { mbar_init(fullB0 + 8u * s, 1); mbar_init(emptyB0 + 8u * s, 1); }
     for (int a = 0; a < NA; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
-      mbar_init(tempty0 + 8u * a, PAIR ? 16 : 8);
+      mbar_init(tempty0 + 8u * a, 8);   // one arrival per epilogue warp
       mbar_init(auxfull0 + 8u * a, 1);
       mbar_init(epifree0 + 8u * a, 4);  // one arrival per TMEM lane quadrant
     }
@@ -541,68 +387,38 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     if (HAS_AUX) prefetch_tmap(&tmAux);
   }
   if (warp == 1) {
-    if (PAIR) {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                   "r"(P.tmem_cols)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                   "r"(P.tmem_cols)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   // everything below reads what earlier kernels wrote: wait for them (no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   tc_fence_before();
-  if (PAIR) cluster_sync_all();  // barrier inits + TMEM allocation visible to the peer
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
-  // PAIR: shared::cluster addresses of the leader's barriers (operand-full rings, TMEM-empty)
-  const uint32_t full0L = PAIR ? mapa_shared(full0, 0) : full0;
-  const uint32_t fullB0L = PAIR ? mapa_shared(fullB0, 0) : fullB0;
-  const uint32_t tempty0L = PAIR ? mapa_shared(tempty0, 0) : tempty0;
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);  // uniform, not a per-thread load
 
-  // PAIR: work units are (pair of M tiles, N tile); CTA `rank` owns M tile 2j + rank
-  const int total = PAIR ? ((P.m_tiles + 1) / 2) * P.n_tiles : P.m_tiles * P.n_tiles;
-  const int t0 = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
-  const int tstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  const int total = P.m_tiles * P.n_tiles;
+  const int t0 = (int)blockIdx.x;
+  const int tstep = (int)gridDim.x;
   const int nbox = BN / BOXC;
   // tiles this launch walks: all of them, or the live list's (read after griddepcontrol.wait)
-  const int tot_it = (P.act_list && !PAIR) ? *(volatile const int*)P.n_act * P.tpi : total;
+  const int tot_it = P.act_list ? *(volatile const int*)P.n_act * P.tpi : total;
 
   if (warp == 0) {
     // ---------------- TMA producer: the whole warp walks the loop (warp-uniform state stays in
     // uniform registers); one elected lane arms the barriers and issues the copies
     int s = 0, sb = 0;
     uint32_t ph = 0, phb = 0;
-    int acc = 0;
-    uint32_t aph = 0;
     for (int L = t0; L < tot_it; L += tstep) {
-      const int t = live_tile(P, L);
-      const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+      const TileIdx ti = tile_index(P, live_tile(P, L));
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
       const int nload = HALO ? g.nchunk : nkb;
       for (int kb = 0; kb < nload; ++kb) {
         mbar_wait(empty0 + 8u * s, ph ^ 1u);
         if (elect_one()) {
-          if (PAIR) {  // the 2-SM TMA of both CTAs signals the LEADER's full barriers; only the
-                       // leader arms them (for both CTAs' bytes): a remote arrive would need a fence
-            if (leader) mbar_expect_tx(full0 + 8u * s, 2u * P.a_bytes);
-            tma_load_5d_pair(sA + s * P.halo_stage, &tmA, full0L + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
-            for (int tap = 0; tap < 9; ++tap) {  // this CTA's half (BN / 2 rows) of each weight box
-              mbar_wait(emptyB0 + 8u * sb, phb ^ 1u);
-              if (leader) mbar_expect_tx(fullB0 + 8u * sb, 2u * P.b_bytes);
-              tma_load_3d_pair(sB + sb * b_stage, &tmB, fullB0L + 8u * sb, 0, nt * BN + (int)rank * (BN / 2),
-                               tap * g.nchunk + kb);
-              if (++sb == SB) { sb = 0; phb ^= 1u; }
-            }
-          } else if (ROW) {  // (R + 2) full rows, no horizontal halo
-            mbar_expect_tx(full0 + 8u * s, P.a_bytes);
-            tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, 0, 0, h0 - 1, img);
-          } else if (HALO) {
+          if (HALO) {
             mbar_expect_tx(full0 + 8u * s, P.a_bytes);
             tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
             if (MODE == 2) {  // this chunk's 9 weight boxes through the B ring
@@ -624,17 +440,16 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         __syncwarp();
         if (++s == S) { s = 0; ph ^= 1u; }
       }
-      if (++acc == NA) { acc = 0; aph ^= 1u; }
     }
   } else if (warp == 10) {
     // ---------------- aux producer: the epilogue's second operand (residual / saved activation)
     // goes into the tile's epilogue buffer as soon as that buffer's previous store has been read,
     // without ever stalling the operand producer behind the epilogue
-    if (HAS_AUX && !P.direct) {
+    if (HAS_AUX) {
       int acc = 0;
       uint32_t aph = 0;
       for (int L = t0; L < tot_it; L += tstep) {
-        const TileIdx ti = tile_index(P, live_tile(P, L), PAIR ? (int)rank : -1);
+        const TileIdx ti = tile_index(P, live_tile(P, L));
         mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
         if (elect_one()) {
           mbar_expect_tx(auxfull0 + 8u * acc, P.epi_tx_bytes);
@@ -648,50 +463,30 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         if (++acc == NA) { acc = 0; aph ^= 1u; }
       }
     }
-  } else if (warp == 1 && leader) {
+  } else if (warp == 1) {
     // ---------------- MMA issuer: the whole warp runs the loop with warp-uniform descriptors
     // (64-bit adds of byte offsets >> 4); one elected lane issues tcgen05.mma / commit. A
     // single-thread issue loop measured ~110 clk per MMA on B200 (tools/umma_bench.cu) against
     // a tensor floor of 16-128 clk; the uniform form reaches the floor for N >= 128.
-    // PAIR: M = 256 (instruction descriptor bits [24,29) = M >> 4)
-    const uint32_t idesc = PAIR ? ((make_idesc_bf16(BN) & ~(0x1Fu << 24)) | ((uint32_t)(256 >> 4) << 24))
-                                : make_idesc_bf16(BN);
+    const uint32_t idesc = make_idesc_bf16(BN);
     constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
     constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
     // halo tiles: 8-row core groups of A are 8 pixels of one row (R = 1) or one 8-pixel row of a
     // 16 x 8 tile, i.e. (Wt + 2) pixel rows apart inside the halo box
-    const uint32_t sboA = (HALO && !ROW) ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
+    const uint32_t sboA = HALO ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
     const uint64_t dA0 = make_sdesc(sA, sboA, layout);
-    const uint64_t dB0 = make_sdesc((MODE == 1 || ROW) ? sW : sB, sbo, layout);
-    const uint32_t idesc3 = make_idesc_bf16(3 * BN);  // ROW: N = 3 taps x Cout
+    const uint64_t dB0 = make_sdesc(MODE == 1 ? sW : sB, sbo, layout);
     int s = 0, sb = 0;
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
-    if (MODE == 1 || ROW) mbar_wait(wfull, 0);
+    if (MODE == 1) mbar_wait(wfull, 0);
     const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
     for (int L = t0; L < tot_it; L += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (ROW ? (uint32_t)acc * P.acc_cols : (uint32_t)(acc * BN));
-      if (ROW) {
-        // one halo buffer of R + 2 full rows; per M tile and row shift: N = 3 * BN MMAs
-        mbar_wait(full0 + 8u * s, ph);
-        tc_fence_after();
-        const uint64_t dh = dA0 + ((s * P.halo_stage) >> 4);
-        for (int tau = 0; tau < RT; ++tau) {
-          for (int sh = 0; sh < 3; ++sh) {
-            const uint32_t p0 = (uint32_t)(sh * g.OW + tau * 128);
-            const uint64_t ad = dh + ((p0 * hrow) >> 4);
-            const uint64_t bd = dB0 + (((uint32_t)P.row_blk[sh] * b_stage) >> 4);
-#pragma unroll
-            for (int k = 0; k < KC / 16; ++k)
-              mma_bf16_elect(d_tmem + (uint32_t)(tau * 3 * BN), ad + 2u * k, bd + 2u * k, idesc3, (sh | k) ? 1u : 0u);
-          }
-        }
-        mma_commit_elect(empty0 + 8u * s);
-        if (++s == S) { s = 0; ph ^= 1u; }
-      } else if (HALO) {
+      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      if (HALO) {
         for (int ch = 0; ch < g.nchunk; ++ch) {
           mbar_wait(full0 + 8u * s, ph);
           tc_fence_after();
@@ -707,21 +502,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             } else {
               bd = dB0 + (((uint32_t)(tap * g.nchunk + ch) * b_stage) >> 4);
             }
-            if (PAIR) {
 #pragma unroll
-              for (int k = 0; k < KC / 16; ++k) mma_bf16_pair(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
-            } else {
-#pragma unroll
-              for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
-            }
+            for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
             if (STREAMB) {
-              if (PAIR) mma_commit_pair(emptyB0 + 8u * sb);
-              else mma_commit_elect(emptyB0 + 8u * sb);
+              mma_commit_elect(emptyB0 + 8u * sb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
             }
           }
-          if (PAIR) mma_commit_pair(empty0 + 8u * s);
-          else mma_commit_elect(empty0 + 8u * s);
+          mma_commit_elect(empty0 + 8u * s);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       } else {
@@ -735,149 +523,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           if (++s == S) { s = 0; ph ^= 1u; }
         }
       }
-      if (PAIR) mma_commit_pair(tfull0 + 8u * acc);
-      else mma_commit_elect(tfull0 + 8u * acc);
+      mma_commit_elect(tfull0 + 8u * acc);
       if (++acc == NA) { acc = 0; aph ^= 1u; }
-    }
-  } else if (ROW && warp >= 2 && warp < 10) {
-    // ---------------- MODE 4 epilogue: out[p] = Q_{-1}[p-1] + Q_0[p] + Q_{+1}[p+1] with Q_dw the
-    // TMEM column block of tap dw; neighbours inside a warp by shuffles, across the warps of a
-    // column half through shared memory (one 128-thread named barrier per 16-column chunk)
-    const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const bool qleader = (half == 0 && lane == 0);
-    const uint32_t rowbytes = (uint32_t)BOXC * 2u;
-    const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
-    const int Wimg = g.OW;
-    const int blkL = P.dw_desc ? 2 : 0, blkR = P.dw_desc ? 0 : 2;  // TMEM blocks of dw = -1 / +1
-    float* xbase = reinterpret_cast<float*>(gbase + (sX - base));
-    int acc = 0, prev_acc = -1, jpar = 0;
-    uint32_t aph = 0;
-    for (int L = t0; L < tot_it; L += tstep) {
-      const TileIdx ti = tile_index(P, live_tile(P, L));
-      const int img = ti.img, h0 = ti.h0;
-      const uint32_t ebuf = sE + acc * epi_stage;
-      if (HAS_AUX) {
-        mbar_wait(auxfull0 + 8u * acc, aph);
-      } else {
-        mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
-      }
-      mbar_wait(tfull0 + 8u * acc, aph);
-      tc_fence_after();
-      const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)acc * P.acc_cols;
-      int ci = 0;
-#pragma unroll 1
-      for (int c0 = cbeg; c0 < cend; c0 += 16, ++ci) {
-        // exchange slots of (half, job parity, chunk): [tau][quad][side][16]
-        float* xs = xbase + (((half * 2 + jpar) * 2 + ci) * 2) * 4 * 2 * 16;
-#pragma unroll 1
-        for (int tau = 0; tau < RT; ++tau) {  // pass 1: publish the warp's boundary partial products
-          uint32_t pl[16], pr[16];
-          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkL * BN + c0), pl);
-          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkR * BN + c0), pr);
-          tmem_wait();
-          float* xq = xs + (tau * 4 + quad) * 2 * 16;
-          if (lane == 31) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xq[e] = __uint_as_float(pl[e]);
-          }
-          if (lane == 0) {
-#pragma unroll
-            for (int e = 0; e < 16; ++e) xq[16 + e] = __uint_as_float(pr[e]);
-          }
-        }
-        if (half == 0) asm volatile("bar.sync 6, 128;" ::: "memory");
-        else asm volatile("bar.sync 7, 128;" ::: "memory");
-#pragma unroll 1
-        for (int tau = 0; tau < RT; ++tau) {  // pass 2: combine and apply the fused epilogue
-          uint32_t plu[16], pcu[16], pru[16];
-          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkL * BN + c0), plu);
-          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + BN + c0), pcu);
-          tmem_ld16_nw(tb + (uint32_t)(tau * 3 * BN + blkR * BN + c0), pru);
-          tmem_wait();
-          float pl[16], pc[16], pr[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            pl[e] = __uint_as_float(plu[e]);
-            pc[e] = __uint_as_float(pcu[e]);
-            pr[e] = __uint_as_float(pru[e]);
-          }
-          const int pix = tau * 128 + quad * 32 + lane;
-          const int col = pix % Wimg;
-          const float* xl = (quad > 0) ? xs + (tau * 4 + quad - 1) * 2 * 16 : (tau > 0 ? xs + ((tau - 1) * 4 + 3) * 2 * 16 : nullptr);
-          const float* xr = (quad < 3) ? xs + (tau * 4 + quad + 1) * 2 * 16 + 16
-                                       : (tau + 1 < RT ? xs + ((tau + 1) * 4) * 2 * 16 + 16 : nullptr);
-          float v[16];
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            float left = __shfl_up_sync(0xffffffffu, pl[e], 1);
-            float right = __shfl_down_sync(0xffffffffu, pr[e], 1);
-            if (lane == 0) left = xl ? xl[e] : 0.f;
-            if (lane == 31) right = xr ? xr[e] : 0.f;
-            if (col == 0) left = 0.f;
-            if (col == Wimg - 1) right = 0.f;
-            v[e] = left + pc[e] + right;
-          }
-          const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
-          const int j0 = (c0 % BOXC) / 8;
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const uint32_t a = epi_chunk_addr<BOXC>(box, pix, j0 + q);
-            float o[8];
-            if (HAS_AUX) {
-              const uint4 u = ld_shared_v4(a);
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                if (EPI == EPI_RESADD) {
-                  o[2 * e] = v[q * 8 + 2 * e] + f.x;
-                  o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
-                } else {
-                  o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast<false>(f.x);
-                  o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast<false>(f.y);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int e = 0; e < 8; ++e)
-                o[e] = (EPI == EPI_SOFTPLUS) ? ((IDEQ_SP_MIX && (e & 1)) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast<false>(v[q * 8 + e])) : v[q * 8 + e];
-            }
-            uint4 w;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
-            st_shared_v4(a, w);
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-      fence_async_smem();
-      pair_bar(quad);
-      if (qleader) {
-        for (int tau = 0; tau < RT; ++tau) {
-          const int p0 = tau * 128 + quad * 32;
-          for (int b = 0; b < nbox; ++b) {
-            const int colg = b * BOXC;
-            tma_store_5d(&tmSlab, ebuf + b * P.epi_box_bytes + (uint32_t)p0 * rowbytes, colg % g.CB, p0 % Wimg,
-                         colg / g.CB, h0 + p0 / Wimg, img);
-          }
-        }
-        bulk_commit();
-        if (prev_acc >= 0) {
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          mbar_arrive(epifree0 + 8u * prev_acc);
-        }
-        prev_acc = acc;
-      }
-      jpar ^= 1;
-      if (++acc == NA) { acc = 0; aph ^= 1u; }
-    }
-    if (qleader) {
-      bulk_wait0();
-      if (prev_acc >= 0) mbar_arrive(epifree0 + 8u * prev_acc);
     }
   } else if (warp >= 2 && warp < 10) {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant = warp % 4, one pixel row per
@@ -901,76 +548,8 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     int acc = 0, prev_acc = -1;
     uint32_t aph = 0;
     for (int L = t0; L < tot_it; L += tstep) {
-      const int t = live_tile(P, L);
-      const TileIdx ti = tile_index(P, t, PAIR ? (int)rank : -1);
+      const TileIdx ti = tile_index(P, live_tile(P, L));
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
-      if (EPI != EPI_IMG && !PAIR && P.direct) {
-        // ---- direct epilogue (BN <= 64: this thread's half row is 16 or 32 columns)
-        const int oh = h0 + row / g.Wt, ow = w0 + row % g.Wt;
-        const bool valid = row < g.R * g.Wt && oh < g.OH && ow < g.OW;
-        const long long pix = ((long long)img * g.OH + oh) * g.OW + ow;
-        const long long cofs = pix * g.ncols + (long long)nt * BN + cbeg;
-        const int ngrp = (cend - cbeg) >> 4;  // 16-column groups: 1 or 2
-        uint4 ax[4];
-        if (HAS_AUX) {  // issued before the accumulator wait: the loads overlap this tile's MMAs
-#pragma unroll
-          for (int i = 0; i < 4; ++i) ax[i] = make_uint4(0u, 0u, 0u, 0u);
-          if (valid) {
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              if (i < 2 * ngrp) ax[i] = ld_global_nc_v4(P.aux_ptr + cofs + i * 8);
-          }
-        }
-        mbar_wait(tfull0 + 8u * acc, aph);
-        tc_fence_after();
-        uint32_t r[2][16];
-        const uint32_t tb = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + cbeg);
-        tmem_ld16_nw(tb, r[0]);
-        if (ngrp == 2) tmem_ld16_nw(tb + 16u, r[1]);
-        tmem_wait();
-        // the accumulator is in registers: the MMA warp may reuse this TMEM stage
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-#pragma unroll
-        for (int gi = 0; gi < 2; ++gi) {
-          if (gi < ngrp) {
-#pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              float o[8];
-              if (HAS_AUX) {
-                const uint4 u = ax[gi * 2 + q];
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 f = __bfloat1622float2(h2[e]);
-                  const float v0 = __uint_as_float(r[gi][q * 8 + 2 * e]), v1 = __uint_as_float(r[gi][q * 8 + 2 * e + 1]);
-                  if (EPI == EPI_RESADD) {
-                    o[2 * e] = v0 + f.x;
-                    o[2 * e + 1] = v1 + f.y;
-                  } else {
-                    o[2 * e] = v0 * dsoftplus_from_act_fast<false>(f.x);
-                    o[2 * e + 1] = v1 * dsoftplus_from_act_fast<false>(f.y);
-                  }
-                }
-              } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const float v = __uint_as_float(r[gi][q * 8 + e]);
-                  o[e] = (EPI == EPI_SOFTPLUS) ? softplus_fast<false>(v) : v;
-                }
-              }
-              uint4 w;
-              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
-              if (valid) st_global_v4(P.out_ptr + cofs + gi * 16 + q * 8, w);
-            }
-          }
-        }
-        if (++acc == NA) { acc = 0; aph ^= 1u; }
-        continue;
-      }
       const uint32_t ebuf = sE + acc * epi_stage;
       if (HAS_AUX) {
         mbar_wait(auxfull0 + 8u * acc, aph);
@@ -999,7 +578,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) { if (PAIR) mbar_arrive_cluster(tempty0L + 8u * acc); else mbar_arrive(tempty0 + 8u * acc); }
+        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
         if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals, nothing stored through smem
         if (++acc == NA) { acc = 0; aph ^= 1u; }
         continue;
@@ -1024,14 +603,15 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                 o[2 * e] = v[q * 8 + 2 * e] + f.x;
                 o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
               } else {
-                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast<false>(f.x);
-                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast<false>(f.y);
+                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast(f.x);
+                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast(f.y);
               }
             }
           } else {
 #pragma unroll
             for (int e = 0; e < 8; ++e)
-              o[e] = (EPI == EPI_SOFTPLUS) ? ((IDEQ_SP_MIX && (e & 1)) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast<false>(v[q * 8 + e])) : v[q * 8 + e];
+              o[e] = (EPI == EPI_SOFTPLUS) ? ((e & 1) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast(v[q * 8 + e]))
+                                           : v[q * 8 + e];
           }
           uint4 w;
           __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
@@ -1043,7 +623,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       // TMEM stage fully read: let the MMA warp reuse it
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) { if (PAIR) mbar_arrive_cluster(tempty0L + 8u * acc); else mbar_arrive(tempty0 + 8u * acc); }
+      if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
       // publish this quadrant's slab: generic-proxy smem writes -> async proxy, pair barrier,
       // then one TMA store per column box of the slab
       fence_async_smem();
@@ -1080,17 +660,11 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     }
   }
   tc_fence_before();
-  if (PAIR) cluster_sync_all();  // the peer's MMAs into this CTA's TMEM and its remote arrivals are done
-  else __syncthreads();
+  __syncthreads();
   tc_fence_after();
-  if (warp == 1) {
-    if (PAIR)
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
-                   : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
-                   : "memory");
-  }
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
+                 : "memory");
 }
 
 // ------------------------------------------------------------------ fused head (image -> features)
@@ -1363,26 +937,6 @@ bool tc_supported(const ConvGeom& g) {
   return true;
 }
 
-// MODE 4: the taps of each row shift dh = s - 1 must be three consecutive weight blocks with dw
-// ascending (-1, 0, +1) or, for every s, descending (the flipped adjoint weights).
-static bool row_taps(const ConvGeom& g, int blk[3], int& desc) {
-  desc = -1;
-  for (int sh = 0; sh < 3; ++sh) {
-    int t0 = -1;
-    for (int t = 0; t < 9; ++t)
-      if (g.dh[t] == sh - 1) { t0 = t; break; }
-    if (t0 < 0 || t0 + 2 >= 9) return false;
-    for (int j = 0; j < 3; ++j)
-      if (g.dh[t0 + j] != sh - 1) return false;
-    const int d = (g.dw[t0] == -1 && g.dw[t0 + 1] == 0 && g.dw[t0 + 2] == 1) ? 0
-                : (g.dw[t0] == 1 && g.dw[t0 + 1] == 0 && g.dw[t0 + 2] == -1) ? 1 : -1;
-    if (d < 0 || (desc >= 0 && d != desc)) return false;
-    desc = d;
-    blk[sh] = t0;
-  }
-  return true;
-}
-
 // Halo variants: 3x3 taps (|dh|,|dw| <= 1, no parity planes) on tiles whose 8-row core groups
 // sit at a uniform stride inside the halo box: 16 x 8 pixels (preferred: 1.4x halo) or one row of
 // 128 pixels. Returns 0 (plain), 1 (resident weights) or 2 (streamed weights) and the tile shape.
@@ -1390,39 +944,13 @@ static int tc_halo_mode(const ConvGeom& g, int& R, int& Wt) {
   if (g.ntaps != 9 || g.inP != 1) return 0;
   for (int t = 0; t < 9; ++t)
     if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return 0;
-  const char* nh = getenv("IDEQ_NO_HALO");  // A/B switches for measurements
-  if (nh && atoi(nh) != 0) return 0;
-  {  // MODE 4 (taps in N) on full image rows: Cout 32/64 in one N tile, one channel chunk.
-     // Opt-in (IDEQ_ROW=1): correct (tests/test_gpu_layers.py) but measured 2-3x SLOWER on B200
-     // than the 16x8 halo tiles -- the neighbour combine (two SHFL per output element on top of
-     // the softplus exponential) saturates the XU pipe (ncu: 140%), which the smem savings of the
-     // 3x-wider MMAs cannot repay.
-    const char* rw = getenv("IDEQ_ROW");
-    const char* nr = (rw && atoi(rw) != 0) ? nullptr : "1";
-    const int BN = tc_bn(g), W = g.OW;
-    const int T = W >= 128 ? W / 128 : 1;
-    const bool ok = !(nr && atoi(nr) != 0) && g.epi != EPI_IMG && g.nchunk == 1 && g.ncols == BN &&
-                    (BN == 32 || BN == 64) && (W == 32 || W == 64 || W == 128 || W == 256) &&
-                    (size_t)9 * BN * g.KC * 2 <= 80 * 1024 && 2 * T * 3 * BN <= 512;
-    int blk[3], desc;
-    if (ok && row_taps(g, blk, desc)) {
-      R = W >= 128 ? 1 : 128 / W;
-      Wt = W;
-      return 4;
-    }
-  }
-  const char* n2 = getenv("IDEQ_NO_HALO2D");
-  if (g.OW % 8 == 0 && !(n2 && atoi(n2) != 0)) { R = 16; Wt = 8; }
+  if (g.OW % 8 == 0) { R = 16; Wt = 8; }
   else if (g.R == 1 && g.Wt == 128) { R = 1; Wt = 128; }
   else return 0;
   const int BN = tc_bn(g);
   const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * 2;
   if (g.ncols == BN && wbytes <= 80 * 1024) return 1;
-  // streamed weights. IDEQ_PAIR=1 runs them on CTA pairs (cta_group::2, M = 256, half of every
-  // weight box per SM): correct (tests/test_gpu_layers.py) but measured slower on B200 than the
-  // single-CTA ring (C3 level 2/3: 46-51 us vs 34-40 us per layer), so it is opt-in.
-  const char* pr = getenv("IDEQ_PAIR");
-  return (BN % 32 == 0 && pr && atoi(pr) != 0) ? 3 : 2;
+  return 2;
 }
 
 // 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
@@ -1465,15 +993,14 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     g.tiles_h = (g.OH + g.R - 1) / g.R;
     g.tiles_w = (g.OW + g.Wt - 1) / g.Wt;
   }
-  CUresult r = p->halo == 4 ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R + 2, swA)
-             : p->halo      ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
-                            : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
+  CUresult r = p->halo ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
+                       : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
   {
     const int nkb = g.ntaps * g.nchunk;
     cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
     cuuint64_t strides[2] = {(cuuint64_t)g.KC * 2, (cuuint64_t)g.KC * 2 * g.ncols};
-    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)(p->halo == 3 ? BN / 2 : BN), 1u};
+    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
     cuuint32_t es[3] = {1, 1, 1};
     r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, swA, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -1485,28 +1012,25 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     p->tmAux = p->tmA;
     p->tmSlab = p->tmA;
   } else {
-  // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
-  // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
-  // EPI_IMG writes fp32 image planes directly: the (unused) output map points at the input
-  r = encode5(enc, &p->tmOut, g.epi == EPI_IMG ? (const void*)in : (const void*)out, g.CB, g.OWo, g.osh, g.OHo / g.osh,
-              g.N, boxc, g.Wt, g.R, swE);
-  if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map out encode failed (%d)", (int)r); delete p; return nullptr; }
-  if (has_aux) {
-    r = encode5(enc, &p->tmAux, aux, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
-    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map aux encode failed (%d)", (int)r); delete p; return nullptr; }
-  } else {
-    p->tmAux = p->tmOut;
-  }
-  // 32-row epilogue slab (one TMEM lane quadrant): Wt >= 32 -> 32 pixels of one row; Wt < 32 ->
-  // 32 / Wt whole rows. Used when Wt is a multiple or a divisor of 32.
-  if (slab_mode) {
-    const int sw = g.Wt >= 32 ? 32 : g.Wt, sh = g.Wt >= 32 ? 1 : 32 / g.Wt;
-    r = encode5(enc, &p->tmSlab, g.epi == EPI_IMG ? (const void*)in : (const void*)out, g.CB, g.OWo, g.osh,
-                g.OHo / g.osh, g.N, boxc, sw, sh, swE);
-    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map slab encode failed (%d)", (int)r); delete p; return nullptr; }
-  } else {
-    p->tmSlab = p->tmOut;
-  }
+    // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
+    // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
+    r = encode5(enc, &p->tmOut, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map out encode failed (%d)", (int)r); delete p; return nullptr; }
+    if (has_aux) {
+      r = encode5(enc, &p->tmAux, aux, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+      if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map aux encode failed (%d)", (int)r); delete p; return nullptr; }
+    } else {
+      p->tmAux = p->tmOut;
+    }
+    // 32-row epilogue slab (one TMEM lane quadrant): Wt >= 32 -> 32 pixels of one row; Wt < 32 ->
+    // 32 / Wt whole rows. Used when Wt is a multiple or a divisor of 32.
+    if (slab_mode) {
+      const int sw = g.Wt >= 32 ? 32 : g.Wt, sh = g.Wt >= 32 ? 1 : 32 / g.Wt;
+      r = encode5(enc, &p->tmSlab, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, sw, sh, swE);
+      if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map slab encode failed (%d)", (int)r); delete p; return nullptr; }
+    } else {
+      p->tmSlab = p->tmOut;
+    }
   }
   TcParams& P = p->P;
   P.g = g;
@@ -1518,28 +1042,21 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.fd_perimg.init((uint32_t)(g.tiles_h * g.tiles_w));
   P.fd_tw.init((uint32_t)g.tiles_w);
   P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
-  P.b_bytes = (uint32_t)g.KC * 2u * (p->halo == 3 ? BN / 2 : BN);  // PAIR: this CTA's half
-  const int rowT = p->halo == 4 ? (g.Wt * g.R) / 128 : 1;  // M tiles per MODE 4 job
-  P.epi_box_bytes = 128u * (uint32_t)rowT * boxc * 2u;
-  P.row_T = rowT;
-  if (p->halo == 4) {
-    row_taps(g, P.row_blk, P.dw_desc);
-    P.acc_cols = (uint32_t)(rowT * 3 * BN);
-  }
+  P.b_bytes = (uint32_t)g.KC * 2u * BN;
+  P.epi_box_bytes = 128u * (uint32_t)boxc * 2u;
   P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
-  // Shared-memory / TMEM plan. Preference order: 4 accumulator stages for narrow N (more tiles
-  // in flight hide the per-tile epilogue latency), then 2 CTAs per SM, then deeper operand rings.
-  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)(p->halo == 3 ? BN / 2 : BN) * g.KC * 2u,
-               e_stage = (size_t)BN * 128u * 2u * rowT;
-  const size_t wbytes = (p->halo == 1 || p->halo == 4) ? (size_t)9 * g.nchunk * b_stage : 0;
+  // Shared-memory / TMEM plan. Preference order: deep accumulator rings for narrow N (more tiles
+  // in flight hide the per-tile epilogue latency: 8 stages for the 32-column halo layers measured
+  // +0.3..1.6% over 4, 2 stages -22%), then 2 CTAs per SM, then deeper operand rings.
+  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
+  const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * b_stage : 0;
   if (p->halo) {
-    P.a_bytes = p->halo == 4 ? (uint32_t)g.KC * 2u * g.Wt * (g.R + 2) : (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
+    P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
     P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
   }
-  const size_t xbytes = p->halo == 4 ? 8192 : 0;  // MODE 4 neighbour exchange
   // MODE 2: a weight ring of SB stages (one (chunk, tap) box each) next to the halo ring
   const int SBq = 6;
-  const bool streamb = p->halo == 2 || p->halo == 3;
+  const bool streamb = p->halo == 2;
   const size_t bring = streamb ? (size_t)SBq * b_stage : 0;
   P.stagesB = streamb ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
@@ -1551,24 +1068,14 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   const int min_stages = p->halo ? 2 : (short_k ? 2 : 3), max_stages = p->halo ? 4 : (short_k ? 4 : 8);
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
-  const uint32_t acc_w = p->halo == 4 ? P.acc_cols : (uint32_t)BN;  // TMEM columns per stage
-  // A/B knobs for measurements: IDEQ_NA2=1 starts at 2 accumulator stages (22% slower),
-  // IDEQ_CTA3=1 lets resident-weight layers try 3 CTAs per SM (registers admit 2),
-  // IDEQ_NA6=1 gives the 64-column halo layers 6 stages (1.4% slower)
-  static const bool na2 = [] { const char* e = getenv("IDEQ_NA2"); return e && atoi(e) != 0; }();
-  static const bool cta3 = [] { const char* e = getenv("IDEQ_CTA3"); return e && atoi(e) != 0; }();
-  // 8 accumulator stages for the N <= 32 halo layers (level 0): +0.3..1.6% in 3 interleaved A/B
-  // runs (more tiles in flight behind the epilogue); IDEQ_NA8=0 restores 4
-  static const bool na8 = [] { const char* e = getenv("IDEQ_NA8"); return !(e && atoi(e) == 0); }();
-  static const bool na6 = [] { const char* e = getenv("IDEQ_NA6"); return e && atoi(e) != 0; }();
-  const int na0 = na2 ? 2 : (na8 && 8 * acc_w <= 256 && p->halo) ? 8
-                : (na6 && acc_w == 64 && p->halo) ? 6 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
+  const uint32_t acc_w = (uint32_t)BN;  // TMEM columns per stage
+  const int na0 = (8 * acc_w <= 256 && p->halo) ? 8 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
   for (int na = na0; na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * acc_w) tc <<= 1;
-    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + xbytes + 512;
-    for (int c = (p->halo == 3 ? 1 : (cta3 && p->halo == 1) ? 3 : 2); c >= 1 && !stages; --c) {  // a CTA pair: one CTA per SM
-      const size_t avail = c == 3 ? (227 * 1024) / 3 - 1024 : c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
+    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
+    for (int c = 2; c >= 1 && !stages; --c) {
+      const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
       int st = (int)((avail - fixed) / op_stage);
       if (st > max_stages) st = max_stages;
@@ -1579,25 +1086,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.stages = stages;
   P.nacc = nacc;
   P.tmem_cols = tcols;
-  {
-    // opt-in (IDEQ_DIRECT=1): correct (the GPU suite passes with it on) but measured 30% SLOWER on
-    // the C3 bench (7.27k vs 10.27k img-it/s): register-to-global 16-byte stores at a 64-byte pixel
-    // stride use the same L1/shared data path at half sector efficiency, so they cost more than the
-    // staged tile + TMA store they replace
-    static const bool want_direct = [] { const char* e = getenv("IDEQ_DIRECT"); return e && atoi(e) != 0; }();
-    P.direct = (want_direct && (p->halo == 1 || p->halo == 2) && g.epi != EPI_IMG && (BN == 32 || BN == 64) &&
-                g.osh == 1 && g.osw == 1 && g.CB == g.ncols && g.OCp == g.ncols && g.OHo == g.OH && g.OWo == g.OW)
-                   ? 1 : 0;
-    P.out_ptr = out;
-    P.aux_ptr = aux;
-  }
-  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + xbytes + 512 + (size_t)stages * op_stage;
-  if (p->halo == 3) {  // units of (2 M tiles, 1 N tile); two CTAs (one cluster) per unit
-    const int units = ((P.m_tiles + 1) / 2) * P.n_tiles;
-    const int maxu = num_sms / 2;
-    p->grid = 2 * (units < maxu ? units : maxu);
-    return p;
-  }
+  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + 512 + (size_t)stages * op_stage;
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -1606,36 +1095,21 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
 
 // Every conv launch carries the programmatic-stream-serialization attribute (PDL): it may start
 // while its predecessor drains; the kernel waits (griddepcontrol.wait) before reading activations.
-// CTA pairs (MODE 3) add the cluster dimension. IDEQ_NO_PDL=1 launches plainly (A/B switch).
 template <int KC, int EPI, int BOXC>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
-  static const bool no_pdl = [] { const char* e = getenv("IDEQ_NO_PDL"); return e && atoi(e) != 0; }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p->grid);
   cfg.blockDim = dim3(TC_THREADS);
   cfg.dynamicSmemBytes = p->smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  int na = 0;
-  if (!no_pdl) {
-    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[na].val.programmaticStreamSerializationAllowed = 1;
-    ++na;
-  }
-  if (p->halo == 3) {  // CTA pairs: cluster of 2 on one TPC
-    at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = 2;
-    at[na].val.clusterDim.y = 1;
-    at[na].val.clusterDim.z = 1;
-    ++na;
-  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = na;
+  cfg.numAttrs = 1;
   switch (p->halo) {
     case 1: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 1>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
     case 2: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 2>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
-    case 3: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
-    case 4: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 4>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
     default: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 0>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
   }
 }
@@ -1652,18 +1126,15 @@ static void launch_epi(const TcPlan* p, cudaStream_t s) {
 }
 
 void tc_plan_set_active(TcPlan* p, const int* act_list, const int* n_act) {
-  // a CTA pair must walk the same units (its tile loop keeps the full order)
-  const char* ns = getenv("IDEQ_NO_SKIP");  // A/B switch for measurements
-  const bool ok = !(p->halo == 3 || (ns && atoi(ns) != 0));
-  p->list_ptr = ok ? act_list : nullptr;
+  p->list_ptr = act_list;
   p->P.n_act = n_act;
   p->P.act_list = nullptr;
   p->P.tpi = p->P.g.tiles_h * p->P.g.tiles_w * p->P.n_tiles;
   p->P.fd_tpi.init((uint32_t)p->P.tpi);
 }
 
-// The live list is switched on only for solves that can freeze images (tol > 0); the CUDA graph
-// of each parameter set captures the choice.
+// The live list is switched on only for solves that can freeze images (tol > 0, per-image rule,
+// unless the caller asks for every tile); the CUDA graph of each parameter set captures the choice.
 void tc_plan_enable_skip(TcPlan* p, bool on) { p->P.act_list = on ? p->list_ptr : nullptr; }
 
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C) {
@@ -1709,14 +1180,6 @@ void init_attrs_tc() {
   attrs_epi<64, 32, 2>();
   attrs_epi<32, 64, 2>();
   attrs_epi<32, 32, 2>();
-  attrs_epi<64, 64, 4>();
-  attrs_epi<64, 32, 4>();
-  attrs_epi<32, 64, 4>();
-  attrs_epi<32, 32, 4>();
-  attrs_epi<64, 64, 3>();
-  attrs_epi<64, 32, 3>();
-  attrs_epi<32, 64, 3>();
-  attrs_epi<32, 32, 3>();
 }
 
 }  // namespace ideq

@@ -971,7 +971,7 @@ FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
   f.tol = p ? p->tol : 0.f;
   f.partials = ctx->partials;
   f.active = ctx->active; f.status = ctx->status; f.iters = ctx->iters;
-  f.res = ctx->res; f.r_now = ctx->r_now; f.trace = ctx->trace; f.rmax = ctx->rmax;
+  f.res = ctx->res; f.r_now = ctx->r_now; f.trace = ctx->trace; f.trace_cap = ctx->trace_cap; f.rmax = ctx->rmax;
   f.n_active = ctx->n_active; f.kdev = ctx->kdev; f.act_list = ctx->act_list;
   const bool next1 = p && (p->restart || p->averaging);
   f.restart = p ? p->restart : 0;
@@ -1027,8 +1027,11 @@ ideq_status validate_params(ideq_ctx* ctx, int batch, const ideq_params* p) {
   if (p->averaging && p->tol != 0.f)
     return fail(ctx, IDEQ_E_INVALID, "averaging (Alg. 1 steps 12-13) needs a fixed iteration count: tol = 0");
   if (!ctx->op_set) return fail(ctx, IDEQ_E_STATE, "ideq_set_operator must be called before solving");
-  if (batch > ctx->op_batch && (ctx->op.kernel_per_image || ctx->op.kind == IDEQ_OP_INPAINT))
+  // the operator's per-image data (kernels, masks) and its FFT work spectrum are sized for the
+  // batch given to ideq_set_operator
+  if (batch > ctx->op_batch)
     return fail(ctx, IDEQ_E_INVALID, "batch %d exceeds the operator's batch %d", batch, ctx->op_batch);
+  if (p->compute_frozen != 0 && p->compute_frozen != 1) return fail(ctx, IDEQ_E_INVALID, "compute_frozen must be 0 or 1");
   return IDEQ_OK;
 }
 
@@ -1062,7 +1065,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
   if (ctx->op.kind == IDEQ_OP_MRI) prepare_mri(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
-  ctx->skip_frozen = p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE;
+  ctx->skip_frozen = p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE && !p->compute_frozen;
   for (auto& L : ctx->prog)  // skip frozen images' tiles only when images can freeze early
     if (L.plan) tc_plan_enable_skip(L.plan, ctx->skip_frozen);
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
@@ -1082,8 +1085,11 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   } else {
     // capture one iteration (plain and with the convergence all-reduce)
     char keybuf[256];
-    snprintf(keybuf, sizeof(keybuf), "%p|%p|%d|%a|%a|%a|%a|%d|%d|%d|%a|%d", (const void*)y, (void*)x, N, p->lambda,
-             p->tau, p->beta, p->tol, p->check_every, (int)p->stop_rule, p->restart, p->restart_B, p->averaging);
+    // every value the captured kernels hold by value: the pointers, the step parameters and the
+    // finalize arguments (max_iter sets the averaging window K, compute_frozen the tile lists)
+    snprintf(keybuf, sizeof(keybuf), "%p|%p|%d|%a|%a|%a|%a|%d|%d|%d|%a|%d|%d|%d", (const void*)y, (void*)x, N,
+             p->lambda, p->tau, p->beta, p->tol, p->check_every, (int)p->stop_rule, p->restart, p->restart_B,
+             p->averaging, p->max_iter, p->compute_frozen);
     if (ctx->graph_key != keybuf) {
       if (ctx->gexec_plain) { cudaGraphExecDestroy(ctx->gexec_plain); ctx->gexec_plain = nullptr; }
       if (ctx->gexec_check) { cudaGraphExecDestroy(ctx->gexec_check); ctx->gexec_check = nullptr; }

@@ -40,7 +40,8 @@ struct FinalizeArgs {
   int* iters;
   float* res;
   float* r_now;
-  float* trace;   // [max_iter] or null
+  float* trace;   // [trace_cap] or null: max_i r_i of iteration k < trace_cap
+  int trace_cap;
   float* rmax;    // 1 float (NCCL all-reduce target)
   int* n_active;
   int* act_list;  // [N] compacted indices of the active images (first *n_active), for the conv tile loops

@@ -475,7 +475,7 @@ __global__ void advance_a_kernel(FinalizeArgs f) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, smax[w]);
     m = fmaxf(m, smax[0]);
     const int k = *f.kdev;
-    if (f.trace) f.trace[k] = m >= 0.f ? m : __int_as_float(0x7fc00000);
+    if (f.trace && k < f.trace_cap) f.trace[k] = m >= 0.f ? m : __int_as_float(0x7fc00000);
     *f.rmax = m;  // -1 = no image updated on this rank
   }
 }
@@ -506,18 +506,31 @@ __global__ void advance_b_kernel(FinalizeArgs f) {
     *f.n_active = s;
     *f.kdev = k + 1;
   }
-  // compacted list of the active images in index order (the conv kernels' live tiles); the
-  // launch has one thread per image (N <= 1024 when skipping is on; the list is unused otherwise)
-  if (f.act_list && f.N <= (int)blockDim.x) {
+  // compacted list of the active images in index order (the conv kernels' live tiles), built in
+  // chunks of blockDim.x images: a ballot per warp, a prefix over the warps of the chunk, and a
+  // running offset carried from chunk to chunk (any N)
+  if (f.act_list) {
+    __shared__ int run;
     __syncthreads();  // thread 0 has read the counts in cnt[] before they are overwritten
-    const int n = threadIdx.x, lane = n & 31, w = n >> 5;
-    const int a = (n < f.N && f.active[n]) ? 1 : 0;
-    const unsigned bal = __ballot_sync(0xffffffffu, a);
-    if (lane == 0) cnt[w] = __popc(bal);   // cnt reused: its totals were consumed above
-    __syncthreads();
-    int off = 0;
-    for (int i = 0; i < w; ++i) off += cnt[i];
-    if (a) f.act_list[off + __popc(bal & ((1u << lane) - 1u))] = n;
+    if (threadIdx.x == 0) run = 0;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < f.N; base += blockDim.x) {
+      const int n = base + threadIdx.x;
+      const int a = (n < f.N && f.active[n]) ? 1 : 0;
+      const unsigned bal = __ballot_sync(0xffffffffu, a);
+      if (lane == 0) cnt[w] = __popc(bal);
+      __syncthreads();
+      int off = run;
+      for (int i = 0; i < w; ++i) off += cnt[i];
+      if (a) f.act_list[off + __popc(bal & ((1u << lane) - 1u))] = n;
+      __syncthreads();  // every thread has read run and cnt[]
+      if (threadIdx.x == 0) {
+        int s = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += cnt[i];
+        run += s;
+      }
+      __syncthreads();
+    }
   }
 }
 
@@ -708,13 +721,13 @@ void launch_inpaint_prox(const float* v, const float* y, const uint8_t* m, float
 }  // namespace ideq
 
 namespace ideq {
-// Off by default: on B200 the programmatic launch of the small per-iteration kernels (and of the
-// fused head) measured ~1% SLOWER on the C3 bench (10.20k vs 10.32k img-it/s, 3 interleaved A/B
-// pairs, tools/ab_lib.sh) and no better on the latency-bound C1 -- the early-launched CTAs wait
-// in SM slots while the persistent conv grids run. IDEQ_PDL_SMALL=1 turns it on (the kernels
-// call griddepcontrol.wait either way; without the launch attribute it returns at once).
-bool pdl_enabled() {
-  static const bool on = [] { const char* e = getenv("IDEQ_PDL_SMALL"); return e && atoi(e) != 0; }();
-  return on;
-}
+// Off: on B200 the programmatic launch of the small per-iteration kernels (and of the fused head)
+// measured ~1% SLOWER on the C3 bench (10.20k vs 10.32k img-it/s, 3 interleaved A/B pairs) and no
+// better on the latency-bound C1 -- the early-launched CTAs wait in SM slots while the persistent
+// conv grids run. The kernels call griddepcontrol.wait either way (a no-op without the attribute);
+// building with -DIDEQ_PDL_SMALL=1 turns the attribute on.
+#ifndef IDEQ_PDL_SMALL
+#define IDEQ_PDL_SMALL 0
+#endif
+bool pdl_enabled() { return IDEQ_PDL_SMALL != 0; }
 }  // namespace ideq

@@ -47,7 +47,7 @@ class OperatorDesc(C.Structure):
 class Params(C.Structure):
     _fields_ = [("lam", C.c_float), ("tau", C.c_float), ("beta", C.c_float), ("max_iter", C.c_int),
                 ("tol", C.c_float), ("check_every", C.c_int), ("stop_rule", C.c_int), ("restart", C.c_int),
-                ("restart_B", C.c_float), ("averaging", C.c_int)]
+                ("restart_B", C.c_float), ("averaging", C.c_int), ("compute_frozen", C.c_int)]
 
 
 class ImageStat(C.Structure):
@@ -224,7 +224,7 @@ class Solver:
 
     # ---------------------------------------------------------------- solve
     def params(self, lam=None, tau=None, beta=None, max_iter=None, tol=None, check_every=None, stop_rule=None,
-               restart=0, restart_B=0.0, averaging=False):
+               restart=0, restart_B=0.0, averaging=False, compute_frozen=False):
         cfg = self.cfg
         p = Params()
         p.lam = cfg["lam"] if lam is None else lam
@@ -237,6 +237,7 @@ class Solver:
         p.restart = int(restart)
         p.restart_B = float(restart_B)
         p.averaging = int(bool(averaging))
+        p.compute_frozen = int(bool(compute_frozen))
         return p
 
     def solve(self, y, x, params: Params, trace: bool = False, batch: int = None):

@@ -37,7 +37,7 @@ def test_headers_declare_the_boundary():
 def test_library_exports_every_declared_symbol(lib):
     for s in _declared_symbols():
         assert hasattr(lib, s), s
-    assert lib.ideq_abi_version() == 2
+    assert lib.ideq_abi_version() == 3
 
 
 def test_python_binding_covers_the_abi():
@@ -48,7 +48,7 @@ def test_python_binding_covers_the_abi():
 def test_struct_layouts_match_header():
     """ctypes mirrors of the ABI structs have the C sizes (x86-64 SysV)."""
     from paper_2605_19705_b200 import ideq
-    assert ctypes.sizeof(ideq.Params) == 10 * 4
+    assert ctypes.sizeof(ideq.Params) == 11 * 4
     assert ctypes.sizeof(ideq.OperatorDesc) == 64  # 5 ints + 3 pointers (+pad) + int + pointer + float (+pad)
     assert ctypes.sizeof(ideq.ImageStat) == 20
     assert ctypes.sizeof(ideq.Dist) == 8 + 128

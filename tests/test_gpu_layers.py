@@ -35,6 +35,16 @@ def _epi_ref(acc, epi, aux):
     return acc
 
 
+def assert_elementwise(got, ref, prec):
+    """Element-wise bound (catches errors confined to a few tile edges that a whole-tensor norm
+    would average away): bf16 outputs carry one rounding of 2^-9 relative to each element, so
+    max|got - ref| <= 2^-8 max|ref|; fp32 accumulation over <= 9 x 256 products stays far below
+    1e-5 max|ref|."""
+    bound = (2.0 ** -8 if prec == "bf16" else 1e-5) * np.abs(ref).max()
+    err = np.abs(got - ref)
+    assert err.max() <= bound, (prec, float(err.max()), float(bound), np.unravel_index(err.argmax(), err.shape))
+
+
 CASES = []
 for kind in range(6):
     pairs = [(32, 32), (64, 128)] + ([(64, 64)] if kind in (0, 1) else [])   # (64,64): resident-weight halo path
@@ -53,8 +63,6 @@ def test_layer_vs_oracle(path, kind, cin, cout, H, W, epi):
     from paper_2605_19705_b200 import ideq
     prec = "fp32" if path == "fp32" else "bf16"
     use_tc = path == "bf16-tc"
-    if use_tc and kind in (3, 4) and epi in (1, 3):
-        pass
     rng = np.random.default_rng(hash((kind, cin, cout, H, W, epi)) % (2 ** 32))
     fn, wshape = KINDS[kind]
     w = rng.standard_normal(wshape(cin, cout)) * np.sqrt(1.0 / (cin * 4))
@@ -82,16 +90,15 @@ def test_layer_vs_oracle(path, kind, cin, cout, H, W, epi):
     tol = 1e-5 if prec == "fp32" else 8e-3
     assert np.isfinite(got).all()
     assert rel_l2(got, ref) <= tol, (path, rel_l2(got, ref))
+    assert_elementwise(got, ref, prec)
 
 
-@pytest.mark.parametrize("pair", [False, True])
 @pytest.mark.parametrize("kind,cin,cout,N,H,W,epi", [(0, 64, 128, 3, 8, 40, 2), (1, 128, 64, 3, 8, 40, 3),
-                                                     (0, 128, 256, 1, 24, 24, 1)])
-def test_streamed_weight_layer_odd_tile_count(kind, cin, cout, N, H, W, epi, pair, monkeypatch):
-    """Streamed-weight 3x3 layers, single CTA (MODE 2) and on CTA pairs (IDEQ_PAIR=1: MODE 3,
-    cta_group::2, two M tiles per unit); an odd number of 16x8 tiles leaves the last pair's second
-    tile outside the batch (zero-filled loads, clipped stores). Checked against the oracle layer."""
-    monkeypatch.setenv("IDEQ_PAIR", "1" if pair else "0")
+                                                     (0, 128, 256, 1, 24, 24, 1), (1, 256, 128, 1, 24, 24, 3)])
+def test_streamed_weight_layer_odd_tile_count(kind, cin, cout, N, H, W, epi):
+    """Streamed-weight 3x3 layers (MODE 2: weights through a second TMA ring) with an odd number
+    of 16x8 tiles and, for 24x24, a partial last tile row (zero-filled loads, clipped stores).
+    Checked against the oracle layer, whole tensor and element by element."""
     torch = torch_cuda()
     from paper_2605_19705_b200 import ideq
     rng = np.random.default_rng(7 + kind)
@@ -112,40 +119,4 @@ def test_streamed_weight_layer_odd_tile_count(kind, cin, cout, N, H, W, epi, pai
     got = from_nhwc_dev(out)
     assert np.isfinite(got).all()
     assert rel_l2(got, ref) <= 8e-3
-
-
-ROW_CASES = []
-for kind in (0, 1):
-    for c, Ws in ((32, (32, 64, 128, 256)), (64, (32, 64, 128))):
-        for W in Ws:
-            for epi in (0, 1, 2, 3):
-                ROW_CASES.append((kind, c, W, epi))
-
-
-@pytest.mark.parametrize("kind,c,W,epi", ROW_CASES)
-def test_taps_in_n_row_layer(kind, c, W, epi, monkeypatch):
-    """MODE 4 (taps folded into N on full image rows, shuffle + exchange epilogue) for every
-    image width it serves, both conv directions and every fused epilogue, vs the oracle layer.
-    H = 11 is ragged for every row-group size. MODE 4 is opt-in (IDEQ_ROW=1)."""
-    monkeypatch.setenv("IDEQ_ROW", "1")
-    torch = torch_cuda()
-    from paper_2605_19705_b200 import ideq
-    rng = np.random.default_rng(1000 + kind * 100 + c + W + epi)
-    fn, wshape = KINDS[kind]
-    w = rng.standard_normal(wshape(c, c)) * np.sqrt(1.0 / (c * 4))
-    N, H = 2, 11
-    x = rng.standard_normal((N, c, H, W))
-    w32 = w.astype(np.float32)
-    xr, wr = bf16_round(x), bf16_round(w32)
-    ref_acc = np.stack([fn(xr[n], wr) for n in range(N)])
-    aux = auxr = None
-    if epi in (2, 3):
-        aux = rng.uniform(0.05, 2.0, ref_acc.shape) if epi == 3 else rng.standard_normal(ref_acc.shape)
-        auxr = bf16_round(aux)
-    ref = _epi_ref(ref_acc, epi, auxr)
-    out = torch.zeros((N, H, W, c), device="cuda", dtype=torch.bfloat16)
-    ideq.debug_conv(kind, "bf16", True, w32, N, H, W, nhwc_dev(x, "bf16"), out,
-                    nhwc_dev(aux, "bf16") if aux is not None else None, epi)
-    got = from_nhwc_dev(out)
-    assert np.isfinite(got).all()
-    assert rel_l2(got, ref) <= 8e-3, rel_l2(got, ref)
+    assert_elementwise(got, ref, "bf16")

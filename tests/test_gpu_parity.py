@@ -97,15 +97,18 @@ def _run_pair(name, precision, K, lam=None, **kw):
     return cfg, prob, xd.cpu().numpy(), st, tr, orc
 
 
-@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10), ("C4", 10), ("C5", 10)])
+@pytest.mark.parametrize("name,K", [("C1", 100), ("C2", 10), ("C3", 10), ("C4", 10), ("C5", 10),
+                                    ("C2", 50), ("C3", 50), ("C4", 50), ("C5s", 50)])
 @pytest.mark.parametrize("stress", [False, True])
 def test_trajectory_fp32(name, K, stress):
     """fp32 iterates after K steps within 1e-4 relative L2, residual within 1e-6 (north_star).
     The stress variant raises lambda so that lam*grad g is not negligible."""
     lam = None
     kw = {}
+    if name == "C5s":  # K = 50 on a smaller C5 plane (U-Net-64: the oracle's cost)
+        name, kw = "C5", dict(H=32, W=64)
     if stress:
-        kw = dict(init_scale=configs.STRESS[name]["init_scale"])
+        kw.update(init_scale=configs.STRESS[name]["init_scale"])
         lam = configs.STRESS[name]["lam"]
     cfg, prob, x, st, tr, orc = _run_pair(name, "fp32", K, lam=lam, **kw)
     assert (st["status"] == 1).all() and (st["iters"] == K).all()
@@ -116,9 +119,17 @@ def test_trajectory_fp32(name, K, stress):
 
 
 @pytest.mark.parametrize("name,K", [("C2", 30), ("C3", 30), ("C4", 30), ("C5", 30)])
-def test_trajectory_bf16_psnr(name, K):
-    """bf16 reconstruction PSNR within 0.05 dB of the oracle's (north_star)."""
-    cfg, prob, x, st, tr, orc = _run_pair(name, "bf16", K)
+@pytest.mark.parametrize("stress", [False, True])
+def test_trajectory_bf16_psnr(name, K, stress):
+    """bf16 reconstruction PSNR within 0.05 dB of the oracle's (north_star). The stress variant
+    (init x0.3 and a lambda with ||lam grad g(x0)|| >= 0.1 ||grad f||) makes the
+    tcgen05 network a visible part of every step."""
+    lam = None
+    kw = {}
+    if stress:
+        kw = dict(init_scale=configs.STRESS[name]["init_scale"])
+        lam = configs.STRESS[name]["lam"]
+    cfg, prob, x, st, tr, orc = _run_pair(name, "bf16", K, lam=lam, **kw)
     for b in range(x.shape[0]):
         d = abs(psnr(x[b], prob["x_true"][b]) - psnr(orc["x"][b], prob["x_true"][b]))
         assert d <= 0.05, d
@@ -219,9 +230,10 @@ def test_determinism_and_batch_independence():
         assert torch.equal(x1[0], xa[2])
 
 
-@pytest.mark.parametrize("ks,H,W", [(25, 64, 96), (9, 72, 64), (7, 48, 40), (9, 32, 40)])
+@pytest.mark.parametrize("ks,H,W", [(25, 64, 96), (9, 72, 64), (15, 64, 80), (15, 128, 72), (7, 48, 40), (9, 32, 40)])
 def test_direct_blur_kernel_sizes(ks, H, W):
-    """Direct-blur gradient step at every register-blocked kernel size (9, 15 in C2 above, 25) and
+    """Direct-blur gradient step at every register-blocked kernel size (9, 15 -- C2's, at >= 64 x 64
+    planes so the register-blocked kernel runs --, 25) and
     the 32-tile kernel (size 7, and planes smaller than 64 x 64): grad f component within 1e-5 and an fp32 trajectory within 1e-4 / 1e-6
     (C5 geometry with the gradient variant; 64 x 64 blur tiles with ragged edges)."""
     torch = torch_cuda()

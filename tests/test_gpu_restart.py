@@ -92,3 +92,16 @@ def test_averaging_needs_fixed_count_and_window():
     st, _, xa = _run(torch, s, prob, max_iter=4, tol=0.0, averaging=True)
     _, _, xb = _run(torch, s, prob, max_iter=4, tol=0.0)
     assert (st["k0"] == -1).all() and np.array_equal(xa, xb)
+
+
+def test_averaging_two_solves_different_max_iter_one_solver():
+    """The CUDA graph of an iteration bakes in the finalize arguments, among them the averaging
+    window K = max_iter: a second solve on the SAME context with another max_iter must not
+    reuse the first solve's graph. Both solves are checked against the oracle (K0 and x-hat)."""
+    torch, cfg, prob, s = _setup("C3", "fp32")
+    for K in (5, 14, 9):
+        orc = osolver.solve_config(cfg, prob, max_iter=K, tol=0.0, averaging=True)
+        st, code, x = _run(torch, s, prob, max_iter=K, tol=0.0, averaging=True)
+        assert np.array_equal(st["k0"], orc["k0"]), (K, st["k0"], orc["k0"])
+        for b in range(x.shape[0]):
+            assert rel_l2(x[b], orc["x"][b]) <= 1e-4, K
