@@ -129,6 +129,7 @@ def cpu_baseline(cfg, n_img=1, iters=3):
     osolver.solve(net, fids, prob["x0"], cfg["lam"], cfg["tau"], cfg["beta"], iters, 0.0, cfg["step"])
     dt = time.perf_counter() - t0
     return {"value": n_img * iters / dt, "unit": UNIT, "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+            "cpu_model": _cpu_model(),
             "sample": f"{n_img} image x {iters} iterations of {cfg['name']} (fp64 numpy oracle, {dt:.1f} s)"}
 
 
@@ -156,11 +157,35 @@ def run_reference(args, cfg, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": _config_dict(cfg, args.batch or (cfg["batch"] // 8 if args.config == "C5" else cfg["batch"]), world),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "config": dict(_config_dict(cfg, args.batch or (cfg["batch"] // world if args.config == "C5" else cfg["batch"]),
+                                        world), timed_images_per_step=1,
+                           timed="one image-iteration of the same workload per step (a bounded sample of the batch)"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": _cpu_model(),
                              "sample": f"1 image-iteration of {cfg['name']} per step (fp64 numpy oracle)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def _relaunch_under_torchrun(args):
+    """`bench.py --gpus N` without a torchrun environment: start N ranks on this node (one process
+    per GPU) through torch.distributed.run, with the same arguments; rank 0 prints the line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 def _config_dict(cfg, per_rank, world):
@@ -188,6 +213,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--batch", type=int, default=0, help="images per GPU (default: the config's per-GPU batch)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", default=None, choices=["bf16", "fp32"],
+                    help="override the config's precision (fp32 = the 3xTF32 tensor-core parity mode)")
     ap.add_argument("--restart", type=float, default=0.0,
                     help="NEXT-1: adaptive restart with this B (Eq. 5, Alg. 1 semantics) in every timed solve")
     ap.add_argument("--averaging", action="store_true", help="NEXT-1: averaging (Alg. 1 steps 12-13) in the timed solves")
@@ -196,9 +223,12 @@ def main():
     args = ap.parse_args()
     assert args.warmup >= 3 or args.impl == "reference", "W >= 3 warm-up steps"
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_relaunch_under_torchrun(args))
     rank = _env_int("RANK", 0)
     world = _env_int("WORLD_SIZE", 1)
     local = _env_int("LOCAL_RANK", 0)
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
     from paper_2605_19705_b200 import configs
     cfg = configs.get(args.config)
     if args.impl == "reference":
@@ -206,19 +236,32 @@ def main():
 
     import torch
     import torch.distributed as dist
+    from paper_2605_19705_b200 import dist as dist_util
     from paper_2605_19705_b200 import ideq, synth
 
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    # per-GPU images: the config's batch, except C5 whose 512 images are sharded 64 per GPU at P = 8
-    # (its weak-scaling unit); --batch overrides
-    per = args.batch or (cfg["batch"] // 8 if args.config == "C5" else cfg["batch"])
-    images = list(range(rank * per, (rank + 1) * per))
+    # per-GPU images: the config's batch on every rank (weak scaling: the per-GPU work is fixed),
+    # except C5 whose 512 images are sharded over the ranks (the largest batch, BASELINE C5);
+    # --batch overrides
+    if args.config == "C5" and not args.batch:
+        shard = dist_util.shard(cfg["batch"], world, rank)
+        images, scaling = list(shard), "strong"
+    else:
+        per0 = args.batch or cfg["batch"]
+        images, scaling = list(range(rank * per0, (rank + 1) * per0)), "weak"
+    per = len(images)
     prob = synth.make_problem(cfg, images=images)
     stream = torch.cuda.Stream()
-    prec = cfg.get("precision", "bf16")   # C1 is an fp32 config (BASELINE), the others bf16
-    s = ideq.Solver(cfg, prob["weights"], precision=prec, device=local, stream=stream, max_batch=per)
+    prec = args.precision or cfg.get("precision", "bf16")   # C1 is an fp32 config (BASELINE), the others bf16
+    # NCCL communicator for the GLOBAL_MAX stop rule (C5): rank 0 draws the id, torch.distributed
+    # broadcasts it; per-image configs need no collective
+    nccl_id = None
+    if world > 1 and cfg["stop_rule"] == "global_max":
+        nccl_id = dist_util.broadcast_nccl_id()
+    s = ideq.Solver(cfg, prob["weights"], precision=prec, device=local, stream=stream, max_batch=per,
+                    rank=rank, world=world, nccl_id=nccl_id)
     s.set_operator(prob)
     y = torch.tensor(prob["y"]).cuda()
     x = torch.tensor(prob["x0"]).cuda()
@@ -252,7 +295,7 @@ def main():
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     assert (stats["iters"] == args.steps).all(), "timed solve did not run K iterations on every image"
-    value = per * world * args.steps / (ms / 1000.0)
+    value = (cfg["batch"] if scaling == "strong" else per * world) * args.steps / (ms / 1000.0)
 
     # ---- e2e: same K iterations through ideq_solve_host (pinned host y/x, H2D + D2H inside)
     yh = torch.tensor(prob["y"]).pin_memory().numpy()
@@ -265,50 +308,59 @@ def main():
     s.solve_host(yh, xh, s.params(max_iter=args.steps, tol=0.0, **nx1))
     barrier()
     e2e_s = max_over_ranks(time.perf_counter() - t0)
-    e2e_v = per * world * args.steps / e2e_s
+    e2e_v = (cfg["batch"] if scaling == "strong" else per * world) * args.steps / e2e_s
 
-    # ---- roofline of the dominant kernel class (tcgen05 convolutions): CUDA events around
-    #      every launch inside an eager (profiled) run of the same iterations
-    kprof = min(args.steps, 10)
-    x.copy_(torch.tensor(prob["x0"]))
-    s.set_profiling(True)
-    s.profile(reset=True)
-    s.solve(y, x, s.params(max_iter=kprof, tol=0.0, **nx1))
-    prof = s.profile(reset=True)
-    s.set_profiling(False)
+    # ---- roofline of the dominant kernel class: its launches of one iteration, in the iteration's
+    #      order and launch configuration, captured into one CUDA graph and replayed back to back
+    #      (ideq_time_class: CUDA events on the solve stream); its share of the device-timed step
     peaks, peak_src = _peaks()
-    tc = prof["conv_tc"]
-    achieved = tc["flops"] / (tc["ms"] / 1000.0) / 1e12 if tc["ms"] > 0 else None
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
-    total_ms = sum(v["ms"] for v in prof.values())
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "conv_tc_traffic.json")
-    if os.path.exists(tp) and args.config == "C3" and per == cfg["batch"]:  # captured on C3 only
-        try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
-        except Exception:
-            traffic = None
-    if tc["ms"] == 0 and prof["conv_simt"]["ms"] > 0:  # FFMA path (C1 fp32): ALU roofline
-        sm = prof["conv_simt"]
+    cls = "conv_tc" if prec == "bf16" or cfg["net"] == "unet4" else "conv_simt"
+    reps = 20
+    kt = s.time_class(cls, reps)
+    st_t = s.time_class("step", reps)
+    ht_t = s.time_class("headtail", reps)
+    clocks = clk.summary()
+    burst = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and ms * args.steps < 1000.0
+                 and clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
+    if cls == "conv_simt":   # FFMA convolutions (C1's tiny net): ALU roofline
         ffma_peak = 148 * 128 * 2 * 1965e6 / 1e12   # derived: SMs x FP32 lanes x 2 x max SM clock
-        roofline = {"bound": "alu", "achieved": sm["flops"] / (sm["ms"] / 1000.0) / 1e12, "peak": ffma_peak,
-                    "unit": "TFLOP/s", "frac": sm["flops"] / (sm["ms"] / 1000.0) / 1e12 / ffma_peak, "traffic": None,
-                    "kernel": "conv_simt_kernel (all FFMA conv launches of a step)",
-                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz",
-                    "share_of_step": sm["ms"] / total_ms if total_ms else None,
-                    "per_class_ms_per_step": {k: v["ms"] / kprof for k, v in prof.items()},
-                    "algorithmic_flops_per_step": sm["flops"] / kprof}
+        ach = kt["flops"] / (kt["ms"] / 1000.0) / 1e12
+        roofline = {"bound": "alu", "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s", "frac": ach / ffma_peak,
+                    "traffic": None, "kernel": "conv_simt_kernel (all FFMA conv launches of a step)",
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"}
     else:
-      roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                "kernel": "conv_tc_kernel (all tcgen05 conv launches of a step)",
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside the step)",
-                "share_of_step": tc["ms"] / total_ms if total_ms else None,
-                "per_class_ms_per_step": {k: v["ms"] / kprof for k, v in prof.items()},
-                "algorithmic_flops_per_step": tc["flops"] / kprof,
-                # algorithmic HBM bytes per launch (each activation read / written once, weights
-                # once) beside the ncu-measured `traffic` of the same launches
-                "algorithmic_bytes_per_launch": (tc["bytes"] / tc["launches"]) if tc["launches"] else None}
+        # tensor peak of the path's own dtype: bf16 measured; 3xTF32 = measured bf16 x (TF32/bf16
+        # nominal ratio 1/2) / 3 MMAs per product
+        scale = 1.0 if prec == "bf16" else 0.5 / 3.0
+        pk_b = peaks.get("bf16_tflops") * scale
+        pk_s = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * scale
+        peak = pk_b if burst else pk_s
+        ach = kt["flops"] / (kt["ms"] / 1000.0) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "conv_tc_traffic.json")
+        if os.path.exists(tp) and args.config == "C3" and per == cfg["batch"] and prec == "bf16":
+            try:
+                traffic = json.load(open(tp)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": traffic,
+                    "kernel": "conv_tc_kernel (all tcgen05 conv launches of a step)" + ("" if prec == "bf16" else
+                              ", 3xTF32 (kind::tf32, 3 MMAs per product)"),
+                    "peak_source": f"{peak_src} {'bf16_tflops (burst: sub-second region at max clock)' if burst else 'bf16_tflops_sustained'}"
+                                   + ("" if prec == "bf16" else " x 1/2 (TF32 nominal) / 3 (3xTF32)"),
+                    "frac_burst": ach / pk_b, "frac_sustained": ach / pk_s}
+    roofline.update({
+        "timing": f"ideq_time_class: the class's launches of one iteration in one CUDA graph, {reps} replays",
+        "ms_per_step": kt["ms"], "share_of_step": kt["ms"] / (ms / args.steps),
+        "algorithmic_flops_per_step": kt["flops"], "algorithmic_bytes_per_step": kt["bytes"],
+        "launches_per_step": s.launches_per_iteration(),
+        "other_classes_ms_per_step": {"step": st_t["ms"], "headtail": ht_t["ms"]},
+        "step_kernel": {"bound": "hbm", "algorithmic_bytes_per_step": st_t["bytes"], "ms": st_t["ms"],
+                        "achieved_gbs": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9,
+                        "frac": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9 / peaks["hbm_gbs"],
+                        "peak_gbs": peaks["hbm_gbs"]},
+    })
 
     # ---- ms to tolerance (tol = 1e-4, per-image stop)
     tol_info = None
@@ -324,7 +376,7 @@ def main():
                     "converged": int((st2["status"] == 0).sum()), "images": per}
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f32" if prec == "fp32" else "bf16", "data": "synthetic (seeded piecewise-smooth images, random-init "
             "U-Net weights" + {"inpaint": "; stands in for the paper's BSDS500 inpainting split)",
                                "mri": "; stand-in phantoms for the paper's fastMRI knee data)"}.get(cfg["op"], ")"),
@@ -334,7 +386,7 @@ def main():
                     "d2h_bytes_per_step": xh.nbytes / args.steps,
                     "note": "one ideq_solve_host call of K iterations: H2D of y and x0, D2H of x-hat inside"},
             "gpu_launches": s.launches_per_iteration() * args.steps + 4,
-            "roofline": roofline, "clocks": clk.summary()}
+            "roofline": roofline, "clocks": clocks, "plan": s.plan()}
     if tol_info:
         line["ms_to_tolerance"] = tol_info
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

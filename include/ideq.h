@@ -108,12 +108,35 @@ typedef struct {
 
 IDEQ_API ideq_status ideq_get_nccl_id(unsigned char out[128]);
 
-/* Create a context on `device`, enqueuing on `cuda_stream` (cudaStream_t, NULL =
- * legacy default stream). Workspaces are sized for up to max_batch images of
- * H x W; ideq_solve never allocates. dist may be NULL (single process). */
+/* Create a context on `device`, enqueuing on `cuda_stream` (cudaStream_t, NULL = a stream the
+ * context owns). Workspaces are sized for up to max_batch images of H x W (network activations
+ * for the planned micro-batch, see ideq_create_ex; ideq_create = ideq_create_ex with opts NULL);
+ * ideq_solve never allocates. dist may be NULL (single process). IDEQ_E_NOMEM when even one
+ * image's workspace does not fit. */
 IDEQ_API ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int device,
                         void* cuda_stream, int max_batch, int H, int W,
                         const ideq_dist* dist, ideq_ctx** out);
+
+/* Workspace plan (ideq_create_ex). The solver state -- iterates, gradients, residual
+ * bookkeeping -- is allocated for max_batch images; the network's activations (3 work tensors
+ * per U-Net level plus the saved activation of every residual block, ~432 MB per 512 x 512 image
+ * for U-Net-64 in bf16) for a MICRO-BATCH of images: a solve runs U_theta and its VJP once per
+ * micro-batch, in order, then the fidelity step over the whole batch. Results do not depend on
+ * the micro-batch (every kernel is per image). micro_batch = 0: the largest balanced
+ * micro-batch whose workspace fits in workspace_bytes (0: 90% of the device memory left after
+ * the state, minus a reserve of 2 GB + 3 planes per image for the operator and host staging).
+ * With more than one micro-batch, early-stopping solves compute frozen images' tiles (the
+ * live-image list indexes a whole batch). */
+typedef struct {
+  int micro_batch;
+  size_t workspace_bytes;
+} ideq_plan_opts;
+
+IDEQ_API ideq_status ideq_create_ex(const ideq_net_desc* net, ideq_precision prec, int device,
+                           void* cuda_stream, int max_batch, int H, int W,
+                           const ideq_dist* dist, const ideq_plan_opts* opts, ideq_ctx** out);
+/* The plan chosen at create: images per network pass and the network workspace in bytes. */
+IDEQ_API ideq_status ideq_get_plan(const ideq_ctx* ctx, int* micro_batch, size_t* workspace_bytes);
 
 typedef enum { IDEQ_OP_BLUR = 0, IDEQ_OP_INPAINT = 1, IDEQ_OP_PHASE = 2, IDEQ_OP_RICIAN = 3, IDEQ_OP_MRI = 4 } ideq_op_kind;
 typedef enum { IDEQ_STEP_GRAD = 0, IDEQ_STEP_PROX = 1 } ideq_step;   /* Alg. 1 vs Alg. 2 */
@@ -253,6 +276,16 @@ typedef struct {
 
 IDEQ_API ideq_status ideq_set_profiling(ideq_ctx* ctx, int enable);
 IDEQ_API ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int reset);
+
+/* In-graph timing of one kernel class (ideq_kernel_class: CONV_TC, CONV_SIMT, HEADTAIL or STEP)
+ * of the LAST solve's iteration: the class's launches, in the iteration's order and launch
+ * configuration, captured into one CUDA graph and replayed `reps` times back to back on the
+ * context stream (CUDA events around the replays). *ms = milliseconds per iteration; flops and
+ * bytes = the class's algorithmic FLOPs and HBM bytes per iteration. The kernels read and write
+ * the context's workspaces (the last solve's data); the solve's result in x_inout is untouched.
+ * IDEQ_E_STATE before the first solve. */
+IDEQ_API ideq_status ideq_time_class(ideq_ctx* ctx, int kernel_class, int reps, double* ms, double* flops,
+                                     double* bytes);
 
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches). */
 IDEQ_API int ideq_launches_per_iteration(const ideq_ctx* ctx);

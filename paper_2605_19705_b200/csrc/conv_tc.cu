@@ -97,6 +97,28 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uin
 // base-offset encodings give wrong results).
 
 // Instruction descriptor for kind::f16: bf16 x bf16 -> f32, both K-major, M=128, N=n.
+// kind::tf32: tf32 x tf32 -> f32 (A/B format 2), K-major, M = 128, N = n
+__device__ __forceinline__ uint32_t make_idesc_tf32(int n) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// x = hi + lo with hi = x rounded to tf32 (10-bit mantissa, low 13 bits zero) and lo = x - hi
+// (exact in fp32); the tensor core reads lo to tf32 precision, so hi*b + lo*b carries ~21 bits.
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  uint32_t h;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
+  hi = __uint_as_float(h);
+  lo = x - hi;
+}
 __device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
   return (1u << 4)                       // D format f32
          | (1u << 7)                     // A format bf16
@@ -294,14 +316,15 @@ __device__ __forceinline__ TileIdx tile_index(const TcParams& P, int t) {
   return r;
 }
 
-constexpr int TC_THREADS = 352;  // warp 0 TMA operands, warp 1 MMA, warps 2..9 epilogue, warp 10 TMA aux
+constexpr int TC_THREADS = 352;     // warp 0 TMA operands, warp 1 MMA, warps 2..9 epilogue, warp 10 TMA aux
+constexpr int TC_THREADS_X3 = 480;  // 3xTF32: + warps 11..14 split every staged fp32 A tile into tf32 hi / lo
 
-// Epilogue boxes are BOXC = min(BN, 64) columns wide: 128-byte rows (SW128) for 64 columns,
-// 64-byte rows (SW64) for 32. A thread owns one pixel row; 16-byte chunk j of row r lives at
-// chunk j ^ swz(r) so a quarter-warp touches 8 distinct bank groups.
-template <int BOXC>
+// Epilogue boxes have RB-byte rows: 128 (SW128: 64 bf16 or 32 fp32 columns) or 64 (SW64: 32 bf16
+// columns). A thread owns one pixel row; 16-byte chunk j of row r lives at chunk j ^ swz(r) so a
+// quarter-warp touches 8 distinct bank groups.
+template <int RB>
 __device__ __forceinline__ uint32_t epi_chunk_addr(uint32_t box_base, int r, int j) {
-  if (BOXC == 64) return box_base + (uint32_t)r * 128u + (uint32_t)((j ^ (r & 7)) << 4);
+  if (RB == 128) return box_base + (uint32_t)r * 128u + (uint32_t)((j ^ (r & 7)) << 4);
   return box_base + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
 }
 
@@ -322,41 +345,63 @@ __device__ __forceinline__ void st_shared_v4(uint32_t a, uint4 v) {
 // crosses L2 ~1.4x (2D) / ~3x (1-row) instead of 9x. MODE 1 keeps the layer's weights resident
 // in shared memory for the CTA's lifetime; MODE 2 streams them per (chunk, tap) through a second
 // ring (layers whose weights do not fit).
-template <int KC, int EPI, int BOXC, int MODE>
-__global__ void __launch_bounds__(TC_THREADS, 2)
+//
+// KB = bytes of one K-block row (one pixel's channel chunk): 64 (SW64) or 128 (SW128); one MMA
+// consumes 32 bytes of K (16 bf16 / 8 tf32). BOXB = bytes of one epilogue-box row (64 or 128).
+//
+// X3 (the fp32 parity mode, 3xTF32): operands are fp32 in HBM. The weights arrive pre-split into
+// tf32 hi / lo tensors (tmB, tmBlo); every staged fp32 A tile is split in shared memory by four
+// converter warps (hi in place, lo beside it) before the MMA warp may read it, and every K step
+// issues A_hi*B_hi + A_lo*B_hi + A_hi*B_lo (kind::tf32) into the fp32 TMEM accumulator
+// (the A_lo*B_lo term is below fp32 rounding). The epilogue keeps fp32 and the exact fp32
+// softplus / sp'. Reference: the network of Eq. 2 and its VJP.
+template <int KB, int EPI, int BOXB, int MODE, bool X3>
+__global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
     conv_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const __grid_constant__ CUtensorMap tmOut, const __grid_constant__ CUtensorMap tmAux,
-                   const __grid_constant__ CUtensorMap tmSlab, const __grid_constant__ TcParams P) {
+                   const __grid_constant__ CUtensorMap tmSlab, const __grid_constant__ CUtensorMap tmBlo,
+                   const __grid_constant__ TcParams P) {
   constexpr bool HAS_AUX = (EPI == EPI_RESADD || EPI == EPI_SIGMUL);
+  constexpr int ES = X3 ? 4 : 2;           // element bytes (fp32 / bf16)
+  constexpr int BOXC = BOXB / ES;          // columns per epilogue box
+  constexpr int NBUF = X3 ? 2 : 1;         // operand buffers per stage (hi, lo)
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
   const int S = P.stages;
   const int BN = P.BN;
-  const uint32_t a_stage = 128u * KC * 2u;
+  const uint32_t a_stage = 128u * KB;
   constexpr bool STREAMB = MODE == 2;
-  const uint32_t b_stage = (uint32_t)BN * KC * 2u;
-  const uint32_t epi_stage = (uint32_t)BN * 128u * 2u;  // BN/BOXC boxes of 128 x BOXC
+  const uint32_t b_stage = (uint32_t)BN * KB;             // one weight box (hi or lo)
+  const uint32_t bslot = b_stage * NBUF;                  // one ring slot: hi (+ lo)
+  const uint32_t epi_stage = (uint32_t)BN * 128u * ES;    // BN/BOXC boxes of 128 x BOXC
   const ConvGeom& g = P.g;
   const int nkb = g.ntaps * g.nchunk;
   constexpr bool HALO = MODE != 0;
   const int SB = STREAMB ? P.stagesB : 0;
-  // MODE 0: [A stages][B stages][epi]; MODE 1: [resident W (nkb B boxes)][halo stages][epi];
-  // MODE 2: [halo stages][B ring][epi]
+  const uint32_t op_a = HALO ? P.halo_stage : a_stage;    // one A buffer (hi or lo)
+  // MODE 0: [A hi S][A lo S][B slots S][epi]; MODE 1: [W hi nkb][W lo nkb][halo hi S][halo lo S][epi];
+  // MODE 2: [halo hi S][halo lo S][B ring slots SB][epi]      (lo buffers in 3xTF32 only)
   const uint32_t sW = base;
-  const uint32_t sA = (MODE == 1) ? sW + (uint32_t)nkb * b_stage : base;
-  const uint32_t sB = sA + S * (HALO ? P.halo_stage : a_stage);
-  const uint32_t sE = (MODE == 1) ? sB : sB + (STREAMB ? SB : S) * b_stage;
+  const uint32_t sA = (MODE == 1) ? sW + (uint32_t)nkb * bslot : base;
+  const uint32_t sAlo = sA + S * op_a;
+  const uint32_t sB = sA + S * op_a * NBUF;
+  const uint32_t sE = (MODE == 1) ? sB : sB + (STREAMB ? SB : S) * bslot;
   const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
   const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
-  // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB], emptyB[SB]
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1 + 2 * SB);
+  // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB],
+  // emptyB[SB], split[S] (3xTF32: the A tile of stage s is split)
+  const int NSPL = X3 ? S : 0;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 4 * NA + 1 + 2 * SB + NSPL);
   const uint32_t full0 = sBar, empty0 = sBar + 8u * S;
   const uint32_t tfull0 = sBar + 16u * S, tempty0 = tfull0 + 8u * NA, auxfull0 = tempty0 + 8u * NA,
                  epifree0 = auxfull0 + 8u * NA;
   const uint32_t wfull = epifree0 + 8u * NA;
   const uint32_t fullB0 = wfull + 8u, emptyB0 = fullB0 + 8u * SB;
+  const uint32_t split0 = emptyB0 + 8u * SB;
+  // the MMA warp waits for the split tile (3xTF32) or the landed tile
+  const uint32_t ready0 = X3 ? split0 : full0;
 
   // warp index broadcast from lane 0 so the compiler knows it is warp-uniform (uniform datapath)
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
@@ -368,11 +413,14 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     mbar_init(wfull, 1);
     if (MODE == 1) {  // resident weights (constant since create): loaded before the wait
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes);
+      mbar_expect_tx(wfull, (uint32_t)nkb * P.b_bytes * NBUF);
       for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + kb * b_stage, &tmB, wfull, 0, 0, kb);
+      if (X3)
+        for (int kb = 0; kb < nkb; ++kb) tma_load_3d(sW + (nkb + kb) * b_stage, &tmBlo, wfull, 0, 0, kb);
     }
     for (int s = 0; s < S; ++s) { mbar_init(full0 + 8u * s, 1); mbar_init(empty0 + 8u * s, 1); }
     for (int s = 0; s < SB; ++s) { mbar_init(fullB0 + 8u * s, 1); mbar_init(emptyB0 + 8u * s, 1); }
+    for (int s = 0; s < NSPL; ++s) mbar_init(split0 + 8u * s, 4);  // one arrival per converter warp
     for (int a = 0; a < NA; ++a) {
       mbar_init(tfull0 + 8u * a, 1);
       mbar_init(tempty0 + 8u * a, 8);   // one arrival per epilogue warp
@@ -385,6 +433,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     prefetch_tmap(&tmOut);
     prefetch_tmap(&tmSlab);
     if (HAS_AUX) prefetch_tmap(&tmAux);
+    if (X3) prefetch_tmap(&tmBlo);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
@@ -405,6 +454,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
   const int nbox = BN / BOXC;
   // tiles this launch walks: all of them, or the live list's (read after griddepcontrol.wait)
   const int tot_it = P.act_list ? *(volatile const int*)P.n_act * P.tpi : total;
+  const int nload = HALO ? g.nchunk : nkb;  // A stages per tile
 
   if (warp == 0) {
     // ---------------- TMA producer: the whole warp walks the loop (warp-uniform state stays in
@@ -414,30 +464,60 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     for (int L = t0; L < tot_it; L += tstep) {
       const TileIdx ti = tile_index(P, live_tile(P, L));
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
-      const int nload = HALO ? g.nchunk : nkb;
       for (int kb = 0; kb < nload; ++kb) {
         mbar_wait(empty0 + 8u * s, ph ^ 1u);
         if (elect_one()) {
           if (HALO) {
             mbar_expect_tx(full0 + 8u * s, P.a_bytes);
-            tma_load_5d(sA + s * P.halo_stage, &tmA, full0 + 8u * s, kb * KC, w0 - 1, 0, h0 - 1, img);
-            if (MODE == 2) {  // this chunk's 9 weight boxes through the B ring
+            tma_load_5d(sA + s * op_a, &tmA, full0 + 8u * s, kb * (KB / ES), w0 - 1, 0, h0 - 1, img);
+            if (MODE == 2) {  // this chunk's 9 weight boxes (hi, lo) through the B ring
               for (int tap = 0; tap < 9; ++tap) {
                 mbar_wait(emptyB0 + 8u * sb, phb ^ 1u);
-                mbar_expect_tx(fullB0 + 8u * sb, P.b_bytes);
-                tma_load_3d(sB + sb * b_stage, &tmB, fullB0 + 8u * sb, 0, nt * BN, tap * g.nchunk + kb);
+                mbar_expect_tx(fullB0 + 8u * sb, P.b_bytes * NBUF);
+                tma_load_3d(sB + sb * bslot, &tmB, fullB0 + 8u * sb, 0, nt * BN, tap * g.nchunk + kb);
+                if (X3) tma_load_3d(sB + sb * bslot + b_stage, &tmBlo, fullB0 + 8u * sb, 0, nt * BN, tap * g.nchunk + kb);
                 if (++sb == SB) { sb = 0; phb ^= 1u; }
               }
             }
           } else {
             const int tap = kb / g.nchunk, chunk = kb - tap * g.nchunk;
-            mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes);
-            tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * KC, w0 + g.dw[tap], g.dp[tap],
+            mbar_expect_tx(full0 + 8u * s, P.a_bytes + P.b_bytes * NBUF);
+            tma_load_5d(sA + s * a_stage, &tmA, full0 + 8u * s, chunk * (KB / ES), w0 + g.dw[tap], g.dp[tap],
                         h0 + g.dh[tap], img);
-            tma_load_3d(sB + s * b_stage, &tmB, full0 + 8u * s, 0, nt * BN, kb);
+            tma_load_3d(sB + s * bslot, &tmB, full0 + 8u * s, 0, nt * BN, kb);
+            if (X3) tma_load_3d(sB + s * bslot + b_stage, &tmBlo, full0 + 8u * s, 0, nt * BN, kb);
           }
         }
         __syncwarp();
+        if (++s == S) { s = 0; ph ^= 1u; }
+      }
+    }
+  } else if (X3 && warp >= 11) {
+    // ---------------- 3xTF32 converter warps 11..14: split each landed fp32 A tile (the whole
+    // staged box, element-wise, so the swizzle is irrelevant) into hi (in place) and lo
+    const int ct = threadIdx.x - 11 * 32;  // 0..127
+    int s = 0;
+    uint32_t ph = 0;
+    const uint32_t nchunks = P.a_bytes >> 4;
+    for (int L = t0; L < tot_it; L += tstep) {
+      for (int kb = 0; kb < nload; ++kb) {
+        mbar_wait(full0 + 8u * s, ph);
+        const uint32_t hi0 = sA + s * op_a, lo0 = sAlo + s * op_a;
+        for (uint32_t c = ct; c < nchunks; c += 128) {
+          const uint4 u = ld_shared_v4(hi0 + (c << 4));
+          float h[4], l[4];
+          split_tf32(__uint_as_float(u.x), h[0], l[0]);
+          split_tf32(__uint_as_float(u.y), h[1], l[1]);
+          split_tf32(__uint_as_float(u.z), h[2], l[2]);
+          split_tf32(__uint_as_float(u.w), h[3], l[3]);
+          st_shared_v4(hi0 + (c << 4), make_uint4(__float_as_uint(h[0]), __float_as_uint(h[1]), __float_as_uint(h[2]),
+                                                  __float_as_uint(h[3])));
+          st_shared_v4(lo0 + (c << 4), make_uint4(__float_as_uint(l[0]), __float_as_uint(l[1]), __float_as_uint(l[2]),
+                                                  __float_as_uint(l[3])));
+        }
+        fence_async_smem();  // generic-proxy writes -> visible to the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(split0 + 8u * s);
         if (++s == S) { s = 0; ph ^= 1u; }
       }
     }
@@ -468,42 +548,54 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     // (64-bit adds of byte offsets >> 4); one elected lane issues tcgen05.mma / commit. A
     // single-thread issue loop measured ~110 clk per MMA on B200 (tools/umma_bench.cu) against
     // a tensor floor of 16-128 clk; the uniform form reaches the floor for N >= 128.
-    const uint32_t idesc = make_idesc_bf16(BN);
-    constexpr uint32_t layout = (KC == 64) ? 2u : 4u;   // SW128 / SW64
-    constexpr uint32_t sbo = (KC == 64) ? 1024u : 512u; // 8 rows x row bytes
+    const uint32_t idesc = X3 ? make_idesc_tf32(BN) : make_idesc_bf16(BN);
+    constexpr uint32_t layout = (KB == 128) ? 2u : 4u;   // SW128 / SW64
+    constexpr uint32_t sbo = (KB == 128) ? 1024u : 512u; // 8 rows x row bytes
     // halo tiles: 8-row core groups of A are 8 pixels of one row (R = 1) or one 8-pixel row of a
     // 16 x 8 tile, i.e. (Wt + 2) pixel rows apart inside the halo box
-    const uint32_t sboA = HALO ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KC * 2u) : sbo;
+    const uint32_t sboA = HALO ? (g.R == 1 ? sbo : (uint32_t)(g.Wt + 2) * KB) : sbo;
     const uint64_t dA0 = make_sdesc(sA, sboA, layout);
     const uint64_t dB0 = make_sdesc(MODE == 1 ? sW : sB, sbo, layout);
+    const uint64_t loA = (uint64_t)((sAlo - sA) >> 4);                                   // A lo - A hi
+    const uint64_t loB = (uint64_t)(((MODE == 1 ? (uint32_t)nkb * b_stage : b_stage)) >> 4);  // B lo - B hi
     int s = 0, sb = 0;
     uint32_t ph = 0, phb = 0;
     int acc = 0;
     uint32_t aph = 0;
     if (MODE == 1) mbar_wait(wfull, 0);
-    const uint32_t hrow = (uint32_t)KC * 2u;  // bytes per halo pixel row
+    auto mma_k = [&](uint32_t d_tmem, uint64_t ad, uint64_t bd, uint32_t first) {
+#pragma unroll
+      for (int k = 0; k < KB / 32; ++k) {
+        if (X3) {
+          mma_tf32_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (first | k) ? 1u : 0u);
+          mma_tf32_elect(d_tmem, ad + loA + 2u * k, bd + 2u * k, idesc, 1u);
+          mma_tf32_elect(d_tmem, ad + 2u * k, bd + loB + 2u * k, idesc, 1u);
+        } else {
+          mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (first | k) ? 1u : 0u);
+        }
+      }
+    };
     for (int L = t0; L < tot_it; L += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
       if (HALO) {
         for (int ch = 0; ch < g.nchunk; ++ch) {
-          mbar_wait(full0 + 8u * s, ph);
+          mbar_wait(ready0 + 8u * s, ph);
           tc_fence_after();
-          const uint64_t dh = dA0 + ((s * P.halo_stage) >> 4);
+          const uint64_t dh = dA0 + ((s * op_a) >> 4);
           for (int tap = 0; tap < 9; ++tap) {
             const uint32_t p0 = (uint32_t)((g.dh[tap] + 1) * (g.Wt + 2) + (g.dw[tap] + 1));
-            const uint64_t ad = dh + ((p0 * hrow) >> 4);
+            const uint64_t ad = dh + ((p0 * (uint32_t)KB) >> 4);
             uint64_t bd;
             if (STREAMB) {
               mbar_wait(fullB0 + 8u * sb, phb);
               tc_fence_after();
-              bd = dB0 + (((uint32_t)sb * b_stage) >> 4);
+              bd = dB0 + (((uint32_t)sb * bslot) >> 4);
             } else {
               bd = dB0 + (((uint32_t)(tap * g.nchunk + ch) * b_stage) >> 4);
             }
-#pragma unroll
-            for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (ch | tap | k) ? 1u : 0u);
+            mma_k(d_tmem, ad, bd, (uint32_t)(ch | tap));
             if (STREAMB) {
               mma_commit_elect(emptyB0 + 8u * sb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
@@ -514,11 +606,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         }
       } else {
         for (int kb = 0; kb < nkb; ++kb) {
-          mbar_wait(full0 + 8u * s, ph);
+          mbar_wait(ready0 + 8u * s, ph);
+          if (X3) mbar_wait(full0 + 8u * s, ph);  // the B boxes of the stage (same transaction)
           tc_fence_after();
-          const uint64_t ad = dA0 + ((s * a_stage) >> 4), bd = dB0 + ((s * b_stage) >> 4);
-#pragma unroll
-          for (int k = 0; k < KC / 16; ++k) mma_bf16_elect(d_tmem, ad + 2u * k, bd + 2u * k, idesc, (kb | k) ? 1u : 0u);
+          mma_k(d_tmem, dA0 + ((s * a_stage) >> 4), dB0 + ((s * bslot) >> 4), (uint32_t)kb);
           mma_commit_elect(empty0 + 8u * s);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
@@ -536,7 +627,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
     const int half = (warp - 2) >> 2;
     const int row = quad * 32 + lane;
     const bool qleader = (half == 0 && lane == 0);
-    const uint32_t rowbytes = (uint32_t)BOXC * 2u;
     const int cbeg = half * (BN >> 1), cend = cbeg + (BN >> 1);
     const bool slab_live = quad * 32 < g.R * g.Wt;
     // slab mode: 4 storers (one per quadrant); whole-tile mode (Wt neither a multiple nor a divisor
@@ -588,35 +678,50 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
         float v[16];
         tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
         const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
-        const int j0 = (c0 % BOXC) / 8;
+        constexpr int VPC = 16 / ES;               // values per 16-byte chunk
+        const int j0 = ((c0 % BOXC) * ES) >> 4;    // first chunk of these 16 columns in the row
 #pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const uint32_t a = epi_chunk_addr<BOXC>(box, row, j0 + q);
-          float o[8];
-          if (HAS_AUX) {
-            const uint4 u = ld_shared_v4(a);
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(h2[e]);
-              if (EPI == EPI_RESADD) {
-                o[2 * e] = v[q * 8 + 2 * e] + f.x;
-                o[2 * e + 1] = v[q * 8 + 2 * e + 1] + f.y;
-              } else {
-                o[2 * e] = v[q * 8 + 2 * e] * dsoftplus_from_act_fast(f.x);
-                o[2 * e + 1] = v[q * 8 + 2 * e + 1] * dsoftplus_from_act_fast(f.y);
-              }
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < 8; ++e)
-              o[e] = (EPI == EPI_SOFTPLUS) ? ((e & 1) ? softplus_poly_log(v[q * 8 + e]) : softplus_fast(v[q * 8 + e]))
-                                           : v[q * 8 + e];
-          }
+        for (int q = 0; q < ES; ++q) {             // 16 columns = ES chunks
+          const uint32_t a = epi_chunk_addr<BOXB>(box, row, j0 + q);
+          const float* vq = v + q * VPC;
           uint4 w;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+          if (X3) {
+            float o[4];
+            if (HAS_AUX) {
+              const uint4 u = ld_shared_v4(a);
+              const float f[4] = {__uint_as_float(u.x), __uint_as_float(u.y), __uint_as_float(u.z), __uint_as_float(u.w)};
 #pragma unroll
-          for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+              for (int e = 0; e < 4; ++e) o[e] = (EPI == EPI_RESADD) ? vq[e] + f[e] : vq[e] * dsoftplus_from_act(f[e]);
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e) o[e] = (EPI == EPI_SOFTPLUS) ? softplus_f(vq[e]) : vq[e];
+            }
+            w = make_uint4(__float_as_uint(o[0]), __float_as_uint(o[1]), __float_as_uint(o[2]), __float_as_uint(o[3]));
+          } else {
+            float o[8];
+            if (HAS_AUX) {
+              const uint4 u = ld_shared_v4(a);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(h2[e]);
+                if (EPI == EPI_RESADD) {
+                  o[2 * e] = vq[2 * e] + f.x;
+                  o[2 * e + 1] = vq[2 * e + 1] + f.y;
+                } else {
+                  o[2 * e] = vq[2 * e] * dsoftplus_from_act_fast(f.x);
+                  o[2 * e + 1] = vq[2 * e + 1] * dsoftplus_from_act_fast(f.y);
+                }
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                o[e] = (EPI == EPI_SOFTPLUS) ? ((e & 1) ? softplus_poly_log(vq[e]) : softplus_fast(vq[e])) : vq[e];
+            }
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+          }
           st_shared_v4(a, w);
         }
       }
@@ -634,7 +739,7 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
           if (slab_live) {
             for (int b = 0; b < nbox; ++b) {
               const int col = nt * BN + b * BOXC;
-              tma_store_5d(&tmSlab, ebuf + b * P.epi_box_bytes + (uint32_t)(quad * 32) * rowbytes, col % g.CB,
+              tma_store_5d(&tmSlab, ebuf + b * P.epi_box_bytes + (uint32_t)(quad * 32) * BOXB, col % g.CB,
                            w0 + sw, col / g.CB, h0 + sh, img);
             }
           }
@@ -835,7 +940,7 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
         __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&wv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(r[q * 8 + 2 * e], r[q * 8 + 2 * e + 1]);
-        st_shared_v4(epi_chunk_addr<NC>(so, tid, c0 / 8 + q), wv);
+        st_shared_v4(epi_chunk_addr<NC * 2>(so, tid, c0 / 8 + q), wv);
       }
     }
     tc_fence_before();
@@ -914,23 +1019,30 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
 
 struct TcPlan {
   const int* list_ptr;  // the solver's compacted active-image list (tile skipping)
-  CUtensorMap tmA, tmB, tmOut, tmAux, tmSlab;
+  CUtensorMap tmA, tmB, tmOut, tmAux, tmSlab, tmBlo;
   TcParams P;
-  int KC, epi, boxc, grid, halo;
+  int KB, epi, boxb, grid, halo;
+  bool x3;
   size_t smem;
 };
 
-static int tc_bn(const ConvGeom& g) { return g.ncols >= 128 ? 128 : g.ncols; }
+// N tile: up to 128 columns (bf16); 64 in 3xTF32 (fp32 staging and the hi / lo operand pairs
+// double every shared-memory buffer)
+static int tc_bn(const ConvGeom& g, bool x3) {
+  const int cap = x3 ? 64 : 128;
+  return g.ncols >= cap ? cap : g.ncols;
+}
 
-bool tc_supported(const ConvGeom& g) {
-  if (!(g.KC == 32 || g.KC == 64)) return false;
+bool tc_supported(const ConvGeom& g, bool x3) {
+  if (x3 ? g.KC != 32 : !(g.KC == 32 || g.KC == 64)) return false;
   if (g.R * g.Wt > 128 || g.Wt > 256 || g.R > 256) return false;
+  if (x3 && g.epi == EPI_IMG) return false;  // the fp32 mode's head / tail run on the FFMA path
   // EPI_IMG (tail / head adjoint: C <= 3 image columns) runs with N = 16; its epilogue writes
   // fp32 planes from registers and never uses the smem boxes / store maps
   if (g.epi == EPI_IMG ? (g.ncols != 16 && g.ncols != 32) : (g.ncols % 32 != 0)) return false;
-  const int BN = tc_bn(g);
+  const int BN = tc_bn(g, x3);
   if (g.ncols % BN != 0) return false;
-  const int boxc = BN >= 64 ? 64 : 32;
+  const int boxc = x3 ? 32 : (BN >= 64 ? 64 : 32);
   if (g.epi != EPI_IMG && (g.CB % boxc != 0 || g.OCp % 8 != 0)) return false;
   if ((g.inC * 2) % 16 != 0) return false;
   if (g.OHo % g.osh != 0) return false;
@@ -940,37 +1052,52 @@ bool tc_supported(const ConvGeom& g) {
 // Halo variants: 3x3 taps (|dh|,|dw| <= 1, no parity planes) on tiles whose 8-row core groups
 // sit at a uniform stride inside the halo box: 16 x 8 pixels (preferred: 1.4x halo) or one row of
 // 128 pixels. Returns 0 (plain), 1 (resident weights) or 2 (streamed weights) and the tile shape.
-static int tc_halo_mode(const ConvGeom& g, int& R, int& Wt) {
+static int tc_halo_mode(const ConvGeom& g, bool x3, int& R, int& Wt) {
   if (g.ntaps != 9 || g.inP != 1) return 0;
   for (int t = 0; t < 9; ++t)
     if (g.dp[t] != 0 || g.dh[t] < -1 || g.dh[t] > 1 || g.dw[t] < -1 || g.dw[t] > 1) return 0;
   if (g.OW % 8 == 0) { R = 16; Wt = 8; }
   else if (g.R == 1 && g.Wt == 128) { R = 1; Wt = 128; }
   else return 0;
-  const int BN = tc_bn(g);
-  const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * 2;
+  const int BN = tc_bn(g, x3);
+  const size_t wbytes = (size_t)9 * g.nchunk * BN * g.KC * (x3 ? 8 : 2);  // hi (+ lo)
   if (g.ncols == BN && wbytes <= 80 * 1024) return 1;
   return 2;
 }
 
-// 5-D view (c, w, p, h, n) of an NHWC bf16 tensor: dims {C, W, P, H, N} (P parity planes interleaved in h)
-static CUresult encode5(EncodeTiledFn enc, CUtensorMap* m, const void* ptr, int C, int W, int P, int H, int N,
+// 5-D view (c, w, p, h, n) of an NHWC tensor of es-byte elements: dims {C, W, P, H, N} (P parity
+// planes interleaved in h)
+static CUresult encode5(EncodeTiledFn enc, CUtensorMap* m, const void* ptr, int es, int C, int W, int P, int H, int N,
                         int boxc, int boxw, int boxh, CUtensorMapSwizzle sw) {
   cuuint64_t dims[5] = {(cuuint64_t)C, (cuuint64_t)W, (cuuint64_t)P, (cuuint64_t)H, (cuuint64_t)N};
   cuuint64_t strides[4];
-  strides[0] = (cuuint64_t)C * 2;
+  strides[0] = (cuuint64_t)C * es;
   strides[1] = strides[0] * W;
   strides[2] = strides[1] * P;
   strides[3] = strides[2] * H;
   cuuint32_t box[5] = {(cuuint32_t)boxc, (cuuint32_t)boxw, 1u, (cuuint32_t)boxh, 1u};
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint32_t es5[5] = {1, 1, 1, 1, 1};
+  return enc(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(ptr),
+             dims, strides, box, es5, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
-                     const __nv_bfloat16* aux, int num_sms, char* err, size_t errlen) {
-  if (!tc_supported(g_in)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
+static CUresult encode_w(EncodeTiledFn enc, CUtensorMap* m, const void* w, int es, const ConvGeom& g, int BN,
+                         CUtensorMapSwizzle sw) {
+  const int nkb = g.ntaps * g.nchunk;
+  cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
+  cuuint64_t strides[2] = {(cuuint64_t)g.KC * es, (cuuint64_t)g.KC * es * g.ncols};
+  cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
+  cuuint32_t e3[3] = {1, 1, 1};
+  return enc(m, es == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(w),
+             dims, strides, box, e3, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+TcPlan* tc_make_plan(const ConvGeom& g_in, bool x3, const void* in, const void* wB, const void* wBlo, void* out,
+                     const void* aux, int num_sms, char* err, size_t errlen) {
+  if (!tc_supported(g_in, x3)) { snprintf(err, errlen, "tcgen05 conv: unsupported geometry"); return nullptr; }
+  if (x3 && !wBlo) { snprintf(err, errlen, "3xTF32 conv needs the lo weights"); return nullptr; }
   ConvGeom g = g_in;
   EncodeTiledFn enc = get_encode();
   if (!enc) { snprintf(err, errlen, "cuTensorMapEncodeTiled unavailable"); return nullptr; }
@@ -978,34 +1105,30 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   if (has_aux && !aux) { snprintf(err, errlen, "epilogue needs an aux tensor"); return nullptr; }
   TcPlan* p = new TcPlan();
   memset(p, 0, sizeof(TcPlan));
-  p->KC = g.KC;
+  const int es = x3 ? 4 : 2;
+  const int nbuf = x3 ? 2 : 1;
+  p->x3 = x3;
+  p->KB = g.KC * es;
   p->epi = g.epi;
-  const int BN = tc_bn(g);
-  const int boxc = BN >= 64 ? 64 : 32;
-  p->boxc = boxc;
-  const CUtensorMapSwizzle swA = g.KC == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
-  const CUtensorMapSwizzle swE = boxc == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const int BN = tc_bn(g, x3);
+  const int boxc = x3 ? 32 : (BN >= 64 ? 64 : 32);
+  p->boxb = boxc * es;
+  const CUtensorMapSwizzle swA = p->KB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  const CUtensorMapSwizzle swE = p->boxb == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
   int hR = g.R, hW = g.Wt;
-  p->halo = tc_halo_mode(g, hR, hW);
+  p->halo = tc_halo_mode(g, x3, hR, hW);
   if (p->halo) {  // halo tiles may re-shape the M tile (16 x 8 pixels)
     g.R = hR;
     g.Wt = hW;
     g.tiles_h = (g.OH + g.R - 1) / g.R;
     g.tiles_w = (g.OW + g.Wt - 1) / g.Wt;
   }
-  CUresult r = p->halo ? encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
-                       : encode5(enc, &p->tmA, in, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
+  CUresult r = p->halo ? encode5(enc, &p->tmA, in, es, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt + 2, g.R + 2, swA)
+                       : encode5(enc, &p->tmA, in, es, g.inC, g.inW, g.inP, g.inH, g.N, g.KC, g.Wt, g.R, swA);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map A encode failed (%d)", (int)r); delete p; return nullptr; }
-  {
-    const int nkb = g.ntaps * g.nchunk;
-    cuuint64_t dims[3] = {(cuuint64_t)g.KC, (cuuint64_t)g.ncols, (cuuint64_t)nkb};
-    cuuint64_t strides[2] = {(cuuint64_t)g.KC * 2, (cuuint64_t)g.KC * 2 * g.ncols};
-    cuuint32_t box[3] = {(cuuint32_t)g.KC, (cuuint32_t)BN, 1u};
-    cuuint32_t es[3] = {1, 1, 1};
-    r = enc(&p->tmB, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<__nv_bfloat16*>(wB), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, swA, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map B encode failed (%d)", (int)r); delete p; return nullptr; }
-  }
+  r = encode_w(enc, &p->tmB, wB, es, g, BN, swA);
+  if (r == CUDA_SUCCESS) r = encode_w(enc, &p->tmBlo, x3 ? wBlo : wB, es, g, BN, swA);
+  if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map B encode failed (%d)", (int)r); delete p; return nullptr; }
   const int slab_mode = (g.Wt % 32 == 0 || 32 % g.Wt == 0) ? 1 : 0;
   if (g.epi == EPI_IMG) {  // no smem-staged output: the store / aux / slab maps are never used
     p->tmOut = p->tmA;
@@ -1014,10 +1137,10 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   } else {
     // output / aux: 5-D view (CB, OWo, osh, OHo/osh, N) -- plain NHWC store (osh = 1) or the
     // 2x2 pixel scatter of the transposed / adjoint strided convs (osh = 2, CB = 2 x channels)
-    r = encode5(enc, &p->tmOut, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+    r = encode5(enc, &p->tmOut, out, es, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
     if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map out encode failed (%d)", (int)r); delete p; return nullptr; }
     if (has_aux) {
-      r = encode5(enc, &p->tmAux, aux, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
+      r = encode5(enc, &p->tmAux, aux, es, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, g.Wt, g.R, swE);
       if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map aux encode failed (%d)", (int)r); delete p; return nullptr; }
     } else {
       p->tmAux = p->tmOut;
@@ -1026,7 +1149,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
     // 32 / Wt whole rows. Used when Wt is a multiple or a divisor of 32.
     if (slab_mode) {
       const int sw = g.Wt >= 32 ? 32 : g.Wt, sh = g.Wt >= 32 ? 1 : 32 / g.Wt;
-      r = encode5(enc, &p->tmSlab, out, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, sw, sh, swE);
+      r = encode5(enc, &p->tmSlab, out, es, g.CB, g.OWo, g.osh, g.OHo / g.osh, g.N, boxc, sw, sh, swE);
       if (r != CUDA_SUCCESS) { snprintf(err, errlen, "tensor map slab encode failed (%d)", (int)r); delete p; return nullptr; }
     } else {
       p->tmSlab = p->tmOut;
@@ -1041,25 +1164,26 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.fd_ntiles.init((uint32_t)P.n_tiles);
   P.fd_perimg.init((uint32_t)(g.tiles_h * g.tiles_w));
   P.fd_tw.init((uint32_t)g.tiles_w);
-  P.a_bytes = (uint32_t)g.KC * 2u * g.Wt * g.R;
-  P.b_bytes = (uint32_t)g.KC * 2u * BN;
-  P.epi_box_bytes = 128u * (uint32_t)boxc * 2u;
-  P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)boxc * 2u * g.Wt * g.R;
+  P.a_bytes = (uint32_t)p->KB * g.Wt * g.R;
+  P.b_bytes = (uint32_t)p->KB * BN;
+  P.epi_box_bytes = 128u * (uint32_t)p->boxb;
+  P.epi_tx_bytes = (uint32_t)(BN / boxc) * (uint32_t)p->boxb * g.Wt * g.R;
   // Shared-memory / TMEM plan. Preference order: deep accumulator rings for narrow N (more tiles
   // in flight hide the per-tile epilogue latency: 8 stages for the 32-column halo layers measured
-  // +0.3..1.6% over 4, 2 stages -22%), then 2 CTAs per SM, then deeper operand rings.
-  const size_t a_stage = 128u * g.KC * 2u, b_stage = (size_t)BN * g.KC * 2u, e_stage = (size_t)BN * 128u * 2u;
-  const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * b_stage : 0;
+  // +0.3..1.6% over 4, 2 stages -22%), then 2 CTAs per SM (bf16), then deeper operand rings.
+  const size_t a_stage = 128u * (size_t)p->KB, b_stage = (size_t)BN * p->KB, bslot = b_stage * nbuf,
+               e_stage = (size_t)BN * 128u * es;
+  const size_t wbytes = p->halo == 1 ? (size_t)9 * g.nchunk * bslot : 0;
   if (p->halo) {
-    P.a_bytes = (uint32_t)g.KC * 2u * (g.Wt + 2) * (g.R + 2);
+    P.a_bytes = (uint32_t)p->KB * (g.Wt + 2) * (g.R + 2);
     P.halo_stage = (P.a_bytes + 1023u) & ~1023u;
   }
-  // MODE 2: a weight ring of SB stages (one (chunk, tap) box each) next to the halo ring
-  const int SBq = 6;
+  // MODE 2: a weight ring of SB slots (one (chunk, tap) box pair each) next to the halo ring
+  const int SBq = x3 ? 3 : 6;
   const bool streamb = p->halo == 2;
-  const size_t bring = streamb ? (size_t)SBq * b_stage : 0;
+  const size_t bring = streamb ? (size_t)SBq * bslot : 0;
   P.stagesB = streamb ? SBq : 0;
-  const size_t op_stage = p->halo ? (size_t)P.halo_stage : a_stage + b_stage;
+  const size_t op_stage = p->halo ? (size_t)P.halo_stage * nbuf : a_stage * nbuf + bslot;
   // short-K layers (the 2x2 up / down scatters: 1-2 K-blocks per tile) are bound by the per-tile
   // epilogue round trip (aux load, store), so they take 4 accumulator/epilogue stages and only the
   // operand stages one tile needs
@@ -1070,11 +1194,12 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   uint32_t tcols = 0;
   const uint32_t acc_w = (uint32_t)BN;  // TMEM columns per stage
   const int na0 = (8 * acc_w <= 256 && p->halo) ? 8 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
+  const size_t nbar = 64 * 8 + 64;  // barriers and the TMEM holder
   for (int na = na0; na >= 2 && !stages; na -= 2) {
     uint32_t tc = 32;
     while (tc < (uint32_t)na * acc_w) tc <<= 1;
-    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + 512;
-    for (int c = 2; c >= 1 && !stages; --c) {
+    const size_t fixed = 1024 + (size_t)na * e_stage + wbytes + bring + nbar;
+    for (int c = x3 ? 1 : 2; c >= 1 && !stages; --c) {
       const size_t avail = c == 2 ? (227 * 1024) / 2 - 1024 : 220 * 1024;
       if (tc * c > 512 || avail <= fixed) continue;
       int st = (int)((avail - fixed) / op_stage);
@@ -1086,7 +1211,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
   P.stages = stages;
   P.nacc = nacc;
   P.tmem_cols = tcols;
-  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + 512 + (size_t)stages * op_stage;
+  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + nbar + (size_t)stages * op_stage;
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
@@ -1095,11 +1220,11 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, const __nv_bfloat16* in, const __nv_b
 
 // Every conv launch carries the programmatic-stream-serialization attribute (PDL): it may start
 // while its predecessor drains; the kernel waits (griddepcontrol.wait) before reading activations.
-template <int KC, int EPI, int BOXC>
+template <int KB, int EPI, int BOXB, bool X3>
 static void launch_one(const TcPlan* p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p->grid);
-  cfg.blockDim = dim3(TC_THREADS);
+  cfg.blockDim = dim3(X3 ? TC_THREADS_X3 : TC_THREADS);
   cfg.dynamicSmemBytes = p->smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -1108,20 +1233,20 @@ static void launch_one(const TcPlan* p, cudaStream_t s) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   switch (p->halo) {
-    case 1: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 1>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
-    case 2: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 2>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
-    default: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KC, EPI, BOXC, 0>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->P); break;
+    case 1: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KB, EPI, BOXB, 1, X3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->tmBlo, p->P); break;
+    case 2: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KB, EPI, BOXB, 2, X3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->tmBlo, p->P); break;
+    default: cudaLaunchKernelEx(&cfg, conv_tc_kernel<KB, EPI, BOXB, 0, X3>, p->tmA, p->tmB, p->tmOut, p->tmAux, p->tmSlab, p->tmBlo, p->P); break;
   }
 }
 
-template <int KC, int BOXC>
+template <int KB, int BOXB, bool X3>
 static void launch_epi(const TcPlan* p, cudaStream_t s) {
   switch (p->epi) {
-    case EPI_SOFTPLUS: launch_one<KC, EPI_SOFTPLUS, BOXC>(p, s); break;
-    case EPI_RESADD: launch_one<KC, EPI_RESADD, BOXC>(p, s); break;
-    case EPI_SIGMUL: launch_one<KC, EPI_SIGMUL, BOXC>(p, s); break;
-    case EPI_IMG: launch_one<KC, EPI_IMG, BOXC>(p, s); break;
-    default: launch_one<KC, EPI_STORE, BOXC>(p, s); break;
+    case EPI_SOFTPLUS: launch_one<KB, EPI_SOFTPLUS, BOXB, X3>(p, s); break;
+    case EPI_RESADD: launch_one<KB, EPI_RESADD, BOXB, X3>(p, s); break;
+    case EPI_SIGMUL: launch_one<KB, EPI_SIGMUL, BOXB, X3>(p, s); break;
+    case EPI_IMG: if constexpr (!X3) launch_one<KB, EPI_IMG, BOXB, X3>(p, s); break;
+    default: launch_one<KB, EPI_STORE, BOXB, X3>(p, s); break;
   }
 }
 
@@ -1145,10 +1270,12 @@ void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int
 }
 
 void tc_launch(const TcPlan* p, cudaStream_t s) {
-  if (p->KC == 64) {
-    if (p->boxc == 64) launch_epi<64, 64>(p, s); else launch_epi<64, 32>(p, s);
+  if (p->x3) {
+    launch_epi<128, 128, true>(p, s);
+  } else if (p->KB == 128) {
+    if (p->boxb == 128) launch_epi<128, 128, false>(p, s); else launch_epi<128, 64, false>(p, s);
   } else {
-    if (p->boxc == 64) launch_epi<32, 64>(p, s); else launch_epi<32, 32>(p, s);
+    if (p->boxb == 128) launch_epi<64, 128, false>(p, s); else launch_epi<64, 64, false>(p, s);
   }
 }
 
@@ -1156,30 +1283,30 @@ int tc_plan_is_halo(const TcPlan* p) { return p->halo; }
 
 void tc_free_plan(TcPlan* p) { delete p; }
 
-template <int KC, int BOXC, int HALO>
+template <int KB, int BOXB, int HALO, bool X3>
 static void attrs_epi() {
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_STORE, BOXC, HALO>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SOFTPLUS, BOXC, HALO>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_RESADD, BOXC, HALO>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_SIGMUL, BOXC, HALO>);
-  set_max_dyn_smem(conv_tc_kernel<KC, EPI_IMG, BOXC, HALO>);
+  set_max_dyn_smem(conv_tc_kernel<KB, EPI_STORE, BOXB, HALO, X3>);
+  set_max_dyn_smem(conv_tc_kernel<KB, EPI_SOFTPLUS, BOXB, HALO, X3>);
+  set_max_dyn_smem(conv_tc_kernel<KB, EPI_RESADD, BOXB, HALO, X3>);
+  set_max_dyn_smem(conv_tc_kernel<KB, EPI_SIGMUL, BOXB, HALO, X3>);
+  if constexpr (!X3) set_max_dyn_smem(conv_tc_kernel<KB, EPI_IMG, BOXB, HALO, X3>);
+}
+
+template <int HALO>
+static void attrs_mode() {
+  attrs_epi<128, 128, HALO, false>();
+  attrs_epi<128, 64, HALO, false>();
+  attrs_epi<64, 128, HALO, false>();
+  attrs_epi<64, 64, HALO, false>();
+  attrs_epi<128, 128, HALO, true>();
 }
 
 void init_attrs_tc() {
   set_max_dyn_smem(img2feat_tc_kernel<32>);
   set_max_dyn_smem(img2feat_tc_kernel<64>);
-  attrs_epi<64, 64, 0>();
-  attrs_epi<64, 32, 0>();
-  attrs_epi<32, 64, 0>();
-  attrs_epi<32, 32, 0>();
-  attrs_epi<64, 64, 1>();
-  attrs_epi<64, 32, 1>();
-  attrs_epi<32, 64, 1>();
-  attrs_epi<32, 32, 1>();
-  attrs_epi<64, 64, 2>();
-  attrs_epi<64, 32, 2>();
-  attrs_epi<32, 64, 2>();
-  attrs_epi<32, 32, 2>();
+  attrs_mode<0>();
+  attrs_mode<1>();
+  attrs_mode<2>();
 }
 
 }  // namespace ideq

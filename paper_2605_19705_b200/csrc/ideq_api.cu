@@ -81,6 +81,12 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// The network program for one micro-batch size: forward then VJP launches, in order.
+struct Program {
+  std::vector<Layer> layers;
+  int n_fwd = 0;
+};
+
 }  // namespace
 
 struct ideq_ctx {
@@ -107,9 +113,20 @@ struct ideq_ctx {
   // feature buffers: per level 3 work buffers; saved activations
   std::vector<std::vector<void*>> lvl_buf;  // [level][3]
   std::map<std::string, void*> saved;
-  int prog_batch = -1;
-  std::vector<Layer> prog;  // forward then VJP
+  // network programs keyed by micro-batch size (the full micro-batch and a smaller last one);
+  // `prog` is the build target of build_program
+  std::map<int, Program> progs;
+  std::vector<Layer> prog;
   int n_fwd = 0;
+  // workspace plan: the network's activations are allocated for `mb` images (the micro-batch);
+  // the solver state (iterates, gradients, operator data) for every image of a solve
+  int mb = 0;
+  size_t net_bytes = 0;
+  // the last solve's step arguments (class timing replays its kernels)
+  bool have_last = false;
+  int last_N = 0;
+  StepArgs last_a{};
+  FinalizeArgs last_f{};
 
   // solver buffers (fp32 NCHW)
   float *X1 = nullptr, *Z = nullptr, *G = nullptr, *Hc = nullptr, *fbuf = nullptr, *fbuf2 = nullptr;
@@ -159,6 +176,8 @@ struct ideq_ctx {
 
   // profiling
   bool profiling = false;
+  bool counting = false;  // class timing: Prof adds each launch's algorithmic work to cnt_*
+  double cnt_flops[IDEQ_K_NCLASSES] = {0}, cnt_bytes[IDEQ_K_NCLASSES] = {0};
   bool skip_frozen = false;  // current solve may freeze images early: kernels skip their work
   ideq_profile prof{};
   struct Ev { cudaEvent_t a, b; int cls; double flops, bytes; };
@@ -330,14 +349,37 @@ std::vector<float> flip_transpose3x3(const float* Wt, int o_n, int i_n) {
   return F;
 }
 
-// K-block width: the tcgen05 path stages 32/64 channels (64B/128B swizzle rows); the
-// FFMA path walks 16 channels at a time.
-int pick_kc(bool tc, int ktap) {
-  if (tc) return (ktap % 64 == 0) ? 64 : 32;
+// K-block width: the bf16 tcgen05 path stages 32/64 channels (64B/128B swizzle rows), the 3xTF32
+// path 32 fp32 channels (128B rows); the FFMA path walks 16 channels at a time.
+int pick_kc(bool tc, bool x3, int ktap) {
+  if (tc) return x3 ? 32 : ((ktap % 64 == 0) ? 64 : 32);
   return 16;
 }
+int pick_kc(bool tc, int ktap) { return pick_kc(tc, false, ktap); }
 
-bool use_tc(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_BF16 && ctx->net.arch == IDEQ_NET_UNET4; }
+// The U-Net's convolutions run on tcgen05 in both precisions: bf16 operands (headline) or fp32
+// operands as 3xTF32 (the parity mode, every width a multiple of 32). The C <-> w0 head / tail
+// run on tcgen05 in bf16 and on the FFMA path in fp32; the tiny C1 net is FFMA.
+bool use_tc(ideq_ctx* ctx) {
+  if (ctx->net.arch != IDEQ_NET_UNET4) return false;
+  if (ctx->prec == IDEQ_PREC_BF16) return true;
+  for (int l = 0; l < 4; ++l)
+    if (ctx->net.widths[l] % 32) return false;
+  return true;
+}
+bool use_x3(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_FP32 && use_tc(ctx); }
+bool use_tc_headtail(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_BF16 && use_tc(ctx); }
+
+// 3xTF32 operand split on the host: hi = w rounded to tf32 (round to nearest, ties away from zero,
+// as cvt.rna.tf32.f32), lo = w - hi (exact in fp32).
+float tf32_rna(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  memcpy(&r, &u, 4);
+  return r;
+}
 
 ideq_status upload_gemm_weights(ideq_ctx* ctx, const std::string& key, const std::vector<float>& B) {
   void* d = nullptr;
@@ -440,9 +482,20 @@ ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, c
   else { ncols = 4 * shp[1]; ktap = shp[0]; }
   const int cin_tensor = (kind == 2 || kind == 5) ? ktap / 2 : ktap;
   L.tc = use_tc(ctx);
-  const int KC = kind == 6 ? 32 : pick_kc(L.tc, ktap);
+  const bool x3 = L.tc && ctx->prec == IDEQ_PREC_FP32;
+  const int KC = kind == 6 ? 32 : pick_kc(L.tc, x3, ktap);
   if (!ctx->wdev.count(key)) {
     std::vector<float> B = gemm_weights(kind, Wt, shp, KC, ncols, ntaps, ktap);
+    if (x3) {  // tf32 hi / lo halves
+      std::vector<float> lo(B.size());
+      for (size_t i = 0; i < B.size(); ++i) {
+        const float h = tf32_rna(B[i]);
+        lo[i] = B[i] - h;
+        B[i] = h;
+      }
+      ideq_status st = upload_gemm_weights(ctx, key + "#lo", lo);
+      if (st) return st;
+    }
     ideq_status st = upload_gemm_weights(ctx, key, B);
     if (st) return st;
   }
@@ -458,10 +511,10 @@ ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, c
   L.bytes = ctx->elt * (in_elems + out_elems * ((L.g.epi == EPI_RESADD || L.g.epi == EPI_SIGMUL) ? 2.0 : 1.0)) +
             ctx->elt * (double)ncols * L.g.ntaps * ktap;
   if (L.tc) {
-    if (!tc_supported(L.g)) return fail(ctx, IDEQ_E_UNSUPPORTED, "layer %s: geometry not supported by tcgen05 path", lname.c_str());
+    if (!tc_supported(L.g, x3)) return fail(ctx, IDEQ_E_UNSUPPORTED, "layer %s: geometry not supported by tcgen05 path", lname.c_str());
     char err[256] = {0};
-    L.plan = tc_make_plan(L.g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)L.wB, (__nv_bfloat16*)out,
-                          (const __nv_bfloat16*)aux, ctx->num_sms, err, sizeof(err));
+    L.plan = tc_make_plan(L.g, x3, in, L.wB, x3 ? ctx->wdev[key + "#lo"] : nullptr, out, aux, ctx->num_sms, err,
+                          sizeof(err));
     if (!L.plan) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
     tc_plan_set_active(L.plan, ctx->act_list, ctx->n_active);  // frozen images cost nothing
   }
@@ -611,10 +664,24 @@ std::string rb(const char* p, int l, int r, const char* ab) {
 }
 
 // Build the forward + VJP program for batch N (buffers sized for maxN at create).
+ideq_status build_program_impl(ideq_ctx* ctx, int N);
 ideq_status build_program(ideq_ctx* ctx, int N) {
-  if (ctx->prog_batch == N) return IDEQ_OK;
-  for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
+  if (ctx->progs.count(N)) return IDEQ_OK;
   ctx->prog.clear();
+  ideq_status st = build_program_impl(ctx, N);
+  if (st) {
+    for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
+    ctx->prog.clear();
+    return st;
+  }
+  Program& P = ctx->progs[N];
+  P.layers.swap(ctx->prog);
+  P.n_fwd = ctx->n_fwd;
+  ctx->graph_key.clear();
+  return IDEQ_OK;
+}
+
+ideq_status build_program_impl(ideq_ctx* ctx, int N) {
   const auto& n = ctx->net;
   const int C = ctx->C;
   ideq_status st;
@@ -644,7 +711,7 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
     int Hl[4], Wl[4];
     for (int l = 0; l < 4; ++l) { Hl[l] = ctx->H >> l; Wl[l] = ctx->W >> l; }
     auto B = [&](int l, int i) { return ctx->lvl_buf[l][i]; };
-    const bool tc = use_tc(ctx);
+    const bool tc = use_tc_headtail(ctx);
     const float* skip_aux_z = n.identity_skip ? nullptr : ctx->Z;
     const float* skip_aux_c = n.identity_skip ? nullptr : ctx->Hc;
     const float skip_alpha = n.identity_skip ? 0.f : -1.f;
@@ -744,8 +811,6 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
                            skip_alpha, EPI_STORE, "headT");
     if (st) return st;
   }
-  ctx->prog_batch = N;
-  ctx->graph_key.clear();
   return IDEQ_OK;
 }
 
@@ -765,6 +830,7 @@ struct Prof {
   double flops, bytes;
   cudaEvent_t a = nullptr;
   Prof(ideq_ctx* c, int k, double f = 0, double b = 0) : ctx(c), cls(k), flops(f), bytes(b) {
+    if (ctx->counting) { ctx->cnt_flops[k] += f; ctx->cnt_bytes[k] += b; }
     if (ctx->profiling) { a = next_event(ctx); cudaEventRecord(a, ctx->stream); }
   }
   ~Prof() {
@@ -791,17 +857,22 @@ void collect_profile(ideq_ctx* ctx) {
   ctx->ev_used = 0;
 }
 
-void run_layer(ideq_ctx* ctx, const Layer& L) {
+// `off` = first image of the micro-batch x (C*H*W): the head / tail layers read and write the
+// solver's image planes of those images; every other layer works in the network workspace.
+void run_layer(ideq_ctx* ctx, const Layer& L, long long off) {
   cudaStream_t s = ctx->stream;
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
+  auto sh = [off](const float* p) { return p ? p + off : p; };
+  auto shw = [off](float* p) { return p ? p + off : p; };
   if (L.kind == L_IMG2FEAT_TC) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
-    launch_img2feat_tc(L.i2f, L.in_img, (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->act_list : nullptr,
+    launch_img2feat_tc(L.i2f, sh(L.in_img), (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->act_list : nullptr,
                        ctx->n_active,
                        L.N, L.C, L.H, L.W, L.wfeat, ctx->num_sms, s);
   } else if (L.kind == L_GEMM) {
     if (L.tc) {
       Prof p(ctx, L.headtail ? IDEQ_K_HEADTAIL : IDEQ_K_CONV_TC, L.flops, L.bytes);
+      if (L.out_img) tc_plan_set_image(L.plan, shw(L.out_img), sh(L.aux_img), L.alpha, ctx->C);
       tc_launch(L.plan, s);
     } else {
       Prof p(ctx, IDEQ_K_CONV_SIMT, L.flops, L.bytes);
@@ -814,24 +885,55 @@ void run_layer(ideq_ctx* ctx, const Layer& L) {
   } else if (L.kind == L_IMG2FEAT) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
     if (bf)
-      launch_img2feat<__nv_bfloat16>(L.in_img, (const float*)L.wB, (__nv_bfloat16*)L.out, (const __nv_bfloat16*)L.aux,
-                                     L.epi, L.N, L.C, L.H, L.W, L.wfeat, s);
+      launch_img2feat<__nv_bfloat16>(sh(L.in_img), (const float*)L.wB, (__nv_bfloat16*)L.out,
+                                     (const __nv_bfloat16*)L.aux, L.epi, L.N, L.C, L.H, L.W, L.wfeat, s);
     else
-      launch_img2feat<float>(L.in_img, (const float*)L.wB, (float*)L.out, (const float*)L.aux, L.epi, L.N, L.C, L.H,
-                             L.W, L.wfeat, s);
+      launch_img2feat<float>(sh(L.in_img), (const float*)L.wB, (float*)L.out, (const float*)L.aux, L.epi, L.N, L.C,
+                             L.H, L.W, L.wfeat, s);
   } else {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
     if (bf)
-      launch_feat2img<__nv_bfloat16>((const __nv_bfloat16*)L.in, (const float*)L.wB, L.out_img, L.aux_img, L.alpha,
-                                     L.N, L.C, L.H, L.W, L.wfeat, s);
+      launch_feat2img<__nv_bfloat16>((const __nv_bfloat16*)L.in, (const float*)L.wB, shw(L.out_img), sh(L.aux_img),
+                                     L.alpha, L.N, L.C, L.H, L.W, L.wfeat, s);
     else
-      launch_feat2img<float>((const float*)L.in, (const float*)L.wB, L.out_img, L.aux_img, L.alpha, L.N, L.C, L.H,
-                             L.W, L.wfeat, s);
+      launch_feat2img<float>((const float*)L.in, (const float*)L.wB, shw(L.out_img), sh(L.aux_img), L.alpha, L.N,
+                             L.C, L.H, L.W, L.wfeat, s);
   }
 }
 
-void run_network(ideq_ctx* ctx) {
-  for (const auto& L : ctx->prog) run_layer(ctx, L);
+// Kernel-class filter of run_network: -1 = every layer (the iteration); otherwise only the layers
+// of that ideq_kernel_class (class timing).
+int layer_class(const Layer& L) {
+  if (L.kind == L_GEMM && L.tc && !L.headtail) return IDEQ_K_CONV_TC;
+  if (L.kind == L_GEMM && !L.tc) return IDEQ_K_CONV_SIMT;
+  return IDEQ_K_HEADTAIL;
+}
+
+// U_theta and its VJP for images [0, N): one pass of the program per micro-batch of <= mb images
+// (the programs are built by prepare_programs before any capture).
+void run_network(ideq_ctx* ctx, int N, int cls = -1) {
+  const long long d = (long long)ctx->C * ctx->H * ctx->W;
+  for (int first = 0; first < N; first += ctx->mb) {
+    const int n = N - first < ctx->mb ? N - first : ctx->mb;
+    const Program& P = ctx->progs.at(n);
+    for (const auto& L : P.layers)
+      if (cls < 0 || layer_class(L) == cls) run_layer(ctx, L, first * d);
+  }
+}
+
+ideq_status prepare_programs(ideq_ctx* ctx, int N) {
+  ideq_status st;
+  const int n_full = N < ctx->mb ? N : ctx->mb;
+  if ((st = build_program(ctx, n_full))) return st;
+  if (N > ctx->mb && N % ctx->mb && (st = build_program(ctx, N % ctx->mb))) return st;
+  return IDEQ_OK;
+}
+
+// The live-image list indexes images of the batch: used when one network pass covers the batch.
+void enable_skip(ideq_ctx* ctx, bool on) {
+  for (auto& kv : ctx->progs)
+    for (auto& L : kv.second.layers)
+      if (L.plan) tc_plan_enable_skip(L.plan, on);
 }
 
 // ------------------------------------------------------------------ fidelity + step
@@ -880,7 +982,9 @@ void run_step(ideq_ctx* ctx, const StepArgs& a0) {
   cudaStream_t s = ctx->stream;
   const auto& op = ctx->op;
   if (op.kind == IDEQ_OP_INPAINT) {
-    Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 7.0);
+    // reads z, grad g, x^k, y (fp32) and the u8 mask (one byte per pixel, shared by the C channels);
+    // writes x^{k+1}, z^{k+1}
+    Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * (24.0 + 1.0 / a.C));
     launch_pointwise_step(op.step == IDEQ_STEP_PROX ? STEP_PROX_INPAINT : STEP_GRAD_INPAINT, a, s);
   } else if (op.kind == IDEQ_OP_RICIAN) {
     Prof p(ctx, IDEQ_K_STEP, 0, (double)a.N * a.d * 4.0 * 6.0);
@@ -985,7 +1089,7 @@ FinalizeArgs make_fin(ideq_ctx* ctx, int N, const ideq_params* p) {
 
 // One iteration: network (forward + VJP), fidelity + update + partials, finalize, advance.
 ideq_status enqueue_iteration(ideq_ctx* ctx, const StepArgs& a, const FinalizeArgs& f, bool with_allreduce) {
-  run_network(ctx);
+  run_network(ctx, a.N);
   run_step(ctx, a);
   {
     Prof p(ctx, IDEQ_K_REDUCE);
@@ -1052,7 +1156,7 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if ((st = validate_params(ctx, N, p))) return st;
   if ((st = operator_runnable(ctx))) return st;
   if (!y || !x || !stats) return fail(ctx, IDEQ_E_INVALID, "NULL y/x/stats");
-  if ((st = build_program(ctx, N))) return st;
+  if ((st = prepare_programs(ctx, N))) return st;
   const long long d = (long long)ctx->C * ctx->H * ctx->W;
   cudaStream_t s = ctx->stream;
   // x^{-1} = x^0; z^0 = x^0
@@ -1065,9 +1169,14 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   if (ctx->op.kind == IDEQ_OP_BLUR && ctx->op.step == IDEQ_STEP_PROX) prepare_blur_prox(ctx, y, p->tau, N);
   if (ctx->op.kind == IDEQ_OP_MRI) prepare_mri(ctx, y, p->tau, N);
   StepArgs a = make_step_args(ctx, N, y, x, p);
-  ctx->skip_frozen = p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE && !p->compute_frozen;
-  for (auto& L : ctx->prog)  // skip frozen images' tiles only when images can freeze early
-    if (L.plan) tc_plan_enable_skip(L.plan, ctx->skip_frozen);
+  // skip frozen images' tiles only when images can freeze early and one network pass covers the
+  // batch (the live list indexes the batch)
+  ctx->skip_frozen = p->tol > 0.f && p->stop_rule == IDEQ_STOP_PER_IMAGE && !p->compute_frozen && N <= ctx->mb;
+  enable_skip(ctx, ctx->skip_frozen);
+  ctx->have_last = true;
+  ctx->last_N = N;
+  ctx->last_a = a;
+  ctx->last_f = f;
   const bool global = p->stop_rule == IDEQ_STOP_GLOBAL_MAX;
   const bool poll = p->tol > 0.f;
   const int poll_every = global ? p->check_every : 4;
@@ -1186,6 +1295,18 @@ ideq_status ideq_get_nccl_id(unsigned char out[128]) {
 
 ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int device, void* cuda_stream, int max_batch,
                         int H, int W, const ideq_dist* dist, ideq_ctx** out) {
+  return ideq_create_ex(net, prec, device, cuda_stream, max_batch, H, W, dist, nullptr, out);
+}
+
+ideq_status ideq_get_plan(const ideq_ctx* ctx, int* micro_batch, size_t* workspace_bytes) {
+  if (!ctx) return IDEQ_E_INVALID;
+  if (micro_batch) *micro_batch = ctx->mb;
+  if (workspace_bytes) *workspace_bytes = ctx->net_bytes;
+  return IDEQ_OK;
+}
+
+ideq_status ideq_create_ex(const ideq_net_desc* net, ideq_precision prec, int device, void* cuda_stream, int max_batch,
+                           int H, int W, const ideq_dist* dist, const ideq_plan_opts* opts, ideq_ctx** out) {
   if (!net || !out || !net->weights) return IDEQ_E_INVALID;
   *out = nullptr;
   std::unique_ptr<ideq_ctx> holder(new ideq_ctx());
@@ -1249,34 +1370,9 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
     ctx->own_stream = true;
   }
 
-  // ---- feature buffers
+  // ---- solver state (every image of a solve)
   const int N = max_batch;
   ideq_status st;
-  if (net->arch == IDEQ_NET_TINY3) {
-    const size_t e = (size_t)N * H * W * net->widths[0] * ctx->elt;
-    ctx->lvl_buf.assign(1, std::vector<void*>(3, nullptr));
-    for (int i = 0; i < 2; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[0][i], e))) { *out = holder.release(); return st; }
-    void* a1; void* a2;
-    if ((st = dalloc(ctx, &a1, e)) || (st = dalloc(ctx, &a2, e))) { *out = holder.release(); return st; }
-    ctx->saved["a1"] = a1;
-    ctx->saved["a2"] = a2;
-  } else {
-    ctx->lvl_buf.assign(4, std::vector<void*>(3, nullptr));
-    for (int l = 0; l < 4; ++l) {
-      const size_t e = (size_t)N * (H >> l) * (W >> l) * net->widths[l] * ctx->elt;
-      for (int i = 0; i < 3; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[l][i], e))) { *out = holder.release(); return st; }
-      for (int r = 0; r < net->res_blocks; ++r) {
-        void* a;
-        if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
-        ctx->saved["e" + std::to_string(l) + "." + std::to_string(r)] = a;
-        if (l < 3) {
-          if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
-          ctx->saved["d" + std::to_string(l) + "." + std::to_string(r)] = a;
-        }
-      }
-    }
-  }
-  // ---- solver state
   const size_t plane = (size_t)N * ctx->C * H * W * sizeof(float);
   void* p;
 #define AL(field, bytes)                                                          \
@@ -1299,6 +1395,67 @@ ideq_status ideq_create(const ideq_net_desc* net, ideq_precision prec, int devic
 #undef AL
   if (cudaMallocHost(&ctx->h_pinned, 64) != cudaSuccess) { *out = holder.release(); return fail(*out, IDEQ_E_NOMEM, "pinned alloc"); }
   cudaMemset(ctx->trace, 0xff, ctx->trace_cap * sizeof(float));
+
+  // ---- workspace plan: the network's activations (work buffers + saved activations of every
+  // residual block) for a micro-batch of mb images; a solve runs the network once per micro-batch
+  // (C5's 512 images need ~221 GB of activations in bf16, beyond one GPU)
+  size_t per_img = 0;  // network workspace bytes per image
+  if (net->arch == IDEQ_NET_TINY3) {
+    per_img = (size_t)4 * H * W * net->widths[0] * ctx->elt;
+  } else {
+    for (int l = 0; l < 4; ++l)
+      per_img += (size_t)(3 + net->res_blocks + (l < 3 ? net->res_blocks : 0)) * (H >> l) * (W >> l) * net->widths[l] * ctx->elt;
+  }
+  {
+    int mb = opts ? opts->micro_batch : 0;
+    if (mb < 0) { *out = holder.release(); return fail(*out, IDEQ_E_INVALID, "micro_batch must be >= 0"); }
+    if (mb == 0) {
+      size_t budget = opts ? opts->workspace_bytes : 0;
+      if (budget == 0) {
+        size_t fr = 0, tot = 0;
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) { cudaGetLastError(); fr = 0; }
+        // kept free for what set_operator / solve_host allocate later (operator data, FFT work
+        // spectrum, host staging of y and x) and for the runtime: 2 GB + 3 fp32 planes per image
+        const size_t reserve = ((size_t)2 << 30) + 3 * plane;
+        budget = fr > reserve ? (size_t)((double)(fr - reserve) * 0.9) : 0;
+      }
+      mb = (int)std::min<size_t>((size_t)N, budget / (per_img ? per_img : 1));
+      if (mb < 1) {
+        *out = holder.release();
+        return fail(*out, IDEQ_E_NOMEM, "network workspace of one image (%zu bytes) exceeds the budget (%zu bytes)",
+                    per_img, budget);
+      }
+    }
+    if (mb > N) mb = N;
+    const int nmb = (N + mb - 1) / mb;  // balanced micro-batches
+    ctx->mb = (N + nmb - 1) / nmb;
+    ctx->net_bytes = per_img * ctx->mb;
+  }
+  const int M = ctx->mb;
+  if (net->arch == IDEQ_NET_TINY3) {
+    const size_t e = (size_t)M * H * W * net->widths[0] * ctx->elt;
+    ctx->lvl_buf.assign(1, std::vector<void*>(3, nullptr));
+    for (int i = 0; i < 2; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[0][i], e))) { *out = holder.release(); return st; }
+    void* a1; void* a2;
+    if ((st = dalloc(ctx, &a1, e)) || (st = dalloc(ctx, &a2, e))) { *out = holder.release(); return st; }
+    ctx->saved["a1"] = a1;
+    ctx->saved["a2"] = a2;
+  } else {
+    ctx->lvl_buf.assign(4, std::vector<void*>(3, nullptr));
+    for (int l = 0; l < 4; ++l) {
+      const size_t e = (size_t)M * (H >> l) * (W >> l) * net->widths[l] * ctx->elt;
+      for (int i = 0; i < 3; ++i) if ((st = dalloc(ctx, &ctx->lvl_buf[l][i], e))) { *out = holder.release(); return st; }
+      for (int r = 0; r < net->res_blocks; ++r) {
+        void* a;
+        if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
+        ctx->saved["e" + std::to_string(l) + "." + std::to_string(r)] = a;
+        if (l < 3) {
+          if ((st = dalloc(ctx, &a, e))) { *out = holder.release(); return st; }
+          ctx->saved["d" + std::to_string(l) + "." + std::to_string(r)] = a;
+        }
+      }
+    }
+  }
 
   // ---- distribution
   if (dist && dist->world >= 1) {
@@ -1474,14 +1631,13 @@ ideq_status ideq_grad_g(ideq_ctx* ctx, const float* z, float* grad_out, float* u
   if ((st = check_ctx(ctx))) return st;
   if (!z || !grad_out) return fail(ctx, IDEQ_E_INVALID, "NULL z/grad");
   if (batch < 1 || batch > ctx->maxN) return fail(ctx, IDEQ_E_INVALID, "batch out of range");
-  if ((st = build_program(ctx, batch))) return st;
+  if ((st = prepare_programs(ctx, batch))) return st;
   const size_t n = (size_t)batch * ctx->C * ctx->H * ctx->W;
   CK(cudaMemcpyAsync(ctx->Z, z, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   launch_init_state(make_fin(ctx, batch, nullptr), ctx->stream);  // every image active: no tile skipped
   ctx->skip_frozen = false;
-  for (auto& L : ctx->prog)
-    if (L.plan) tc_plan_enable_skip(L.plan, false);
-  run_network(ctx);
+  enable_skip(ctx, false);
+  run_network(ctx, batch);
   CK(cudaMemcpyAsync(grad_out, ctx->G, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   if (u_out) CK(cudaMemcpyAsync(u_out, ctx->Hc, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1910,6 +2066,52 @@ ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, con
   return IDEQ_OK;
 }
 
+ideq_status ideq_time_class(ideq_ctx* ctx, int cls, int reps, double* ms, double* flops, double* bytes) {
+  ideq_status st;
+  if ((st = check_ctx(ctx))) return st;
+  if (!ctx->have_last) return fail(ctx, IDEQ_E_STATE, "ideq_time_class needs a solve first");
+  if (!ms || reps < 1 ||
+      !(cls == IDEQ_K_CONV_TC || cls == IDEQ_K_CONV_SIMT || cls == IDEQ_K_HEADTAIL || cls == IDEQ_K_STEP))
+    return fail(ctx, IDEQ_E_INVALID, "class must be CONV_TC, CONV_SIMT, HEADTAIL or STEP; reps >= 1");
+  cudaStream_t s = ctx->stream;
+  const bool prof = ctx->profiling;
+  ctx->profiling = false;
+  ctx->counting = true;
+  for (int k = 0; k < IDEQ_K_NCLASSES; ++k) ctx->cnt_flops[k] = ctx->cnt_bytes[k] = 0.0;
+  StepArgs a = ctx->last_a;
+  a.X0 = ctx->Xsnap;  // the step writes x^{k+1} into scratch, never into the caller's x
+  cudaGraph_t graph;
+  CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  if (cls == IDEQ_K_STEP) run_step(ctx, a);
+  else run_network(ctx, ctx->last_N, cls);
+  cudaError_t ec = cudaStreamEndCapture(s, &graph);
+  ctx->counting = false;
+  ctx->profiling = prof;
+  if (ec != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "class capture: %s", cudaGetErrorString(ec));
+  cudaGraphExec_t ge;
+  CK(cudaGraphInstantiate(&ge, graph, 0));
+  cudaGraphDestroy(graph);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaGraphLaunch(ge, s);  // warm-up
+  cudaEventRecord(e0, s);
+  for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
+  cudaEventRecord(e1, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  float t = 0.f;
+  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGraphExecDestroy(ge);
+  if (e != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "class timing: %s", cudaGetErrorString(e));
+  *ms = (double)t / reps;
+  const bool step = cls == IDEQ_K_STEP;  // the step's fidelity passes count with it
+  if (flops) *flops = ctx->cnt_flops[cls] + (step ? ctx->cnt_flops[IDEQ_K_FIDELITY] : 0.0);
+  if (bytes) *bytes = ctx->cnt_bytes[cls] + (step ? ctx->cnt_bytes[IDEQ_K_FIDELITY] : 0.0);
+  return IDEQ_OK;
+}
+
 ideq_status ideq_set_profiling(ideq_ctx* ctx, int enable) {
   if (!ctx) return IDEQ_E_INVALID;
   ctx->profiling = enable != 0;
@@ -1925,8 +2127,13 @@ ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int reset) {
 }
 
 int ideq_launches_per_iteration(const ideq_ctx* ctx) {
-  if (!ctx) return 0;
-  int n = (int)ctx->prog.size();
+  if (!ctx || !ctx->have_last) return 0;
+  int n = 0;
+  for (int first = 0; first < ctx->last_N; first += ctx->mb) {
+    const int m = ctx->last_N - first < ctx->mb ? ctx->last_N - first : ctx->mb;
+    auto it = ctx->progs.find(m);
+    if (it != ctx->progs.end()) n += (int)it->second.layers.size();
+  }
   if (ctx->op.kind == IDEQ_OP_BLUR) n += 2; else n += 1;
   n += 3;  // finalize, advance_a, advance_b
   return n;
@@ -1936,8 +2143,8 @@ int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0
                     const void* in, void* out, const void* aux, int epi, char* err, int errlen) {
   auto seterr = [&](const char* m) { if (err && errlen > 0) { snprintf(err, errlen, "%s", m); } };
   if (kind < 0 || kind > 5 || !w || !in || !out) { seterr("bad arguments"); return IDEQ_E_INVALID; }
-  if (use_tc_ && precision != IDEQ_PREC_BF16) { seterr("tcgen05 path is bf16 only"); return IDEQ_E_INVALID; }
   init_kernel_attributes();
+  const bool x3 = use_tc_ && precision == IDEQ_PREC_FP32;  // fp32 on tcgen05 = 3xTF32
   const int kh = (kind <= 1) ? 3 : 2;
   std::vector<int> shp = {s0, s1, kh, kh};
   int ncols = 0, ntaps = 0, ktap = 0;
@@ -1946,30 +2153,36 @@ int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0
   else if (kind == 2 || kind == 5) { ncols = s0; ktap = 2 * s1; }
   else { ncols = 4 * s1; ktap = s0; }
   const int cin_tensor = (kind == 2 || kind == 5) ? ktap / 2 : ktap;
-  const int KC = pick_kc(use_tc_ != 0, ktap);
+  const int KC = pick_kc(use_tc_ != 0, x3, ktap);
   if (ktap % KC) { seterr("channel count not a multiple of the K-block"); return IDEQ_E_INVALID; }
   std::vector<float> B = gemm_weights(kind, w, shp, KC, ncols, ntaps, ktap);
   ConvGeom g = make_geom(kind, N, Hin, Win, cin_tensor, ncols, KC, ktap, epi);
   const size_t esz = precision == IDEQ_PREC_BF16 ? 2 : 4;
   void* dW = nullptr;
+  void* dWlo = nullptr;
   if (cudaMalloc(&dW, B.size() * esz) != cudaSuccess) { seterr("cudaMalloc"); return IDEQ_E_NOMEM; }
   if (precision == IDEQ_PREC_BF16) {
     std::vector<uint16_t> hb(B.size());
     for (size_t i = 0; i < B.size(); ++i) hb[i] = f2bf(B[i]);
     cudaMemcpy(dW, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
+  } else if (x3) {
+    std::vector<float> hi(B.size()), lo(B.size());
+    for (size_t i = 0; i < B.size(); ++i) { hi[i] = tf32_rna(B[i]); lo[i] = B[i] - hi[i]; }
+    if (cudaMalloc(&dWlo, B.size() * 4) != cudaSuccess) { seterr("cudaMalloc"); cudaFree(dW); return IDEQ_E_NOMEM; }
+    cudaMemcpy(dW, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dWlo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice);
   } else {
     cudaMemcpy(dW, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
   }
   int rc = IDEQ_OK;
   if (use_tc_) {
-    if (!tc_supported(g)) { seterr("geometry unsupported by tcgen05 path"); cudaFree(dW); return IDEQ_E_UNSUPPORTED; }
+    if (!tc_supported(g, x3)) { seterr("geometry unsupported by tcgen05 path"); cudaFree(dW); cudaFree(dWlo); return IDEQ_E_UNSUPPORTED; }
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     char e2[256] = {0};
-    TcPlan* plan = tc_make_plan(g, (const __nv_bfloat16*)in, (const __nv_bfloat16*)dW, (__nv_bfloat16*)out,
-                                (const __nv_bfloat16*)aux, sms, e2, sizeof(e2));
-    if (!plan) { seterr(e2); cudaFree(dW); return IDEQ_E_CUDA; }
+    TcPlan* plan = tc_make_plan(g, x3, in, dW, dWlo, out, aux, sms, e2, sizeof(e2));
+    if (!plan) { seterr(e2); cudaFree(dW); cudaFree(dWlo); return IDEQ_E_CUDA; }
     tc_launch(plan, 0);
     tc_free_plan(plan);
   } else if (precision == IDEQ_PREC_BF16) {
@@ -1982,6 +2195,7 @@ int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) { seterr(cudaGetErrorString(e)); rc = IDEQ_E_CUDA; }
   cudaFree(dW);
+  if (dWlo) cudaFree(dWlo);
   return rc;
 }
 
@@ -1991,7 +2205,8 @@ void ideq_destroy(ideq_ctx* ctx) {
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   if (ctx->gexec_plain) cudaGraphExecDestroy(ctx->gexec_plain);
   if (ctx->gexec_check) cudaGraphExecDestroy(ctx->gexec_check);
-  for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
+  for (auto& kv : ctx->progs)
+    for (auto& L : kv.second.layers) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
   for (auto& a : ctx->allocs) cudaFree(a.p);
   for (auto& b : ctx->jfb_pool) cudaFree(b.first);
   if (ctx->jfb_ws) cudaFree(ctx->jfb_ws);

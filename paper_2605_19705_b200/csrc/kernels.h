@@ -153,12 +153,13 @@ template <typename T>
 void launch_feat2img(const T* in, const float* w_t, float* out, const float* aux, float alpha, int N, int C, int H,
                      int W, int win, cudaStream_t s);
 
-// tcgen05 implicit GEMM (bf16 operands, fp32 TMEM accumulators). Returns false if the
-// geometry is unsupported (the runtime then refuses the configuration).
+// tcgen05 implicit GEMM, fp32 TMEM accumulators: bf16 operands, or (x3) fp32 operands as 3xTF32
+// (wBlo = the lo half of the pre-split weights). Returns false / null if the geometry is
+// unsupported (the runtime then refuses the configuration).
 struct TcPlan;
-bool tc_supported(const ConvGeom& g);
-TcPlan* tc_make_plan(const ConvGeom& g, const __nv_bfloat16* in, const __nv_bfloat16* wB, __nv_bfloat16* out,
-                     const __nv_bfloat16* aux, int num_sms, char* err, size_t errlen);
+bool tc_supported(const ConvGeom& g, bool x3);
+TcPlan* tc_make_plan(const ConvGeom& g, bool x3, const void* in, const void* wB, const void* wBlo, void* out,
+                     const void* aux, int num_sms, char* err, size_t errlen);
 void tc_launch(const TcPlan* p, cudaStream_t s);
 void tc_free_plan(TcPlan* p);
 void tc_plan_set_image(TcPlan* p, float* out, const float* aux, float alpha, int C);

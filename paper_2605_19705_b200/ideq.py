@@ -50,6 +50,10 @@ class Params(C.Structure):
                 ("restart_B", C.c_float), ("averaging", C.c_int), ("compute_frozen", C.c_int)]
 
 
+class PlanOpts(C.Structure):
+    _fields_ = [("micro_batch", C.c_int), ("workspace_bytes", C.c_size_t)]
+
+
 class ImageStat(C.Structure):
     _fields_ = [("iters", C.c_int), ("residual", C.c_float), ("status", C.c_int), ("restarts", C.c_int),
                 ("k0", C.c_int)]
@@ -63,7 +67,7 @@ class Profile(C.Structure):
 SYMBOLS = ["ideq_get_nccl_id", "ideq_create", "ideq_set_operator", "ideq_solve", "ideq_solve_host", "ideq_grad_g",
            "ideq_fidelity_grad", "ideq_fidelity_prox", "ideq_set_profiling", "ideq_get_profile",
            "ideq_launches_per_iteration", "ideq_last_error", "ideq_destroy", "ideq_abi_version", "ideq_debug_conv",
-           "ideq_jfb_grad"]
+           "ideq_jfb_grad", "ideq_create_ex", "ideq_get_plan", "ideq_time_class"]
 
 _lib = None
 
@@ -79,6 +83,10 @@ def load_library(path: str = LIB_PATH):
     vp, i, f, fp = C.c_void_p, C.c_int, C.c_float, C.POINTER(C.c_float)
     lib.ideq_get_nccl_id.argtypes = [C.POINTER(C.c_ubyte)]
     lib.ideq_create.argtypes = [C.POINTER(NetDesc), i, i, vp, i, i, i, C.POINTER(Dist), C.POINTER(vp)]
+    lib.ideq_create_ex.argtypes = [C.POINTER(NetDesc), i, i, vp, i, i, i, C.POINTER(Dist), C.POINTER(PlanOpts),
+                                   C.POINTER(vp)]
+    lib.ideq_get_plan.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_size_t)]
+    lib.ideq_time_class.argtypes = [vp, i, i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.ideq_set_operator.argtypes = [vp, C.POINTER(OperatorDesc), i]
     lib.ideq_solve.argtypes = [vp, vp, vp, i, C.POINTER(Params), C.POINTER(ImageStat), fp]
     lib.ideq_solve_host.argtypes = [vp, vp, vp, i, C.POINTER(Params), C.POINTER(ImageStat), fp]
@@ -134,7 +142,7 @@ class Solver:
 
     def __init__(self, cfg: dict, weights: np.ndarray, precision: str = None, device: int = 0, stream=None,
                  max_batch: int = None, H: int = None, W: int = None, rank: int = 0, world: int = 1,
-                 nccl_id: bytes = None):
+                 nccl_id: bytes = None, micro_batch: int = 0, workspace_bytes: int = 0):
         self.lib = load_library()
         self.cfg = cfg
         self.C = cfg["C"]
@@ -161,8 +169,9 @@ class Solver:
             C.memmove(dist.nccl_id, nccl_id, 128)
         ctx = C.c_void_p()
         s = None if stream is None else C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
-        r = self.lib.ideq_create(C.byref(nd), PREC[prec], device, s, self.max_batch, self.H, self.W,
-                                 C.byref(dist) if dist is not None else None, C.byref(ctx))
+        opts = PlanOpts(int(micro_batch), int(workspace_bytes))
+        r = self.lib.ideq_create_ex(C.byref(nd), PREC[prec], device, s, self.max_batch, self.H, self.W,
+                                    C.byref(dist) if dist is not None else None, C.byref(opts), C.byref(ctx))
         self.ctx = ctx
         if r != OK:
             msg = self.lib.ideq_last_error(ctx).decode() if ctx.value else "invalid create arguments"
@@ -290,6 +299,20 @@ class Solver:
         self._check(self.lib.ideq_get_profile(self.ctx, C.byref(p), int(reset)))
         return {k: dict(ms=p.ms[i], launches=p.launches[i], flops=p.flops[i], bytes=p.bytes[i])
                 for i, k in enumerate(KCLASS)}
+
+    def plan(self) -> dict:
+        """The workspace plan chosen at create (ideq_get_plan)."""
+        mb, nb = C.c_int(), C.c_size_t()
+        self._check(self.lib.ideq_get_plan(self.ctx, C.byref(mb), C.byref(nb)))
+        return {"micro_batch": mb.value, "workspace_bytes": nb.value}
+
+    def time_class(self, cls: str, reps: int = 10) -> dict:
+        """In-graph timing of one kernel class of the last solve's iteration (ideq_time_class):
+        ms per iteration and the class's algorithmic FLOPs / bytes per iteration."""
+        ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+        self._check(self.lib.ideq_time_class(self.ctx, KCLASS.index(cls), int(reps), C.byref(ms), C.byref(fl),
+                                             C.byref(by)))
+        return {"ms": ms.value, "flops": fl.value, "bytes": by.value}
 
     def launches_per_iteration(self) -> int:
         return int(self.lib.ideq_launches_per_iteration(self.ctx))

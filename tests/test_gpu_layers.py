@@ -56,13 +56,15 @@ for kind in range(6):
                 CASES.append((kind, cin, cout, H, W, epi))
 
 
-@pytest.mark.parametrize("path", ["fp32", "bf16-simt", "bf16-tc"])
+@pytest.mark.parametrize("path", ["fp32", "fp32-tc", "bf16-simt", "bf16-tc"])
 @pytest.mark.parametrize("kind,cin,cout,H,W,epi", CASES)
 def test_layer_vs_oracle(path, kind, cin, cout, H, W, epi):
+    """Paths: fp32 FFMA (the JFB gradient's convolutions), fp32 on tcgen05 as 3xTF32 (the parity
+    mode's network), bf16 FFMA, bf16 tcgen05 (the headline)."""
     torch = torch_cuda()
     from paper_2605_19705_b200 import ideq
-    prec = "fp32" if path == "fp32" else "bf16"
-    use_tc = path == "bf16-tc"
+    prec = "fp32" if path.startswith("fp32") else "bf16"
+    use_tc = path.endswith("-tc")
     rng = np.random.default_rng(hash((kind, cin, cout, H, W, epi)) % (2 ** 32))
     fn, wshape = KINDS[kind]
     w = rng.standard_normal(wshape(cin, cout)) * np.sqrt(1.0 / (cin * 4))

