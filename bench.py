@@ -351,7 +351,7 @@ def main():
                                    + ("" if prec == "bf16" else " x 1/2 (TF32 nominal) / 3 (3xTF32)"),
                     "frac_burst": ach / pk_b, "frac_sustained": ach / pk_s}
     roofline.update({
-        "timing": f"ideq_time_class: the class's launches of one iteration in one CUDA graph, {reps} replays",
+        "timing": f"ideq_time_class: event-record nodes at the class boundaries of one captured iteration, {reps} replays",
         "ms_per_step": kt["ms"], "share_of_step": kt["ms"] / (ms / args.steps),
         "algorithmic_flops_per_step": kt["flops"], "algorithmic_bytes_per_step": kt["bytes"],
         "launches_per_step": s.launches_per_iteration(),

@@ -277,13 +277,14 @@ typedef struct {
 IDEQ_API ideq_status ideq_set_profiling(ideq_ctx* ctx, int enable);
 IDEQ_API ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int reset);
 
-/* In-graph timing of one kernel class (ideq_kernel_class: CONV_TC, CONV_SIMT, HEADTAIL or STEP)
- * of the LAST solve's iteration: the class's launches, in the iteration's order and launch
- * configuration, captured into one CUDA graph and replayed `reps` times back to back on the
- * context stream (CUDA events around the replays). *ms = milliseconds per iteration; flops and
- * bytes = the class's algorithmic FLOPs and HBM bytes per iteration. The kernels read and write
- * the context's workspaces (the last solve's data); the solve's result in x_inout is untouched.
- * IDEQ_E_STATE before the first solve. */
+/* In-graph timing of one kernel class (ideq_kernel_class: CONV_TC, CONV_SIMT, HEADTAIL, STEP --
+ * with its fidelity passes -- or REDUCE) of the LAST solve's iteration: that iteration is captured
+ * again into a CUDA graph (same kernels, order and launch configuration) with event-record nodes
+ * wherever the class of consecutive launches changes, and replayed `reps` times; *ms = the summed
+ * duration of the class's runs of launches per iteration (<= the iteration's time by
+ * construction); flops / bytes = the class's algorithmic FLOPs and HBM bytes per iteration. The
+ * update writes into scratch: the caller's buffers are untouched, the context's solver state is
+ * overwritten. IDEQ_E_STATE before the first solve. */
 IDEQ_API ideq_status ideq_time_class(ideq_ctx* ctx, int kernel_class, int reps, double* ms, double* flops,
                                      double* bytes);
 

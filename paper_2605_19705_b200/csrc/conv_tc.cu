@@ -111,13 +111,15 @@ __device__ __forceinline__ void mma_tf32_elect(uint32_t tmem_d, uint64_t adesc, 
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// x = hi + lo with hi = x rounded to tf32 (10-bit mantissa, low 13 bits zero) and lo = x - hi
-// (exact in fp32); the tensor core reads lo to tf32 precision, so hi*b + lo*b carries ~21 bits.
+// x ~ hi + lo with hi = x rounded to tf32 (10-bit mantissa, low 13 bits zero) and lo = (x - hi)
+// rounded to tf32 as well (the tensor core would otherwise truncate its low bits): |x - hi - lo|
+// <= 2^-22 |x|, so hi*b + lo*b carries ~22 bits.
 __device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  uint32_t h;
+  uint32_t h, l;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
   hi = __uint_as_float(h);
-  lo = x - hi;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
+  lo = __uint_as_float(l);
 }
 __device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
   return (1u << 4)                       // D format f32

@@ -81,6 +81,36 @@ struct DevBuf {
   size_t bytes = 0;
 };
 
+// In-graph timing of kernel classes (ideq_time_class): while an iteration is captured, an
+// event-record node is placed wherever the kernel class of consecutive launches changes, so each
+// run of same-class launches is bracketed by two events of the replayed graph.
+struct SegTimer {
+  cudaStream_t s = nullptr;
+  int cur = -1;
+  cudaEvent_t open = nullptr;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> seg[IDEQ_K_NCLASSES];
+  std::vector<cudaEvent_t> all;
+  cudaEvent_t rec() {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    all.push_back(e);
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    return e;
+  }
+  void enter(int cls) {
+    if (cls == cur) return;
+    close();
+    open = rec();
+    cur = cls;
+  }
+  void close() {
+    if (cur < 0) return;
+    seg[cur].push_back({open, rec()});
+    cur = -1;
+  }
+  ~SegTimer() { for (auto e : all) cudaEventDestroy(e); }
+};
+
 // The network program for one micro-batch size: forward then VJP launches, in order.
 struct Program {
   std::vector<Layer> layers;
@@ -177,6 +207,7 @@ struct ideq_ctx {
   // profiling
   bool profiling = false;
   bool counting = false;  // class timing: Prof adds each launch's algorithmic work to cnt_*
+  SegTimer* segt = nullptr;  // class timing: event nodes at class boundaries of the captured iteration
   double cnt_flops[IDEQ_K_NCLASSES] = {0}, cnt_bytes[IDEQ_K_NCLASSES] = {0};
   bool skip_frozen = false;  // current solve may freeze images early: kernels skip their work
   ideq_profile prof{};
@@ -371,7 +402,7 @@ bool use_x3(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_FP32 && use_tc(ctx); 
 bool use_tc_headtail(ideq_ctx* ctx) { return ctx->prec == IDEQ_PREC_BF16 && use_tc(ctx); }
 
 // 3xTF32 operand split on the host: hi = w rounded to tf32 (round to nearest, ties away from zero,
-// as cvt.rna.tf32.f32), lo = w - hi (exact in fp32).
+// as cvt.rna.tf32.f32), lo = (w - hi) rounded the same way (|w - hi - lo| <= 2^-22 |w|).
 float tf32_rna(float f) {
   uint32_t u;
   memcpy(&u, &f, 4);
@@ -490,7 +521,7 @@ ideq_status add_gemm_w(ideq_ctx* ctx, const std::string& key, const float* Wt, c
       std::vector<float> lo(B.size());
       for (size_t i = 0; i < B.size(); ++i) {
         const float h = tf32_rna(B[i]);
-        lo[i] = B[i] - h;
+        lo[i] = tf32_rna(B[i] - h);
         B[i] = h;
       }
       ideq_status st = upload_gemm_weights(ctx, key + "#lo", lo);
@@ -831,6 +862,7 @@ struct Prof {
   cudaEvent_t a = nullptr;
   Prof(ideq_ctx* c, int k, double f = 0, double b = 0) : ctx(c), cls(k), flops(f), bytes(b) {
     if (ctx->counting) { ctx->cnt_flops[k] += f; ctx->cnt_bytes[k] += b; }
+    if (ctx->segt) ctx->segt->enter(k == IDEQ_K_FIDELITY ? IDEQ_K_STEP : k);  // the step's passes count with it
     if (ctx->profiling) { a = next_event(ctx); cudaEventRecord(a, ctx->stream); }
   }
   ~Prof() {
@@ -2070,42 +2102,51 @@ ideq_status ideq_time_class(ideq_ctx* ctx, int cls, int reps, double* ms, double
   ideq_status st;
   if ((st = check_ctx(ctx))) return st;
   if (!ctx->have_last) return fail(ctx, IDEQ_E_STATE, "ideq_time_class needs a solve first");
-  if (!ms || reps < 1 ||
-      !(cls == IDEQ_K_CONV_TC || cls == IDEQ_K_CONV_SIMT || cls == IDEQ_K_HEADTAIL || cls == IDEQ_K_STEP))
-    return fail(ctx, IDEQ_E_INVALID, "class must be CONV_TC, CONV_SIMT, HEADTAIL or STEP; reps >= 1");
+  if (!ms || reps < 1 || cls < 0 || cls >= IDEQ_K_NCLASSES || cls == IDEQ_K_FIDELITY)
+    return fail(ctx, IDEQ_E_INVALID, "class must be CONV_TC, CONV_SIMT, HEADTAIL, STEP or REDUCE; reps >= 1");
   cudaStream_t s = ctx->stream;
+  // one whole iteration of the last solve (same kernels, order and launch configuration as its
+  // graph) with event-record nodes at the class boundaries; the update writes x^{k+1} into
+  // scratch, never into the caller's x (the context's solver state is overwritten)
+  StepArgs a = ctx->last_a;
+  a.X0 = ctx->Xsnap;
+  FinalizeArgs f = ctx->last_f;
+  f.trace = nullptr;
+  SegTimer T;
+  T.s = s;
   const bool prof = ctx->profiling;
   ctx->profiling = false;
   ctx->counting = true;
   for (int k = 0; k < IDEQ_K_NCLASSES; ++k) ctx->cnt_flops[k] = ctx->cnt_bytes[k] = 0.0;
-  StepArgs a = ctx->last_a;
-  a.X0 = ctx->Xsnap;  // the step writes x^{k+1} into scratch, never into the caller's x
   cudaGraph_t graph;
   CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-  if (cls == IDEQ_K_STEP) run_step(ctx, a);
-  else run_network(ctx, ctx->last_N, cls);
+  ctx->segt = &T;
+  ideq_status st2 = enqueue_iteration(ctx, a, f, false);
+  T.close();
+  ctx->segt = nullptr;
   cudaError_t ec = cudaStreamEndCapture(s, &graph);
   ctx->counting = false;
   ctx->profiling = prof;
+  if (st2) return st2;
   if (ec != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "class capture: %s", cudaGetErrorString(ec));
   cudaGraphExec_t ge;
   CK(cudaGraphInstantiate(&ge, graph, 0));
   cudaGraphDestroy(graph);
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  cudaGraphLaunch(ge, s);  // warm-up
-  cudaEventRecord(e0, s);
-  for (int r = 0; r < reps; ++r) cudaGraphLaunch(ge, s);
-  cudaEventRecord(e1, s);
-  cudaError_t e = cudaStreamSynchronize(s);
-  float t = 0.f;
-  if (e == cudaSuccess) e = cudaEventElapsedTime(&t, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
+  CK(cudaGraphLaunch(ge, s));  // warm-up
+  CK(cudaStreamSynchronize(s));
+  double tot = 0.0;
+  for (int r = 0; r < reps; ++r) {
+    CK(cudaGraphLaunch(ge, s));
+    CK(cudaStreamSynchronize(s));
+    for (auto& pr : T.seg[cls]) {
+      float t = 0.f;
+      cudaError_t e = cudaEventElapsedTime(&t, pr.first, pr.second);
+      if (e != cudaSuccess) { cudaGraphExecDestroy(ge); return fail(ctx, IDEQ_E_CUDA, "class timing: %s", cudaGetErrorString(e)); }
+      tot += t;
+    }
+  }
   cudaGraphExecDestroy(ge);
-  if (e != cudaSuccess) return fail(ctx, IDEQ_E_CUDA, "class timing: %s", cudaGetErrorString(e));
-  *ms = (double)t / reps;
+  *ms = tot / reps;
   const bool step = cls == IDEQ_K_STEP;  // the step's fidelity passes count with it
   if (flops) *flops = ctx->cnt_flops[cls] + (step ? ctx->cnt_flops[IDEQ_K_FIDELITY] : 0.0);
   if (bytes) *bytes = ctx->cnt_bytes[cls] + (step ? ctx->cnt_bytes[IDEQ_K_FIDELITY] : 0.0);
@@ -2167,7 +2208,7 @@ int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0
     cudaMemcpy(dW, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
   } else if (x3) {
     std::vector<float> hi(B.size()), lo(B.size());
-    for (size_t i = 0; i < B.size(); ++i) { hi[i] = tf32_rna(B[i]); lo[i] = B[i] - hi[i]; }
+    for (size_t i = 0; i < B.size(); ++i) { hi[i] = tf32_rna(B[i]); lo[i] = tf32_rna(B[i] - hi[i]); }
     if (cudaMalloc(&dWlo, B.size() * 4) != cudaSuccess) { seterr("cudaMalloc"); cudaFree(dW); return IDEQ_E_NOMEM; }
     cudaMemcpy(dW, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dWlo, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice);

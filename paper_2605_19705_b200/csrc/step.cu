@@ -150,6 +150,85 @@ __global__ void __launch_bounds__(256) pointwise_step_kernel(StepArgs a) {
   block_reduce_store(acc, a.partials + ((long long)n * a.parts + part) * 3);
 }
 
+// Vectorised form (every config: d and H*W multiples of 4): each thread moves float4 of z, grad g,
+// x^k, y (and a uchar4 of the mask: 4 consecutive pixels of one channel plane) and writes float4
+// of x^{k+1}, z^{k+1}; 32-bit indices inside the image (d < 2^31), the image offset applied once
+// to the base pointers. Per element it reads 16 B (+ 1/C B of mask) and writes 8 B.
+template <int MODE>
+__device__ __forceinline__ float step_x1(const StepArgs& a, float z, float gg, float y, float m, float fb, float fb2) {
+  if (MODE == STEP_PROX_INPAINT) {
+    const float v = z - a.tau * a.lam * gg;
+    return (a.tau * m * y + v) / (a.tau * m + 1.f);
+  } else if (MODE == STEP_GRAD_BUF) {
+    return z - a.tau * (fb + a.lam * gg);
+  } else if (MODE == STEP_GRAD_MRI) {
+    return z - a.tau * (fb - fb2 + a.lam * gg);              // Alg. 1 l.8, grad f = fbuf - fbuf2
+  } else if (MODE == STEP_GRAD_RICIAN) {
+    return z - a.tau * (rician_grad_f(z, y, a.inv_s2) + a.lam * gg);
+  } else if (MODE == STEP_GRAD_INPAINT) {
+    return z - a.tau * (m * (m * z - y) + a.lam * gg);
+  }
+  return fb;  // STEP_X1_BUF
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) pointwise_step_v4_kernel(StepArgs a) {
+  pdl_enter();
+  const int n = blockIdx.y, part = blockIdx.x;
+  if (!a.active[n]) return;
+  const int k = *a.kdev;
+  constexpr bool USE_Y = MODE == STEP_PROX_INPAINT || MODE == STEP_GRAD_RICIAN || MODE == STEP_GRAD_INPAINT;
+  constexpr bool USE_M = MODE == STEP_PROX_INPAINT || MODE == STEP_GRAD_INPAINT;
+  constexpr bool USE_FB = MODE == STEP_GRAD_BUF || MODE == STEP_GRAD_MRI || MODE == STEP_X1_BUF;
+  const long long off = (long long)n * a.d;
+  const float4* z4 = reinterpret_cast<const float4*>(a.z + off);
+  const float4* g4 = reinterpret_cast<const float4*>(a.gg + off);
+  const float4* xk4 = reinterpret_cast<const float4*>(((k & 1) ? a.X1 : a.X0) + off);
+  float4* xn4 = reinterpret_cast<float4*>(((k & 1) ? a.X0 : a.X1) + off);
+  float4* zn4 = reinterpret_cast<float4*>(a.zout + off);
+  const float4* y4 = USE_Y ? reinterpret_cast<const float4*>(a.y + off) : nullptr;
+  const float4* f4 = USE_FB ? reinterpret_cast<const float4*>(a.fbuf + off) : nullptr;
+  const float4* f24 = MODE == STEP_GRAD_MRI ? reinterpret_cast<const float4*>(a.fbuf2 + off) : nullptr;
+  const uint32_t HW4 = (uint32_t)(a.H * a.W) >> 2;
+  const uchar4* m4 = USE_M ? reinterpret_cast<const uchar4*>(a.mask + (long long)n * a.H * a.W) : nullptr;
+  const uint32_t d4 = (uint32_t)(a.d >> 2);
+  const uint32_t chunk = (d4 + a.parts - 1) / a.parts;
+  const uint32_t beg = part * chunk;
+  const uint32_t end = min(d4, beg + chunk);
+  uint32_t pix = (beg + threadIdx.x) % HW4;  // float4 index inside the channel plane
+  Partial3 acc{0.f, 0.f, 0.f};
+  for (uint32_t e = beg + threadIdx.x; e < end; e += blockDim.x) {
+    const float4 z = z4[e], gg = __ldg(g4 + e), xk = xk4[e];  // z^{k+1} overwrites z in place
+    const float4 y = USE_Y ? __ldg(y4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 fb = USE_FB ? f4[e] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 fb2 = MODE == STEP_GRAD_MRI ? __ldg(f24 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 m = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (USE_M) {
+      const uchar4 mu = __ldg(m4 + pix);
+      m = make_float4((float)mu.x, (float)mu.y, (float)mu.z, (float)mu.w);
+    }
+    float4 x1, zn;
+    x1.x = step_x1<MODE>(a, z.x, gg.x, y.x, m.x, fb.x, fb2.x);
+    x1.y = step_x1<MODE>(a, z.y, gg.y, y.y, m.y, fb.y, fb2.y);
+    x1.z = step_x1<MODE>(a, z.z, gg.z, y.z, m.z, fb.z, fb2.z);
+    x1.w = step_x1<MODE>(a, z.w, gg.w, y.w, m.w, fb.w, fb2.w);
+    // z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4 of the next iteration) and the residual partials
+    const float dx = x1.x - xk.x, dy = x1.y - xk.y, dz = x1.z - xk.z, dw = x1.w - xk.w;
+    zn = make_float4(x1.x + a.beta * dx, x1.y + a.beta * dy, x1.z + a.beta * dz, x1.w + a.beta * dw);
+    xn4[e] = x1;
+    zn4[e] = zn;
+    if (isfinite(x1.x) && isfinite(x1.y) && isfinite(x1.z) && isfinite(x1.w)) {
+      acc.d2 += dx * dx + dy * dy + dz * dz + dw * dw;
+    } else {
+      acc.bad += 1.f;
+    }
+    acc.n2 += xk.x * xk.x + xk.y * xk.y + xk.z * xk.z + xk.w * xk.w;
+    pix += blockDim.x;
+    while (pix >= HW4) pix -= HW4;
+  }
+  block_reduce_store(acc, a.partials + ((long long)n * a.parts + part) * 3);
+}
+
 // ------------------------------------------------------------------ direct periodic blur
 // (A x)[m,n] = sum_{i,j} k[i,j] x[(m-i+kc) mod H, (n-j+kc) mod W]   (true convolution, Q8)
 // (A^T r)[m,n] = sum_{i,j} k[i,j] r[(m+i-kc) mod H, (n+j-kc) mod W] (correlation)
@@ -632,6 +711,16 @@ __global__ void inpaint_prox_kernel(const float* __restrict__ v, const float* __
 // ------------------------------------------------------------------ launchers
 void launch_pointwise_step(int mode, const StepArgs& a, cudaStream_t s) {
   dim3 grid(a.parts, a.N);
+  if (a.d % 4 == 0 && ((long long)a.H * a.W) % 4 == 0) {
+    switch (mode) {
+      case STEP_PROX_INPAINT: launch_k(pointwise_step_v4_kernel<STEP_PROX_INPAINT>, grid, 256, 0, s, a); return;
+      case STEP_GRAD_BUF: launch_k(pointwise_step_v4_kernel<STEP_GRAD_BUF>, grid, 256, 0, s, a); return;
+      case STEP_GRAD_INPAINT: launch_k(pointwise_step_v4_kernel<STEP_GRAD_INPAINT>, grid, 256, 0, s, a); return;
+      case STEP_GRAD_RICIAN: launch_k(pointwise_step_v4_kernel<STEP_GRAD_RICIAN>, grid, 256, 0, s, a); return;
+      case STEP_GRAD_MRI: launch_k(pointwise_step_v4_kernel<STEP_GRAD_MRI>, grid, 256, 0, s, a); return;
+      default: launch_k(pointwise_step_v4_kernel<STEP_X1_BUF>, grid, 256, 0, s, a); return;
+    }
+  }
   switch (mode) {
     case STEP_PROX_INPAINT: launch_k(pointwise_step_kernel<STEP_PROX_INPAINT>, grid, 256, 0, s, a); break;
     case STEP_GRAD_BUF: launch_k(pointwise_step_kernel<STEP_GRAD_BUF>, grid, 256, 0, s, a); break;
