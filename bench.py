@@ -204,6 +204,80 @@ def _config_dict(cfg, per_rank, world):
             "timed": "one ideq_solve of K iterations, tol=0 (no early stop)"}
 
 
+def _tiny_roofline(cfg, per, step_ms):
+    """C1's whole-solve kernel (one 8-SM cluster per image): ALU roofline of the algorithmic FLOPs
+    (network forward + input VJP, 2 FLOP / MAC, and the blur A z, A^T r) against the chip's derived
+    FFMA peak and against the 8 SMs one image's cluster can use."""
+    w, C, HW, ks = cfg["widths"][0], cfg["C"], cfg["H"] * cfg["W"], cfg["ksize"]
+    macs = 9 * (C * w + w * w + w * C) * HW * 2 + 2 * ks * ks * HW * C
+    flops = 2.0 * macs * per
+    ach = flops / (step_ms / 1000.0) / 1e12
+    chip = 148 * 128 * 2 * 1965e6 / 1e12
+    cluster = 8 * 128 * 2 * 1965e6 / 1e12 * per
+    return {"bound": "alu", "achieved": ach, "peak": chip, "unit": "TFLOP/s", "frac": ach / chip, "traffic": None,
+            "kernel": "tiny_solve_kernel (the whole solve in one launch, one 8-CTA cluster per image)",
+            "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz",
+            "frac_of_cluster_sms": ach / cluster, "us_per_iteration": step_ms * 1000.0,
+            "algorithmic_flops_per_step": flops, "launches_per_solve": 1}
+
+
+def _class_roofline(s, cfg, prec, per, args, ms, clk, peaks, peak_src):
+    cls = "conv_tc" if prec == "bf16" or cfg["net"] == "unet4" else "conv_simt"
+    reps = 20
+    kt = s.time_class(cls, reps)
+    st_t = s.time_class("step", reps)
+    ht_t = s.time_class("headtail", reps)
+    clocks = clk.summary()
+    # the class's time inside the device-timed step: its share of the bracketed iteration (event
+    # nodes at class boundaries of the replayed graph) times the step's own duration
+    step_ms = ms / args.steps
+    conv_ms = kt["share"] * step_ms
+    burst = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and ms < 1000.0
+                 and clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
+    if cls == "conv_simt":   # FFMA convolutions (C1's tiny net): ALU roofline
+        ffma_peak = 148 * 128 * 2 * 1965e6 / 1e12   # derived: SMs x FP32 lanes x 2 x max SM clock
+        ach = kt["flops"] / (conv_ms / 1000.0) / 1e12
+        roofline = {"bound": "alu", "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s", "frac": ach / ffma_peak,
+                    "traffic": None, "kernel": "conv_simt_kernel (all FFMA conv launches of a step)",
+                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"}
+    else:
+        # tensor peak of the path's own dtype: bf16 measured; 3xTF32 = measured bf16 x (TF32/bf16
+        # nominal ratio 1/2) / 3 MMAs per product
+        scale = 1.0 if prec == "bf16" else 0.5 / 3.0
+        pk_b = peaks.get("bf16_tflops") * scale
+        pk_s = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * scale
+        peak = pk_b if burst else pk_s
+        ach = kt["flops"] / (conv_ms / 1000.0) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "conv_tc_traffic.json")
+        if os.path.exists(tp) and args.config == "C3" and per == cfg["batch"] and prec == "bf16":
+            try:
+                traffic = json.load(open(tp)).get("bytes_per_launch")
+            except Exception:
+                traffic = None
+        roofline = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
+                    "traffic": traffic,
+                    "kernel": "conv_tc_kernel (all tcgen05 conv launches of a step)" + ("" if prec == "bf16" else
+                              ", 3xTF32 (kind::tf32, 3 MMAs per product)"),
+                    "peak_source": f"{peak_src} {'bf16_tflops (burst: sub-second region at max clock)' if burst else 'bf16_tflops_sustained'}"
+                                   + ("" if prec == "bf16" else " x 1/2 (TF32 nominal) / 3 (3xTF32)"),
+                    "frac_burst": ach / pk_b, "frac_sustained": ach / pk_s}
+    roofline.update({
+        "timing": f"ideq_time_class: event-record nodes at the class boundaries of one captured iteration, {reps} replays",
+        "ms_per_step": conv_ms, "share_of_step": kt["share"],
+        "class_ms_in_replay": kt["ms"], "replayed_iteration_ms": kt["iter_ms"],
+        "algorithmic_flops_per_step": kt["flops"], "algorithmic_bytes_per_step": kt["bytes"],
+        "launches_per_step": s.launches_per_iteration(),
+        "other_classes_ms_per_step": {"step": st_t["ms"], "headtail": ht_t["ms"]},
+        "step_kernel": {"bound": "hbm", "algorithmic_bytes_per_step": st_t["bytes"], "ms": st_t["ms"],
+                        "achieved_gbs": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9,
+                        "frac": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9 / peaks["hbm_gbs"],
+                        "peak_gbs": peaks["hbm_gbs"],
+                        "timing": "event nodes around the update's launches in the replayed iteration"},
+    })
+    return roofline
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -314,53 +388,11 @@ def main():
     #      order and launch configuration, captured into one CUDA graph and replayed back to back
     #      (ideq_time_class: CUDA events on the solve stream); its share of the device-timed step
     peaks, peak_src = _peaks()
-    cls = "conv_tc" if prec == "bf16" or cfg["net"] == "unet4" else "conv_simt"
-    reps = 20
-    kt = s.time_class(cls, reps)
-    st_t = s.time_class("step", reps)
-    ht_t = s.time_class("headtail", reps)
-    clocks = clk.summary()
-    burst = bool(clocks.get("sm_mhz") and clocks.get("sm_max_mhz") and ms * args.steps < 1000.0
-                 and clocks["sm_mhz"] >= 0.97 * clocks["sm_max_mhz"])
-    if cls == "conv_simt":   # FFMA convolutions (C1's tiny net): ALU roofline
-        ffma_peak = 148 * 128 * 2 * 1965e6 / 1e12   # derived: SMs x FP32 lanes x 2 x max SM clock
-        ach = kt["flops"] / (kt["ms"] / 1000.0) / 1e12
-        roofline = {"bound": "alu", "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s", "frac": ach / ffma_peak,
-                    "traffic": None, "kernel": "conv_simt_kernel (all FFMA conv launches of a step)",
-                    "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz"}
+    if s.launches_per_iteration() == 0:
+        roofline = _tiny_roofline(cfg, per, ms / args.steps)
     else:
-        # tensor peak of the path's own dtype: bf16 measured; 3xTF32 = measured bf16 x (TF32/bf16
-        # nominal ratio 1/2) / 3 MMAs per product
-        scale = 1.0 if prec == "bf16" else 0.5 / 3.0
-        pk_b = peaks.get("bf16_tflops") * scale
-        pk_s = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * scale
-        peak = pk_b if burst else pk_s
-        ach = kt["flops"] / (kt["ms"] / 1000.0) / 1e12
-        traffic = None
-        tp = os.path.join(ROOT, "profiles", "conv_tc_traffic.json")
-        if os.path.exists(tp) and args.config == "C3" and per == cfg["batch"] and prec == "bf16":
-            try:
-                traffic = json.load(open(tp)).get("bytes_per_launch")
-            except Exception:
-                traffic = None
-        roofline = {"bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak,
-                    "traffic": traffic,
-                    "kernel": "conv_tc_kernel (all tcgen05 conv launches of a step)" + ("" if prec == "bf16" else
-                              ", 3xTF32 (kind::tf32, 3 MMAs per product)"),
-                    "peak_source": f"{peak_src} {'bf16_tflops (burst: sub-second region at max clock)' if burst else 'bf16_tflops_sustained'}"
-                                   + ("" if prec == "bf16" else " x 1/2 (TF32 nominal) / 3 (3xTF32)"),
-                    "frac_burst": ach / pk_b, "frac_sustained": ach / pk_s}
-    roofline.update({
-        "timing": f"ideq_time_class: event-record nodes at the class boundaries of one captured iteration, {reps} replays",
-        "ms_per_step": kt["ms"], "share_of_step": kt["ms"] / (ms / args.steps),
-        "algorithmic_flops_per_step": kt["flops"], "algorithmic_bytes_per_step": kt["bytes"],
-        "launches_per_step": s.launches_per_iteration(),
-        "other_classes_ms_per_step": {"step": st_t["ms"], "headtail": ht_t["ms"]},
-        "step_kernel": {"bound": "hbm", "algorithmic_bytes_per_step": st_t["bytes"], "ms": st_t["ms"],
-                        "achieved_gbs": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9,
-                        "frac": st_t["bytes"] / (st_t["ms"] / 1000.0) / 1e9 / peaks["hbm_gbs"],
-                        "peak_gbs": peaks["hbm_gbs"]},
-    })
+        roofline = _class_roofline(s, cfg, prec, per, args, ms, clk, peaks, peak_src)
+    clocks = clk.summary()
 
     # ---- ms to tolerance (tol = 1e-4, per-image stop)
     tol_info = None
@@ -385,7 +417,7 @@ def main():
             "e2e": {"value": e2e_v, "unit": UNIT, "h2d_bytes_per_step": (yh.nbytes + xh.nbytes) / args.steps,
                     "d2h_bytes_per_step": xh.nbytes / args.steps,
                     "note": "one ideq_solve_host call of K iterations: H2D of y and x0, D2H of x-hat inside"},
-            "gpu_launches": s.launches_per_iteration() * args.steps + 4,
+            "gpu_launches": (s.launches_per_iteration() * args.steps + 4) if s.launches_per_iteration() else 1,
             "roofline": roofline, "clocks": clocks, "plan": s.plan()}
     if tol_info:
         line["ms_to_tolerance"] = tol_info

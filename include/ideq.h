@@ -282,11 +282,13 @@ IDEQ_API ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int rese
  * again into a CUDA graph (same kernels, order and launch configuration) with event-record nodes
  * wherever the class of consecutive launches changes, and replayed `reps` times; *ms = the summed
  * duration of the class's runs of launches per iteration (<= the iteration's time by
- * construction); flops / bytes = the class's algorithmic FLOPs and HBM bytes per iteration. The
+ * construction); flops / bytes = the class's algorithmic FLOPs and HBM bytes per iteration;
+ * iter_ms (may be NULL) = the summed duration of every class's runs, i.e. the bracketed
+ * iteration (ms / iter_ms = the class's share of an iteration). The
  * update writes into scratch: the caller's buffers are untouched, the context's solver state is
  * overwritten. IDEQ_E_STATE before the first solve. */
 IDEQ_API ideq_status ideq_time_class(ideq_ctx* ctx, int kernel_class, int reps, double* ms, double* flops,
-                                     double* bytes);
+                                     double* bytes, double* iter_ms);
 
 /* Number of kernel launches one iteration issues (for the bench's gpu_launches). */
 IDEQ_API int ideq_launches_per_iteration(const ideq_ctx* ctx);

@@ -277,7 +277,8 @@ struct TcParams {
   uint32_t epi_tx_bytes;   // TMA bytes of one aux tile (R*Wt rows x BN columns)
   uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x (R+2) x KC halo buffer (1 KB aligned)
   int stagesB;             // MODE 2: depth of the weight ring
-  int nacc;                // TMEM accumulator stages (2..4)
+  int nacc;                // TMEM accumulator stages (2..8)
+  int nsplit;              // 3xTF32: partial accumulators per tile (summed in fp32 by the epilogue)
   // EPI_IMG: the first img_c GEMM columns are an image (tail / head adjoint); written as fp32
   // NCHW planes [N][img_c][OH][OW] plus img_alpha * img_aux (same layout, may be null)
   float* img_out;
@@ -580,7 +581,11 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
     for (int L = t0; L < tot_it; L += tstep) {
       mbar_wait(tempty0 + 8u * acc, aph ^ 1u);
       tc_fence_after();
-      const uint32_t d_tmem = tmem_base + (uint32_t)(acc * BN);
+      // 3xTF32: K step i of the tile accumulates into partial accumulator i % G (G = nsplit), so no
+      // fp32 accumulation chain in TMEM is longer than K / (8 G) MMAs (the tensor core's fp32 adds
+      // are not round-to-nearest: their error grows with the chain, tools/x3_accuracy.py)
+      const int G = X3 ? P.nsplit : 1;
+      const uint32_t d_base = tmem_base + (uint32_t)(acc * BN * G);
       if (HALO) {
         for (int ch = 0; ch < g.nchunk; ++ch) {
           mbar_wait(ready0 + 8u * s, ph);
@@ -597,7 +602,8 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
             } else {
               bd = dB0 + (((uint32_t)(tap * g.nchunk + ch) * b_stage) >> 4);
             }
-            mma_k(d_tmem, ad, bd, (uint32_t)(ch | tap));
+            const int i = ch * 9 + tap;
+            mma_k(d_base + (uint32_t)((i % G) * BN), ad, bd, (uint32_t)(i >= G));
             if (STREAMB) {
               mma_commit_elect(emptyB0 + 8u * sb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
@@ -611,7 +617,8 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
           mbar_wait(ready0 + 8u * s, ph);
           if (X3) mbar_wait(full0 + 8u * s, ph);  // the B boxes of the stage (same transaction)
           tc_fence_after();
-          mma_k(d_tmem, dA0 + ((s * a_stage) >> 4), dB0 + ((s * bslot) >> 4), (uint32_t)kb);
+          mma_k(d_base + (uint32_t)((kb % G) * BN), dA0 + ((s * a_stage) >> 4), dB0 + ((s * bslot) >> 4),
+                (uint32_t)(kb >= G));
           mma_commit_elect(empty0 + 8u * s);
           if (++s == S) { s = 0; ph ^= 1u; }
         }
@@ -675,10 +682,18 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
         if (++acc == NA) { acc = 0; aph ^= 1u; }
         continue;
       }
+      const int G = X3 ? P.nsplit : 1;
 #pragma unroll 1
       for (int c0 = cbeg; c0 < cend; c0 += 16) {
         float v[16];
-        tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+        const uint32_t tq = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN * G + c0);
+        tmem_ld16(tq, v);
+        for (int j = 1; j < G; ++j) {  // 3xTF32 partial accumulators, summed in fp32 (RNE)
+          float u[16];
+          tmem_ld16(tq + (uint32_t)(j * BN), u);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] += u[e];
+        }
         const uint32_t box = ebuf + (uint32_t)(c0 / BOXC) * P.epi_box_bytes;
         constexpr int VPC = 16 / ES;               // values per 16-byte chunk
         const int j0 = ((c0 % BOXC) * ES) >> 4;    // first chunk of these 16 columns in the row
@@ -1028,10 +1043,10 @@ struct TcPlan {
   size_t smem;
 };
 
-// N tile: up to 128 columns (bf16); 64 in 3xTF32 (fp32 staging and the hi / lo operand pairs
-// double every shared-memory buffer)
+// N tile: up to 128 columns (bf16); 32 in 3xTF32 (fp32 staging and the hi / lo operand pairs
+// double every shared-memory buffer, and each tile keeps up to 8 partial accumulators in TMEM)
 static int tc_bn(const ConvGeom& g, bool x3) {
-  const int cap = x3 ? 64 : 128;
+  const int cap = x3 ? 32 : 128;
   return g.ncols >= cap ? cap : g.ncols;
 }
 
@@ -1194,7 +1209,10 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, bool x3, const void* in, const void* 
   const int min_stages = p->halo ? 2 : (short_k ? 2 : 3), max_stages = p->halo ? 4 : (short_k ? 4 : 8);
   int stages = 0, ctas = 1, nacc = 0;
   uint32_t tcols = 0;
-  const uint32_t acc_w = (uint32_t)BN;  // TMEM columns per stage
+  // 3xTF32: up to 8 partial accumulators per tile (one per K step of the tile, cyclically)
+  const int ksteps = p->halo ? 9 * g.nchunk : g.ntaps * g.nchunk;
+  P.nsplit = x3 ? (ksteps < 8 ? ksteps : 8) : 1;
+  const uint32_t acc_w = (uint32_t)BN * P.nsplit;  // TMEM columns per stage
   const int na0 = (8 * acc_w <= 256 && p->halo) ? 8 : ((BN <= 64 || short_k) && 4 * acc_w <= 512 ? 4 : 2);
   const size_t nbar = 64 * 8 + 64;  // barriers and the TMEM holder
   for (int na = na0; na >= 2 && !stages; na -= 2) {

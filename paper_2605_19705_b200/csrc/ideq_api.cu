@@ -154,6 +154,7 @@ struct ideq_ctx {
   size_t net_bytes = 0;
   // the last solve's step arguments (class timing replays its kernels)
   bool have_last = false;
+  bool last_fused = false;  // the last solve ran the whole-solve tiny-network kernel
   int last_N = 0;
   StepArgs last_a{};
   FinalizeArgs last_f{};
@@ -1182,12 +1183,59 @@ ideq_status operator_runnable(ideq_ctx* ctx) {
   return IDEQ_OK;
 }
 
+ideq_status finish_solve(ideq_ctx* ctx, float* x, int N, const ideq_params* p, ideq_image_stat* stats,
+                         float* trace_host, bool next1);
+
+// The whole solve of a tiny-network deblurring problem (BASELINE C1) fits one persistent kernel per
+// image (tiny_solve.cu): no per-iteration launches. Eligible: TINY3 with hidden width 16, C = 1,
+// identity skip, softplus, fp32, direct blur gradient step, per-image stop, no restart /
+// averaging, not profiling.
+bool tiny_fused_ok(ideq_ctx* ctx, const ideq_params* p) {
+  const auto& n = ctx->net;
+  const auto& op = ctx->op;
+  return n.arch == IDEQ_NET_TINY3 && n.widths[0] == 16 && ctx->C == 1 && n.identity_skip &&
+         n.act == IDEQ_ACT_SOFTPLUS && ctx->prec == IDEQ_PREC_FP32 && op.kind == IDEQ_OP_BLUR &&
+         op.step == IDEQ_STEP_GRAD && op.blur_impl == IDEQ_BLUR_DIRECT && p->stop_rule == IDEQ_STOP_PER_IMAGE &&
+         !p->restart && !p->averaging && !ctx->profiling && tiny_solve_supported(ctx->H, ctx->W, op.ksize);
+}
+
+ideq_status launch_tiny_fused(ideq_ctx* ctx, const float* y, float* x, int N, const ideq_params* p) {
+  if (!ctx->wdev.count("tiny#blob")) {  // the fp32 blob (c1, c2, c3 in blob order), uploaded once
+    ideq_status st = upload_f32(ctx, "tiny#blob", ctx->blob);
+    if (st) return st;
+  }
+  const float* wb = (const float*)ctx->wdev["tiny#blob"];
+  const int w = 16, C = 1;
+  TinySolveArgs a{};
+  a.N = N; a.H = ctx->H; a.W = ctx->W; a.ks = ctx->op.ksize; a.kper = ctx->op.kernel_per_image;
+  a.kern = ctx->d_kern;
+  a.w1 = wb; a.w2 = wb + w * C * 9; a.w3 = wb + w * C * 9 + w * w * 9;
+  a.y = y; a.x = x;
+  a.lam = p->lambda; a.tau = p->tau; a.beta = p->beta; a.tol = p->tol;
+  a.max_iter = p->max_iter; a.check_every = p->check_every;
+  a.iters = ctx->iters; a.res = ctx->res; a.status = ctx->status;
+  a.trace = ctx->trace; a.trace_cap = ctx->trace_cap; a.kdone = ctx->kdev;
+  CK(cudaMemsetAsync(ctx->trace, 0, sizeof(float) * ctx->trace_cap, ctx->stream));
+  CK(cudaMemsetAsync(ctx->kdev, 0, sizeof(int), ctx->stream));
+  launch_tiny_solve(a, ctx->stream);
+  CK(cudaGetLastError());
+  return IDEQ_OK;
+}
+
 ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const ideq_params* p,
                          ideq_image_stat* stats, float* trace_host) {
   ideq_status st;
   if ((st = validate_params(ctx, N, p))) return st;
   if ((st = operator_runnable(ctx))) return st;
   if (!y || !x || !stats) return fail(ctx, IDEQ_E_INVALID, "NULL y/x/stats");
+  const bool fused = tiny_fused_ok(ctx, p);
+  ctx->last_fused = fused;
+  if (fused) {
+    ctx->have_last = true;
+    ctx->last_N = N;
+    if ((st = launch_tiny_fused(ctx, y, x, N, p))) return st;
+    return finish_solve(ctx, x, N, p, stats, trace_host, false);
+  }
   if ((st = prepare_programs(ctx, N))) return st;
   const long long d = (long long)ctx->C * ctx->H * ctx->W;
   cudaStream_t s = ctx->stream;
@@ -1261,9 +1309,17 @@ ideq_status solve_device(ideq_ctx* ctx, const float* y, float* x, int N, const i
   }
   launch_gather(ctx->iters, ctx->X1, x, N, d, s);
   if (p->averaging) launch_avg_out(ctx->k0, ctx->status, ctx->iters, p->max_iter, ctx->Xsnap, x, N, d, s);
+  return finish_solve(ctx, x, N, p, stats, trace_host, true);
+}
+
+// Per-image statistics and the trace back to the host; IDEQ_E_DIVERGED if any image diverged.
+ideq_status finish_solve(ideq_ctx* ctx, float* x, int N, const ideq_params* p, ideq_image_stat* stats,
+                         float* trace_host, bool next1) {
+  (void)x;
+  cudaStream_t s = ctx->stream;
   std::vector<int> it(N), stv(N), nr(N, 0), k0v(N, -1);
-  if (p->restart) CK(cudaMemcpyAsync(nr.data(), ctx->nrest, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
-  if (p->averaging) CK(cudaMemcpyAsync(k0v.data(), ctx->k0, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  if (next1 && p->restart) CK(cudaMemcpyAsync(nr.data(), ctx->nrest, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
+  if (next1 && p->averaging) CK(cudaMemcpyAsync(k0v.data(), ctx->k0, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
   std::vector<float> rs(N);
   CK(cudaMemcpyAsync(it.data(), ctx->iters, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(stv.data(), ctx->status, sizeof(int) * N, cudaMemcpyDeviceToHost, s));
@@ -1304,6 +1360,7 @@ void init_kernel_attributes() {
   init_attrs_tc();
   init_attrs_step();
   init_attrs_fft();
+  init_attrs_tiny();
   done = true;
 }
 }  // namespace ideq
@@ -2098,10 +2155,13 @@ ideq_status ideq_jfb_grad(ideq_ctx* ctx, const float* y, const float* x_hat, con
   return IDEQ_OK;
 }
 
-ideq_status ideq_time_class(ideq_ctx* ctx, int cls, int reps, double* ms, double* flops, double* bytes) {
+ideq_status ideq_time_class(ideq_ctx* ctx, int cls, int reps, double* ms, double* flops, double* bytes,
+                            double* iter_ms) {
   ideq_status st;
   if ((st = check_ctx(ctx))) return st;
   if (!ctx->have_last) return fail(ctx, IDEQ_E_STATE, "ideq_time_class needs a solve first");
+  if (ctx->last_fused)
+    return fail(ctx, IDEQ_E_UNSUPPORTED, "the last solve ran the whole-solve kernel: no iteration graph to time");
   if (!ms || reps < 1 || cls < 0 || cls >= IDEQ_K_NCLASSES || cls == IDEQ_K_FIDELITY)
     return fail(ctx, IDEQ_E_INVALID, "class must be CONV_TC, CONV_SIMT, HEADTAIL, STEP or REDUCE; reps >= 1");
   cudaStream_t s = ctx->stream;
@@ -2134,19 +2194,22 @@ ideq_status ideq_time_class(ideq_ctx* ctx, int cls, int reps, double* ms, double
   cudaGraphDestroy(graph);
   CK(cudaGraphLaunch(ge, s));  // warm-up
   CK(cudaStreamSynchronize(s));
-  double tot = 0.0;
+  double tot = 0.0, all = 0.0;
   for (int r = 0; r < reps; ++r) {
     CK(cudaGraphLaunch(ge, s));
     CK(cudaStreamSynchronize(s));
-    for (auto& pr : T.seg[cls]) {
-      float t = 0.f;
-      cudaError_t e = cudaEventElapsedTime(&t, pr.first, pr.second);
-      if (e != cudaSuccess) { cudaGraphExecDestroy(ge); return fail(ctx, IDEQ_E_CUDA, "class timing: %s", cudaGetErrorString(e)); }
-      tot += t;
-    }
+    for (int c = 0; c < IDEQ_K_NCLASSES; ++c)
+      for (auto& pr : T.seg[c]) {
+        float t = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&t, pr.first, pr.second);
+        if (e != cudaSuccess) { cudaGraphExecDestroy(ge); return fail(ctx, IDEQ_E_CUDA, "class timing: %s", cudaGetErrorString(e)); }
+        all += t;
+        if (c == cls) tot += t;
+      }
   }
   cudaGraphExecDestroy(ge);
   *ms = tot / reps;
+  if (iter_ms) *iter_ms = all / reps;
   const bool step = cls == IDEQ_K_STEP;  // the step's fidelity passes count with it
   if (flops) *flops = ctx->cnt_flops[cls] + (step ? ctx->cnt_flops[IDEQ_K_FIDELITY] : 0.0);
   if (bytes) *bytes = ctx->cnt_bytes[cls] + (step ? ctx->cnt_bytes[IDEQ_K_FIDELITY] : 0.0);
@@ -2168,7 +2231,7 @@ ideq_status ideq_get_profile(ideq_ctx* ctx, ideq_profile* out, int reset) {
 }
 
 int ideq_launches_per_iteration(const ideq_ctx* ctx) {
-  if (!ctx || !ctx->have_last) return 0;
+  if (!ctx || !ctx->have_last || ctx->last_fused) return 0;  // fused: one launch per solve
   int n = 0;
   for (int first = 0; first < ctx->last_N; first += ctx->mb) {
     const int m = ctx->last_N - first < ctx->mb ? ctx->last_N - first : ctx->mb;

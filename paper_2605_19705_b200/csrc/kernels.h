@@ -174,6 +174,27 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
                         const int* n_act, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s);
 
+// Whole-solve persistent kernel of the tiny network (tiny_solve.cu): one 8-CTA cluster per image.
+struct TinySolveArgs {
+  int N, H, W, ks, kper;
+  const float* kern;
+  const float *w1, *w2, *w3;  // c1 [16][1][3][3], c2 [16][16][3][3], c3 [1][16][3][3] (blob order)
+  const float* y;
+  float* x;                   // in: x^0, out: x-hat
+  float lam, tau, beta, tol;
+  int max_iter, check_every;
+  int* iters;
+  float* res;
+  int* status;
+  float* trace;  // zeroed by the caller
+  int trace_cap;
+  int* kdone;    // zeroed by the caller
+};
+bool tiny_solve_supported(int H, int W, int ks);
+size_t tiny_solve_smem(int H, int W, int ks);
+void launch_tiny_solve(const TinySolveArgs& a, cudaStream_t s);
+void init_attrs_tiny();
+
 // Raise the dynamic shared-memory limit of every kernel once (before any graph capture).
 void init_kernel_attributes();
 void init_attrs_simt();

@@ -86,7 +86,8 @@ def load_library(path: str = LIB_PATH):
     lib.ideq_create_ex.argtypes = [C.POINTER(NetDesc), i, i, vp, i, i, i, C.POINTER(Dist), C.POINTER(PlanOpts),
                                    C.POINTER(vp)]
     lib.ideq_get_plan.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_size_t)]
-    lib.ideq_time_class.argtypes = [vp, i, i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.ideq_time_class.argtypes = [vp, i, i, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_double)]
     lib.ideq_set_operator.argtypes = [vp, C.POINTER(OperatorDesc), i]
     lib.ideq_solve.argtypes = [vp, vp, vp, i, C.POINTER(Params), C.POINTER(ImageStat), fp]
     lib.ideq_solve_host.argtypes = [vp, vp, vp, i, C.POINTER(Params), C.POINTER(ImageStat), fp]
@@ -309,10 +310,11 @@ class Solver:
     def time_class(self, cls: str, reps: int = 10) -> dict:
         """In-graph timing of one kernel class of the last solve's iteration (ideq_time_class):
         ms per iteration and the class's algorithmic FLOPs / bytes per iteration."""
-        ms, fl, by = C.c_double(), C.c_double(), C.c_double()
+        ms, fl, by, it = C.c_double(), C.c_double(), C.c_double(), C.c_double()
         self._check(self.lib.ideq_time_class(self.ctx, KCLASS.index(cls), int(reps), C.byref(ms), C.byref(fl),
-                                             C.byref(by)))
-        return {"ms": ms.value, "flops": fl.value, "bytes": by.value}
+                                             C.byref(by), C.byref(it)))
+        return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "iter_ms": it.value,
+                "share": ms.value / it.value if it.value > 0 else None}
 
     def launches_per_iteration(self) -> int:
         return int(self.lib.ideq_launches_per_iteration(self.ctx))

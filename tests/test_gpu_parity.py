@@ -256,3 +256,31 @@ def test_direct_blur_kernel_sizes(ks, H, W):
     for b in range(xg.shape[0]):
         assert rel_l2(xg[b], orc["x"][b]) <= 1e-4
         assert abs(st["residual"][b] - orc["residual"][b]) <= 1e-6
+
+
+@pytest.mark.parametrize("batch,tol,K", [(1, 0.0, 100), (3, 0.0, 40), (3, 5e-4, 200)])
+def test_tiny_whole_solve_kernel(batch, tol, K):
+    """C1's whole solve in one launch (tiny_solve.cu: one 8-CTA cluster per image, DSMEM halos):
+    fp32 iterates within 1e-4 and residuals within 1e-6 of the oracle, stop iterations equal
+    (tol > 0, per-image rule), and the same result as the per-iteration kernels (the profiling
+    mode launches those eagerly) within fp32 rounding."""
+    torch = torch_cuda()
+    cfg = _mini("C1", batch=batch)
+    prob = synth.make_problem(cfg)
+    orc = osolver.solve_config(cfg, prob, max_iter=K, tol=tol, trace=True)
+    s = _solver(cfg, prob, "fp32")
+    outs = []
+    for prof in (False, True):
+        s.set_profiling(prof)
+        xd = _dev(torch, prob["x0"])
+        st, code, tr = s.solve(_dev(torch, prob["y"]), xd, s.params(max_iter=K, tol=tol), trace=True)
+        assert (s.launches_per_iteration() == 0) == (not prof)   # fused <=> one launch per solve
+        outs.append((st, xd.cpu().numpy(), tr))
+    for st, x, tr in outs:
+        assert np.array_equal(st["iters"], orc["iters"]) and np.array_equal(st["status"], orc["status"])
+        for b in range(batch):
+            assert rel_l2(x[b], orc["x"][b]) <= 1e-4
+            assert abs(st["residual"][b] - orc["residual"][b]) <= 1e-6
+        n = int(orc["iters"].max())
+        assert np.allclose(tr[:n], orc["rmax_trace"][:n], rtol=1e-3, atol=1e-6)
+    assert rel_l2(outs[0][1], outs[1][1]) <= 1e-5

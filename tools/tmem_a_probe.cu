@@ -44,6 +44,24 @@ __device__ __forceinline__ void mma_ss(uint32_t d, uint64_t adesc, uint64_t bdes
 __device__ __forceinline__ void cp128x256(uint32_t taddr, uint64_t sdesc) {
   asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(taddr), "l"(sdesc) : "memory");
 }
+__device__ __forceinline__ void mma_ts_e(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_ss_e(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void cp_e(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}\n"
+               ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void commit_wait(uint32_t bar, uint32_t& ph) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
   asm volatile(
@@ -154,25 +172,34 @@ __global__ void __launch_bounds__(128, 1) rate(int n, int iters, int mode, long 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_holder;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {
     const uint32_t idesc = make_idesc_bf16(n);
     const uint64_t ad = make_sdesc(base, 512u, 4u), bd = make_sdesc(base + 32 * 1024, 512u, 4u);
     uint32_t ph = 0;
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
       if (mode == 0) {
-        for (int k = 0; k < 8; ++k) mma_ts(tmem, tmem + 256 + k * 8, bd + 2ull * (k & 1), idesc, 1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_ts_e(tmem, tmem + 256 + k * 8, bd + 2ull * (k & 1), idesc, 1);
       } else if (mode == 1) {
-        for (int k = 0; k < 8; ++k) mma_ss(tmem, ad + 2ull * (k & 1), bd + 2ull * (k & 1), idesc, 1);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_ss_e(tmem, ad + 2ull * (k & 1), bd + 2ull * (k & 1), idesc, 1);
       } else if (mode == 2) {
-        for (int k = 0; k < 8; ++k) cp128x256(tmem + 256 + (k & 7) * 8, ad + 2ull * (k & 1));
+#pragma unroll
+        for (int k = 0; k < 8; ++k) cp_e(tmem + 256 + k * 8, ad + 2ull * (k & 1));
       } else {
-        for (int k = 0; k < 6; ++k) cp128x256(tmem + 256 + ((it & 3) * 48) % 192 + k * 8, ad + 4ull * k);
-        for (int k = 0; k < 18; ++k) mma_ts(tmem + (it & 3) * 32, tmem + 256 + (k % 18) * 8 % 192, bd + 2ull * (k & 1), idesc, 1);
+        const uint32_t slot = (uint32_t)(it & 3) * 48u;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) cp_e(tmem + 256 + ((slot + k * 8) % 192), ad + 4ull * k);
+#pragma unroll
+        for (int k = 0; k < 18; ++k) mma_ts_e(tmem + (it & 3) * 32, tmem + 256 + ((k * 8) % 192), bd + 2ull * (k & 1), idesc, 1);
       }
     }
-    commit_wait(smem_u32(&bar), ph);
-    out[blockIdx.x] = clock64() - t0;
+    if (threadIdx.x == 0) {
+      commit_wait(smem_u32(&bar), ph);
+      out[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
