@@ -8,11 +8,21 @@
 //
 // One image = one thread-block cluster of 8 CTAs (a batch runs one cluster per image). CTA r owns
 // rows [r R, (r + 1) R) of the image (R = H / 8) and keeps every tensor of the iteration for those
-// rows plus a halo of HB rows above and below: z, the blur residual, U, and the 16-channel
-// activations a1, a2 and cotangents q2, q1. After each stage the CTAs meet at a cluster barrier
-// and copy the halo rows they need from their neighbours' shared memory (DSMEM). The residual's
-// three partial sums are written into every CTA's shared memory and combined in fp64 in a fixed
-// order, so all 8 CTAs take the identical stop decision without a second barrier.
+// rows plus halo rows above and below. A stage's producer PUSHES its boundary rows straight into
+// the neighbours' halo rows (st.shared::cluster, DSMEM) as it computes them, so one cluster barrier
+// per stage both publishes a tensor and completes every halo -- no copy phase. Cheap layers are
+// recomputed on the halo rows instead of exchanged (a1 and U on rows -1 and R), which removes two
+// of the barriers: 6 per iteration. The residual's three partial sums are pushed into every CTA
+// and combined in fp64 in a fixed order, so all 8 CTAs take the identical stop decision.
+//
+// Layouts: the network tensors (a1, a2, q2, q1 with 16 channels, U) are planes of (R + 4) rows x
+// (W + 2) columns whose border (columns -1 and W, and halo rows outside the image) is zero, so the
+// 3x3 convolutions read without bounds checks. The blur operands (z, the residual rb) are planes of
+// (R + 2 kc) rows x (W + 2 kc) columns with PERIODIC borders (the blur is a circular convolution,
+// reading Q9); c1 reads z through an explicit zero-padding mask. The 16 -> 16 convolutions give a
+// thread 2 rows x 4 output channels (register blocking: 12 input and 9 weight loads per 72 FMAs);
+// the single-channel outputs and the blur split the contraction over adjacent lanes, combined by
+// fixed-order shuffles.
 //
 // fp32 throughout (the FFMA path's arithmetic: exact fp32 softplus / sigmoid), matching the fp32
 // parity mode. Supported: TINY3 with hidden width 16, C = 1, identity skip, softplus, direct blur
@@ -22,9 +32,9 @@
 
 namespace ideq {
 
-constexpr int TS_P = 8;          // CTAs per image (cluster size)
-constexpr int TS_T = 256;        // threads per CTA
-constexpr int TS_C = 16;         // hidden width
+constexpr int TS_P = 8;    // CTAs per image (cluster size)
+constexpr int TS_T = 512;  // threads per CTA: 4 per pixel for R x W = 128
+constexpr int TS_C = 16;   // hidden width
 
 __device__ __forceinline__ uint32_t ts_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -51,30 +61,47 @@ __device__ __forceinline__ uint32_t ts_rank() {
   return r;
 }
 
-// Shared-memory layout (floats): halo planes hold rows -HB .. R+HB-1 of one channel, PL = (R+2HB) W.
+// Shared-memory layout (floats).
 struct TsLayout {
-  int R, W, HB, PL;
-  int z, rb, u, a1, a2, q2, q1;    // halo planes (a1..q1: 16 channels each)
-  int xk, gf, gg, y;               // own-row planes (R W)
+  int R, W, kc;
+  int WP, PN;      // network planes: pitch W + 2, (R + 4) rows (2 halo rows each side)
+  int WB, PB, HB;  // blur planes: pitch W + 2 kc, (R + 2 HB) rows, HB = max(kc, 1)
+  int z, rb, u, a1, a2, q2, q1;
+  int xk, gf, xn, y;
   int w1f, w2f, w3f, w1t, w2t, w3t, kern, red;
   int total;
-  __host__ __device__ void init(int R_, int W_, int HB_, int ks) {
-    R = R_; W = W_; HB = HB_;
-    PL = (R + 2 * HB) * W;
+  __host__ __device__ void init(int R_, int W_, int ks) {
+    R = R_; W = W_; kc = (ks - 1) / 2;
+    HB = kc > 1 ? kc : 1;
+    WP = W + 2; PN = (R + 4) * WP;
+    WB = W + 2 * kc; PB = (R + 2 * HB) * WB;
     int o = 0;
     auto take = [&](int n) { const int b = o; o += (n + 3) & ~3; return b; };
-    z = take(PL); rb = take(PL); u = take(PL);
-    a1 = take(TS_C * PL); a2 = take(TS_C * PL); q2 = take(TS_C * PL); q1 = take(TS_C * PL);
-    xk = take(R * W); gf = take(R * W); gg = take(R * W); y = take(R * W);
+    z = take(PB); rb = take(PB); u = take(PN);
+    a1 = take(TS_C * PN); a2 = take(TS_C * PN); q2 = take(TS_C * PN); q1 = take(TS_C * PN);
+    xk = take(R * W); gf = take(R * W); xn = take(R * W); y = take(R * W);
     w1f = take(9 * TS_C); w2f = take(TS_C * 9 * TS_C); w3f = take(TS_C * 9);
     w1t = take(TS_C * 9); w2t = take(TS_C * 9 * TS_C); w3t = take(9 * TS_C);
     kern = take(ks * ks); red = take(TS_P * 4);
     total = o;
   }
+  __device__ int n_at(int plane, int ch, int r, int c) const { return plane + ch * PN + (r + 2) * WP + c + 1; }
+  __device__ int b_at(int plane, int r, int c) const { return plane + (r + HB) * WB + c + kc; }
 };
 
+#ifndef TS_PROF
+#define TS_PROF 0
+#endif
+__device__ long long ts_prof[16];  // TS_PROF builds: clock64 per stage, summed over iterations (CTA 0)
+#define TS_MARK(i)                                                   \
+  if (TS_PROF && blockIdx.x == 0 && threadIdx.x == 0) {              \
+    const long long now = clock64();                                 \
+    ts_prof[i] += now - t_mark;                                      \
+    t_mark = now;                                                    \
+  }
+
 struct TinyArgs {
-  int N, H, W, R, HB, ks, kper;
+  int N, H, W, R, ks, kper;
   const float* kern;  // [1 or N][ks][ks]
   const float* w1;    // c1 [16][1][3][3]
   const float* w2;    // c2 [16][16][3][3]
@@ -91,32 +118,70 @@ struct TinyArgs {
   int* kdone;    // iterations run by the longest image (atomicMax)
 };
 
-// Copy rows [-h, -1] and [R, R + h - 1] of `nch` halo planes starting at smem float offset `off`
-// from the owners' shared memory (periodic in the image row; conv stages mask rows outside the
-// image themselves).
-__device__ __forceinline__ void ts_halo(float* sm, const TsLayout& L, int off, int nch, int h, int row0, int H) {
-  const uint32_t base = ts_smem_u32(sm);
-  const int per = 2 * h * L.W;
-  for (int t = threadIdx.x; t < nch * per; t += TS_T) {
-    const int ch = t / per, q = t % per;
-    const int rr = q / L.W, c = q % L.W;
-    const int r = rr < h ? rr - h : L.R + (rr - h);  // local row
-    int gr = row0 + r;
-    gr = ((gr % H) + H) % H;
-    const uint32_t src_cta = (uint32_t)(gr / L.R), src_row = (uint32_t)(gr % L.R);
-    const int src = off + ch * L.PL + (int)(src_row + L.HB) * L.W + c;
-    sm[off + ch * L.PL + (r + L.HB) * L.W + c] = ts_ld_cluster(ts_mapa(base + 4u * (uint32_t)src, src_cta));
+// Store v at row r (own, 0 <= r < R), column c of a network plane and push it into the halo rows of
+// the CTAs above (their row R + r, if r < nh) and below (their row r - R, if r >= R - nh); image
+// borders have no neighbour there (those halo rows stay zero = the convolutions' zero padding).
+__device__ __forceinline__ void ts_put_net(float* sm, const TsLayout& L, int o, float v, int r, int rank, int H, int nh,
+                                          uint32_t base) {
+  sm[o] = v;
+  if (r < nh && rank > 0) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)(o + L.R * L.WP), (uint32_t)(rank - 1)), v);
+  if (r >= L.R - nh && (rank + 1) * L.R < H)
+    ts_st_cluster(ts_mapa(base + 4u * (uint32_t)(o - L.R * L.WP), (uint32_t)(rank + 1)), v);
+}
+// Store v at (r, c) of a blur plane, its periodic column copies, and push the row into the
+// neighbours' halo rows (periodic in the image: the first CTA's rows are the last one's lower halo).
+__device__ __forceinline__ void ts_put_blur(float* sm, const TsLayout& L, int plane, int r, int c, float v, int rank,
+                                           uint32_t base) {
+  int cols[2] = {c, c};
+  int nc = 1;
+  if (c < L.kc) cols[nc++] = c + L.W;
+  else if (c >= L.W - L.kc) cols[nc++] = c - L.W;
+  const uint32_t up = (uint32_t)((rank + TS_P - 1) % TS_P), dn = (uint32_t)((rank + 1) % TS_P);
+  for (int i = 0; i < nc; ++i) {
+    sm[L.b_at(plane, r, cols[i])] = v;
+    if (r < L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r + L.R, cols[i]), up), v);
+    if (r >= L.R - L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r - L.R, cols[i]), dn), v);
   }
 }
 
 __device__ __forceinline__ float ts_softplus(float t) { return fmaxf(t, 0.f) + log1pf(__expf(-fabsf(t))); }
 __device__ __forceinline__ float ts_dsp(float a) { return -expm1f(-a); }  // sigmoid(p) from a = sp(p)
+// fixed-order sums over the 4 (2) adjacent lanes of one pixel
+__device__ __forceinline__ float ts_sum4(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
 
-// in-plane value with the conv's zero padding: local row r (may be in the halo), column c
-__device__ __forceinline__ float ts_at(const float* p, const TsLayout& L, int r, int c, int row0, int H) {
-  const int gr = row0 + r;
-  if (gr < 0 || gr >= H || c < 0 || c >= L.W) return 0.f;
-  return p[(r + L.HB) * L.W + c];
+// 16 -> 16 3x3 convolution, 2 output rows (r0, r0 + 1) x 4 output channels (4q .. 4q + 3) at column c;
+// w: [ci][tap][co] (forward) or, ADJ (conv3x3^T: flipped taps), [co][tap][ci] -- same indexing
+template <bool ADJ>
+__device__ __forceinline__ void ts_conv16(const float* sm, const TsLayout& L, int in_plane, int w, int r0, int c,
+                                          int q, float (&acc)[2][4]) {
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
+#pragma unroll 2
+  for (int ci = 0; ci < TS_C; ++ci) {
+    const float* in = sm + L.n_at(in_plane, ci, r0, c);
+    float v[4][3];  // input rows r0 - 1 .. r0 + 2, columns c - 1 .. c + 1
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) v[a][b] = in[(a - 1) * L.WP + (b - 1)];
+#pragma unroll
+    for (int tap = 0; tap < 9; ++tap) {
+      const int ta = tap / 3, tb = tap % 3;
+      const float x0 = ADJ ? v[2 - ta][2 - tb] : v[ta][tb];
+      const float x1 = ADJ ? v[3 - ta][2 - tb] : v[ta + 1][tb];
+      const float4 wv = *reinterpret_cast<const float4*>(sm + w + (ci * 9 + tap) * TS_C + 4 * q);
+      acc[0][0] = fmaf(wv.x, x0, acc[0][0]); acc[0][1] = fmaf(wv.y, x0, acc[0][1]);
+      acc[0][2] = fmaf(wv.z, x0, acc[0][2]); acc[0][3] = fmaf(wv.w, x0, acc[0][3]);
+      acc[1][0] = fmaf(wv.x, x1, acc[1][0]); acc[1][1] = fmaf(wv.y, x1, acc[1][1]);
+      acc[1][2] = fmaf(wv.z, x1, acc[1][2]); acc[1][3] = fmaf(wv.w, x1, acc[1][3]);
+    }
+  }
 }
 
 __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
@@ -126,15 +191,18 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
   const int H = A.H, W = A.W, R = A.R;
   const int row0 = rank * R;
   TsLayout L;
-  L.init(R, W, A.HB, A.ks);
+  L.init(R, W, A.ks);
   const int RW = R * W;
-  const int kc = (A.ks - 1) / 2;
-  // ---- weights (fwd layouts [tap][co] / [ci][tap][co]; adjoint layouts over the input channel)
+  const int ks = A.ks, kc = L.kc;
+  const uint32_t base = ts_smem_u32(sm);
+  // ---- zero everything (network plane borders stay zero), weights in stage-friendly layouts
+  for (int t = threadIdx.x; t < L.total; t += TS_T) sm[t] = 0.f;
+  __syncthreads();
   for (int t = threadIdx.x; t < 9 * TS_C; t += TS_T) {
     const int co = t / 9, tap = t % 9;
-    sm[L.w1f + tap * TS_C + co] = A.w1[co * 9 + tap];  // c1 [co][0][tap]
+    sm[L.w1f + tap * TS_C + co] = A.w1[co * 9 + tap];  // c1 [co][0][tap] -> [tap][co]
     sm[L.w1t + co * 9 + tap] = A.w1[co * 9 + tap];     // c1^T: [co][tap]
-    sm[L.w3f + co * 9 + tap] = A.w3[co * 9 + tap];     // c3 [0][ci = co][tap]
+    sm[L.w3f + co * 9 + tap] = A.w3[co * 9 + tap];     // c3 [0][ci][tap] -> [ci][tap]
     sm[L.w3t + tap * TS_C + co] = A.w3[co * 9 + tap];  // c3^T: [tap][ci]
   }
   for (int t = threadIdx.x; t < TS_C * TS_C * 9; t += TS_T) {
@@ -142,196 +210,159 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     sm[L.w2f + (ci * 9 + tap) * TS_C + co] = A.w2[t];  // c2: [ci][tap][co]
     sm[L.w2t + (co * 9 + tap) * TS_C + ci] = A.w2[t];  // c2^T: [co][tap][ci]
   }
-  const float* kg = A.kern + (A.kper ? (long long)n * A.ks * A.ks : 0);
-  for (int t = threadIdx.x; t < A.ks * A.ks; t += TS_T) sm[L.kern + t] = kg[t];
-  // ---- state: x^0 (own rows), z^0 = x^0, y
-  const long long img = (long long)n * H * W;
+  const float* kg = A.kern + (A.kper ? (long long)n * ks * ks : 0);
+  for (int t = threadIdx.x; t < ks * ks; t += TS_T) sm[L.kern + t] = kg[t];
+  const long long img = (long long)n * H * W + (long long)row0 * W;
+  // z^0 = x^0 must be complete in every CTA of the cluster (own rows, pushed halos) before [1]
+  ts_cluster_sync();
   for (int t = threadIdx.x; t < RW; t += TS_T) {
-    const float v = A.x[img + (long long)row0 * W + t];
+    const float v = A.x[img + t];
     sm[L.xk + t] = v;
-    sm[L.z + L.HB * W + t] = v;
-    sm[L.y + t] = A.y[img + (long long)row0 * W + t];
+    sm[L.y + t] = A.y[img + t];
+    ts_put_blur(sm, L, L.z, t / W, t % W, v, rank, base);
   }
   int iters = 0, status = 1;
   float res = __int_as_float(0x7fc00000);
-  __syncthreads();
+  // blocked 16 -> 16 stages: thread -> (column, row pair, channel quarter) for t < 2 RW... 4 RW / 2
+  const int nb = W * (R / 2) * 4;  // blocked threads
+  const int cb = threadIdx.x % W, rb0 = 2 * ((threadIdx.x / W) % (R / 2)), qb = threadIdx.x / (W * (R / 2));
+  // split-K stages: 4 lanes per pixel
+  const int pk = threadIdx.x >> 2, qk = threadIdx.x & 3;
+  const int rk = pk / W, ck = pk % W;
+  const bool act_k = pk < RW;
+  long long t_mark = clock64();
   for (int k = 0; k < A.max_iter; ++k) {
-    // [S0] z complete on every CTA: halo rows (+-HB, periodic: the blur reads them wrapped)
+    // [S0] z (own rows + pushed halos) complete on every CTA
     ts_cluster_sync();
-    ts_halo(sm, L, L.z, 1, L.HB, row0, H);
-    __syncthreads();
-    // [1] a1 = sp(c1(z)); blur residual rb = A z - y (true periodic convolution, reading Q8)
-    for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const int r = t / W, c = t % W;
-      float acc[TS_C];
-#pragma unroll
-      for (int co = 0; co < TS_C; ++co) acc[co] = 0.f;
-#pragma unroll
-      for (int tap = 0; tap < 9; ++tap) {
-        const float v = ts_at(sm + L.z, L, r + tap / 3 - 1, c + tap % 3 - 1, row0, H);
-        const float4* w4 = reinterpret_cast<const float4*>(sm + L.w1f + tap * TS_C);
-#pragma unroll
-        for (int q = 0; q < TS_C / 4; ++q) {
-          const float4 w = w4[q];
-          acc[4 * q] = fmaf(w.x, v, acc[4 * q]);
-          acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-          acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-        }
-      }
-#pragma unroll
-      for (int co = 0; co < TS_C; ++co) sm[L.a1 + co * L.PL + (r + L.HB) * W + c] = ts_softplus(acc[co]);
-      float s = 0.f;
-      for (int i = 0; i < A.ks; ++i) {
-        const float* zr = sm + L.z + (r - i + kc + L.HB) * W;
-        for (int j = 0; j < A.ks; ++j) {
-          int cc = c - j + kc;
-          cc = cc < 0 ? cc + W : (cc >= W ? cc - W : cc);
-          s = fmaf(sm[L.kern + i * A.ks + j], zr[cc], s);
-        }
-      }
-      sm[L.rb + (r + L.HB) * W + c] = s - sm[L.y + t];
-    }
-    // [S1] a1 (+-1) and rb (+-HB) halos
-    ts_cluster_sync();
-    ts_halo(sm, L, L.a1, TS_C, 1, row0, H);
-    ts_halo(sm, L, L.rb, 1, L.HB, row0, H);
-    __syncthreads();
-    // [2] a2 = sp(c2(a1)) (thread = pixel x half of the output channels); gf = A^T rb
-    for (int t = threadIdx.x; t < 2 * RW; t += TS_T) {
-      const int p = t % RW, half = t / RW;
-      const int r = p / W, c = p % W;
-      float acc[TS_C / 2];
-#pragma unroll
-      for (int co = 0; co < TS_C / 2; ++co) acc[co] = 0.f;
-      for (int ci = 0; ci < TS_C; ++ci) {
-        const float* in = sm + L.a1 + ci * L.PL;
+    TS_MARK(0)
+    // [1] a1 = sp(c1(z)) on rows -1 .. R (the halo rows recomputed locally; zero outside the image);
+    //     rb = A z - y (true periodic convolution, reading Q8), pushed to the neighbours' halos
+    for (int t = threadIdx.x; t < (R + 2) * W * 4; t += TS_T) {
+      const int p = t % ((R + 2) * W), q = t / ((R + 2) * W);
+      const int r = p / W - 1, c = p % W;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const bool inside = row0 + r >= 0 && row0 + r < H;
+      if (inside) {
 #pragma unroll
         for (int tap = 0; tap < 9; ++tap) {
-          const float v = ts_at(in, L, r + tap / 3 - 1, c + tap % 3 - 1, row0, H);
-          const float4* w4 = reinterpret_cast<const float4*>(sm + L.w2f + (ci * 9 + tap) * TS_C + half * (TS_C / 2));
-#pragma unroll
-          for (int q = 0; q < TS_C / 8; ++q) {
-            const float4 w = w4[q];
-            acc[4 * q] = fmaf(w.x, v, acc[4 * q]);
-            acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-            acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-            acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-          }
+          const int gr = row0 + r + tap / 3 - 1, cc = c + tap % 3 - 1;
+          const float v = (gr >= 0 && gr < H && cc >= 0 && cc < W) ? sm[L.b_at(L.z, r + tap / 3 - 1, cc)] : 0.f;
+          const float4 w = *reinterpret_cast<const float4*>(sm + L.w1f + tap * TS_C + 4 * q);
+          acc[0] = fmaf(w.x, v, acc[0]); acc[1] = fmaf(w.y, v, acc[1]);
+          acc[2] = fmaf(w.z, v, acc[2]); acc[3] = fmaf(w.w, v, acc[3]);
         }
       }
 #pragma unroll
-      for (int co = 0; co < TS_C / 2; ++co)
-        sm[L.a2 + (half * (TS_C / 2) + co) * L.PL + (r + L.HB) * W + c] = ts_softplus(acc[co]);
-      if (half == 0) {  // (A^T rb)[r][c] = sum_ij k[i][j] rb[r + i - kc][(c + j - kc) mod W]   (correlation)
-        float s = 0.f;
-        for (int i = 0; i < A.ks; ++i) {
-          const float* rr = sm + L.rb + (r + i - kc + L.HB) * W;
-          for (int j = 0; j < A.ks; ++j) {
-            int cc = c + j - kc;
-            cc = cc < 0 ? cc + W : (cc >= W ? cc - W : cc);
-            s = fmaf(sm[L.kern + i * A.ks + j], rr[cc], s);
-          }
-        }
-        sm[L.gf + p] = s;
-      }
+      for (int e = 0; e < 4; ++e) sm[L.n_at(L.a1, 4 * q + e, r, c)] = inside ? ts_softplus(acc[e]) : 0.f;
     }
-    // [S2] a2 halo
-    ts_cluster_sync();
-    ts_halo(sm, L, L.a2, TS_C, 1, row0, H);
-    __syncthreads();
-    // [3] U = c3(a2): with the identity skip N(z) = z + U, grad g = J_U^T U (cotangent U)
-    for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const int r = t / W, c = t % W;
+    if (act_k) {  // kernel rows i = qk, qk + 4, ...: (A z)[r][c] = sum k[i][j] z[r - i + kc][c - j + kc]
       float s = 0.f;
-      for (int ci = 0; ci < TS_C; ++ci) {
-        const float* in = sm + L.a2 + ci * L.PL;
-#pragma unroll
-        for (int tap = 0; tap < 9; ++tap)
-          s = fmaf(sm[L.w3f + ci * 9 + tap], ts_at(in, L, r + tap / 3 - 1, c + tap % 3 - 1, row0, H), s);
+      for (int i = qk; i < ks; i += 4) {
+        const float* zr = sm + L.b_at(L.z, rk - i + kc, ck + kc);
+        const float* kr = sm + L.kern + i * ks;
+        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], zr[-j], s);
       }
-      sm[L.u + (r + L.HB) * W + c] = s;
+      s = ts_sum4(s);
+      if (qk == 0) ts_put_blur(sm, L, L.rb, rk, ck, s - sm[L.y + pk], rank, base);
     }
-    ts_cluster_sync();
-    ts_halo(sm, L, L.u, 1, 1, row0, H);
-    __syncthreads();
-    // [4] q2 = c3^T(U) . sp'(a2)   (conv3x3^T: flipped taps)
-    for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const int r = t / W, c = t % W;
-      float acc[TS_C];
+    TS_MARK(1)
+    ts_cluster_sync();  // [S1] rb halos (a1 is local)
+    TS_MARK(2)
+    // [2] a2 = sp(c2(a1)) (blocked threads), pushed with a 2-row halo; gf = A^T rb (the others)
+    if (threadIdx.x < nb) {
+      float acc[2][4];
+      ts_conv16<false>(sm, L, L.a1, L.w2f, rb0, cb, qb, acc);
 #pragma unroll
-      for (int ci = 0; ci < TS_C; ++ci) acc[ci] = 0.f;
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          ts_put_net(sm, L, L.n_at(L.a2, 4 * qb + e, rb0 + i, cb), ts_softplus(acc[i][e]), rb0 + i, rank, H, 2, base);
+    } else if (threadIdx.x - nb < 2 * RW) {  // 2 lanes per pixel: (A^T rb)[r][c] = sum k[i][j] rb[r + i - kc][c + j - kc]
+      const int t = threadIdx.x - nb, p = t >> 1, h = t & 1, r = p / W, c = p % W;
+      float s = 0.f;
+      for (int i = h; i < ks; i += 2) {
+        const float* rr = sm + L.b_at(L.rb, r + i - kc, c - kc);
+        const float* kr = sm + L.kern + i * ks;
+        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], rr[j], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (h == 0) sm[L.gf + p] = s;
+    }
+    TS_MARK(3)
+    ts_cluster_sync();  // [S2] a2 halos (2 rows)
+    TS_MARK(4)
+    // [3] U = c3(a2) on rows -1 .. R (zero outside the image): the identity skip makes grad g =
+    //     J_U^T U (cotangent U); 4 lanes per pixel over the input channels
+    for (int t = threadIdx.x; t < (R + 2) * W * 4; t += TS_T) {
+      const int p = t >> 2, q = t & 3, r = p / W - 1, c = p % W;
+      float s = 0.f;
+#pragma unroll
+      for (int cj = 0; cj < TS_C / 4; ++cj) {
+        const int ci = 4 * q + cj;
+        const float* in = sm + L.n_at(L.a2, ci, r, c);
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) s = fmaf(sm[L.w3f + ci * 9 + tap], in[(tap / 3 - 1) * L.WP + tap % 3 - 1], s);
+      }
+      s = ts_sum4(s);
+      if (q == 0) sm[L.n_at(L.u, 0, r, c)] = (row0 + r >= 0 && row0 + r < H) ? s : 0.f;
+    }
+    __syncthreads();
+    // [4] q2 = c3^T(U) . sp'(a2)   (conv3x3^T: flipped taps), pushed (1-row halo)
+    for (int t = threadIdx.x; t < RW * 4; t += TS_T) {
+      const int p = t % RW, q = t / RW, r = p / W, c = p % W;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* in = sm + L.n_at(L.u, 0, r, c);
 #pragma unroll
       for (int tap = 0; tap < 9; ++tap) {
-        const float v = ts_at(sm + L.u, L, r + 1 - tap / 3, c + 1 - tap % 3, row0, H);
-        const float4* w4 = reinterpret_cast<const float4*>(sm + L.w3t + tap * TS_C);
-#pragma unroll
-        for (int q = 0; q < TS_C / 4; ++q) {
-          const float4 w = w4[q];
-          acc[4 * q] = fmaf(w.x, v, acc[4 * q]);
-          acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-          acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-          acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-        }
+        const float v = in[(1 - tap / 3) * L.WP + 1 - tap % 3];
+        const float4 w = *reinterpret_cast<const float4*>(sm + L.w3t + tap * TS_C + 4 * q);
+        acc[0] = fmaf(w.x, v, acc[0]); acc[1] = fmaf(w.y, v, acc[1]);
+        acc[2] = fmaf(w.z, v, acc[2]); acc[3] = fmaf(w.w, v, acc[3]);
       }
 #pragma unroll
-      for (int ci = 0; ci < TS_C; ++ci) {
-        const int o = ci * L.PL + (r + L.HB) * W + c;
-        sm[L.q2 + o] = acc[ci] * ts_dsp(sm[L.a2 + o]);
+      for (int e = 0; e < 4; ++e) {
+        const int o = L.n_at(0, 4 * q + e, r, c);
+        ts_put_net(sm, L, L.q2 + o, acc[e] * ts_dsp(sm[L.a2 + o]), r, rank, H, 1, base);
       }
     }
-    ts_cluster_sync();
-    ts_halo(sm, L, L.q2, TS_C, 1, row0, H);
-    __syncthreads();
-    // [5] q1 = c2^T(q2) . sp'(a1)
-    for (int t = threadIdx.x; t < 2 * RW; t += TS_T) {
-      const int p = t % RW, half = t / RW;
-      const int r = p / W, c = p % W;
-      float acc[TS_C / 2];
+    TS_MARK(5)
+    ts_cluster_sync();  // [S3] q2 halos
+    TS_MARK(6)
+    // [5] q1 = c2^T(q2) . sp'(a1) (blocked threads), pushed (1-row halo)
+    if (threadIdx.x < nb) {
+      float acc[2][4];
+      ts_conv16<true>(sm, L, L.q2, L.w2t, rb0, cb, qb, acc);
 #pragma unroll
-      for (int ci = 0; ci < TS_C / 2; ++ci) acc[ci] = 0.f;
-      for (int co = 0; co < TS_C; ++co) {
-        const float* in = sm + L.q2 + co * L.PL;
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const float v = ts_at(in, L, r + 1 - tap / 3, c + 1 - tap % 3, row0, H);
-          const float4* w4 = reinterpret_cast<const float4*>(sm + L.w2t + (co * 9 + tap) * TS_C + half * (TS_C / 2));
-#pragma unroll
-          for (int q = 0; q < TS_C / 8; ++q) {
-            const float4 w = w4[q];
-            acc[4 * q] = fmaf(w.x, v, acc[4 * q]);
-            acc[4 * q + 1] = fmaf(w.y, v, acc[4 * q + 1]);
-            acc[4 * q + 2] = fmaf(w.z, v, acc[4 * q + 2]);
-            acc[4 * q + 3] = fmaf(w.w, v, acc[4 * q + 3]);
-          }
+        for (int e = 0; e < 4; ++e) {
+          const int o = L.n_at(0, 4 * qb + e, rb0 + i, cb);
+          ts_put_net(sm, L, L.q1 + o, acc[i][e] * ts_dsp(sm[L.a1 + o]), rb0 + i, rank, H, 1, base);
         }
-      }
-#pragma unroll
-      for (int ci = 0; ci < TS_C / 2; ++ci) {
-        const int o = (half * (TS_C / 2) + ci) * L.PL + (r + L.HB) * W + c;
-        sm[L.q1 + o] = acc[ci] * ts_dsp(sm[L.a1 + o]);
-      }
     }
-    ts_cluster_sync();
-    ts_halo(sm, L, L.q1, TS_C, 1, row0, H);
-    __syncthreads();
+    TS_MARK(7)
+    ts_cluster_sync();  // [S4] q1 halos
+    TS_MARK(8)
     // [6] grad g = c1^T(q1); x^{k+1} = z - tau (grad f + lam grad g) (Alg. 1 l.8); residual partials
     float d2 = 0.f, n2 = 0.f, bad = 0.f;
-    for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const int r = t / W, c = t % W;
+    if (act_k) {
       float s = 0.f;
-      for (int co = 0; co < TS_C; ++co) {
-        const float* in = sm + L.q1 + co * L.PL;
 #pragma unroll
-        for (int tap = 0; tap < 9; ++tap)
-          s = fmaf(sm[L.w1t + co * 9 + tap], ts_at(in, L, r + 1 - tap / 3, c + 1 - tap % 3, row0, H), s);
+      for (int cj = 0; cj < TS_C / 4; ++cj) {
+        const int co = 4 * qk + cj;
+        const float* in = sm + L.n_at(L.q1, co, rk, ck);
+#pragma unroll
+        for (int tap = 0; tap < 9; ++tap) s = fmaf(sm[L.w1t + co * 9 + tap], in[(1 - tap / 3) * L.WP + 1 - tap % 3], s);
       }
-      const float z = sm[L.z + (r + L.HB) * W + c], xk = sm[L.xk + t];
-      const float x1 = z - A.tau * (sm[L.gf + t] + A.lam * s);
-      sm[L.gg + t] = x1;  // candidate x^{k+1}
-      const float d = x1 - xk;
-      if (isfinite(x1)) d2 += d * d; else bad += 1.f;
-      n2 += xk * xk;
+      s = ts_sum4(s);
+      if (qk == 0) {
+        const float z = sm[L.b_at(L.z, rk, ck)], xk = sm[L.xk + pk];
+        const float x1 = z - A.tau * (sm[L.gf + pk] + A.lam * s);
+        sm[L.xn + pk] = x1;  // candidate x^{k+1}
+        const float d = x1 - xk;
+        if (isfinite(x1)) d2 = d * d; else bad = 1.f;
+        n2 = xk * xk;
+      }
     }
     // block reduction (fixed order), then this CTA's partials into slot `rank` of every CTA
     {
@@ -348,14 +379,15 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
       if (threadIdx.x < TS_P) {
         float a = 0.f, b = 0.f, e = 0.f;
         for (int w = 0; w < TS_T / 32; ++w) { a += wred[0][w]; b += wred[1][w]; e += wred[2][w]; }
-        const uint32_t slot = ts_smem_u32(sm + L.red + rank * 4);
-        const uint32_t dst = ts_mapa(slot, (uint32_t)threadIdx.x);
+        const uint32_t dst = ts_mapa(base + 4u * (uint32_t)(L.red + rank * 4), (uint32_t)threadIdx.x);
         ts_st_cluster(dst, a);
         ts_st_cluster(dst + 4, b);
         ts_st_cluster(dst + 8, e);
       }
     }
-    ts_cluster_sync();
+    TS_MARK(9)
+    ts_cluster_sync();  // [S5] partials
+    TS_MARK(10)
     double D2 = 0.0, N2 = 0.0, BAD = 0.0;
     for (int q = 0; q < TS_P; ++q) {  // fixed order: identical on every CTA
       D2 += (double)sm[L.red + q * 4];
@@ -369,55 +401,57 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     const double rr = N2 > 0.0 ? sqrt(D2) / sqrt(N2) : (double)INFINITY;
     res = (float)rr;
     iters = k + 1;
-    // accept: z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4), x^k <- x^{k+1}
+    // accept: z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4), pushed; x^k <- x^{k+1}
     for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const float x1 = sm[L.gg + t], xk = sm[L.xk + t];
-      sm[L.z + L.HB * W + t] = x1 + A.beta * (x1 - xk);
+      const float x1 = sm[L.xn + t], xk = sm[L.xk + t];
+      ts_put_blur(sm, L, L.z, t / W, t % W, x1 + A.beta * (x1 - xk), rank, base);
       sm[L.xk + t] = x1;
     }
     if (rank == 0 && threadIdx.x == 0 && A.trace && k < A.trace_cap)
       atomicMax(reinterpret_cast<int*>(A.trace) + k, __float_as_int(res));
+    TS_MARK(11)
     if (((k + 1) % A.check_every) == 0 && res <= A.tol) {
       status = 0;
       break;
     }
-    __syncthreads();
   }
   // x-hat = the last accepted iterate (Remark 1)
   __syncthreads();
-  for (int t = threadIdx.x; t < RW; t += TS_T) A.x[img + (long long)row0 * W + t] = sm[L.xk + t];
+  for (int t = threadIdx.x; t < RW; t += TS_T) A.x[img + t] = sm[L.xk + t];
   if (rank == 0 && threadIdx.x == 0) {
     A.iters[n] = iters;
     A.res[n] = res;
     A.status[n] = status;
     atomicMax(A.kdone, iters);
   }
-  ts_cluster_sync();  // no CTA exits while a neighbour may still read its shared memory
+  ts_cluster_sync();  // no CTA exits while a neighbour may still write into its shared memory
 }
 
 size_t tiny_solve_smem(int H, int W, int ks) {
   TsLayout L;
-  L.init(H / TS_P, W, (ks - 1) / 2 > 1 ? (ks - 1) / 2 : 1, ks);
+  L.init(H / TS_P, W, ks);
   return sizeof(float) * (size_t)L.total;
 }
 
+// (R + 2) W x 4 items per recomputed stage are looped; R x W <= 128 keeps one pixel per 4 lanes
 bool tiny_solve_supported(int H, int W, int ks) {
-  if (H % TS_P != 0 || (H / TS_P) < (ks - 1) / 2 || W < ks || W > 128) return false;
+  if (H % TS_P != 0 || W % 32 != 0 || W < ks) return false;
+  const int R = H / TS_P;
+  // 4 lanes per pixel, whole warps per stage, 2-row blocks, halo rows from the two neighbours only
+  if (R * W > TS_T / 4 || R % 2 != 0 || R < 2 || R < (ks - 1) / 2) return false;
   return tiny_solve_smem(H, W, ks) <= 200 * 1024;
 }
 
 void launch_tiny_solve(const TinySolveArgs& a, cudaStream_t s) {
   TinyArgs A{};
   A.N = a.N; A.H = a.H; A.W = a.W; A.R = a.H / TS_P;
-  A.HB = (a.ks - 1) / 2 > 1 ? (a.ks - 1) / 2 : 1;
   A.ks = a.ks; A.kper = a.kper; A.kern = a.kern;
   A.w1 = a.w1; A.w2 = a.w2; A.w3 = a.w3; A.y = a.y; A.x = a.x;
   A.lam = a.lam; A.tau = a.tau; A.beta = a.beta; A.tol = a.tol;
   A.max_iter = a.max_iter; A.check_every = a.check_every;
   A.iters = a.iters; A.res = a.res; A.status = a.status; A.trace = a.trace; A.trace_cap = a.trace_cap;
   A.kdone = a.kdone;
-  const size_t smem = tiny_solve_smem(a.H, a.W, a.ks);
-  tiny_solve_kernel<<<dim3(TS_P * a.N), dim3(TS_T), smem, s>>>(A);
+  tiny_solve_kernel<<<dim3(TS_P * a.N), dim3(TS_T), tiny_solve_smem(a.H, a.W, a.ks), s>>>(A);
 }
 
 void init_attrs_tiny() { set_max_dyn_smem(tiny_solve_kernel); }
