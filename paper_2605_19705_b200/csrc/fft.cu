@@ -77,6 +77,8 @@ __device__ __forceinline__ void fft_row(float2* d, const float2* tw, int N, int 
   }
 }
 
+__host__ __device__ __forceinline__ int fft_tpr(int W) { return (W / 4) < 32 ? (W / 4 > 0 ? W / 4 : 1) : 32; }
+
 __device__ __forceinline__ int bitrev(int i, int logN) { return (int)(__brev((unsigned)i) >> (32 - logN)); }
 
 // natural -> bit-reversed order in place (the owner of the smaller index swaps each pair), then a
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
   pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW;
-  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int tpr = fft_tpr(W);
   const int rpb = 256 / tpr;
   float2* tw = sm2;
   float2* rows = sm2 + W / 2;
@@ -176,7 +178,11 @@ __global__ void __launch_bounds__(256) blur_rows_fwd_kernel(FftArgs f, const flo
 //   op 1: multiply by conj(K^[ky][kx])                                     (A^T)
 //   op 2: forward only (no inverse): used to build K^ itself
 //   op 3: inverse only (the half spectrum is already in k-space: MRI A^T y)
-constexpr int FFT_CPB = 8;  // columns per block in column passes
+// Columns per block in column passes (16 threads per column) and threads per row in row passes
+// (32, so a 256-thread block transforms 8 rows of 256 points): enough independent transforms per
+// block to amortise the twiddle load and the per-pass barriers (2 rows / 8 columns per block ran
+// the C4 passes at ~0.5 TB/s).
+constexpr int FFT_CPB = 16;
 
 __global__ void __launch_bounds__(256) blur_cols_kernel(FftArgs f, int op) {
   pdl_enter();
@@ -246,7 +252,7 @@ __global__ void __launch_bounds__(256) blur_rows_inv_kernel(FftArgs f, StepArgs 
   pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW, H = f.H;
-  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int tpr = fft_tpr(W);
   const int rpb = 256 / tpr;
   float2* tw = sm2;
   float2* rows = sm2 + W / 2;
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(256) phase_rows_fwd_kernel(FftArgs f) {
   pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW;
-  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int tpr = fft_tpr(W);
   const int rpb = 256 / tpr;
   float2* tw = sm2;
   float2* rows = sm2 + W / 2;
@@ -415,7 +421,7 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
   pdl_enter();
   extern __shared__ float2 sm2[];
   const int W = f.W, logW = f.logW, H = f.H;
-  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int tpr = fft_tpr(W);
   const int rpb = 256 / tpr;
   float2* tw = sm2;
   float2* rows = sm2 + W / 2;
@@ -425,7 +431,10 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
   const int n = blockIdx.y;
   if (f.active && !f.active[n]) return;
   float2* d = rows + r * row_pitch(W);
-  float gacc[4] = {0.f, 0.f, 0.f, 0.f};  // W / tpr <= 4 for W <= 1024
+  constexpr int QMAX = 32;  // W / tpr <= 1024 / 32
+  float gacc[QMAX];
+#pragma unroll
+  for (int q = 0; q < QMAX; ++q) gacc[q] = 0.f;
   const float s = rsqrtf((float)H * (float)W);
   for (int j = 0; j < f.J; ++j) {
     if (h < H) {
@@ -436,10 +445,13 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
     fft_row(d, tw, W, logW, t, tpr, true);
     if (h < H) {
       const float2* Dr = f.pmask + ((long long)j * H + h) * W;
-      int q = 0;
-      for (int i = t; i < W; i += tpr, ++q) {
-        const float2 v = make_float2(d[pd(i)].x * s, d[pd(i)].y * s);
-        gacc[q] += 2.f * cconjmul(Dr[i], v).x;
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q) {
+        const int i = t + q * tpr;
+        if (i < W) {
+          const float2 v = make_float2(d[pd(i)].x * s, d[pd(i)].y * s);
+          gacc[q] += 2.f * cconjmul(Dr[i], v).x;
+        }
       }
     }
     __syncthreads();
@@ -447,8 +459,9 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
   const long long base = (long long)n * H * W + (long long)h * W;
   if (mode == 0) {
     if (h < H) {
-      int q = 0;
-      for (int i = t; i < W; i += tpr, ++q) dst[base + i] = gacc[q];
+#pragma unroll
+      for (int q = 0; q < QMAX; ++q)
+        if (t + q * tpr < W) dst[base + t + q * tpr] = gacc[q];
     }
     return;
   }
@@ -457,29 +470,421 @@ __global__ void __launch_bounds__(256) phase_rows_inv_kernel(FftArgs f, StepArgs
   float* xn_base = (k & 1) ? a.X0 : a.X1;
   P3 acc{0.f, 0.f, 0.f};
   if (h < H) {
-    int q = 0;
-    for (int i = t; i < W; i += tpr, ++q) {
-      const long long e = base + i;
-      // x^{k+1} = z - tau (grad f(z) + lam grad g(z))       (Alg. 1 l.8)
-      step_tail(a.z[e] - a.tau * (gacc[q] + a.lam * a.gg[e]), e, a, xk_base, xn_base, acc);
+#pragma unroll
+    for (int q = 0; q < QMAX; ++q) {
+      const int i = t + q * tpr;
+      if (i < W) {
+        const long long e = base + i;
+        // x^{k+1} = z - tau (grad f(z) + lam grad g(z))       (Alg. 1 l.8)
+        step_tail(a.z[e] - a.tau * (gacc[q] + a.lam * a.gg[e]), e, a, xk_base, xn_base, acc);
+      }
     }
   }
   reduce_store_p3(acc, a.partials + ((long long)n * a.parts + blockIdx.x) * 3);
+}
+
+// ================================================================== register FFTs (N = 256, 512)
+// The shared-memory radix-2/4 passes above move each row through shared memory ~5 times per
+// transform (~10 bytes of shared traffic per byte of HBM traffic: shared-memory bound at ~1 TB/s
+// of HBM on B200). For the configs' sizes a transform of N = 16 T points is done by a TEAM of T
+// threads (T = 16 for 256, 32 for 512) almost entirely in registers (four-step / Stockham):
+//   thread t holds x[t + T k], k < 16 -> 16-point DFT in registers -> twiddle W_N^(t k') ->
+//   one transpose through a padded per-team buffer -> a T-point DFT over the old thread index
+//   (T = 16: one more 16-point DFT; T = 32: two 16-point DFTs over the even / odd samples joined
+//   by one radix-2 step across a lane pair) -> thread holds X[n] for n = team_out(t, k).
+// One shared-memory round trip per transform; loads and stores of x[t + T k] / X[team_out] are
+// coalesced in 128-byte runs. Inverse transforms use conj(FFT(conj(x))). Twiddles: the
+// fp64-derived table W_N^m, m < N/2 (tw_w / tw_h), with W_N^(m + N/2) = -W_N^m.
+__device__ __forceinline__ float2 cfma_tw(float2 a, float c, float s) {  // a * (c + i s)
+  return make_float2(a.x * c - a.y * s, a.x * s + a.y * c);
+}
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
+
+// In-register 16-point DFT, natural order in and out (radix-2 decimation in frequency, the output
+// permutation folded into register names at compile time).
+__device__ __forceinline__ void dft16(float2 (&v)[16]) {
+  // W_16^m, m < 8
+  const float C[8] = {1.f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                      0.f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f};
+  const float S[8] = {0.f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                      -1.f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f};
+#pragma unroll
+  for (int h = 8; h >= 1; h >>= 1) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if ((i & h) == 0) {
+        const float2 a = v[i], b = v[i + h];
+        v[i] = cadd(a, b);
+        const int m = (i & (h - 1)) * (8 / h);
+        v[i + h] = cfma_tw(csub(a, b), C[m], S[m]);
+      }
+    }
+  }
+  float2 o[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) o[k] = v[((k & 1) << 3) | ((k & 2) << 1) | ((k & 4) >> 1) | ((k & 8) >> 3)];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = o[k];
+}
+
+__device__ __forceinline__ float2 tw_get(const float2* tw, int m, int N) {  // W_N^m for any m >= 0
+  m &= N - 1;
+  const float2 w = tw[m & (N / 2 - 1)];
+  return m >= N / 2 ? make_float2(-w.x, -w.y) : w;
+}
+
+// Forward DFT of N = 16 T points held by a team of T threads: in v[k] = x[t + T k]; out v[k] =
+// X[team_out<T>(t, k)]. buf: the team's (16 x (T + 1)) scratch; tw: W_N^m, m < N/2 (shared).
+template <int T>
+__device__ __forceinline__ int team_out(int t, int k) {
+  if (T == 16) return t + 16 * k;
+  return (t >> 1) + 16 * (k + 16 * (t & 1));
+}
+template <int T>
+__device__ __forceinline__ void team_fft(float2 (&v)[16], int t, float2* buf, const float2* tw) {
+  constexpr int N = 16 * T, P = T + 1;
+  dft16(v);
+#pragma unroll
+  for (int k = 1; k < 16; ++k) v[k] = cmul(v[k], tw_get(tw, t * k, N));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) buf[k * P + t] = v[k];
+  __syncwarp();
+  if (T == 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = buf[t * P + j];
+    dft16(v);
+  } else {
+    const int kp = t >> 1, h = t & 1;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = buf[kp * P + 2 * m + h];
+    dft16(v);
+    // X[k] = V0[k] + W_32^k V1[k], X[k + 16] = V0[k] - W_32^k V1[k]
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float2 p;
+      p.x = __shfl_xor_sync(0xffffffffu, v[k].x, 1);
+      p.y = __shfl_xor_sync(0xffffffffu, v[k].y, 1);
+      const float2 w = tw_get(tw, k * (N / 32), N);  // W_32^k
+      v[k] = h ? csub(p, cmul(w, v[k])) : cadd(v[k], cmul(w, p));
+    }
+  }
+  __syncwarp();  // the team buffer may be reused by the next transform
+}
+
+__device__ __forceinline__ void load_tw_all(float2* s_tw, const float2* g_tw, int N) {
+  for (int k = threadIdx.x; k < N / 2; k += blockDim.x) s_tw[k] = g_tw[k];
+}
+
+// ---- blur / MRI rows (real planes): forward R2C (mode 0: src plane; 1: prox right-hand side)
+template <int T>
+__global__ void __launch_bounds__(16 * T) rblur_rows_fwd_kernel(FftArgs f, const float* __restrict__ src, int mode) {
+  pdl_enter();
+  constexpr int W = 16 * T, P = T + 1;
+  extern __shared__ float2 smr[];
+  float2* tw = smr;                       // W/2
+  float2 (*bufs)[16 * P] = reinterpret_cast<float2 (*)[16 * P]>(smr + W / 2);  // 16 teams
+  load_tw_all(tw, f.tw_w, W);
+  __syncthreads();
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int h = blockIdx.x * 16 + team, c = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;  // uniform per block
+  if (h >= f.H) return;                  // whole team
+  const long long e0 = ((long long)n * f.C + c) * f.H * W + (long long)h * W;
+  float2 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const long long e = e0 + t + T * k;
+    const float x = mode == 1 ? f.z[e] - f.tau * f.lam * f.gg[e] + f.tau * f.aty[e] : src[e];
+    v[k] = make_float2(x, 0.f);
+  }
+  team_fft<T>(v, t, bufs[team], tw);
+  const int Wh = W / 2 + 1;
+  float2* S = f.spec + ((long long)n * f.C + c) * f.H * Wh + (long long)h * Wh;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int o = team_out<T>(t, k);
+    if (o < Wh) S[o] = v[k];
+  }
+}
+
+// ---- blur / MRI columns of the half spectrum: forward H-point FFT, op, inverse (as blur_cols)
+template <int T>
+__global__ void __launch_bounds__(256) rblur_cols_kernel(FftArgs f, int op) {
+  pdl_enter();
+  constexpr int H = 16 * T, P = T + 1, CPB = 256 / T, CP = CPB + 1;  // CPB columns per block
+  extern __shared__ float2 smc[];
+  float2* tw = smc;                       // H/2
+  float2* tile = smc + H / 2;             // [H][CP]
+  float2* bufs = tile + H * CP;           // CPB teams x 16 P
+  float2* otile = bufs + CPB * 16 * P;    // [H][CPB] the op's diagonal (dgl as .x, or K^)
+  load_tw_all(tw, f.tw_h, H);
+  const int Wh = f.W / 2 + 1;
+  const int kx0 = blockIdx.x * CPB, c = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* S = f.spec + ((long long)n * f.C + c) * H * Wh;
+  const bool diag = op == 0 || op == 1;
+  for (int q = threadIdx.x; q < H * CPB; q += blockDim.x) {
+    const int r = q / CPB, j = q % CPB;
+    const bool in = kx0 + j < Wh;
+    tile[r * CP + j] = in ? S[(long long)r * Wh + kx0 + j] : make_float2(0.f, 0.f);
+    if (diag && in)
+      otile[q] = op == 0 ? make_float2(__ldg(f.dgl + (long long)r * Wh + kx0 + j), 0.f)
+                         : __ldg(f.khat + (long long)r * Wh + kx0 + j);
+  }
+  __syncthreads();
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int kx = kx0 + team;
+  float2* buf = bufs + team * 16 * P;
+  float2 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = tile[(t + T * k) * CP + team];
+  const bool fwd = op != 3, inv = op != 2;
+  if (fwd) team_fft<T>(v, t, buf, tw);
+  if (fwd && inv) {  // pointwise op at ky = team_out, then back to the x[t + T k] distribution
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int ky = team_out<T>(t, k);
+      float2 w = v[k];
+      if (kx < Wh) {
+        const float2 o = otile[ky * CPB + team];
+        if (op == 0) {
+          w.x *= o.x; w.y *= o.x;
+        } else {
+          w = cconjmul(o, w);
+        }
+      }
+      tile[ky * CP + team] = w;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = tile[(t + T * k) * CP + team];
+  }
+  if (inv) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cconj(v[k]);
+    team_fft<T>(v, t, buf, tw);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cconj(v[k]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tile[team_out<T>(t, k) * CP + team] = v[k];
+  __syncthreads();
+  for (int q = threadIdx.x; q < H * CPB; q += blockDim.x) {
+    const int r = q / CPB, j = q % CPB;
+    if (kx0 + j < Wh) S[(long long)r * Wh + kx0 + j] = tile[r * CP + j];
+  }
+}
+
+// ---- blur / MRI rows, inverse C2R (mode 0: store into dst; 1: x^{k+1} -> update + partials)
+template <int T>
+__global__ void __launch_bounds__(16 * T) rblur_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  pdl_enter();
+  constexpr int W = 16 * T, P = T + 1;
+  extern __shared__ float2 smr[];
+  float2* tw = smr;                       // W/2
+  float2 (*bufs)[16 * P] = reinterpret_cast<float2 (*)[16 * P]>(smr + W / 2);  // 16 teams
+  load_tw_all(tw, f.tw_w, W);
+  __syncthreads();
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int c = blockIdx.y, n = blockIdx.z, H = f.H;
+  const bool valid = blockIdx.x * 16 + team < H;
+  const int h = valid ? blockIdx.x * 16 + team : H - 1;  // rows past H (H < 16) redo row H-1, unused
+  if (f.active && !f.active[n]) return;
+  const int Wh = W / 2 + 1;
+  const float2* S = f.spec + ((long long)n * f.C + c) * H * Wh + (long long)h * Wh;
+  float2 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {  // Hermitian row: X[W - i] = conj(X[i]); loaded conjugated (inverse)
+    const int i = t + T * k;
+    const float2 x = i < Wh ? S[i] : cconj(S[W - i]);
+    v[k] = cconj(x);
+  }
+  team_fft<T>(v, t, bufs[team], tw);
+  const float scale = 1.f / ((float)H * (float)W);
+  const long long plane = ((long long)n * f.C + c) * H * W + (long long)h * W;
+  if (mode == 0) {
+    if (valid)
+#pragma unroll
+      for (int k = 0; k < 16; ++k) dst[plane + team_out<T>(t, k)] = v[k].x * scale;  // Re(conj(.)) = Re(.)
+    return;
+  }
+  const int kk = *a.kdev;
+  const float* xk_base = (kk & 1) ? a.X1 : a.X0;
+  float* xn_base = (kk & 1) ? a.X0 : a.X1;
+  P3 acc{0.f, 0.f, 0.f};
+  if (valid)
+#pragma unroll
+    for (int k = 0; k < 16; ++k) step_tail(v[k].x * scale, plane + team_out<T>(t, k), a, xk_base, xn_base, acc);
+  const int part = c * gridDim.x + blockIdx.x;
+  reduce_store_p3(acc, a.partials + ((long long)n * a.parts + part) * 3);
+}
+
+// ---- phase retrieval rows forward: U[n][j][h][:] = FFT_row(D_j[h][:] z[n][h][:])
+template <int T>
+__global__ void __launch_bounds__(16 * T) rphase_rows_fwd_kernel(FftArgs f) {
+  pdl_enter();
+  constexpr int W = 16 * T, P = T + 1;
+  extern __shared__ float2 smr[];
+  float2* tw = smr;                       // W/2
+  float2 (*bufs)[16 * P] = reinterpret_cast<float2 (*)[16 * P]>(smr + W / 2);  // 16 teams
+  load_tw_all(tw, f.tw_w, W);
+  __syncthreads();
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int h = blockIdx.x * 16 + team, j = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  if (h >= f.H) return;  // whole team
+  const float* zr = f.z + (long long)n * f.H * W + (long long)h * W;
+  const float2* Dr = f.pmask + ((long long)j * f.H + h) * W;
+  float2 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int i = t + T * k;
+    const float zv = zr[i];
+    const float2 dv = __ldg(Dr + i);
+    v[k] = make_float2(dv.x * zv, dv.y * zv);
+  }
+  team_fft<T>(v, t, bufs[team], tw);
+  float2* U = f.spec + (((long long)n * f.J + j) * f.H + h) * W;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) U[team_out<T>(t, k)] = v[k];
+}
+
+// ---- phase columns: forward FFT -> u = col / sqrt(HW) -> w = (|u|^2 - y_j) u -> inverse FFT
+template <int T>
+__global__ void __launch_bounds__(256) rphase_cols_kernel(FftArgs f) {
+  pdl_enter();
+  constexpr int H = 16 * T, P = T + 1, CPB = 256 / T, CP = CPB + 1;
+  extern __shared__ float2 smc[];
+  float2* tw = smc;
+  float2* tile = smc + H / 2;
+  float2* bufs = tile + H * CP;
+  float* ytile = reinterpret_cast<float*>(bufs + CPB * 16 * P);  // [H][CPB]
+  load_tw_all(tw, f.tw_h, H);
+  const int W = f.W;
+  const int kx0 = blockIdx.x * CPB, j = blockIdx.y, n = blockIdx.z;
+  if (f.active && !f.active[n]) return;
+  float2* U = f.spec + ((long long)n * f.J + j) * H * W;
+  const float* Y = f.y + ((long long)n * f.J + j) * H * W;
+  for (int q = threadIdx.x; q < H * CPB; q += blockDim.x) {
+    const int r = q / CPB, jj = q % CPB;
+    tile[r * CP + jj] = U[(long long)r * W + kx0 + jj];
+    ytile[q] = __ldg(Y + (long long)r * W + kx0 + jj);
+  }
+  __syncthreads();
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int kx = kx0 + team;
+  float2* buf = bufs + team * 16 * P;
+  float2 v[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = tile[(t + T * k) * CP + team];
+  team_fft<T>(v, t, buf, tw);
+  const float sc = rsqrtf((float)H * (float)W);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const int ky = team_out<T>(t, k);
+    const float2 u = make_float2(v[k].x * sc, v[k].y * sc);
+    const float m = u.x * u.x + u.y * u.y - ytile[ky * CPB + team];
+    tile[ky * CP + team] = make_float2(m * u.x, m * u.y);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = cconj(tile[(t + T * k) * CP + team]);
+  team_fft<T>(v, t, buf, tw);
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 16; ++k) tile[team_out<T>(t, k) * CP + team] = cconj(v[k]);
+  __syncthreads();
+  for (int q = threadIdx.x; q < H * CPB; q += blockDim.x) {
+    const int r = q / CPB, jj = q % CPB;
+    U[(long long)r * W + kx0 + jj] = tile[r * CP + jj];
+  }
+}
+
+// ---- phase rows inverse: v_j = IFFT_row(U_j) / sqrt(HW); grad f = sum_j 2 Re(conj(D_j) v_j). One
+// team per (row, mask): a block is RB = 16 / J rows x J masks (J in {1, 2, 4, 8, 16}); the J
+// contributions of a pixel are summed in a fixed order through shared memory before the update.
+template <int T>
+__global__ void __launch_bounds__(16 * T) rphase_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+  pdl_enter();
+  constexpr int W = 16 * T, P = T + 1;
+  extern __shared__ float2 smr[];
+  float2* tw = smr;
+  float2 (*bufs)[16 * P] = reinterpret_cast<float2 (*)[16 * P]>(smr + W / 2);
+  float* gsum = reinterpret_cast<float*>(smr + W / 2 + 16 * 16 * P);  // [16 teams][W]
+  load_tw_all(tw, f.tw_w, W);
+  __syncthreads();
+  const int J = f.J, RB = 16 / J;
+  const int team = threadIdx.x / T, t = threadIdx.x % T;
+  const int rl = team / J, j = team % J;
+  const int n = blockIdx.y, H = f.H;
+  const int h = blockIdx.x * RB + rl < H ? blockIdx.x * RB + rl : H - 1;  // rows past H: redo the last, unused
+  if (f.active && !f.active[n]) return;
+  const float sc = rsqrtf((float)H * (float)W);
+  {
+    const float2* U = f.spec + (((long long)n * J + j) * H + h) * W;
+    float2 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) v[k] = cconj(U[t + T * k]);
+    team_fft<T>(v, t, bufs[team], tw);
+    const float2* Dr = f.pmask + ((long long)j * H + h) * W;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int o = team_out<T>(t, k);
+      const float2 w = make_float2(v[k].x * sc, -v[k].y * sc);  // conj back
+      gsum[team * W + o] = 2.f * cconjmul(__ldg(Dr + o), w).x;
+    }
+  }
+  __syncthreads();
+  // per pixel of the block's RB rows: fixed-order sum over the masks, then store / update
+  const long long base0 = (long long)n * H * W + (long long)blockIdx.x * RB * W;
+  const int kk = mode == 1 ? *a.kdev : 0;  // the component call (mode 0) passes no solver state
+  const float* xk_base = (kk & 1) ? a.X1 : a.X0;
+  float* xn_base = (kk & 1) ? a.X0 : a.X1;
+  P3 acc{0.f, 0.f, 0.f};
+  const int rows = H - (int)blockIdx.x * RB < RB ? H - (int)blockIdx.x * RB : RB;
+  for (int q = threadIdx.x; q < rows * W; q += blockDim.x) {
+    const int r = q / W, i = q % W;
+    float g = 0.f;
+    for (int jj = 0; jj < J; ++jj) g += gsum[(r * J + jj) * W + i];
+    const long long e = base0 + (long long)r * W + i;
+    if (mode == 0) dst[e] = g;
+    // x^{k+1} = z - tau (grad f(z) + lam grad g(z))       (Alg. 1 l.8)
+    else step_tail(a.z[e] - a.tau * (g + a.lam * a.gg[e]), e, a, xk_base, xn_base, acc);
+  }
+  if (mode == 1) reduce_store_p3(acc, a.partials + ((long long)n * a.parts + blockIdx.x) * 3);
+}
+
+static bool reg_n(int N) { return N == 256 || N == 512; }
+template <int T>
+static size_t rrow_smem() { return sizeof(float2) * ((size_t)8 * T + (size_t)16 * 16 * (T + 1)); }
+template <int T>
+static size_t rpinv_smem() { return rrow_smem<T>() + sizeof(float) * (size_t)16 * 16 * T; }
+static bool phase_j_ok(int J) { return J >= 1 && J <= 16 && (16 % J) == 0; }
+template <int T>
+static size_t rcol_smem() {
+  constexpr int CPB = 256 / T;  // twiddles, tile, team buffers, op / observation tile
+  return sizeof(float2) * ((size_t)8 * T + (size_t)16 * T * (CPB + 1) + (size_t)CPB * 16 * (T + 1) +
+                           (size_t)16 * T * CPB);
 }
 
 // ------------------------------------------------------------------ launchers
 static int ilog2(int v) { int l = 0; while ((1 << l) < v) ++l; return l; }
 
 static size_t row_smem(int W) {
-  const int tpr = (W / 2) < 256 ? (W / 2) : 256;
+  const int tpr = fft_tpr(W);
   const int rpb = 256 / tpr;
   return sizeof(float2) * (W / 2 + (size_t)rpb * row_pitch(W));
 }
 static size_t col_smem(int H) { return sizeof(float2) * (H / 2 + (size_t)FFT_CPB * col_pitch(H)); }
-static int rows_per_block(int W) { const int tpr = (W / 2) < 256 ? (W / 2) : 256; return 256 / tpr; }
+static int rows_per_block(int W) { return 256 / fft_tpr(W); }            // shared-memory row passes
+static int rows_per_block_any(int W) { return reg_n(W) ? 16 : rows_per_block(W); }  // the pass launched
 
-int fft_parts_per_image(int C, int H, int W) { return C * ((H + rows_per_block(W) - 1) / rows_per_block(W)); }
-int phase_parts_per_image(int H, int W) { return (H + rows_per_block(W) - 1) / rows_per_block(W); }
+int fft_parts_per_image(int C, int H, int W) { return C * ((H + rows_per_block_any(W) - 1) / rows_per_block_any(W)); }
+// the register row pass of phase retrieval covers 16 / J rows per block (J <= 16 masks)
+int phase_parts_per_image(int H, int W, int J) {
+  return (reg_n(W) && phase_j_ok(J)) ? (H * J + 15) / 16 : (H + rows_per_block(W) - 1) / rows_per_block(W);
+}
 
 bool fft_size_ok(int H, int W) {
   auto pow2 = [](int v) { return v >= 4 && v <= 1024 && (v & (v - 1)) == 0; };
@@ -489,15 +894,26 @@ bool fft_size_ok(int H, int W) {
 void fft_fill_args(FftArgs& f) { f.logH = ilog2(f.H); f.logW = ilog2(f.W); }
 
 void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s) {
-  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
+  dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.C, N);
+  if (f.W == 256) { launch_k(rblur_rows_fwd_kernel<16>, grid, 256, rrow_smem<16>(), s, f, src, mode); return; }
+  if (f.W == 512) { launch_k(rblur_rows_fwd_kernel<32>, grid, 512, rrow_smem<32>(), s, f, src, mode); return; }
   launch_k(blur_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f, src, mode);
 }
 void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s) {
+  if (reg_n(f.H)) {
+    const int cpb = f.H == 256 ? 16 : 8;
+    dim3 g((f.W / 2 + 1 + cpb - 1) / cpb, f.C, N);
+    if (f.H == 256) launch_k(rblur_cols_kernel<16>, g, 256, rcol_smem<16>(), s, f, op);
+    else launch_k(rblur_cols_kernel<32>, g, 256, rcol_smem<32>(), s, f, op);
+    return;
+  }
   dim3 grid((f.W / 2 + 1 + FFT_CPB - 1) / FFT_CPB, f.C, N);
   launch_k(blur_cols_kernel, grid, 256, col_smem(f.H), s, f, op);
 }
 void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
-  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.C, N);
+  dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.C, N);
+  if (f.W == 256) { launch_k(rblur_rows_inv_kernel<16>, grid, 256, rrow_smem<16>(), s, f, a, dst, mode); return; }
+  if (f.W == 512) { launch_k(rblur_rows_inv_kernel<32>, grid, 512, rrow_smem<32>(), s, f, a, dst, mode); return; }
   launch_k(blur_rows_inv_kernel, grid, 256, row_smem(f.W), s, f, a, dst, mode);
 }
 void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s) {
@@ -517,19 +933,46 @@ void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStre
   blur_diag_kernel<<<(n + 255) / 256, 256, 0, s>>>(khat, tau, dgl, n);
 }
 void launch_phase_rows_fwd(const FftArgs& f, int N, cudaStream_t s) {
-  dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), f.J, N);
+  dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.J, N);
+  if (f.W == 256) { launch_k(rphase_rows_fwd_kernel<16>, grid, 256, rrow_smem<16>(), s, f); return; }
+  if (f.W == 512) { launch_k(rphase_rows_fwd_kernel<32>, grid, 512, rrow_smem<32>(), s, f); return; }
   launch_k(phase_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f);
 }
 void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s) {
+  if (reg_n(f.H) && f.W % 16 == 0) {
+    const int cpb = f.H == 256 ? 16 : 8;
+    dim3 g(f.W / cpb, f.J, N);
+    if (f.H == 256) launch_k(rphase_cols_kernel<16>, g, 256, rcol_smem<16>(), s, f);
+    else launch_k(rphase_cols_kernel<32>, g, 256, rcol_smem<32>(), s, f);
+    return;
+  }
   dim3 grid(f.W / FFT_CPB, f.J, N);
   launch_k(phase_cols_kernel, grid, 256, col_smem(f.H), s, f);
 }
 void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
+  if (reg_n(f.W) && phase_j_ok(f.J)) {
+    dim3 g((f.H * f.J + 15) / 16, N);
+    if (f.W == 256) launch_k(rphase_rows_inv_kernel<16>, g, 256, rpinv_smem<16>(), s, f, a, dst, mode);
+    else launch_k(rphase_rows_inv_kernel<32>, g, 512, rpinv_smem<32>(), s, f, a, dst, mode);
+    return;
+  }
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), N);
   launch_k(phase_rows_inv_kernel, grid, 256, row_smem(f.W), s, f, a, dst, mode);
 }
 
 void init_attrs_fft() {
+  set_max_dyn_smem(rblur_rows_fwd_kernel<16>);
+  set_max_dyn_smem(rblur_rows_fwd_kernel<32>);
+  set_max_dyn_smem(rblur_rows_inv_kernel<16>);
+  set_max_dyn_smem(rblur_rows_inv_kernel<32>);
+  set_max_dyn_smem(rphase_rows_fwd_kernel<16>);
+  set_max_dyn_smem(rphase_rows_fwd_kernel<32>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<16>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<32>);
+  set_max_dyn_smem(rblur_cols_kernel<16>);
+  set_max_dyn_smem(rblur_cols_kernel<32>);
+  set_max_dyn_smem(rphase_cols_kernel<16>);
+  set_max_dyn_smem(rphase_cols_kernel<32>);
   set_max_dyn_smem(blur_rows_fwd_kernel);
   set_max_dyn_smem(blur_cols_kernel);
   set_max_dyn_smem(blur_rows_inv_kernel);

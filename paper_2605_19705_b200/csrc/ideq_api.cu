@@ -1001,7 +1001,7 @@ int step_parts(ideq_ctx* ctx) {
     return blur_parts_per_image(ctx->C, ctx->H, ctx->W, ctx->op.ksize);
   if ((ctx->op.kind == IDEQ_OP_BLUR || ctx->op.kind == IDEQ_OP_MRI) && ctx->op.step == IDEQ_STEP_PROX)
     return fft_parts_per_image(ctx->C, ctx->H, ctx->W);
-  if (ctx->op.kind == IDEQ_OP_PHASE) return phase_parts_per_image(ctx->H, ctx->W);
+  if (ctx->op.kind == IDEQ_OP_PHASE) return phase_parts_per_image(ctx->H, ctx->W, ctx->op.n_phase);
   const long long d = (long long)ctx->C * ctx->H * ctx->W;
   long long parts = d / 4096;
   if (parts < 1) parts = 1;
@@ -1471,7 +1471,7 @@ ideq_status ideq_create_ex(const ideq_net_desc* net, ideq_precision prec, int de
   {  // residual partials per image: the largest count any fidelity/step kernel can produce at this size
     int pc = 256;
     const int cand[3] = {blur_parts_per_image(ctx->C, H, W, 0) /* 32-pixel tiles: the larger count */, fft_parts_per_image(ctx->C, H, W),
-                         phase_parts_per_image(H, W)};
+                         phase_parts_per_image(H, W, 16) /* the most masks the register pass takes */};
     for (int v : cand) pc = v > pc ? v : pc;
     ctx->parts_cap = pc;
   }

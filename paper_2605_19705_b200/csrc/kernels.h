@@ -89,7 +89,7 @@ struct FftArgs {
 bool fft_size_ok(int H, int W);
 void fft_fill_args(FftArgs& f);
 int fft_parts_per_image(int C, int H, int W);
-int phase_parts_per_image(int H, int W);
+int phase_parts_per_image(int H, int W, int J);  // J = number of phase masks
 void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s);
 void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s);
 struct StepArgs;

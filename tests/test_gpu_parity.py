@@ -284,3 +284,46 @@ def test_tiny_whole_solve_kernel(batch, tol, K):
         n = int(orc["iters"].max())
         assert np.allclose(tr[:n], orc["rmax_trace"][:n], rtol=1e-3, atol=1e-6)
     assert rel_l2(outs[0][1], outs[1][1]) <= 1e-5
+
+
+@pytest.mark.parametrize("name,H,W,batch", [("C4", 256, 256, 16), ("C4", 512, 256, 2), ("C4", 128, 512, 2),
+                                            ("C5", 512, 512, 2), ("C5", 256, 512, 2), ("C5", 512, 128, 2),
+                                            ("C5", 256, 256, 3)])
+def test_fft_operators_at_register_fft_sizes(name, H, W, batch):
+    """The register-resident FFT passes (N = 256 / 512 along either axis, mixed with the shared-
+    memory passes for other sizes): phase-retrieval gradient (C4, P:958-970 style unitary F) and
+    FFT blur prox (C5) against the oracle's numpy FFT definitions, per image."""
+    torch = torch_cuda()
+    kw = dict(H=H, W=W, batch=batch)
+    if name == "C4":
+        kw["tau"] = 0.5 / 17
+    cfg = configs.get(name, **kw)
+    prob = synth.make_problem(cfg)
+    s = _solver(cfg, prob, "fp32")
+    fids = osolver.make_fidelities(cfg, prob)
+    x = (0.9 * prob["x_true"] + 0.05).astype(np.float32)
+    out = torch.zeros_like(_dev(torch, x))
+    if name == "C4":
+        s.fidelity_grad(_dev(torch, prob["y"]), _dev(torch, x), out)
+        for b in range(batch):
+            assert rel_l2(out[b].cpu().numpy(), fids[b].grad(x[b].astype(np.float64))) <= 1e-5, b
+    else:
+        s.fidelity_prox(_dev(torch, prob["y"]), _dev(torch, x), 0.7, out)
+        for b in range(batch):
+            assert rel_l2(out[b].cpu().numpy(), fids[b].prox(x[b].astype(np.float64), 0.7)) <= 2e-6, b
+
+
+@pytest.mark.parametrize("J,H", [(4, 256), (2, 256), (1, 8), (3, 256)])
+def test_phase_gradient_mask_counts(J, H):
+    """Phase-retrieval gradient with J masks (the register row pass sums the J inverse rows of a
+    pixel in a fixed order; J not dividing 16 takes the shared-memory pass) at W = 256."""
+    torch = torch_cuda()
+    cfg = configs.get("C4", batch=2, H=H, W=256, n_phase=J, tau=0.5 / 17)
+    prob = synth.make_problem(cfg)
+    s = _solver(cfg, prob, "fp32")
+    fids = osolver.make_fidelities(cfg, prob)
+    x = (0.9 * prob["x_true"] + 0.05).astype(np.float32)
+    out = torch.zeros_like(_dev(torch, x))
+    s.fidelity_grad(_dev(torch, prob["y"]), _dev(torch, x), out)
+    for b in range(2):
+        assert rel_l2(out[b].cpu().numpy(), fids[b].grad(x[b].astype(np.float64))) <= 1e-5, b
