@@ -571,13 +571,17 @@ __device__ __forceinline__ void team_fft(float2 (&v)[16], int t, float2* buf, co
   __syncwarp();  // the team buffer may be reused by the next transform
 }
 
+// Row passes: RNT teams (rows) per block. Small blocks keep the grid many waves deep for the
+// configs' small batches (C4: 16 images x 4 masks x 256 rows = 16384 row transforms).
+constexpr int RNT = 4;
+
 __device__ __forceinline__ void load_tw_all(float2* s_tw, const float2* g_tw, int N) {
   for (int k = threadIdx.x; k < N / 2; k += blockDim.x) s_tw[k] = g_tw[k];
 }
 
 // ---- blur / MRI rows (real planes): forward R2C (mode 0: src plane; 1: prox right-hand side)
 template <int T>
-__global__ void __launch_bounds__(16 * T) rblur_rows_fwd_kernel(FftArgs f, const float* __restrict__ src, int mode) {
+__global__ void __launch_bounds__(RNT * T) rblur_rows_fwd_kernel(FftArgs f, const float* __restrict__ src, int mode) {
   pdl_enter();
   constexpr int W = 16 * T, P = T + 1;
   extern __shared__ float2 smr[];
@@ -586,7 +590,7 @@ __global__ void __launch_bounds__(16 * T) rblur_rows_fwd_kernel(FftArgs f, const
   load_tw_all(tw, f.tw_w, W);
   __syncthreads();
   const int team = threadIdx.x / T, t = threadIdx.x % T;
-  const int h = blockIdx.x * 16 + team, c = blockIdx.y, n = blockIdx.z;
+  const int h = blockIdx.x * RNT + team, c = blockIdx.y, n = blockIdx.z;
   if (f.active && !f.active[n]) return;  // uniform per block
   if (h >= f.H) return;                  // whole team
   const long long e0 = ((long long)n * f.C + c) * f.H * W + (long long)h * W;
@@ -678,7 +682,7 @@ __global__ void __launch_bounds__(256) rblur_cols_kernel(FftArgs f, int op) {
 
 // ---- blur / MRI rows, inverse C2R (mode 0: store into dst; 1: x^{k+1} -> update + partials)
 template <int T>
-__global__ void __launch_bounds__(16 * T) rblur_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+__global__ void __launch_bounds__(RNT * T) rblur_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
   pdl_enter();
   constexpr int W = 16 * T, P = T + 1;
   extern __shared__ float2 smr[];
@@ -688,8 +692,8 @@ __global__ void __launch_bounds__(16 * T) rblur_rows_inv_kernel(FftArgs f, StepA
   __syncthreads();
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   const int c = blockIdx.y, n = blockIdx.z, H = f.H;
-  const bool valid = blockIdx.x * 16 + team < H;
-  const int h = valid ? blockIdx.x * 16 + team : H - 1;  // rows past H (H < 16) redo row H-1, unused
+  const bool valid = blockIdx.x * RNT + team < H;
+  const int h = valid ? blockIdx.x * RNT + team : H - 1;  // rows past H (H < RNT) redo row H-1, unused
   if (f.active && !f.active[n]) return;
   const int Wh = W / 2 + 1;
   const float2* S = f.spec + ((long long)n * f.C + c) * H * Wh + (long long)h * Wh;
@@ -722,7 +726,7 @@ __global__ void __launch_bounds__(16 * T) rblur_rows_inv_kernel(FftArgs f, StepA
 
 // ---- phase retrieval rows forward: U[n][j][h][:] = FFT_row(D_j[h][:] z[n][h][:])
 template <int T>
-__global__ void __launch_bounds__(16 * T) rphase_rows_fwd_kernel(FftArgs f) {
+__global__ void __launch_bounds__(RNT * T) rphase_rows_fwd_kernel(FftArgs f) {
   pdl_enter();
   constexpr int W = 16 * T, P = T + 1;
   extern __shared__ float2 smr[];
@@ -731,7 +735,7 @@ __global__ void __launch_bounds__(16 * T) rphase_rows_fwd_kernel(FftArgs f) {
   load_tw_all(tw, f.tw_w, W);
   __syncthreads();
   const int team = threadIdx.x / T, t = threadIdx.x % T;
-  const int h = blockIdx.x * 16 + team, j = blockIdx.y, n = blockIdx.z;
+  const int h = blockIdx.x * RNT + team, j = blockIdx.y, n = blockIdx.z;
   if (f.active && !f.active[n]) return;
   if (h >= f.H) return;  // whole team
   const float* zr = f.z + (long long)n * f.H * W + (long long)h * W;
@@ -802,19 +806,20 @@ __global__ void __launch_bounds__(256) rphase_cols_kernel(FftArgs f) {
 }
 
 // ---- phase rows inverse: v_j = IFFT_row(U_j) / sqrt(HW); grad f = sum_j 2 Re(conj(D_j) v_j). One
-// team per (row, mask): a block is RB = 16 / J rows x J masks (J in {1, 2, 4, 8, 16}); the J
-// contributions of a pixel are summed in a fixed order through shared memory before the update.
-template <int T>
-__global__ void __launch_bounds__(16 * T) rphase_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
+// team per (row, mask): a block is RB = NTI / J rows x J masks (NTI = 4 for J <= 4, else 16; J a
+// power of two <= 16); the J contributions of a pixel are summed in a fixed order through shared
+// memory before the update.
+template <int T, int NTI>
+__global__ void __launch_bounds__(NTI * T) rphase_rows_inv_kernel(FftArgs f, StepArgs a, float* __restrict__ dst, int mode) {
   pdl_enter();
   constexpr int W = 16 * T, P = T + 1;
   extern __shared__ float2 smr[];
   float2* tw = smr;
   float2 (*bufs)[16 * P] = reinterpret_cast<float2 (*)[16 * P]>(smr + W / 2);
-  float* gsum = reinterpret_cast<float*>(smr + W / 2 + 16 * 16 * P);  // [16 teams][W]
+  float* gsum = reinterpret_cast<float*>(smr + W / 2 + NTI * 16 * P);  // [NTI teams][W]
   load_tw_all(tw, f.tw_w, W);
   __syncthreads();
-  const int J = f.J, RB = 16 / J;
+  const int J = f.J, RB = NTI / J;
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   const int rl = team / J, j = team % J;
   const int n = blockIdx.y, H = f.H;
@@ -856,10 +861,10 @@ __global__ void __launch_bounds__(16 * T) rphase_rows_inv_kernel(FftArgs f, Step
 }
 
 static bool reg_n(int N) { return N == 256 || N == 512; }
-template <int T>
-static size_t rrow_smem() { return sizeof(float2) * ((size_t)8 * T + (size_t)16 * 16 * (T + 1)); }
-template <int T>
-static size_t rpinv_smem() { return rrow_smem<T>() + sizeof(float) * (size_t)16 * 16 * T; }
+template <int T, int NT = RNT>
+static size_t rrow_smem() { return sizeof(float2) * ((size_t)8 * T + (size_t)NT * 16 * (T + 1)); }
+template <int T, int NTI>
+static size_t rpinv_smem() { return rrow_smem<T, NTI>() + sizeof(float) * (size_t)NTI * 16 * T; }
 static bool phase_j_ok(int J) { return J >= 1 && J <= 16 && (16 % J) == 0; }
 template <int T>
 static size_t rcol_smem() {
@@ -878,12 +883,14 @@ static size_t row_smem(int W) {
 }
 static size_t col_smem(int H) { return sizeof(float2) * (H / 2 + (size_t)FFT_CPB * col_pitch(H)); }
 static int rows_per_block(int W) { return 256 / fft_tpr(W); }            // shared-memory row passes
-static int rows_per_block_any(int W) { return reg_n(W) ? 16 : rows_per_block(W); }  // the pass launched
+static int rows_per_block_any(int W) { return reg_n(W) ? RNT : rows_per_block(W); }  // the pass launched
 
 int fft_parts_per_image(int C, int H, int W) { return C * ((H + rows_per_block_any(W) - 1) / rows_per_block_any(W)); }
 // the register row pass of phase retrieval covers 16 / J rows per block (J <= 16 masks)
+static int phase_nti(int J) { return J <= 4 ? 4 : 16; }
 int phase_parts_per_image(int H, int W, int J) {
-  return (reg_n(W) && phase_j_ok(J)) ? (H * J + 15) / 16 : (H + rows_per_block(W) - 1) / rows_per_block(W);
+  return (reg_n(W) && phase_j_ok(J)) ? (H * J + phase_nti(J) - 1) / phase_nti(J)
+                                     : (H + rows_per_block(W) - 1) / rows_per_block(W);
 }
 
 bool fft_size_ok(int H, int W) {
@@ -895,8 +902,8 @@ void fft_fill_args(FftArgs& f) { f.logH = ilog2(f.H); f.logW = ilog2(f.W); }
 
 void launch_blur_rows_fwd(const FftArgs& f, const float* src, int mode, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.C, N);
-  if (f.W == 256) { launch_k(rblur_rows_fwd_kernel<16>, grid, 256, rrow_smem<16>(), s, f, src, mode); return; }
-  if (f.W == 512) { launch_k(rblur_rows_fwd_kernel<32>, grid, 512, rrow_smem<32>(), s, f, src, mode); return; }
+  if (f.W == 256) { launch_k(rblur_rows_fwd_kernel<16>, grid, RNT * 16, rrow_smem<16>(), s, f, src, mode); return; }
+  if (f.W == 512) { launch_k(rblur_rows_fwd_kernel<32>, grid, RNT * 32, rrow_smem<32>(), s, f, src, mode); return; }
   launch_k(blur_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f, src, mode);
 }
 void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s) {
@@ -912,8 +919,8 @@ void launch_blur_cols(const FftArgs& f, int op, int N, cudaStream_t s) {
 }
 void launch_blur_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.C, N);
-  if (f.W == 256) { launch_k(rblur_rows_inv_kernel<16>, grid, 256, rrow_smem<16>(), s, f, a, dst, mode); return; }
-  if (f.W == 512) { launch_k(rblur_rows_inv_kernel<32>, grid, 512, rrow_smem<32>(), s, f, a, dst, mode); return; }
+  if (f.W == 256) { launch_k(rblur_rows_inv_kernel<16>, grid, RNT * 16, rrow_smem<16>(), s, f, a, dst, mode); return; }
+  if (f.W == 512) { launch_k(rblur_rows_inv_kernel<32>, grid, RNT * 32, rrow_smem<32>(), s, f, a, dst, mode); return; }
   launch_k(blur_rows_inv_kernel, grid, 256, row_smem(f.W), s, f, a, dst, mode);
 }
 void launch_embed_kernel(const float* k, int ks, float* plane, int H, int W, cudaStream_t s) {
@@ -934,8 +941,8 @@ void launch_blur_diag(const float2* khat, float tau, float* dgl, int n, cudaStre
 }
 void launch_phase_rows_fwd(const FftArgs& f, int N, cudaStream_t s) {
   dim3 grid((f.H + rows_per_block_any(f.W) - 1) / rows_per_block_any(f.W), f.J, N);
-  if (f.W == 256) { launch_k(rphase_rows_fwd_kernel<16>, grid, 256, rrow_smem<16>(), s, f); return; }
-  if (f.W == 512) { launch_k(rphase_rows_fwd_kernel<32>, grid, 512, rrow_smem<32>(), s, f); return; }
+  if (f.W == 256) { launch_k(rphase_rows_fwd_kernel<16>, grid, RNT * 16, rrow_smem<16>(), s, f); return; }
+  if (f.W == 512) { launch_k(rphase_rows_fwd_kernel<32>, grid, RNT * 32, rrow_smem<32>(), s, f); return; }
   launch_k(phase_rows_fwd_kernel, grid, 256, row_smem(f.W), s, f);
 }
 void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s) {
@@ -951,9 +958,15 @@ void launch_phase_cols(const FftArgs& f, int N, cudaStream_t s) {
 }
 void launch_phase_rows_inv(const FftArgs& f, const StepArgs& a, float* dst, int mode, int N, cudaStream_t s) {
   if (reg_n(f.W) && phase_j_ok(f.J)) {
-    dim3 g((f.H * f.J + 15) / 16, N);
-    if (f.W == 256) launch_k(rphase_rows_inv_kernel<16>, g, 256, rpinv_smem<16>(), s, f, a, dst, mode);
-    else launch_k(rphase_rows_inv_kernel<32>, g, 512, rpinv_smem<32>(), s, f, a, dst, mode);
+    const int nti = phase_nti(f.J);
+    dim3 g((f.H * f.J + nti - 1) / nti, N);
+    if (nti == 4) {
+      if (f.W == 256) launch_k(rphase_rows_inv_kernel<16, 4>, g, 64, rpinv_smem<16, 4>(), s, f, a, dst, mode);
+      else launch_k(rphase_rows_inv_kernel<32, 4>, g, 128, rpinv_smem<32, 4>(), s, f, a, dst, mode);
+    } else {
+      if (f.W == 256) launch_k(rphase_rows_inv_kernel<16, 16>, g, 256, rpinv_smem<16, 16>(), s, f, a, dst, mode);
+      else launch_k(rphase_rows_inv_kernel<32, 16>, g, 512, rpinv_smem<32, 16>(), s, f, a, dst, mode);
+    }
     return;
   }
   dim3 grid((f.H + rows_per_block(f.W) - 1) / rows_per_block(f.W), N);
@@ -967,8 +980,10 @@ void init_attrs_fft() {
   set_max_dyn_smem(rblur_rows_inv_kernel<32>);
   set_max_dyn_smem(rphase_rows_fwd_kernel<16>);
   set_max_dyn_smem(rphase_rows_fwd_kernel<32>);
-  set_max_dyn_smem(rphase_rows_inv_kernel<16>);
-  set_max_dyn_smem(rphase_rows_inv_kernel<32>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<16, 4>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<32, 4>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<16, 16>);
+  set_max_dyn_smem(rphase_rows_inv_kernel<32, 16>);
   set_max_dyn_smem(rblur_cols_kernel<16>);
   set_max_dyn_smem(rblur_cols_kernel<32>);
   set_max_dyn_smem(rphase_cols_kernel<16>);

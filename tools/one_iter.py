@@ -3,9 +3,10 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2605_19705_b200 import configs, ideq, synth
-cfg = configs.get(os.environ.get("CFG", "C3"))
+name = os.environ.get("CFG", "C3")
+cfg = configs.get(name, **({"batch": int(os.environ["BATCH"])} if "BATCH" in os.environ else {}))
 prob = synth.make_problem(cfg)
-s = ideq.Solver(cfg, prob["weights"], precision="bf16")
+s = ideq.Solver(cfg, prob["weights"], precision=cfg.get("precision", "bf16"))
 s.set_operator(prob)
 y = torch.tensor(prob["y"]).cuda(); x = torch.tensor(prob["x0"]).cuda()
 s.set_profiling(True)
