@@ -15,8 +15,17 @@
  * in/out/aux: DEVICE NHWC tensors of fp32 (precision 0) or bf16 (precision 1).
  *   Hin, Win: spatial size of `in`; out has the kind's output size.
  * epi: 0 store, 1 softplus, 2 out = acc + aux, 3 out = acc * (1 - exp(-aux)).
- * use_tc: 1 = tcgen05 kernel (precision 1 only), 0 = FFMA kernel.
+ * use_tc: 1 = tcgen05 kernel (precision 1: bf16 operands; precision 0: 3xTF32), 0 = FFMA kernel.
  * Synchronises the device; returns an ideq_status code.
+ *
+ * ideq_debug_rb runs ONE fused level-0 residual block (rbf.cu), bf16, 32 channels, W in {128, 256}:
+ *   vjp 0: act = sp(A x) (written), out = x + B act
+ *   vjp 1: out = x + A^T((B^T x) . (1 - exp(-act)))          (act read: the saved activation)
+ * with A, B the block's two 3x3 convolutions (wA, wB: HOST fp32 [32][32][3][3]); x, out, act:
+ * DEVICE NHWC bf16 [N][H][W][32].
+ *
+ * ideq_debug_set_fusion switches the fused residual blocks of a context's network off (0) or on
+ * (1, the default) for the programs built afterwards (tests compare the two).
  */
 #ifndef IDEQ_DEBUG_H
 #define IDEQ_DEBUG_H
@@ -27,6 +36,9 @@ extern "C" {
 
 IDEQ_API int ideq_debug_conv(int kind, int precision, int use_tc, const float* w, int s0, int s1, int N, int Hin,
                              int Win, const void* in, void* out, const void* aux, int epi, char* err, int errlen);
+IDEQ_API int ideq_debug_rb(int vjp, const float* wA, const float* wB, int N, int H, int W, const void* x, void* out,
+                           void* act, char* err, int errlen);
+IDEQ_API int ideq_debug_set_fusion(ideq_ctx* ctx, int on);
 
 #ifdef __cplusplus
 }

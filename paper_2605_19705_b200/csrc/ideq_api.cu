@@ -53,7 +53,7 @@ NcclApi g_nccl;
 constexpr int NCCL_FLOAT32 = 7, NCCL_MAX = 2;
 
 // ------------------------------------------------------------------ program description
-enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IMG2FEAT_TC = 4 };
+enum LayerKind { L_GEMM = 0, L_IMG2FEAT = 1, L_FEAT2IMG = 2, L_IMG2FEAT_TC = 4, L_RBF = 5 };
 
 struct Layer {
   LayerKind kind;
@@ -70,6 +70,7 @@ struct Layer {
   int C = 0, wfeat = 0, epi = 0, N = 0, H = 0, W = 0;
   TcPlan* plan = nullptr;
   I2FPlan* i2f = nullptr;  // fused head (L_IMG2FEAT_TC): output tensor map
+  RbfPlan* rbf = nullptr;  // fused residual block (L_RBF)
   bool tc = false;  // tcgen05 path (bf16 U-Net layers) vs FFMA path
   bool headtail = false;  // head/tail layer (profiled in the head/tail class, not the conv roofline)
   double flops = 0, bytes = 0;
@@ -153,6 +154,7 @@ struct ideq_ctx {
   int mb = 0;
   size_t net_bytes = 0;
   // the last solve's step arguments (class timing replays its kernels)
+  bool fuse_rb = false;  // level-0 residual blocks as one launch (rbf.cu); ideq_debug_set_fusion
   bool have_last = false;
   bool last_fused = false;  // the last solve ran the whole-solve tiny-network kernel
   int last_N = 0;
@@ -691,6 +693,54 @@ ideq_status add_headtail(ideq_ctx* ctx, LayerKind kind, const std::string& wname
   return IDEQ_OK;
 }
 
+// Fused residual block at level 0 (rbf.cu): the two 3x3 convolutions of one block in one launch.
+// Forward: x = t, out = t', act = the saved activation a (written). VJP: x = g, out = g', act = a
+// (read). The GEMM operands are those of the two unfused layers (kind 0 forward, kind 1 adjoint).
+bool use_rbf(ideq_ctx* ctx, int l) {
+  return ctx->prec == IDEQ_PREC_BF16 && ctx->net.arch == IDEQ_NET_UNET4 && l == 0 && ctx->net.act == IDEQ_ACT_SOFTPLUS &&
+         rbf_supported(ctx->W, ctx->net.widths[0]) && ctx->fuse_rb;
+}
+
+ideq_status add_rbf(ideq_ctx* ctx, bool vjp, const std::string& nA, const std::string& nB, int N, int H, int W,
+                    const void* x, void* out, void* act, const std::string& lname) {
+  WeightSlices ws;
+  size_t tot;
+  slice_weights(ctx->net, ws, tot);
+  const int kind = vjp ? 1 : 0;
+  const std::string n1 = vjp ? nB : nA, n2 = vjp ? nA : nB;  // VJP: B^T first, then A^T
+  const void* w[2];
+  for (int i = 0; i < 2; ++i) {
+    const std::string& nm = i == 0 ? n1 : n2;
+    const std::string key = nm + "#" + std::to_string(kind) + "tc";
+    if (!ctx->wdev.count(key)) {
+      int ncols = 0, ntaps = 0, ktap = 0;
+      auto& sl = ws.t[nm];
+      std::vector<float> B = gemm_weights(kind, ctx->blob.data() + sl.first, sl.second, 32, ncols, ntaps, ktap);
+      ideq_status st = upload_gemm_weights(ctx, key, B);
+      if (st) return st;
+    }
+    w[i] = ctx->wdev[key];
+  }
+  const int C = ctx->net.widths[0];
+  ConvGeom g = make_geom(kind, N, H, W, C, C, 32, C, EPI_STORE);
+  Layer L;
+  L.kind = L_RBF;
+  L.name = lname;
+  L.tc = true;
+  L.in = x;
+  L.out = out;
+  L.aux = act;
+  L.flops = 2.0 * (2.0 * N * H * W * 9.0 * C * C);
+  L.bytes = 3.0 * (double)N * H * W * C * ctx->elt;  // read x (+ a), write a (forward) and the output
+  char err[256] = {0};
+  L.rbf = rbf_make_plan(vjp, N, H, W, g.dh, g.dw, g.dh, g.dw, (const __nv_bfloat16*)w[0], (const __nv_bfloat16*)w[1],
+                        x, out, act, ctx->num_sms, err, sizeof(err));
+  if (!L.rbf) return fail(ctx, IDEQ_E_CUDA, "layer %s: %s", lname.c_str(), err);
+  rbf_set_active(L.rbf, ctx->act_list, ctx->n_active);
+  ctx->prog.push_back(L);
+  return IDEQ_OK;
+}
+
 std::string rb(const char* p, int l, int r, const char* ab) {
   return std::string(p) + std::to_string(l) + "." + std::to_string(r) + "." + ab;
 }
@@ -702,7 +752,7 @@ ideq_status build_program(ideq_ctx* ctx, int N) {
   ctx->prog.clear();
   ideq_status st = build_program_impl(ctx, N);
   if (st) {
-    for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
+    for (auto& L : ctx->prog) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); if (L.rbf) rbf_free_plan(L.rbf); }
     ctx->prog.clear();
     return st;
   }
@@ -758,12 +808,18 @@ ideq_status build_program_impl(ideq_ctx* ctx, int N) {
       for (int r = 0; r < R; ++r) {
         void* a = ctx->saved["e" + std::to_string(l) + "." + std::to_string(r)];
         const int o = cur[l] == 0 ? 1 : 0;
-        if ((st = add_gemm(ctx, rb("e", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
-                           rb("e", l, r, "A"))))
-          return st;
-        if ((st = add_gemm(ctx, rb("e", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o), B(l, cur[l]), EPI_RESADD,
-                           rb("e", l, r, "B"))))
-          return st;
+        if (use_rbf(ctx, l)) {
+          if ((st = add_rbf(ctx, false, rb("e", l, r, "A"), rb("e", l, r, "B"), N, Hl[l], Wl[l], B(l, cur[l]), B(l, o), a,
+                            rb("e", l, r, "AB"))))
+            return st;
+        } else {
+          if ((st = add_gemm(ctx, rb("e", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
+                             rb("e", l, r, "A"))))
+            return st;
+          if ((st = add_gemm(ctx, rb("e", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o), B(l, cur[l]), EPI_RESADD,
+                             rb("e", l, r, "B"))))
+            return st;
+        }
         cur[l] = o;
       }
       if (l < 3) {
@@ -783,12 +839,18 @@ ideq_status build_program_impl(ideq_ctx* ctx, int N) {
       for (int r = 0; r < R; ++r) {
         void* a = ctx->saved["d" + std::to_string(l) + "." + std::to_string(r)];
         const int o2 = cur[l] == 0 ? 1 : 0;
-        if ((st = add_gemm(ctx, rb("d", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
-                           rb("d", l, r, "A"))))
-          return st;
-        if ((st = add_gemm(ctx, rb("d", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o2), B(l, cur[l]), EPI_RESADD,
-                           rb("d", l, r, "B"))))
-          return st;
+        if (use_rbf(ctx, l)) {
+          if ((st = add_rbf(ctx, false, rb("d", l, r, "A"), rb("d", l, r, "B"), N, Hl[l], Wl[l], B(l, cur[l]), B(l, o2),
+                            a, rb("d", l, r, "AB"))))
+            return st;
+        } else {
+          if ((st = add_gemm(ctx, rb("d", l, r, "A"), 0, N, Hl[l], Wl[l], B(l, cur[l]), a, nullptr, EPI_SOFTPLUS,
+                             rb("d", l, r, "A"))))
+            return st;
+          if ((st = add_gemm(ctx, rb("d", l, r, "B"), 0, N, Hl[l], Wl[l], a, B(l, o2), B(l, cur[l]), EPI_RESADD,
+                             rb("d", l, r, "B"))))
+            return st;
+        }
         cur[l] = o2;
       }
     }
@@ -809,6 +871,13 @@ ideq_status build_program_impl(ideq_ctx* ctx, int N) {
       const int o = g[l] == 0 ? 1 : 0;
       ideq_status s2;
       // q = (B^T g) . sp'(a) ; g' = g + A^T q
+      if (use_rbf(ctx, l)) {
+        if ((s2 = add_rbf(ctx, true, rb(p, l, r, "A"), rb(p, l, r, "B"), N, Hl[l], Wl[l], B(l, g[l]), B(l, o), a,
+                          rb(p, l, r, "BTAT"))))
+          return s2;
+        g[l] = o;
+        return IDEQ_OK;
+      }
       if ((s2 = add_gemm(ctx, rb(p, l, r, "B"), 1, N, Hl[l], Wl[l], B(l, g[l]), B(l, 2), a, EPI_SIGMUL,
                          rb(p, l, r, "BT"))))
         return s2;
@@ -897,7 +966,10 @@ void run_layer(ideq_ctx* ctx, const Layer& L, long long off) {
   const bool bf = ctx->prec == IDEQ_PREC_BF16;
   auto sh = [off](const float* p) { return p ? p + off : p; };
   auto shw = [off](float* p) { return p ? p + off : p; };
-  if (L.kind == L_IMG2FEAT_TC) {
+  if (L.kind == L_RBF) {
+    Prof p(ctx, IDEQ_K_CONV_TC, L.flops, L.bytes);
+    rbf_launch(L.rbf, s);
+  } else if (L.kind == L_IMG2FEAT_TC) {
     Prof p(ctx, IDEQ_K_HEADTAIL, L.flops, L.bytes);
     launch_img2feat_tc(L.i2f, sh(L.in_img), (const __nv_bfloat16*)L.wB, ctx->skip_frozen ? ctx->act_list : nullptr,
                        ctx->n_active,
@@ -937,6 +1009,7 @@ void run_layer(ideq_ctx* ctx, const Layer& L, long long off) {
 // Kernel-class filter of run_network: -1 = every layer (the iteration); otherwise only the layers
 // of that ideq_kernel_class (class timing).
 int layer_class(const Layer& L) {
+  if (L.kind == L_RBF) return IDEQ_K_CONV_TC;
   if (L.kind == L_GEMM && L.tc && !L.headtail) return IDEQ_K_CONV_TC;
   if (L.kind == L_GEMM && !L.tc) return IDEQ_K_CONV_SIMT;
   return IDEQ_K_HEADTAIL;
@@ -965,8 +1038,10 @@ ideq_status prepare_programs(ideq_ctx* ctx, int N) {
 // The live-image list indexes images of the batch: used when one network pass covers the batch.
 void enable_skip(ideq_ctx* ctx, bool on) {
   for (auto& kv : ctx->progs)
-    for (auto& L : kv.second.layers)
+    for (auto& L : kv.second.layers) {
       if (L.plan) tc_plan_enable_skip(L.plan, on);
+      if (L.rbf) rbf_enable_skip(L.rbf, on);
+    }
 }
 
 // ------------------------------------------------------------------ fidelity + step
@@ -1361,6 +1436,7 @@ void init_kernel_attributes() {
   init_attrs_step();
   init_attrs_fft();
   init_attrs_tiny();
+  init_attrs_rbf();
   done = true;
 }
 }  // namespace ideq
@@ -2303,6 +2379,62 @@ int ideq_debug_conv(int kind, int precision, int use_tc_, const float* w, int s0
   return rc;
 }
 
+int ideq_debug_rb(int vjp, const float* wA, const float* wB, int N, int H, int W, const void* x, void* out, void* act,
+                  char* err, int errlen) {
+  auto seterr = [&](const char* m) { if (err && errlen > 0) { snprintf(err, errlen, "%s", m); } };
+  if (!wA || !wB || !x || !out || !act || N < 1 || H < 1) { seterr("bad arguments"); return IDEQ_E_INVALID; }
+  if (!rbf_supported(W, 32)) { seterr("fused residual block: W must be 128 or 256"); return IDEQ_E_UNSUPPORTED; }
+  init_kernel_attributes();
+  const int kind = (vjp & 1) ? 1 : 0;
+  const float* w1 = (vjp & 1) ? wB : wA;
+  const float* w2 = (vjp & 1) ? wA : wB;
+  void* dW[2] = {nullptr, nullptr};
+  int rc = IDEQ_OK;
+  for (int i = 0; i < 2 && rc == IDEQ_OK; ++i) {
+    int ncols = 0, ntaps = 0, ktap = 0;
+    std::vector<float> B = gemm_weights(kind, i == 0 ? w1 : w2, {32, 32, 3, 3}, 32, ncols, ntaps, ktap);
+    std::vector<uint16_t> hb(B.size());
+    for (size_t k = 0; k < B.size(); ++k) hb[k] = f2bf(B[k]);
+    if (cudaMalloc(&dW[i], hb.size() * 2) != cudaSuccess) { seterr("cudaMalloc"); rc = IDEQ_E_NOMEM; break; }
+    cudaMemcpy(dW[i], hb.data(), hb.size() * 2, cudaMemcpyHostToDevice);
+  }
+  if (rc == IDEQ_OK) {
+    ConvGeom g = make_geom(kind, N, H, W, 32, 32, 32, 32, EPI_STORE);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    char e2[256] = {0};
+    RbfPlan* plan = rbf_make_plan((vjp & 1) != 0, N, H, W, g.dh, g.dw, g.dh, g.dw, (const __nv_bfloat16*)dW[0],
+                                  (const __nv_bfloat16*)dW[1], x, out, act, sms, e2, sizeof(e2));
+    if (plan) rbf_set_debug(plan, vjp >> 8);
+    if (!plan) { seterr(e2); rc = IDEQ_E_CUDA; }
+    else {
+      cudaError_t e0 = cudaDeviceSynchronize();
+      if (e0 != cudaSuccess) { seterr("error before the fused-block launch"); rc = IDEQ_E_CUDA; }
+      rbf_launch(plan, 0);
+      cudaError_t el = cudaGetLastError();
+      if (el != cudaSuccess && rc == IDEQ_OK) { seterr(cudaGetErrorString(el)); rc = IDEQ_E_CUDA; }
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess && rc == IDEQ_OK) { seterr(cudaGetErrorString(e)); rc = IDEQ_E_CUDA; }
+      if (vjp >> 8) rbf_set_debug(plan, vjp >> 8);  // prints the progress markers
+      rbf_free_plan(plan);
+    }
+  }
+  for (int i = 0; i < 2; ++i) if (dW[i]) cudaFree(dW[i]);
+  return rc;
+}
+
+int ideq_debug_set_fusion(ideq_ctx* ctx, int on) {
+  if (!ctx) return IDEQ_E_INVALID;
+  ctx->fuse_rb = on != 0;
+  for (auto& kv : ctx->progs)
+    for (auto& L : kv.second.layers) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); if (L.rbf) rbf_free_plan(L.rbf); }
+  ctx->progs.clear();
+  ctx->graph_key.clear();
+  return IDEQ_OK;
+}
+
 void ideq_destroy(ideq_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -2310,7 +2442,7 @@ void ideq_destroy(ideq_ctx* ctx) {
   if (ctx->gexec_plain) cudaGraphExecDestroy(ctx->gexec_plain);
   if (ctx->gexec_check) cudaGraphExecDestroy(ctx->gexec_check);
   for (auto& kv : ctx->progs)
-    for (auto& L : kv.second.layers) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); }
+    for (auto& L : kv.second.layers) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); if (L.rbf) rbf_free_plan(L.rbf); }
   for (auto& a : ctx->allocs) cudaFree(a.p);
   for (auto& b : ctx->jfb_pool) cudaFree(b.first);
   if (ctx->jfb_ws) cudaFree(ctx->jfb_ws);

@@ -174,6 +174,20 @@ void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat1
                         const int* n_act, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s);
 
+// Residual-block-fused level-0 convolutions (rbf.cu): forward t' = t + B sp(A t) (+ saved a) or
+// VJP g' = g + A^T((B^T g) . sp'(a)), full rows of W in {128, 256} pixels, 32 channels, bf16.
+struct RbfPlan;
+bool rbf_supported(int W, int C);
+RbfPlan* rbf_make_plan(bool vjp, int N, int H, int W, const int dh1[9], const int dw1[9], const int dh2[9],
+                       const int dw2[9], const __nv_bfloat16* w1, const __nv_bfloat16* w2, const void* x, void* out,
+                       void* act, int num_sms, char* err, size_t errlen);
+void rbf_set_active(RbfPlan* p, const int* act_list, const int* n_act);
+void rbf_enable_skip(RbfPlan* p, bool on);
+void rbf_launch(const RbfPlan* p, cudaStream_t s);
+void rbf_free_plan(RbfPlan* p);
+void rbf_set_debug(RbfPlan* p, int dbg);
+void init_attrs_rbf();
+
 // Whole-solve persistent kernel of the tiny network (tiny_solve.cu): one 8-CTA cluster per image.
 struct TinySolveArgs {
   int N, H, W, ks, kper;

@@ -67,7 +67,8 @@ class Profile(C.Structure):
 SYMBOLS = ["ideq_get_nccl_id", "ideq_create", "ideq_set_operator", "ideq_solve", "ideq_solve_host", "ideq_grad_g",
            "ideq_fidelity_grad", "ideq_fidelity_prox", "ideq_set_profiling", "ideq_get_profile",
            "ideq_launches_per_iteration", "ideq_last_error", "ideq_destroy", "ideq_abi_version", "ideq_debug_conv",
-           "ideq_jfb_grad", "ideq_create_ex", "ideq_get_plan", "ideq_time_class"]
+           "ideq_jfb_grad", "ideq_create_ex", "ideq_get_plan", "ideq_time_class", "ideq_debug_rb",
+           "ideq_debug_set_fusion"]
 
 _lib = None
 
@@ -316,6 +317,13 @@ class Solver:
         return {"ms": ms.value, "flops": fl.value, "bytes": by.value, "iter_ms": it.value,
                 "share": ms.value / it.value if it.value > 0 else None}
 
+    def set_fusion(self, on: bool):
+        """include/ideq_debug.h ideq_debug_set_fusion: fused level-0 residual blocks on / off."""
+        fn = self.lib.ideq_debug_set_fusion
+        fn.argtypes = [C.c_void_p, C.c_int]
+        fn.restype = C.c_int
+        self._check(fn(self.ctx, int(on)))
+
     def launches_per_iteration(self) -> int:
         return int(self.lib.ideq_launches_per_iteration(self.ctx))
 
@@ -332,6 +340,21 @@ def debug_conv(kind: int, precision: str, use_tc: bool, w: np.ndarray, N: int, H
     err = C.create_string_buffer(256)
     r = fn(kind, PREC[precision], int(use_tc), _fptr(w), w.shape[0], w.shape[1], N, Hin, Win, _ptr(inp), _ptr(out),
            _ptr(aux), epi, err, 256)
+    if r != OK:
+        raise IdeqError(r, err.value.decode())
+
+
+def debug_rb(vjp: bool, wA: np.ndarray, wB: np.ndarray, N: int, H: int, W: int, x, out, act):
+    """include/ideq_debug.h: one fused level-0 residual block on device NHWC bf16 tensors."""
+    lib = load_library()
+    fn = lib.ideq_debug_rb
+    fn.argtypes = [C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_int, C.c_int, C.c_int, C.c_void_p,
+                   C.c_void_p, C.c_void_p, C.c_char_p, C.c_int]
+    fn.restype = C.c_int
+    wa = np.ascontiguousarray(wA, dtype=np.float32)
+    wb = np.ascontiguousarray(wB, dtype=np.float32)
+    err = C.create_string_buffer(256)
+    r = fn(int(vjp), _fptr(wa), _fptr(wb), N, H, W, _ptr(x), _ptr(out), _ptr(act), err, 256)
     if r != OK:
         raise IdeqError(r, err.value.decode())
 

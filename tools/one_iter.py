@@ -8,6 +8,7 @@ cfg = configs.get(name, **({"batch": int(os.environ["BATCH"])} if "BATCH" in os.
 prob = synth.make_problem(cfg)
 s = ideq.Solver(cfg, prob["weights"], precision=cfg.get("precision", "bf16"))
 s.set_operator(prob)
+if "FUSE" in os.environ: s.set_fusion(os.environ["FUSE"] == "1")
 y = torch.tensor(prob["y"]).cuda(); x = torch.tensor(prob["x0"]).cuda()
 s.set_profiling(True)
 s.solve(y, x, s.params(max_iter=int(os.environ.get("ITERS", "1")), tol=0.0))
