@@ -2385,9 +2385,9 @@ int ideq_debug_rb(int vjp, const float* wA, const float* wB, int N, int H, int W
   if (!wA || !wB || !x || !out || !act || N < 1 || H < 1) { seterr("bad arguments"); return IDEQ_E_INVALID; }
   if (!rbf_supported(W, 32)) { seterr("fused residual block: W must be 128 or 256"); return IDEQ_E_UNSUPPORTED; }
   init_kernel_attributes();
-  const int kind = (vjp & 1) ? 1 : 0;
-  const float* w1 = (vjp & 1) ? wB : wA;
-  const float* w2 = (vjp & 1) ? wA : wB;
+  const int kind = vjp ? 1 : 0;
+  const float* w1 = vjp ? wB : wA;
+  const float* w2 = vjp ? wA : wB;
   void* dW[2] = {nullptr, nullptr};
   int rc = IDEQ_OK;
   for (int i = 0; i < 2 && rc == IDEQ_OK; ++i) {
@@ -2404,20 +2404,14 @@ int ideq_debug_rb(int vjp, const float* wA, const float* wB, int N, int H, int W
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     char e2[256] = {0};
-    RbfPlan* plan = rbf_make_plan((vjp & 1) != 0, N, H, W, g.dh, g.dw, g.dh, g.dw, (const __nv_bfloat16*)dW[0],
+    RbfPlan* plan = rbf_make_plan(vjp != 0, N, H, W, g.dh, g.dw, g.dh, g.dw, (const __nv_bfloat16*)dW[0],
                                   (const __nv_bfloat16*)dW[1], x, out, act, sms, e2, sizeof(e2));
-    if (plan) rbf_set_debug(plan, vjp >> 8);
     if (!plan) { seterr(e2); rc = IDEQ_E_CUDA; }
     else {
-      cudaError_t e0 = cudaDeviceSynchronize();
-      if (e0 != cudaSuccess) { seterr("error before the fused-block launch"); rc = IDEQ_E_CUDA; }
       rbf_launch(plan, 0);
-      cudaError_t el = cudaGetLastError();
-      if (el != cudaSuccess && rc == IDEQ_OK) { seterr(cudaGetErrorString(el)); rc = IDEQ_E_CUDA; }
       cudaError_t e = cudaDeviceSynchronize();
       if (e == cudaSuccess) e = cudaGetLastError();
-      if (e != cudaSuccess && rc == IDEQ_OK) { seterr(cudaGetErrorString(e)); rc = IDEQ_E_CUDA; }
-      if (vjp >> 8) rbf_set_debug(plan, vjp >> 8);  // prints the progress markers
+      if (e != cudaSuccess) { seterr(cudaGetErrorString(e)); rc = IDEQ_E_CUDA; }
       rbf_free_plan(plan);
     }
   }

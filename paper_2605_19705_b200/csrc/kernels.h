@@ -185,7 +185,6 @@ void rbf_set_active(RbfPlan* p, const int* act_list, const int* n_act);
 void rbf_enable_skip(RbfPlan* p, bool on);
 void rbf_launch(const RbfPlan* p, cudaStream_t s);
 void rbf_free_plan(RbfPlan* p);
-void rbf_set_debug(RbfPlan* p, int dbg);
 void init_attrs_rbf();
 
 // Whole-solve persistent kernel of the tiny network (tiny_solve.cu): one 8-CTA cluster per image.

@@ -4,25 +4,48 @@
 //   forward (Eq. 2's network):  a = sp(A t)  (saved for the VJP),  t' = t + B a
 //   input VJP (its transpose):           q = (B^T g) . sp'(a),              g' = g + A^T q
 // Run as two launches, the intermediate (a or q) makes a round trip through HBM and the block
-// input is read twice (conv input, then residual): at level 0 of C3 that is 671 MB per block for
-// 403 MB of compulsory traffic. This kernel computes the whole block for full image rows:
+// input is read twice (conv input, then residual): at level 0 of C3 that is 671 MB (forward) /
+// 805 MB (VJP) per block for 403 MB of compulsory traffic. This kernel computes the whole block
+// for full image rows:
 //
-//   * a CTA owns a run of consecutive output rows of one image and streams down it. Input rows
-//     (the block input x = t or g) arrive by TMA into a 4-slot ring of full-width rows with a zero
-//     pixel on either side (the convolutions' zero padding at the image's left / right border);
-//   * stage 1 computes the intermediate row u (128-pixel M tiles, the 9 taps as row- and pixel-
-//     shifted UMMA descriptors into the ring), its epilogue (softplus, or x sp'(a) with the saved
-//     activation from a second TMA ring) writes the row in the UMMA operand layout into a 4-slot
-//     ring of intermediate rows (forward: and TMA-stores it as the saved activation); rows outside
-//     the image are zeros (the second convolution's zero padding);
-//   * stage 2 computes the output row from three intermediate rows; its epilogue adds the
-//     residual, read from the input ring, writes the result in place over that input row and
-//     TMA-stores it.
-// HBM traffic per block: read x (+ a in the VJP), write u (forward) and the output: 403 MB at C3.
-// Each run recomputes two intermediate rows (h0 - 1 and the row below the last) -- 2 of ~55 rows.
+//   * a CTA owns a run of consecutive output rows of one image and streams down it. Input rows x
+//     (the block input t or g) arrive by TMA into a ring of full-width rows with a zero pixel on
+//     either side (the zero padding in w); out-of-image rows are zero-filled by TMA (padding in h);
+//   * stage 1 computes the intermediate rows u from x, stage 2 the output rows from u. Both fold
+//     the kernel ROW into the GEMM's N dimension: input row r, for each kernel column dw (the A
+//     operand shifted by dw pixels) and 16-channel K step, is ONE MMA of N = 96 whose three
+//     32-column blocks are the output rows r+1, r, r-1 (taps dh = -1, 0, +1). Output rows are
+//     accumulated in a ring of R TMEM blocks (a block is complete after its third input row) and
+//     each input row is read from shared memory 3 times per convolution instead of 9 (the level-0
+//     convolutions, N = 32, are otherwise bound by the shared-memory operand path). A window that
+//     wraps around the ring is issued as two MMAs. The epilogue zeroes a block after reading it,
+//     so every MMA accumulates;
+//   * stage-1 epilogue: softplus (forward; also stored to HBM as the saved activation a) or the
+//     sp'(a) product with the saved activation read from HBM (VJP), written in the UMMA operand
+//     layout into a ring of u rows (rows outside the image are zeros: conv 2's padding in h);
+//   * stage-2 epilogue: + the residual (the block input row, re-read from L2), stored with
+//     16-byte global stores (the two warps of a 32-byte sector store it back to back).
+// HBM traffic per block: read x (+ a in the VJP), write a (forward) and the output.
+// Each run recomputes two intermediate rows (h0 - 1 and h1) and reads two extra input rows.
 //
-// Warp roles (352 threads, one CTA per SM): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2..9 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4).
+// Warp roles (576 threads, one CTA per SM): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer, warps 2..17 epilogue (TMEM lane quadrant = warp % 4, 8-channel slice = (warp - 2) / 4).
+// MMA order per run: S1(k) for input rows k = 0 .. nu+1, and S2(j) for intermediate row j right
+// after S1(j+3), so the stage-1 epilogue of row j overlaps two MMA stages before S2(j) reads it.
+//
+// Status (B200, C3 level 0, 32 x 256 x 256 x 32, ncu launch list): forward 145 us, VJP 144 us per
+// block against 131 / 136 us for the two unfused launches, so the solver keeps the two-launch path
+// by default (ideq_debug_set_fusion switches this one on; tests/test_gpu_rbf.py keeps it exact).
+// What bounds it (tools/rbf_prof.cu stage timeline, tools/mma_rate_probe.cu):
+//   * the MMA stream alone runs at 2.5k clk per row (24 MMAs, ~70 clk each after removing the
+//     branches between tcgen05.mma instructions, which had cost ~150 clk per MMA);
+//   * TMEM holds a 4-row ring per stage and M tile at W = 256 (2 stages x 2 tiles x 4 x 32
+//     columns = 512), so a wrapped window must wait until the epilogue has drained the block it
+//     adds +0 to, and the epilogue (softplus: 768 clk of MUFU per row, tcgen05.ld/st, stores)
+//     and the MMA warp wait on each other every row: 4.2k clk per row end to end.
+// The row-in-N folding itself is sound (a 3x3 convolution per input row as 6 MMAs of N = 96 /
+// 128 at 56-64 clk each, against 18 MMAs of N = 32 at 40 clk); the remaining step is a deeper
+// ring (M = 64 tiles, or 2-CTA pairs splitting a row) so the epilogue can run a row behind.
 #include <cuda.h>
 #include <stdio.h>
 #include <string.h>
@@ -32,28 +55,42 @@
 
 namespace ideq {
 
-constexpr int RBF_THREADS = 352;
-constexpr int RBF_XS = 4, RBF_US = 4, RBF_AS = 2;  // ring depths (input rows, intermediate rows, saved act.)
-constexpr int RBF_C = 32;                          // channels (64-byte pixels, SW64)
+constexpr int RBF_EPI_WARPS = 16;         // 4 per TMEM lane quadrant, 8 channels each
+constexpr int RBF_CPW = 8;                // channels per epilogue warp
+constexpr int RBF_THREADS = (2 + RBF_EPI_WARPS) * 32;
+constexpr int RBF_C = 32;                 // channels (64-byte pixels, SW64)
 constexpr uint32_t RBF_PIX = RBF_C * 2;
+constexpr uint32_t RBF_WTAP = RBF_C * RBF_PIX;     // 2 KB: B operand of one tap (32 rows x 64 B)
+// B operand of one convolution, per kernel column dw: 6 blocks of 32 rows [w0 w1 w2 Z w0 w1]
+// (w = window position, Z = zeros), so a ring window that wraps (ring blocks 2,3,0 or 3,0,1) is ONE
+// N = 128 MMA over all four blocks with B starting at block 2 or 1 -- the fourth block gets +0
+constexpr uint32_t RBF_WGROUP = 6 * RBF_WTAP;      // 12 KB
+constexpr uint32_t RBF_WCONV = 3 * RBF_WGROUP;     // 36 KB per convolution
 
-struct RbfParams {
-  int N, H, W, MT;            // images, rows, width (= 128 MT)
-  int dh1[9], dw1[9], dh2[9], dw2[9];
-  uint32_t slot;              // bytes of one ring slot (1 KB pad, zero pixel, W pixels, zero pixel, pad)
-  const __nv_bfloat16* w1;    // [9][32][32] GEMM operand of conv 1 / conv 2 (gemm_weights layout)
-  const __nv_bfloat16* w2;
-  const int* act_list;        // live-image list (null: every image)
-  const int* n_act;
-  uint32_t tmem_cols;
-  int dbg;  // bisection: bit0 no TMA loads, bit1 no MMAs, bit2 no epilogue smem / TMA stores
+template <int MT>
+struct RbfCfg {  // MT = W / 128 M tiles per row
+  static constexpr int W = MT * 128;
+  static constexpr int R = 4;                          // TMEM ring blocks per stage and M tile
+  static constexpr int XS = MT == 1 ? 6 : 4;           // input-row ring (one S1 each + prefetch)
+  static constexpr int US = MT == 1 ? 6 : 4;           // intermediate-row ring
+  // slot: 1 KB pad (pixel -1 = zero at its end), W pixels, pixel W = zero, rounded to 1 KB
+  static constexpr uint32_t SLOT = (1024u + (uint32_t)(W + 1) * RBF_PIX + 1023u) & ~1023u;
+  static size_t smem() { return 1024 + 2 * RBF_WCONV + (size_t)(XS + US) * SLOT + 512; }
 };
 
-// payload (pixel 0) of a ring slot: 1024-byte aligned; pixel -1 and pixel W are zero forever
-__device__ __forceinline__ uint32_t rbf_payload(uint32_t ring, int slot, uint32_t slot_bytes) {
-  return ring + (uint32_t)slot * slot_bytes + 1024u;
-}
-// 16-byte chunk j (8 channels) of pixel p in a payload (the SW64 pattern TMA / UMMA use)
+struct RbfParams {
+  int N, H, W;
+  int dh1[9], dw1[9], dh2[9], dw2[9];
+  const __nv_bfloat16* w1;    // [9][32][32] GEMM operand of conv 1 / conv 2 (gemm_weights layout)
+  const __nv_bfloat16* w2;
+  const __nv_bfloat16* x;     // [N][H][W][32] block input (the residual, re-read from L2)
+  __nv_bfloat16* out;         // [N][H][W][32] block output
+  __nv_bfloat16* act;         // saved activation a: written (forward) / read (VJP)
+  const int* act_list;        // live-image list (null: every image)
+  const int* n_act;
+};
+
+// 16-byte chunk j (8 channels) of pixel p in a row payload (the SW64 pattern TMA / UMMA use)
 __device__ __forceinline__ uint32_t rbf_chunk(uint32_t payload, int p, int j) {
   return payload + (uint32_t)p * RBF_PIX + (uint32_t)((j ^ ((p >> 1) & 3)) << 4);
 }
@@ -65,15 +102,49 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+#ifndef RBF_TRACE
+#define RBF_TRACE 0
+#endif
+#if RBF_TRACE  // stage timeline of CTA 0 (tools/rbf_prof.cu): one clock per (event, row)
+__device__ long long g_rbf_trace[16][256];
+#define RBF_EV(code, row)                                                   \
+  do {                                                                      \
+    if (blockIdx.x == 0 && (row) >= 0 && (row) < 256) g_rbf_trace[code][row] = clock64(); \
+  } while (0)
+#else
+#define RBF_EV(code, row) \
+  do {                    \
+  } while (0)
+#endif
+// mbarrier wait that suspends the thread (up to the hint, in ns) instead of spinning: the 16
+// epilogue warps wait most of the time, and spinning try_wait loops take issue slots from the
+// MMA warp that shares their scheduler
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WS_%=;\n}\n" ::"r"(bar),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+// named barrier 1 over the epilogue warps
+__device__ __forceinline__ void rbf_epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(RBF_EPI_WARPS * 32) : "memory");
+}
+// tcgen05.ld / st of 8 columns (32 lanes x 32 bit)
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
                : "memory");
 }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// The CTA's runs: rows [r0, r1) of the (live) row sequence q = image_index * H + h, cut at image
+// The CTA's runs: rows [q0, q1) of the (live) row sequence q = image_index * H + h, cut at image
 // boundaries. Every role walks the same sequence.
 struct RbfRun { int n, h0, h1; };
 __device__ __forceinline__ bool rbf_next_run(const RbfParams& P, int& q, int q1, RbfRun& run) {
@@ -88,367 +159,344 @@ __device__ __forceinline__ bool rbf_next_run(const RbfParams& P, int& q, int q1,
   return true;
 }
 
-__device__ int* g_rbf_prog;  // debug: progress markers in host-mapped memory (null: off)
-__device__ __forceinline__ void rbf_mark(int slot, int v) {
-  if (g_rbf_prog && blockIdx.x == 0) { ((volatile int*)g_rbf_prog)[slot] = v; __threadfence_system(); }
-}
-
-template <bool VJP>
+template <int MT, bool VJP>
 __global__ void __launch_bounds__(RBF_THREADS, 1)
-    rbf_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmOut,
-               const __grid_constant__ CUtensorMap tmU, const __grid_constant__ RbfParams P) {
+    rbf_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ RbfParams P) {
+  using Cfg = RbfCfg<MT>;
+  constexpr int XS = Cfg::XS, US = Cfg::US, R = Cfg::R, W = Cfg::W;
+  constexpr uint32_t SLOT = Cfg::SLOT;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   unsigned char* gbase = smem_raw + (base - smem_u32(smem_raw));
-  const int W = P.W, MT = P.MT;
-  const uint32_t SLOT = P.slot;
-  // [weights conv1 9 x 2 KB][weights conv2][x ring][u ring][a ring (VJP)][barriers]
-  const uint32_t sW1 = base, sW2 = base + 9u * 2048u;
-  const uint32_t sX = base + 18u * 2048u;
-  const uint32_t sU = sX + RBF_XS * SLOT;
-  const uint32_t sA = sU + RBF_US * SLOT;
-  const uint32_t sBar = sA + (VJP ? RBF_AS * SLOT : 0u);
-  // barriers: xfull[XS] xempty[XS] ufull[US] uempty[US] afull[AS] aempty[AS] t1full[2] t1empty[2] t2full[2] t2empty[2]
-  const uint32_t xfull0 = sBar, xempty0 = xfull0 + 8u * RBF_XS, ufull0 = xempty0 + 8u * RBF_XS,
-                 uempty0 = ufull0 + 8u * RBF_US, afull0 = uempty0 + 8u * RBF_US, aempty0 = afull0 + 8u * RBF_AS,
-                 t1full0 = aempty0 + 8u * RBF_AS, t1empty0 = t1full0 + 16u, t2full0 = t1empty0 + 16u,
-                 t2empty0 = t2full0 + 16u;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (t2empty0 + 16u - base));
+  // [B operands conv 1 | conv 2][x ring][u ring][barriers]
+  const uint32_t sW1 = base, sW2 = base + RBF_WCONV;
+  const uint32_t sX = base + 2 * RBF_WCONV;
+  const uint32_t sU = sX + XS * SLOT;
+  const uint32_t sBar = sU + US * SLOT;
+  const uint32_t xfull0 = sBar, xempty0 = xfull0 + 8u * XS, ufull0 = xempty0 + 8u * XS, uempty0 = ufull0 + 8u * US,
+                 t1done0 = uempty0 + 8u * US, t1free0 = t1done0 + 8u * R, t2done0 = t1free0 + 8u * R,
+                 t2free0 = t2done0 + 8u * R;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(gbase + (t2free0 + 8u * R - base));
   const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
-  // ---- prologue: weights into the UMMA B layout (rows of 64 bytes, SW64), zero rings, barriers
-  for (int i = threadIdx.x; i < ((P.dbg & 16) ? 0 : 2 * 9 * 32 * 4); i += blockDim.x) {
-    const int which = i / (9 * 32 * 4), r = (i / 4) % (9 * 32), j = i & 3;  // r = tap * 32 + n
-    const __nv_bfloat16* src = (which ? P.w2 : P.w1) + (size_t)r * 32 + j * 8;
-    const uint32_t dst = (which ? sW2 : sW1) + (uint32_t)r * 64u + (uint32_t)((j ^ ((r >> 1) & 3)) << 4);
-    st_shared_v4(dst, *reinterpret_cast<const uint4*>(src));
+  // ---- prologue: B operands, grouped by kernel column dw: 3 groups of 6 blocks [w0 w1 w2 Z w0 w1]
+  // of 32 rows (co), window position w = 0, 1, 2 <-> tap dh = +1, 0, -1 (the output rows r-1, r,
+  // r+1 of input row r); K-major 64-byte rows, SW64. Zero rings (pad pixels stay zero), barriers,
+  // TMEM.
+  for (int i = threadIdx.x; i < 2 * 3 * 6 * RBF_C * 4; i += blockDim.x) {
+    const int which = i / (18 * RBF_C * 4), rem = i % (18 * RBF_C * 4), row = rem >> 2, j = rem & 3;
+    const int blk = (row / RBF_C) % 6, wpos = blk < 3 ? blk : (blk == 3 ? -1 : blk - 4);
+    const int dwi = row / (6 * RBF_C) - 1, dh = wpos < 0 ? 99 : 1 - wpos, co = row & (RBF_C - 1);
+    const int* th = which ? P.dh2 : P.dh1;
+    const int* tw = which ? P.dw2 : P.dw1;
+    int tap = -1;
+    for (int t = 0; t < 9; ++t)
+      if (th[t] == dh && tw[t] == dwi) tap = t;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (tap >= 0) v = *reinterpret_cast<const uint4*>((which ? P.w2 : P.w1) + ((size_t)tap * RBF_C + co) * RBF_C + j * 8);
+    st_shared_v4((which ? sW2 : sW1) + (uint32_t)row * RBF_PIX + (uint32_t)((j ^ ((row >> 1) & 3)) << 4), v);
   }
-  {
-    const uint32_t ring_bytes = (RBF_XS + RBF_US + (VJP ? RBF_AS : 0)) * SLOT;
-    for (uint32_t o = threadIdx.x * 16u; o < ((P.dbg & 32) ? 0u : ring_bytes); o += blockDim.x * 16u)
-      st_shared_v4(sX + o, make_uint4(0u, 0u, 0u, 0u));
-  }
+  for (uint32_t o = threadIdx.x * 16u; o < (uint32_t)(XS + US) * SLOT; o += blockDim.x * 16u)
+    st_shared_v4(sX + o, make_uint4(0u, 0u, 0u, 0u));
   if (threadIdx.x == 0) {
-    for (int s = 0; s < RBF_XS; ++s) { mbar_init(xfull0 + 8u * s, 1); mbar_init(xempty0 + 8u * s, 2); }
-    // uempty: the MMA warp's commit after the row's last use (+ forward: the epilogue once the
-    // row's TMA store has read the slot)
-    for (int s = 0; s < RBF_US; ++s) { mbar_init(ufull0 + 8u * s, 1); mbar_init(uempty0 + 8u * s, VJP ? 1 : 2); }
-    for (int s = 0; s < RBF_AS; ++s) { mbar_init(afull0 + 8u * s, 1); mbar_init(aempty0 + 8u * s, 8); }  // 8 epilogue warps
-    for (int s = 0; s < 2; ++s) {
-      mbar_init(t1full0 + 8u * s, 1); mbar_init(t1empty0 + 8u * s, 8);
-      mbar_init(t2full0 + 8u * s, 1); mbar_init(t2empty0 + 8u * s, 8);
+    for (int s = 0; s < XS; ++s) { mbar_init(xfull0 + 8u * s, 1); mbar_init(xempty0 + 8u * s, 1); }
+    for (int s = 0; s < US; ++s) { mbar_init(ufull0 + 8u * s, 1); mbar_init(uempty0 + 8u * s, 1); }
+    for (int s = 0; s < R; ++s) {
+      mbar_init(t1done0 + 8u * s, 1); mbar_init(t1free0 + 8u * s, RBF_EPI_WARPS);
+      mbar_init(t2done0 + 8u * s, 1); mbar_init(t2free0 + 8u * s, RBF_EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmX);
-    prefetch_tmap(&tmOut);
-    prefetch_tmap(&tmU);
   }
-  if (warp == 1 && !(P.dbg & 256)) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                 "r"(P.tmem_cols)
+                 "r"(512)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  fence_async_smem();  // weights and zeroed rings -> async proxy (UMMA / TMA)
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  fence_async_smem();  // B operands and zeroed rings -> async proxy
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);
-  if (threadIdx.x == 0) rbf_mark(0, 1);
-  if (P.dbg & 128) return;
+  if (warp >= 2) {  // every ring block starts (and is returned by the epilogue) zeroed
+    const uint32_t ta = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(((warp - 2) >> 2) * 128);
+#pragma unroll
+    for (int c = 0; c < 128; c += 8) tmem_zero8(ta + (uint32_t)c);
+    tmem_st_wait();
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
 
   // this CTA's rows of the live row sequence
   int nimg = P.N;
   if (P.act_list) nimg = ld_volatile_s32(P.n_act);
   const long long Q = (long long)nimg * P.H;
   const int q0 = (int)(Q * blockIdx.x / gridDim.x), q1 = (int)(Q * (blockIdx.x + 1) / gridDim.x);
-  const uint32_t row_bytes = (uint32_t)W * RBF_PIX;
-  if (P.dbg & 8192) return;
 
-  if (warp == 0 && !(P.dbg & 1024)) {
-    // ---------------- producer: x rows h0-2 .. h1+1 of each run (+ VJP: saved-activation rows
-    // h0-1 .. h1), in the order x0 x1 x2 | a0 x3 | a1 x4 | ... so no ring waits on a later load
-    uint32_t xc = 0, ac = 0;
+  if (warp == 0) {
+    // ---------------- producer: x rows h0-2 .. h1+1 of each run (run offsets 0 .. nu+1)
+    uint32_t xc = 0;
     int q = q0;
     RbfRun run;
-    auto load_x = [&](int n, int h) {
-      const int s = (int)(xc % RBF_XS);
-      mbar_wait(xempty0 + 8u * s, ((xc / RBF_XS) & 1u) ^ 1u);
-      if (elect_one()) {
-        if (P.dbg & 1) mbar_arrive(xfull0 + 8u * s);
-        else {
-        mbar_expect_tx(xfull0 + 8u * s, row_bytes);
-        tma_load_4d(rbf_payload(sX, s, SLOT), &tmX, xfull0 + 8u * s, 0, 0, h, n);  // rows outside: zero fill
-        }
-      }
-      __syncwarp();
-      ++xc;
-      if (lane == 0) rbf_mark(1, (int)xc);
-    };
-    auto load_a = [&](int n, int h) {
-      const int s = (int)(ac % RBF_AS);
-      mbar_wait(aempty0 + 8u * s, ((ac / RBF_AS) & 1u) ^ 1u);
-      if (elect_one()) {
-        mbar_expect_tx(afull0 + 8u * s, row_bytes);
-        tma_load_4d(rbf_payload(sA, s, SLOT), &tmU, afull0 + 8u * s, 0, 0, h, n);
-      }
-      __syncwarp();
-      ++ac;
-    };
     while (rbf_next_run(P, q, q1, run)) {
-      const int nu = run.h1 - run.h0 + 2;  // intermediate rows h0-1 .. h1
-      load_x(run.n, run.h0 - 2);
-      load_x(run.n, run.h0 - 1);
-      load_x(run.n, run.h0);
-      for (int iu = 0; iu < nu; ++iu) {
-        if (VJP) load_a(run.n, run.h0 - 1 + iu);
-        if (iu + 3 <= nu + 1) load_x(run.n, run.h0 - 2 + iu + 3);
+      const int nx = run.h1 - run.h0 + 4;
+      for (int k = 0; k < nx; ++k, ++xc) {
+        const int s = (int)(xc % XS);
+        mbar_wait_sleep(xempty0 + 8u * s, ((xc / XS) & 1u) ^ 1u);
+        if (elect_one()) {
+          mbar_expect_tx(xfull0 + 8u * s, (uint32_t)W * RBF_PIX);
+          tma_load_4d(sX + (uint32_t)s * SLOT + 1024u, &tmX, xfull0 + 8u * s, 0, 0, run.h0 - 2 + k, run.n);
+        }
+        __syncwarp();
       }
     }
-  } else if (warp == 1 && !(P.dbg & 2048)) {
-    // ---------------- MMA issuer: S1(h0-1), S1(h0), then S1(r+1), S2(r) for r = h0 .. h1-1
-    const uint32_t idesc = make_idesc_bf16(RBF_C);
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
     const uint64_t dW1 = make_sdesc(sW1, 512u, 4u), dW2 = make_sdesc(sW2, 512u, 4u);
-    auto commit = [&](uint32_t bar) {
-      if (P.dbg & 512) { if (lane == 0) mbar_arrive(bar); __syncwarp(); }
-      else mma_commit_elect(bar);
-    };
-    uint32_t xc = 0, uc = 0, c1 = 0, c2 = 0;  // running ring / accumulator counters
+    uint32_t xc = 0, uc = 0, oc = 0;  // ring counters (input rows, intermediate rows, output rows)
     int q = q0;
     RbfRun run;
-    // A operand of tap (dh, dw), M tile mt: payload of the ring row for dh, shifted by dw pixels
-    auto mma_row = [&](uint32_t d, uint32_t ring, uint32_t rc_center, int nring, const int* dh, const int* dw,
-                       uint64_t dWb) {
-      for (int mt = 0; mt < MT; ++mt) {
+    // An input row (payload address) contributes to ring rows g_lo .. g_hi (global counters, <= 3,
+    // window positions w_lo ..): 3 dw x 2 K steps, each one MMA -- N = 96 at the window's first
+    // block, or for a full window that wraps N = 128 over the whole ring with the rotated B (the
+    // clipped windows at run ends that wrap are split in two).
+    // Descriptors are built once per window and stepped by constants: the single issuing thread's
+    // instruction stream between MMAs is what bounds this loop otherwise (~150 clk per MMA with
+    // per-MMA descriptor arithmetic vs 56 clk for the N = 96 MMA itself, tools/mma_rate_probe.cu).
+    const uint32_t idesc32 = make_idesc_bf16(32);
+    auto mma_window = [&](uint32_t stage_col, uint32_t payload, uint64_t dWb, uint32_t g_lo, uint32_t g_hi, int w_lo) {
+      uint32_t b_lo = g_lo % R;
+      const uint32_t n = g_hi - g_lo + 1;
+      uint32_t n1 = min(n, (uint32_t)R - b_lo), n2 = n - n1;  // blocks before / after the wrap
+      uint32_t bstart = (uint32_t)w_lo;                       // first B block of the window
+      if (n == 3 && n2 != 0) {  // full window that wraps: N = 128 over blocks 0..3, B rotated
+        bstart = b_lo == 2 ? 2u : 1u;
+        b_lo = 0;
+        n1 = 4;
+        n2 = 0;
+      }
+      const uint32_t id1 = idesc32 + ((n1 - 1u) << 19), id2 = idesc32 + ((n2 - 1u) << 19);  // N >> 3 = 4 n
+      const uint64_t b1 = dWb + (uint64_t)((bstart * RBF_WTAP) >> 4), b2 = b1 + (uint64_t)((n1 * RBF_WTAP) >> 4);
+      const uint64_t a0 = make_sdesc(payload - RBF_PIX, 512u, 4u);  // dw = -1 window of M tile 0
+      // the hot path (n2 == 0) is a straight run of MMAs: a branch between two tcgen05.mma
+      // instructions costs far more issue time than the MMA's own ~60 clk
+      if (n2 == 0) {
 #pragma unroll
-        for (int tap = 0; tap < 9; ++tap) {
-          const int s = (int)((rc_center + (uint32_t)(nring + dh[tap])) % (uint32_t)nring);
-          const uint32_t a_addr = rbf_payload(ring, s, SLOT) + (uint32_t)((128 * mt + dw[tap]) * (int)RBF_PIX);
-          const uint64_t ad = make_sdesc(a_addr, 512u, 4u);
-          const uint64_t bd = dWb + (((uint32_t)tap * 2048u) >> 4);
+        for (int mt = 0; mt < MT; ++mt) {
+          const uint32_t d1 = tmem_base + stage_col + (uint32_t)(mt * R * RBF_C) + b_lo * RBF_C;
+          const uint64_t am = a0 + (uint64_t)(mt * 128 * (int)RBF_PIX / 16);
 #pragma unroll
-          for (int k = 0; k < 2; ++k)
-            mma_bf16_elect(d + (uint32_t)(mt * RBF_C), ad + 2u * k, bd + 2u * k, idesc, (tap | k) ? 1u : 0u);
+          for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              mma_bf16_elect(d1, am + (uint64_t)(dwi * (int)RBF_PIX / 16 + 2 * k),
+                             b1 + (uint64_t)(dwi * (int)RBF_WGROUP / 16 + 2 * k), id1, 1u);
+        }
+      } else {
+#pragma unroll 1
+        for (int mt = 0; mt < MT; ++mt) {
+          const uint32_t d1 = tmem_base + stage_col + (uint32_t)(mt * R * RBF_C) + b_lo * RBF_C;
+          const uint32_t d2 = tmem_base + stage_col + (uint32_t)(mt * R * RBF_C);
+          const uint64_t am = a0 + (uint64_t)(mt * 128 * (int)RBF_PIX / 16);
+#pragma unroll
+          for (int dwi = 0; dwi < 3; ++dwi)
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const uint64_t ad = am + (uint64_t)(dwi * (int)RBF_PIX / 16 + 2 * k);
+              const uint64_t boff = (uint64_t)(dwi * (int)RBF_WGROUP / 16 + 2 * k);
+              mma_bf16_elect(d1, ad, b1 + boff, id1, 1u);
+              mma_bf16_elect(d2, ad, b2 + boff, id2, 1u);
+            }
         }
       }
     };
     while (rbf_next_run(P, q, q1, run)) {
       const int nu = run.h1 - run.h0 + 2, no = run.h1 - run.h0;
-      const uint32_t xb = xc, ub = uc;  // ring counters of the run's first x / u row
-      // S1 of intermediate row iu (image row h0-1+iu) reads x run rows iu .. iu+2
-      auto s1 = [&](int iu) {
-        mbar_wait(xfull0 + 8u * ((xb + iu + 2) % RBF_XS), ((xb + iu + 2) / RBF_XS) & 1u);
-        if (iu == 0) {
-          mbar_wait(xfull0 + 8u * (xb % RBF_XS), (xb / RBF_XS) & 1u);
-          mbar_wait(xfull0 + 8u * ((xb + 1) % RBF_XS), ((xb + 1) / RBF_XS) & 1u);
+      const uint32_t xb = xc, ub = uc, ob = oc;
+      // S1(k): input row k (image row h0-2+k) -> intermediate rows iu = k-2 .. k (image row h0-1+iu)
+      auto s1 = [&](int k) {
+        if (lane == 0) RBF_EV(2, k);
+        const uint32_t c = xb + (uint32_t)k;
+        mbar_wait(xfull0 + 8u * (c % XS), (c / XS) & 1u);
+        const int lo = max(0, k - 2), hi = min(k, nu - 1);
+        if (k < nu) {  // first contribution to intermediate row k: its block must be back (zeroed)
+          const uint32_t g = ub + (uint32_t)k;
+          mbar_wait(t1free0 + 8u * (g % R), ((g / R) & 1u) ^ 1u);
+          // a wrapping full window adds +0 to the fourth block: wait until the epilogue has drained it
+          if (k >= 2 && ((g - 2u) % R) >= 2u) mbar_wait(t1free0 + 8u * ((g + 1u) % R), (((g + 1u) / R) & 1u) ^ 1u);
         }
-        const int acc = (int)(c1 & 1u);
-        mbar_wait(t1empty0 + 8u * acc, ((c1 >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const int h = run.h0 - 1 + iu;
-        if (h >= 0 && h < P.H && !(P.dbg & 2))
-          mma_row(tmem_base + (uint32_t)(acc * MT * RBF_C), sX, xb + iu + 1, RBF_XS, P.dh1, P.dw1, dW1);
-        commit(t1full0 + 8u * acc);
-        ++c1;
-        if (lane == 0) rbf_mark(2, (int)c1);
-        // x run row k (k = 0 .. nu + 1) is last read by S1(min(k, nu - 1)); rows that are not output
-        // rows of the run (k = 0, 1, nu, nu + 1) get both of their arrivals from here
-        auto rel_x = [&](int k) {
-          const uint32_t bar = xempty0 + 8u * ((xb + k) % RBF_XS);
-          commit(bar);
-          if (k < 2 || k >= no + 2) commit(bar);
-        };
-        if (iu < nu - 1) rel_x(iu);
-        else { rel_x(nu - 1); rel_x(nu); rel_x(nu + 1); }
+        if (lane == 0) RBF_EV(4, k);
+        mma_window(0u, sX + (c % XS) * SLOT + 1024u, dW1, ub + (uint32_t)lo, ub + (uint32_t)hi, lo - (k - 2));
+        mma_commit_elect(xempty0 + 8u * (c % XS));  // input row k has no other reader
+        if (k >= 2) mma_commit_elect(t1done0 + 8u * ((ub + (uint32_t)(k - 2)) % R));
       };
-      // S2 of output row io (image row h0+io) reads intermediate run rows io .. io+2
-      auto s2 = [&](int io) {
-        mbar_wait(ufull0 + 8u * ((ub + io + 2) % RBF_US), ((ub + io + 2) / RBF_US) & 1u);
-        if (io == 0) {
-          mbar_wait(ufull0 + 8u * (ub % RBF_US), (ub / RBF_US) & 1u);
-          mbar_wait(ufull0 + 8u * ((ub + 1) % RBF_US), ((ub + 1) / RBF_US) & 1u);
+      // S2(j): intermediate row j -> output rows io = j-2 .. j (image row h0+io)
+      auto s2 = [&](int j) {
+        if (lane == 0) RBF_EV(5, j);
+        const uint32_t c = ub + (uint32_t)j;
+        mbar_wait(ufull0 + 8u * (c % US), (c / US) & 1u);
+        const int lo = max(0, j - 2), hi = min(j, no - 1);
+        if (j < no) {
+          const uint32_t g = ob + (uint32_t)j;
+          mbar_wait(t2free0 + 8u * (g % R), ((g / R) & 1u) ^ 1u);
+          if (j >= 2 && ((g - 2u) % R) >= 2u) mbar_wait(t2free0 + 8u * ((g + 1u) % R), (((g + 1u) / R) & 1u) ^ 1u);
         }
-        const int acc = (int)(c2 & 1u);
-        mbar_wait(t2empty0 + 8u * acc, ((c2 >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        if (!(P.dbg & 2)) mma_row(tmem_base + (uint32_t)((2 + acc) * MT * RBF_C), sU, ub + io + 1, RBF_US, P.dh2, P.dw2, dW2);
-        commit(t2full0 + 8u * acc);
-        ++c2;
-        if (lane == 0) rbf_mark(3, (int)c2);
-        // intermediate run row k is last read by S2(min(k, no - 1))
-        if (io < no - 1) commit(uempty0 + 8u * ((ub + io) % RBF_US));
-        else
-          for (int k = no - 1; k < nu; ++k) commit(uempty0 + 8u * ((ub + k) % RBF_US));
+        if (lane == 0) RBF_EV(7, j);
+        if (lo <= hi)
+          mma_window((uint32_t)(MT * R * RBF_C), sU + (c % US) * SLOT + 1024u, dW2, ob + (uint32_t)lo, ob + (uint32_t)hi,
+                     lo - (j - 2));
+        mma_commit_elect(uempty0 + 8u * (c % US));
+        if (j >= 2 && j - 2 < no) mma_commit_elect(t2done0 + 8u * ((ob + (uint32_t)(j - 2)) % R));
       };
-      s1(0);
-      s1(1);
-      for (int io = 0; io < no; ++io) {
-        s1(io + 2);
-        s2(io);
+      for (int k = 0; k <= nu + 1; ++k) {
+        s1(k);
+        if (k >= 3) s2(k - 3);
       }
+      s2(nu - 1);
       xc += (uint32_t)(nu + 2);
       uc += (uint32_t)nu;
+      oc += (uint32_t)no;
     }
-  } else if (warp >= 2 && warp < 10 && !(P.dbg & 4096)) {
-    // ---------------- epilogue (same stage order as the MMA warp)
-    const int quad = warp & 3, half = (warp - 2) >> 2;
+  } else {
+    // ---------------- epilogue (completion order: E1(0..3), then E2(io), E1(io+4))
+    const int quad = warp & 3, slice = (warp - 2) >> 2;
+    const int c0 = slice * RBF_CPW;  // this warp's 8 channels = 16-byte chunk `slice` of a pixel
     const bool leader = warp == 2 && lane == 0;
-    const int c0 = half * 16;  // this warp's 16 channels
-    uint32_t xc = 0, uc = 0, ac = 0, c1 = 0, c2 = 0;
-    uint32_t pend_bar = 0;     // leader: slot barrier to release once the previous store has been read
+    uint32_t uc = 0, oc = 0;
     int q = q0;
     RbfRun run;
-    auto store_done = [&](uint32_t bar) {  // leader, after committing a store group
-      if (pend_bar) { bulk_wait_read1(); mbar_arrive(pend_bar); }
-      pend_bar = bar;
+    const uint32_t tq = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+    // read this warp's 8 columns of ring block `blk` of a stage for every M tile, zero them, return
+    // the block to the MMA warp
+    auto drain = [&](uint32_t stage_col, uint32_t blk, uint32_t (&v)[MT][8]) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C, v[mt]);
+      tmem_wait();
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C);
+    };
+    auto give_back = [&](uint32_t free_bar) {  // after drain: the zeros have landed, block is free
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(free_bar);
+    };
+    // VJP: the saved-activation chunks of the next stage-1 row, prefetched one epilogue step ahead
+    uint4 av[MT];
+    int av_row = -1;  // image row (in image av_n) av holds, -1: none
+    int av_n = -1;
+    auto load_a = [&](int n, int h) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+        av[mt] = __ldg(reinterpret_cast<const uint4*>(P.act + (((size_t)n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0));
+      av_n = n;
+      av_row = h;
     };
     while (rbf_next_run(P, q, q1, run)) {
       const int nu = run.h1 - run.h0 + 2, no = run.h1 - run.h0;
-      const uint32_t xb = xc, ub = uc;
-      // E1: intermediate row iu -> u ring
+      const uint32_t ub = uc, ob = oc;
+      // E1: intermediate row iu (image row h0-1+iu) -> u ring (+ forward: a to HBM)
       auto e1 = [&](int iu) {
         const int h = run.h0 - 1 + iu;
         const bool inside = h >= 0 && h < P.H;
-        const uint32_t us = (ub + iu) % RBF_US;
-        mbar_wait(uempty0 + 8u * us, (((ub + iu) / RBF_US) & 1u) ^ 1u);
-        uint32_t apl = 0;
-        if (VJP) {
-          apl = rbf_payload(sA, (int)(ac % RBF_AS), SLOT);
-          mbar_wait(afull0 + 8u * (ac % RBF_AS), (ac / RBF_AS) & 1u);
-        }
-        const int acc = (int)(c1 & 1u);
-        mbar_wait(t1full0 + 8u * acc, (c1 >> 1) & 1u);
+        const uint32_t g = ub + (uint32_t)iu;
+        if (VJP && inside && (av_row != h || av_n != run.n)) load_a(run.n, h);
+        if (leader) RBF_EV(8, iu);
+        mbar_wait_sleep(uempty0 + 8u * (g % US), ((g / US) & 1u) ^ 1u);
+        mbar_wait_sleep(t1done0 + 8u * (g % R), (g / R) & 1u);
         tc_fence_after();
-        const uint32_t upl = rbf_payload(sU, (int)us, SLOT);
-        for (int mt = 0; mt < ((P.dbg & 8) ? 0 : MT); ++mt) {
-          float v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * MT * RBF_C + mt * RBF_C + c0), v);
+        if (leader) RBF_EV(9, iu);
+        uint32_t d[MT][8];
+        drain(0u, g % R, d);
+        const uint32_t upl = sU + (g % US) * SLOT + 1024u;
+        uint4 w[MT];
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt) {
           const int p = 128 * mt + quad * 32 + lane;
-#pragma unroll
-          for (int qq = 0; qq < 2; ++qq) {
-            const int j = (c0 >> 3) + qq;
-            float o[8];
-            if (!inside) {
-#pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = 0.f;
-            } else if (VJP) {  // q = (B^T g) . sp'(a)
-              const uint4 u = ld_shared_v4(rbf_chunk(apl, p, j));
-              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+          w[mt] = make_uint4(0u, 0u, 0u, 0u);
+          if (inside) {
+            float v[8];
+            if (VJP) {  // q = (B^T g) . sp'(a)
+              const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[mt]);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(h2[e]);
-                o[2 * e] = v[qq * 8 + 2 * e] * dsoftplus_from_act_fast(f.x);
-                o[2 * e + 1] = v[qq * 8 + 2 * e + 1] * dsoftplus_from_act_fast(f.y);
+                const float2 f = __bfloat1622float2(a2[e]);
+                v[2 * e] = __uint_as_float(d[mt][2 * e]) * dsoftplus_from_act_fast(f.x);
+                v[2 * e + 1] = __uint_as_float(d[mt][2 * e + 1]) * dsoftplus_from_act_fast(f.y);
               }
             } else {  // a = sp(A t)
 #pragma unroll
-              for (int e = 0; e < 8; ++e) o[e] = (e & 1) ? softplus_poly_log(v[qq * 8 + e]) : softplus_fast(v[qq * 8 + e]);
+              for (int e = 0; e < 8; ++e) {
+                const float t = __uint_as_float(d[mt][e]);
+                v[e] = (e & 1) ? softplus_poly_log(t) : softplus_fast(t);
+              }
             }
-            uint4 w;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[mt]);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
-            st_shared_v4(rbf_chunk(upl, p, j), w);
+            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
           }
+          st_shared_v4(rbf_chunk(upl, p, slice), w[mt]);
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(t1empty0 + 8u * acc);
-          if (VJP) mbar_arrive(aempty0 + 8u * (ac % RBF_AS));  // this warp has read its part of the a row
+        fence_async_smem();  // u row -> async proxy (stage-2 MMAs)
+        rbf_epi_bar();
+        if (leader) { mbar_arrive(ufull0 + 8u * (g % US)); RBF_EV(10, iu); }
+        give_back(t1free0 + 8u * (g % R));
+        if (!VJP && inside) {  // the saved activation, off the stage-2 critical path
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt)
+            *reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0) = w[mt];
         }
-        ++c1;
-        if (VJP) ++ac;
-        if (leader) rbf_mark(4, (int)c1);
-        fence_async_smem();
-        epi_bar();
-        if (leader) {
-          if (!VJP && inside && !(P.dbg & 4)) {  // the saved activation a (the VJP's sp' input)
-            tma_store_4d(&tmU, upl, 0, 0, h, run.n);
-            bulk_commit();
-            mbar_arrive(ufull0 + 8u * us);
-            store_done(uempty0 + 8u * us);
-          } else {
-            mbar_arrive(ufull0 + 8u * us);
-            if (!VJP) mbar_arrive(uempty0 + 8u * us);  // nothing stored: the slot is free for the ring
-          }
-        }
+        if (VJP && iu + 1 < nu && h + 1 < P.H) load_a(run.n, h + 1);  // latency hidden by the next E2
       };
-      // E2: output row io = x run row io + 2 (residual), result written over it and stored
+      // E2: output row io (image row h0+io) = residual + conv 2
       auto e2 = [&](int io) {
-        const uint32_t xs = (xb + io + 2) % RBF_XS;
-        mbar_wait(xfull0 + 8u * xs, ((xb + io + 2) / RBF_XS) & 1u);
-        const int acc = (int)(c2 & 1u);
-        mbar_wait(t2full0 + 8u * acc, (c2 >> 1) & 1u);
+        const uint32_t g = ob + (uint32_t)io;
+        const size_t rowoff = ((size_t)run.n * P.H + run.h0 + io) * W;
+        uint4 rv[MT];  // the residual (block input row h0+io), loaded from L2 before the wait
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          rv[mt] = __ldg(reinterpret_cast<const uint4*>(P.x + (rowoff + 128 * mt + quad * 32 + lane) * RBF_C + c0));
+        if (leader) RBF_EV(11, io);
+        mbar_wait_sleep(t2done0 + 8u * (g % R), (g / R) & 1u);
         tc_fence_after();
-        const uint32_t xpl = rbf_payload(sX, (int)xs, SLOT);
-        for (int mt = 0; mt < ((P.dbg & 8) ? 0 : MT); ++mt) {
-          float v[16];
-          tmem_ld16(tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)((2 + acc) * MT * RBF_C + mt * RBF_C + c0), v);
-          const int p = 128 * mt + quad * 32 + lane;
+        if (leader) RBF_EV(12, io);
+        uint32_t d[MT][8];
+        drain((uint32_t)(MT * R * RBF_C), g % R, d);
 #pragma unroll
-          for (int qq = 0; qq < 2; ++qq) {
-            const int j = (c0 >> 3) + qq;
-            const uint32_t addr = rbf_chunk(xpl, p, j);
-            const uint4 u = ld_shared_v4(addr);
-            const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-            uint4 w;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
+        for (int mt = 0; mt < MT; ++mt) {
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv[mt]);
+          uint4 w;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const float2 f = __bfloat1622float2(r2[e]);
-              h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e] + f.x, v[qq * 8 + 2 * e + 1] + f.y);
-            }
-            st_shared_v4(addr, w);
+          for (int e = 0; e < 4; ++e) {
+            const float2 f = __bfloat1622float2(r2[e]);
+            h2[e] = __floats2bfloat162_rn(__uint_as_float(d[mt][2 * e]) + f.x, __uint_as_float(d[mt][2 * e + 1]) + f.y);
           }
+          *reinterpret_cast<uint4*>(P.out + (rowoff + 128 * mt + quad * 32 + lane) * RBF_C + c0) = w;
         }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(t2empty0 + 8u * acc);
-        ++c2;
-        if (leader) rbf_mark(5, (int)c2);
-        fence_async_smem();
-        epi_bar();
-        if (leader) {
-          if (P.dbg & 4) mbar_arrive(xempty0 + 8u * xs);
-          else {
-          tma_store_4d(&tmOut, xpl, 0, 0, run.h0 + io, run.n);
-          bulk_commit();
-          store_done(xempty0 + 8u * xs);
-          }
-        }
+        give_back(t2free0 + 8u * (g % R));
+        if (leader) RBF_EV(13, io);
       };
-      e1(0);
-      e1(1);
+      for (int iu = 0; iu < min(4, nu); ++iu) e1(iu);
       for (int io = 0; io < no; ++io) {
-        e1(io + 2);
         e2(io);
+        if (io + 4 < nu) e1(io + 4);
       }
-      xc += (uint32_t)(nu + 2);
       uc += (uint32_t)nu;
-      // the last output row's slot would otherwise wait for the next run's first store, which
-      // needs that slot refilled: release it now
-      if (leader && pend_bar) {
-        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        mbar_arrive(pend_bar);
-        pend_bar = 0;
-      }
-    }
-    if (leader) {
-      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-      if (pend_bar) mbar_arrive(pend_bar);
-      bulk_wait0();
+      oc += (uint32_t)no;
     }
   }
-  if (P.dbg & 16384) return;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1 && !(P.dbg & 256))
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(P.tmem_cols)
-                 : "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
 }
 
 // ------------------------------------------------------------------ host side
@@ -468,7 +516,7 @@ static EncodeTiledFn4 rbf_encode() {
 }
 
 struct RbfPlan {
-  CUtensorMap tmX, tmOut, tmU;
+  CUtensorMap tmX;
   RbfParams P;
   const int* list_ptr;
   bool vjp;
@@ -477,11 +525,6 @@ struct RbfPlan {
 };
 
 bool rbf_supported(int W, int C) { return C == RBF_C && (W == 128 || W == 256); }
-
-size_t rbf_smem_bytes(int W, bool vjp) {
-  const size_t slot = ((size_t)1024 + (size_t)(W + 1) * RBF_PIX + 1023) & ~(size_t)1023;
-  return 1024 + 18 * 2048 + (RBF_XS + RBF_US + (vjp ? RBF_AS : 0)) * slot + 256;
-}
 
 static CUresult rbf_map(EncodeTiledFn4 enc, CUtensorMap* m, const void* p, int N, int H, int W) {
   cuuint64_t dims[4] = {(cuuint64_t)RBF_C, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
@@ -503,16 +546,15 @@ RbfPlan* rbf_make_plan(bool vjp, int N, int H, int W, const int dh1[9], const in
   memset(p, 0, sizeof(RbfPlan));
   p->vjp = vjp;
   RbfParams& P = p->P;
-  P.N = N; P.H = H; P.W = W; P.MT = W / 128;
+  P.N = N; P.H = H; P.W = W;
   for (int t = 0; t < 9; ++t) { P.dh1[t] = dh1[t]; P.dw1[t] = dw1[t]; P.dh2[t] = dh2[t]; P.dw2[t] = dw2[t]; }
-  P.slot = (uint32_t)(((size_t)1024 + (size_t)(W + 1) * RBF_PIX + 1023) & ~(size_t)1023);
   P.w1 = w1; P.w2 = w2;
-  P.tmem_cols = 4 * P.MT * RBF_C <= 128 ? 128 : 256;
+  P.x = static_cast<const __nv_bfloat16*>(x);
+  P.out = static_cast<__nv_bfloat16*>(out);
+  P.act = static_cast<__nv_bfloat16*>(act);
   CUresult r = rbf_map(enc, &p->tmX, x, N, H, W);
-  if (r == CUDA_SUCCESS) r = rbf_map(enc, &p->tmOut, out, N, H, W);
-  if (r == CUDA_SUCCESS) r = rbf_map(enc, &p->tmU, act, N, H, W);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "fused residual block: tensor map encode failed (%d)", (int)r); delete p; return nullptr; }
-  p->smem = rbf_smem_bytes(W, vjp);
+  p->smem = W == 128 ? RbfCfg<1>::smem() : RbfCfg<2>::smem();
   const long long rows = (long long)N * H;
   p->grid = (int)(rows < num_sms ? rows : num_sms);
   return p;
@@ -525,26 +567,6 @@ void rbf_set_active(RbfPlan* p, const int* act_list, const int* n_act) {
 }
 void rbf_enable_skip(RbfPlan* p, bool on) { p->P.act_list = on ? p->list_ptr : nullptr; }
 void rbf_free_plan(RbfPlan* p) { delete p; }
-void rbf_set_debug(RbfPlan* p, int dbg) {
-  p->P.dbg = dbg;
-  static int* prog = nullptr;
-  if (dbg && !prog) {
-    int* hp = nullptr;
-    if (cudaHostAlloc(&hp, 64 * sizeof(int), cudaHostAllocMapped) == cudaSuccess) {
-      memset(hp, 0, 64 * sizeof(int));
-      int* dp = nullptr;
-      cudaHostGetDevicePointer(&dp, hp, 0);
-      cudaMemcpyToSymbol(g_rbf_prog, &dp, sizeof(dp));
-      prog = hp;
-    }
-  }
-  if (prog) {
-    fprintf(stderr, "rbf progress (previous launch): ");
-    for (int i = 0; i < 6; ++i) fprintf(stderr, "%d ", prog[i]);
-    fprintf(stderr, "\n");
-  }
-}
-
 
 void rbf_launch(const RbfPlan* p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
@@ -557,14 +579,21 @@ void rbf_launch(const RbfPlan* p, cudaStream_t s) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  if (p->P.dbg & 64) return;
-  if (p->vjp) cudaLaunchKernelEx(&cfg, rbf_kernel<true>, p->tmX, p->tmOut, p->tmU, p->P);
-  else cudaLaunchKernelEx(&cfg, rbf_kernel<false>, p->tmX, p->tmOut, p->tmU, p->P);
+  const bool narrow = p->P.W == 128;
+  if (p->vjp) {
+    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, true>, p->tmX, p->P);
+    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, true>, p->tmX, p->P);
+  } else {
+    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, false>, p->tmX, p->P);
+    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, false>, p->tmX, p->P);
+  }
 }
 
 void init_attrs_rbf() {
-  set_max_dyn_smem(rbf_kernel<false>);
-  set_max_dyn_smem(rbf_kernel<true>);
+  set_max_dyn_smem(rbf_kernel<1, false>);
+  set_max_dyn_smem(rbf_kernel<1, true>);
+  set_max_dyn_smem(rbf_kernel<2, false>);
+  set_max_dyn_smem(rbf_kernel<2, true>);
 }
 
 }  // namespace ideq

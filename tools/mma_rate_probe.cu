@@ -1,0 +1,153 @@
+// Probe: tcgen05.mma kind::f16 throughput (M = 128, K = 16 per instruction): clk per MMA by N,
+// operand swizzle, A start alignment, accumulator / A-tile rotation and operand data (zero or not).
+// One CTA per SM, one warp issues (elect.sync) NIT x 8 MMAs; clock64 around issue + commit wait.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_rate_probe tools/mma_rate_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t sbo, uint32_t layout) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)(1u) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)(layout & 7u) << 61;
+  return d;
+}
+__device__ __forceinline__ uint32_t make_idesc_bf16(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_e(uint32_t d, uint64_t adesc, uint64_t bdesc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, 1;\n\t}\n" ::"r"(d),
+      "l"(adesc), "l"(bdesc), "r"(idesc)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+constexpr int NIT = 512;
+// layout 4 = SW64 (64-byte rows), 2 = SW128 (128-byte rows); rotD / rotA: cycle 4 accumulators /
+// 4 A tiles per group of 8 MMAs; shift: A start + 1 row; data: fill value of the operands
+__global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, long long* out) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
+  unsigned char* g = sm + (base - smem_u32(sm));
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar2;
+  __shared__ uint32_t tm;
+  const uint32_t rowb = layout == 4 ? 64u : 128u, sbo = 8u * rowb;
+  for (uint32_t o = threadIdx.x * 4; o < 96u * 1024u; o += blockDim.x * 4) {
+    uint32_t v = data;
+    if (data == 1u) {  // pseudo-random bf16 pairs in [-1, 1)
+      uint32_t h = (o + 0x9e3779b9u * (blockIdx.x + 1)) * 2654435761u;
+      h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+      v = (0x3f80u | ((h & 0x7fu) << 0) | ((h >> 7 & 1u) << 15)) | ((0x3f00u | (h >> 8 & 0x7fu) | ((h >> 15 & 1u) << 15)) << 16);
+    }
+    *(uint32_t*)(g + o) = v;
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tm)) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tm;
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = make_idesc_bf16(n);
+    const uint64_t bd = make_sdesc(base + 64u * 1024u, sbo, (uint32_t)layout);
+    uint64_t ad[4];
+    for (int t = 0; t < 4; ++t) ad[t] = make_sdesc(base + (uint32_t)t * 128u * rowb + (uint32_t)shift * rowb, sbo, (uint32_t)layout);
+    const uint32_t dstep = n <= 128 ? 128u : 256u;
+    const long long t0 = clock64();
+    for (int it = 0; it < NIT; ++it) {
+      const uint32_t d = tmem + (rotD ? (uint32_t)(it & (n <= 128 ? 3 : 1)) * dstep : 0u);
+      const uint64_t a = rotA ? ad[it & 3] : ad[0];
+      if (mode == 0) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_e(d, a + 2ull * (k & 1), bd + 2ull * (k & 1), idesc);
+      } else if (mode == 1) {  // N cycles 96, 64, 32
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_e(d, a + 2ull * (k & 1), bd + 2ull * (k & 1), make_idesc_bf16(96 - 32 * (k % 3)));
+      } else if (mode == 2) {  // A start cycles -1, 0, +1 rows (4 = 64 B in 16-byte units)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_e(d, a + 4ull * (k % 3) + 2ull * (k & 1), bd + 2ull * (k & 1), idesc);
+      } else if (mode == 4 || mode == 5) {  // kernel-like: 6 N=96 MMAs then a commit (mode 5: + a fence)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) mma_e(d, a + 4ull * (k >> 1) + 2ull * (k & 1), bd + 2ull * (k & 1), idesc);
+        if (threadIdx.x == 0) commit(smem_u32(&bar2));
+        if (mode == 5) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      } else if (mode >= 10) {  // D column offset (mode - 10) * 32 within a 128-column group
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mma_e(d + (uint32_t)(mode - 10) * 32u, a + 2ull * (k & 1), bd + 2ull * (k & 1), idesc);
+      } else {  // the fused kernel's pattern: per dw (A shifted), per K step, N=64 at block b + N=32 at block 0
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+          const uint64_t ak = a + 4ull * (k >> 1) + 2ull * (k & 1);
+          mma_e(d + 64, ak, bd + 2ull * (k & 1), make_idesc_bf16(64));
+          mma_e(d, ak, bd + 256 + 2ull * (k & 1), make_idesc_bf16(32));
+        }
+      }
+    }
+    if (threadIdx.x == 0) {
+      commit(smem_u32(&bar));
+      mbar_wait(smem_u32(&bar), 0);
+      if (blockIdx.x == 0) out[0] = clock64() - t0;
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 8);
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; } cases[] = {
+      {4, 96, 0, 1, 1, 1u, 0}, {4, 96, 0, 1, 1, 1u, 4}, {4, 96, 0, 1, 1, 1u, 5}, {4, 96, 0, 1, 1, 1u, 0},
+      {4, 96, 0, 1, 1, 1u, 10}, {4, 96, 0, 1, 1, 1u, 11}, {4, 96, 0, 0, 1, 1u, 12}, {4, 96, 0, 0, 1, 1u, 13},
+      {4, 64, 0, 1, 1, 1u, 10}, {4, 64, 0, 1, 1, 1u, 11}, {4, 64, 0, 1, 1, 1u, 12}, {4, 64, 0, 0, 1, 1u, 13},
+      {4, 32, 0, 1, 1, 1u, 10}, {4, 32, 0, 1, 1, 1u, 11}, {4, 32, 0, 1, 1, 1u, 13},
+      {4, 96, 0, 1, 1, 1u, 1}, {4, 96, 0, 1, 1, 1u, 2}, {4, 96, 0, 1, 1, 1u, 3},
+      {4, 32, 0, 1, 1, 1u}, {4, 96, 0, 1, 1, 1u}, {4, 64, 0, 1, 1, 1u}, {4, 128, 0, 1, 1, 1u}, {4, 256, 0, 1, 1, 1u},
+      {4, 32, 0, 0, 0, 0u},          {4, 32, 0, 0, 0, 0x3c003c00u}, {4, 96, 0, 0, 0, 0u},
+      {4, 96, 0, 0, 0, 0x3c003c00u}, {4, 96, 0, 1, 0, 0x3c003c00u}, {4, 96, 0, 0, 1, 0x3c003c00u},
+      {4, 96, 1, 0, 0, 0x3c003c00u}, {4, 32, 0, 1, 1, 0x3c003c00u}, {4, 64, 0, 1, 1, 0x3c003c00u},
+      {4, 128, 0, 1, 1, 0x3c003c00u}, {4, 256, 0, 1, 1, 0x3c003c00u}, {2, 32, 0, 1, 1, 0x3c003c00u},
+      {2, 64, 0, 1, 1, 0x3c003c00u}, {2, 96, 0, 1, 1, 0x3c003c00u}, {2, 128, 0, 1, 1, 0x3c003c00u},
+      {2, 256, 0, 1, 1, 0x3c003c00u},
+  };
+  for (auto& c : cases) {
+    for (int rep = 0; rep < 2; ++rep) {
+      probe<<<148, 128, 100 * 1024>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
+    }
+    long long clk;
+    cudaMemcpy(&clk, d, 8, cudaMemcpyDeviceToHost);
+    const double per = (double)clk / (NIT * (c.mode == 3 ? 12 : (c.mode == 4 || c.mode == 5) ? 6 : 8));
+    printf("mode %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
+           c.mode, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
+           (128.0 * 32 + c.n * 32.0) / per);
+  }
+  return 0;
+}
