@@ -60,7 +60,9 @@ typedef enum {
 } ideq_status;
 
 typedef enum {
-  IDEQ_PREC_FP32 = 0, /* parity mode: fp32 storage, fp32 FFMA convolutions  */
+  IDEQ_PREC_FP32 = 0, /* parity mode: fp32 storage; U-Net convolutions on tcgen05 as 3xTF32
+                         (kind::tf32, hi/lo operand halves, 3 MMAs per product; widths
+                         multiple of 32), the tiny net and the JFB gradient on fp32 FFMA  */
   IDEQ_PREC_BF16 = 1  /* bf16 weights/activations on tcgen05, fp32 accumulate;
                          iterate state x, z, grad g, fidelity stay fp32 (Q19) */
 } ideq_precision;
