@@ -12,7 +12,8 @@
 // the neighbours' halo rows (st.shared::cluster, DSMEM) as it computes them, so one cluster barrier
 // per stage both publishes a tensor and completes every halo -- no copy phase. Cheap layers are
 // recomputed on the halo rows instead of exchanged (a1 and U on rows -1 and R), which removes two
-// of the barriers: 6 per iteration. The residual's three partial sums are pushed into every CTA
+// of the barriers, and the residual's barrier also completes the next iteration's z halos: 5 per
+// iteration. The residual's three partial sums are pushed into every CTA
 // and combined in fp64 in a fixed order, so all 8 CTAs take the identical stop decision.
 //
 // Layouts: the network tensors (a1, a2, q2, q1 with 16 channels, U) are planes of (R + 4) rows x
@@ -231,9 +232,8 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
   const int rk = pk / W, ck = pk % W;
   const bool act_k = pk < RW;
   long long t_mark = clock64();
+  ts_cluster_sync();  // z^0 (own rows + pushed halos) complete on every CTA
   for (int k = 0; k < A.max_iter; ++k) {
-    // [S0] z (own rows + pushed halos) complete on every CTA
-    ts_cluster_sync();
     TS_MARK(0)
     // [1] a1 = sp(c1(z)) on rows -1 .. R (the halo rows recomputed locally; zero outside the image);
     //     rb = A z - y (true periodic convolution, reading Q8), pushed to the neighbours' halos
@@ -362,6 +362,10 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
         const float d = x1 - xk;
         if (isfinite(x1)) d2 = d * d; else bad = 1.f;
         n2 = xk * xk;
+        // candidate z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4), pushed now so that the
+        // residual's barrier also completes the next iteration's z halos (every read of z^k by
+        // a neighbour happened before [S1]; a diverged or converged image exits before using it)
+        ts_put_blur(sm, L, L.z, rk, ck, x1 + A.beta * (x1 - xk), rank, base);
       }
     }
     // block reduction (fixed order), then this CTA's partials into slot `rank` of every CTA
@@ -386,7 +390,7 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
       }
     }
     TS_MARK(9)
-    ts_cluster_sync();  // [S5] partials
+    ts_cluster_sync();  // [S5] partials, z^{k+1}
     TS_MARK(10)
     double D2 = 0.0, N2 = 0.0, BAD = 0.0;
     for (int q = 0; q < TS_P; ++q) {  // fixed order: identical on every CTA
@@ -401,12 +405,8 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     const double rr = N2 > 0.0 ? sqrt(D2) / sqrt(N2) : (double)INFINITY;
     res = (float)rr;
     iters = k + 1;
-    // accept: z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4), pushed; x^k <- x^{k+1}
-    for (int t = threadIdx.x; t < RW; t += TS_T) {
-      const float x1 = sm[L.xn + t], xk = sm[L.xk + t];
-      ts_put_blur(sm, L, L.z, t / W, t % W, x1 + A.beta * (x1 - xk), rank, base);
-      sm[L.xk + t] = x1;
-    }
+    // accept: x^k <- x^{k+1} (z^{k+1} is already in place)
+    for (int t = threadIdx.x; t < RW; t += TS_T) sm[L.xk + t] = sm[L.xn + t];
     if (rank == 0 && threadIdx.x == 0 && A.trace && k < A.trace_cap)
       atomicMax(reinterpret_cast<int*>(A.trace) + k, __float_as_int(res));
     TS_MARK(11)

@@ -32,7 +32,7 @@ int main() {
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     long long p[16]; cudaMemcpyFromSymbol(p, ideq::ts_prof, sizeof(p));
-    const char* names[16] = {"S0 sync", "[1] c1+Az", "S1 sync", "[2] c2+ATr", "S2 sync", "[3,4] c3,c3T", "S3 sync", "[5] c2T", "S4 sync", "[6] c1T+upd", "S5 sync", "accept", "", "", "", ""};
+    const char* names[16] = {"(loop top)", "[1] c1+Az", "S1 sync", "[2] c2+ATr", "S2 sync", "[3,4] c3,c3T", "S3 sync", "[5] c2T", "S4 sync", "[6] c1T+upd", "S5 sync (+z)", "accept", "", "", "", ""};
     printf("total %.1f us per iteration\n", 1000.0 * ms / K);
     for (int i = 0; i < 12; ++i) printf("  %-16s %7.0f clk/iter\n", names[i], (double)p[i] / K);
   }
