@@ -571,6 +571,42 @@ __device__ __forceinline__ void team_fft(float2 (&v)[16], int t, float2* buf, co
   __syncwarp();  // the team buffer may be reused by the next transform
 }
 
+// Same transform with the team's transpose buffer laid over its OWN column of a column-pass tile
+// (col[r * stride], r < 16 T: the column is in registers while the transform runs), skewed so
+// both the column-wise writes and the row-wise reads are conflict-free: element (k, t) of the
+// 16 x T buffer -> row T k + ((t + k) mod T). Frees the column passes' separate team buffers
+// (a third of their shared memory), which doubles their occupancy.
+template <int T>
+__device__ __forceinline__ void team_fft_col(float2 (&v)[16], int t, float2* col, int stride, const float2* tw) {
+  constexpr int N = 16 * T;
+  auto at = [&](int k, int u) -> float2& { return col[(T * k + ((u + k) & (T - 1))) * stride]; };
+  dft16(v);
+#pragma unroll
+  for (int k = 1; k < 16; ++k) v[k] = cmul(v[k], tw_get(tw, t * k, N));
+#pragma unroll
+  for (int k = 0; k < 16; ++k) at(k, t) = v[k];
+  __syncwarp();
+  if (T == 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = at(t, j);
+    dft16(v);
+  } else {
+    const int kp = t >> 1, h = t & 1;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = at(kp, 2 * m + h);
+    dft16(v);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      float2 p;
+      p.x = __shfl_xor_sync(0xffffffffu, v[k].x, 1);
+      p.y = __shfl_xor_sync(0xffffffffu, v[k].y, 1);
+      const float2 w = tw_get(tw, k * (N / 32), N);  // W_32^k
+      v[k] = h ? csub(p, cmul(w, v[k])) : cadd(v[k], cmul(w, p));
+    }
+  }
+  __syncwarp();  // the column is written by the caller next
+}
+
 // Row passes: RNT teams (rows) per block. Small blocks keep the grid many waves deep for the
 // configs' small batches (C4: 16 images x 4 masks x 256 rows = 16384 row transforms).
 constexpr int RNT = 4;
@@ -615,12 +651,11 @@ __global__ void __launch_bounds__(RNT * T) rblur_rows_fwd_kernel(FftArgs f, cons
 template <int T>
 __global__ void __launch_bounds__(256) rblur_cols_kernel(FftArgs f, int op) {
   pdl_enter();
-  constexpr int H = 16 * T, P = T + 1, CPB = 256 / T, CP = CPB + 1;  // CPB columns per block
+  constexpr int H = 16 * T, CPB = 256 / T, CP = CPB + 1;  // CPB columns per block
   extern __shared__ float2 smc[];
   float2* tw = smc;                       // H/2
-  float2* tile = smc + H / 2;             // [H][CP]
-  float2* bufs = tile + H * CP;           // CPB teams x 16 P
-  float2* otile = bufs + CPB * 16 * P;    // [H][CPB] the op's diagonal (dgl as .x, or K^)
+  float2* tile = smc + H / 2;             // [H][CP]; column j doubles as team j's FFT buffer
+  float2* otile = tile + H * CP;          // [H][CPB] the op's diagonal (dgl as .x, or K^)
   load_tw_all(tw, f.tw_h, H);
   const int Wh = f.W / 2 + 1;
   const int kx0 = blockIdx.x * CPB, c = blockIdx.y, n = blockIdx.z;
@@ -638,12 +673,12 @@ __global__ void __launch_bounds__(256) rblur_cols_kernel(FftArgs f, int op) {
   __syncthreads();
   const int team = threadIdx.x / T, t = threadIdx.x % T;
   const int kx = kx0 + team;
-  float2* buf = bufs + team * 16 * P;
+  float2* col = tile + team;
   float2 v[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) v[k] = tile[(t + T * k) * CP + team];
   const bool fwd = op != 3, inv = op != 2;
-  if (fwd) team_fft<T>(v, t, buf, tw);
+  if (fwd) team_fft_col<T>(v, t, col, CP, tw);
   if (fwd && inv) {  // pointwise op at ky = team_out, then back to the x[t + T k] distribution
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
@@ -666,7 +701,7 @@ __global__ void __launch_bounds__(256) rblur_cols_kernel(FftArgs f, int op) {
   if (inv) {
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = cconj(v[k]);
-    team_fft<T>(v, t, buf, tw);
+    team_fft_col<T>(v, t, col, CP, tw);
 #pragma unroll
     for (int k = 0; k < 16; ++k) v[k] = cconj(v[k]);
   }
@@ -758,12 +793,11 @@ __global__ void __launch_bounds__(RNT * T) rphase_rows_fwd_kernel(FftArgs f) {
 template <int T>
 __global__ void __launch_bounds__(256) rphase_cols_kernel(FftArgs f) {
   pdl_enter();
-  constexpr int H = 16 * T, P = T + 1, CPB = 256 / T, CP = CPB + 1;
+  constexpr int H = 16 * T, CPB = 256 / T, CP = CPB + 1;
   extern __shared__ float2 smc[];
   float2* tw = smc;
-  float2* tile = smc + H / 2;
-  float2* bufs = tile + H * CP;
-  float* ytile = reinterpret_cast<float*>(bufs + CPB * 16 * P);  // [H][CPB]
+  float2* tile = smc + H / 2;  // [H][CP]; column j doubles as team j's FFT buffer
+  float* ytile = reinterpret_cast<float*>(tile + H * CP);  // [H][CPB]
   load_tw_all(tw, f.tw_h, H);
   const int W = f.W;
   const int kx0 = blockIdx.x * CPB, j = blockIdx.y, n = blockIdx.z;
@@ -777,12 +811,11 @@ __global__ void __launch_bounds__(256) rphase_cols_kernel(FftArgs f) {
   }
   __syncthreads();
   const int team = threadIdx.x / T, t = threadIdx.x % T;
-  const int kx = kx0 + team;
-  float2* buf = bufs + team * 16 * P;
+  float2* col = tile + team;
   float2 v[16];
 #pragma unroll
   for (int k = 0; k < 16; ++k) v[k] = tile[(t + T * k) * CP + team];
-  team_fft<T>(v, t, buf, tw);
+  team_fft_col<T>(v, t, col, CP, tw);
   const float sc = rsqrtf((float)H * (float)W);
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
@@ -794,7 +827,7 @@ __global__ void __launch_bounds__(256) rphase_cols_kernel(FftArgs f) {
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 16; ++k) v[k] = cconj(tile[(t + T * k) * CP + team]);
-  team_fft<T>(v, t, buf, tw);
+  team_fft_col<T>(v, t, col, CP, tw);
   __syncthreads();
 #pragma unroll
   for (int k = 0; k < 16; ++k) tile[team_out<T>(t, k) * CP + team] = cconj(v[k]);
@@ -868,9 +901,8 @@ static size_t rpinv_smem() { return rrow_smem<T, NTI>() + sizeof(float) * (size_
 static bool phase_j_ok(int J) { return J >= 1 && J <= 16 && (16 % J) == 0; }
 template <int T>
 static size_t rcol_smem() {
-  constexpr int CPB = 256 / T;  // twiddles, tile, team buffers, op / observation tile
-  return sizeof(float2) * ((size_t)8 * T + (size_t)16 * T * (CPB + 1) + (size_t)CPB * 16 * (T + 1) +
-                           (size_t)16 * T * CPB);
+  constexpr int CPB = 256 / T;  // twiddles, tile (its columns are the team buffers), op / observation tile
+  return sizeof(float2) * ((size_t)8 * T + (size_t)16 * T * (CPB + 1) + (size_t)16 * T * CPB);
 }
 
 // ------------------------------------------------------------------ launchers
