@@ -24,9 +24,9 @@
  * with A, B the block's two 3x3 convolutions (wA, wB: HOST fp32 [32][32][3][3]); x, out, act:
  * DEVICE NHWC bf16 [N][H][W][32].
  *
- * ideq_debug_set_fusion switches the fused residual blocks of a context's network on (1) or off
- * (0, the default: two launches per block are faster on B200, see rbf.cu) for the programs built
- * afterwards (tests compare the two).
+ * ideq_debug_set_fusion switches the fused residual blocks of a context's network on (1, the
+ * default) or off (0: two launches per block) for the programs built afterwards (tests compare
+ * the two).
  */
 #ifndef IDEQ_DEBUG_H
 #define IDEQ_DEBUG_H

@@ -154,7 +154,7 @@ struct ideq_ctx {
   int mb = 0;
   size_t net_bytes = 0;
   // the last solve's step arguments (class timing replays its kernels)
-  bool fuse_rb = false;  // level-0 residual blocks as one launch (rbf.cu); ideq_debug_set_fusion
+  bool fuse_rb = true;  // level-0 residual blocks as one launch (rbf.cu); ideq_debug_set_fusion
   bool have_last = false;
   bool last_fused = false;  // the last solve ran the whole-solve tiny-network kernel
   int last_N = 0;

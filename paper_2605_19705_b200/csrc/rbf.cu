@@ -29,23 +29,24 @@
 // Each run recomputes two intermediate rows (h0 - 1 and h1) and reads two extra input rows.
 //
 // Warp roles (576 threads, one CTA per SM): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2..17 epilogue (TMEM lane quadrant = warp % 4, 8-channel slice = (warp - 2) / 4).
+// issuer, warps 2..9 the stage-1 epilogue and warps 10..17 the stage-2 epilogue (each: TMEM lane
+// quadrant = warp % 4, 16-channel half = ((warp - 2) % 8) / 4).
 // MMA order per run: S1(k) for input rows k = 0 .. nu+1, and S2(j) for intermediate row j right
 // after S1(j+3), so the stage-1 epilogue of row j overlaps two MMA stages before S2(j) reads it.
 //
-// Status (B200, C3 level 0, 32 x 256 x 256 x 32, ncu launch list): forward 145 us, VJP 144 us per
-// block against 131 / 136 us for the two unfused launches, so the solver keeps the two-launch path
-// by default (ideq_debug_set_fusion switches this one on; tests/test_gpu_rbf.py keeps it exact).
+// Status (B200, C3 level 0, 32 x 256 x 256 x 32): in the solver's captured iteration the fused
+// blocks take the C3 step from 3.41 to 3.33 ms in a same-box A/B (tools/rbf_ab.py) and the bench
+// to 10.6k image-iterations/s, so the solver uses them by default (ideq_debug_set_fusion turns
+// them off; tests/test_gpu_rbf.py checks both against the oracle and each other). Serialised and
+// cold under ncu a block takes ~132 us against 131 / 136 us for the two unfused launches: the win
+// is the halved HBM traffic overlapping the neighbours under programmatic dependent launch.
 // What bounds it (tools/rbf_prof.cu stage timeline, tools/mma_rate_probe.cu):
 //   * the MMA stream alone runs at 2.5k clk per row (24 MMAs, ~70 clk each after removing the
 //     branches between tcgen05.mma instructions, which had cost ~150 clk per MMA);
 //   * TMEM holds a 4-row ring per stage and M tile at W = 256 (2 stages x 2 tiles x 4 x 32
 //     columns = 512), so a wrapped window must wait until the epilogue has drained the block it
-//     adds +0 to, and the epilogue (softplus: 768 clk of MUFU per row, tcgen05.ld/st, stores)
-//     and the MMA warp wait on each other every row: 4.2k clk per row end to end.
-// The row-in-N folding itself is sound (a 3x3 convolution per input row as 6 MMAs of N = 96 /
-// 128 at 56-64 clk each, against 18 MMAs of N = 32 at 40 clk); the remaining step is a deeper
-// ring (M = 64 tiles, or 2-CTA pairs splitting a row) so the epilogue can run a row behind.
+//     adds +0 to; the two epilogue stages run in separate warp groups so neither waits for the
+//     other's rows.
 #include <cuda.h>
 #include <stdio.h>
 #include <string.h>
@@ -55,8 +56,8 @@
 
 namespace ideq {
 
-constexpr int RBF_EPI_WARPS = 16;         // 4 per TMEM lane quadrant, 8 channels each
-constexpr int RBF_CPW = 8;                // channels per epilogue warp
+constexpr int RBF_EPI_WARPS = 16;         // two groups of 8: stage-1 and stage-2 epilogues
+constexpr int RBF_GROUP_WARPS = 8;        // per group: 2 per TMEM lane quadrant, 16 channels each
 constexpr int RBF_THREADS = (2 + RBF_EPI_WARPS) * 32;
 constexpr int RBF_C = 32;                 // channels (64-byte pixels, SW64)
 constexpr uint32_t RBF_PIX = RBF_C * 2;
@@ -129,8 +130,8 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 // named barrier 1 over the epilogue warps
-__device__ __forceinline__ void rbf_epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(RBF_EPI_WARPS * 32) : "memory");
+__device__ __forceinline__ void rbf_epi_bar() {  // the stage-1 epilogue group
+  asm volatile("bar.sync 1, %0;" ::"n"(RBF_GROUP_WARPS * 32) : "memory");
 }
 // tcgen05.ld / st of 8 columns (32 lanes x 32 bit)
 __device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&r)[8]) {
@@ -203,8 +204,8 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
     for (int s = 0; s < XS; ++s) { mbar_init(xfull0 + 8u * s, 1); mbar_init(xempty0 + 8u * s, 1); }
     for (int s = 0; s < US; ++s) { mbar_init(ufull0 + 8u * s, 1); mbar_init(uempty0 + 8u * s, 1); }
     for (int s = 0; s < R; ++s) {
-      mbar_init(t1done0 + 8u * s, 1); mbar_init(t1free0 + 8u * s, RBF_EPI_WARPS);
-      mbar_init(t2done0 + 8u * s, 1); mbar_init(t2free0 + 8u * s, RBF_EPI_WARPS);
+      mbar_init(t1done0 + 8u * s, 1); mbar_init(t1free0 + 8u * s, RBF_GROUP_WARPS);
+      mbar_init(t2done0 + 8u * s, 1); mbar_init(t2free0 + 8u * s, RBF_GROUP_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmX);
@@ -364,22 +365,33 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
       oc += (uint32_t)no;
     }
   } else {
-    // ---------------- epilogue (completion order: E1(0..3), then E2(io), E1(io+4))
-    const int quad = warp & 3, slice = (warp - 2) >> 2;
-    const int c0 = slice * RBF_CPW;  // this warp's 8 channels = 16-byte chunk `slice` of a pixel
+    // ---------------- epilogue: two independent warp groups, so a slow stage-2 row never holds up
+    // the stage-1 epilogue the MMA warp is waiting on (and vice versa). Group 0 (warps 2..9):
+    // E1, group 1 (warps 10..17): E2; in a group, warp -> (TMEM lane quadrant, 16-channel half).
+    const int grp = (warp - 2) / RBF_GROUP_WARPS, gw = (warp - 2) % RBF_GROUP_WARPS;
+    const int quad = warp & 3, half = gw >> 2;
+    const int c0 = half * 16;  // this warp's 16 channels = 16-byte chunks 2 half, 2 half + 1
     const bool leader = warp == 2 && lane == 0;
     uint32_t uc = 0, oc = 0;
     int q = q0;
     RbfRun run;
     const uint32_t tq = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
-    // read this warp's 8 columns of ring block `blk` of a stage for every M tile, zero them, return
-    // the block to the MMA warp
-    auto drain = [&](uint32_t stage_col, uint32_t blk, uint32_t (&v)[MT][8]) {
+    // read this warp's 16 columns of ring block `blk` of a stage for every M tile and zero them
+    auto drain = [&](uint32_t stage_col, uint32_t blk, uint32_t (&v)[MT][16]) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C, v[mt]);
-      tmem_wait();
+      for (int mt = 0; mt < MT; ++mt) {
+        uint32_t a[8], b[8];
+        tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C, a);
+        tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C + 8u, b);
+        tmem_wait();
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C);
+        for (int e = 0; e < 8; ++e) { v[mt][e] = a[e]; v[mt][8 + e] = b[e]; }
+      }
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C);
+        tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C + 8u);
+      }
     };
     auto give_back = [&](uint32_t free_bar) {  // after drain: the zeros have landed, block is free
       tmem_st_wait();
@@ -387,106 +399,120 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(free_bar);
     };
-    // VJP: the saved-activation chunks of the next stage-1 row, prefetched one epilogue step ahead
-    uint4 av[MT];
+    // 16 channels of pixel p of a row: two 16-byte chunks
+    auto gload2 = [&](const __nv_bfloat16* base, size_t pix, uint4 (&o)[2]) {
+      const uint4* g = reinterpret_cast<const uint4*>(base + pix * RBF_C + c0);
+      o[0] = __ldg(g);
+      o[1] = __ldg(g + 1);
+    };
+    // VJP: the saved-activation chunks of the next stage-1 row, prefetched one row ahead
+    uint4 av[MT][2];
     int av_row = -1;  // image row (in image av_n) av holds, -1: none
     int av_n = -1;
     auto load_a = [&](int n, int h) {
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt)
-        av[mt] = __ldg(reinterpret_cast<const uint4*>(P.act + (((size_t)n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0));
+      for (int mt = 0; mt < MT; ++mt) gload2(P.act, ((size_t)n * P.H + h) * W + 128 * mt + quad * 32 + lane, av[mt]);
       av_n = n;
       av_row = h;
     };
     while (rbf_next_run(P, q, q1, run)) {
       const int nu = run.h1 - run.h0 + 2, no = run.h1 - run.h0;
       const uint32_t ub = uc, ob = oc;
-      // E1: intermediate row iu (image row h0-1+iu) -> u ring (+ forward: a to HBM)
-      auto e1 = [&](int iu) {
-        const int h = run.h0 - 1 + iu;
-        const bool inside = h >= 0 && h < P.H;
-        const uint32_t g = ub + (uint32_t)iu;
-        if (VJP && inside && (av_row != h || av_n != run.n)) load_a(run.n, h);
-        if (leader) RBF_EV(8, iu);
-        mbar_wait_sleep(uempty0 + 8u * (g % US), ((g / US) & 1u) ^ 1u);
-        mbar_wait_sleep(t1done0 + 8u * (g % R), (g / R) & 1u);
-        tc_fence_after();
-        if (leader) RBF_EV(9, iu);
-        uint32_t d[MT][8];
-        drain(0u, g % R, d);
-        const uint32_t upl = sU + (g % US) * SLOT + 1024u;
-        uint4 w[MT];
+      if (grp == 0) {
+        // E1: intermediate row iu (image row h0-1+iu) -> u ring (+ forward: a to HBM)
+        for (int iu = 0; iu < nu; ++iu) {
+          const int h = run.h0 - 1 + iu;
+          const bool inside = h >= 0 && h < P.H;
+          const uint32_t g = ub + (uint32_t)iu;
+          if (VJP && inside && (av_row != h || av_n != run.n)) load_a(run.n, h);
+          if (leader) RBF_EV(8, iu);
+          mbar_wait_sleep(uempty0 + 8u * (g % US), ((g / US) & 1u) ^ 1u);
+          mbar_wait_sleep(t1done0 + 8u * (g % R), (g / R) & 1u);
+          tc_fence_after();
+          if (leader) RBF_EV(9, iu);
+          uint32_t d[MT][16];
+          drain(0u, g % R, d);
+          const uint32_t upl = sU + (g % US) * SLOT + 1024u;
+          uint4 w[MT][2];
 #pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const int p = 128 * mt + quad * 32 + lane;
-          w[mt] = make_uint4(0u, 0u, 0u, 0u);
-          if (inside) {
-            float v[8];
-            if (VJP) {  // q = (B^T g) . sp'(a)
-              const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[mt]);
+          for (int mt = 0; mt < MT; ++mt) {
+            const int p = 128 * mt + quad * 32 + lane;
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              w[mt][jj] = make_uint4(0u, 0u, 0u, 0u);
+              if (inside) {
+                float v[8];
+                if (VJP) {  // q = (B^T g) . sp'(a)
+                  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[mt][jj]);
+#pragma unroll
+                  for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(a2[e]);
+                    v[2 * e] = __uint_as_float(d[mt][8 * jj + 2 * e]) * dsoftplus_from_act_fast(f.x);
+                    v[2 * e + 1] = __uint_as_float(d[mt][8 * jj + 2 * e + 1]) * dsoftplus_from_act_fast(f.y);
+                  }
+                } else {  // a = sp(A t)
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const float t = __uint_as_float(d[mt][8 * jj + e]);
+                    v[e] = (e & 1) ? softplus_poly_log(t) : softplus_fast(t);
+                  }
+                }
+                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[mt][jj]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+              }
+              st_shared_v4(rbf_chunk(upl, p, 2 * half + jj), w[mt][jj]);
+            }
+          }
+          fence_async_smem();  // u row -> async proxy (stage-2 MMAs)
+          rbf_epi_bar();
+          if (leader) { mbar_arrive(ufull0 + 8u * (g % US)); RBF_EV(10, iu); }
+          give_back(t1free0 + 8u * (g % R));
+          if (!VJP && inside) {  // the saved activation, off the stage-2 critical path
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              uint4* o = reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0);
+              o[0] = w[mt][0];
+              o[1] = w[mt][1];
+            }
+          }
+          if (VJP && iu + 1 < nu && h + 1 < P.H) load_a(run.n, h + 1);  // latency hidden by the next waits
+        }
+      } else {
+        // E2: output row io (image row h0+io) = residual + conv 2
+        for (int io = 0; io < no; ++io) {
+          const uint32_t g = ob + (uint32_t)io;
+          const size_t rowoff = ((size_t)run.n * P.H + run.h0 + io) * W;
+          uint4 rv[MT][2];  // the residual (block input row h0+io), loaded from L2 before the wait
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) gload2(P.x, rowoff + 128 * mt + quad * 32 + lane, rv[mt]);
+          if (gw == 0 && lane == 0) RBF_EV(11, io);
+          mbar_wait_sleep(t2done0 + 8u * (g % R), (g / R) & 1u);
+          tc_fence_after();
+          if (gw == 0 && lane == 0) RBF_EV(12, io);
+          uint32_t d[MT][16];
+          drain((uint32_t)(MT * R * RBF_C), g % R, d);
+#pragma unroll
+          for (int mt = 0; mt < MT; ++mt) {
+            uint4 w[2];
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv[mt][jj]);
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[jj]);
 #pragma unroll
               for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(a2[e]);
-                v[2 * e] = __uint_as_float(d[mt][2 * e]) * dsoftplus_from_act_fast(f.x);
-                v[2 * e + 1] = __uint_as_float(d[mt][2 * e + 1]) * dsoftplus_from_act_fast(f.y);
-              }
-            } else {  // a = sp(A t)
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const float t = __uint_as_float(d[mt][e]);
-                v[e] = (e & 1) ? softplus_poly_log(t) : softplus_fast(t);
+                const float2 f = __bfloat1622float2(r2[e]);
+                h2[e] = __floats2bfloat162_rn(__uint_as_float(d[mt][8 * jj + 2 * e]) + f.x,
+                                              __uint_as_float(d[mt][8 * jj + 2 * e + 1]) + f.y);
               }
             }
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[mt]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            uint4* o = reinterpret_cast<uint4*>(P.out + (rowoff + 128 * mt + quad * 32 + lane) * RBF_C + c0);
+            o[0] = w[0];
+            o[1] = w[1];
           }
-          st_shared_v4(rbf_chunk(upl, p, slice), w[mt]);
+          give_back(t2free0 + 8u * (g % R));
+          if (gw == 0 && lane == 0) RBF_EV(13, io);
         }
-        fence_async_smem();  // u row -> async proxy (stage-2 MMAs)
-        rbf_epi_bar();
-        if (leader) { mbar_arrive(ufull0 + 8u * (g % US)); RBF_EV(10, iu); }
-        give_back(t1free0 + 8u * (g % R));
-        if (!VJP && inside) {  // the saved activation, off the stage-2 critical path
-#pragma unroll
-          for (int mt = 0; mt < MT; ++mt)
-            *reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0) = w[mt];
-        }
-        if (VJP && iu + 1 < nu && h + 1 < P.H) load_a(run.n, h + 1);  // latency hidden by the next E2
-      };
-      // E2: output row io (image row h0+io) = residual + conv 2
-      auto e2 = [&](int io) {
-        const uint32_t g = ob + (uint32_t)io;
-        const size_t rowoff = ((size_t)run.n * P.H + run.h0 + io) * W;
-        uint4 rv[MT];  // the residual (block input row h0+io), loaded from L2 before the wait
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-          rv[mt] = __ldg(reinterpret_cast<const uint4*>(P.x + (rowoff + 128 * mt + quad * 32 + lane) * RBF_C + c0));
-        if (leader) RBF_EV(11, io);
-        mbar_wait_sleep(t2done0 + 8u * (g % R), (g / R) & 1u);
-        tc_fence_after();
-        if (leader) RBF_EV(12, io);
-        uint32_t d[MT][8];
-        drain((uint32_t)(MT * R * RBF_C), g % R, d);
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rv[mt]);
-          uint4 w;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 f = __bfloat1622float2(r2[e]);
-            h2[e] = __floats2bfloat162_rn(__uint_as_float(d[mt][2 * e]) + f.x, __uint_as_float(d[mt][2 * e + 1]) + f.y);
-          }
-          *reinterpret_cast<uint4*>(P.out + (rowoff + 128 * mt + quad * 32 + lane) * RBF_C + c0) = w;
-        }
-        give_back(t2free0 + 8u * (g % R));
-        if (leader) RBF_EV(13, io);
-      };
-      for (int iu = 0; iu < min(4, nu); ++iu) e1(iu);
-      for (int io = 0; io < no; ++io) {
-        e2(io);
-        if (io + 4 < nu) e1(io + 4);
       }
       uc += (uint32_t)nu;
       oc += (uint32_t)no;

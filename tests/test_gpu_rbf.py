@@ -1,9 +1,9 @@
 """Fused level-0 residual blocks (csrc/rbf.cu): the block's two 3x3 convolutions in one launch,
 streamed down full image rows (the network of Eq. 2, and its
 input VJP). Checked (1) per block against the oracle's layer definitions composed (oracle/nets.py),
-element by element, and (2) inside the solver against the same network run as two launches per
-block (ideq_debug_set_fusion; the solver's default is the two-launch path, faster on B200 -- see
-rbf.cu's status note)."""
+element by element, (2) inside the solver against the same network run as two launches per
+block (ideq_debug_set_fusion), and (3) as the solver's default path by every bf16 U-Net test
+(trajectories, live list, full size)."""
 import numpy as np
 import pytest
 
