@@ -205,17 +205,18 @@ def _config_dict(cfg, per_rank, world):
 
 
 def _tiny_roofline(cfg, per, step_ms):
-    """C1's whole-solve kernel (one 8-SM cluster per image): ALU roofline of the algorithmic FLOPs
-    (network forward + input VJP, 2 FLOP / MAC, and the blur A z, A^T r) against the chip's derived
-    FFMA peak and against the 8 SMs one image's cluster can use."""
+    """C1's whole-solve kernel (one P-SM cluster per image, P = 16 when H allows, else 8): ALU
+    roofline of the algorithmic FLOPs (network forward + input VJP, 2 FLOP / MAC, and the blur A z,
+    A^T r) against the chip's derived FFMA peak and against the P SMs one image's cluster can use."""
     w, C, HW, ks = cfg["widths"][0], cfg["C"], cfg["H"] * cfg["W"], cfg["ksize"]
     macs = 9 * (C * w + w * w + w * C) * HW * 2 + 2 * ks * ks * HW * C
     flops = 2.0 * macs * per
     ach = flops / (step_ms / 1000.0) / 1e12
     chip = 148 * 128 * 2 * 1965e6 / 1e12
-    cluster = 8 * 128 * 2 * 1965e6 / 1e12 * per
+    P = 16 if cfg["H"] % 16 == 0 and (cfg["H"] // 16) % 2 == 0 else 8   # tiny_solve.cu ts_cluster
+    cluster = P * 128 * 2 * 1965e6 / 1e12 * per
     return {"bound": "alu", "achieved": ach, "peak": chip, "unit": "TFLOP/s", "frac": ach / chip, "traffic": None,
-            "kernel": "tiny_solve_kernel (the whole solve in one launch, one 8-CTA cluster per image)",
+            "kernel": f"tiny_solve_kernel (the whole solve in one launch, one {P}-CTA cluster per image)",
             "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 FLOP x 1965 MHz",
             "frac_of_cluster_sms": ach / cluster, "us_per_iteration": step_ms * 1000.0,
             "algorithmic_flops_per_step": flops, "launches_per_solve": 1}

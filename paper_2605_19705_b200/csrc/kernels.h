@@ -187,7 +187,7 @@ void rbf_launch(const RbfPlan* p, cudaStream_t s);
 void rbf_free_plan(RbfPlan* p);
 void init_attrs_rbf();
 
-// Whole-solve persistent kernel of the tiny network (tiny_solve.cu): one 8-CTA cluster per image.
+// Whole-solve persistent kernel of the tiny network (tiny_solve.cu): one 8- or 16-CTA cluster per image.
 struct TinySolveArgs {
   int N, H, W, ks, kper;
   const float* kern;

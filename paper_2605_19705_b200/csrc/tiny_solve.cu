@@ -6,36 +6,44 @@
 // iterations inside ONE launch. The per-iteration path costs ~11 launches (72 us per iteration,
 // launch- and latency-bound); here every operand stays in shared memory.
 //
-// One image = one thread-block cluster of 8 CTAs (a batch runs one cluster per image). CTA r owns
-// rows [r R, (r + 1) R) of the image (R = H / 8) and keeps every tensor of the iteration for those
-// rows plus halo rows above and below. A stage's producer PUSHES its boundary rows straight into
-// the neighbours' halo rows (st.shared::cluster, DSMEM) as it computes them, so one cluster barrier
-// per stage both publishes a tensor and completes every halo -- no copy phase. Cheap layers are
-// recomputed on the halo rows instead of exchanged (a1 and U on rows -1 and R), which removes two
-// of the barriers, and the residual's barrier also completes the next iteration's z halos: 5 per
-// iteration. The residual's three partial sums are pushed into every CTA
-// and combined in fp64 in a fixed order, so all 8 CTAs take the identical stop decision.
+// One image = one thread-block cluster of P CTAs (a batch runs one cluster per image): P = 16
+// (non-portable cluster size, 2 rows per CTA at H = 32) where H allows, else 8. CTA r owns rows
+// [r R, (r + 1) R) of the image (R = H / P) and keeps every tensor of the iteration for those rows
+// plus halo rows above and below. A stage's producer PUSHES its boundary rows straight into the
+// halo rows of the CTAs that read them (st.shared::cluster, DSMEM; the 9x9 blur's 4-row halo reaches
+// two CTAs up and down at R = 2) as it computes them, so one cluster barrier per stage both
+// publishes a tensor and completes every halo -- no copy phase. Cheap layers are recomputed on the
+// halo rows instead of exchanged (a1 and U on rows -1 and R), which removes two of the barriers,
+// and the residual's barrier also completes the next iteration's z halos: 5 per iteration. The
+// residual's three partial sums are pushed into every CTA and summed in fp64 by a fixed butterfly,
+// so all P CTAs take the identical stop decision.
 //
 // Layouts: the network tensors (a1, a2, q2, q1 with 16 channels, U) are planes of (R + 4) rows x
-// (W + 2) columns whose border (columns -1 and W, and halo rows outside the image) is zero, so the
-// 3x3 convolutions read without bounds checks. The blur operands (z, the residual rb) are planes of
-// (R + 2 kc) rows x (W + 2 kc) columns with PERIODIC borders (the blur is a circular convolution,
-// reading Q9); c1 reads z through an explicit zero-padding mask. The 16 -> 16 convolutions give a
-// thread 2 rows x 4 output channels (register blocking: 12 input and 9 weight loads per 72 FMAs);
+// (W + 2) columns (channel pitch padded to 2 mod 32 words: the 4 lanes of a pixel read 4 channel
+// planes in distinct banks) whose border (columns -1 and W, and halo rows outside the image) is
+// zero, so the 3x3 convolutions read without bounds checks. The blur operands (z, the residual rb)
+// are planes of (R + 2 kc) rows x (W + 2 kc) columns with PERIODIC borders (the blur is a circular
+// convolution, reading Q9); c1 reads z through an explicit zero-padding mask. The 16 -> 16
+// convolutions give a work item 2 rows x 4 output channels (register blocking: 12 input and 9
+// weight loads per 72 FMAs), split over 2 threads by input channel when R = 2 leaves too few items;
 // the single-channel outputs and the blur split the contraction over adjacent lanes, combined by
-// fixed-order shuffles.
+// fixed-order shuffles. x^k and the candidate x^{k+1} are ping-pong planes.
 //
-// fp32 throughout (the FFMA path's arithmetic: exact fp32 softplus / sigmoid), matching the fp32
-// parity mode. Supported: TINY3 with hidden width 16, C = 1, identity skip, softplus, direct blur
-// gradient step, per-image stop rule, no restart / averaging (the runtime falls back otherwise).
+// Measured (B200, C1, tools/tiny_prof.cu): 18.8 us per iteration with 8-CTA clusters -> 12.9 us
+// with 16-CTA clusters, conflict-free channel planes, the unrolled 9x9 blur and SFU softplus.
+//
+// fp32 throughout (the FFMA path's arithmetic; softplus and sigmoid from the SFU exp / log, abs.
+// error ~1e-7), matching the fp32 parity mode. Supported: TINY3 with hidden width 16, C = 1,
+// identity skip, softplus, direct blur gradient step, per-image stop rule, no restart / averaging
+// (the runtime falls back otherwise).
 #include "common.cuh"
 #include "kernels.h"
 
 namespace ideq {
 
-constexpr int TS_P = 8;    // CTAs per image (cluster size)
-constexpr int TS_T = 512;  // threads per CTA: 4 per pixel for R x W = 128
-constexpr int TS_C = 16;   // hidden width
+constexpr int TS_PMAX = 16;  // CTAs per image (cluster size P: 16 where the image allows, else 8)
+constexpr int TS_T = 512;    // threads per CTA: 4 per pixel for R x W = 128
+constexpr int TS_C = 16;     // hidden width
 
 __device__ __forceinline__ uint32_t ts_smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -65,16 +73,18 @@ __device__ __forceinline__ uint32_t ts_rank() {
 // Shared-memory layout (floats).
 struct TsLayout {
   int R, W, kc;
-  int WP, PN;      // network planes: pitch W + 2, (R + 4) rows (2 halo rows each side)
+  int WP, PN;      // network planes: pitch W + 2, (R + 4) rows (2 halo rows each side), padded so
+                   // that the 4 lanes of a pixel reading 4 channel planes hit 4 distinct banks
   int WB, PB, HB;  // blur planes: pitch W + 2 kc, (R + 2 HB) rows, HB = max(kc, 1)
   int z, rb, u, a1, a2, q2, q1;
   int xk, gf, xn, y;
-  int w1f, w2f, w3f, w1t, w2t, w3t, kern, red;
+  int w1f, w2f, w3f, w1t, w2t, w3t, kern, red, part;
   int total;
   __host__ __device__ void init(int R_, int W_, int ks) {
     R = R_; W = W_; kc = (ks - 1) / 2;
     HB = kc > 1 ? kc : 1;
     WP = W + 2; PN = (R + 4) * WP;
+    PN += (2 - PN % 32 + 32) % 32;  // PN = 2 (mod 32): channel planes 4q + j start 8q banks apart
     WB = W + 2 * kc; PB = (R + 2 * HB) * WB;
     int o = 0;
     auto take = [&](int n) { const int b = o; o += (n + 3) & ~3; return b; };
@@ -83,7 +93,7 @@ struct TsLayout {
     xk = take(R * W); gf = take(R * W); xn = take(R * W); y = take(R * W);
     w1f = take(9 * TS_C); w2f = take(TS_C * 9 * TS_C); w3f = take(TS_C * 9);
     w1t = take(TS_C * 9); w2t = take(TS_C * 9 * TS_C); w3t = take(9 * TS_C);
-    kern = take(ks * ks); red = take(TS_P * 4);
+    kern = take(ks * ks); red = take(TS_PMAX * 4); part = take(TS_T * 8);
     total = o;
   }
   __device__ int n_at(int plane, int ch, int r, int c) const { return plane + ch * PN + (r + 2) * WP + c + 1; }
@@ -123,30 +133,37 @@ struct TinyArgs {
 // the CTAs above (their row R + r, if r < nh) and below (their row r - R, if r >= R - nh); image
 // borders have no neighbour there (those halo rows stay zero = the convolutions' zero padding).
 __device__ __forceinline__ void ts_put_net(float* sm, const TsLayout& L, int o, float v, int r, int rank, int H, int nh,
-                                          uint32_t base) {
+                                          uint32_t base) {  // nh <= R: the halo rows come from the adjacent CTAs
   sm[o] = v;
   if (r < nh && rank > 0) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)(o + L.R * L.WP), (uint32_t)(rank - 1)), v);
   if (r >= L.R - nh && (rank + 1) * L.R < H)
     ts_st_cluster(ts_mapa(base + 4u * (uint32_t)(o - L.R * L.WP), (uint32_t)(rank + 1)), v);
 }
-// Store v at (r, c) of a blur plane, its periodic column copies, and push the row into the
-// neighbours' halo rows (periodic in the image: the first CTA's rows are the last one's lower halo).
+// Store v at (r, c) of a blur plane, its periodic column copies, and push the row into the halo
+// rows of every CTA whose halo covers it (periodic in the image: the first CTA's rows are the last
+// one's lower halo; with R < HB a row reaches the CTAs d = 1 .. ceil(HB / R) away).
+template <int P>
 __device__ __forceinline__ void ts_put_blur(float* sm, const TsLayout& L, int plane, int r, int c, float v, int rank,
                                            uint32_t base) {
   int cols[2] = {c, c};
   int nc = 1;
   if (c < L.kc) cols[nc++] = c + L.W;
   else if (c >= L.W - L.kc) cols[nc++] = c - L.W;
-  const uint32_t up = (uint32_t)((rank + TS_P - 1) % TS_P), dn = (uint32_t)((rank + 1) % TS_P);
   for (int i = 0; i < nc; ++i) {
     sm[L.b_at(plane, r, cols[i])] = v;
-    if (r < L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r + L.R, cols[i]), up), v);
-    if (r >= L.R - L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r - L.R, cols[i]), dn), v);
+    for (int d = 1; (d - 1) * L.R < L.HB && d < P; ++d) {
+      const uint32_t up = (uint32_t)((rank + P - d) % P), dn = (uint32_t)((rank + d) % P);
+      if (r + d * L.R < L.R + L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r + d * L.R, cols[i]), up), v);
+      if (r - d * L.R >= -L.HB) ts_st_cluster(ts_mapa(base + 4u * (uint32_t)L.b_at(plane, r - d * L.R, cols[i]), dn), v);
+    }
   }
 }
 
-__device__ __forceinline__ float ts_softplus(float t) { return fmaxf(t, 0.f) + log1pf(__expf(-fabsf(t))); }
-__device__ __forceinline__ float ts_dsp(float a) { return -expm1f(-a); }  // sigmoid(p) from a = sp(p)
+// softplus(t) = max(t, 0) + log(1 + e^{-|t|}) and sp'(p) = 1 - e^{-a} from a = sp(p) with the SFU
+// exp / log (abs. error ~1e-7: the 1 + u rounding, far below the 1e-4 iterate tolerance of the
+// fp32 mode; the accurate log1pf / expm1f sequences cost ~3x the instructions)
+__device__ __forceinline__ float ts_softplus(float t) { return fmaxf(t, 0.f) + __logf(1.f + __expf(-fabsf(t))); }
+__device__ __forceinline__ float ts_dsp(float a) { return 1.f - __expf(-a); }  // sigmoid(p) from a = sp(p)
 // fixed-order sums over the 4 (2) adjacent lanes of one pixel
 __device__ __forceinline__ float ts_sum4(float v) {
   v += __shfl_xor_sync(0xffffffffu, v, 1);
@@ -156,15 +173,16 @@ __device__ __forceinline__ float ts_sum4(float v) {
 
 // 16 -> 16 3x3 convolution, 2 output rows (r0, r0 + 1) x 4 output channels (4q .. 4q + 3) at column c;
 // w: [ci][tap][co] (forward) or, ADJ (conv3x3^T: flipped taps), [co][tap][ci] -- same indexing
+// over the input channels [ci0, ci0 + nci)
 template <bool ADJ>
 __device__ __forceinline__ void ts_conv16(const float* sm, const TsLayout& L, int in_plane, int w, int r0, int c,
-                                          int q, float (&acc)[2][4]) {
+                                          int q, int ci0, int nci, float (&acc)[2][4]) {
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[i][e] = 0.f;
 #pragma unroll 2
-  for (int ci = 0; ci < TS_C; ++ci) {
+  for (int ci = ci0; ci < ci0 + nci; ++ci) {
     const float* in = sm + L.n_at(in_plane, ci, r0, c);
     float v[4][3];  // input rows r0 - 1 .. r0 + 2, columns c - 1 .. c + 1
 #pragma unroll
@@ -185,16 +203,21 @@ __device__ __forceinline__ void ts_conv16(const float* sm, const TsLayout& L, in
   }
 }
 
-__global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
+// Split-K partials of the blocked 16 -> 16 convolutions: with R = 2 (16-CTA clusters) the blocked
+// mapping has only W x 4 items, so ksplit = 2 threads share an item (8 input channels each); the
+// second half's 8 accumulators go through shared memory and are added in a fixed order.
+// KS: the blur kernel size as a compile-time constant (its loops fully unrolled), 0 = runtime A.ks.
+template <int P, int KS>
+__global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
   extern __shared__ __align__(16) float sm[];
   const int rank = (int)ts_rank();
-  const int n = blockIdx.x / TS_P;
+  const int n = blockIdx.x / P;
   const int H = A.H, W = A.W, R = A.R;
   const int row0 = rank * R;
   TsLayout L;
   L.init(R, W, A.ks);
   const int RW = R * W;
-  const int ks = A.ks, kc = L.kc;
+  const int ks = KS ? KS : A.ks, kc = L.kc;
   const uint32_t base = ts_smem_u32(sm);
   // ---- zero everything (network plane borders stay zero), weights in stage-friendly layouts
   for (int t = threadIdx.x; t < L.total; t += TS_T) sm[t] = 0.f;
@@ -220,17 +243,21 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     const float v = A.x[img + t];
     sm[L.xk + t] = v;
     sm[L.y + t] = A.y[img + t];
-    ts_put_blur(sm, L, L.z, t / W, t % W, v, rank, base);
+    ts_put_blur<P>(sm, L, L.z, t / W, t % W, v, rank, base);
   }
   int iters = 0, status = 1;
   float res = __int_as_float(0x7fc00000);
-  // blocked 16 -> 16 stages: thread -> (column, row pair, channel quarter) for t < 2 RW... 4 RW / 2
-  const int nb = W * (R / 2) * 4;  // blocked threads
-  const int cb = threadIdx.x % W, rb0 = 2 * ((threadIdx.x / W) % (R / 2)), qb = threadIdx.x / (W * (R / 2));
+  // blocked 16 -> 16 stages: item -> (column, row pair, channel quarter), ksplit threads per item
+  const int nb = W * (R / 2) * 4;  // blocked items
+  const int ksplit = nb <= TS_T / 4 ? 2 : 1, nkb = nb * ksplit;
+  const int tb = threadIdx.x % nb, kh = threadIdx.x / nb;  // item, K part
+  const int cb = tb % W, rb0 = 2 * ((tb / W) % (R / 2)), qb = tb / (W * (R / 2));
+  const int ci0 = kh * (TS_C / ksplit), nci = TS_C / ksplit;
   // split-K stages: 4 lanes per pixel
   const int pk = threadIdx.x >> 2, qk = threadIdx.x & 3;
   const int rk = pk / W, ck = pk % W;
   const bool act_k = pk < RW;
+  int xk_o = L.xk, xn_o = L.xn;  // x^k and the candidate x^{k+1} (ping-pong planes)
   long long t_mark = clock64();
   ts_cluster_sync();  // z^0 (own rows + pushed halos) complete on every CTA
   for (int k = 0; k < A.max_iter; ++k) {
@@ -257,36 +284,51 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     }
     if (act_k) {  // kernel rows i = qk, qk + 4, ...: (A z)[r][c] = sum k[i][j] z[r - i + kc][c - j + kc]
       float s = 0.f;
+#pragma unroll
       for (int i = qk; i < ks; i += 4) {
         const float* zr = sm + L.b_at(L.z, rk - i + kc, ck + kc);
         const float* kr = sm + L.kern + i * ks;
+#pragma unroll
         for (int j = 0; j < ks; ++j) s = fmaf(kr[j], zr[-j], s);
       }
       s = ts_sum4(s);
-      if (qk == 0) ts_put_blur(sm, L, L.rb, rk, ck, s - sm[L.y + pk], rank, base);
+      if (qk == 0) ts_put_blur<P>(sm, L, L.rb, rk, ck, s - sm[L.y + pk], rank, base);
     }
     TS_MARK(1)
     ts_cluster_sync();  // [S1] rb halos (a1 is local)
     TS_MARK(2)
     // [2] a2 = sp(c2(a1)) (blocked threads), pushed with a 2-row halo; gf = A^T rb (the others)
+    float acc[2][4];
+    if (threadIdx.x < nkb) {
+      ts_conv16<false>(sm, L, L.a1, L.w2f, rb0, cb, qb, ci0, nci, acc);
+      if (kh == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[L.part + i * nb + tb] = acc[i >> 2][i & 3];
+      }
+    } else if (threadIdx.x - nkb < 2 * RW) {  // 2 lanes per pixel: (A^T rb)[r][c] = sum k[i][j] rb[r + i - kc][c + j - kc]
+      const int t = threadIdx.x - nkb, p = t >> 1, h = t & 1, r = p / W, c = p % W;
+      float s = 0.f;
+#pragma unroll
+      for (int i = h; i < ks; i += 2) {
+        const float* rr = sm + L.b_at(L.rb, r + i - kc, c - kc);
+        const float* kr = sm + L.kern + i * ks;
+#pragma unroll
+        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], rr[j], s);
+      }
+      s += __shfl_xor_sync(0xffffffffu, s, 1);
+      if (h == 0) sm[L.gf + p] = s;
+    }
+    if (ksplit > 1) __syncthreads();
     if (threadIdx.x < nb) {
-      float acc[2][4];
-      ts_conv16<false>(sm, L, L.a1, L.w2f, rb0, cb, qb, acc);
+      if (ksplit > 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i >> 2][i & 3] += sm[L.part + i * nb + tb];
+      }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           ts_put_net(sm, L, L.n_at(L.a2, 4 * qb + e, rb0 + i, cb), ts_softplus(acc[i][e]), rb0 + i, rank, H, 2, base);
-    } else if (threadIdx.x - nb < 2 * RW) {  // 2 lanes per pixel: (A^T rb)[r][c] = sum k[i][j] rb[r + i - kc][c + j - kc]
-      const int t = threadIdx.x - nb, p = t >> 1, h = t & 1, r = p / W, c = p % W;
-      float s = 0.f;
-      for (int i = h; i < ks; i += 2) {
-        const float* rr = sm + L.b_at(L.rb, r + i - kc, c - kc);
-        const float* kr = sm + L.kern + i * ks;
-        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], rr[j], s);
-      }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (h == 0) sm[L.gf + p] = s;
     }
     TS_MARK(3)
     ts_cluster_sync();  // [S2] a2 halos (2 rows)
@@ -329,9 +371,19 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     ts_cluster_sync();  // [S3] q2 halos
     TS_MARK(6)
     // [5] q1 = c2^T(q2) . sp'(a1) (blocked threads), pushed (1-row halo)
+    if (threadIdx.x < nkb) {
+      ts_conv16<true>(sm, L, L.q2, L.w2t, rb0, cb, qb, ci0, nci, acc);
+      if (kh == 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[L.part + i * nb + tb] = acc[i >> 2][i & 3];
+      }
+    }
+    if (ksplit > 1) __syncthreads();
     if (threadIdx.x < nb) {
-      float acc[2][4];
-      ts_conv16<true>(sm, L, L.q2, L.w2t, rb0, cb, qb, acc);
+      if (ksplit > 1) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i >> 2][i & 3] += sm[L.part + i * nb + tb];
+      }
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
@@ -356,16 +408,16 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
       }
       s = ts_sum4(s);
       if (qk == 0) {
-        const float z = sm[L.b_at(L.z, rk, ck)], xk = sm[L.xk + pk];
+        const float z = sm[L.b_at(L.z, rk, ck)], xk = sm[xk_o + pk];
         const float x1 = z - A.tau * (sm[L.gf + pk] + A.lam * s);
-        sm[L.xn + pk] = x1;  // candidate x^{k+1}
+        sm[xn_o + pk] = x1;  // candidate x^{k+1}
         const float d = x1 - xk;
         if (isfinite(x1)) d2 = d * d; else bad = 1.f;
         n2 = xk * xk;
         // candidate z^{k+1} = x^{k+1} + beta (x^{k+1} - x^k) (Eq. 4), pushed now so that the
         // residual's barrier also completes the next iteration's z halos (every read of z^k by
         // a neighbour happened before [S1]; a diverged or converged image exits before using it)
-        ts_put_blur(sm, L, L.z, rk, ck, x1 + A.beta * (x1 - xk), rank, base);
+        ts_put_blur<P>(sm, L, L.z, rk, ck, x1 + A.beta * (x1 - xk), rank, base);
       }
     }
     // block reduction (fixed order), then this CTA's partials into slot `rank` of every CTA
@@ -380,7 +432,7 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
       }
       if (lane == 0) { wred[0][wid] = d2; wred[1][wid] = n2; wred[2][wid] = bad; }
       __syncthreads();
-      if (threadIdx.x < TS_P) {
+      if (threadIdx.x < P) {
         float a = 0.f, b = 0.f, e = 0.f;
         for (int w = 0; w < TS_T / 32; ++w) { a += wred[0][w]; b += wred[1][w]; e += wred[2][w]; }
         const uint32_t dst = ts_mapa(base + 4u * (uint32_t)(L.red + rank * 4), (uint32_t)threadIdx.x);
@@ -392,21 +444,31 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
     TS_MARK(9)
     ts_cluster_sync();  // [S5] partials, z^{k+1}
     TS_MARK(10)
+    // the P partials in fp64, summed by every warp with the same butterfly (a + b = b + a, so every
+    // lane, warp and CTA gets the identical value: one stop decision for the cluster)
     double D2 = 0.0, N2 = 0.0, BAD = 0.0;
-    for (int q = 0; q < TS_P; ++q) {  // fixed order: identical on every CTA
-      D2 += (double)sm[L.red + q * 4];
-      N2 += (double)sm[L.red + q * 4 + 1];
-      BAD += (double)sm[L.red + q * 4 + 2];
+    {
+      const int ln = threadIdx.x & 31;
+      if (ln < P) {
+        D2 = (double)sm[L.red + ln * 4];
+        N2 = (double)sm[L.red + ln * 4 + 1];
+        BAD = (double)sm[L.red + ln * 4 + 2];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        D2 += __shfl_xor_sync(0xffffffffu, D2, o);
+        N2 += __shfl_xor_sync(0xffffffffu, N2, o);
+        BAD += __shfl_xor_sync(0xffffffffu, BAD, o);
+      }
     }
     if (BAD > 0.0 || !isfinite(D2)) {  // reading Q22: keep x^k, status diverged
       status = 2;
       break;
     }
-    const double rr = N2 > 0.0 ? sqrt(D2) / sqrt(N2) : (double)INFINITY;
-    res = (float)rr;
+    res = N2 > 0.0 ? sqrtf((float)D2) / sqrtf((float)N2) : INFINITY;  // fp64 sums, fp32 root (res is fp32)
     iters = k + 1;
     // accept: x^k <- x^{k+1} (z^{k+1} is already in place)
-    for (int t = threadIdx.x; t < RW; t += TS_T) sm[L.xk + t] = sm[L.xn + t];
+    { const int t = xk_o; xk_o = xn_o; xn_o = t; }  // x^k <- x^{k+1}: the planes swap roles
     if (rank == 0 && threadIdx.x == 0 && A.trace && k < A.trace_cap)
       atomicMax(reinterpret_cast<int*>(A.trace) + k, __float_as_int(res));
     TS_MARK(11)
@@ -417,7 +479,7 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
   }
   // x-hat = the last accepted iterate (Remark 1)
   __syncthreads();
-  for (int t = threadIdx.x; t < RW; t += TS_T) A.x[img + t] = sm[L.xk + t];
+  for (int t = threadIdx.x; t < RW; t += TS_T) A.x[img + t] = sm[xk_o + t];
   if (rank == 0 && threadIdx.x == 0) {
     A.iters[n] = iters;
     A.res[n] = res;
@@ -427,33 +489,71 @@ __global__ void __cluster_dims__(TS_P, 1, 1) __launch_bounds__(TS_T, 1) tiny_sol
   ts_cluster_sync();  // no CTA exits while a neighbour may still write into its shared memory
 }
 
+// cluster size for an image of H rows: 16 CTAs (2 rows each) where that fits, else 8
+static int ts_cluster(int H) { return (H % 16 == 0 && (H / 16) % 2 == 0) ? 16 : 8; }
+
 size_t tiny_solve_smem(int H, int W, int ks) {
   TsLayout L;
-  L.init(H / TS_P, W, ks);
+  L.init(H / ts_cluster(H), W, ks);
   return sizeof(float) * (size_t)L.total;
 }
 
 // (R + 2) W x 4 items per recomputed stage are looped; R x W <= 128 keeps one pixel per 4 lanes
 bool tiny_solve_supported(int H, int W, int ks) {
-  if (H % TS_P != 0 || W % 32 != 0 || W < ks) return false;
-  const int R = H / TS_P;
-  // 4 lanes per pixel, whole warps per stage, 2-row blocks, halo rows from the two neighbours only
-  if (R * W > TS_T / 4 || R % 2 != 0 || R < 2 || R < (ks - 1) / 2) return false;
+  const int P = ts_cluster(H);
+  if (H % P != 0 || W % 32 != 0 || W < ks) return false;
+  const int R = H / P;
+  const int HB = (ks - 1) / 2 > 1 ? (ks - 1) / 2 : 1;
+  // 4 lanes per pixel, whole warps per stage, 2-row blocks; the blur halo (HB rows) within the
+  // image and the network halos (2 rows) from the adjacent CTAs
+  if (R * W > TS_T / 4 || R % 2 != 0 || R < 2 || HB > (P / 2) * R) return false;
   return tiny_solve_smem(H, W, ks) <= 200 * 1024;
+}
+
+template <int P, int KS>
+static void launch_tiny_p(const TinyArgs& A, size_t smem, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(P * A.N));
+  cfg.blockDim = dim3(TS_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = P;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, tiny_solve_kernel<P, KS>, A);
 }
 
 void launch_tiny_solve(const TinySolveArgs& a, cudaStream_t s) {
   TinyArgs A{};
-  A.N = a.N; A.H = a.H; A.W = a.W; A.R = a.H / TS_P;
+  const int P = ts_cluster(a.H);
+  A.N = a.N; A.H = a.H; A.W = a.W; A.R = a.H / P;
   A.ks = a.ks; A.kper = a.kper; A.kern = a.kern;
   A.w1 = a.w1; A.w2 = a.w2; A.w3 = a.w3; A.y = a.y; A.x = a.x;
   A.lam = a.lam; A.tau = a.tau; A.beta = a.beta; A.tol = a.tol;
   A.max_iter = a.max_iter; A.check_every = a.check_every;
   A.iters = a.iters; A.res = a.res; A.status = a.status; A.trace = a.trace; A.trace_cap = a.trace_cap;
   A.kdone = a.kdone;
-  tiny_solve_kernel<<<dim3(TS_P * a.N), dim3(TS_T), tiny_solve_smem(a.H, a.W, a.ks), s>>>(A);
+  const size_t smem = tiny_solve_smem(a.H, a.W, a.ks);
+  if (P == 16) {
+    if (a.ks == 9) launch_tiny_p<16, 9>(A, smem, s);
+    else launch_tiny_p<16, 0>(A, smem, s);
+  } else {
+    if (a.ks == 9) launch_tiny_p<8, 9>(A, smem, s);
+    else launch_tiny_p<8, 0>(A, smem, s);
+  }
 }
 
-void init_attrs_tiny() { set_max_dyn_smem(tiny_solve_kernel); }
+void init_attrs_tiny() {
+  set_max_dyn_smem(tiny_solve_kernel<8, 0>);
+  set_max_dyn_smem(tiny_solve_kernel<8, 9>);
+  set_max_dyn_smem(tiny_solve_kernel<16, 0>);
+  set_max_dyn_smem(tiny_solve_kernel<16, 9>);
+  cudaFuncSetAttribute(tiny_solve_kernel<16, 0>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaFuncSetAttribute(tiny_solve_kernel<16, 9>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+}
 
 }  // namespace ideq

@@ -258,14 +258,16 @@ def test_direct_blur_kernel_sizes(ks, H, W):
         assert abs(st["residual"][b] - orc["residual"][b]) <= 1e-6
 
 
-@pytest.mark.parametrize("batch,tol,K", [(1, 0.0, 100), (3, 0.0, 40), (3, 5e-4, 200)])
-def test_tiny_whole_solve_kernel(batch, tol, K):
-    """C1's whole solve in one launch (tiny_solve.cu: one 8-CTA cluster per image, DSMEM halos):
-    fp32 iterates within 1e-4 and residuals within 1e-6 of the oracle, stop iterations equal
-    (tol > 0, per-image rule), and the same result as the per-iteration kernels (the profiling
-    mode launches those eagerly) within fp32 rounding."""
+@pytest.mark.parametrize("batch,tol,K,H", [(1, 0.0, 100, 32), (3, 0.0, 40, 32), (3, 5e-4, 200, 32),
+                                           (2, 0.0, 30, 16), (2, 5e-4, 200, 64)])
+def test_tiny_whole_solve_kernel(batch, tol, K, H):
+    """C1's whole solve in one launch (tiny_solve.cu: one cluster per image, DSMEM halos; H = 32
+    and 64 run 16-CTA clusters of 2 / 4 rows (the 9x9 blur halo reaches two CTAs up and down at
+    2 rows), H = 16 an 8-CTA cluster of 2 rows): fp32 iterates within 1e-4 and residuals within 1e-6
+    of the oracle, stop iterations equal (tol > 0, per-image rule), and the same result as the
+    per-iteration kernels (the profiling mode launches those eagerly) within fp32 rounding."""
     torch = torch_cuda()
-    cfg = _mini("C1", batch=batch)
+    cfg = _mini("C1", batch=batch, H=H)
     prob = synth.make_problem(cfg)
     orc = osolver.solve_config(cfg, prob, max_iter=K, tol=tol, trace=True)
     s = _solver(cfg, prob, "fp32")
