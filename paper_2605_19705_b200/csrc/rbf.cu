@@ -28,9 +28,9 @@
 // HBM traffic per block: read x (+ a in the VJP), write a (forward) and the output.
 // Each run recomputes two intermediate rows (h0 - 1 and h1) and reads two extra input rows.
 //
-// Warp roles (576 threads, one CTA per SM): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2..9 the stage-1 epilogue and warps 10..17 the stage-2 epilogue (each: TMEM lane
-// quadrant = warp % 4, 16-channel half = ((warp - 2) % 8) / 4).
+// Warp roles (one CTA per SM): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer, then
+// 8 stage-1 epilogue warps per M tile (W = 256: warps 2..17, one tile each) and 8 stage-2
+// epilogue warps for the whole row (each: TMEM lane quadrant = warp % 4, 16-channel half).
 // MMA order per run: S1(k) for input rows k = 0 .. nu+1, and S2(j) for intermediate row j right
 // after S1(j+3), so the stage-1 epilogue of row j overlaps two MMA stages before S2(j) reads it.
 //
@@ -48,6 +48,7 @@
 //     adds +0 to; the two epilogue stages run in separate warp groups so neither waits for the
 //     other's rows.
 #include <cuda.h>
+#include <type_traits>
 #include <stdio.h>
 #include <string.h>
 #include "common.cuh"
@@ -56,9 +57,11 @@
 
 namespace ideq {
 
-constexpr int RBF_EPI_WARPS = 16;         // two groups of 8: stage-1 and stage-2 epilogues
-constexpr int RBF_GROUP_WARPS = 8;        // per group: 2 per TMEM lane quadrant, 16 channels each
-constexpr int RBF_THREADS = (2 + RBF_EPI_WARPS) * 32;
+// Epilogue groups: stage 1 has 8 warps per M tile (one tile per warp: 2 per TMEM lane quadrant,
+// 16 channels each), stage 2 has 8 warps for all tiles of a row.
+constexpr int RBF_GROUP_WARPS = 8;
+template <int MT>
+constexpr int rbf_threads() { return (2 + RBF_GROUP_WARPS * MT + RBF_GROUP_WARPS) * 32; }
 constexpr int RBF_C = 32;                 // channels (64-byte pixels, SW64)
 constexpr uint32_t RBF_PIX = RBF_C * 2;
 constexpr uint32_t RBF_WTAP = RBF_C * RBF_PIX;     // 2 KB: B operand of one tap (32 rows x 64 B)
@@ -129,9 +132,10 @@ __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
       "r"(parity), "r"(1000000u)
       : "memory");
 }
-// named barrier 1 over the epilogue warps
-__device__ __forceinline__ void rbf_epi_bar() {  // the stage-1 epilogue group
-  asm volatile("bar.sync 1, %0;" ::"n"(RBF_GROUP_WARPS * 32) : "memory");
+// named barrier 1 over the stage-1 epilogue group
+template <int MT>
+__device__ __forceinline__ void rbf_epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(RBF_GROUP_WARPS * MT * 32) : "memory");
 }
 // tcgen05.ld / st of 8 columns (32 lanes x 32 bit)
 __device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&r)[8]) {
@@ -161,7 +165,7 @@ __device__ __forceinline__ bool rbf_next_run(const RbfParams& P, int& q, int q1,
 }
 
 template <int MT, bool VJP>
-__global__ void __launch_bounds__(RBF_THREADS, 1)
+__global__ void __launch_bounds__(rbf_threads<MT>(), 1)
     rbf_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ RbfParams P) {
   using Cfg = RbfCfg<MT>;
   constexpr int XS = Cfg::XS, US = Cfg::US, R = Cfg::R, W = Cfg::W;
@@ -204,7 +208,7 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
     for (int s = 0; s < XS; ++s) { mbar_init(xfull0 + 8u * s, 1); mbar_init(xempty0 + 8u * s, 1); }
     for (int s = 0; s < US; ++s) { mbar_init(ufull0 + 8u * s, 1); mbar_init(uempty0 + 8u * s, 1); }
     for (int s = 0; s < R; ++s) {
-      mbar_init(t1done0 + 8u * s, 1); mbar_init(t1free0 + 8u * s, RBF_GROUP_WARPS);
+      mbar_init(t1done0 + 8u * s, 1); mbar_init(t1free0 + 8u * s, RBF_GROUP_WARPS * MT);
       mbar_init(t2done0 + 8u * s, 1); mbar_init(t2free0 + 8u * s, RBF_GROUP_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -221,7 +225,7 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = __shfl_sync(0xffffffffu, *tmem_holder, 0);
-  if (warp >= 2) {  // every ring block starts (and is returned by the epilogue) zeroed
+  if (warp >= 2 && warp < 18) {  // every ring block starts (and is returned by the epilogue) zeroed
     const uint32_t ta = tmem_base + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(((warp - 2) >> 2) * 128);
 #pragma unroll
     for (int c = 0; c < 128; c += 8) tmem_zero8(ta + (uint32_t)c);
@@ -366,9 +370,13 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
     }
   } else {
     // ---------------- epilogue: two independent warp groups, so a slow stage-2 row never holds up
-    // the stage-1 epilogue the MMA warp is waiting on (and vice versa). Group 0 (warps 2..9):
-    // E1, group 1 (warps 10..17): E2; in a group, warp -> (TMEM lane quadrant, 16-channel half).
-    const int grp = (warp - 2) / RBF_GROUP_WARPS, gw = (warp - 2) % RBF_GROUP_WARPS;
+    // the stage-1 epilogue the MMA warp is waiting on (and vice versa). Group 0 (warps 2 ..
+    // 1 + 8 MT): E1, one M tile per warp (tile = (warp - 2) / 8), group 1 (the last 8 warps): E2,
+    // every tile; in a group, warp -> (TMEM lane quadrant, 16-channel half).
+    constexpr int E1W = RBF_GROUP_WARPS * MT;
+    const int grp = warp - 2 < E1W ? 0 : 1;
+    const int gw = grp == 0 ? (warp - 2) % RBF_GROUP_WARPS : warp - 2 - E1W;
+    const int e1_mt = grp == 0 ? (warp - 2) / RBF_GROUP_WARPS : 0;
     const int quad = warp & 3, half = gw >> 2;
     const int c0 = half * 16;  // this warp's 16 channels = 16-byte chunks 2 half, 2 half + 1
     const bool leader = warp == 2 && lane == 0;
@@ -376,21 +384,22 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
     int q = q0;
     RbfRun run;
     const uint32_t tq = tmem_base + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
-    // read this warp's 16 columns of ring block `blk` of a stage for every M tile and zero them
-    auto drain = [&](uint32_t stage_col, uint32_t blk, uint32_t (&v)[MT][16]) {
+    // read this warp's 16 columns of ring block `blk` of a stage for M tiles [m0, m0 + NM) and zero them
+    auto drain = [&](uint32_t stage_col, uint32_t blk, int m0, auto nm_tag, uint32_t (&v)[decltype(nm_tag)::value][16]) {
+      constexpr int NM = decltype(nm_tag)::value;
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
+      for (int i = 0; i < NM; ++i) {
         uint32_t a[8], b[8];
-        tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C, a);
-        tmem_ld8_nw(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C + 8u, b);
+        tmem_ld8_nw(tq + stage_col + (uint32_t)((m0 + i) * R * RBF_C) + blk * RBF_C, a);
+        tmem_ld8_nw(tq + stage_col + (uint32_t)((m0 + i) * R * RBF_C) + blk * RBF_C + 8u, b);
         tmem_wait();
 #pragma unroll
-        for (int e = 0; e < 8; ++e) { v[mt][e] = a[e]; v[mt][8 + e] = b[e]; }
+        for (int e = 0; e < 8; ++e) { v[i][e] = a[e]; v[i][8 + e] = b[e]; }
       }
 #pragma unroll
-      for (int mt = 0; mt < MT; ++mt) {
-        tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C);
-        tmem_zero8(tq + stage_col + (uint32_t)(mt * R * RBF_C) + blk * RBF_C + 8u);
+      for (int i = 0; i < NM; ++i) {
+        tmem_zero8(tq + stage_col + (uint32_t)((m0 + i) * R * RBF_C) + blk * RBF_C);
+        tmem_zero8(tq + stage_col + (uint32_t)((m0 + i) * R * RBF_C) + blk * RBF_C + 8u);
       }
     };
     auto give_back = [&](uint32_t free_bar) {  // after drain: the zeros have landed, block is free
@@ -405,13 +414,13 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
       o[0] = __ldg(g);
       o[1] = __ldg(g + 1);
     };
-    // VJP: the saved-activation chunks of the next stage-1 row, prefetched one row ahead
-    uint4 av[MT][2];
+    // VJP: the saved-activation chunks of the next stage-1 row (this warp's tile), prefetched one row ahead
+    uint4 av[2];
     int av_row = -1;  // image row (in image av_n) av holds, -1: none
     int av_n = -1;
+    const int p1 = 128 * e1_mt + quad * 32 + lane;  // E1: this thread's pixel of the row
     auto load_a = [&](int n, int h) {
-#pragma unroll
-      for (int mt = 0; mt < MT; ++mt) gload2(P.act, ((size_t)n * P.H + h) * W + 128 * mt + quad * 32 + lane, av[mt]);
+      gload2(P.act, ((size_t)n * P.H + h) * W + p1, av);
       av_n = n;
       av_row = h;
     };
@@ -430,51 +439,44 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
           mbar_wait_sleep(t1done0 + 8u * (g % R), (g / R) & 1u);
           tc_fence_after();
           if (leader) RBF_EV(9, iu);
-          uint32_t d[MT][16];
-          drain(0u, g % R, d);
+          uint32_t d[1][16];
+          drain(0u, g % R, e1_mt, std::integral_constant<int, 1>{}, d);
           const uint32_t upl = sU + (g % US) * SLOT + 1024u;
-          uint4 w[MT][2];
+          uint4 w[2];
 #pragma unroll
-          for (int mt = 0; mt < MT; ++mt) {
-            const int p = 128 * mt + quad * 32 + lane;
+          for (int jj = 0; jj < 2; ++jj) {
+            w[jj] = make_uint4(0u, 0u, 0u, 0u);
+            if (inside) {
+              float v[8];
+              if (VJP) {  // q = (B^T g) . sp'(a)
+                const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[jj]);
 #pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              w[mt][jj] = make_uint4(0u, 0u, 0u, 0u);
-              if (inside) {
-                float v[8];
-                if (VJP) {  // q = (B^T g) . sp'(a)
-                  const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&av[mt][jj]);
-#pragma unroll
-                  for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(a2[e]);
-                    v[2 * e] = __uint_as_float(d[mt][8 * jj + 2 * e]) * dsoftplus_from_act_fast(f.x);
-                    v[2 * e + 1] = __uint_as_float(d[mt][8 * jj + 2 * e + 1]) * dsoftplus_from_act_fast(f.y);
-                  }
-                } else {  // a = sp(A t)
-#pragma unroll
-                  for (int e = 0; e < 8; ++e) {
-                    const float t = __uint_as_float(d[mt][8 * jj + e]);
-                    v[e] = (e & 1) ? softplus_poly_log(t) : softplus_fast(t);
-                  }
+                for (int e = 0; e < 4; ++e) {
+                  const float2 f = __bfloat1622float2(a2[e]);
+                  v[2 * e] = __uint_as_float(d[0][8 * jj + 2 * e]) * dsoftplus_from_act_fast(f.x);
+                  v[2 * e + 1] = __uint_as_float(d[0][8 * jj + 2 * e + 1]) * dsoftplus_from_act_fast(f.y);
                 }
-                __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[mt][jj]);
+              } else {  // a = sp(A t)
 #pragma unroll
-                for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+                for (int e = 0; e < 8; ++e) {
+                  const float t = __uint_as_float(d[0][8 * jj + e]);
+                  v[e] = (e & 1) ? softplus_poly_log(t) : softplus_fast(t);
+                }
               }
-              st_shared_v4(rbf_chunk(upl, p, 2 * half + jj), w[mt][jj]);
+              __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w[jj]);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
             }
+            st_shared_v4(rbf_chunk(upl, p1, 2 * half + jj), w[jj]);
           }
           fence_async_smem();  // u row -> async proxy (stage-2 MMAs)
-          rbf_epi_bar();
+          rbf_epi_bar<MT>();
           if (leader) { mbar_arrive(ufull0 + 8u * (g % US)); RBF_EV(10, iu); }
           give_back(t1free0 + 8u * (g % R));
           if (!VJP && inside) {  // the saved activation, off the stage-2 critical path
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-              uint4* o = reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + 128 * mt + quad * 32 + lane) * RBF_C + c0);
-              o[0] = w[mt][0];
-              o[1] = w[mt][1];
-            }
+            uint4* o = reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + p1) * RBF_C + c0);
+            o[0] = w[0];
+            o[1] = w[1];
           }
           if (VJP && iu + 1 < nu && h + 1 < P.H) load_a(run.n, h + 1);  // latency hidden by the next waits
         }
@@ -491,7 +493,7 @@ __global__ void __launch_bounds__(RBF_THREADS, 1)
           tc_fence_after();
           if (gw == 0 && lane == 0) RBF_EV(12, io);
           uint32_t d[MT][16];
-          drain((uint32_t)(MT * R * RBF_C), g % R, d);
+          drain((uint32_t)(MT * R * RBF_C), g % R, 0, std::integral_constant<int, MT>{}, d);
 #pragma unroll
           for (int mt = 0; mt < MT; ++mt) {
             uint4 w[2];
@@ -597,7 +599,7 @@ void rbf_free_plan(RbfPlan* p) { delete p; }
 void rbf_launch(const RbfPlan* p, cudaStream_t s) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)p->grid);
-  cfg.blockDim = dim3(RBF_THREADS);
+  cfg.blockDim = dim3(p->P.W == 128 ? rbf_threads<1>() : rbf_threads<2>());
   cfg.dynamicSmemBytes = p->smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
