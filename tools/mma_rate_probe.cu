@@ -1,6 +1,8 @@
 // Probe: tcgen05.mma kind::f16 throughput (M = 128, K = 16 per instruction): clk per MMA by N,
 // operand swizzle, A start alignment, accumulator / A-tile rotation and operand data (zero or not).
 // One CTA per SM, one warp issues (elect.sync) NIT x 8 MMAs; clock64 around issue + commit wait.
+// Inter-warp interference modes (inter 1..5): TMEM loads / stores and shared-memory traffic from
+// three other warps while the MMAs run.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_rate_probe tools/mma_rate_probe.cu
 #include <cstdio>
 #include <cstdint>
@@ -39,15 +41,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 constexpr int NIT = 512;
 // layout 4 = SW64 (64-byte rows), 2 = SW128 (128-byte rows); rotD / rotA: cycle 4 accumulators /
 // 4 A tiles per group of 8 MMAs; shift: A start + 1 row; data: fill value of the operands
-__global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, long long* out) {
+__global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, int inter, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
   unsigned char* g = sm + (base - smem_u32(sm));
   __shared__ __align__(8) uint64_t bar;
   __shared__ __align__(8) uint64_t bar2;
   __shared__ uint32_t tm;
+  __shared__ volatile int stop_flag;
   const uint32_t rowb = layout == 4 ? 64u : 128u, sbo = 8u * rowb;
-  for (uint32_t o = threadIdx.x * 4; o < 96u * 1024u; o += blockDim.x * 4) {
+  for (uint32_t o = threadIdx.x * 4; o < 96u * 1024u; o += blockDim.x * 4) {  // operands
     uint32_t v = data;
     if (data == 1u) {  // pseudo-random bf16 pairs in [-1, 1)
       uint32_t h = (o + 0x9e3779b9u * (blockIdx.x + 1)) * 2654435761u;
@@ -57,6 +60,7 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
     *(uint32_t*)(g + o) = v;
   }
   if (threadIdx.x == 0) {
+    stop_flag = 0;
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar2)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -110,8 +114,57 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
       commit(smem_u32(&bar));
       mbar_wait(smem_u32(&bar), 0);
       if (blockIdx.x == 0) out[0] = clock64() - t0;
+      stop_flag = 1;
     }
     __syncwarp();
+  } else if (inter > 0) {
+    // interference warps 1..3 (TMEM lane quadrants 1..3) until the MMA warp is done:
+    // 1 = tcgen05.ld 16 columns + wait, 2 = st.shared 16 B per lane, 3 = tcgen05.st 8 zero columns
+    // + wait, 4 = ld.shared 16 B per lane, 5 = 1 + 2 (an epilogue's mix)
+    const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (inter >= 6) {  // 6: warps 4, 8, 12 (the MMA warp's scheduler) run FMA / SFU math; 7: the other warps do
+      const bool busy = inter == 6 ? (w % 4 == 0) : (w % 4 != 0);
+      float x = (float)ln * 1e-3f, y = 1.f;
+      while (busy && !stop_flag) {
+#pragma unroll 16
+        for (int r = 0; r < 64; ++r) {
+          x = fmaf(x, 0.999f, 1e-4f);
+          float e;
+          asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-x));
+          y = fmaf(y, e, x);
+        }
+      }
+      if (y == 12345.f) out[1] = 1;
+      return;
+    }
+    const uint32_t ta = tmem + ((uint32_t)(w * 32) << 16) + 256u;
+    const uint32_t sa = base + 96u * 1024u + (uint32_t)w * 512u + (uint32_t)ln * 16u;
+    uint32_t acc = 0;
+    while (!stop_flag) {
+      for (int r = 0; r < 16; ++r) {
+        if (inter == 1 || inter == 5) {
+          uint32_t v[16];
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                         "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                       : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          for (int e = 0; e < 16; ++e) acc += v[e];
+        }
+        if (inter == 2 || inter == 5)
+          asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(sa), "r"(acc) : "memory");
+        if (inter == 3) {
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(ta), "r"(0u) : "memory");
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        if (inter == 4) {
+          uint32_t a0, a1, a2, a3;
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3) : "r"(sa));
+          acc += a0 ^ a1 ^ a2 ^ a3;
+        }
+      }
+    }
+    if (acc == 0x12345678u) out[1] = acc;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -120,9 +173,14 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
 
 int main() {
   long long* d;
-  cudaMalloc(&d, 8);
-  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; } cases[] = {
+  cudaMalloc(&d, 16);
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 4096);
+  struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; } cases[] = {
+      // concurrent traffic from 3 other warps (inter 1..5) during N = 96 / 128 MMAs, D fixed (columns 0..N-1)
+      {4, 96, 0, 0, 1, 1u, 0, 0}, {4, 96, 0, 0, 1, 1u, 0, 1}, {4, 96, 0, 0, 1, 1u, 0, 2}, {4, 96, 0, 0, 1, 1u, 0, 3},
+      {4, 96, 0, 0, 1, 1u, 0, 4}, {4, 96, 0, 0, 1, 1u, 0, 5}, {4, 96, 0, 0, 1, 1u, 4, 0}, {4, 96, 0, 0, 1, 1u, 4, 5},
+      {2, 128, 0, 0, 1, 1u, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 1}, {2, 128, 0, 0, 1, 1u, 0, 2}, {2, 128, 0, 0, 1, 1u, 0, 5},
+      {4, 96, 0, 0, 1, 1u, 0, 6}, {4, 96, 0, 0, 1, 1u, 0, 7}, {4, 96, 0, 0, 1, 1u, 4, 6}, {2, 128, 0, 0, 1, 1u, 0, 6},
       {4, 96, 0, 1, 1, 1u, 0}, {4, 96, 0, 1, 1, 1u, 4}, {4, 96, 0, 1, 1, 1u, 5}, {4, 96, 0, 1, 1, 1u, 0},
       {4, 96, 0, 1, 1, 1u, 10}, {4, 96, 0, 1, 1, 1u, 11}, {4, 96, 0, 0, 1, 1u, 12}, {4, 96, 0, 0, 1, 1u, 13},
       {4, 64, 0, 1, 1, 1u, 10}, {4, 64, 0, 1, 1, 1u, 11}, {4, 64, 0, 1, 1, 1u, 12}, {4, 64, 0, 0, 1, 1u, 13},
@@ -138,15 +196,15 @@ int main() {
   };
   for (auto& c : cases) {
     for (int rep = 0; rep < 2; ++rep) {
-      probe<<<148, 128, 100 * 1024>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, d);
+      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
     }
     long long clk;
     cudaMemcpy(&clk, d, 8, cudaMemcpyDeviceToHost);
     const double per = (double)clk / (NIT * (c.mode == 3 ? 12 : (c.mode == 4 || c.mode == 5) ? 6 : 8));
-    printf("mode %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
-           c.mode, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
+    printf("mode %d inter %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
+           c.mode, c.inter, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
            (128.0 * 32 + c.n * 32.0) / per);
   }
   return 0;
