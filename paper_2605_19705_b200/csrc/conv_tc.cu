@@ -30,6 +30,21 @@
 
 namespace ideq {
 
+// Bisection switches for timing studies only (tools/build_variant.sh, tools/run_gpu_s2j.sh ->
+// profiles/r2c_conv_bisect.txt; results are NOT correct with any of them on, the product build
+// leaves them 0): TCX_NO_EPI -- the epilogue only hands the accumulator back (no TMEM loads, math
+// or stores); TCX_NO_B -- streamed weights are neither loaded nor waited for; TCX_NO_A -- the input
+// boxes are not loaded (the producer arrives without data).
+#ifndef TCX_NO_EPI
+#define TCX_NO_EPI 0
+#endif
+#ifndef TCX_NO_B
+#define TCX_NO_B 0
+#endif
+#ifndef TCX_NO_A
+#define TCX_NO_A 0
+#endif
+
 // ------------------------------------------------------------------ PTX helpers
 // ------------------------------------------------------------------ kernel
 struct TcParams {
@@ -217,9 +232,13 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
         mbar_wait(empty0 + 8u * s, ph ^ 1u);
         if (elect_one()) {
           if (HALO) {
-            mbar_expect_tx(full0 + 8u * s, P.a_bytes);
-            tma_load_5d(sA + s * op_a, &tmA, full0 + 8u * s, kb * (KB / ES), w0 - 1, 0, h0 - 1, img);
-            if (MODE == 2) {  // this chunk's 9 weight boxes (hi, lo) through the B ring
+            if (TCX_NO_A) {
+              mbar_arrive(full0 + 8u * s);
+            } else {
+              mbar_expect_tx(full0 + 8u * s, P.a_bytes);
+              tma_load_5d(sA + s * op_a, &tmA, full0 + 8u * s, kb * (KB / ES), w0 - 1, 0, h0 - 1, img);
+            }
+            if (MODE == 2 && !TCX_NO_B) {  // this chunk's 9 weight boxes (hi, lo) through the B ring
               for (int tap = 0; tap < 9; ++tap) {
                 mbar_wait(emptyB0 + 8u * sb, phb ^ 1u);
                 mbar_expect_tx(fullB0 + 8u * sb, P.b_bytes * NBUF);
@@ -342,7 +361,7 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
             const uint64_t ad = dh + ((p0 * (uint32_t)KB) >> 4);
             uint64_t bd;
             if (STREAMB) {
-              mbar_wait(fullB0 + 8u * sb, phb);
+              if (!TCX_NO_B) mbar_wait(fullB0 + 8u * sb, phb);
               tc_fence_after();
               bd = dB0 + (((uint32_t)sb * bslot) >> 4);
             } else {
@@ -351,7 +370,7 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
             const int i = ch * 9 + tap;
             mma_k(d_base + (uint32_t)((i % G) * BN), ad, bd, (uint32_t)(i >= G));
             if (STREAMB) {
-              mma_commit_elect(emptyB0 + 8u * sb);
+              if (!TCX_NO_B) mma_commit_elect(emptyB0 + 8u * sb);
               if (++sb == SB) { sb = 0; phb ^= 1u; }
             }
           }
@@ -403,6 +422,14 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
       }
       mbar_wait(tfull0 + 8u * acc, aph);
       tc_fence_after();
+      if (TCX_NO_EPI) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
+        if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals
+        if (++acc == NA) { acc = 0; aph ^= 1u; }
+        continue;
+      }
       if (EPI == EPI_IMG) {
         // image planes straight from TMEM: the warps of the first column half own columns 0..15
         if (half == 0) {

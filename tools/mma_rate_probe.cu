@@ -41,7 +41,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 constexpr int NIT = 512;
 // layout 4 = SW64 (64-byte rows), 2 = SW128 (128-byte rows); rotD / rotA: cycle 4 accumulators /
 // 4 A tiles per group of 8 MMAs; shift: A start + 1 row; data: fill value of the operands
-__global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, int inter, long long* out) {
+__global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, int inter, int sboA,
+                      long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
   unsigned char* g = sm + (base - smem_u32(sm));
@@ -78,7 +79,10 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
     const uint32_t idesc = make_idesc_bf16(n);
     const uint64_t bd = make_sdesc(base + 64u * 1024u, sbo, (uint32_t)layout);
     uint64_t ad[4];
-    for (int t = 0; t < 4; ++t) ad[t] = make_sdesc(base + (uint32_t)t * 128u * rowb + (uint32_t)shift * rowb, sbo, (uint32_t)layout);
+    // sboA != 0: A's 8-row core groups sboA bytes apart (the halo tiles' (Wt + 2) x row bytes)
+    const uint32_t sa = sboA ? (uint32_t)sboA : sbo;
+    for (int t = 0; t < 4; ++t)
+      ad[t] = make_sdesc(base + (uint32_t)t * (sboA ? 2048u : 128u * rowb) + (uint32_t)shift * rowb, sa, (uint32_t)layout);
     const uint32_t dstep = n <= 128 ? 128u : 256u;
     const long long t0 = clock64();
     for (int it = 0; it < NIT; ++it) {
@@ -175,7 +179,11 @@ int main() {
   long long* d;
   cudaMalloc(&d, 16);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 4096);
-  struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; } cases[] = {
+  struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; int sboA; } cases[] = {
+      // halo-tile A operands: core groups (Wt + 2) rows apart (SW128: 1280 B, SW64: 640 B), starts shifted by 0..2 rows
+      {2, 128, 0, 0, 1, 1u, 0, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 0, 1280}, {2, 128, 1, 0, 1, 1u, 0, 0, 1280},
+      {2, 128, 2, 0, 1, 1u, 0, 0, 1280}, {2, 64, 0, 0, 1, 1u, 0, 0, 0}, {2, 64, 1, 0, 1, 1u, 0, 0, 1280},
+      {4, 32, 0, 0, 1, 1u, 0, 0, 0}, {4, 32, 1, 0, 1, 1u, 0, 0, 640}, {4, 96, 1, 0, 1, 1u, 0, 0, 640},
       // concurrent traffic from 3 other warps (inter 1..5) during N = 96 / 128 MMAs, D fixed (columns 0..N-1)
       {4, 96, 0, 0, 1, 1u, 0, 0}, {4, 96, 0, 0, 1, 1u, 0, 1}, {4, 96, 0, 0, 1, 1u, 0, 2}, {4, 96, 0, 0, 1, 1u, 0, 3},
       {4, 96, 0, 0, 1, 1u, 0, 4}, {4, 96, 0, 0, 1, 1u, 0, 5}, {4, 96, 0, 0, 1, 1u, 4, 0}, {4, 96, 0, 0, 1, 1u, 4, 5},
@@ -196,15 +204,15 @@ int main() {
   };
   for (auto& c : cases) {
     for (int rep = 0; rep < 2; ++rep) {
-      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, d);
+      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, c.sboA, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
     }
     long long clk;
     cudaMemcpy(&clk, d, 8, cudaMemcpyDeviceToHost);
     const double per = (double)clk / (NIT * (c.mode == 3 ? 12 : (c.mode == 4 || c.mode == 5) ? 6 : 8));
-    printf("mode %d inter %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
-           c.mode, c.inter, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
+    printf("sboA %4d mode %d inter %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
+           c.sboA, c.mode, c.inter, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
            (128.0 * 32 + c.n * 32.0) / per);
   }
   return 0;
