@@ -56,6 +56,8 @@ struct TcParams {
   uint32_t halo_stage;     // HALO: bytes of one (Wt+2) x (R+2) x KC halo buffer (1 KB aligned)
   int stagesB;             // MODE 2: depth of the weight ring
   int nacc;                // TMEM accumulator stages (2..8)
+  int nepi;                // epilogue staging buffers (<= nacc): tile k uses accumulator k % nacc and
+                           // buffer k % nepi
   int nsplit;              // 3xTF32: partial accumulators per tile (summed in fp32 by the epilogue)
   // EPI_IMG: the first img_c GEMM columns are an image (tail / head adjoint); written as fp32
   // NCHW planes [N][img_c][OH][OW] plus img_alpha * img_aux (same layout, may be null)
@@ -150,8 +152,9 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
   const uint32_t sAlo = sA + S * op_a;
   const uint32_t sB = sA + S * op_a * NBUF;
   const uint32_t sE = (MODE == 1) ? sB : sB + (STREAMB ? SB : S) * bslot;
-  const int NA = P.nacc;  // TMEM accumulator stages (each with its own epilogue buffer)
-  const uint32_t sBar = sE + (uint32_t)NA * epi_stage;
+  const int NA = P.nacc;  // TMEM accumulator stages
+  const int NE = P.nepi;  // epilogue buffers
+  const uint32_t sBar = sE + (uint32_t)NE * epi_stage;
   uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + (sBar - base));
   // barriers: full[S], empty[S], tfull[NA], tempty[NA], auxfull[NA], epifree[NA], wfull, fullB[SB],
   // emptyB[SB], split[S] (3xTF32: the A tile of stage s is split)
@@ -308,7 +311,7 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
           }
         }
         __syncwarp();
-        if (++acc == NA) { acc = 0; aph ^= 1u; }
+        if (++acc == NE) { acc = 0; aph ^= 1u; }  // (aux producer: epilogue buffers)
       }
     }
   } else if (warp == 1) {
@@ -409,16 +412,16 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
     const uint32_t arrivals = P.slab_mode ? 1u : 4u;
     // slab origin inside the tile (pixel rows of the M tile are row-major R x Wt)
     const int sh = (quad * 32) / g.Wt, sw = (quad * 32) % g.Wt;
-    int acc = 0, prev_acc = -1;
-    uint32_t aph = 0;
+    int acc = 0, eb = 0, prev_eb = -1;  // accumulator stage, epilogue buffer
+    uint32_t aph = 0, eph = 0;
     for (int L = t0; L < tot_it; L += tstep) {
       const TileIdx ti = tile_index(P, live_tile(P, L));
       const int img = ti.img, h0 = ti.h0, w0 = ti.w0, nt = ti.nt;
-      const uint32_t ebuf = sE + acc * epi_stage;
+      const uint32_t ebuf = sE + eb * epi_stage;
       if (HAS_AUX) {
-        mbar_wait(auxfull0 + 8u * acc, aph);
+        mbar_wait(auxfull0 + 8u * eb, eph);
       } else {
-        mbar_wait(epifree0 + 8u * acc, aph ^ 1u);
+        mbar_wait(epifree0 + 8u * eb, eph ^ 1u);
       }
       mbar_wait(tfull0 + 8u * acc, aph);
       tc_fence_after();
@@ -426,8 +429,9 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-        if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals
+        if (qleader) mbar_arrive(epifree0 + 8u * eb);  // 4 arrivals
         if (++acc == NA) { acc = 0; aph ^= 1u; }
+        if (++eb == NE) { eb = 0; eph ^= 1u; }
         continue;
       }
       if (EPI == EPI_IMG) {
@@ -451,8 +455,9 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty0 + 8u * acc);
-        if (qleader) mbar_arrive(epifree0 + 8u * acc);  // 4 arrivals, nothing stored through smem
+        if (qleader) mbar_arrive(epifree0 + 8u * eb);  // 4 arrivals, nothing stored through smem
         if (++acc == NA) { acc = 0; aph ^= 1u; }
+        if (++eb == NE) { eb = 0; eph ^= 1u; }
         continue;
       }
       const int G = X3 ? P.nsplit : 1;
@@ -541,17 +546,23 @@ __global__ void __launch_bounds__(X3 ? TC_THREADS_X3 : TC_THREADS, X3 ? 1 : 2)
         }
         bulk_commit();
         // release the previous tile's buffer once its stores have been read
-        if (prev_acc >= 0) {
-          asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-          mbar_arrive_n(epifree0 + 8u * prev_acc, arrivals);
+        if (NE == 1) {  // one buffer: released as soon as this tile's stores have read it
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive_n(epifree0, arrivals);
+        } else {
+          if (prev_eb >= 0) {
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            mbar_arrive_n(epifree0 + 8u * prev_eb, arrivals);
+          }
+          prev_eb = eb;
         }
-        prev_acc = acc;
       }
       if (++acc == NA) { acc = 0; aph ^= 1u; }
+      if (++eb == NE) { eb = 0; eph ^= 1u; }
     }
     if (storer) {
       bulk_wait0();
-      if (prev_acc >= 0) mbar_arrive_n(epifree0 + 8u * prev_acc, arrivals);
+      if (prev_eb >= 0) mbar_arrive_n(epifree0 + 8u * prev_eb, arrivals);
     }
   }
   tc_fence_before();
@@ -971,7 +982,7 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, bool x3, const void* in, const void* 
   // MODE 2: a weight ring of SB slots (one (chunk, tap) box pair each) next to the halo ring
   const int SBq = x3 ? 3 : 6;
   const bool streamb = p->halo == 2;
-  const size_t bring = streamb ? (size_t)SBq * bslot : 0;
+  size_t bring = streamb ? (size_t)SBq * bslot : 0;
   P.stagesB = streamb ? SBq : 0;
   const size_t op_stage = p->halo ? (size_t)P.halo_stage * nbuf : a_stage * nbuf + bslot;
   // short-K layers (the 2x2 up / down scatters: 1-2 K-blocks per tile) are bound by the per-tile
@@ -1001,10 +1012,21 @@ TcPlan* tc_make_plan(const ConvGeom& g_in, bool x3, const void* in, const void* 
     }
   }
   if (!stages) { snprintf(err, errlen, "tcgen05 conv: shared memory plan failed"); delete p; return nullptr; }
+  // streamed-weight layers (bf16): one epilogue buffer (released as soon as its TMA stores have read
+  // it) and the freed shared memory added to the weight ring -- the ring's lookahead in time is what
+  // bounds these layers (profiles/r2c_conv_bisect.txt: the weight stream costs ~5 us per launch)
+  int nepi = nacc;
+  if (streamb && !x3 && ctas == 1 && nacc >= 2) {
+    nepi = 1;
+    const int extra = (int)(((size_t)(nacc - 1) * e_stage) / bslot);
+    P.stagesB = SBq + extra > 12 ? 12 : SBq + extra;
+    bring = (size_t)P.stagesB * bslot;
+  }
   P.stages = stages;
   P.nacc = nacc;
+  P.nepi = nepi;
   P.tmem_cols = tcols;
-  p->smem = 1024 + (size_t)nacc * e_stage + wbytes + bring + nbar + (size_t)stages * op_stage;
+  p->smem = 1024 + (size_t)nepi * e_stage + wbytes + bring + nbar + (size_t)stages * op_stage;
   const int total = P.m_tiles * P.n_tiles;
   const int maxg = num_sms * ctas;
   p->grid = total < maxg ? total : maxg;
