@@ -42,7 +42,7 @@ constexpr int NIT = 512;
 // layout 4 = SW64 (64-byte rows), 2 = SW128 (128-byte rows); rotD / rotA: cycle 4 accumulators /
 // 4 A tiles per group of 8 MMAs; shift: A start + 1 row; data: fill value of the operands
 __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t data, int mode, int inter, int sboA,
-                      long long* out) {
+                      const uint4* __restrict__ gsrc, long long* out) {
   extern __shared__ __align__(1024) unsigned char sm[];
   const uint32_t base = (smem_u32(sm) + 1023u) & ~1023u;
   unsigned char* g = sm + (base - smem_u32(sm));
@@ -126,6 +126,33 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
     // 1 = tcgen05.ld 16 columns + wait, 2 = st.shared 16 B per lane, 3 = tcgen05.st 8 zero columns
     // + wait, 4 = ld.shared 16 B per lane, 5 = 1 + 2 (an epilogue's mix)
     const int w = threadIdx.x >> 5, ln = threadIdx.x & 31;
+    if (inter == 8 || inter == 9) {  // warp 1: bulk copies global -> shared (8: 16 KB, 9: 4 KB per copy) into scratch
+      __shared__ __align__(8) uint64_t cbar;
+      const uint32_t bytes = inter == 8 ? 16384u : 4096u;
+      if (w == 1) {
+        const uint32_t b = smem_u32(&cbar);
+        if (ln == 0) {
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+          asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+        uint32_t ph = 0;
+        long long nb = 0;
+        while (!stop_flag) {
+          if (ln == 0) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+            asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                         ::"r"(base + 100u * 1024u - 16384u + 0u), "l"(gsrc + (nb & 63) * 1024), "r"(bytes), "r"(b) : "memory");
+            asm volatile("{\n\t.reg .pred p;\nWC_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WC_%=;\n}\n" ::"r"(b), "r"(ph) : "memory");
+          }
+          __syncwarp();
+          ph ^= 1u;
+          ++nb;
+        }
+        if (ln == 0 && blockIdx.x == 0) out[1] = nb;
+      }
+      return;
+    }
     if (inter >= 6) {  // 6: warps 4, 8, 12 (the MMA warp's scheduler) run FMA / SFU math; 7: the other warps do
       const bool busy = inter == 6 ? (w % 4 == 0) : (w % 4 != 0);
       float x = (float)ln * 1e-3f, y = 1.f;
@@ -178,9 +205,13 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
 int main() {
   long long* d;
   cudaMalloc(&d, 16);
+  uint4* gsrc;
+  cudaMalloc(&gsrc, 64 * 16384 + 16384);
+  cudaMemset(gsrc, 0, 64 * 16384 + 16384);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 4096);
   struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; int sboA; } cases[] = {
       // halo-tile A operands: core groups (Wt + 2) rows apart (SW128: 1280 B, SW64: 640 B), starts shifted by 0..2 rows
+      {2, 128, 0, 0, 1, 1u, 0, 8, 0}, {2, 128, 0, 0, 1, 1u, 0, 9, 0}, {4, 96, 0, 0, 1, 1u, 0, 8, 0}, {4, 64, 0, 0, 1, 1u, 0, 8, 0},
       {2, 128, 0, 0, 1, 1u, 0, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 0, 1280}, {2, 128, 1, 0, 1, 1u, 0, 0, 1280},
       {2, 128, 2, 0, 1, 1u, 0, 0, 1280}, {2, 64, 0, 0, 1, 1u, 0, 0, 0}, {2, 64, 1, 0, 1, 1u, 0, 0, 1280},
       {4, 32, 0, 0, 1, 1u, 0, 0, 0}, {4, 32, 1, 0, 1, 1u, 0, 0, 640}, {4, 96, 1, 0, 1, 1u, 0, 0, 640},
@@ -204,12 +235,14 @@ int main() {
   };
   for (auto& c : cases) {
     for (int rep = 0; rep < 2; ++rep) {
-      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, c.sboA, d);
+      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, c.sboA, gsrc, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
     }
-    long long clk;
+    long long clk, nb = 0;
     cudaMemcpy(&clk, d, 8, cudaMemcpyDeviceToHost);
+    if (c.inter == 8 || c.inter == 9) cudaMemcpy(&nb, d + 1, 8, cudaMemcpyDeviceToHost);
+    if (nb) printf("  (bulk copies during the run: %lld, %.1f B/clk)\n", nb, (double)nb * (c.inter == 8 ? 16384 : 4096) / clk);
     const double per = (double)clk / (NIT * (c.mode == 3 ? 12 : (c.mode == 4 || c.mode == 5) ? 6 : 8));
     printf("sboA %4d mode %d inter %d %s N=%3d shift=%d rotD=%d rotA=%d data=%s : %6.1f clk/MMA (tensor floor %5.1f), operand B/clk %6.1f\n",
            c.sboA, c.mode, c.inter, c.layout == 4 ? "SW64 " : "SW128", c.n, c.shift, c.rotD, c.rotA, c.data == 1u ? "rand " : c.data ? "1/128" : "zero ", per, c.n / 2.0,
