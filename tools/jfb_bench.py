@@ -5,8 +5,10 @@ residual, the two-stream forward with tape, the reverse with weight gradients, t
 Timed with CUDA events around the synchronous call, after warm-up (the call's tape cudaMallocs
 are inside the timed region: this is the user-visible call latency). Algorithmic FLOPs: F = one
 forward of the U-Net convolutions on the batch; the call issues ~8F (grad g = forward + VJP = 2F,
-two-stream forward 2F, two-stream adjoints 2F, two-stream weight gradients 2F), all fp32 FFMA;
-the FFMA peak is derived as 148 SMs x 128 lanes x 2 FLOP x 1965 MHz = 74.4 TFLOP/s.
+two-stream forward 2F, two-stream adjoints 2F, two-stream weight gradients 2F). In the fp32 mode
+the U-Net convolutions of grad g and of the two-stream passes run on tcgen05 (3xTF32) and the weight
+gradients on FFMA; `frac` is quoted against the derived FFMA peak (148 SMs x 128 lanes x 2 FLOP x
+1965 MHz = 74.4 TFLOP/s) for comparability with the round-1 lines, where every pass was FFMA.
 The oracle (oracle/jfb.py, fp64, 1 image) is timed beside it on the host.
 
 usage: python tools/jfb_bench.py [--config C3] [--batch 4] [--steps 5] [--warmup 2]
