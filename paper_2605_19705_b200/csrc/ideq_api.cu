@@ -128,6 +128,7 @@ struct ideq_ctx {
   float* jfb_ws = nullptr;
   size_t jfb_ws_n = 0;
   std::map<std::string, std::vector<uint32_t>> jfb_map;  // operand index -> blob index per layer
+  std::map<std::string, TcPlan*> jfb_plans;  // 3xTF32 tcgen05 plans of the JFB passes (keyed by geometry + buffers)
   cudaStream_t stream = nullptr;
   ideq_precision prec = IDEQ_PREC_FP32;
   ideq_net_desc net{};
@@ -1954,8 +1955,46 @@ struct JfbRun {
     dims(kind, ws.t[wname].second, ncols, ktap, cin);
     return make_geom(kind, N, Hin, Win, cin, ncols, pick_kc(false, ktap), ktap, epi);
   }
+  // One layer of the two-stream passes. With the tensor-core fp32 mode (3xTF32) the layer runs on
+  // the solver's own tcgen05 kernel (same GEMM operands, hi / lo tf32 halves); the plan binds the
+  // tape buffers, which keep their addresses across calls (the pool hands out the same blocks), so
+  // it is built once per (layer, buffers). Otherwise the FFMA implicit GEMM.
   void conv(const std::string& wname, int kind, int Hin, int Win, const float* in, float* out, const float* aux,
             int epi) {
+    if (use_x3(ctx)) {
+      char key[256];
+      snprintf(key, sizeof(key), "%s#%d#%d#%d#%d#%d#%p#%p#%p", wname.c_str(), kind, N, Hin, Win, epi, (const void*)in,
+               (const void*)out, (const void*)aux);
+      auto it = ctx->jfb_plans.find(key);
+      if (it == ctx->jfb_plans.end()) {
+        int ncols, ktap, cin;
+        dims(kind, ws.t[wname].second, ncols, ktap, cin);
+        const ConvGeom g = make_geom(kind, N, Hin, Win, cin, ncols, pick_kc(true, true, ktap), ktap, epi);
+        TcPlan* plan = nullptr;
+        if (tc_supported(g, true)) {
+          const std::string wk = wname + "#" + std::to_string(kind) + "x3";
+          if (!ctx->wdev.count(wk)) {  // hi / lo tf32 halves of the GEMM operand
+            auto& sl = ws.t[wname];
+            int nc, nt, kt;
+            std::vector<float> B = gemm_weights(kind, ctx->blob.data() + sl.first, sl.second, g.KC, nc, nt, kt);
+            std::vector<float> lo(B.size());
+            for (size_t i = 0; i < B.size(); ++i) {
+              const float h = tf32_rna(B[i]);
+              lo[i] = tf32_rna(B[i] - h);
+              B[i] = h;
+            }
+            if (upload_gemm_weights(ctx, wk + "#lo", lo) || upload_gemm_weights(ctx, wk, B)) { st = IDEQ_E_CUDA; return; }
+          }
+          char err[256] = {0};
+          plan = tc_make_plan(g, true, in, ctx->wdev[wk], ctx->wdev[wk + "#lo"], out, aux, ctx->num_sms, err, sizeof(err));
+        }
+        it = ctx->jfb_plans.emplace(key, plan).first;  // null: geometry the tensor-core path does not take
+      }
+      if (it->second) {
+        tc_launch(it->second, s);
+        return;
+      }
+    }
     ConvGeom g = geom(wname, kind, Hin, Win, epi);
     const float* w = weights(wname, kind, g.KC);
     if (w) launch_conv_simt<float>(g, in, w, out, aux, s);
@@ -2438,6 +2477,7 @@ void ideq_destroy(ideq_ctx* ctx) {
   for (auto& kv : ctx->progs)
     for (auto& L : kv.second.layers) { if (L.plan) tc_free_plan(L.plan); if (L.i2f) img2feat_free_plan(L.i2f); if (L.rbf) rbf_free_plan(L.rbf); }
   for (auto& a : ctx->allocs) cudaFree(a.p);
+  for (auto& kv : ctx->jfb_plans) tc_free_plan(kv.second);
   for (auto& b : ctx->jfb_pool) cudaFree(b.first);
   if (ctx->jfb_ws) cudaFree(ctx->jfb_ws);
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
