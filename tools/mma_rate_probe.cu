@@ -153,7 +153,7 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
       }
       return;
     }
-    if (inter >= 6) {  // 6: warps 4, 8, 12 (the MMA warp's scheduler) run FMA / SFU math; 7: the other warps do
+    if (inter == 6 || inter == 7) {  // 6: warps 4, 8, 12 (the MMA warp's scheduler) run FMA / SFU math; 7: the other warps do
       const bool busy = inter == 6 ? (w % 4 == 0) : (w % 4 != 0);
       float x = (float)ln * 1e-3f, y = 1.f;
       while (busy && !stop_flag) {
@@ -168,12 +168,13 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
       if (y == 12345.f) out[1] = 1;
       return;
     }
-    const uint32_t ta = tmem + ((uint32_t)(w * 32) << 16) + 256u;
-    const uint32_t sa = base + 96u * 1024u + (uint32_t)w * 512u + (uint32_t)ln * 16u;
+    if (inter == 10 && w < 4) return;  // 10: warps 4..19 (every scheduler, 16 warps) run the mix of 5 plus TMEM stores
+    const uint32_t ta = tmem + ((uint32_t)((w & 3) * 32) << 16) + 256u + (uint32_t)((w >> 2) & 3) * 64u;
+    const uint32_t sa = base + 96u * 1024u + (uint32_t)(w & 7) * 512u + (uint32_t)ln * 16u;
     uint32_t acc = 0;
     while (!stop_flag) {
       for (int r = 0; r < 16; ++r) {
-        if (inter == 1 || inter == 5) {
+        if (inter == 1 || inter == 5 || inter == 10) {
           uint32_t v[16];
           asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
@@ -182,9 +183,9 @@ __global__ void probe(int layout, int n, int shift, int rotD, int rotA, uint32_t
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           for (int e = 0; e < 16; ++e) acc += v[e];
         }
-        if (inter == 2 || inter == 5)
+        if (inter == 2 || inter == 5 || inter == 10)
           asm volatile("st.shared.v4.b32 [%0], {%1, %1, %1, %1};" ::"r"(sa), "r"(acc) : "memory");
-        if (inter == 3) {
+        if (inter == 3 || inter == 10) {
           asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(ta), "r"(0u) : "memory");
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
@@ -211,6 +212,7 @@ int main() {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 4096);
   struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; int sboA; } cases[] = {
       // halo-tile A operands: core groups (Wt + 2) rows apart (SW128: 1280 B, SW64: 640 B), starts shifted by 0..2 rows
+      {4, 96, 0, 0, 1, 1u, 0, 10, 0}, {4, 96, 0, 0, 1, 1u, 4, 10, 0}, {2, 128, 0, 0, 1, 1u, 0, 10, 0},
       {2, 128, 0, 0, 1, 1u, 0, 8, 0}, {2, 128, 0, 0, 1, 1u, 0, 9, 0}, {4, 96, 0, 0, 1, 1u, 0, 8, 0}, {4, 64, 0, 0, 1, 1u, 0, 8, 0},
       {2, 128, 0, 0, 1, 1u, 0, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 0, 1280}, {2, 128, 1, 0, 1, 1u, 0, 0, 1280},
       {2, 128, 2, 0, 1, 1u, 0, 0, 1280}, {2, 64, 0, 0, 1, 1u, 0, 0, 0}, {2, 64, 1, 0, 1, 1u, 0, 0, 1280},
@@ -235,7 +237,7 @@ int main() {
   };
   for (auto& c : cases) {
     for (int rep = 0; rep < 2; ++rep) {
-      probe<<<148, c.inter >= 6 ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, c.sboA, gsrc, d);
+      probe<<<148, c.inter == 10 ? 640 : (c.inter == 6 || c.inter == 7) ? 512 : 128, 100 * 1024 + 4096>>>(c.layout, c.n, c.shift, c.rotD, c.rotA, c.data, c.mode, c.inter, c.sboA, gsrc, d);
       cudaError_t e = cudaDeviceSynchronize();
       if (e != cudaSuccess) { printf("error: %s\n", cudaGetErrorString(e)); return 1; }
     }
