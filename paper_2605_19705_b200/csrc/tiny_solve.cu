@@ -15,6 +15,8 @@
 // publishes a tensor and completes every halo -- no copy phase. Cheap layers are recomputed on the
 // halo rows instead of exchanged (a1 and U on rows -1 and R), which removes two of the barriers,
 // and the residual's barrier also completes the next iteration's z halos: 5 per iteration. The
+// first barrier is split: its arrive follows the pushed A z - y rows, and a1 (local) is computed
+// before the wait. The
 // residual's three partial sums are pushed into every CTA and summed in fp64 by a fixed butterfly,
 // so all P CTAs take the identical stop decision.
 //
@@ -60,6 +62,12 @@ __device__ __forceinline__ float ts_ld_cluster(uint32_t a) {
 }
 __device__ __forceinline__ void ts_st_cluster(uint32_t a, float v) {
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void ts_cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void ts_cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void ts_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -262,8 +270,22 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
   ts_cluster_sync();  // z^0 (own rows + pushed halos) complete on every CTA
   for (int k = 0; k < A.max_iter; ++k) {
     TS_MARK(0)
-    // [1] a1 = sp(c1(z)) on rows -1 .. R (the halo rows recomputed locally; zero outside the image);
-    //     rb = A z - y (true periodic convolution, reading Q8), pushed to the neighbours' halos
+    // [1] rb = A z - y (true periodic convolution, reading Q8), pushed to the neighbours' halos, and
+    //     the cluster barrier's arrive; then a1 = sp(c1(z)) on rows -1 .. R (the halo rows recomputed
+    //     locally; zero outside the image), which needs no neighbour, while the barrier completes
+    if (act_k) {  // kernel rows i = qk, qk + 4, ...: (A z)[r][c] = sum k[i][j] z[r - i + kc][c - j + kc]
+      float s = 0.f;
+#pragma unroll
+      for (int i = qk; i < ks; i += 4) {
+        const float* zr = sm + L.b_at(L.z, rk - i + kc, ck + kc);
+        const float* kr = sm + L.kern + i * ks;
+#pragma unroll
+        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], zr[-j], s);
+      }
+      s = ts_sum4(s);
+      if (qk == 0) ts_put_blur<P>(sm, L, L.rb, rk, ck, s - sm[L.y + pk], rank, base);
+    }
+    ts_cluster_arrive();  // [S1] rb halos published
     for (int t = threadIdx.x; t < (R + 2) * W * 4; t += TS_T) {
       const int p = t % ((R + 2) * W), q = t / ((R + 2) * W);
       const int r = p / W - 1, c = p % W;
@@ -282,20 +304,9 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) sm[L.n_at(L.a1, 4 * q + e, r, c)] = inside ? ts_softplus(acc[e]) : 0.f;
     }
-    if (act_k) {  // kernel rows i = qk, qk + 4, ...: (A z)[r][c] = sum k[i][j] z[r - i + kc][c - j + kc]
-      float s = 0.f;
-#pragma unroll
-      for (int i = qk; i < ks; i += 4) {
-        const float* zr = sm + L.b_at(L.z, rk - i + kc, ck + kc);
-        const float* kr = sm + L.kern + i * ks;
-#pragma unroll
-        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], zr[-j], s);
-      }
-      s = ts_sum4(s);
-      if (qk == 0) ts_put_blur<P>(sm, L, L.rb, rk, ck, s - sm[L.y + pk], rank, base);
-    }
+    __syncthreads();  // a1 was written after this CTA's arrive: the barrier does not order it
     TS_MARK(1)
-    ts_cluster_sync();  // [S1] rb halos (a1 is local)
+    ts_cluster_wait();  // [S1] rb halos complete
     TS_MARK(2)
     // [2] a2 = sp(c2(a1)) (blocked threads), pushed with a 2-row halo; gf = A^T rb (the others)
     float acc[2][4];
