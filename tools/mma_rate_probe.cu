@@ -212,6 +212,8 @@ int main() {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024 + 4096);
   struct Case { int layout, n, shift, rotD, rotA; uint32_t data; int mode; int inter; int sboA; } cases[] = {
       // halo-tile A operands: core groups (Wt + 2) rows apart (SW128: 1280 B, SW64: 640 B), starts shifted by 0..2 rows
+      {2, 192, 0, 0, 1, 1u, 0, 0, 0}, {2, 160, 0, 0, 1, 1u, 0, 0, 0}, {2, 224, 0, 0, 1, 1u, 0, 0, 0},
+      {2, 256, 0, 0, 1, 1u, 0, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 0, 0}, {2, 64, 0, 0, 1, 1u, 0, 0, 0},
       {4, 96, 0, 0, 1, 1u, 0, 10, 0}, {4, 96, 0, 0, 1, 1u, 4, 10, 0}, {2, 128, 0, 0, 1, 1u, 0, 10, 0},
       {2, 128, 0, 0, 1, 1u, 0, 8, 0}, {2, 128, 0, 0, 1, 1u, 0, 9, 0}, {4, 96, 0, 0, 1, 1u, 0, 8, 0}, {4, 64, 0, 0, 1, 1u, 0, 8, 0},
       {2, 128, 0, 0, 1, 1u, 0, 0, 0}, {2, 128, 0, 0, 1, 1u, 0, 0, 1280}, {2, 128, 1, 0, 1, 1u, 0, 0, 1280},
