@@ -27,9 +27,10 @@
 // are planes of (R + 2 kc) rows x (W + 2 kc) columns with PERIODIC borders (the blur is a circular
 // convolution, reading Q9); c1 reads z through an explicit zero-padding mask. The 16 -> 16
 // convolutions give a work item 2 rows x 4 output channels (register blocking: 12 input and 9
-// weight loads per 72 FMAs), split over 2 threads by input channel when R = 2 leaves too few items;
-// the single-channel outputs and the blur split the contraction over adjacent lanes, combined by
-// fixed-order shuffles. x^k and the candidate x^{k+1} are ping-pong planes.
+// weight loads per 72 FMAs), split over all 512 threads by input channel (4 K parts at R = 2, 2 at
+// R = 4) whose partial sums meet in shared memory, every thread finishing 8 / ksplit outputs (the
+// blur adjoint A^T rb moved to stage [4], whose q2 items leave threads idle); the single-channel
+// outputs and the blur split the contraction over adjacent lanes, combined by fixed-order shuffles. x^k and the candidate x^{k+1} are ping-pong planes.
 //
 // Measured (B200, C1, tools/tiny_prof.cu): 18.8 us per iteration with 8-CTA clusters -> 12.9 us
 // with 16-CTA clusters, conflict-free channel planes, the unrolled 9x9 blur and SFU softplus.
@@ -255,12 +256,15 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
   }
   int iters = 0, status = 1;
   float res = __int_as_float(0x7fc00000);
-  // blocked 16 -> 16 stages: item -> (column, row pair, channel quarter), ksplit threads per item
-  const int nb = W * (R / 2) * 4;  // blocked items
-  const int ksplit = nb <= TS_T / 4 ? 2 : 1, nkb = nb * ksplit;
+  // blocked 16 -> 16 stages: item -> (column, row pair, channel quarter); every thread of the CTA
+  // takes part: ksplit = TS_T / nb threads per item (4 at R x W = 64, 2 at 128), each over
+  // 16 / ksplit input channels, and each finishes 8 / ksplit of the item's 8 outputs
+  const int nb = W * (R / 2) * 4;  // blocked items (R x W <= 128: nb <= TS_T / 2)
+  const int ksplit = TS_T / nb;
   const int tb = threadIdx.x % nb, kh = threadIdx.x / nb;  // item, K part
   const int cb = tb % W, rb0 = 2 * ((tb / W) % (R / 2)), qb = tb / (W * (R / 2));
   const int ci0 = kh * (TS_C / ksplit), nci = TS_C / ksplit;
+  const int nout = 8 / ksplit;  // outputs i = kh * nout .. (kh + 1) * nout - 1 (row i / 4, channel 4 qb + i % 4)
   // split-K stages: 4 lanes per pixel
   const int pk = threadIdx.x >> 2, qk = threadIdx.x & 3;
   const int rk = pk / W, ck = pk % W;
@@ -308,38 +312,20 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
     TS_MARK(1)
     ts_cluster_wait();  // [S1] rb halos complete
     TS_MARK(2)
-    // [2] a2 = sp(c2(a1)) (blocked threads), pushed with a 2-row halo; gf = A^T rb (the others)
+    // [2] a2 = sp(c2(a1)) (blocked threads, split over the input channels), pushed with a 2-row
+    //     halo. The K parts' partial sums meet in shared memory and every output is their sum in
+    //     the fixed order part 0 + part 1 + ...
     float acc[2][4];
-    if (threadIdx.x < nkb) {
-      ts_conv16<false>(sm, L, L.a1, L.w2f, rb0, cb, qb, ci0, nci, acc);
-      if (kh == 1) {
+    ts_conv16<false>(sm, L, L.a1, L.w2f, rb0, cb, qb, ci0, nci, acc);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sm[L.part + i * nb + tb] = acc[i >> 2][i & 3];
-      }
-    } else if (threadIdx.x - nkb < 2 * RW) {  // 2 lanes per pixel: (A^T rb)[r][c] = sum k[i][j] rb[r + i - kc][c + j - kc]
-      const int t = threadIdx.x - nkb, p = t >> 1, h = t & 1, r = p / W, c = p % W;
-      float s = 0.f;
-#pragma unroll
-      for (int i = h; i < ks; i += 2) {
-        const float* rr = sm + L.b_at(L.rb, r + i - kc, c - kc);
-        const float* kr = sm + L.kern + i * ks;
-#pragma unroll
-        for (int j = 0; j < ks; ++j) s = fmaf(kr[j], rr[j], s);
-      }
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      if (h == 0) sm[L.gf + p] = s;
-    }
-    if (ksplit > 1) __syncthreads();
-    if (threadIdx.x < nb) {
-      if (ksplit > 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i >> 2][i & 3] += sm[L.part + i * nb + tb];
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          ts_put_net(sm, L, L.n_at(L.a2, 4 * qb + e, rb0 + i, cb), ts_softplus(acc[i][e]), rb0 + i, rank, H, 2, base);
+    for (int i = 0; i < 8; ++i) sm[L.part + (kh * 8 + i) * nb + tb] = acc[i >> 2][i & 3];
+    __syncthreads();
+    for (int j = 0; j < nout; ++j) {
+      const int i = kh * nout + j;
+      float s = sm[L.part + i * nb + tb];
+      for (int h = 1; h < ksplit; ++h) s += sm[L.part + (h * 8 + i) * nb + tb];
+      ts_put_net(sm, L, L.n_at(L.a2, 4 * qb + (i & 3), rb0 + (i >> 2), cb), ts_softplus(s), rb0 + (i >> 2), rank, H,
+                 2, base);
     }
     TS_MARK(3)
     ts_cluster_sync();  // [S2] a2 halos (2 rows)
@@ -360,8 +346,25 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
       if (q == 0) sm[L.n_at(L.u, 0, r, c)] = (row0 + r >= 0 && row0 + r < H) ? s : 0.f;
     }
     __syncthreads();
-    // [4] q2 = c3^T(U) . sp'(a2)   (conv3x3^T: flipped taps), pushed (1-row halo)
-    for (int t = threadIdx.x; t < RW * 4; t += TS_T) {
+    // [4] q2 = c3^T(U) . sp'(a2)   (conv3x3^T: flipped taps), pushed (1-row halo);
+    //     gf = A^T rb on the threads past the q2 items (rb is complete since [S1] and unchanged
+    //     until the next iteration's [1]; gf is read in [6])
+    for (int t = threadIdx.x; t < RW * 6; t += TS_T) {
+      if (t >= RW * 4) {  // warp-uniform (RW is a multiple of 32): 2 lanes per pixel,
+                          // (A^T rb)[r][c] = sum k[i][j] rb[r + i - kc][c + j - kc]
+        const int u = t - RW * 4, p = u >> 1, h = u & 1, r = p / W, c = p % W;
+        float s = 0.f;
+#pragma unroll
+        for (int i = h; i < ks; i += 2) {
+          const float* rr = sm + L.b_at(L.rb, r + i - kc, c - kc);
+          const float* kr = sm + L.kern + i * ks;
+#pragma unroll
+          for (int j = 0; j < ks; ++j) s = fmaf(kr[j], rr[j], s);
+        }
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (h == 0) sm[L.gf + p] = s;
+        continue;
+      }
       const int p = t % RW, q = t / RW, r = p / W, c = p % W;
       float acc[4] = {0.f, 0.f, 0.f, 0.f};
       const float* in = sm + L.n_at(L.u, 0, r, c);
@@ -381,27 +384,17 @@ __global__ void __launch_bounds__(TS_T, 1) tiny_solve_kernel(TinyArgs A) {
     TS_MARK(5)
     ts_cluster_sync();  // [S3] q2 halos
     TS_MARK(6)
-    // [5] q1 = c2^T(q2) . sp'(a1) (blocked threads), pushed (1-row halo)
-    if (threadIdx.x < nkb) {
-      ts_conv16<true>(sm, L, L.q2, L.w2t, rb0, cb, qb, ci0, nci, acc);
-      if (kh == 1) {
+    // [5] q1 = c2^T(q2) . sp'(a1) (blocked threads, split as in [2]), pushed (1-row halo)
+    ts_conv16<true>(sm, L, L.q2, L.w2t, rb0, cb, qb, ci0, nci, acc);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sm[L.part + i * nb + tb] = acc[i >> 2][i & 3];
-      }
-    }
-    if (ksplit > 1) __syncthreads();
-    if (threadIdx.x < nb) {
-      if (ksplit > 1) {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[i >> 2][i & 3] += sm[L.part + i * nb + tb];
-      }
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int o = L.n_at(0, 4 * qb + e, rb0 + i, cb);
-          ts_put_net(sm, L, L.q1 + o, acc[i][e] * ts_dsp(sm[L.a1 + o]), rb0 + i, rank, H, 1, base);
-        }
+    for (int i = 0; i < 8; ++i) sm[L.part + (kh * 8 + i) * nb + tb] = acc[i >> 2][i & 3];
+    __syncthreads();
+    for (int j = 0; j < nout; ++j) {
+      const int i = kh * nout + j;
+      float s = sm[L.part + i * nb + tb];
+      for (int h = 1; h < ksplit; ++h) s += sm[L.part + (h * 8 + i) * nb + tb];
+      const int o = L.n_at(0, 4 * qb + (i & 3), rb0 + (i >> 2), cb);
+      ts_put_net(sm, L, L.q1 + o, s * ts_dsp(sm[L.a1 + o]), rb0 + (i >> 2), rank, H, 1, base);
     }
     TS_MARK(7)
     ts_cluster_sync();  // [S4] q1 halos

@@ -118,6 +118,23 @@ def test_trajectory_fp32(name, K, stress):
     assert np.allclose(tr, orc["rmax_trace"], rtol=1e-3, atol=1e-6)
 
 
+@pytest.mark.parametrize("name,kw", [("C2", dict(H=32, W=32)), ("C3", dict(H=32, W=32)), ("C4", dict()),
+                                     ("C5", dict(H=32, W=32))])
+def test_trajectory_fp32_max_iter(name, kw):
+    """The whole horizon of each config (K = max_iter: 200 / 300 / 300 / 200 operator
+    applications), fp32 mode, images 0 and N-1 of the reduced batch: iterates
+    within 1e-4 relative L2 and residuals within 1e-6 of the oracle at the LAST step, and the
+    max-residual trace along the way. Smaller planes than the K = 10 / 50 cases keep the fp64
+    oracle's 200-300 iterations at about a minute per config."""
+    K = configs.CONFIGS[name]["max_iter"]
+    cfg, prob, x, st, tr, orc = _run_pair(name, "fp32", K, **kw)
+    assert (st["status"] == 1).all() and (st["iters"] == K).all()
+    for b in range(x.shape[0]):
+        assert rel_l2(x[b], orc["x"][b]) <= 1e-4
+        assert abs(st["residual"][b] - orc["residual"][b]) <= 1e-6
+    assert np.allclose(tr, orc["rmax_trace"], rtol=1e-3, atol=1e-6)
+
+
 @pytest.mark.parametrize("name,K", [("C2", 30), ("C3", 30), ("C4", 30), ("C5", 30)])
 @pytest.mark.parametrize("stress", [False, True])
 def test_trajectory_bf16_psnr(name, K, stress):

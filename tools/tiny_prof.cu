@@ -1,6 +1,6 @@
 // Stage profile of the C1 whole-solve kernel: builds tiny_solve.cu with TS_PROF=1 and prints the
 // clock cycles per iteration spent in each stage (CTA 0, thread 0).
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DTS_PROF=1 -I include
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -rdc=true -DTS_PROF=1 -I include
 //        -o tools/tiny_prof tools/tiny_prof.cu paper_2605_19705_b200/csrc/tiny_solve.cu
 #include <cstdio>
 #include <vector>
@@ -32,7 +32,7 @@ int main() {
     if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     long long p[16]; cudaMemcpyFromSymbol(p, ideq::ts_prof, sizeof(p));
-    const char* names[16] = {"(loop top)", "[1] c1+Az", "S1 sync", "[2] c2+ATr", "S2 sync", "[3,4] c3,c3T", "S3 sync", "[5] c2T", "S4 sync", "[6] c1T+upd", "S5 sync (+z)", "accept", "", "", "", ""};
+    const char* names[16] = {"(loop top)", "[1] c1+Az", "S1 sync", "[2] c2", "S2 sync", "[3,4] c3,c3T+ATr", "S3 sync", "[5] c2T", "S4 sync", "[6] c1T+upd", "S5 sync (+z)", "accept", "", "", "", ""};
     printf("total %.1f us per iteration\n", 1000.0 * ms / K);
     for (int i = 0; i < 12; ++i) printf("  %-16s %7.0f clk/iter\n", names[i], (double)p[i] / K);
   }
