@@ -40,13 +40,21 @@
 // them off; tests/test_gpu_rbf.py checks both against the oracle and each other). Serialised and
 // cold under ncu a block takes ~132 us against 131 / 136 us for the two unfused launches: the win
 // is the halved HBM traffic overlapping the neighbours under programmatic dependent launch.
-// What bounds it (tools/rbf_prof.cu stage timeline, tools/mma_rate_probe.cu):
-//   * the MMA stream alone runs at 2.5k clk per row (24 MMAs, ~70 clk each after removing the
-//     branches between tcgen05.mma instructions, which had cost ~150 clk per MMA);
+// What bounds it (tools/rbf_prof.cu stage timeline and its RBF_NO_MMA / RBF_NO_EPI bisection
+// builds, ncu source-level stalls, tools/mma_rate_probe.cu):
+//   * the MMA stream alone (epilogues reduced to their barrier arrivals) takes ~97 us per block,
+//     the epilogues alone (no MMAs) ~101 us (forward) / ~135 us (VJP), the skeleton of barriers
+//     and row loads ~43 us; together 139 / 142 us: the two halves overlap only partly, each
+//     epilogue group waiting most of the time on the MMA commits and the MMA warp on the freed
+//     ring blocks;
+//   * the epilogue's fixed per-row latency: its proxy fence (MEMBAR.ALL.CTA) waits for every
+//     outstanding global access of the thread. Hence the forward's saved activation goes out by
+//     TMA from the u ring (157 -> 139 us) and the VJP's saved-activation rows are bulk-prefetched
+//     into L2 three rows ahead (152 -> 142 us);
 //   * TMEM holds a 4-row ring per stage and M tile at W = 256 (2 stages x 2 tiles x 4 x 32
 //     columns = 512), so a wrapped window must wait until the epilogue has drained the block it
-//     adds +0 to; the two epilogue stages run in separate warp groups so neither waits for the
-//     other's rows.
+//     adds +0 to (issuing it as two MMAs instead measured 2-3% slower); the two epilogue stages
+//     run in separate warp groups so neither waits for the other's rows.
 #include <cuda.h>
 #include <type_traits>
 #include <stdio.h>
@@ -106,6 +114,13 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
       : "memory");
 }
+// timing-only bisection switches (tools/rbf_prof.cu builds; results are garbage when set)
+#ifndef RBF_NO_MMA
+#define RBF_NO_MMA 0
+#endif
+#ifndef RBF_NO_EPI
+#define RBF_NO_EPI 0
+#endif
 #ifndef RBF_TRACE
 #define RBF_TRACE 0
 #endif
@@ -120,9 +135,20 @@ __device__ long long g_rbf_trace[16][256];
   do {                    \
   } while (0)
 #endif
+// forward: the saved activation row leaves shared memory (the u ring slot, already in the act
+// tensor's SW64 layout) by one TMA tensor store per row. Per-thread global stores made the next
+// row's proxy fence (MEMBAR.ALL.CTA + FENCE.VIEW.ASYNC) wait for them to complete: 157 -> 139 us
+// per forward block (tools/rbf_prof.cu)
+__device__ __forceinline__ void tma_store_4d(uint32_t src, const CUtensorMap* map, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(src)
+               : "memory");
+}
 // mbarrier wait that suspends the thread (up to the hint, in ns) instead of spinning: the 16
 // epilogue warps wait most of the time, and spinning try_wait loops take issue slots from the
 // MMA warp that shares their scheduler
+// (a plain try_wait or a test_wait spin measured the same, tools/rbf_prof.cu)
 __device__ __forceinline__ void mbar_wait_sleep(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -166,7 +192,8 @@ __device__ __forceinline__ bool rbf_next_run(const RbfParams& P, int& q, int q1,
 
 template <int MT, bool VJP>
 __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
-    rbf_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ RbfParams P) {
+    rbf_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmAct,
+               const __grid_constant__ RbfParams P) {
   using Cfg = RbfCfg<MT>;
   constexpr int XS = Cfg::XS, US = Cfg::US, R = Cfg::R, W = Cfg::W;
   constexpr uint32_t SLOT = Cfg::SLOT;
@@ -213,6 +240,7 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_tmap(&tmX);
+    if (!VJP) prefetch_tmap(&tmAct);
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
@@ -289,6 +317,7 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
       const uint64_t a0 = make_sdesc(payload - RBF_PIX, 512u, 4u);  // dw = -1 window of M tile 0
       // the hot path (n2 == 0) is a straight run of MMAs: a branch between two tcgen05.mma
       // instructions costs far more issue time than the MMA's own ~60 clk
+      if (RBF_NO_MMA) return;
       if (n2 == 0) {
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
@@ -439,6 +468,13 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
           mbar_wait_sleep(t1done0 + 8u * (g % R), (g / R) & 1u);
           tc_fence_after();
           if (leader) RBF_EV(9, iu);
+          if (RBF_NO_EPI) {
+            rbf_epi_bar<MT>();
+            if (leader) mbar_arrive(ufull0 + 8u * (g % US));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(t1free0 + 8u * (g % R));
+            continue;
+          }
           uint32_t d[1][16];
           drain(0u, g % R, e1_mt, std::integral_constant<int, 1>{}, d);
           const uint32_t upl = sU + (g % US) * SLOT + 1024u;
@@ -469,16 +505,24 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
             }
             st_shared_v4(rbf_chunk(upl, p1, 2 * half + jj), w[jj]);
           }
-          fence_async_smem();  // u row -> async proxy (stage-2 MMAs)
+          fence_async_smem();  // u row -> async proxy (stage-2 MMAs, the act store)
+          // the u slot written next row (US - 1 rows after this one) must have been read by its
+          // act store, issued US - 1 rows ago: at most US - 2 stores may still be reading
+          if (!VJP && leader) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(US - 2) : "memory");
           rbf_epi_bar<MT>();
           if (leader) { mbar_arrive(ufull0 + 8u * (g % US)); RBF_EV(10, iu); }
-          give_back(t1free0 + 8u * (g % R));
-          if (!VJP && inside) {  // the saved activation, off the stage-2 critical path
-            uint4* o = reinterpret_cast<uint4*>(P.act + (((size_t)run.n * P.H + h) * W + p1) * RBF_C + c0);
-            o[0] = w[0];
-            o[1] = w[1];
+          if (!VJP && leader && inside) {  // the saved activation a, straight from the u row
+            tma_store_4d(upl, &tmAct, 0, 0, h, run.n);
+            bulk_commit();
           }
+          give_back(t1free0 + 8u * (g % R));
           if (VJP && iu + 1 < nu && h + 1 < P.H) load_a(run.n, h + 1);  // latency hidden by the next waits
+          // VJP: the saved-activation row three rows ahead is pulled into L2 by one bulk prefetch, so
+          // the per-thread loads above (one row ahead) hit L2 instead of waiting on HBM
+          if (VJP && leader && iu + 3 < nu && h + 3 < P.H)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.act + ((size_t)run.n * P.H + h + 3) * W * RBF_C),
+                         "r"((uint32_t)(W * RBF_PIX))
+                         : "memory");
         }
       } else {
         // E2: output row io (image row h0+io) = residual + conv 2
@@ -492,6 +536,11 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
           mbar_wait_sleep(t2done0 + 8u * (g % R), (g / R) & 1u);
           tc_fence_after();
           if (gw == 0 && lane == 0) RBF_EV(12, io);
+          if (RBF_NO_EPI) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(t2free0 + 8u * (g % R));
+            continue;
+          }
           uint32_t d[MT][16];
           drain((uint32_t)(MT * R * RBF_C), g % R, 0, std::integral_constant<int, MT>{}, d);
 #pragma unroll
@@ -520,6 +569,7 @@ __global__ void __launch_bounds__(rbf_threads<MT>(), 1)
       oc += (uint32_t)no;
     }
   }
+  if (!VJP && warp == 2 && lane == 0) bulk_wait0();  // the act stores are complete
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -545,6 +595,7 @@ static EncodeTiledFn4 rbf_encode() {
 
 struct RbfPlan {
   CUtensorMap tmX;
+  CUtensorMap tmAct;  // forward: the saved activation (same layout as x)
   RbfParams P;
   const int* list_ptr;
   bool vjp;
@@ -581,6 +632,7 @@ RbfPlan* rbf_make_plan(bool vjp, int N, int H, int W, const int dh1[9], const in
   P.out = static_cast<__nv_bfloat16*>(out);
   P.act = static_cast<__nv_bfloat16*>(act);
   CUresult r = rbf_map(enc, &p->tmX, x, N, H, W);
+  if (r == CUDA_SUCCESS && !vjp) r = rbf_map(enc, &p->tmAct, act, N, H, W);
   if (r != CUDA_SUCCESS) { snprintf(err, errlen, "fused residual block: tensor map encode failed (%d)", (int)r); delete p; return nullptr; }
   p->smem = W == 128 ? RbfCfg<1>::smem() : RbfCfg<2>::smem();
   const long long rows = (long long)N * H;
@@ -609,11 +661,11 @@ void rbf_launch(const RbfPlan* p, cudaStream_t s) {
   cfg.numAttrs = 1;
   const bool narrow = p->P.W == 128;
   if (p->vjp) {
-    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, true>, p->tmX, p->P);
-    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, true>, p->tmX, p->P);
+    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, true>, p->tmX, p->tmX, p->P);
+    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, true>, p->tmX, p->tmX, p->P);
   } else {
-    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, false>, p->tmX, p->P);
-    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, false>, p->tmX, p->P);
+    if (narrow) cudaLaunchKernelEx(&cfg, rbf_kernel<1, false>, p->tmX, p->tmAct, p->P);
+    else cudaLaunchKernelEx(&cfg, rbf_kernel<2, false>, p->tmX, p->tmAct, p->P);
   }
 }
 
