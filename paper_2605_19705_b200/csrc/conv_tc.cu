@@ -589,15 +589,19 @@ __global__ void __launch_bounds__(128) img2feat_tc_kernel(const float* __restric
                                                           const __grid_constant__ CUtensorMap tmO, int N, int C,
                                                           int H, int W, const FastDiv fdHW, const FastDiv fdW,
                                                           const int* __restrict__ act_list, const int* n_act) {
-  __shared__ __align__(1024) unsigned char sAraw[128 * 64];  // one A tile: the loop waits for each MMA
-  __shared__ __align__(1024) unsigned char sBraw[NC * 64];
-  // output staging [2][128 pixels x NC] in the TMA store's swizzle (SW64 for NC = 32, SW128 for
+  // ONE static array carved by hand (A tile | B tile | output staging | barriers | TMEM address):
+  // separate 1024-aligned arrays get padded to 28 / 46 KB, and a dynamic staging buffer needs 1 KB
+  // of alignment slack -- either costs one resident CTA per SM (8 fit at NC = 32; NC = 64 fits 4 either way).
+  // Output staging [2][128 pixels x NC] is in the TMA store's swizzle (SW64 for NC = 32, SW128 for
   // 64): conflict-free 16-byte writes (a linear layout at a 64/128-byte pixel stride put 8 lanes
   // on 2 / 1 bank groups), un-swizzled by the TMA tensor store
-  extern __shared__ __align__(1024) unsigned char sOraw[];
-  unsigned char* sOdyn = sOraw + ((1024u - (smem_u32(sOraw) & 1023u)) & 1023u);
-  __shared__ __align__(8) uint64_t bar[2];
-  __shared__ uint32_t tmem_holder;
+  constexpr int SM_A = 128 * 64, SM_B = NC * 64, SM_O = 2 * 128 * NC * 2;
+  __shared__ __align__(1024) unsigned char smem_all[SM_A + SM_B + SM_O + 32];
+  unsigned char* const sAraw = smem_all;                 // one A tile: the loop waits for each MMA
+  unsigned char* const sBraw = smem_all + SM_A;
+  unsigned char* const sOdyn = smem_all + SM_A + SM_B;
+  uint64_t* const bar = reinterpret_cast<uint64_t*>(smem_all + SM_A + SM_B + SM_O);
+  uint32_t& tmem_holder = *reinterpret_cast<uint32_t*>(smem_all + SM_A + SM_B + SM_O + 16);
   const int tid = threadIdx.x;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
   const uint32_t sA = smem_u32(sAraw), sB = smem_u32(sBraw);
@@ -799,13 +803,40 @@ I2FPlan* img2feat_make_plan(__nv_bfloat16* out, int N, int H, int W, int NC, cha
 }
 void img2feat_free_plan(I2FPlan* p) { delete p; }
 
+// resident img2feat CTAs per SM (0 = not known yet), from the kernel's attributes: shared memory
+// (static + the per-block reserve) against the SM's 228 KB, registers (allocated in units of 8 per
+// thread), and the 512 TMEM columns. The runtime's occupancy calculator is of no use here: it
+// answers 1 for a kernel that allocates TMEM (tools/occ_probe.cu), while ncu's launch__occupancy
+// limits agree with this count (8 at NC = 32, 4 at NC = 64). Filled by init_attrs_tc().
+static int i2f_occ[2] = {0, 0};
+static int img2feat_residency(int NC) {
+  cudaFuncAttributes a;
+  const cudaError_t e = NC == 64 ? cudaFuncGetAttributes(&a, img2feat_tc_kernel<64>)
+                                 : cudaFuncGetAttributes(&a, img2feat_tc_kernel<32>);
+  if (e != cudaSuccess) { cudaGetLastError(); return 0; }
+  int dev = 0, smem_sm = 0, reserve = 0, regs_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  cudaDeviceGetAttribute(&reserve, cudaDevAttrReservedSharedMemoryPerBlock, dev);
+  cudaDeviceGetAttribute(&regs_sm, cudaDevAttrMaxRegistersPerMultiprocessor, dev);
+  if (smem_sm <= 0 || regs_sm <= 0) return 0;
+  const int by_smem = smem_sm / ((int)a.sharedSizeBytes + reserve);
+  const int by_regs = regs_sm / (((a.numRegs + 7) / 8 * 8) * 128);
+  const int by_tmem = 512 / NC;
+  const int o = by_smem < by_regs ? by_smem : by_regs;
+  return o < 1 ? 0 : (o > by_tmem ? by_tmem : o);
+}
+
 void launch_img2feat_tc(const I2FPlan* plan, const float* in, const __nv_bfloat16* wB, const int* act_list,
                         const int* n_act, int N, int C,
                         int H, int W, int NC, int num_sms, cudaStream_t s) {
-  // residency is capped by shared memory; the CTAs' TMEM allocations (NC columns each, <= 8 x 32 or
-  // 5 x 64) stay within the SM's 512 columns
-  const int per_sm = NC == 64 ? 5 : 8;   // shared memory (27 KB / 45 KB per CTA) admits 8 (NC 32) / 5 (NC 64) CTAs per SM
-  const size_t pad = (size_t)2 * 128 * NC * 2 + 1024;  // output staging (+ alignment slack)
+  // one wave of resident CTAs (each walks tiles at a grid stride): a grid above the residency
+  // (8 CTAs per SM at NC = 32, 4 at NC = 64, img2feat_residency) leaves a second, partial wave that
+  // starts only when a first-wave CTA retires -- the earlier 8 / 5 per SM ran 7 / 4 + a tail wave
+  int per_sm = i2f_occ[NC == 64];
+  if (per_sm == 0) per_sm = i2f_occ[NC == 64] = img2feat_residency(NC);
+  if (per_sm == 0) per_sm = NC == 64 ? 4 : 8;  // attributes unavailable: ncu's residency for this layout
+  const size_t pad = 0;
   const long long total = (long long)N * H * W, tiles = (total + 127) / 128;
   const long long cap = (long long)num_sms * per_sm;
   const unsigned grid = (unsigned)(tiles < cap ? tiles : cap);
@@ -1117,8 +1148,8 @@ static void attrs_mode() {
 }
 
 void init_attrs_tc() {
-  set_max_dyn_smem(img2feat_tc_kernel<32>);
-  set_max_dyn_smem(img2feat_tc_kernel<64>);
+  i2f_occ[0] = img2feat_residency(32);
+  i2f_occ[1] = img2feat_residency(64);
   attrs_mode<0>();
   attrs_mode<1>();
   attrs_mode<2>();
